@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the FastDOG deferred-MMA hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload NAME]
+
+A step = one iteration of Alg. parallel-MMA: averaging -> forward
+pass -> averaging -> backward pass, each pass with its bound.  Workload at N=1:
+BASELINE.json configs[1] (synthetic graph matching shaped like 'worms'), fp32
+sweeps (north_star target).  L2 (126 MB) is flushed before every timed step;
+each step is timed with CUDA events on the solver's stream and the step times
+are summed (max over ranks for N > 1).
+
+value   = BDD arcs relaxed per second = 2 * nodes * 2 passes * steps / time
+e2e     = same metric through the public C ABI with host buffers: upload of the
+          packed plan (H2D) + K x (iterate(1) + lower_bound D2H) + get_lambda D2H.
+roofline: the sweep kernels' algorithmic bytes per launch over
+          their CUDA-event launch time vs MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline / --impl reference: the fp64 oracle (oracle/, test infrastructure)
+          timed as it stands on the host cores, on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+OMEGA = 0.5
+METRIC = "BDD arcs/s"
+UNIT = "arcs/s"
+
+
+def _workload(name):
+    if name == "gm_worms_like":
+        return synth.gm_worms_like(0)
+    if name == "mrf_potts":
+        return synth.mrf_potts(0)
+    if name == "qap50":
+        return synth.qap(0, 50)
+    if name == "celltrack":
+        return synth.celltrack(0)
+    if name == "lap4":
+        return synth.lap_random(4, 0)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _cpu_baseline(problem, arcs_per_iter, budget_s=15.0):
+    """The oracle as it stands, all host cores, bounded sample."""
+    import oracle
+    t0 = time.perf_counter()
+    o = oracle.Oracle(problem)
+    setup = time.perf_counter() - t0
+    iters = 0
+    t0 = time.perf_counter()
+    while True:
+        o.iterate(1, OMEGA)
+        iters += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or iters >= 1000:
+            break
+    return {"value": arcs_per_iter * iters / el, "unit": UNIT, "cores": o.threads, "kind": "oracle",
+            "iters_per_s": iters / el,
+            "sample": f"{iters} oracle iterations (fp64, OpenMP over BDDs) of the full instance after "
+                      f"a {setup:.1f}s untimed create; {el:.1f}s of CPU work",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    problem = _workload(args.workload)
+    import oracle
+    o = oracle.Oracle(problem)
+    nodes = o.total_nodes()
+    arcs_per_iter = 2 * nodes * 2
+    # bounded: each step is one full oracle iteration of the workload
+    for _ in range(args.warmup):
+        o.iterate(1, OMEGA)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.iterate(1, OMEGA)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    v = arcs_per_iter * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": problem.name, "nodes": nodes, "omega": OMEGA},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": o.threads, "kind": "oracle",
+                             "sample": f"{args.steps} full oracle iterations after {args.warmup} warm-up",
+                             "cpu": _cpu_model()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2111_10270_b200 as F
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and not (world == 1 and args.gpus == 1):
+        if world == 1:
+            raise SystemExit(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes")
+    torch.cuda.set_device(local)
+    uid = None
+    nccl_lib = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+        import nvidia.nccl
+        nccl_lib = os.path.join(os.path.dirname(nvidia.nccl.__file__), "lib", "libnccl.so.2")
+    stream = torch.cuda.current_stream()
+    problem = _workload(args.workload)
+    t0 = time.perf_counter()
+    plan = F.Plan(problem, rank=rank, world=world)
+    plan_s = time.perf_counter() - t0
+    prec = 64 if args.fp64 else 32
+    solver = F.Solver(plan=plan, precision=prec, device=local, profile=True, rank=rank, world=world,
+                      nccl_unique_id=uid, nccl_library=nccl_lib, stream=stream.cuda_stream)
+    st = solver.stats()
+    arcs_local = st["arcs"]
+    arcs_total = arcs_local
+    if world > 1:
+        t = torch.tensor([arcs_local], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        arcs_total = int(t.item())
+    lb0 = solver.lower_bound()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    for _ in range(args.warmup):
+        solver.iterate(1, OMEGA)
+    torch.cuda.synchronize()
+    solver.profile_reset()
+    launches0 = solver.stats()["launches"]
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush (256 MB > 126 MB), outside the timed interval
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        solver.iterate(1, OMEGA)
+        b.record(stream)
+        step_ms.append((a, b))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = [x.elapsed_time(y) for x, y in step_ms]
+    tot_ms = float(sum(ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    launches = solver.stats()["launches"] - launches0
+    prof = solver.profile()
+    lb = solver.lower_bound()
+
+    # roofline of the dominant kernel (the two sweeps share one code path)
+    peak, peak_kind = _peaks()
+    sweep = {k: v for k, v in prof.items() if k.startswith("sweep_")}
+    sw_ms = sum(v["ms"] for v in sweep.values())
+    sw_n = sum(v["launches"] for v in sweep.values())
+    sw_bytes = next(iter(sweep.values()))["bytes_per_launch"] if sweep else 0.0
+    achieved = sw_bytes / (sw_ms / sw_n * 1e-3) / 1e9 if sw_n else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(problem.name + f"/fp{prec}")
+        except Exception:
+            traffic = None
+    step_total_ms = sum(v["ms"] for v in prof.values())
+    shares = {k: v["ms"] / step_total_ms for k, v in prof.items()} if step_total_ms else {}
+
+    # e2e through the public API with host buffers (fresh solver; upload inside)
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        s2 = F.Solver(plan=plan, precision=prec, device=local, rank=rank, world=world,
+                      nccl_unique_id=uid, nccl_library=nccl_lib, stream=stream.cuda_stream)
+        for _ in range(args.steps):
+            s2.iterate(1, OMEGA)
+            s2.lower_bound()  # D2H of the step's result (8 bytes)
+        lam = s2.lam()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        up = s2.stats()["device_bytes"]
+        s2.close()
+        e2e = {"value": arcs_total * 2 * args.steps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(up / args.steps),
+               "d2h_bytes_per_step": int(8 + lam.nbytes / args.steps),
+               "includes": "device allocation + H2D upload of the packed plan, K x (iterate(1) + "
+                           "lower_bound D2H), get_lambda D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = _cpu_baseline(problem, 2 * 2 * st["nodes"], budget_s=args.cpu_budget)
+
+    if rank == 0:
+        iters_s = args.steps / (tot_ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": arcs_total * 2 * iters_s, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
+            "config": {"workload": problem.name, "bdds": st["bdds"], "nodes": st["nodes"],
+                       "arcs": st["arcs"], "slots": st["slots"], "vars": problem.n_vars,
+                       "omega": OMEGA, "parallelism": f"bdd-shard{world}",
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "plan_s": round(plan_s, 3)},
+            "iters_per_s": iters_s,
+            "lower_bound": {"initial": lb0, "after": lb, "iterations": args.warmup + args.steps},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "sweep_forward+sweep_backward",
+                         "bytes_per_launch": sw_bytes, "peak_kind": peak_kind,
+                         "launch_us": 1e3 * sw_ms / sw_n if sw_n else None},
+            "kernel_share": shares,
+            "kernels": prof,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="gm_worms_like")
+    ap.add_argument("--fp64", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+/*
+ * fastdog.h -- C ABI of the B200-native hot path of FastDOG (arXiv 2111.10270):
+ * Alg. "Parallel Deferred Min-Marginal Averaging" over one
+ * quasi-reduced ordered BDD per constraint (Def. BDD).
+ *
+ * Citations "P:n" are lines of the paper text; readings A1..A16 of
+ * ambiguous passages are listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns fdog_status; no C++ exception crosses the ABI.
+ *     On error, fdog_last_error() returns a thread-local message.
+ *   - Input arrays are HOST pointers borrowed for the duration of the call
+ *     (copied).  Output arrays are caller-allocated HOST arrays with an
+ *     explicit length; a length that is too small returns FDOG_EINVAL.
+ *   - A solver handle owns all of its device memory (and its NCCL
+ *     communicator when world > 1); fdog_destroy frees them.  A handle is
+ *     not thread-safe.  Device work is stream-ordered on opts.stream;
+ *     getters synchronise that stream.
+ *   - Slot = one multiplier lambda_i^j, i.e. one (constraint j, position h
+ *     in I_j) pair.  Getters return slots in canonical order: j ascending,
+ *     h ascending, over the BDDs held by this rank.
+ */
+#ifndef FASTDOG_H
+#define FASTDOG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FDOG_OK = 0,
+  FDOG_EINVAL = 1,      /* bad argument / length / omega outside (0,1] (A14)       */
+  FDOG_EINFEASIBLE = 2, /* some row has an empty feasible set X_j           */
+  FDOG_ENOMEM = 3,      /* host or device allocation failed                         */
+  FDOG_ECUDA = 4,       /* CUDA runtime error (message in fdog_last_error)          */
+  FDOG_ENCCL = 5,       /* NCCL error (multi-GPU)                                   */
+  FDOG_ESTATE = 6,      /* call not valid in this state (e.g. min_marginals w/o record_mm) */
+  FDOG_ETOOBIG = 7      /* a BDD exceeds the kernels' on-chip limits                */
+} fdog_status;
+
+/* Binary program (BP) P:555-565 in the row form of Example ILP P:567-577.
+ * Row j: sum_{p in [row_ptr[j], row_ptr[j+1])} col_coef[p] * x[col_var[p]]  rel[j]  rhs[j].
+ * col_var strictly ascending within a row (the BDD variable order, A12);
+ * col_coef nonzero; rel: -1 "<=", 0 "==", +1 ">=".  Layout: CSR, host memory. */
+typedef struct {
+  int32_t n_vars;
+  const double *cost;      /* c, length n_vars                         */
+  int32_t n_cons;
+  const int64_t *row_ptr;  /* length n_cons + 1                        */
+  const int32_t *col_var;  /* length row_ptr[n_cons]                   */
+  const int32_t *col_coef; /* length row_ptr[n_cons]                   */
+  const int8_t *rel;       /* length n_cons                            */
+  const int64_t *rhs;      /* length n_cons                            */
+} fdog_problem;
+
+typedef struct {
+  int32_t precision;        /* 32 (fp32 sweeps, fp64 bound accumulation) or 64  */
+  int32_t device;           /* CUDA device ordinal                              */
+  double clamp;             /* C substituted for an infinite m1-m0 (A5); <= 0:
+                               default 1e4 * (1 + max_i |c_i|)                  */
+  int32_t record_mm;        /* 1: store m0, m1 per slot each pass (parity)     */
+  int32_t profile;          /* 1: CUDA events around every launch (fdog_profile) */
+  int32_t rank, world;      /* BDD shard of this process; world == 1: no NCCL   */
+  const void *nccl_unique_id; /* 128-byte ncclUniqueId, required if world > 1   */
+  const char *nccl_library; /* path of libnccl.so.2 to dlopen (NULL: default)   */
+  void *stream;             /* cudaStream_t to run on; NULL: solver-owned stream */
+  int32_t host_threads;     /* threads for host BDD compilation (<= 0: all)    */
+} fdog_options;
+
+/* Sizes of this rank's part of the problem. */
+typedef struct {
+  int64_t bdds;          /* BDDs (non-empty rows) on this rank                        */
+  int64_t nodes;         /* non-terminal BDD nodes (A12)                              */
+  int64_t arcs;          /* 2 * nodes (arcs to bottom included)                */
+  int64_t slots;         /* multipliers lambda_i^j                                    */
+  int64_t vars_local;    /* variables with >= 1 slot on this rank                     */
+  int64_t vars_shared;   /* of those, variables also held by another rank             */
+  int64_t free_vars;     /* |J_i| = 0 (A13)                                           */
+  int64_t shapes;        /* distinct compiled BDD topologies                          */
+  int64_t tiles;         /* 32-BDD warp tiles                                         */
+  int64_t tiles_shared_topology; /* tiles whose 32 BDDs share one topology           */
+  int64_t padded_slots;  /* device slots incl. padding lanes                          */
+  int64_t device_bytes;  /* device memory held by the solver                          */
+  int64_t launches;      /* kernels launched by this handle so far                    */
+  int32_t max_hops;      /* max |I_j|                                                 */
+  int32_t max_width;     /* max partition size |P_h|                                  */
+} fdog_stats_t;
+
+typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */
+typedef struct fdog_solver fdog_solver; /* device-resident solver state        */
+
+void fdog_default_options(fdog_options *opts);
+
+/* ---- host setup (no GPU needed) -------------------------------------- */
+/* Compile every row of this rank's shard into a quasi-reduced ordered BDD
+ * (host compiler "B") and pack them into
+ * the device layout.  Only opts->rank, world, host_threads are read. */
+fdog_status fdog_plan_create(const fdog_problem *p, const fdog_options *opts, fdog_plan **out);
+void fdog_plan_destroy(fdog_plan *plan);
+fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out);
+/* Export BDD j (global row index) if held by this plan: hop_start[k+1],
+ * lo[n], hi[n] with successor codes node index within the BDD, -1 bottom,
+ * -2 top.  *k and *n_nodes are always written; arrays only if cap_nodes >= n
+ * and cap_hops >= k (otherwise FDOG_EINVAL after writing the sizes). */
+fdog_status fdog_plan_bdd(const fdog_plan *plan, int32_t j, int32_t *k, int32_t *n_nodes,
+                          int32_t *hop_start, int32_t *lo, int32_t *hi, int32_t cap_hops,
+                          int32_t cap_nodes);
+/* Global row -> owning rank for every row (length n_cons). */
+fdog_status fdog_plan_owner(const fdog_plan *plan, int32_t *owner, int64_t len);
+/* Ascending global indices of the variables exchanged between ranks (held by
+ * >= 2 ranks; identical on every rank).  *n = their number; vars is written
+ * if cap >= *n (may be NULL to query the size). */
+fdog_status fdog_plan_shared_vars(const fdog_plan *plan, int32_t *vars, int64_t cap, int64_t *n);
+
+/* ---- device solver ------------------------------------------------------ */
+/* fdog_create = fdog_plan_create + fdog_create_from_plan + fdog_plan_destroy.
+ * Initialises lambda_i^j = c_i/|J_i| (A9), mbar = 0 and the
+ * lower bound sum_j E^j(lambda^j) + sum_free min(c_i, 0). */
+fdog_status fdog_create(const fdog_problem *p, const fdog_options *opts, fdog_solver **out);
+/* Upload a plan (host -> device copies inside) and initialise.  The plan may
+ * be destroyed afterwards. */
+fdog_status fdog_create_from_plan(const fdog_plan *plan, const fdog_options *opts,
+                                  fdog_solver **out);
+void fdog_destroy(fdog_solver *s);
+
+/* n_iter x [averaging -> forward pass -> mbar<-m -> averaging -> backward pass
+ * -> mbar<-m] (A2); asynchronous on the stream.  omega in (0,1]. */
+fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega);
+/* One pass only: forward (1, ascending) or backward (0). */
+fdog_status fdog_pass(fdog_solver *s, int32_t forward, double omega);
+/* Lower bound of the last completed pass (A7): sum_j E^j(lambda^j) +
+ * sum_slots min(delta_bar, 0) + sum_free min(c_i, 0); summed over ranks.
+ * Synchronises the stream. */
+fdog_status fdog_lower_bound(fdog_solver *s, double *out);
+/* Final correction P:650-652 (per slot, A11): lambda += delta_bar,
+ * delta_bar = 0; the bound becomes sum_j E^j(lambda^j). */
+fdog_status fdog_finalize(fdog_solver *s);
+
+fdog_status fdog_num_slots(const fdog_solver *s, int64_t *out);
+/* (j, h) of every canonical slot. */
+fdog_status fdog_slot_index(const fdog_solver *s, int32_t *con, int32_t *pos, int64_t len);
+/* Current lambda_i^j (not finalized), canonical slot order. */
+fdog_status fdog_get_lambda(fdog_solver *s, double *out, int64_t len);
+/* delta_bar = omega * clamp(mbar1 - mbar0) of the last pass (A10). */
+fdog_status fdog_get_deferred(fdog_solver *s, double *out, int64_t len);
+/* m0, m1 (Eq. MM) recorded during the last pass; needs record_mm. */
+fdog_status fdog_min_marginals(fdog_solver *s, double *m0, double *m1, int64_t len);
+/* Overwrite (lambda, delta_bar) -- checkpoint/resume; either may be NULL. */
+fdog_status fdog_set_state(fdog_solver *s, const double *lambda, const double *delta, int64_t len);
+fdog_status fdog_stats(const fdog_solver *s, fdog_stats_t *out);
+
+/* Per-kernel device time (opts.profile = 1): names[i] (static strings),
+ * total milliseconds and launch counts since the last reset.  Synchronises. */
+typedef struct {
+  const char *name;
+  double ms;
+  int64_t launches;
+  double bytes_per_launch; /* algorithmic bytes of one launch */
+} fdog_kernel_time;
+fdog_status fdog_profile(fdog_solver *s, fdog_kernel_time *out, int32_t cap, int32_t *n);
+fdog_status fdog_profile_reset(fdog_solver *s);
+
+const char *fdog_last_error(void);
+int32_t fdog_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

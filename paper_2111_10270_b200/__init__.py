@@ -1,0 +1,306 @@
+"""Python binding of the FastDOG B200 hot path (include/fastdog.h).
+
+Argument marshalling only: every step of the path runs in libfastdog.so
+(host C++ BDD compiler + packer, sm_100a CUDA kernels).  There is no CPU
+fallback: if the extension is missing, importing the solver raises.
+
+Names follow the C ABI:  Plan (fdog_plan_*), Solver (fdog_create / iterate /
+pass_ / lower_bound / get_lambda / min_marginals / finalize / ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfastdog.so")
+
+STATUS = {0: "OK", 1: "EINVAL", 2: "EINFEASIBLE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE",
+          7: "ETOOBIG"}
+
+
+class FastdogError(RuntimeError):
+    def __init__(self, code, what, msg):
+        super().__init__(f"{what}: FDOG_{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Problem(C.Structure):
+    _fields_ = [("n_vars", C.c_int32), ("cost", C.c_void_p), ("n_cons", C.c_int32),
+                ("row_ptr", C.c_void_p), ("col_var", C.c_void_p), ("col_coef", C.c_void_p),
+                ("rel", C.c_void_p), ("rhs", C.c_void_p)]
+
+
+class Options(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("device", C.c_int32), ("clamp", C.c_double),
+                ("record_mm", C.c_int32), ("profile", C.c_int32), ("rank", C.c_int32),
+                ("world", C.c_int32), ("nccl_unique_id", C.c_void_p), ("nccl_library", C.c_char_p),
+                ("stream", C.c_void_p), ("host_threads", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("bdds", "nodes", "arcs", "slots", "vars_local", "vars_shared",
+                                          "free_vars", "shapes", "tiles", "tiles_shared_topology",
+                                          "padded_slots", "device_bytes", "launches")] + \
+               [("max_hops", C.c_int32), ("max_width", C.c_int32)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("ms", C.c_double), ("launches", C.c_int64),
+                ("bytes_per_launch", C.c_double)]
+
+
+EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdog_plan_stats",
+           "fdog_plan_bdd", "fdog_plan_owner", "fdog_plan_shared_vars", "fdog_create",
+           "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_lower_bound",
+           "fdog_finalize", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
+           "fdog_get_deferred", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
+           "fdog_profile", "fdog_profile_reset", "fdog_last_error", "fdog_version"]
+
+_lib = None
+
+
+def load():
+    """Load libfastdog.so (built by __graft_entry__.build() / make); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build(); "
+                          "there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    i64, i32, dbl = C.c_int64, C.c_int32, C.c_double
+    sig = {
+        "fdog_default_options": ([P], None),
+        "fdog_plan_create": ([P, P, C.POINTER(P)], C.c_int),
+        "fdog_plan_destroy": ([P], None),
+        "fdog_plan_stats": ([P, P], C.c_int),
+        "fdog_plan_bdd": ([P, i32, P, P, P, P, P, i32, i32], C.c_int),
+        "fdog_plan_owner": ([P, P, i64], C.c_int),
+        "fdog_plan_shared_vars": ([P, P, i64, P], C.c_int),
+        "fdog_create": ([P, P, C.POINTER(P)], C.c_int),
+        "fdog_create_from_plan": ([P, P, C.POINTER(P)], C.c_int),
+        "fdog_destroy": ([P], None),
+        "fdog_iterate": ([P, i32, dbl], C.c_int),
+        "fdog_pass": ([P, i32, dbl], C.c_int),
+        "fdog_lower_bound": ([P, P], C.c_int),
+        "fdog_finalize": ([P], C.c_int),
+        "fdog_num_slots": ([P, P], C.c_int),
+        "fdog_slot_index": ([P, P, P, i64], C.c_int),
+        "fdog_get_lambda": ([P, P, i64], C.c_int),
+        "fdog_get_deferred": ([P, P, i64], C.c_int),
+        "fdog_min_marginals": ([P, P, P, i64], C.c_int),
+        "fdog_set_state": ([P, P, P, i64], C.c_int),
+        "fdog_stats": ([P, P], C.c_int),
+        "fdog_profile": ([P, P, i32, P], C.c_int),
+        "fdog_profile_reset": ([P], C.c_int),
+        "fdog_last_error": ([], C.c_char_p),
+        "fdog_version": ([], C.c_int32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _check(rc, what):
+    if rc:
+        raise FastdogError(rc, what, load().fdog_last_error().decode())
+
+
+class _ProblemArrays:
+    """Keeps contiguous host copies alive and builds the fdog_problem struct."""
+
+    def __init__(self, problem):
+        self.arrays = [np.ascontiguousarray(problem.cost, dtype=np.float64),
+                       np.ascontiguousarray(problem.row_ptr, dtype=np.int64),
+                       np.ascontiguousarray(problem.col_var, dtype=np.int32),
+                       np.ascontiguousarray(problem.col_coef, dtype=np.int32),
+                       np.ascontiguousarray(problem.rel, dtype=np.int8),
+                       np.ascontiguousarray(problem.rhs, dtype=np.int64)]
+        c, rp, cv, cc, rel, rhs = self.arrays
+        self.struct = Problem(int(problem.n_vars), _ptr(c), int(rp.size - 1), _ptr(rp), _ptr(cv),
+                              _ptr(cc), _ptr(rel), _ptr(rhs))
+
+
+def make_options(precision=32, device=0, clamp=0.0, record_mm=False, profile=False, rank=0, world=1,
+                 nccl_unique_id=None, nccl_library=None, stream=None, host_threads=0):
+    lib = load()
+    o = Options()
+    lib.fdog_default_options(C.byref(o))
+    o.precision = int(precision)
+    o.device = int(device)
+    o.clamp = float(clamp)
+    o.record_mm = int(bool(record_mm))
+    o.profile = int(bool(profile))
+    o.rank = int(rank)
+    o.world = int(world)
+    o._uid = None
+    if nccl_unique_id is not None:
+        o._uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
+        o.nccl_unique_id = C.cast(o._uid, C.c_void_p)
+    o._lib = nccl_library.encode() if nccl_library else None
+    o.nccl_library = o._lib
+    o.stream = stream
+    o.host_threads = int(host_threads)
+    return o
+
+
+class Plan:
+    """Host-side compiled + packed problem (no GPU needed)."""
+
+    def __init__(self, problem, rank=0, world=1, host_threads=0):
+        lib = load()
+        self._pa = _ProblemArrays(problem)
+        self._opts = make_options(rank=rank, world=world, host_threads=host_threads)
+        h = C.c_void_p()
+        _check(lib.fdog_plan_create(C.byref(self._pa.struct), C.byref(self._opts), C.byref(h)),
+               "fdog_plan_create")
+        self._h = h
+        self._lib = lib
+        self.n_cons = int(problem.row_ptr.size - 1)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.fdog_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(self._lib.fdog_plan_stats(self._h, C.byref(s)), "fdog_plan_stats")
+        return s.as_dict()
+
+    def bdd(self, j):
+        """(hop_start, lo, hi) of row j; codes: node index, -1 bottom, -2 top."""
+        k = C.c_int32(); n = C.c_int32()
+        rc = self._lib.fdog_plan_bdd(self._h, int(j), C.byref(k), C.byref(n), None, None, None, 0, 0)
+        if rc not in (0, 1):
+            _check(rc, "fdog_plan_bdd")
+        hs = np.empty(k.value + 1, np.int32)
+        lo = np.empty(max(n.value, 1), np.int32)
+        hi = np.empty(max(n.value, 1), np.int32)
+        _check(self._lib.fdog_plan_bdd(self._h, int(j), C.byref(k), C.byref(n), _ptr(hs), _ptr(lo),
+                                       _ptr(hi), k.value, n.value), "fdog_plan_bdd")
+        return hs, lo[:n.value], hi[:n.value]
+
+    def owner(self):
+        o = np.empty(max(self.n_cons, 1), np.int32)
+        _check(self._lib.fdog_plan_owner(self._h, _ptr(o), o.size), "fdog_plan_owner")
+        return o[:self.n_cons]
+
+    def shared_vars(self):
+        n = C.c_int64()
+        _check(self._lib.fdog_plan_shared_vars(self._h, None, 0, C.byref(n)), "fdog_plan_shared_vars")
+        v = np.empty(max(n.value, 1), np.int32)
+        _check(self._lib.fdog_plan_shared_vars(self._h, _ptr(v), n.value, C.byref(n)),
+               "fdog_plan_shared_vars")
+        return v[:n.value]
+
+
+class Solver:
+    """Device-resident solver (fdog_create ... fdog_destroy)."""
+
+    def __init__(self, problem=None, *, plan: Plan | None = None, precision=32, device=0, clamp=0.0,
+                 record_mm=False, profile=False, rank=0, world=1, nccl_unique_id=None,
+                 nccl_library=None, stream=None, host_threads=0):
+        lib = load()
+        self._lib = lib
+        self._opts = make_options(precision, device, clamp, record_mm, profile, rank, world,
+                                  nccl_unique_id, nccl_library, stream, host_threads)
+        h = C.c_void_p()
+        if plan is not None:
+            _check(lib.fdog_create_from_plan(plan._h, C.byref(self._opts), C.byref(h)),
+                   "fdog_create_from_plan")
+        else:
+            pa = _ProblemArrays(problem)
+            _check(lib.fdog_create(C.byref(pa.struct), C.byref(self._opts), C.byref(h)), "fdog_create")
+        self._h = h
+        self.precision = precision
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.fdog_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def iterate(self, n: int, omega: float = 0.5):
+        _check(self._lib.fdog_iterate(self._h, int(n), float(omega)), "fdog_iterate")
+
+    def pass_(self, forward: bool, omega: float = 0.5):
+        _check(self._lib.fdog_pass(self._h, 1 if forward else 0, float(omega)), "fdog_pass")
+
+    def lower_bound(self) -> float:
+        x = C.c_double()
+        _check(self._lib.fdog_lower_bound(self._h, C.byref(x)), "fdog_lower_bound")
+        return x.value
+
+    def finalize(self):
+        _check(self._lib.fdog_finalize(self._h), "fdog_finalize")
+
+    def num_slots(self) -> int:
+        x = C.c_int64()
+        _check(self._lib.fdog_num_slots(self._h, C.byref(x)), "fdog_num_slots")
+        return x.value
+
+    def slot_index(self):
+        n = self.num_slots()
+        con = np.empty(max(n, 1), np.int32); pos = np.empty(max(n, 1), np.int32)
+        _check(self._lib.fdog_slot_index(self._h, _ptr(con), _ptr(pos), n), "fdog_slot_index")
+        return con[:n], pos[:n]
+
+    def _get(self, fn):
+        n = self.num_slots()
+        out = np.empty(max(n, 1), np.float64)
+        _check(getattr(self._lib, fn)(self._h, _ptr(out), n), fn)
+        return out[:n]
+
+    def lam(self):
+        return self._get("fdog_get_lambda")
+
+    def deferred(self):
+        return self._get("fdog_get_deferred")
+
+    def min_marginals(self):
+        n = self.num_slots()
+        m0 = np.empty(max(n, 1)); m1 = np.empty(max(n, 1))
+        _check(self._lib.fdog_min_marginals(self._h, _ptr(m0), _ptr(m1), n), "fdog_min_marginals")
+        return m0[:n], m1[:n]
+
+    def set_state(self, lam=None, delta=None):
+        n = self.num_slots()
+        a = None if lam is None else np.ascontiguousarray(lam, dtype=np.float64)
+        b = None if delta is None else np.ascontiguousarray(delta, dtype=np.float64)
+        _check(self._lib.fdog_set_state(self._h, None if a is None else _ptr(a),
+                                        None if b is None else _ptr(b), n), "fdog_set_state")
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(self._lib.fdog_stats(self._h, C.byref(s)), "fdog_stats")
+        return s.as_dict()
+
+    def profile(self) -> dict:
+        cap = 16
+        arr = (KernelTime * cap)()
+        n = C.c_int32()
+        _check(self._lib.fdog_profile(self._h, arr, cap, C.byref(n)), "fdog_profile")
+        return {arr[i].name.decode(): {"ms": arr[i].ms, "launches": arr[i].launches,
+                                       "bytes_per_launch": arr[i].bytes_per_launch}
+                for i in range(min(n.value, cap))}
+
+    def profile_reset(self):
+        _check(self._lib.fdog_profile_reset(self._h), "fdog_profile_reset")

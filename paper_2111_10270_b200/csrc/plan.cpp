@@ -1,0 +1,653 @@
+// plan.cpp -- host setup of the hot path (untimed):
+//   * compiler "B": linear row -> quasi-reduced ordered BDD (Def. BDD P:241-257,
+//     canonical form P:273-277, reading A12) by canonical residual classes
+//     computed from the suffix-sum sets (a different algorithm from the
+//     oracle's compiler "A");
+//   * sharder: contiguous row ranges per rank balanced by row length;
+//   * packer: rows -> 32-lane warp tiles in the hop-major SoA layout of
+//     DESIGN.md §5 (partition-contiguous per BDD, made tile-local),
+//     slot arrays, CSR variable -> slots (J_i).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <unordered_map>
+
+#include "internal.h"
+
+namespace fdog {
+
+static thread_local std::string g_err;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+const char *last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------------------
+// Compiler B.
+//
+// For row sum_h a_h x_h (rel) b, let T_h be the set of achievable suffix sums
+// sum_{t>=h} a_t x_t (T_k = {0}).  A top-down state at partition h is the
+// residual r = b - sum_{t<h} a_t x_t; its set of feasible completions is
+// {x : sum_{t>=h} a_t x_t in R(r)} with R(r) = (-inf, r], [r, inf) or {r}.
+// Two residuals have the same completion set iff they select the same subset
+// of T_h, so the canonical node of r is the representative
+//   <= : max{t in T_h : t <= r}     >= : min{t in T_h : t >= r}     == : r if r in T_h
+// (none: dead -> bottom).  Nodes of P_h are the distinct representatives
+// reached from the root; the children of representative r are the
+// representatives of r (x_h = 0) and r - a_h (x_h = 1) in T_{h+1}.
+// ---------------------------------------------------------------------------
+static bool representative(const std::vector<int64_t> &T, int rel, int64_t r, int64_t *out) {
+  if (rel < 0) {
+    auto it = std::upper_bound(T.begin(), T.end(), r);
+    if (it == T.begin()) return false;
+    *out = *(it - 1);
+    return true;
+  }
+  if (rel > 0) {
+    auto it = std::lower_bound(T.begin(), T.end(), r);
+    if (it == T.end()) return false;
+    *out = *it;
+    return true;
+  }
+  if (!std::binary_search(T.begin(), T.end(), r)) return false;
+  *out = r;
+  return true;
+}
+
+static fdog_status compile_B(int32_t k, const int32_t *a, int rel, int64_t b, Shape &out) {
+  const size_t kMaxSums = size_t(1) << 22;
+  std::vector<std::vector<int64_t>> T(k + 1);
+  T[k] = {0};
+  for (int32_t h = k - 1; h >= 0; --h) {
+    const auto &nx = T[h + 1];
+    std::vector<int64_t> shifted(nx.size());
+    for (size_t q = 0; q < nx.size(); ++q) shifted[q] = nx[q] + a[h];
+    T[h].resize(nx.size() * 2);
+    auto e = std::set_union(nx.begin(), nx.end(), shifted.begin(), shifted.end(), T[h].begin());
+    T[h].resize(e - T[h].begin());
+    if (T[h].size() > kMaxSums) {
+      set_error("row with %d variables has more than %zu distinct suffix sums", k, kMaxSums);
+      return FDOG_ETOOBIG;
+    }
+  }
+  int64_t r0;
+  if (k == 0 || !representative(T[0], rel, b, &r0)) return FDOG_EINFEASIBLE;
+  out.k = k;
+  out.hop_start.assign(1, 0);
+  out.lo.clear();
+  out.hi.clear();
+  out.max_w = 0;
+  std::vector<int64_t> level = {r0}, next;
+  std::unordered_map<int64_t, int32_t> index;
+  for (int32_t h = 0; h < k; ++h) {
+    next.clear();
+    index.clear();
+    for (int64_t r : level) {
+      int64_t res[2] = {r, r - a[h]};
+      uint32_t code[2];
+      for (int beta = 0; beta < 2; ++beta) {
+        if (h == k - 1) {
+          int64_t q;
+          code[beta] = representative(T[k], rel, res[beta], &q) ? kTop : kBot;
+        } else {
+          int64_t q;
+          if (!representative(T[h + 1], rel, res[beta], &q)) {
+            code[beta] = kBot;
+          } else {
+            auto it = index.find(q);
+            if (it == index.end()) {
+              int32_t id = (int32_t)next.size();
+              index.emplace(q, id);
+              next.push_back(q);
+              code[beta] = (uint32_t)id;
+            } else {
+              code[beta] = (uint32_t)it->second;
+            }
+          }
+        }
+      }
+      out.lo.push_back((uint16_t)code[0]);
+      out.hi.push_back((uint16_t)code[1]);
+    }
+    out.max_w = std::max<int32_t>(out.max_w, (int32_t)level.size());
+    if ((int64_t)next.size() > kMaxWidth) {
+      set_error("BDD partition wider than %d nodes", kMaxWidth);
+      return FDOG_ETOOBIG;
+    }
+    out.hop_start.push_back(out.hop_start.back() + (int32_t)level.size());
+    level.swap(next);
+  }
+  return FDOG_OK;
+}
+
+// 64-bit FNV-1a over the row signature (relation, rhs, coefficients).
+static uint64_t signature_hash(int32_t k, const int32_t *a, int8_t rel, int64_t rhs) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    for (int q = 0; q < 8; ++q) {
+      h ^= (v >> (8 * q)) & 0xff;
+      h *= 1099511628211ull;
+    }
+  };
+  mix((uint64_t)(uint8_t)rel);
+  mix((uint64_t)rhs);
+  mix((uint64_t)k);
+  for (int32_t q = 0; q < k; ++q) mix((uint64_t)(uint32_t)a[q]);
+  return h;
+}
+
+static fdog_status validate(const fdog_problem *p) {
+  if (!p || p->n_vars < 0 || p->n_cons < 0) {
+    set_error("null problem or negative sizes");
+    return FDOG_EINVAL;
+  }
+  if ((p->n_vars > 0 && !p->cost) || (p->n_cons > 0 && (!p->row_ptr || !p->rel || !p->rhs))) {
+    set_error("null problem array");
+    return FDOG_EINVAL;
+  }
+  if (p->n_cons > 0 && p->row_ptr[0] != 0) {
+    set_error("row_ptr[0] must be 0");
+    return FDOG_EINVAL;
+  }
+  for (int32_t j = 0; j < p->n_cons; ++j) {
+    int64_t a = p->row_ptr[j], b = p->row_ptr[j + 1];
+    if (b < a || b - a > 0x7fffffff) {
+      set_error("row %d: bad row_ptr", j);
+      return FDOG_EINVAL;
+    }
+    if (p->rel[j] < -1 || p->rel[j] > 1) {
+      set_error("row %d: rel must be -1, 0 or 1", j);
+      return FDOG_EINVAL;
+    }
+    for (int64_t q = a; q < b; ++q) {
+      if (p->col_var[q] < 0 || p->col_var[q] >= p->n_vars) {
+        set_error("row %d: variable index out of range", j);
+        return FDOG_EINVAL;
+      }
+      if (p->col_coef[q] == 0) {
+        set_error("row %d: zero coefficient", j);
+        return FDOG_EINVAL;
+      }
+      if (q > a && p->col_var[q] <= p->col_var[q - 1]) {
+        set_error("row %d: variables must be strictly ascending", j);
+        return FDOG_EINVAL;
+      }
+    }
+  }
+  for (int32_t i = 0; i < p->n_vars; ++i)
+    if (!std::isfinite(p->cost[i])) {
+      set_error("cost[%d] is not finite", i);
+      return FDOG_EINVAL;
+    }
+  return FDOG_OK;
+}
+
+// Contiguous row ranges with (approximately) equal total row length.
+static void shard_rows(const fdog_problem *p, int world, std::vector<int32_t> &owner) {
+  owner.assign(p->n_cons, 0);
+  if (world <= 1 || p->n_cons == 0) return;
+  const int64_t total = p->row_ptr[p->n_cons];
+  for (int32_t j = 0; j < p->n_cons; ++j) {
+    // the rank whose share contains the row's midpoint
+    int64_t mid2 = p->row_ptr[j] + p->row_ptr[j + 1];  // 2 * midpoint
+    int64_t r = total > 0 ? (mid2 * world) / (2 * total) : 0;
+    owner[j] = (int32_t)std::min<int64_t>(std::max<int64_t>(r, 0), world - 1);
+  }
+}
+
+fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
+  fdog_status st = validate(p);
+  if (st) return st;
+  const int world = o ? std::max(1, o->world) : 1;
+  const int rank = o ? o->rank : 0;
+  if (rank < 0 || rank >= world) {
+    set_error("rank %d outside [0, %d)", rank, world);
+    return FDOG_EINVAL;
+  }
+  int threads = o && o->host_threads > 0 ? o->host_threads : (int)std::thread::hardware_concurrency();
+  threads = std::max(1, std::min(threads, 64));
+
+  P.n_vars = p->n_vars;
+  P.n_cons = p->n_cons;
+  P.rank = rank;
+  P.world = world;
+  P.cost.assign(p->cost, p->cost + p->n_vars);
+  P.max_abs_cost = 0.0;
+  for (double c : P.cost) P.max_abs_cost = std::max(P.max_abs_cost, std::fabs(c));
+  P.row_ptr.assign(p->row_ptr, p->row_ptr + p->n_cons + 1);
+  if (p->n_cons == 0) P.row_ptr.assign(1, 0);
+  const int64_t nnz = P.row_ptr.back();
+  P.col_var.assign(p->col_var, p->col_var + nnz);
+
+  // rows with no variable: feasible (dropped) or infeasible (error)
+  for (int32_t j = 0; j < p->n_cons; ++j)
+    if (p->row_ptr[j + 1] == p->row_ptr[j]) {
+      int64_t b = p->rhs[j];
+      bool ok = p->rel[j] < 0 ? 0 <= b : p->rel[j] > 0 ? 0 >= b : b == 0;
+      if (!ok) {
+        set_error("row %d has no variables and is infeasible", j);
+        return FDOG_EINFEASIBLE;
+      }
+    }
+
+  shard_rows(p, world, P.owner);
+  // global |J_i| and the free-variable term (A13)
+  P.deg_global.assign(p->n_vars, 0);
+  for (int64_t q = 0; q < nnz; ++q) P.deg_global[p->col_var[q]]++;
+  P.free_term = 0.0;
+  for (int32_t i = 0; i < p->n_vars; ++i)
+    if (P.deg_global[i] == 0 && P.cost[i] < 0) P.free_term += P.cost[i];
+
+  // local rows, dedupe by signature, compile unique signatures in parallel
+  P.row_shape.assign(p->n_cons, -1);
+  P.local_rows.clear();
+  std::unordered_map<uint64_t, std::vector<int32_t>> sig;
+  for (int32_t j = 0; j < p->n_cons; ++j) {
+    if (P.owner[j] != rank) continue;
+    int64_t a = p->row_ptr[j];
+    int32_t k = (int32_t)(p->row_ptr[j + 1] - a);
+    if (k == 0) continue;
+    P.local_rows.push_back(j);
+    const int32_t *c = p->col_coef + a;
+    uint64_t h = signature_hash(k, c, p->rel[j], p->rhs[j]);
+    auto &cands = sig[h];
+    int32_t id = -1;
+    for (int32_t s : cands) {
+      const Shape &S = P.shapes[s];
+      if (S.rel == p->rel[j] && S.rhs == p->rhs[j] && (int32_t)S.coef.size() == k &&
+          std::equal(c, c + k, S.coef.begin())) {
+        id = s;
+        break;
+      }
+    }
+    if (id < 0) {
+      id = (int32_t)P.shapes.size();
+      P.shapes.emplace_back();
+      Shape &S = P.shapes.back();
+      S.rel = p->rel[j];
+      S.rhs = p->rhs[j];
+      S.coef.assign(c, c + k);
+      cands.push_back(id);
+    }
+    P.row_shape[j] = id;
+  }
+  {
+    std::atomic<int64_t> next{0};
+    std::atomic<int> bad{0};
+    std::mutex mu;
+    std::string err;
+    auto work = [&]() {
+      for (;;) {
+        int64_t s = next.fetch_add(1);
+        if (s >= (int64_t)P.shapes.size()) break;
+        Shape &S = P.shapes[s];
+        fdog_status r = compile_B((int32_t)S.coef.size(), S.coef.data(), S.rel, S.rhs, S);
+        if (r != FDOG_OK) {
+          std::lock_guard<std::mutex> g(mu);
+          if (!bad.load()) {
+            bad = (int)r;
+            err = r == FDOG_EINFEASIBLE ? "a constraint has an empty feasible set" : last_error();
+          }
+        }
+      }
+    };
+    int nt = (int)std::min<int64_t>(threads, (int64_t)P.shapes.size());
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto &t : pool) t.join();
+    if (bad.load()) {
+      set_error("%s", err.c_str());
+      return (fdog_status)bad.load();
+    }
+  }
+
+  // ---------------------------------------------------------------- packing
+  P.max_hops = 0;
+  P.max_width = 0;
+  P.n_nodes = 0;
+  P.n_slots = 0;
+  for (int32_t j : P.local_rows) {
+    const Shape &S = P.shapes[P.row_shape[j]];
+    P.max_hops = std::max(P.max_hops, S.k);
+    P.max_width = std::max(P.max_width, S.max_w);
+    P.n_nodes += S.nodes();
+    P.n_slots += S.k;
+  }
+  // group rows by shape (ascending j inside a group)
+  std::vector<std::vector<int32_t>> by_shape(P.shapes.size());
+  for (int32_t j : P.local_rows) by_shape[P.row_shape[j]].push_back(j);
+
+  struct PendingTile {
+    int kind;
+    int32_t shape;               // kind 0
+    std::vector<int32_t> rows;   // lanes
+    int64_t cost;
+  };
+  std::vector<PendingTile> pend;
+  std::vector<int32_t> pool;  // rows for per-lane tiles
+  for (size_t s = 0; s < P.shapes.size(); ++s) {
+    auto &rows = by_shape[s];
+    size_t full = rows.size() / kLanes * kLanes;
+    for (size_t q = 0; q < full; q += kLanes) {
+      PendingTile t;
+      t.kind = 0;
+      t.shape = (int32_t)s;
+      t.rows.assign(rows.begin() + q, rows.begin() + q + kLanes);
+      t.cost = (int64_t)P.shapes[s].nodes() + P.shapes[s].k;
+      pend.push_back(std::move(t));
+    }
+    pool.insert(pool.end(), rows.begin() + full, rows.end());
+  }
+  // per-lane tiles: same K within a tile; similar shapes adjacent
+  std::stable_sort(pool.begin(), pool.end(), [&](int32_t x, int32_t y) {
+    const Shape &a = P.shapes[P.row_shape[x]], &b = P.shapes[P.row_shape[y]];
+    if (a.k != b.k) return a.k < b.k;
+    if (a.nodes() != b.nodes()) return a.nodes() < b.nodes();
+    return P.row_shape[x] < P.row_shape[y];
+  });
+  for (size_t q = 0; q < pool.size();) {
+    int32_t K = P.shapes[P.row_shape[pool[q]]].k;
+    PendingTile t;
+    t.kind = 1;
+    t.shape = -1;
+    while (q < pool.size() && (int)t.rows.size() < kLanes && P.shapes[P.row_shape[pool[q]]].k == K)
+      t.rows.push_back(pool[q++]);
+    t.cost = 0;
+    pend.push_back(std::move(t));
+  }
+  // expensive tiles first so the static round-robin spreads them
+  for (auto &t : pend)
+    if (t.kind == 1) {
+      int64_t c = 0;
+      for (int32_t j : t.rows) c = std::max<int64_t>(c, P.shapes[P.row_shape[j]].nodes());
+      t.cost = c + P.shapes[P.row_shape[t.rows[0]]].k;
+    }
+  std::stable_sort(pend.begin(), pend.end(),
+                   [](const PendingTile &a, const PendingTile &b) { return a.cost > b.cost; });
+
+  P.tiles.clear();
+  P.hop_off.clear();
+  P.topo.clear();
+  P.slot_var.clear();
+  P.tiles_shared = 0;
+  P.max_tile_nodes = 0;
+  std::vector<int64_t> shape_topo(P.shapes.size(), -1);
+  std::vector<int32_t> shape_hop(P.shapes.size(), -1);
+  // device slot of (row j, hop h): row_slot[j] + h*32
+  std::vector<int64_t> row_slot(p->n_cons, -1);
+  int64_t slot_base = 0;
+  for (const PendingTile &t : pend) {
+    TileDesc d{};
+    const Shape &S0 = P.shapes[P.row_shape[t.rows[0]]];
+    d.K = S0.k;
+    d.n_lanes = (int32_t)t.rows.size();
+    d.kind = t.kind;
+    d.slot_base = slot_base;
+    if (t.kind == 0) {
+      if (shape_topo[t.shape] < 0) {
+        shape_topo[t.shape] = (int64_t)P.topo.size();
+        shape_hop[t.shape] = (int32_t)P.hop_off.size();
+        for (int32_t n = 0; n < S0.nodes(); ++n) P.topo.push_back(uint32_t(S0.lo[n]) | (uint32_t(S0.hi[n]) << 16));
+        for (int32_t h = 0; h <= S0.k; ++h) P.hop_off.push_back(S0.hop_start[h]);
+      }
+      d.topo_base = shape_topo[t.shape];
+      d.hop_base = shape_hop[t.shape];
+      d.nodes = S0.nodes();
+      d.max_w = S0.max_w;
+      P.tiles_shared++;
+    } else {
+      // padded partition widths
+      std::vector<int32_t> W(d.K, 0);
+      for (int32_t j : t.rows) {
+        const Shape &S = P.shapes[P.row_shape[j]];
+        for (int32_t h = 0; h < d.K; ++h) W[h] = std::max(W[h], S.hop_start[h + 1] - S.hop_start[h]);
+      }
+      d.hop_base = (int32_t)P.hop_off.size();
+      int32_t acc = 0;
+      d.max_w = 0;
+      for (int32_t h = 0; h < d.K; ++h) {
+        P.hop_off.push_back(acc);
+        acc += W[h];
+        d.max_w = std::max(d.max_w, W[h]);
+      }
+      P.hop_off.push_back(acc);
+      d.nodes = acc;
+      d.topo_base = (int64_t)P.topo.size();
+      P.topo.resize(P.topo.size() + (size_t)acc * kLanes, kBot | (kBot << 16));
+      for (int32_t l = 0; l < d.n_lanes; ++l) {
+        const Shape &S = P.shapes[P.row_shape[t.rows[l]]];
+        for (int32_t h = 0; h < d.K; ++h) {
+          int32_t base = P.hop_off[d.hop_base + h];
+          for (int32_t w = 0; w < S.hop_start[h + 1] - S.hop_start[h]; ++w) {
+            int32_t n = S.hop_start[h] + w;
+            P.topo[d.topo_base + (int64_t)(base + w) * kLanes + l] = uint32_t(S.lo[n]) | (uint32_t(S.hi[n]) << 16);
+          }
+        }
+      }
+    }
+    P.max_tile_nodes = std::max(P.max_tile_nodes, d.nodes);
+    // slots
+    P.slot_var.resize((size_t)(slot_base + (int64_t)d.K * kLanes), -1);
+    for (int32_t l = 0; l < d.n_lanes; ++l) {
+      int32_t j = t.rows[l];
+      row_slot[j] = slot_base + l;
+      const int32_t *vars = P.col_var.data() + P.row_ptr[j];
+      for (int32_t h = 0; h < d.K; ++h) P.slot_var[slot_base + (int64_t)h * kLanes + l] = vars[h];
+    }
+    slot_base += (int64_t)d.K * kLanes;
+    P.tiles.push_back(d);
+  }
+  if (slot_base > 0x7fffffffLL) {
+    set_error("more than 2^31 device slots on one rank");
+    return FDOG_ETOOBIG;
+  }
+  // canonical slots and CSR variable -> device slots (j ascending, A1)
+  P.canon_slot.clear();
+  P.canon_con.clear();
+  P.canon_pos.clear();
+  std::vector<int64_t> cnt(p->n_vars + 1, 0);
+  for (int32_t j : P.local_rows) {
+    int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
+    for (int32_t h = 0; h < k; ++h) {
+      P.canon_slot.push_back(row_slot[j] + (int64_t)h * kLanes);
+      P.canon_con.push_back(j);
+      P.canon_pos.push_back(h);
+      cnt[P.col_var[P.row_ptr[j] + h]]++;
+    }
+  }
+  P.var_list.clear();
+  P.var_ptr.assign(1, 0);
+  std::vector<int64_t> where(p->n_vars, -1);
+  for (int32_t i = 0; i < p->n_vars; ++i)
+    if (cnt[i]) {
+      where[i] = P.var_ptr.back();
+      P.var_list.push_back(i);
+      P.var_ptr.push_back(P.var_ptr.back() + cnt[i]);
+    }
+  P.var_slots.assign(P.var_ptr.back(), -1);
+  for (size_t q = 0; q < P.canon_slot.size(); ++q) {
+    int32_t j = P.canon_con[q];
+    int32_t i = P.col_var[P.row_ptr[j] + P.canon_pos[q]];
+    P.var_slots[where[i]++] = (int32_t)P.canon_slot[q];
+  }
+  // shared variables: held by this rank and by another one
+  P.shared_vars.clear();
+  P.var_xidx.assign(P.var_list.size(), -1);
+  if (world > 1) {
+    // the exchange vector must be identical on every rank: all variables held
+    // by >= 2 ranks, ascending; this rank contributes zeros for those it lacks
+    std::vector<int32_t> first(p->n_vars, -1);
+    std::vector<uint8_t> multi(p->n_vars, 0);
+    for (int32_t j = 0; j < p->n_cons; ++j)
+      for (int64_t q = P.row_ptr[j]; q < P.row_ptr[j + 1]; ++q) {
+        int32_t i = P.col_var[q];
+        if (first[i] < 0) first[i] = P.owner[j];
+        else if (first[i] != P.owner[j]) multi[i] = 1;
+      }
+    for (int32_t i = 0; i < p->n_vars; ++i)
+      if (multi[i]) P.shared_vars.push_back(i);
+    std::vector<int32_t> xpos(p->n_vars, -1);
+    for (size_t q = 0; q < P.shared_vars.size(); ++q) xpos[P.shared_vars[q]] = (int32_t)q;
+    for (size_t q = 0; q < P.var_list.size(); ++q) P.var_xidx[q] = xpos[P.var_list[q]];
+  }
+  return FDOG_OK;
+}
+
+}  // namespace fdog
+
+// ---------------------------------------------------------------------------
+// C ABI: plan
+
+using namespace fdog;
+
+struct fdog_plan {
+  Plan p;
+};
+
+extern "C" {
+
+void fdog_default_options(fdog_options *o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->precision = 32;
+  o->world = 1;
+}
+
+const char *fdog_last_error(void) { return fdog::last_error(); }
+
+int32_t fdog_version(void) { return 1; }
+
+fdog_status fdog_plan_create(const fdog_problem *p, const fdog_options *opts, fdog_plan **out) {
+  if (!out) {
+    set_error("null output handle");
+    return FDOG_EINVAL;
+  }
+  *out = nullptr;
+  try {
+    auto *pl = new fdog_plan();
+    fdog_status st = build_plan(p, opts, pl->p);
+    if (st != FDOG_OK) {
+      delete pl;
+      return st;
+    }
+    *out = pl;
+    return FDOG_OK;
+  } catch (const std::bad_alloc &) {
+    set_error("host out of memory while building the plan");
+    return FDOG_ENOMEM;
+  } catch (const std::exception &e) {
+    set_error("plan: %s", e.what());
+    return FDOG_EINVAL;
+  }
+}
+
+void fdog_plan_destroy(fdog_plan *plan) { delete plan; }
+
+fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out) {
+  if (!plan || !out) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  const Plan &P = plan->p;
+  std::memset(out, 0, sizeof *out);
+  out->bdds = (int64_t)P.local_rows.size();
+  out->nodes = P.n_nodes;
+  out->arcs = 2 * P.n_nodes;
+  out->slots = P.n_slots;
+  out->vars_local = (int64_t)P.var_list.size();
+  out->vars_shared = 0;
+  for (int32_t x : P.var_xidx) out->vars_shared += x >= 0;
+  int64_t fv = 0;
+  for (int32_t d : P.deg_global) fv += d == 0;
+  out->free_vars = fv;
+  out->shapes = (int64_t)P.shapes.size();
+  out->tiles = (int64_t)P.tiles.size();
+  out->tiles_shared_topology = P.tiles_shared;
+  out->padded_slots = (int64_t)P.slot_var.size();
+  out->max_hops = P.max_hops;
+  out->max_width = P.max_width;
+  return FDOG_OK;
+}
+
+fdog_status fdog_plan_bdd(const fdog_plan *plan, int32_t j, int32_t *k, int32_t *n_nodes,
+                          int32_t *hop_start, int32_t *lo, int32_t *hi, int32_t cap_hops,
+                          int32_t cap_nodes) {
+  if (!plan || !k || !n_nodes || j < 0 || j >= plan->p.n_cons) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  const Plan &P = plan->p;
+  if (P.owner[j] != P.rank) {
+    set_error("row %d is not held by this rank", j);
+    return FDOG_ESTATE;
+  }
+  if (P.row_shape[j] < 0) {
+    *k = 0;
+    *n_nodes = 0;
+    return FDOG_OK;
+  }
+  const Shape &S = P.shapes[P.row_shape[j]];
+  *k = S.k;
+  *n_nodes = S.nodes();
+  if (cap_hops < S.k || cap_nodes < S.nodes() || !hop_start || !lo || !hi) {
+    set_error("output arrays too small");
+    return FDOG_EINVAL;
+  }
+  for (int32_t h = 0; h <= S.k; ++h) hop_start[h] = S.hop_start[h];
+  for (int32_t h = 0; h < S.k; ++h)
+    for (int32_t v = S.hop_start[h]; v < S.hop_start[h + 1]; ++v) {
+      auto conv = [&](uint32_t c) -> int32_t {
+        if (c == kBot) return -1;
+        if (c == kTop) return -2;
+        return S.hop_start[h + 1] + (int32_t)c;
+      };
+      lo[v] = conv(S.lo[v]);
+      hi[v] = conv(S.hi[v]);
+    }
+  return FDOG_OK;
+}
+
+fdog_status fdog_plan_owner(const fdog_plan *plan, int32_t *owner, int64_t len) {
+  if (!plan || !owner || len < plan->p.n_cons) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  std::copy(plan->p.owner.begin(), plan->p.owner.end(), owner);
+  return FDOG_OK;
+}
+
+fdog_status fdog_plan_shared_vars(const fdog_plan *plan, int32_t *vars, int64_t cap, int64_t *n) {
+  if (!plan || !n) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  const auto &sv = plan->p.shared_vars;
+  *n = (int64_t)sv.size();
+  if (!vars) return FDOG_OK;
+  if (cap < (int64_t)sv.size()) {
+    set_error("output array too small");
+    return FDOG_EINVAL;
+  }
+  std::copy(sv.begin(), sv.end(), vars);
+  return FDOG_OK;
+}
+
+}  // extern "C"
+
+// accessor for solver.cpp
+namespace fdog {
+const Plan &plan_of(const fdog_plan *p) { return p->p; }
+}

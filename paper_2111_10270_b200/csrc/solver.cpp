@@ -1,0 +1,705 @@
+// solver.cpp -- device runtime of the hot path and the solver half of the C ABI.
+//
+// fdog_iterate(n, omega) enqueues, per pass (A2):
+//     avg_kernel (deferred averaging)  [+ ncclAllReduce + avg_finish, world > 1]
+//  -> sweep_kernel<forward|backward>          (min-marginals, dual update, bound)
+//  -> swap(delta_bar, delta_new)              (mbar <- m)
+// all stream-ordered, no host synchronisation.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+namespace fdog {
+const Plan &plan_of(const fdog_plan *p);
+}
+
+using namespace fdog;
+
+namespace {
+
+// ---- minimal NCCL surface, resolved with dlopen (world > 1 only) --------
+typedef struct {
+  char internal[128];
+} nccl_uid;
+typedef void *nccl_comm;
+typedef int (*nccl_init_fn)(nccl_comm *, int, nccl_uid, int);
+typedef int (*nccl_allreduce_fn)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t);
+typedef int (*nccl_destroy_fn)(nccl_comm);
+typedef const char *(*nccl_errstr_fn)(int);
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0;
+
+struct Nccl {
+  void *lib = nullptr;
+  nccl_init_fn init = nullptr;
+  nccl_allreduce_fn allreduce = nullptr;
+  nccl_destroy_fn destroy = nullptr;
+  nccl_errstr_fn errstr = nullptr;
+  nccl_comm comm = nullptr;
+};
+
+enum KernelId { kKSweepFwd = 0, kKSweepBwd, kKEnergy, kKAvg, kKAvgFinish, kKAllreduce, kKAddDeferred, kKFill, kKCount };
+const char *kKernelNames[kKCount] = {"sweep_forward", "sweep_backward", "sweep_energy", "avg", "avg_finish",
+                                     "nccl_allreduce", "add_deferred", "fill"};
+
+struct EventRec {
+  int kernel;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct fdog_solver {
+  int precision = 32;
+  int device = 0;
+  size_t tsz = 4;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool record_mm = false;
+  bool profile = false;
+  double clamp = 0.0;
+  int rank = 0, world = 1;
+
+  // host copies needed by getters
+  std::vector<int64_t> canon_slot;
+  std::vector<int32_t> canon_con, canon_pos;
+  double free_term = 0.0;
+  int64_t n_dev_slots = 0;
+  int32_t n_tiles = 0, n_varlist = 0, n_shared = 0;
+  int32_t max_nodes = 0, max_w = 0, max_hops = 0;
+  int64_t n_vars = 0;
+  fdog_stats_t st{};
+
+  // device buffers
+  TileDesc *d_tiles = nullptr;
+  int32_t *d_hop_off = nullptr;
+  uint32_t *d_topo = nullptr;
+  int32_t *d_slot_var = nullptr;
+  void *d_lambda = nullptr;
+  void *d_delta[2] = {nullptr, nullptr};
+  void *d_m0 = nullptr, *d_m1 = nullptr;
+  void *d_avg = nullptr;
+  int32_t *d_var_list = nullptr, *d_var_slots = nullptr, *d_var_xidx = nullptr, *d_deg = nullptr;
+  int64_t *d_var_ptr = nullptr;
+  double *d_lb_part = nullptr, *d_lb = nullptr;
+  unsigned int *d_counter = nullptr;
+  void *d_xbuf = nullptr;
+  int32_t *d_shared_vars = nullptr;
+  std::vector<void *> allocs;
+
+  int cur = 0;        // delta_bar = d_delta[cur]
+  int64_t passes = 0;
+  int64_t launches = 0;
+  int grid = 0, block = 0;
+  size_t smem = 0;
+
+  Nccl nccl;
+  std::vector<EventRec> events;
+  std::vector<cudaEvent_t> event_pool;
+  double prof_ms[kKCount] = {0};
+  int64_t prof_n[kKCount] = {0};
+  double bytes[kKCount] = {0};
+};
+
+namespace {
+
+fdog_status cuda_fail(cudaError_t e, const char *what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  if (e == cudaErrorMemoryAllocation) return FDOG_ENOMEM;
+  return FDOG_ECUDA;
+}
+
+#define CK(call, what)                                 \
+  do {                                                 \
+    cudaError_t e__ = (cudaError_t)(call);             \
+    if (e__ != cudaSuccess) return cuda_fail(e__, what); \
+  } while (0)
+
+template <typename V>
+fdog_status upload(fdog_solver *s, V **dst, const std::vector<V> &src, size_t min_elems = 1) {
+  size_t n = std::max(src.size(), min_elems);
+  void *p = nullptr;
+  CK(cudaMalloc(&p, n * sizeof(V)), "cudaMalloc");
+  s->allocs.push_back(p);
+  s->st.device_bytes += (int64_t)(n * sizeof(V));
+  if (!src.empty()) CK(cudaMemcpyAsync(p, src.data(), src.size() * sizeof(V), cudaMemcpyHostToDevice, s->stream), "H2D");
+  *dst = (V *)p;
+  return FDOG_OK;
+}
+
+fdog_status alloc(fdog_solver *s, void **dst, size_t bytes) {
+  void *p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc");
+  s->allocs.push_back(p);
+  s->st.device_bytes += (int64_t)bytes;
+  *dst = p;
+  return FDOG_OK;
+}
+
+cudaEvent_t get_event(fdog_solver *s) {
+  if (!s->event_pool.empty()) {
+    cudaEvent_t e = s->event_pool.back();
+    s->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Timed {
+  fdog_solver *s;
+  int k;
+  cudaEvent_t a = nullptr;
+  Timed(fdog_solver *s_, int k_) : s(s_), k(k_) {
+    s->launches++;
+    if (s->profile) {
+      a = get_event(s);
+      cudaEventRecord(a, s->stream);
+    }
+  }
+  ~Timed() {
+    if (s->profile) {
+      cudaEvent_t b = get_event(s);
+      cudaEventRecord(b, s->stream);
+      s->events.push_back({k, a, b});
+    }
+  }
+};
+
+fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
+  SweepArgs a{};
+  a.tiles = s->d_tiles;
+  a.n_tiles = s->n_tiles;
+  a.hop_off = s->d_hop_off;
+  a.topo = s->d_topo;
+  a.slot_var = s->d_slot_var;
+  a.lambda = s->d_lambda;
+  a.avg = s->d_avg;
+  a.delta_out = s->d_delta[s->cur ^ 1];
+  a.m0 = s->d_m0;
+  a.m1 = s->d_m1;
+  a.omega = omega;
+  a.clamp = s->clamp;
+  a.lb_part = s->d_lb_part;
+  a.lb_out = s->d_lb;
+  a.done_counter = s->d_counter;
+  a.max_nodes = s->max_nodes;
+  a.max_w = s->max_w;
+  a.max_hops = s->max_hops;
+  const bool rec = s->record_mm && mode != kEnergy;
+  int e;
+  {
+    Timed t(s, mode == kForward ? kKSweepFwd : mode == kBackward ? kKSweepBwd : kKEnergy);
+    e = launch_sweep(s->precision, mode, rec, a, s->grid, s->block, s->smem, s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "sweep launch");
+  return FDOG_OK;
+}
+
+fdog_status run_avg(fdog_solver *s) {
+  AvgArgs a{};
+  a.n = s->n_varlist;
+  a.var_list = s->d_var_list;
+  a.var_ptr = s->d_var_ptr;
+  a.var_slots = s->d_var_slots;
+  a.var_xidx = s->world > 1 ? s->d_var_xidx : nullptr;
+  a.deg = s->d_deg;
+  a.delta_bar = s->d_delta[s->cur];
+  a.avg = s->d_avg;
+  a.xbuf = s->d_xbuf;
+  int e;
+  {
+    Timed t(s, kKAvg);
+    e = launch_avg(s->precision, a, s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "avg launch");
+  if (s->world > 1 && s->n_shared > 0) {
+    int r;
+    {
+      Timed t(s, kKAllreduce);
+      s->launches--;  // not our kernel
+      r = s->nccl.allreduce(s->d_xbuf, s->d_xbuf, (size_t)s->n_shared, s->precision == 64 ? kNcclFloat64 : kNcclFloat32,
+                            kNcclSum, s->nccl.comm, s->stream);
+    }
+    if (r) {
+      set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(r) : "error");
+      return FDOG_ENCCL;
+    }
+    {
+      Timed t(s, kKAvgFinish);
+      e = launch_avg_finish(s->precision, s->n_shared, s->d_shared_vars, s->d_deg, s->d_xbuf, s->d_avg, s->stream);
+    }
+    if (e) return cuda_fail((cudaError_t)e, "avg_finish launch");
+  }
+  return FDOG_OK;
+}
+
+fdog_status do_pass(fdog_solver *s, bool forward, double omega) {
+  fdog_status st = run_avg(s);
+  if (st) return st;
+  st = run_sweep(s, forward ? kForward : kBackward, omega);
+  if (st) return st;
+  s->cur ^= 1;  // mbar <- m
+  s->passes++;
+  return FDOG_OK;
+}
+
+fdog_status energy(fdog_solver *s) { return run_sweep(s, kEnergy, 0.5); }
+
+void free_solver(fdog_solver *s) {
+  if (!s) return;
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  for (auto &e : s->events) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : s->event_pool) cudaEventDestroy(e);
+  for (void *p : s->allocs) cudaFree(p);
+  if (s->nccl.comm && s->nccl.destroy) s->nccl.destroy(s->nccl.comm);
+  if (s->nccl.lib) dlclose(s->nccl.lib);
+  if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+fdog_status fetch_slots(fdog_solver *s, const void *dev, double *out, int64_t len) {
+  const int64_t n = (int64_t)s->canon_slot.size();
+  if (!out || len < n) {
+    set_error("output length %lld < %lld slots", (long long)len, (long long)n);
+    return FDOG_EINVAL;
+  }
+  std::vector<unsigned char> buf((size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz);
+  CK(cudaMemcpyAsync(buf.data(), dev, (size_t)s->n_dev_slots * s->tsz, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  if (s->precision == 64) {
+    const double *b = (const double *)buf.data();
+    for (int64_t q = 0; q < n; ++q) out[q] = b[s->canon_slot[q]];
+  } else {
+    const float *b = (const float *)buf.data();
+    for (int64_t q = 0; q < n; ++q) out[q] = (double)b[s->canon_slot[q]];
+  }
+  return FDOG_OK;
+}
+
+fdog_status put_slots(fdog_solver *s, void *dev, const double *in, int64_t len) {
+  const int64_t n = (int64_t)s->canon_slot.size();
+  if (len != n) {
+    set_error("input length %lld != %lld slots", (long long)len, (long long)n);
+    return FDOG_EINVAL;
+  }
+  std::vector<unsigned char> buf((size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz);
+  CK(cudaMemcpyAsync(buf.data(), dev, (size_t)s->n_dev_slots * s->tsz, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  if (s->precision == 64) {
+    double *b = (double *)buf.data();
+    for (int64_t q = 0; q < n; ++q) b[s->canon_slot[q]] = in[q];
+  } else {
+    float *b = (float *)buf.data();
+    for (int64_t q = 0; q < n; ++q) b[s->canon_slot[q]] = (float)in[q];
+  }
+  CK(cudaMemcpyAsync(dev, buf.data(), (size_t)s->n_dev_slots * s->tsz, cudaMemcpyHostToDevice, s->stream), "H2D");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  return FDOG_OK;
+}
+
+fdog_status init_nccl(fdog_solver *s, const fdog_options *o) {
+  if (!o->nccl_unique_id) {
+    set_error("world > 1 needs nccl_unique_id");
+    return FDOG_EINVAL;
+  }
+  const char *path = o->nccl_library ? o->nccl_library : "libnccl.so.2";
+  s->nccl.lib = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+  if (!s->nccl.lib) {
+    set_error("dlopen(%s): %s", path, dlerror());
+    return FDOG_ENCCL;
+  }
+  s->nccl.init = (nccl_init_fn)dlsym(s->nccl.lib, "ncclCommInitRank");
+  s->nccl.allreduce = (nccl_allreduce_fn)dlsym(s->nccl.lib, "ncclAllReduce");
+  s->nccl.destroy = (nccl_destroy_fn)dlsym(s->nccl.lib, "ncclCommDestroy");
+  s->nccl.errstr = (nccl_errstr_fn)dlsym(s->nccl.lib, "ncclGetErrorString");
+  if (!s->nccl.init || !s->nccl.allreduce || !s->nccl.destroy) {
+    set_error("libnccl is missing ncclCommInitRank/ncclAllReduce/ncclCommDestroy");
+    return FDOG_ENCCL;
+  }
+  nccl_uid uid;
+  std::memcpy(uid.internal, o->nccl_unique_id, sizeof uid.internal);
+  int r = s->nccl.init(&s->nccl.comm, s->world, uid, s->rank);
+  if (r) {
+    set_error("ncclCommInitRank: %s", s->nccl.errstr ? s->nccl.errstr(r) : "error");
+    return FDOG_ENCCL;
+  }
+  return FDOG_OK;
+}
+
+fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
+  s->precision = o->precision == 64 ? 64 : 32;
+  if (o->precision != 32 && o->precision != 64) {
+    set_error("precision must be 32 or 64");
+    return FDOG_EINVAL;
+  }
+  s->tsz = s->precision == 64 ? 8 : 4;
+  s->device = o->device;
+  s->record_mm = o->record_mm != 0;
+  s->profile = o->profile != 0;
+  s->rank = P.rank;
+  s->world = P.world;
+  s->clamp = o->clamp > 0 ? o->clamp : 1e4 * (1.0 + P.max_abs_cost);  // A5
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (s->device < 0 || s->device >= ndev) {
+    set_error("device %d not present (%d devices)", s->device, ndev);
+    return FDOG_EINVAL;
+  }
+  CK(cudaSetDevice(s->device), "cudaSetDevice");
+  if (o->stream) {
+    s->stream = (cudaStream_t)o->stream;
+  } else {
+    CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    s->own_stream = true;
+  }
+  s->canon_slot = P.canon_slot;
+  s->canon_con = P.canon_con;
+  s->canon_pos = P.canon_pos;
+  s->free_term = P.rank == 0 ? P.free_term : 0.0;
+  s->n_dev_slots = (int64_t)P.slot_var.size();
+  s->n_tiles = (int32_t)P.tiles.size();
+  s->n_varlist = (int32_t)P.var_list.size();
+  s->n_shared = (int32_t)P.shared_vars.size();
+  s->n_vars = P.n_vars;
+  s->max_nodes = std::max(1, P.max_tile_nodes);
+  s->max_w = std::max(1, P.max_width);
+  s->max_hops = std::max(1, P.max_hops);
+
+  // launch configuration: persistent grid of warps, smem sized by the largest tile
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, s->device), "cudaGetDeviceProperties");
+  const int smem_limit = (int)prop.sharedMemPerBlockOptin;
+  int warps = 8;
+  while (warps > 1 && sweep_smem_bytes(s->precision, s->max_nodes, s->max_w, s->max_hops, warps) > smem_limit) warps /= 2;
+  if (sweep_smem_bytes(s->precision, s->max_nodes, s->max_w, s->max_hops, warps) > smem_limit) {
+    set_error("a BDD tile needs more shared memory than %d bytes (nodes %d, hops %d)", smem_limit, s->max_nodes,
+              s->max_hops);
+    return FDOG_ETOOBIG;
+  }
+  s->block = warps * 32;
+  s->smem = (size_t)sweep_smem_bytes(s->precision, s->max_nodes, s->max_w, s->max_hops, warps);
+  int bps = 1;
+  for (int mode = 0; mode < 3; ++mode)
+    for (int rec = 0; rec < 2; ++rec) {
+      int b = 0;
+      int e = sweep_occupancy(s->precision, mode, rec && mode != kEnergy, s->block, s->smem, &b);
+      if (e) return cuda_fail((cudaError_t)e, "occupancy");
+      if (mode == kForward && rec == (int)s->record_mm) bps = std::max(1, b);
+    }
+  const int64_t want = ((int64_t)s->n_tiles + warps - 1) / warps;
+  s->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)prop.multiProcessorCount * bps));
+
+  fdog_status st;
+  if ((st = upload(s, &s->d_tiles, P.tiles))) return st;
+  if ((st = upload(s, &s->d_hop_off, P.hop_off))) return st;
+  if ((st = upload(s, &s->d_topo, P.topo))) return st;
+  if ((st = upload(s, &s->d_slot_var, P.slot_var))) return st;
+  if ((st = upload(s, &s->d_var_list, P.var_list))) return st;
+  if ((st = upload(s, &s->d_var_ptr, P.var_ptr))) return st;
+  if ((st = upload(s, &s->d_var_slots, P.var_slots))) return st;
+  if ((st = upload(s, &s->d_var_xidx, P.var_xidx))) return st;
+  if ((st = upload(s, &s->d_deg, P.deg_global))) return st;
+  if ((st = upload(s, &s->d_shared_vars, P.shared_vars))) return st;
+  const size_t slot_bytes = (size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz;
+  if ((st = alloc(s, &s->d_lambda, slot_bytes))) return st;
+  if ((st = alloc(s, &s->d_delta[0], slot_bytes))) return st;
+  if ((st = alloc(s, &s->d_delta[1], slot_bytes))) return st;
+  if (s->record_mm) {
+    if ((st = alloc(s, &s->d_m0, slot_bytes))) return st;
+    if ((st = alloc(s, &s->d_m1, slot_bytes))) return st;
+  }
+  if ((st = alloc(s, &s->d_avg, (size_t)std::max<int64_t>(P.n_vars, 1) * s->tsz))) return st;
+  if ((st = alloc(s, &s->d_xbuf, (size_t)std::max<int32_t>(s->n_shared, 1) * s->tsz))) return st;
+  if ((st = alloc(s, (void **)&s->d_lb_part, (size_t)std::max(s->n_tiles, 1) * sizeof(double)))) return st;
+  if ((st = alloc(s, (void **)&s->d_lb, sizeof(double)))) return st;
+  if ((st = alloc(s, (void **)&s->d_counter, sizeof(unsigned int)))) return st;
+  CK(cudaMemsetAsync(s->d_counter, 0, sizeof(unsigned int), s->stream), "memset");
+  CK(cudaMemsetAsync(s->d_lb, 0, sizeof(double), s->stream), "memset");
+  CK(cudaMemsetAsync(s->d_delta[0], 0, slot_bytes, s->stream), "memset");
+  CK(cudaMemsetAsync(s->d_delta[1], 0, slot_bytes, s->stream), "memset");
+  CK(cudaMemsetAsync(s->d_avg, 0, (size_t)std::max<int64_t>(P.n_vars, 1) * s->tsz, s->stream), "memset");
+  if (s->record_mm) {
+    CK(cudaMemsetAsync(s->d_m0, 0, slot_bytes, s->stream), "memset");
+    CK(cudaMemsetAsync(s->d_m1, 0, slot_bytes, s->stream), "memset");
+  }
+  // lambda_i^j = c_i / |J_i| (A9) computed on the host in fp64, rounded once
+  {
+    std::vector<unsigned char> lam(slot_bytes, 0);
+    for (size_t q = 0; q < P.slot_var.size(); ++q) {
+      int32_t i = P.slot_var[q];
+      double v = i >= 0 ? P.cost[i] / (double)P.deg_global[i] : 0.0;
+      if (s->precision == 64) ((double *)lam.data())[q] = v;
+      else ((float *)lam.data())[q] = (float)v;
+    }
+    CK(cudaMemcpyAsync(s->d_lambda, lam.data(), slot_bytes, cudaMemcpyHostToDevice, s->stream), "H2D");
+    CK(cudaStreamSynchronize(s->stream), "sync");
+  }
+  if (s->world > 1 && (st = init_nccl(s, o))) return st;
+
+  // algorithmic bytes per launch
+  {
+    const double T = (double)s->tsz;
+    const double slots = (double)P.n_slots, nv = (double)P.var_list.size();
+    const double topo = (double)P.topo.size() * 4.0;
+    const double rec = s->record_mm ? 2 * T : 0.0;
+    s->bytes[kKSweepFwd] = s->bytes[kKSweepBwd] = topo + slots * (3 * T + 4 + T + rec);
+    s->bytes[kKEnergy] = topo + slots * T;
+    s->bytes[kKAvg] = slots * (4 + T) + nv * (8 + 4 + 4 + T);
+    s->bytes[kKAvgFinish] = (double)s->n_shared * (4 + 4 + 2 * T);
+    s->bytes[kKAllreduce] = (double)s->n_shared * T;
+    s->bytes[kKAddDeferred] = (double)s->n_dev_slots * 4 * T;
+  }
+  // stats
+  s->st.bdds = (int64_t)P.local_rows.size();
+  s->st.nodes = P.n_nodes;
+  s->st.arcs = 2 * P.n_nodes;
+  s->st.slots = P.n_slots;
+  s->st.vars_local = (int64_t)P.var_list.size();
+  for (int32_t x : P.var_xidx) s->st.vars_shared += x >= 0;
+  for (int32_t d : P.deg_global) s->st.free_vars += d == 0;
+  s->st.shapes = (int64_t)P.shapes.size();
+  s->st.tiles = (int64_t)P.tiles.size();
+  s->st.tiles_shared_topology = P.tiles_shared;
+  s->st.padded_slots = s->n_dev_slots;
+  s->st.max_hops = P.max_hops;
+  s->st.max_width = P.max_width;
+
+  // initial bound sum_j E^j(lambda) (+ free term on the host)
+  if ((st = energy(s))) return st;
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  return FDOG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fdog_status fdog_create_from_plan(const fdog_plan *plan, const fdog_options *opts, fdog_solver **out) {
+  if (!plan || !out) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  *out = nullptr;
+  fdog_options def;
+  fdog_default_options(&def);
+  const fdog_options *o = opts ? opts : &def;
+  fdog_solver *s = nullptr;
+  try {
+    s = new fdog_solver();
+    fdog_status st = create_impl(plan_of(plan), o, s);
+    if (st) {
+      free_solver(s);
+      return st;
+    }
+  } catch (const std::bad_alloc &) {
+    free_solver(s);
+    set_error("host out of memory");
+    return FDOG_ENOMEM;
+  }
+  *out = s;
+  return FDOG_OK;
+}
+
+fdog_status fdog_create(const fdog_problem *p, const fdog_options *opts, fdog_solver **out) {
+  fdog_plan *plan = nullptr;
+  fdog_status st = fdog_plan_create(p, opts, &plan);
+  if (st) return st;
+  st = fdog_create_from_plan(plan, opts, out);
+  fdog_plan_destroy(plan);
+  return st;
+}
+
+void fdog_destroy(fdog_solver *s) { free_solver(s); }
+
+fdog_status fdog_pass(fdog_solver *s, int32_t forward, double omega) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  if (!(omega > 0.0 && omega <= 1.0)) {
+    set_error("omega %g outside (0, 1]", omega);
+    return FDOG_EINVAL;
+  }
+  return do_pass(s, forward != 0, omega);
+}
+
+fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
+  if (!s || n_iter < 0) {
+    set_error("null solver or negative n_iter");
+    return FDOG_EINVAL;
+  }
+  if (!(omega > 0.0 && omega <= 1.0)) {
+    set_error("omega %g outside (0, 1]", omega);
+    return FDOG_EINVAL;
+  }
+  for (int32_t t = 0; t < n_iter; ++t) {
+    fdog_status st = do_pass(s, true, omega);
+    if (st) return st;
+    st = do_pass(s, false, omega);
+    if (st) return st;
+  }
+  return FDOG_OK;
+}
+
+fdog_status fdog_lower_bound(fdog_solver *s, double *out) {
+  if (!s || !out) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  double v = 0.0;
+  CK(cudaMemcpyAsync(&v, s->d_lb, sizeof(double), cudaMemcpyDeviceToHost, s->stream), "D2H");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  double tot = v + s->free_term;
+  if (s->world > 1) {
+    // scalar allreduce of the per-rank partials (fp64)
+    double *d = (double *)s->d_lb_part;  // scratch: reuse slot 0 after the sync above
+    CK(cudaMemcpyAsync(d, &tot, sizeof(double), cudaMemcpyHostToDevice, s->stream), "H2D");
+    int r = s->nccl.allreduce(d, d, 1, kNcclFloat64, kNcclSum, s->nccl.comm, s->stream);
+    if (r) {
+      set_error("ncclAllReduce(lb): %s", s->nccl.errstr ? s->nccl.errstr(r) : "error");
+      return FDOG_ENCCL;
+    }
+    CK(cudaMemcpyAsync(&tot, d, sizeof(double), cudaMemcpyDeviceToHost, s->stream), "D2H");
+    CK(cudaStreamSynchronize(s->stream), "sync");
+  }
+  *out = tot;
+  return FDOG_OK;
+}
+
+fdog_status fdog_finalize(fdog_solver *s) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  int e;
+  {
+    Timed t(s, kKAddDeferred);
+    e = launch_add_deferred(s->precision, s->n_dev_slots, s->d_lambda, s->d_delta[s->cur], s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "add_deferred");
+  return energy(s);
+}
+
+fdog_status fdog_num_slots(const fdog_solver *s, int64_t *out) {
+  if (!s || !out) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  *out = (int64_t)s->canon_slot.size();
+  return FDOG_OK;
+}
+
+fdog_status fdog_slot_index(const fdog_solver *s, int32_t *con, int32_t *pos, int64_t len) {
+  if (!s || !con || !pos || len < (int64_t)s->canon_slot.size()) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  std::copy(s->canon_con.begin(), s->canon_con.end(), con);
+  std::copy(s->canon_pos.begin(), s->canon_pos.end(), pos);
+  return FDOG_OK;
+}
+
+fdog_status fdog_get_lambda(fdog_solver *s, double *out, int64_t len) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  return fetch_slots(s, s->d_lambda, out, len);
+}
+
+fdog_status fdog_get_deferred(fdog_solver *s, double *out, int64_t len) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  return fetch_slots(s, s->d_delta[s->cur], out, len);
+}
+
+fdog_status fdog_min_marginals(fdog_solver *s, double *m0, double *m1, int64_t len) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  if (!s->record_mm || s->passes == 0) {
+    set_error("min_marginals needs record_mm and at least one pass");
+    return FDOG_ESTATE;
+  }
+  fdog_status st = fetch_slots(s, s->d_m0, m0, len);
+  return st ? st : fetch_slots(s, s->d_m1, m1, len);
+}
+
+fdog_status fdog_set_state(fdog_solver *s, const double *lambda, const double *delta, int64_t len) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  fdog_status st;
+  if (lambda && (st = put_slots(s, s->d_lambda, lambda, len))) return st;
+  if (delta && (st = put_slots(s, s->d_delta[s->cur], delta, len))) return st;
+  return energy(s);
+}
+
+fdog_status fdog_stats(const fdog_solver *s, fdog_stats_t *out) {
+  if (!s || !out) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  *out = s->st;
+  out->launches = s->launches;
+  return FDOG_OK;
+}
+
+fdog_status fdog_profile(fdog_solver *s, fdog_kernel_time *out, int32_t cap, int32_t *n) {
+  if (!s || !n) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  for (auto &e : s->events) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e.a, e.b), "cudaEventElapsedTime");
+    s->prof_ms[e.kernel] += ms;
+    s->prof_n[e.kernel] += 1;
+    s->event_pool.push_back(e.a);
+    s->event_pool.push_back(e.b);
+  }
+  s->events.clear();
+  int32_t k = 0;
+  for (int q = 0; q < kKCount; ++q) {
+    if (!s->prof_n[q]) continue;
+    if (out && k < cap) out[k] = {kKernelNames[q], s->prof_ms[q], s->prof_n[q], s->bytes[q]};
+    ++k;
+  }
+  *n = k;
+  return FDOG_OK;
+}
+
+fdog_status fdog_profile_reset(fdog_solver *s) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  for (auto &e : s->events) {
+    s->event_pool.push_back(e.a);
+    s->event_pool.push_back(e.b);
+  }
+  s->events.clear();
+  for (int q = 0; q < kKCount; ++q) {
+    s->prof_ms[q] = 0;
+    s->prof_n[q] = 0;
+  }
+  return FDOG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star):
+  * fp64 build after 1 iteration: |a - b| <= 1e-9 * (|b| + s), s = max(1, max|c|),
+    on lambda, (m0, m1), delta_bar and the lower bound;
+  * fp32 build after 100 iterations: lower bound within 1e-4 relative;
+  * dyadic instances (LAP literal, iterations 1-2): bit-exact in fp64 and fp32;
+  * node / arc counts: exact (tests/test_host.py and below).
+"""
+import numpy as np
+import pytest
+
+import paper_2111_10270_b200 as F
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _s(problem):
+    return max(1.0, float(np.max(np.abs(problem.cost))) if problem.n_vars else 1.0)
+
+
+def _close(a, b, tol):
+    a = np.asarray(a, float)
+    b = np.asarray(b, float)
+    inf_a, inf_b = np.isinf(a), np.isinf(b)
+    assert np.array_equal(inf_a, inf_b), "infinite min-marginals differ"
+    assert np.array_equal(np.sign(a[inf_a]), np.sign(b[inf_b]))
+    fa, fb = a[~inf_a], b[~inf_b]
+    err = np.abs(fa - fb) - tol * np.abs(fb)
+    return float(err.max()) if err.size else -1.0
+
+
+def _compare_pass_by_pass(problem, oracle_mod, passes, precision=64, rtol=1e-9, omega=0.5):
+    s = _s(problem)
+    o = oracle_mod.Oracle(problem)
+    g = F.Solver(problem, precision=precision, record_mm=True)
+    assert g.num_slots() == o.num_slots()
+    con, pos = g.slot_index()
+    assert np.array_equal(con, np.repeat(np.arange(problem.n_cons), np.diff(problem.row_ptr)))
+    abs_tol = rtol * s
+    assert abs(g.lower_bound() - o.lower_bound()) <= rtol * (abs(o.lower_bound()) + s)
+    for t in range(passes):
+        fwd = t % 2 == 0
+        o.pass_(fwd, omega)
+        g.pass_(fwd, omega)
+        for name, a, b in (("lambda", g.lam(), o.lam()), ("delta", g.deferred(), o.deferred())):
+            err = np.abs(a - b) - rtol * np.abs(b)
+            assert err.max(initial=-1) <= abs_tol, f"pass {t} {name}: max err {np.max(np.abs(a - b))}"
+        gm0, gm1 = g.min_marginals()
+        om0, om1 = o.min_marginals()
+        assert _close(gm0, om0, rtol) <= abs_tol, f"pass {t} m0"
+        assert _close(gm1, om1, rtol) <= abs_tol, f"pass {t} m1"
+        lb_g, lb_o = g.lower_bound(), o.lower_bound()
+        assert abs(lb_g - lb_o) <= rtol * (abs(lb_o) + s), f"pass {t} lb {lb_g} vs {lb_o}"
+    return g, o
+
+
+def test_figure_example(oracle_mod):
+    _compare_pass_by_pass(synth.figure_bdd_problem(), oracle_mod, passes=4)
+
+
+def test_spec_two_constraint(oracle_mod):
+    _compare_pass_by_pass(synth.spec_two_constraint(), oracle_mod, passes=20)
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_lap4_literal_bit_exact(oracle_mod, precision):
+    """Iterations 1-2 on the literal LAP are dyadic rationals: bit-exact."""
+    p = synth.lap(synth.LAP4_LITERAL)
+    o = oracle_mod.Oracle(p)
+    g = F.Solver(p, precision=precision, record_mm=True)
+    assert g.lower_bound() == o.lower_bound() == 6.5
+    for t in range(4):
+        o.pass_(t % 2 == 0, 0.5)
+        g.pass_(t % 2 == 0, 0.5)
+        assert np.array_equal(g.lam(), o.lam())
+        assert np.array_equal(g.deferred(), o.deferred())
+        assert g.lower_bound() == o.lower_bound()
+    assert g.lower_bound() == 8.109375
+    if precision == 64:
+        g.iterate(48, 0.5)
+        assert g.lower_bound() == pytest.approx(10.0, abs=1e-9)
+
+
+def test_random_tiny_ilps_fp64(oracle_mod):
+    """200 random tiny ILPs (ragged tiles, per-lane topologies), 1 iteration, fp64."""
+    for seed in range(200):
+        p = synth.random_ilp(seed, n=10, m=7, kmax=7, coef=3)
+        _compare_pass_by_pass(p, oracle_mod, passes=2)
+
+
+def test_random_ilps_with_forced_vars(oracle_mod):
+    """Forced variables: infinite min-marginals and the clamp (A5), fp64."""
+    for seed in range(30):
+        p = synth.random_ilp(900 + seed, n=8, m=6, kmax=5, coef=3, forced_ok=True)
+        _compare_pass_by_pass(p, oracle_mod, passes=4)
+
+
+@pytest.mark.parametrize("name,make", [
+    ("gm", lambda: synth.gm_worms_like(4, n_src=80, k_cand=6, knn=8)),
+    ("mrf", lambda: synth.mrf_potts(4, H=12, W=14, L=4)),
+    ("qap", lambda: synth.qap(4, n=7)),
+    ("celltrack", lambda: synth.celltrack(4, frames=5, dets=40)),
+    ("wide_rows", lambda: synth.random_ilp(7, n=40, m=60, kmax=12, coef=5)),
+])
+def test_workload_shapes_fp64(oracle_mod, name, make):
+    """Several tiles, ragged tails, both tile kinds: 1 iteration element-wise, then 10 more."""
+    p = make()
+    g, o = _compare_pass_by_pass(p, oracle_mod, passes=2)
+    g.iterate(10, 0.5)
+    o.iterate(10, 0.5)
+    s = _s(p)
+    assert abs(g.lower_bound() - o.lower_bound()) <= 1e-8 * (abs(o.lower_bound()) + s)
+    assert np.allclose(g.lam(), o.lam(), rtol=1e-8, atol=1e-8 * s)
+
+
+@pytest.mark.parametrize("name,make", [
+    ("lap4", lambda: synth.lap_random(4, 0)),
+    ("gm", lambda: synth.gm_worms_like(5, n_src=120, k_cand=8, knn=10)),
+    ("mrf", lambda: synth.mrf_potts(5, H=20, W=20, L=5)),
+    ("qap", lambda: synth.qap(5, n=8)),
+])
+def test_fp32_lower_bound_100_iterations(oracle_mod, name, make):
+    """fp32 build: LB within 1e-4 relative after 100 iterations; monotone within
+    1e-6 (1 + |LB|) (Prop. 1)."""
+    p = make()
+    o = oracle_mod.Oracle(p)
+    g = F.Solver(p, precision=32)
+    lbs = [g.lower_bound()]
+    for _ in range(10):
+        g.iterate(10, 0.5)
+        lbs.append(g.lower_bound())
+    o.iterate(100, 0.5)
+    lb_o = o.lower_bound()
+    assert abs(lbs[-1] - lb_o) <= 1e-4 * max(abs(lb_o), 1.0), f"{lbs[-1]} vs {lb_o}"
+    lbs = np.array(lbs)
+    assert np.all(np.diff(lbs) >= -1e-6 * (1 + np.abs(lbs[:-1])))
+
+
+def test_finalize_feasible(oracle_mod):
+    """after finalize sum_j lambda_i^j = c_i, bound = sum_j E^j (I5)."""
+    p = synth.gm_worms_like(6, n_src=50, k_cand=5, knn=6)
+    g = F.Solver(p, precision=64)
+    o = oracle_mod.Oracle(p)
+    g.iterate(7, 0.5); o.iterate(7, 0.5)
+    g.finalize(); o.finalize()
+    lam = g.lam()
+    acc = np.zeros(p.n_vars)
+    np.add.at(acc, p.col_var, lam)
+    used = np.bincount(p.col_var, minlength=p.n_vars) > 0
+    assert np.max(np.abs(acc - p.cost)[used]) < 1e-9 * _s(p)
+    assert g.lower_bound() == pytest.approx(o.lower_bound(), rel=1e-9, abs=1e-9)
+    # iterate again after finalize (restart from feasible lambda with mbar = 0)
+    g.iterate(2, 0.5); o.iterate(2, 0.5)
+    assert g.lower_bound() == pytest.approx(o.lower_bound(), rel=1e-9, abs=1e-9)
+
+
+def test_edge_cases(oracle_mod):
+    # no constraints: bound = sum min(c, 0)
+    p = synth.from_rows(3, [-1.0, 2.0, -0.5], [])
+    g = F.Solver(p, precision=64)
+    assert g.lower_bound() == -1.5 and g.num_slots() == 0
+    g.iterate(2, 0.5)
+    assert g.lower_bound() == -1.5
+    # single one-variable row + a free variable
+    p = synth.from_rows(2, [3.0, -1.0], [([0], [1], 1, 1)])
+    _compare_pass_by_pass(p, oracle_mod, passes=4)
+    # 33 identical rows: one shared-topology tile + one ragged per-lane tile
+    rows = [([i, i + 1, i + 2], [1, 1, 1], 0, 1) for i in range(33)]
+    p = synth.from_rows(35, np.linspace(-1, 1, 35), rows)
+    g, _ = _compare_pass_by_pass(p, oracle_mod, passes=4)
+    st = g.stats()
+    assert st["tiles"] == 2 and st["tiles_shared_topology"] == 1
+    # omega = 1 and omega small
+    _compare_pass_by_pass(synth.spec_two_constraint(), oracle_mod, passes=4, omega=1.0)
+    _compare_pass_by_pass(synth.spec_two_constraint(), oracle_mod, passes=4, omega=0.1)
+
+
+def test_errors_and_state():
+    p = synth.spec_two_constraint()
+    g = F.Solver(p, precision=64)
+    with pytest.raises(F.FastdogError) as e:
+        g.min_marginals()
+    assert e.value.code == 6
+    with pytest.raises(F.FastdogError) as e:
+        g.iterate(1, 1.5)
+    assert e.value.code == 1
+    g.iterate(3, 0.5)
+    lam, dl, lb = g.lam(), g.deferred(), g.lower_bound()
+    h = F.Solver(p, precision=64)
+    h.set_state(lam, dl)            # checkpoint / resume
+    assert np.array_equal(h.lam(), lam) and np.array_equal(h.deferred(), dl)
+    g.iterate(2, 0.5); h.iterate(2, 0.5)
+    assert np.array_equal(g.lam(), h.lam()) and g.lower_bound() == h.lower_bound()
+    with pytest.raises(F.FastdogError) as e:
+        F.Solver(synth.from_rows(2, [0, 0], [([0, 1], [1, 1], -1, -1)]))
+    assert e.value.code == 2
+
+
+def test_full_size_gm_fp32(oracle_mod):
+    """BASELINE configs[1] at full size in bench.py's launch configuration (fp32):
+    lambda after 1 iteration vs the oracle (fp64) element-wise at fp32 tolerance,
+    bound after 20 iterations within 1e-4 relative, node/arc counts exact."""
+    p = synth.gm_worms_like(0)
+    g = F.Solver(p, precision=32)
+    o = oracle_mod.Oracle(p)
+    st = g.stats()
+    assert st["nodes"] == o.total_nodes() and st["arcs"] == 2 * o.total_nodes()
+    assert abs(g.lower_bound() - o.lower_bound()) <= 1e-6 * abs(o.lower_bound())
+    g.iterate(1, 0.5); o.iterate(1, 0.5)
+    s = _s(p)
+    a, b = g.lam(), o.lam()
+    assert np.max(np.abs(a - b) - 1e-5 * np.abs(b)) <= 1e-5 * s
+    g.iterate(19, 0.5); o.iterate(19, 0.5)
+    assert abs(g.lower_bound() - o.lower_bound()) <= 1e-4 * abs(o.lower_bound())
+
+
+def test_full_size_gm_fp64_sampled(oracle_mod):
+    """fp64 at full GM size: every slot after 1 iteration within 1e-9 (the oracle
+    finishes the whole instance in seconds)."""
+    p = synth.gm_worms_like(0)
+    g = F.Solver(p, precision=64)
+    o = oracle_mod.Oracle(p)
+    g.iterate(1, 0.5); o.iterate(1, 0.5)
+    s = _s(p)
+    a, b = g.lam(), o.lam()
+    assert np.max(np.abs(a - b) - 1e-9 * np.abs(b)) <= 1e-9 * s
+    assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)

@@ -1,0 +1,179 @@
+"""Host-side product checks that need no GPU (-m "not gpu").
+
+* the C-ABI library loads and exports every symbol include/fastdog.h declares;
+* compiler B (product, plan.cpp) vs brute force and vs the oracle's compiler A:
+  path sets, per-partition node counts bit-exact (BJ: "node and arc counts
+  bit-exact"), closed forms;
+* sharder / shared-variable index invariants for world > 1.
+"""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2111_10270_b200 as F
+import synth
+from tests import bruteforce as bf
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_header_symbols():
+    hdr = open(os.path.join(ROOT, "include", "fastdog.h")).read()
+    declared = set(re.findall(r"\b(fdog_[a-z_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    lib = F.load()
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in fastdog.h but not exported"
+    assert set(F.EXPORTS) == declared
+    assert lib.fdog_version() >= 1
+
+
+def _paths(hs, lo, hi):
+    k = len(hs) - 1
+    out = []
+
+    def rec(v, h, bits):
+        for beta, w in ((0, lo[v]), (1, hi[v])):
+            if w == -1:
+                continue
+            if h == k - 1:
+                if w == -2:
+                    out.append(tuple(bits + [beta]))
+                continue
+            assert hs[h + 1] <= w < hs[h + 2]
+            rec(w, h + 1, bits + [beta])
+
+    rec(0, 0, [])
+    return out
+
+
+def test_compiler_b_path_sets_random_rows():
+    """Compiler B: paths == brute-force X_j, canonical, P_1 = {r}."""
+    rng = np.random.default_rng(77)
+    done = 0
+    while done < 400:
+        k = int(rng.integers(1, 11))
+        a = rng.integers(-5, 6, size=k)
+        a[a == 0] = -2
+        rel = int(rng.choice([-1, 0, 1]))
+        b = int(rng.integers(-6, 7))
+        X = bf.feasible_set(a, rel, b)
+        p = synth.from_rows(k, np.zeros(k), [(np.arange(k), a, rel, b)])
+        if X.shape[0] == 0:
+            with pytest.raises(F.FastdogError) as e:
+                F.Plan(p)
+            assert e.value.code == 2
+            continue
+        hs, lo, hi = F.Plan(p).bdd(0)
+        paths = _paths(hs, lo, hi)
+        assert len(paths) == len(set(paths)) and set(paths) == set(map(tuple, X.tolist()))
+        for h in range(k):
+            sig = [(lo[v], hi[v]) for v in range(hs[h], hs[h + 1])]
+            assert len(sig) == len(set(sig)) and (-1, -1) not in sig
+        assert hs[1] == 1
+        done += 1
+
+
+def _per_hop_counts_equal(problem, oracle_mod):
+    pl = F.Plan(problem)
+    o = oracle_mod.Oracle(problem)
+    st = pl.stats()
+    assert st["nodes"] == o.total_nodes()
+    assert st["arcs"] == 2 * o.total_nodes()
+    for j in range(problem.n_cons):
+        hs, _, _ = pl.bdd(j)
+        assert np.array_equal(np.diff(hs), o.hop_widths(j)), f"row {j}"
+    return st
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_node_counts_random_ilp(oracle_mod, seed):
+    _per_hop_counts_equal(synth.random_ilp(seed, n=14, m=10, kmax=10, coef=4, forced_ok=True), oracle_mod)
+
+
+@pytest.mark.parametrize("name,make", [
+    ("lap4", lambda: synth.lap(synth.LAP4_LITERAL)),
+    ("gm_small", lambda: synth.gm_worms_like(1, n_src=40, k_cand=5, knn=6)),
+    ("mrf_small", lambda: synth.mrf_potts(1, H=6, W=7, L=3)),
+    ("qap_small", lambda: synth.qap(1, n=6)),
+    ("celltrack_small", lambda: synth.celltrack(1, frames=4, dets=30)),
+])
+def test_node_counts_workload_shapes(oracle_mod, name, make):
+    """Per-partition node counts of compiler B == compiler A (bit-exact, BJ)."""
+    st = _per_hop_counts_equal(make(), oracle_mod)
+    assert st["bdds"] > 0
+
+
+def test_closed_forms_product():
+    for k in (2, 5, 11, 50):
+        p = synth.from_rows(k, np.zeros(k), [(np.arange(k), np.ones(k), 0, 1)])
+        assert F.Plan(p).stats()["nodes"] == 2 * k - 1
+        c = np.ones(k); c[0] = -1
+        p = synth.from_rows(k, np.zeros(k), [(np.arange(k), c, 0, 0)])
+        assert F.Plan(p).stats()["nodes"] == 2 * k - 1
+
+
+def test_mrf_full_size_counts():
+    """MRF 300x400x8 closed form: simplex rows 2*8-1, marginalisation rows 2*9-1."""
+    H, W, L = 30, 40, 8   # scaled grid, same per-row shapes as the BJ config
+    p = synth.mrf_potts(0, H=H, W=W, L=L)
+    st = F.Plan(p).stats()
+    E = H * (W - 1) + (H - 1) * W + 2 * (H - 1) * (W - 1)
+    assert st["bdds"] == H * W + 2 * L * E
+    assert st["nodes"] == H * W * (2 * L - 1) + 2 * L * E * (2 * (L + 1) - 1)
+    assert st["shapes"] == 2
+
+
+def test_invalid_inputs():
+    base = synth.spec_two_constraint()
+    bad = synth.Problem(base.n_vars, base.cost, base.row_ptr, base.col_var.copy(), base.col_coef.copy(),
+                        base.rel, base.rhs)
+    bad.col_coef[0] = 0
+    with pytest.raises(F.FastdogError) as e:
+        F.Plan(bad)
+    assert e.value.code == 1
+    bad = synth.Problem(base.n_vars, base.cost, base.row_ptr, base.col_var[::-1].copy(), base.col_coef,
+                        base.rel, base.rhs)
+    with pytest.raises(F.FastdogError):
+        F.Plan(bad)
+    # empty problem and free variables are fine
+    p = synth.from_rows(3, [-1.0, 2.0, -0.5], [])
+    st = F.Plan(p).stats()
+    assert st["bdds"] == 0 and st["free_vars"] == 3
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_sharder_and_shared_index(world):
+    """Every row on exactly one rank; the exchange list is identical on all ranks
+    and equals the variables touched by rows of >= 2 ranks; local degrees sum to
+    the global |J_i|."""
+    p = synth.gm_worms_like(2, n_src=60, k_cand=5, knn=6)
+    plans = [F.Plan(p, rank=r, world=world) for r in range(world)]
+    owner = plans[0].owner()
+    for pl in plans[1:]:
+        assert np.array_equal(pl.owner(), owner)
+    assert owner.min() >= 0 and owner.max() < world
+    assert np.all(np.diff(owner) >= 0), "contiguous ranges"
+    bdds = [pl.stats()["bdds"] for pl in plans]
+    assert sum(bdds) == p.n_cons
+    sv = plans[0].shared_vars()
+    for pl in plans[1:]:
+        assert np.array_equal(pl.shared_vars(), sv)
+    ranks_of = [set() for _ in range(p.n_vars)]
+    for j in range(p.n_cons):
+        for i in p.row(j)[0]:
+            ranks_of[i].add(int(owner[j]))
+    expect = [i for i in range(p.n_vars) if len(ranks_of[i]) >= 2]
+    assert list(sv) == expect
+    deg = np.bincount(p.col_var, minlength=p.n_vars)
+    loc = np.zeros(p.n_vars, np.int64)
+    for r in range(world):
+        rows = np.flatnonzero(owner == r)
+        for j in rows:
+            loc[p.row(j)[0]] += 1
+    assert np.array_equal(loc, deg)
+    # balance by row length
+    nnz = np.array([sum(len(p.row(j)[0]) for j in np.flatnonzero(owner == r)) for r in range(world)])
+    assert nnz.max() <= 1.1 * nnz.mean() + 64
