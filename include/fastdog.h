@@ -85,6 +85,9 @@ typedef struct {
   int64_t launches;      /* kernels launched by this handle so far                    */
   int32_t max_hops;      /* max |I_j|                                                 */
   int32_t max_width;     /* max partition size |P_h|                                  */
+  int64_t staged_tiles;  /* tiles staged on chip by TMA (the rest run from global)    */
+  int32_t sweep_grid, sweep_block; /* persistent sweep launch configuration           */
+  int64_t sweep_smem_per_warp;     /* bytes of shared memory per warp                 */
 } fdog_stats_t;
 
 typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */

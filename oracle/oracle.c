@@ -72,6 +72,10 @@ struct oracle_solver {
   double free_term;    /* sum over free variables of min(c_i, 0) (A13) */
   double lb;
   int passes;
+  /* which stored distances are valid for the current lambda: the incremental
+   * reuse of P:315-316 holds when forward and backward passes alternate; any
+   * other sequence recomputes them from their definition */
+  int ctt_ok, cfr_ok;
 };
 
 /* ------------------------------------------------------------------ */
@@ -246,6 +250,22 @@ static void backward_dp(obdd *d, const double *lam) {
       double a = ctt_of(d, d->lo[v]);
       double b = lam[h] + ctt_of(d, d->hi[v]);
       d->ctt[v] = a < b ? a : b;
+    }
+}
+
+/* Forward DP over all partitions with the current lambda, no updates:
+ * shp(r,v) = min over parents (arc cost lambda_{h-1}, A4). */
+static void forward_dp(obdd *d, const double *lam) {
+  if (d->k == 0) return;
+  d->cfr[0] = 0.0;
+  for (int32_t h = 1; h < d->k; ++h)
+    for (int32_t v = d->hop_start[h]; v < d->hop_start[h + 1]; ++v) {
+      double best = INFINITY;
+      for (int32_t u = d->hop_start[h - 1]; u < d->hop_start[h]; ++u) {
+        if (d->lo[u] == v && d->cfr[u] < best) best = d->cfr[u];
+        if (d->hi[u] == v && d->cfr[u] + lam[h - 1] < best) best = d->cfr[u] + lam[h - 1];
+      }
+      d->cfr[v] = best;
     }
 }
 
@@ -473,10 +493,15 @@ int oracle_create(const oracle_problem *p, double clamp, int n_threads, oracle_s
     for (int64_t q = s->var_ptr[i]; q < s->var_ptr[i + 1]; ++q)
       s->lambda[s->var_slots[q]] = s->cost[i] / (double)deg;
   }
-  /* shp(v, T) under the initial lambda, so the first forward pass can use it */
-  for (int32_t j = 0; j < p->n_cons; ++j) backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+  /* shp(v, T) under the initial lambda, so the first forward pass can use it;
+   * shp(r, v) too, for a caller that starts with a backward pass */
+  for (int32_t j = 0; j < p->n_cons; ++j) {
+    backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+    forward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+  }
   s->lb = raw_energy(s);
   s->passes = 0;
+  s->ctt_ok = s->cfr_ok = 1;
   *out = s;
   return O_OK;
 fail:
@@ -497,6 +522,11 @@ int oracle_pass(oracle_solver *s, int forward, double omega) {
     for (int64_t q = s->var_ptr[i]; q < s->var_ptr[i + 1]; ++q) sum += s->delta_bar[s->var_slots[q]];
     s->avg[i] = sum / (double)deg;
   }
+  /* stored distances of the opposite direction must match the current lambda */
+  if (forward && !s->ctt_ok)
+    for (int32_t q = 0; q < s->n_cons; ++q) backward_dp(&s->bdd[q], s->lambda + s->bdd[q].slot0);
+  if (!forward && !s->cfr_ok)
+    for (int32_t q = 0; q < s->n_cons; ++q) forward_dp(&s->bdd[q], s->lambda + s->bdd[q].slot0);
   /* for j in J in parallel */
   int j;
 #pragma omp parallel for num_threads(s->n_threads) schedule(dynamic, 256)
@@ -515,6 +545,8 @@ int oracle_pass(oracle_solver *s, int forward, double omega) {
   for (int64_t q = 0; q < s->n_slots; ++q) neg += s->delta_bar[q] < 0 ? s->delta_bar[q] : 0.0;
   s->lb = e + neg;
   s->passes++;
+  s->ctt_ok = !forward; /* a forward pass leaves shp(r,v) valid, a backward pass shp(v,T) */
+  s->cfr_ok = forward;
   return O_OK;
 }
 
@@ -548,8 +580,12 @@ int oracle_finalize(oracle_solver *s) {
     s->lambda[q] += s->delta_bar[q];
     s->delta_bar[q] = 0.0;
   }
-  for (int32_t j = 0; j < s->n_cons; ++j) backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+  for (int32_t j = 0; j < s->n_cons; ++j) {
+    backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+    forward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+  }
   s->lb = raw_energy(s);
+  s->ctt_ok = s->cfr_ok = 1;
   return O_OK;
 }
 
@@ -585,8 +621,12 @@ int oracle_min_marginals(const oracle_solver *s, double *m0, double *m1, int64_t
 int oracle_set_lambda(oracle_solver *s, const double *lambda, int64_t len) {
   if (!s || !lambda || len != s->n_slots) return O_EINVAL;
   memcpy(s->lambda, lambda, (size_t)len * sizeof(double));
-  for (int32_t j = 0; j < s->n_cons; ++j) backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+  for (int32_t j = 0; j < s->n_cons; ++j) {
+    backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+    forward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+  }
   s->lb = raw_energy(s);
+  s->ctt_ok = s->cfr_ok = 1;
   return O_OK;
 }
 

@@ -30,25 +30,59 @@ struct Shape {
   int32_t nodes() const { return hop_start.empty() ? 0 : hop_start.back(); }
 };
 
-// Device tile descriptor: 32 BDDs with the same number of hops K, one per lane.
-//   kind 0 ("shared topology"): all lanes use one Shape, topology entry of node n
-//          at topo[topo_base + n]  (warp-uniform load);
-//   kind 1 ("per-lane topology"): entry of node n, lane l at
-//          topo[topo_base + n*32 + l]  (coalesced), partitions padded to the
-//          widest lane with (bot, bot) nodes.
+// Device tile descriptor: L (= lanes, 4..32) BDDs with the same number of
+// partitions K, one per lane.  Per-lane arrays use the [index][L] layout.
+//   kind bit 0 clear ("shared topology"): all lanes use one Shape; topology
+//          entry of node n at topo[topo_base + n]  (warp-uniform load);
+//   kind bit 0 set ("per-lane topology"): entry of node n, lane l at
+//          topo[topo_base + n*L + l], partitions padded to the widest lane
+//          with (bottom, bottom) nodes;
+//   kind bit 1 set: staged through shared memory by TMA (fits the per-warp
+//          budget); clear: processed from global memory (L = 32).
+// Topology entries are absolute child indices within the tile (s^0 in the low
+// 16 bits, s^1 in the high 16 bits), top = nodes, bottom = nodes + 1.
 // Partition offsets of the tile: hop_off[hop_base + h], h = 0..K.
-// Slot (h, lane) of the tile: slot_base + h*32 + lane.
+// Slot (h, lane) of the tile: slot_base + h*L + lane.
 struct TileDesc {
   int64_t slot_base;
   int64_t topo_base;
+  int64_t dist_base;  // distances: dist[dist_base + n*L + l], n < nodes + 2 (two sentinels)
   int32_t hop_base;
   int32_t K;
-  int32_t n_lanes;
+  int32_t n_lanes;  // valid lanes (<= lanes)
   int32_t kind;
-  int32_t nodes;   // nodes per lane (hop_off[hop_base + K])
-  int32_t max_w;   // widest partition of the tile
+  int32_t nodes;    // nodes per lane (hop_off[hop_base + K])
+  int32_t max_w;    // widest partition of the tile
+  int32_t lanes;    // L
+  int32_t pad_;
 };
-static_assert(sizeof(TileDesc) == 40, "TileDesc layout");
+static_assert(sizeof(TileDesc) == 56, "TileDesc layout");
+
+#if defined(__CUDACC__)
+#define FDOG_HD __host__ __device__ __forceinline__
+#else
+#define FDOG_HD inline
+#endif
+
+// Shared-memory layout of one warp (identical on host and device):
+//   [0, 16)                   two mbarriers
+//   [16, 16 + SB)             stage buffer 0: lambda | avg->delta | distances D[nodes + 2][L] |
+//                             topology | partition offsets
+//   [16 + SB, 16 + 2 SB)      stage buffer 1 (NB = 2 only)
+//   [16 + NB SB, + DB)        relaxation buffers R[3 (W + 1)][L]
+FDOG_HD int r16(int bytes) { return (bytes + 15) & ~15; }
+FDOG_HD int stage_lam_bytes(int tsz, int K, int L) { return r16(K * L * tsz); }
+FDOG_HD int stage_va_bytes(int tsz, int K, int L) { return r16(K * L * tsz); }
+FDOG_HD int stage_dist_bytes(int tsz, int nodes, int L) { return r16((nodes + 2) * L * tsz); }
+FDOG_HD int stage_topo_bytes(int kind, int nodes, int L) { return r16(((kind & 1) ? nodes * L : nodes) * 4); }
+FDOG_HD int stage_hop_bytes(int K) { return r16((K + 1) * 4); }
+FDOG_HD int stage_bytes(int tsz, int kind, int K, int nodes, int L) {
+  return stage_lam_bytes(tsz, K, L) + stage_va_bytes(tsz, K, L) +
+         stage_dist_bytes(tsz, nodes, L) + stage_topo_bytes(kind, nodes, L) + stage_hop_bytes(K);
+}
+FDOG_HD int relax_slots(int W) { return 3 * (W + 1); }
+FDOG_HD int relax_bytes(int tsz, int W, int L) { return r16(relax_slots(W) * L * tsz); }
+FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (16 + NB * SB + DB + 127) & ~127; }
 
 struct Plan {
   int32_t n_vars = 0, n_cons = 0, rank = 0, world = 1;
@@ -70,11 +104,19 @@ struct Plan {
   std::vector<int32_t> slot_var;    // padded device slots: variable or -1
   std::vector<int64_t> canon_slot;  // canonical local slot -> device slot
   std::vector<int32_t> canon_con, canon_pos;
-  std::vector<int32_t> var_list;    // variables with local slots, ascending
+  std::vector<int32_t> var_list;    // variables with local slots, by first device slot
   std::vector<int64_t> var_ptr;     // CSR over var_list
   std::vector<int32_t> var_slots;   // device slots, j ascending within a variable
   std::vector<int32_t> var_xidx;    // per var_list entry: index into shared_vars or -1
   std::vector<int32_t> shared_vars; // ascending global ids exchanged with other ranks
+  std::vector<int32_t> deg_list;    // |J_i| (global) per var_list entry
+  std::vector<int32_t> x_local;     // per shared var: index into var_list or -1
+  std::vector<int32_t> x_deg;       // per shared var: |J_i| (global)
+
+  // per-warp shared-memory budget the tiles were packed for (precision-specific)
+  int32_t precision = 32, SB = 0, DB = 0, NB = 2;
+  int64_t n_dist = 0;               // elements of the distance array
+  int64_t direct_tiles = 0;
 
   int64_t n_nodes = 0;              // real (unpadded) nodes on this rank
   int64_t n_slots = 0;              // real slots
@@ -87,7 +129,7 @@ void set_error(const char *fmt, ...);
 fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &plan);
 
 // ---- device launchers (kernels.cu) -------------------------------------
-enum SweepMode { kForward = 0, kBackward = 1, kEnergy = 2 };
+enum SweepMode { kForward = 0, kBackward = 1, kEnergy = 2, kCfr = 3 };
 
 struct SweepArgs {
   const TileDesc *tiles;
@@ -96,36 +138,38 @@ struct SweepArgs {
   const uint32_t *topo;
   const int32_t *slot_var;
   void *lambda;          // T*
-  const void *avg;       // T*, indexed by global variable
-  void *delta_out;       // T*
+  void *delta_out;       // T*: per slot avg_i in, delta out (in place)
   void *m0, *m1;         // T*, recorded min-marginals (may be null)
   double omega, clamp;
   double *lb_part;       // per tile
   double *lb_out;        // final (written by the last CTA)
   unsigned int *done_counter;
-  int32_t max_nodes, max_w, max_hops;
+  unsigned int *tile_counter;  // dynamic tile scheduler (reset by the last CTA)
+  int32_t max_nodes, max_w, max_hops;  // over all tiles (direct-mode scratch)
+  void *dist;               // T*, per-node distances (store design)
+  int32_t SB, DB, NB;       // per-warp stage-buffer / relaxation budgets (bytes), stage buffers
+  void *scratch;            // T*, [warps][scratch_stride] for direct tiles
+  int64_t scratch_stride;   // elements per warp
 };
 
 struct AvgArgs {
   int32_t n;                 // entries of var_list
-  const int32_t *var_list;
-  const int64_t *var_ptr;
-  const int32_t *var_slots;
+  const int64_t *var_ptr;    // CSR over var_list
+  const int32_t *var_slots;  // device slots, ascending j within a variable
   const int32_t *var_xidx;   // may be null (world == 1)
-  const int32_t *deg;        // |J_i| global, indexed by variable
-  const void *delta_bar;     // T*
-  void *avg;                 // T*
+  const int32_t *deg_l;      // |J_i| (global) per var_list entry
+  const void *delta_bar;     // T*: delta of the last pass
+  void *avg_slot;            // T*: avg_i written into every slot of i (the other delta buffer)
   void *xbuf;                // T* partial sums of shared variables (may be null)
 };
 
 // returns the cudaError_t as int
 int launch_sweep(int precision, int mode, bool record, const SweepArgs &a, int grid, int block,
                  size_t smem, void *stream);
-int sweep_smem_bytes(int precision, int max_nodes, int max_w, int max_hops, int warps);
 int sweep_occupancy(int precision, int mode, bool record, int block, size_t smem, int *blocks_per_sm);
 int launch_avg(int precision, const AvgArgs &a, void *stream);
-int launch_avg_finish(int precision, int32_t n_shared, const int32_t *shared_vars, const int32_t *deg,
-                      const void *xbuf, void *avg, void *stream);
+int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,
+                      void *stream);
 int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, void *stream);
 int launch_fill(int precision, int64_t n, void *dst, double value, void *stream);
 

@@ -18,6 +18,7 @@
 // topology + per-slot data only.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -57,8 +58,11 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Last CTA reduces the per-tile bound partials in a fixed order (deterministic).
-__device__ void reduce_lb_last_cta(const double *lb_part, int n, double *out, unsigned int *counter) {
+// Last CTA reduces the per-tile bound partials in a fixed order (deterministic
+// for any tile-to-warp assignment): thread q sums the contiguous chunk q of
+// lb_part with independent L2 loads, then a fixed-shape block reduction.
+__device__ void reduce_lb_last_cta(const double *lb_part, int n, double *out, unsigned int *counter,
+                                   unsigned int *tile_counter) {
   __shared__ bool is_last;
   __shared__ double red[32];
   __syncthreads();
@@ -70,8 +74,18 @@ __device__ void reduce_lb_last_cta(const double *lb_part, int n, double *out, un
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  double s = 0.0;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) s += ((volatile const double *)lb_part)[q];
+  const int chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int q0 = threadIdx.x * chunk, q1 = min(n, q0 + chunk);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int q = q0;
+  for (; q + 3 < q1; q += 4) {
+    s0 += __ldcg(lb_part + q);
+    s1 += __ldcg(lb_part + q + 1);
+    s2 += __ldcg(lb_part + q + 2);
+    s3 += __ldcg(lb_part + q + 3);
+  }
+  for (; q < q1; ++q) s0 += __ldcg(lb_part + q);
+  double s = (s0 + s1) + (s2 + s3);
   s = warp_sum(s);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) red[warp] = s;
@@ -82,213 +96,426 @@ __device__ void reduce_lb_last_cta(const double *lb_part, int n, double *out, un
     if (lane == 0) {
       *out = v;
       *counter = 0u;
+      *tile_counter = 0u;
     }
   }
 }
 
+// ---- PTX helpers: mbarrier + TMA bulk copies (sm_90+/sm_100a) and cp.async
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+// TMA 1D bulk copy global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// TMA 1D bulk copy shared -> global (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T *dst, const T *src) {
+  if (sizeof(T) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// One lane's BDD, one pass (store design).  Pointers are
+// per-lane (column offset applied) with a stride of L elements per
+// partition/node; they point to shared memory (staged tiles) or global memory
+// (direct tiles).  Topology words hold the ABSOLUTE child index within the
+// tile (s^0 low 16 bits, s^1 high 16 bits); top = nodes and bottom = nodes + 1
+// index two constant sentinel slots of D (0 and +inf), so a child lookup is a
+// single load.
+//   D   : per node, on entry shp(v, T) (kForward) or shp(r, v) (kBackward);
+//         on exit the other one (the pass converts it in place, hop by hop).
+//         kEnergy writes shp(v, T), kCfr writes shp(r, v) (no update).
+//   lam : lambda_h at lam[h*L], updated in place
+//   va  : per partition: the deferred average avg_i of its variable in (written
+//         by avg_kernel), delta_h = omega (m1 - m0) out (kForward / kBackward)
+//   R   : 3 * (rw + 1) scratch entries (forward relaxation buffers)
+// Returns the lane's bound contribution E^j + sum_h min(delta_h, 0) (A7), or E^j.
 template <typename T, int MODE, bool REC>
-__global__ void __launch_bounds__(256) sweep_kernel(const SweepArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ double process_bdd(const int K, const int nodes, const int32_t *ho, const uint32_t *tp,
+                                              const int ts, const int L, T *lam, T *va, T *D, T *R, const int rw,
+                                              const bool valid, const T omega, const T clamp, T *m0g, T *m1g) {
+  const T inf = t_inf<T>();
+  double acc = 0.0;
+  auto emit = [&](int h, T lam_new, T delta, T m0, T m1) {
+    if (!valid) {
+      va[h * L] = T(0);
+      return;
+    }
+    lam[h * L] = lam_new;
+    va[h * L] = delta;
+    if (REC) {
+      m0g[h * L] = m0;
+      m1g[h * L] = m1;
+    }
+  };
+  if (MODE == kEnergy) {
+    // shp(v, T) for all nodes under the current lambda
+#pragma unroll 1
+    for (int h = K - 1; h >= 0; --h) {
+      const T l = lam[h * L];
+      const int n1 = ho[h + 1];
+#pragma unroll 1
+      for (int n = ho[h]; n < n1; ++n) {
+        const uint32_t e = tp[n * ts];
+        D[n * L] = fmin(D[(e & 0xFFFFu) * L], l + D[(e >> 16) * L]);
+      }
+    }
+    return valid ? (double)D[0] : 0.0;  // E^j = shp(r, T)
+  }
+  if (MODE == kCfr) {
+    // shp(r, v) for all nodes under the current lambda, relaxed
+    // through the R buffers (no writes into the sentinels)
+    T *cur = R, *nlo = R + (rw + 1) * L, *nhi = R + 2 * (rw + 1) * L;
+    cur[0] = T(0);
+#pragma unroll 1
+    for (int h = 0; h < K; ++h) {
+      const int n0 = ho[h], n1 = ho[h + 1];
+      const int Wn = h == K - 1 ? 0 : ho[h + 2] - n1;
+#pragma unroll 1
+      for (int w = 0; w < Wn; ++w) {
+        nlo[w * L] = inf;
+        nhi[w * L] = inf;
+      }
+      T e_min = inf;
+      const T l = lam[h * L];
+#pragma unroll 1
+      for (int n = n0; n < n1; ++n) {
+        const uint32_t e = tp[n * ts];
+        const int lo = (int)(e & 0xFFFFu), hi = (int)(e >> 16);
+        const T cf = cur[(n - n0) * L];
+        D[n * L] = cf;
+        const int rl = min(lo - n1, rw), rh = min(hi - n1, rw);
+        nlo[rl * L] = fmin(nlo[rl * L], cf);
+        nhi[rh * L] = fmin(nhi[rh * L], cf);
+        if (h == K - 1) e_min = fmin(e_min, fmin(cf + D[lo * L], cf + l + D[hi * L]));
+      }
+#pragma unroll 1
+      for (int w = 0; w < Wn; ++w) cur[w * L] = fmin(nlo[w * L], nhi[w * L] + l);
+      if (h == K - 1 && valid) acc = (double)e_min;
+    }
+    return acc;
+  }
+  if (MODE == kForward) {
+    // forward pass with updates (Alg. forward_pass_mm): D holds
+    // shp(v, T) from the previous pass, valid for P_{h+1} at hop h;
+    // R holds shp(r, .) of P_h (cur) and the 0-/1-arc relaxations into P_{h+1}
+    // (nlo, nhi), each rw + 1 entries (the last is a sink for arcs to bottom).
+    T *cur = R, *nlo = R + (rw + 1) * L, *nhi = R + 2 * (rw + 1) * L;
+    cur[0] = T(0);  // shp(r, r)
+#pragma unroll 1
+    for (int h = 0; h < K; ++h) {
+      const int n0 = ho[h], n1 = ho[h + 1];
+      const bool last = h == K - 1;
+      const int Wn = last ? 0 : ho[h + 2] - n1;
+#pragma unroll 1
+      for (int w = 0; w < Wn; ++w) {
+        nlo[w * L] = inf;
+        nhi[w * L] = inf;
+      }
+      T m0 = inf, m1r = inf;  // m1r = min(shp(r,v) + shp(s1 v, T)); lambda added below
+#pragma unroll 1
+      for (int n = n0; n < n1; ++n) {
+        const uint32_t e = tp[n * ts];
+        const int lo = (int)(e & 0xFFFFu), hi = (int)(e >> 16);
+        const T cf = cur[(n - n0) * L];
+        D[n * L] = cf;  // shp(v, T) of P_h is no longer needed: keep shp(r, v)
+        m0 = fmin(m0, cf + D[lo * L]);
+        m1r = fmin(m1r, cf + D[hi * L]);
+        const int rl = min(lo - n1, rw), rh = min(hi - n1, rw);
+        nlo[rl * L] = fmin(nlo[rl * L], cf);
+        nhi[rh * L] = fmin(nhi[rh * L], cf);
+      }
+      const T l = lam[h * L];
+      const T m1 = l + m1r;  // Eq. (min-marginal-via-shortest-path) P:312
+      const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+      const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
+      emit(h, lam_new, delta, m0, m1);
+      if (valid) acc += (double)fmin(delta, T(0));
+      if (!last) {
+        // shp(r, v), v in P_{h+1}: 1-arcs priced with the updated lambda_h (A4)
+#pragma unroll 1
+        for (int w = 0; w < Wn; ++w) cur[w * L] = fmin(nlo[w * L], nhi[w * L] + lam_new);
+      } else if (valid) {
+        acc += (double)fmin(m0, lam_new + m1r);  // E^j at the updated lambda
+      }
+    }
+    return acc;
+  }
+  // MODE == kBackward (Alg. backward_pass_mm): D holds shp(r, v)
+  // from the forward pass, valid for P_h at hop h; shp(v, T) of P_{h+1} was
+  // written into D by the previous hop of this pass.
+#pragma unroll 1
+  for (int h = K - 1; h >= 0; --h) {
+    const int n0 = ho[h], n1 = ho[h + 1];
+    T m0 = inf, m1r = inf;
+#pragma unroll 1
+    for (int n = n0; n < n1; ++n) {
+      const uint32_t e = tp[n * ts];
+      const T cf = D[n * L];
+      m0 = fmin(m0, cf + D[(e & 0xFFFFu) * L]);
+      m1r = fmin(m1r, cf + D[(e >> 16) * L]);
+    }
+    const T l = lam[h * L];
+    const T m1 = l + m1r;
+    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+    const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
+    emit(h, lam_new, delta, m0, m1);
+    if (valid) acc += (double)fmin(delta, T(0));
+    // shp(v, T), v in P_h, with the updated lambda_h
+#pragma unroll 1
+    for (int n = n0; n < n1; ++n) {
+      const uint32_t e = tp[n * ts];
+      D[n * L] = fmin(D[(e & 0xFFFFu) * L], lam_new + D[(e >> 16) * L]);
+    }
+  }
+  if (valid) acc += (double)D[0];  // E^j = shp(r, T)
+  return acc;
+}
+
+// Stage buffer of one tile (layout: internal.h).
+template <typename T>
+struct Stage {
+  T *lam;
+  T *va;
+  T *dist;
+  uint32_t *topo;
+  int32_t *hop;
+};
+
+template <typename T>
+__device__ __forceinline__ Stage<T> stage_at(unsigned char *base, const TileDesc &d) {
+  constexpr int tsz = sizeof(T);
+  Stage<T> s;
+  unsigned char *p = base;
+  s.lam = reinterpret_cast<T *>(p);
+  p += stage_lam_bytes(tsz, d.K, d.lanes);
+  s.va = reinterpret_cast<T *>(p);
+  p += stage_va_bytes(tsz, d.K, d.lanes);
+  s.dist = reinterpret_cast<T *>(p);
+  p += stage_dist_bytes(tsz, d.nodes, d.lanes);
+  s.topo = reinterpret_cast<uint32_t *>(p);
+  p += stage_topo_bytes(d.kind, d.nodes, d.lanes);
+  s.hop = reinterpret_cast<int32_t *>(p);
+  return s;
+}
+
+// One lane issues the TMA bulk copies of a tile's lambda, variables, topology
+// and partition offsets; completion is counted on the stage's mbarrier.
+template <typename T, int MODE>
+__device__ __forceinline__ void issue_stage(const SweepArgs &a, const TileDesc &d, const Stage<T> &s, uint64_t *bar) {
+  const bool upd = MODE == kForward || MODE == kBackward;
+  const uint32_t lam_b = (uint32_t)d.K * d.lanes * sizeof(T);
+  const uint32_t va_b = upd ? lam_b : 0u;
+  const uint32_t dist_b = (uint32_t)(d.nodes + 2) * d.lanes * sizeof(T);
+  const uint32_t topo_b = (uint32_t)stage_topo_bytes(d.kind, d.nodes, d.lanes);
+  const uint32_t hop_b = (uint32_t)stage_hop_bytes(d.K);
+  mbar_expect_tx(bar, lam_b + va_b + dist_b + topo_b + hop_b);
+  bulk_g2s(s.lam, reinterpret_cast<const T *>(a.lambda) + d.slot_base, lam_b, bar);
+  if (va_b) bulk_g2s(s.va, reinterpret_cast<const T *>(a.delta_out) + d.slot_base, va_b, bar);
+  bulk_g2s(s.dist, reinterpret_cast<const T *>(a.dist) + d.dist_base, dist_b, bar);
+  bulk_g2s(s.topo, a.topo + d.topo_base, topo_b, bar);
+  bulk_g2s(s.hop, a.hop_off + d.hop_base, hop_b, bar);
+}
+
+// One pass over all tiles.  Persistent warps claim tiles dynamically; with
+// two stage buffers the next tile's TMA loads are in flight while the current
+// one is processed.  lambda, delta and the distances go back with TMA bulk
+// stores.
+template <typename T, int MODE, bool REC>
+__global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
+  constexpr bool kUpd = MODE == kForward || MODE == kBackward;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
-  const size_t per_warp = (size_t)(a.max_nodes + 4 * a.max_w + 2 * a.max_hops) * 32;
-  T *const dist = reinterpret_cast<T *>(smem_raw) + warp * per_warp + lane;  // [node][32]
-  T *const ringA = dist + (size_t)a.max_nodes * 32;                          // [2*max_w][32]
-  T *const ringB = ringA + (size_t)2 * a.max_w * 32;                         // [2*max_w][32]
-  T *const lam_s = ringB + (size_t)2 * a.max_w * 32;                         // [max_hops][32]
-  T *const avg_s = lam_s + (size_t)a.max_hops * 32;                          // [max_hops][32]
+  unsigned char *wbase = smem_raw + (size_t)warp * warp_bytes(a.SB, a.DB, a.NB);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(wbase);  // bar[0], bar[1]
+  unsigned char *const sbuf0 = wbase + 16;
+  unsigned char *const sbuf1 = wbase + 16 + (a.NB > 1 ? a.SB : 0);
+  unsigned char *const rbase = wbase + 16 + a.NB * a.SB;
 
-  const T *__restrict__ avg = reinterpret_cast<const T *>(a.avg);
   T *__restrict__ lambda = reinterpret_cast<T *>(a.lambda);
   T *__restrict__ delta_out = reinterpret_cast<T *>(a.delta_out);
-  const T inf = t_inf<T>();
+  T *__restrict__ gdist = reinterpret_cast<T *>(a.dist);
   const T omega = T(a.omega), clamp = T(a.clamp);
+  const int gwarp = blockIdx.x * wpb + warp;
 
-  const int nwarps = gridDim.x * wpb;
-  for (int t = blockIdx.x * wpb + warp; t < a.n_tiles; t += nwarps) {
-    const TileDesc d = a.tiles[t];
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // dynamic tile scheduler: lane 0 claims tiles from a global counter (reset by
+  // the last CTA); claims run one tile ahead so the atomic's latency overlaps
+  // the current tile
+  auto claim = [&]() -> int {
+    int x = 0;
+    if (lane == 0) x = (int)atomicAdd(a.tile_counter, 1u);
+    return __shfl_sync(0xffffffffu, x, 0);
+  };
+  uint32_t phase = 0;  // bit b = parity of bar[b]
+  int b = 0;
+  int t = claim();
+  TileDesc d;
+  if (t < a.n_tiles) {
+    d = a.tiles[t];
+    if ((d.kind & 2) && lane == 0) issue_stage<T, MODE>(a, d, stage_at<T>(sbuf0, d), &bar[0]);
+  }
+  int tn = t < a.n_tiles ? claim() : a.n_tiles;
+  while (t < a.n_tiles) {
+    TileDesc dn;
+    const bool has_next = tn < a.n_tiles;
+    if (has_next) dn = a.tiles[tn];
+    const int bn = a.NB > 1 ? (b ^ 1) : 0;
+    if (a.NB > 1 && has_next && (dn.kind & 2) && lane == 0) {
+      bulk_wait_read_all();  // the bulk stores issued from stage bn have read their source
+      issue_stage<T, MODE>(a, dn, stage_at<T>(bn ? sbuf1 : sbuf0, dn), &bar[bn]);
+    }
+    const int tnn = has_next ? claim() : a.n_tiles;
+    const int L = d.lanes;
+    const bool active = lane < L;
     const bool valid = lane < d.n_lanes;
-    const int32_t *__restrict__ ho = a.hop_off + d.hop_base;
-    const uint32_t *__restrict__ tp;
-    int ts;
-    if (d.kind == 0) {
-      tp = a.topo + d.topo_base;
-      ts = 1;
-    } else {
-      tp = a.topo + d.topo_base + lane;
-      ts = 32;
-    }
     const int K = d.K;
-    const int64_t sb = d.slot_base + lane;
-
-    // stage lambda (and the deferred averages) of this lane's BDD
-    for (int h = 0; h < K; ++h) {
-      const int64_t s = sb + (int64_t)h * 32;
-      lam_s[h * 32] = lambda[s];
-      if (MODE != kEnergy) {
-        const int v = a.slot_var[s];
-        avg_s[h * 32] = v >= 0 ? __ldg(avg + v) : T(0);
-      }
-    }
-
     double acc = 0.0;
-    if (MODE == kForward || MODE == kEnergy) {
-      // phase 1: shp(v, T) for all nodes under the current lambda
-      for (int h = K - 1; h >= 0; --h) {
-        const T lam = lam_s[h * 32];
-        const int n0 = ho[h], n1 = ho[h + 1];
-        for (int n = n0; n < n1; ++n) {
-          const uint32_t e = __ldg(tp + (size_t)n * ts);
-          const uint32_t lo = e & 0xFFFFu, hi = e >> 16;
-          const T c0 = lo == kBot ? inf : lo == kTop ? T(0) : dist[(size_t)(n1 + lo) * 32];
-          const T c1 = hi == kBot ? inf : hi == kTop ? T(0) : dist[(size_t)(n1 + hi) * 32];
-          dist[(size_t)n * 32] = fmin(c0, lam + c1);
-        }
+    if (d.kind & 2) {
+      // staged tile: everything on chip
+      const Stage<T> s = stage_at<T>(b ? sbuf1 : sbuf0, d);
+      mbar_wait(&bar[b], (phase >> b) & 1u);
+      phase ^= 1u << b;
+      if (active) {
+        const uint32_t *tp = (d.kind & 1) ? s.topo + lane : s.topo;
+        T *R = reinterpret_cast<T *>(rbase) + lane;
+        T *m0p = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
+        T *m1p = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
+        acc = process_bdd<T, MODE, REC>(K, d.nodes, s.hop, tp, (d.kind & 1) ? L : 1, L, s.lam + lane, s.va + lane,
+                                        s.dist + lane, R, d.max_w, valid, omega, clamp, m0p, m1p);
       }
-      if (MODE == kEnergy) {
-        acc = valid ? (double)dist[0] : 0.0;  // E^j = shp(r, T)
-      } else {
-        // phase 2: forward pass with updates (Alg. forward_pass_mm)
-        T *cur = ringA, *nxt = ringA + (size_t)a.max_w * 32;
-        T *nlo = ringB, *nhi = ringB + (size_t)a.max_w * 32;
-        cur[0] = T(0);  // shp(r, r)
-        for (int h = 0; h < K; ++h) {
-          const int n0 = ho[h], n1 = ho[h + 1];
-          const bool last = h == K - 1;
-          const int Wn = last ? 0 : ho[h + 2] - n1;
-          for (int w = 0; w < Wn; ++w) {
-            nlo[w * 32] = inf;
-            nhi[w * 32] = inf;
-          }
-          T m0 = inf, m1r = inf;  // m1r = min (shp(r,v) + shp(s1 v, T)), lambda added below
-          for (int n = n0; n < n1; ++n) {
-            const uint32_t e = __ldg(tp + (size_t)n * ts);
-            const uint32_t lo = e & 0xFFFFu, hi = e >> 16;
-            const T cf = cur[(n - n0) * 32];
-            if (lo != kBot) {
-              const T c = lo == kTop ? T(0) : dist[(size_t)(n1 + lo) * 32];
-              m0 = fmin(m0, cf + c);
-              if (!last) nlo[lo * 32] = fmin(nlo[lo * 32], cf);
-            }
-            if (hi != kBot) {
-              const T c = hi == kTop ? T(0) : dist[(size_t)(n1 + hi) * 32];
-              m1r = fmin(m1r, cf + c);
-              if (!last) nhi[hi * 32] = fmin(nhi[hi * 32], cf);
-            }
-          }
-          const T lam = lam_s[h * 32];
-          const T m1 = lam + m1r;  // Eq. (min-marginal-via-shortest-path) P:312
-          const T dd = mm_difference(m1, m0, clamp);
-          const T delta = mul_rn(omega, dd);
-          const T lam_new = add_rn(sub_rn(lam, delta), avg_s[h * 32]);
-          if (valid) {
-            const int64_t s = sb + (int64_t)h * 32;
-            lambda[s] = lam_new;
-            delta_out[s] = delta;
-            if (REC) {
-              reinterpret_cast<T *>(a.m0)[s] = m0;
-              reinterpret_cast<T *>(a.m1)[s] = m1;
-            }
-            acc += (double)fmin(delta, T(0));
-          }
-          if (!last) {
-            // shp(r, v) for v in P_{h+1}, 1-arcs priced with the updated lambda_h (A4)
-            for (int w = 0; w < Wn; ++w) nxt[w * 32] = fmin(nlo[w * 32], nhi[w * 32] + lam_new);
-            T *tmp = cur;
-            cur = nxt;
-            nxt = tmp;
-          } else if (valid) {
-            acc += (double)fmin(m0, lam_new + m1r);  // E^j at the updated lambda
-          }
+      fence_proxy_async();  // lanes' shared-memory writes -> visible to the TMA stores
+      __syncwarp();
+      if (lane == 0) {
+        if (kUpd) {
+          const uint32_t bytes = (uint32_t)K * L * sizeof(T);
+          bulk_s2g(lambda + d.slot_base, s.lam, bytes);
+          bulk_s2g(delta_out + d.slot_base, s.va, bytes);
         }
+        bulk_s2g(gdist + d.dist_base, s.dist, (uint32_t)(d.nodes + 2) * L * sizeof(T));
+        bulk_commit();
       }
     } else {
-      // phase 1: shp(r, v) for all nodes under the current lambda
-      dist[0] = T(0);
-      for (int h = 0; h + 1 < K; ++h) {
-        const T lam = lam_s[h * 32];
-        const int n0 = ho[h], n1 = ho[h + 1], n2 = ho[h + 2];
-        for (int n = n1; n < n2; ++n) dist[(size_t)n * 32] = inf;
-        for (int n = n0; n < n1; ++n) {
-          const uint32_t e = __ldg(tp + (size_t)n * ts);
-          const uint32_t lo = e & 0xFFFFu, hi = e >> 16;
-          const T cf = dist[(size_t)n * 32];
-          if (lo != kBot) dist[(size_t)(n1 + lo) * 32] = fmin(dist[(size_t)(n1 + lo) * 32], cf);
-          if (hi != kBot) dist[(size_t)(n1 + hi) * 32] = fmin(dist[(size_t)(n1 + hi) * 32], cf + lam);
-        }
-      }
-      // phase 2: backward pass with updates (Alg. backward_pass_mm)
-      T *cur = ringA, *nxt = ringA + (size_t)a.max_w * 32;  // shp(., T) of P_{h+1}, P_h
-      T *c0s = ringB, *c1s = ringB + (size_t)a.max_w * 32;
-      for (int h = K - 1; h >= 0; --h) {
-        const int n0 = ho[h], n1 = ho[h + 1];
-        T m0 = inf, m1r = inf;
-        for (int n = n0; n < n1; ++n) {
-          const uint32_t e = __ldg(tp + (size_t)n * ts);
-          const uint32_t lo = e & 0xFFFFu, hi = e >> 16;
-          const T cf = dist[(size_t)n * 32];
-          const T c0 = lo == kBot ? inf : lo == kTop ? T(0) : cur[lo * 32];
-          const T c1 = hi == kBot ? inf : hi == kTop ? T(0) : cur[hi * 32];
-          c0s[(n - n0) * 32] = c0;
-          c1s[(n - n0) * 32] = c1;
-          if (lo != kBot) m0 = fmin(m0, cf + c0);
-          if (hi != kBot) m1r = fmin(m1r, cf + c1);
-        }
-        const T lam = lam_s[h * 32];
-        const T m1 = lam + m1r;
-        const T dd = mm_difference(m1, m0, clamp);
-        const T delta = mul_rn(omega, dd);
-        const T lam_new = add_rn(sub_rn(lam, delta), avg_s[h * 32]);
-        if (valid) {
-          const int64_t s = sb + (int64_t)h * 32;
-          lambda[s] = lam_new;
-          delta_out[s] = delta;
-          if (REC) {
-            reinterpret_cast<T *>(a.m0)[s] = m0;
-            reinterpret_cast<T *>(a.m1)[s] = m1;
-          }
-          acc += (double)fmin(delta, T(0));
-        }
-        // shp(v, T) for v in P_h with the updated lambda_h
-        for (int w = 0; w < n1 - n0; ++w) nxt[w * 32] = fmin(c0s[w * 32], lam_new + c1s[w * 32]);
-        T *tmp = cur;
-        cur = nxt;
-        nxt = tmp;
-      }
-      if (valid) acc += (double)cur[0];  // E^j = shp(r, T)
+      // direct tile (exceeds the per-warp budget; L = 32): global memory and a
+      // per-warp scratch area for the relaxation buffers
+      const int64_t sbase = d.slot_base + lane;
+      const uint32_t *tp = (d.kind & 1) ? a.topo + d.topo_base + lane : a.topo + d.topo_base;
+      T *R = reinterpret_cast<T *>(a.scratch) + (size_t)gwarp * a.scratch_stride + lane;
+      T *m0p = REC ? reinterpret_cast<T *>(a.m0) + sbase : nullptr;
+      T *m1p = REC ? reinterpret_cast<T *>(a.m1) + sbase : nullptr;
+      acc = process_bdd<T, MODE, REC>(K, d.nodes, a.hop_off + d.hop_base, tp, (d.kind & 1) ? 32 : 1, 32,
+                                      lambda + sbase, delta_out + sbase, gdist + d.dist_base + lane, R, d.max_w,
+                                      valid, omega, clamp, m0p, m1p);
     }
     acc = warp_sum(acc);
     if (lane == 0) a.lb_part[t] = acc;
+    __syncwarp();
+    if (a.NB == 1 && has_next && (dn.kind & 2) && lane == 0) {
+      bulk_wait_read_all();  // single stage buffer: its stores must have read it
+      issue_stage<T, MODE>(a, dn, stage_at<T>(sbuf0, dn), &bar[0]);
+    }
+    t = tn;
+    d = dn;
+    tn = tnn;
+    b = bn;
   }
-  reduce_lb_last_cta(a.lb_part, a.n_tiles, a.lb_out, a.done_counter);
+  if (lane == 0) bulk_wait_read_all();  // shared memory must outlive the TMA stores' reads
+  __syncwarp();
+  reduce_lb_last_cta(a.lb_part, a.n_tiles, a.lb_out, a.done_counter, a.tile_counter);
 }
 
+// Deferred averaging (A1): one thread per variable of the local list.
+// avg_i = (sum over the slots of i, in CSR order = ascending j, of delta_bar) /
+// |J_i| is written into every slot of i of the OTHER delta buffer, where the
+// next sweep reads it (and overwrites it with its own delta).
 template <typename T>
 __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
-  T *__restrict__ avg = reinterpret_cast<T *>(a.avg);
+  T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
   T *__restrict__ xbuf = reinterpret_cast<T *>(a.xbuf);
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < a.n; q += gridDim.x * blockDim.x) {
-    const int64_t p0 = a.var_ptr[q], p1 = a.var_ptr[q + 1];
-    T s = T(0);
-    for (int64_t p = p0; p < p1; ++p) s += __ldg(db + a.var_slots[p]);  // k in J_i ascending
-    const int x = a.var_xidx ? a.var_xidx[q] : -1;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= a.n) return;
+  const int64_t p0 = __ldg(a.var_ptr + q), p1 = __ldg(a.var_ptr + q + 1);
+  const int x = a.var_xidx ? __ldg(a.var_xidx + q) : -1;
+  const int deg = __ldg(a.deg_l + q);
+  if (p1 - p0 == 2) {
+    const int sa = __ldg(a.var_slots + p0), sb = __ldg(a.var_slots + p0 + 1);
+    const T s = __ldg(db + sa) + __ldg(db + sb);
     if (x >= 0) {
       xbuf[x] = s;
     } else {
-      const int i = a.var_list[q];
-      avg[i] = s / T(a.deg[i]);
+      const T v = s / T(deg);
+      out[sa] = v;
+      out[sb] = v;
     }
+    return;
   }
+  T s = T(0);
+  int64_t p = p0;
+  for (; p + 1 < p1; p += 2) {
+    const int sa = __ldg(a.var_slots + p), sb = __ldg(a.var_slots + p + 1);
+    const T va = __ldg(db + sa), vb = __ldg(db + sb);
+    s += va;
+    s += vb;
+  }
+  if (p < p1) s += __ldg(db + __ldg(a.var_slots + p));
+  if (x >= 0) {
+    xbuf[x] = s;
+    return;
+  }
+  const T v = s / T(deg);
+  for (p = p0; p < p1; ++p) out[__ldg(a.var_slots + p)] = v;
 }
 
+// Shared variables after the NCCL exchange: average and scatter into the local slots.
 template <typename T>
-__global__ void avg_finish_kernel(int32_t n, const int32_t *__restrict__ vars, const int32_t *__restrict__ deg,
-                                  const T *__restrict__ xbuf, T *__restrict__ avg) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-    const int i = vars[q];
-    avg[i] = xbuf[q] / T(deg[i]);
+__global__ void avg_finish_kernel(const AvgArgs a, int32_t n_shared, const int32_t *__restrict__ xlocal,
+                                  const int32_t *__restrict__ deg_x) {
+  const T *__restrict__ xbuf = reinterpret_cast<const T *>(a.xbuf);
+  T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_shared; q += gridDim.x * blockDim.x) {
+    const int l = xlocal[q];
+    if (l < 0) continue;  // exchanged variable this rank does not hold
+    const T v = xbuf[q] / T(deg_x[q]);
+    for (int64_t p = a.var_ptr[l]; p < a.var_ptr[l + 1]; ++p) out[a.var_slots[p]] = v;
   }
 }
 
@@ -312,17 +539,12 @@ template <typename T>
 static const void *sweep_fn(int mode, bool rec) {
   if (mode == kForward) return rec ? (const void *)sweep_kernel<T, kForward, true> : (const void *)sweep_kernel<T, kForward, false>;
   if (mode == kBackward) return rec ? (const void *)sweep_kernel<T, kBackward, true> : (const void *)sweep_kernel<T, kBackward, false>;
+  if (mode == kCfr) return (const void *)sweep_kernel<T, kCfr, false>;
   return (const void *)sweep_kernel<T, kEnergy, false>;
 }
 
 static const void *sweep_ptr(int precision, int mode, bool rec) {
   return precision == 64 ? sweep_fn<double>(mode, rec) : sweep_fn<float>(mode, rec);
-}
-
-int sweep_smem_bytes(int precision, int max_nodes, int max_w, int max_hops, int warps) {
-  const size_t tsz = precision == 64 ? 8 : 4;
-  size_t b = (size_t)warps * (size_t)(max_nodes + 4 * max_w + 2 * max_hops) * 32 * tsz;
-  return b > (size_t)0x7fffffff ? 0x7fffffff : (int)b;
 }
 
 int sweep_occupancy(int precision, int mode, bool rec, int block, size_t smem, int *blocks_per_sm) {
@@ -348,7 +570,7 @@ static int grid_for(int64_t n, int block) {
 
 int launch_avg(int precision, const AvgArgs &a, void *stream) {
   const int block = 256;
-  const int grid = grid_for(a.n, block);
+  const int grid = (int)std::max<int64_t>(1, ((int64_t)a.n + block - 1) / block);
   if (precision == 64)
     avg_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(a);
   else
@@ -356,14 +578,14 @@ int launch_avg(int precision, const AvgArgs &a, void *stream) {
   return (int)cudaGetLastError();
 }
 
-int launch_avg_finish(int precision, int32_t n, const int32_t *vars, const int32_t *deg, const void *xbuf,
-                      void *avg, void *stream) {
-  if (n <= 0) return 0;
-  const int block = 256, grid = grid_for(n, block);
+int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,
+                      void *stream) {
+  if (n_shared <= 0) return 0;
+  const int block = 256, grid = grid_for(n_shared, block);
   if (precision == 64)
-    avg_finish_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, vars, deg, (const double *)xbuf, (double *)avg);
+    avg_finish_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(a, n_shared, xlocal, deg_x);
   else
-    avg_finish_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, vars, deg, (const float *)xbuf, (float *)avg);
+    avg_finish_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(a, n_shared, xlocal, deg_x);
   return (int)cudaGetLastError();
 }
 

@@ -9,9 +9,11 @@
 //     slot arrays, CSR variable -> slots (J_i).
 #include <algorithm>
 #include <atomic>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -207,6 +209,24 @@ static void shard_rows(const fdog_problem *p, int world, std::vector<int32_t> &o
   }
 }
 
+// Pad a 4-byte array to a multiple of 16 bytes: every tile's topology and
+// partition table starts 16-byte aligned and may be read in whole 16-byte
+// units by the TMA bulk copies.
+template <typename V>
+static void pad16(std::vector<V> &v) {
+  static_assert(sizeof(V) == 4, "4-byte elements");
+  while (v.size() % 4) v.push_back(V(0));
+}
+
+// Device topology code of a successor: absolute node index within the tile
+// (next partition starts at `next`), top = nodes, bottom = nodes + 1 (the two
+// sentinel slots of the kernels' distance arrays).
+static uint32_t abs_code(uint16_t rel, int32_t next, int32_t nodes) {
+  if (rel == kBot) return uint32_t(nodes + 1);
+  if (rel == kTop) return uint32_t(nodes);
+  return uint32_t(next + rel);
+}
+
 fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   fdog_status st = validate(p);
   if (st) return st;
@@ -330,9 +350,70 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   std::vector<std::vector<int32_t>> by_shape(P.shapes.size());
   for (int32_t j : P.local_rows) by_shape[P.row_shape[j]].push_back(j);
 
+  // ---- per-warp shared-memory budget: every tile's stage buffer
+  // must fit SB and its distance arrays DB; a shape whose BDDs are too long for
+  // 32 lanes is packed into tiles of 16, 8 or 4 lanes instead.  The budget is
+  // chosen by a cost model: per-lane sequential chain (latency) over resident
+  // warps vs. issued instructions over the SMs.
+  const int tsz = (o && o->precision == 64) ? 8 : 4;
+  P.precision = tsz * 8;
+  {
+    const char *nb = getenv("FDOG_NBUF");  // experiment knob: stage buffers per warp (1 or 2)
+    P.NB = (nb && atoi(nb) == 1) ? 1 : 2;
+  }
+  auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB) {
+    return stage_bytes(tsz, kind, K, nodes, L) <= SB && relax_bytes(tsz, W, L) <= DB;
+  };
+  auto lanes_for = [&](int kind, int K, int nodes, int W, int SB, int DB) {
+    for (int L = 32; L >= 4; L /= 2)
+      if (fits(kind, K, nodes, W, L, SB, DB)) return L;
+    return 0;
+  };
+  {
+    int maxW = 1;
+    for (size_t s = 0; s < P.shapes.size(); ++s)
+      if (!by_shape[s].empty()) maxW = std::max(maxW, P.shapes[s].max_w);
+    const int DB = relax_bytes(tsz, std::min(maxW, 64), 32);
+    const int cands[] = {6, 7, 8, 9, 10, 11, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 72, 96, 112};
+    double best = 1e300;
+    int bestSB = 0;
+    for (int kb : cands) {
+      const int SB = ((kb * 1024 - 16 - DB) / P.NB) & ~15;
+      if (SB <= 0) continue;
+      double chain = 0, instr = 0;
+      int usedSB = 16;
+      for (size_t s = 0; s < P.shapes.size(); ++s) {
+        if (by_shape[s].empty()) continue;
+        const Shape &S = P.shapes[s];
+        int L = lanes_for(0, S.k, S.nodes(), S.max_w, SB, DB);
+        double pen = 1.0;
+        if (L == 0) {  // direct from global memory: latency-bound
+          L = 32;
+          pen = 10.0;
+        } else {
+          usedSB = std::max(usedSB, stage_bytes(tsz, 0, S.k, S.nodes(), L));
+        }
+        const double tiles = std::ceil((double)by_shape[s].size() / L);
+        chain += pen * tiles * (50.0 * S.nodes() + 120.0 * S.k + (P.NB == 1 ? 1500.0 : 0.0));
+        instr += tiles * (20.0 * S.nodes() + 35.0 * S.k);
+      }
+      const int wb = warp_bytes(usedSB, DB, P.NB);
+      const double warps = std::min(32.0, std::floor(226.0 * 1024 / wb));
+      if (warps < 1) continue;
+      const double t = std::max(chain / (148.0 * warps), instr / (148.0 * 2.0));
+      if (t < best * 0.98) {
+        best = t;
+        bestSB = usedSB;
+      }
+    }
+    P.SB = std::max(bestSB, 64);
+    P.DB = DB;
+  }
+
   struct PendingTile {
-    int kind;
+    int kind;                    // bit 0 per-lane topology, bit 1 staged
     int32_t shape;               // kind 0
+    int L;
     std::vector<int32_t> rows;   // lanes
     int64_t cost;
   };
@@ -340,13 +421,18 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   std::vector<int32_t> pool;  // rows for per-lane tiles
   for (size_t s = 0; s < P.shapes.size(); ++s) {
     auto &rows = by_shape[s];
-    size_t full = rows.size() / kLanes * kLanes;
-    for (size_t q = 0; q < full; q += kLanes) {
+    const Shape &S = P.shapes[s];
+    int L = lanes_for(0, S.k, S.nodes(), S.max_w, P.SB, P.DB);
+    const bool staged = L > 0;
+    if (!staged) L = 32;
+    size_t full = rows.size() / L * L;
+    for (size_t q = 0; q < full; q += L) {
       PendingTile t;
-      t.kind = 0;
+      t.kind = staged ? 2 : 0;
       t.shape = (int32_t)s;
-      t.rows.assign(rows.begin() + q, rows.begin() + q + kLanes);
-      t.cost = (int64_t)P.shapes[s].nodes() + P.shapes[s].k;
+      t.L = L;
+      t.rows.assign(rows.begin() + q, rows.begin() + q + L);
+      t.cost = (int64_t)S.nodes() + S.k;
       pend.push_back(std::move(t));
     }
     pool.insert(pool.end(), rows.begin() + full, rows.end());
@@ -358,50 +444,98 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     if (a.nodes() != b.nodes()) return a.nodes() < b.nodes();
     return P.row_shape[x] < P.row_shape[y];
   });
+  auto padded = [&](const std::vector<int32_t> &rows, size_t n, int *nodes, int *W) {
+    const int K = P.shapes[P.row_shape[rows[0]]].k;
+    std::vector<int32_t> w(K, 0);
+    for (size_t q = 0; q < n; ++q) {
+      const Shape &S = P.shapes[P.row_shape[rows[q]]];
+      for (int h = 0; h < K; ++h) w[h] = std::max(w[h], S.hop_start[h + 1] - S.hop_start[h]);
+    }
+    *nodes = 0;
+    *W = 1;
+    for (int h = 0; h < K; ++h) {
+      *nodes += w[h];
+      *W = std::max(*W, w[h]);
+    }
+  };
   for (size_t q = 0; q < pool.size();) {
-    int32_t K = P.shapes[P.row_shape[pool[q]]].k;
+    const int K = P.shapes[P.row_shape[pool[q]]].k;
+    std::vector<int32_t> rows;
+    while (q < pool.size() && rows.size() < (size_t)kLanes && P.shapes[P.row_shape[pool[q]]].k == K)
+      rows.push_back(pool[q++]);
+    // largest lane count whose padded tile fits the budget
+    int L = 0, nodes = 0, W = 1;
+    for (int Lc = 32; Lc >= 4; Lc /= 2) {
+      size_t n = std::min(rows.size(), (size_t)Lc);
+      padded(rows, n, &nodes, &W);
+      if (fits(1, K, nodes, W, Lc, P.SB, P.DB)) {
+        L = Lc;
+        break;
+      }
+    }
     PendingTile t;
-    t.kind = 1;
     t.shape = -1;
-    while (q < pool.size() && (int)t.rows.size() < kLanes && P.shapes[P.row_shape[pool[q]]].k == K)
-      t.rows.push_back(pool[q++]);
-    t.cost = 0;
+    if (L == 0) {
+      t.kind = 1;  // direct
+      t.L = 32;
+    } else {
+      t.kind = 3;
+      t.L = L;
+      if (rows.size() > (size_t)L) {  // give the surplus back to the pool
+        q -= rows.size() - L;
+        rows.resize(L);
+      }
+    }
+    t.rows = rows;
+    int c = 0;
+    for (int32_t j : t.rows) c = std::max(c, P.shapes[P.row_shape[j]].nodes());
+    t.cost = c + K;
     pend.push_back(std::move(t));
   }
-  // expensive tiles first so the static round-robin spreads them
-  for (auto &t : pend)
-    if (t.kind == 1) {
-      int64_t c = 0;
-      for (int32_t j : t.rows) c = std::max<int64_t>(c, P.shapes[P.row_shape[j]].nodes());
-      t.cost = c + P.shapes[P.row_shape[t.rows[0]]].k;
-    }
-  std::stable_sort(pend.begin(), pend.end(),
-                   [](const PendingTile &a, const PendingTile &b) { return a.cost > b.cost; });
+  // direct tiles first (slowest), then expensive tiles, so the dynamic
+  // scheduler does not leave them for the tail
+  std::stable_sort(pend.begin(), pend.end(), [](const PendingTile &a, const PendingTile &b) {
+    const bool da = !(a.kind & 2), db = !(b.kind & 2);
+    if (da != db) return da;
+    return a.cost * 32 / a.L > b.cost * 32 / b.L;
+  });
 
   P.tiles.clear();
   P.hop_off.clear();
   P.topo.clear();
   P.slot_var.clear();
   P.tiles_shared = 0;
+  P.direct_tiles = 0;
   P.max_tile_nodes = 0;
   std::vector<int64_t> shape_topo(P.shapes.size(), -1);
   std::vector<int32_t> shape_hop(P.shapes.size(), -1);
-  // device slot of (row j, hop h): row_slot[j] + h*32
+  // device slot of (row j, hop h): row_slot[j] + h * row_L[j]
   std::vector<int64_t> row_slot(p->n_cons, -1);
-  int64_t slot_base = 0;
+  std::vector<int32_t> row_L(p->n_cons, 32);
+  int64_t slot_base = 0, dist_base = 0;
   for (const PendingTile &t : pend) {
     TileDesc d{};
     const Shape &S0 = P.shapes[P.row_shape[t.rows[0]]];
+    const int L = t.L;
     d.K = S0.k;
     d.n_lanes = (int32_t)t.rows.size();
     d.kind = t.kind;
+    d.lanes = L;
     d.slot_base = slot_base;
-    if (t.kind == 0) {
+    d.dist_base = dist_base;
+    if (!(t.kind & 1)) {
       if (shape_topo[t.shape] < 0) {
+        pad16(P.topo);
+        pad16(P.hop_off);
         shape_topo[t.shape] = (int64_t)P.topo.size();
         shape_hop[t.shape] = (int32_t)P.hop_off.size();
-        for (int32_t n = 0; n < S0.nodes(); ++n) P.topo.push_back(uint32_t(S0.lo[n]) | (uint32_t(S0.hi[n]) << 16));
+        for (int32_t h = 0; h < S0.k; ++h)
+          for (int32_t n = S0.hop_start[h]; n < S0.hop_start[h + 1]; ++n)
+            P.topo.push_back(abs_code(S0.lo[n], S0.hop_start[h + 1], S0.nodes()) |
+                             (abs_code(S0.hi[n], S0.hop_start[h + 1], S0.nodes()) << 16));
         for (int32_t h = 0; h <= S0.k; ++h) P.hop_off.push_back(S0.hop_start[h]);
+        pad16(P.topo);
+        pad16(P.hop_off);
       }
       d.topo_base = shape_topo[t.shape];
       d.hop_base = shape_hop[t.shape];
@@ -415,6 +549,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         const Shape &S = P.shapes[P.row_shape[j]];
         for (int32_t h = 0; h < d.K; ++h) W[h] = std::max(W[h], S.hop_start[h + 1] - S.hop_start[h]);
       }
+      pad16(P.hop_off);
       d.hop_base = (int32_t)P.hop_off.size();
       int32_t acc = 0;
       d.max_w = 0;
@@ -424,32 +559,48 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         d.max_w = std::max(d.max_w, W[h]);
       }
       P.hop_off.push_back(acc);
+      pad16(P.hop_off);
       d.nodes = acc;
+      pad16(P.topo);
       d.topo_base = (int64_t)P.topo.size();
-      P.topo.resize(P.topo.size() + (size_t)acc * kLanes, kBot | (kBot << 16));
+      const uint32_t pad_node = uint32_t(acc + 1) | (uint32_t(acc + 1) << 16);  // both arcs to bottom
+      P.topo.resize(P.topo.size() + (size_t)acc * L, pad_node);
       for (int32_t l = 0; l < d.n_lanes; ++l) {
         const Shape &S = P.shapes[P.row_shape[t.rows[l]]];
         for (int32_t h = 0; h < d.K; ++h) {
           int32_t base = P.hop_off[d.hop_base + h];
+          const int32_t next = P.hop_off[d.hop_base + h + 1];
           for (int32_t w = 0; w < S.hop_start[h + 1] - S.hop_start[h]; ++w) {
             int32_t n = S.hop_start[h] + w;
-            P.topo[d.topo_base + (int64_t)(base + w) * kLanes + l] = uint32_t(S.lo[n]) | (uint32_t(S.hi[n]) << 16);
+            P.topo[d.topo_base + (int64_t)(base + w) * L + l] =
+                abs_code(S.lo[n], next, acc) | (abs_code(S.hi[n], next, acc) << 16);
           }
         }
       }
     }
+    if (!(t.kind & 2)) P.direct_tiles++;
     P.max_tile_nodes = std::max(P.max_tile_nodes, d.nodes);
     // slots
-    P.slot_var.resize((size_t)(slot_base + (int64_t)d.K * kLanes), -1);
+    P.slot_var.resize((size_t)(slot_base + (int64_t)d.K * L), -1);
     for (int32_t l = 0; l < d.n_lanes; ++l) {
       int32_t j = t.rows[l];
       row_slot[j] = slot_base + l;
+      row_L[j] = L;
       const int32_t *vars = P.col_var.data() + P.row_ptr[j];
-      for (int32_t h = 0; h < d.K; ++h) P.slot_var[slot_base + (int64_t)h * kLanes + l] = vars[h];
+      for (int32_t h = 0; h < d.K; ++h) P.slot_var[slot_base + (int64_t)h * L + l] = vars[h];
     }
-    slot_base += (int64_t)d.K * kLanes;
+    slot_base += (int64_t)d.K * L;
+    dist_base += (int64_t)(d.nodes + 2) * L;
     P.tiles.push_back(d);
   }
+  pad16(P.topo);
+  P.topo.resize(P.topo.size() + 4, 0);  // 16-byte reads of the last topology may run past it
+  P.n_dist = dist_base;
+  for (const auto &d : P.tiles)
+    if (d.nodes + 1 > 0xFFFF) {
+      set_error("a BDD tile has %d nodes; the 16-bit topology codes allow 65534", d.nodes);
+      return FDOG_ETOOBIG;
+    }
   if (slot_base > 0x7fffffffLL) {
     set_error("more than 2^31 device slots on one rank");
     return FDOG_ETOOBIG;
@@ -462,21 +613,33 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   for (int32_t j : P.local_rows) {
     int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
     for (int32_t h = 0; h < k; ++h) {
-      P.canon_slot.push_back(row_slot[j] + (int64_t)h * kLanes);
+      P.canon_slot.push_back(row_slot[j] + (int64_t)h * row_L[j]);
       P.canon_con.push_back(j);
       P.canon_pos.push_back(h);
       cnt[P.col_var[P.row_ptr[j] + h]]++;
     }
   }
+  // variables in the order of their first device slot, so that neighbouring
+  // averaging threads gather and scatter neighbouring slots (the tile layout
+  // puts consecutive rows of a shape in consecutive lanes)
   P.var_list.clear();
+  {
+    std::vector<int64_t> first(p->n_vars, INT64_MAX);
+    for (size_t q = 0; q < P.canon_slot.size(); ++q) {
+      int32_t i = P.col_var[P.row_ptr[P.canon_con[q]] + P.canon_pos[q]];
+      first[i] = std::min(first[i], P.canon_slot[q]);
+    }
+    for (int32_t i = 0; i < p->n_vars; ++i)
+      if (cnt[i]) P.var_list.push_back(i);
+    std::stable_sort(P.var_list.begin(), P.var_list.end(),
+                     [&](int32_t x, int32_t y) { return first[x] < first[y]; });
+  }
   P.var_ptr.assign(1, 0);
   std::vector<int64_t> where(p->n_vars, -1);
-  for (int32_t i = 0; i < p->n_vars; ++i)
-    if (cnt[i]) {
-      where[i] = P.var_ptr.back();
-      P.var_list.push_back(i);
-      P.var_ptr.push_back(P.var_ptr.back() + cnt[i]);
-    }
+  for (int32_t i : P.var_list) {
+    where[i] = P.var_ptr.back();
+    P.var_ptr.push_back(P.var_ptr.back() + cnt[i]);
+  }
   P.var_slots.assign(P.var_ptr.back(), -1);
   for (size_t q = 0; q < P.canon_slot.size(); ++q) {
     int32_t j = P.canon_con[q];
@@ -503,6 +666,13 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     for (size_t q = 0; q < P.shared_vars.size(); ++q) xpos[P.shared_vars[q]] = (int32_t)q;
     for (size_t q = 0; q < P.var_list.size(); ++q) P.var_xidx[q] = xpos[P.var_list[q]];
   }
+  P.deg_list.resize(P.var_list.size());
+  for (size_t q = 0; q < P.var_list.size(); ++q) P.deg_list[q] = P.deg_global[P.var_list[q]];
+  P.x_local.assign(P.shared_vars.size(), -1);
+  P.x_deg.resize(P.shared_vars.size());
+  for (size_t q = 0; q < P.var_list.size(); ++q)
+    if (P.var_xidx[q] >= 0) P.x_local[P.var_xidx[q]] = (int32_t)q;
+  for (size_t q = 0; q < P.shared_vars.size(); ++q) P.x_deg[q] = P.deg_global[P.shared_vars[q]];
   return FDOG_OK;
 }
 
@@ -579,6 +749,8 @@ fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out) {
   out->padded_slots = (int64_t)P.slot_var.size();
   out->max_hops = P.max_hops;
   out->max_width = P.max_width;
+  out->staged_tiles = (int64_t)P.tiles.size() - P.direct_tiles;
+  out->sweep_smem_per_warp = warp_bytes(P.SB, P.DB, P.NB);
   return FDOG_OK;
 }
 

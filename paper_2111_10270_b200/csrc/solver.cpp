@@ -83,13 +83,12 @@ struct fdog_solver {
   void *d_lambda = nullptr;
   void *d_delta[2] = {nullptr, nullptr};
   void *d_m0 = nullptr, *d_m1 = nullptr;
-  void *d_avg = nullptr;
-  int32_t *d_var_list = nullptr, *d_var_slots = nullptr, *d_var_xidx = nullptr, *d_deg = nullptr;
+  int32_t *d_var_slots = nullptr, *d_var_xidx = nullptr, *d_deg_list = nullptr;
   int64_t *d_var_ptr = nullptr;
   double *d_lb_part = nullptr, *d_lb = nullptr;
   unsigned int *d_counter = nullptr;
   void *d_xbuf = nullptr;
-  int32_t *d_shared_vars = nullptr;
+  int32_t *d_x_local = nullptr, *d_x_deg = nullptr;
   std::vector<void *> allocs;
 
   int cur = 0;        // delta_bar = d_delta[cur]
@@ -97,6 +96,12 @@ struct fdog_solver {
   int64_t launches = 0;
   int grid = 0, block = 0;
   size_t smem = 0;
+  int32_t SB = 0, DB = 0, NB = 2;
+  size_t warp_bytes = 0;
+  void *d_dist = nullptr;
+  int dist_state = 0;  // 0: distances hold shp(v, T); 1: shp(r, v)
+  int64_t n_direct = 0, scratch_stride = 0;
+  void *d_scratch = nullptr;
 
   Nccl nccl;
   std::vector<EventRec> events;
@@ -180,8 +185,7 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   a.topo = s->d_topo;
   a.slot_var = s->d_slot_var;
   a.lambda = s->d_lambda;
-  a.avg = s->d_avg;
-  a.delta_out = s->d_delta[s->cur ^ 1];
+  a.delta_out = s->d_delta[s->cur ^ 1];  // avg_i in (avg_kernel), delta out
   a.m0 = s->d_m0;
   a.m1 = s->d_m1;
   a.omega = omega;
@@ -189,9 +193,16 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   a.lb_part = s->d_lb_part;
   a.lb_out = s->d_lb;
   a.done_counter = s->d_counter;
+  a.tile_counter = s->d_counter + 1;
   a.max_nodes = s->max_nodes;
   a.max_w = s->max_w;
   a.max_hops = s->max_hops;
+  a.SB = s->SB;
+  a.DB = s->DB;
+  a.NB = s->NB;
+  a.dist = s->d_dist;
+  a.scratch = s->d_scratch;
+  a.scratch_stride = s->scratch_stride;
   const bool rec = s->record_mm && mode != kEnergy;
   int e;
   {
@@ -205,13 +216,12 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
 fdog_status run_avg(fdog_solver *s) {
   AvgArgs a{};
   a.n = s->n_varlist;
-  a.var_list = s->d_var_list;
   a.var_ptr = s->d_var_ptr;
   a.var_slots = s->d_var_slots;
   a.var_xidx = s->world > 1 ? s->d_var_xidx : nullptr;
-  a.deg = s->d_deg;
+  a.deg_l = s->d_deg_list;
   a.delta_bar = s->d_delta[s->cur];
-  a.avg = s->d_avg;
+  a.avg_slot = s->d_delta[s->cur ^ 1];
   a.xbuf = s->d_xbuf;
   int e;
   {
@@ -233,7 +243,7 @@ fdog_status run_avg(fdog_solver *s) {
     }
     {
       Timed t(s, kKAvgFinish);
-      e = launch_avg_finish(s->precision, s->n_shared, s->d_shared_vars, s->d_deg, s->d_xbuf, s->d_avg, s->stream);
+      e = launch_avg_finish(s->precision, a, s->n_shared, s->d_x_local, s->d_x_deg, s->stream);
     }
     if (e) return cuda_fail((cudaError_t)e, "avg_finish launch");
   }
@@ -241,16 +251,26 @@ fdog_status run_avg(fdog_solver *s) {
 }
 
 fdog_status do_pass(fdog_solver *s, bool forward, double omega) {
-  fdog_status st = run_avg(s);
+  fdog_status st;
+  // the pass needs the distances of the opposite direction; after
+  // an unusual call sequence recompute them first
+  if (forward && s->dist_state != 0 && (st = run_sweep(s, kEnergy, omega))) return st;
+  if (!forward && s->dist_state != 1 && (st = run_sweep(s, kCfr, omega))) return st;
+  st = run_avg(s);
   if (st) return st;
   st = run_sweep(s, forward ? kForward : kBackward, omega);
   if (st) return st;
+  s->dist_state = forward ? 1 : 0;
   s->cur ^= 1;  // mbar <- m
   s->passes++;
   return FDOG_OK;
 }
 
-fdog_status energy(fdog_solver *s) { return run_sweep(s, kEnergy, 0.5); }
+fdog_status energy(fdog_solver *s) {
+  fdog_status st = run_sweep(s, kEnergy, 0.5);
+  if (!st) s->dist_state = 0;
+  return st;
+}
 
 void free_solver(fdog_solver *s) {
   if (!s) return;
@@ -375,21 +395,26 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   s->max_w = std::max(1, P.max_width);
   s->max_hops = std::max(1, P.max_hops);
 
-  // launch configuration: persistent grid of warps, smem sized by the largest tile
+  // launch configuration: persistent grid of warps; per-warp shared-memory
+  // budget chosen so that >= 16 warps fit per SM; tiles within the budget are
+  // staged through TMA (kind bit 2), the rest run directly from global memory
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, s->device), "cudaGetDeviceProperties");
-  const int smem_limit = (int)prop.sharedMemPerBlockOptin;
-  int warps = 8;
-  while (warps > 1 && sweep_smem_bytes(s->precision, s->max_nodes, s->max_w, s->max_hops, warps) > smem_limit) warps /= 2;
-  if (sweep_smem_bytes(s->precision, s->max_nodes, s->max_w, s->max_hops, warps) > smem_limit) {
-    set_error("a BDD tile needs more shared memory than %d bytes (nodes %d, hops %d)", smem_limit, s->max_nodes,
-              s->max_hops);
-    return FDOG_ETOOBIG;
+  std::vector<TileDesc> tiles = P.tiles;
+  if (P.precision != s->precision) {
+    set_error("plan packed for fp%d, solver asked for fp%d", P.precision, s->precision);
+    return FDOG_EINVAL;
   }
+  s->SB = P.SB;
+  s->DB = P.DB;
+  s->NB = P.NB;
+  s->warp_bytes = (size_t)warp_bytes(P.SB, P.DB, P.NB);
+  s->n_direct = P.direct_tiles;
+  int warps = (int)std::max<size_t>(1, std::min<size_t>(4, (size_t)prop.sharedMemPerBlockOptin / s->warp_bytes));
   s->block = warps * 32;
-  s->smem = (size_t)sweep_smem_bytes(s->precision, s->max_nodes, s->max_w, s->max_hops, warps);
+  s->smem = (size_t)warps * s->warp_bytes;
   int bps = 1;
-  for (int mode = 0; mode < 3; ++mode)
+  for (int mode = 0; mode < 4; ++mode)
     for (int rec = 0; rec < 2; ++rec) {
       int b = 0;
       int e = sweep_occupancy(s->precision, mode, rec && mode != kEnergy, s->block, s->smem, &b);
@@ -398,18 +423,19 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
     }
   const int64_t want = ((int64_t)s->n_tiles + warps - 1) / warps;
   s->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)prop.multiProcessorCount * bps));
+  s->scratch_stride = (int64_t)relax_slots(s->max_w) * 32;
 
   fdog_status st;
-  if ((st = upload(s, &s->d_tiles, P.tiles))) return st;
+  if ((st = upload(s, &s->d_tiles, tiles))) return st;
   if ((st = upload(s, &s->d_hop_off, P.hop_off))) return st;
   if ((st = upload(s, &s->d_topo, P.topo))) return st;
   if ((st = upload(s, &s->d_slot_var, P.slot_var))) return st;
-  if ((st = upload(s, &s->d_var_list, P.var_list))) return st;
   if ((st = upload(s, &s->d_var_ptr, P.var_ptr))) return st;
   if ((st = upload(s, &s->d_var_slots, P.var_slots))) return st;
   if ((st = upload(s, &s->d_var_xidx, P.var_xidx))) return st;
-  if ((st = upload(s, &s->d_deg, P.deg_global))) return st;
-  if ((st = upload(s, &s->d_shared_vars, P.shared_vars))) return st;
+  if ((st = upload(s, &s->d_deg_list, P.deg_list))) return st;
+  if ((st = upload(s, &s->d_x_local, P.x_local))) return st;
+  if ((st = upload(s, &s->d_x_deg, P.x_deg))) return st;
   const size_t slot_bytes = (size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz;
   if ((st = alloc(s, &s->d_lambda, slot_bytes))) return st;
   if ((st = alloc(s, &s->d_delta[0], slot_bytes))) return st;
@@ -418,16 +444,37 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
     if ((st = alloc(s, &s->d_m0, slot_bytes))) return st;
     if ((st = alloc(s, &s->d_m1, slot_bytes))) return st;
   }
-  if ((st = alloc(s, &s->d_avg, (size_t)std::max<int64_t>(P.n_vars, 1) * s->tsz))) return st;
+  {
+    // per-node distances; the two sentinel slots per lane hold shp(T, T) = 0 and
+    // bottom = +inf and are never overwritten
+    const size_t nd = (size_t)std::max<int64_t>(P.n_dist, 1);
+    std::vector<unsigned char> buf(nd * s->tsz, 0);
+    for (const auto &d : tiles)
+      for (int l = 0; l < d.lanes; ++l) {
+        const size_t top = (size_t)(d.dist_base + (int64_t)d.nodes * d.lanes + l);
+        const size_t bot = top + d.lanes;
+        if (s->precision == 64) {
+          ((double *)buf.data())[top] = 0.0;
+          ((double *)buf.data())[bot] = INFINITY;
+        } else {
+          ((float *)buf.data())[top] = 0.0f;
+          ((float *)buf.data())[bot] = INFINITY;
+        }
+      }
+    if ((st = alloc(s, &s->d_dist, nd * s->tsz))) return st;
+    CK(cudaMemcpyAsync(s->d_dist, buf.data(), nd * s->tsz, cudaMemcpyHostToDevice, s->stream), "H2D");
+    CK(cudaStreamSynchronize(s->stream), "sync");
+  }
   if ((st = alloc(s, &s->d_xbuf, (size_t)std::max<int32_t>(s->n_shared, 1) * s->tsz))) return st;
   if ((st = alloc(s, (void **)&s->d_lb_part, (size_t)std::max(s->n_tiles, 1) * sizeof(double)))) return st;
   if ((st = alloc(s, (void **)&s->d_lb, sizeof(double)))) return st;
-  if ((st = alloc(s, (void **)&s->d_counter, sizeof(unsigned int)))) return st;
-  CK(cudaMemsetAsync(s->d_counter, 0, sizeof(unsigned int), s->stream), "memset");
+  if ((st = alloc(s, (void **)&s->d_counter, 2 * sizeof(unsigned int)))) return st;
+  if ((st = alloc(s, &s->d_scratch, s->n_direct ? (size_t)s->grid * (s->block / 32) * s->scratch_stride * s->tsz : 16)))
+    return st;
+  CK(cudaMemsetAsync(s->d_counter, 0, 2 * sizeof(unsigned int), s->stream), "memset");
   CK(cudaMemsetAsync(s->d_lb, 0, sizeof(double), s->stream), "memset");
   CK(cudaMemsetAsync(s->d_delta[0], 0, slot_bytes, s->stream), "memset");
   CK(cudaMemsetAsync(s->d_delta[1], 0, slot_bytes, s->stream), "memset");
-  CK(cudaMemsetAsync(s->d_avg, 0, (size_t)std::max<int64_t>(P.n_vars, 1) * s->tsz, s->stream), "memset");
   if (s->record_mm) {
     CK(cudaMemsetAsync(s->d_m0, 0, slot_bytes, s->stream), "memset");
     CK(cudaMemsetAsync(s->d_m1, 0, slot_bytes, s->stream), "memset");
@@ -446,16 +493,22 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   }
   if (s->world > 1 && (st = init_nccl(s, o))) return st;
 
-  // algorithmic bytes per launch
+  // algorithmic bytes per launch: per node 2 T (distance read +
+  // write) + 4 B topology for per-lane-topology tiles; per slot 4 T (lambda
+  // read + write, average read, delta write)
   {
     const double T = (double)s->tsz;
-    const double slots = (double)P.n_slots, nv = (double)P.var_list.size();
-    const double topo = (double)P.topo.size() * 4.0;
+    const double slots = (double)P.n_slots, nv = (double)P.var_list.size(), nodes = (double)P.n_nodes;
+    double lane_topo = 0;
+    for (const auto &d : tiles)
+      if (d.kind & 1) lane_topo += 4.0 * d.nodes * d.n_lanes;
     const double rec = s->record_mm ? 2 * T : 0.0;
-    s->bytes[kKSweepFwd] = s->bytes[kKSweepBwd] = topo + slots * (3 * T + 4 + T + rec);
-    s->bytes[kKEnergy] = topo + slots * T;
-    s->bytes[kKAvg] = slots * (4 + T) + nv * (8 + 4 + 4 + T);
-    s->bytes[kKAvgFinish] = (double)s->n_shared * (4 + 4 + 2 * T);
+    s->bytes[kKSweepFwd] = s->bytes[kKSweepBwd] = nodes * 2 * T + lane_topo + slots * (4 * T + rec);
+    s->bytes[kKEnergy] = nodes * 2 * T + lane_topo + slots * T;
+    // averaging: per slot the slot index, the delta gather and the average scatter;
+    // per variable the CSR pointer and |J_i|
+    s->bytes[kKAvg] = slots * (4 + 2 * T) + nv * (8 + 4);
+    s->bytes[kKAvgFinish] = (double)s->n_shared * (4 + 4 + T);
     s->bytes[kKAllreduce] = (double)s->n_shared * T;
     s->bytes[kKAddDeferred] = (double)s->n_dev_slots * 4 * T;
   }
@@ -473,6 +526,10 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   s->st.padded_slots = s->n_dev_slots;
   s->st.max_hops = P.max_hops;
   s->st.max_width = P.max_width;
+  s->st.staged_tiles = (int64_t)tiles.size() - s->n_direct;
+  s->st.sweep_grid = s->grid;
+  s->st.sweep_block = s->block;
+  s->st.sweep_smem_per_warp = (int64_t)s->warp_bytes;
 
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;

@@ -177,6 +177,23 @@ def test_edge_cases(oracle_mod):
     _compare_pass_by_pass(synth.spec_two_constraint(), oracle_mod, passes=4, omega=0.1)
 
 
+def test_unusual_pass_orders(oracle_mod):
+    """Backward first, two forwards in a row, pass after finalize: the distances
+    of the opposite direction are recomputed when needed."""
+    p = synth.gm_worms_like(8, n_src=40, k_cand=5, knn=6)
+    s = _s(p)
+    o = oracle_mod.Oracle(p)
+    g = F.Solver(p, precision=64)
+    for fwd in (False, True, True, False, False, True):
+        o.pass_(fwd, 0.5)
+        g.pass_(fwd, 0.5)
+        assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s
+        assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+    o.finalize(); g.finalize()
+    o.pass_(False, 0.5); g.pass_(False, 0.5)
+    assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s
+
+
 def test_errors_and_state():
     p = synth.spec_two_constraint()
     g = F.Solver(p, precision=64)
