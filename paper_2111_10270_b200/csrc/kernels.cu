@@ -302,6 +302,104 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
   return acc;
 }
 
+// Narrow tiles (every partition has <= 2 nodes -- all one-hot, at-most-one and
+// marginalisation rows of the BASELINE workloads).  Same arithmetic and the
+// same D / va conventions as process_bdd, with the per-partition values of the
+// sweep direction in registers and no loops over nodes.
+template <typename T>
+__device__ __forceinline__ void push2(T x, int r, T &a0, T &a1) {
+  if (r == 0) a0 = fmin(a0, x);
+  if (r == 1) a1 = fmin(a1, x);
+}
+
+template <typename T, int MODE, bool REC>
+__device__ __forceinline__ double process_bdd_w2(const int K, const int32_t *ho, const uint32_t *tp, const int ts,
+                                                 const int L, T *lam, T *va, T *D, const bool valid, const T omega,
+                                                 const T clamp, T *m0g, T *m1g) {
+  const T inf = t_inf<T>();
+  double acc = 0.0;
+  if (MODE == kForward) {
+    T c0 = T(0), c1 = inf;  // shp(r, .) of the (up to) two nodes of P_h
+#pragma unroll 1
+    for (int h = 0; h < K; ++h) {
+      const int n0 = ho[h], n1 = ho[h + 1];
+      const uint32_t e0 = tp[n0 * ts];
+      const int lo0 = (int)(e0 & 0xFFFFu), hi0 = (int)(e0 >> 16);
+      D[n0 * L] = c0;  // shp(v, T) of P_h is no longer needed: keep shp(r, v)
+      T m0 = c0 + D[lo0 * L], m1r = c0 + D[hi0 * L];
+      T nl0 = inf, nl1 = inf, nh0 = inf, nh1 = inf;
+      push2(c0, lo0 - n1, nl0, nl1);
+      push2(c0, hi0 - n1, nh0, nh1);
+      if (n1 - n0 > 1) {
+        const uint32_t e1 = tp[(n0 + 1) * ts];
+        const int lo1 = (int)(e1 & 0xFFFFu), hi1 = (int)(e1 >> 16);
+        D[(n0 + 1) * L] = c1;
+        m0 = fmin(m0, c1 + D[lo1 * L]);
+        m1r = fmin(m1r, c1 + D[hi1 * L]);
+        push2(c1, lo1 - n1, nl0, nl1);
+        push2(c1, hi1 - n1, nh0, nh1);
+      }
+      const T l = lam[h * L];
+      const T m1 = l + m1r;
+      const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+      const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
+      if (valid) {
+        lam[h * L] = lam_new;
+        va[h * L] = delta;
+        if (REC) {
+          m0g[h * L] = m0;
+          m1g[h * L] = m1;
+        }
+        acc += (double)fmin(delta, T(0));
+      } else {
+        va[h * L] = T(0);
+      }
+      c0 = fmin(nl0, nh0 + lam_new);  // A4: 1-arcs priced with the updated lambda_h
+      c1 = fmin(nl1, nh1 + lam_new);
+      if (h == K - 1 && valid) acc += (double)fmin(m0, lam_new + m1r);  // E^j
+    }
+    return acc;
+  }
+  // kBackward
+#pragma unroll 1
+  for (int h = K - 1; h >= 0; --h) {
+    const int n0 = ho[h], n1 = ho[h + 1];
+    const uint32_t e0 = tp[n0 * ts];
+    const T f0 = D[n0 * L];
+    const T a0 = D[(e0 & 0xFFFFu) * L], b0 = D[(e0 >> 16) * L];
+    T m0 = f0 + a0, m1r = f0 + b0;
+    T a1 = inf, b1 = inf;
+    const bool two = n1 - n0 > 1;
+    if (two) {
+      const uint32_t e1 = tp[(n0 + 1) * ts];
+      const T f1 = D[(n0 + 1) * L];
+      a1 = D[(e1 & 0xFFFFu) * L];
+      b1 = D[(e1 >> 16) * L];
+      m0 = fmin(m0, f1 + a1);
+      m1r = fmin(m1r, f1 + b1);
+    }
+    const T l = lam[h * L];
+    const T m1 = l + m1r;
+    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+    const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
+    if (valid) {
+      lam[h * L] = lam_new;
+      va[h * L] = delta;
+      if (REC) {
+        m0g[h * L] = m0;
+        m1g[h * L] = m1;
+      }
+      acc += (double)fmin(delta, T(0));
+    } else {
+      va[h * L] = T(0);
+    }
+    D[n0 * L] = fmin(a0, lam_new + b0);  // shp(v, T) with the updated lambda_h
+    if (two) D[(n0 + 1) * L] = fmin(a1, lam_new + b1);
+  }
+  if (valid) acc += (double)D[0];  // E^j = shp(r, T)
+  return acc;
+}
+
 // Stage buffer of one tile (layout: internal.h).
 template <typename T>
 struct Stage {
@@ -385,6 +483,10 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     if (lane == 0) x = (int)atomicAdd(a.tile_counter, 1u);
     return __shfl_sync(0xffffffffu, x, 0);
   };
+  // split claim: lane 0 issues the atomic, the broadcast happens one tile later
+  // so the atomic's round trip overlaps the tile's work
+  auto claim_issue = [&]() -> int { return lane == 0 ? (int)atomicAdd(a.tile_counter, 1u) : 0; };
+  auto claim_get = [&](int raw) -> int { return __shfl_sync(0xffffffffu, raw, 0); };
   uint32_t phase = 0;  // bit b = parity of bar[b]
   int b = 0;
   int t = claim();
@@ -403,7 +505,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
       bulk_wait_read_all();  // the bulk stores issued from stage bn have read their source
       issue_stage<T, MODE>(a, dn, stage_at<T>(bn ? sbuf1 : sbuf0, dn), &bar[bn]);
     }
-    const int tnn = has_next ? claim() : a.n_tiles;
+    const int tnn_raw = has_next ? claim_issue() : 0;
     const int L = d.lanes;
     const bool active = lane < L;
     const bool valid = lane < d.n_lanes;
@@ -419,8 +521,12 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
         T *R = reinterpret_cast<T *>(rbase) + lane;
         T *m0p = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
         T *m1p = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
-        acc = process_bdd<T, MODE, REC>(K, d.nodes, s.hop, tp, (d.kind & 1) ? L : 1, L, s.lam + lane, s.va + lane,
-                                        s.dist + lane, R, d.max_w, valid, omega, clamp, m0p, m1p);
+        if (kUpd && d.max_w <= 2)
+          acc = process_bdd_w2<T, MODE, REC>(K, s.hop, tp, (d.kind & 1) ? L : 1, L, s.lam + lane, s.va + lane,
+                                             s.dist + lane, valid, omega, clamp, m0p, m1p);
+        else
+          acc = process_bdd<T, MODE, REC>(K, d.nodes, s.hop, tp, (d.kind & 1) ? L : 1, L, s.lam + lane, s.va + lane,
+                                          s.dist + lane, R, d.max_w, valid, omega, clamp, m0p, m1p);
       }
       fence_proxy_async();  // lanes' shared-memory writes -> visible to the TMA stores
       __syncwarp();
@@ -454,7 +560,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     }
     t = tn;
     d = dn;
-    tn = tnn;
+    tn = has_next ? claim_get(tnn_raw) : a.n_tiles;
     b = bn;
   }
   if (lane == 0) bulk_wait_read_all();  // shared memory must outlive the TMA stores' reads
