@@ -197,7 +197,7 @@ def run_gpu(args):
     plan = F.Plan(problem, rank=rank, world=world)
     plan_s = time.perf_counter() - t0
     prec = 64 if args.fp64 else 32
-    solver = F.Solver(plan=plan, precision=prec, device=local, profile=True, rank=rank, world=world,
+    solver = F.Solver(plan=plan, precision=prec, device=local, profile=False, rank=rank, world=world,
                       nccl_unique_id=uid, nccl_library=nccl_lib, stream=stream.cuda_stream)
     st = solver.stats()
     arcs_local = st["arcs"]
@@ -215,35 +215,45 @@ def run_gpu(args):
     for _ in range(args.warmup):
         solver.iterate(1, OMEGA)
     torch.cuda.synchronize()
-    solver.profile_reset()
+
+    def timed_steps():
+        evs = []
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush, outside the timed interval
+            flush_rd.sum()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            solver.iterate(1, OMEGA)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return [x.elapsed_time(y) for x, y in evs]
+
+    # timed region: K steps, each one iteration (graph replay of the 4 kernels)
     launches0 = solver.stats()["launches"]
     sampler = ClockSampler(local)
     sampler.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    step_ms = []
-    for _ in range(args.steps):
-        flush.zero_()  # L2 flush, outside the timed interval
-        flush_rd.sum()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        solver.iterate(1, OMEGA)
-        b.record(stream)
-        step_ms.append((a, b))
-    torch.cuda.synchronize()
+    ms = timed_steps()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    ms = [x.elapsed_time(y) for x, y in step_ms]
     tot_ms = float(sum(ms))
     if world > 1:
         t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     launches = solver.stats()["launches"] - launches0
+    # the same K steps again with CUDA events around every kernel launch (on the
+    # solver's stream): per-kernel device time for the roofline and the shares
+    solver.profile_enable(True)
+    solver.profile_reset()
+    ms_prof = timed_steps()
     prof = solver.profile()
+    solver.profile_enable(False)
     lb = solver.lower_bound()
 
     # roofline of the dominant kernel (the two sweeps share one code path)
@@ -312,6 +322,7 @@ def run_gpu(args):
                          "bytes_per_launch": sw_bytes, "peak_kind": peak_kind,
                          "launch_us": 1e3 * sw_ms / sw_n if sw_n else None},
             "kernel_share": shares,
+            "ms_per_step_profiled": float(sum(ms_prof)) / args.steps,
             "solver_stats": {k: st[k] for k in ("tiles", "tiles_shared_topology", "staged_tiles", "sweep_grid",
                                                  "sweep_block", "sweep_smem_per_warp", "padded_slots",
                                                  "device_bytes", "shapes", "max_hops", "max_width")},

@@ -163,6 +163,10 @@ typedef struct {
 } fdog_kernel_time;
 fdog_status fdog_profile(fdog_solver *s, fdog_kernel_time *out, int32_t cap, int32_t *n);
 fdog_status fdog_profile_reset(fdog_solver *s);
+/* Turn the per-launch CUDA events on (1) or off (0).  With events on,
+ * fdog_iterate launches kernels one by one; with events off (and world == 1)
+ * it replays a CUDA graph of one iteration. */
+fdog_status fdog_profile_enable(fdog_solver *s, int32_t on);
 
 const char *fdog_last_error(void);
 int32_t fdog_version(void);

@@ -61,7 +61,7 @@ EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdo
            "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_lower_bound",
            "fdog_finalize", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
            "fdog_get_deferred", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
-           "fdog_profile", "fdog_profile_reset", "fdog_last_error", "fdog_version"]
+           "fdog_profile", "fdog_profile_reset", "fdog_profile_enable", "fdog_last_error", "fdog_version"]
 
 _lib = None
 
@@ -101,6 +101,7 @@ def load():
         "fdog_stats": ([P, P], C.c_int),
         "fdog_profile": ([P, P, i32, P], C.c_int),
         "fdog_profile_reset": ([P], C.c_int),
+        "fdog_profile_enable": ([P, i32], C.c_int),
         "fdog_last_error": ([], C.c_char_p),
         "fdog_version": ([], C.c_int32),
     }
@@ -305,3 +306,6 @@ class Solver:
 
     def profile_reset(self):
         _check(self._lib.fdog_profile_reset(self._h), "fdog_profile_reset")
+
+    def profile_enable(self, on: bool):
+        _check(self._lib.fdog_profile_enable(self._h, 1 if on else 0), "fdog_profile_enable")

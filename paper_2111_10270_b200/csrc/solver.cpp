@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -102,6 +103,14 @@ struct fdog_solver {
   int dist_state = 0;  // 0: distances hold shp(v, T); 1: shp(r, v)
   int64_t n_direct = 0, scratch_stride = 0;
   void *d_scratch = nullptr;
+
+  // one captured iteration (avg, forward, avg, backward), keyed by omega and
+  // the parity of the delta buffers; replayed by fdog_iterate
+  cudaGraphExec_t graph = nullptr;
+  double graph_omega = 0.0;
+  int graph_cur = -1;
+  int64_t graph_launches = 0;
+  bool use_graphs = true;
 
   Nccl nccl;
   std::vector<EventRec> events;
@@ -280,6 +289,7 @@ void free_solver(fdog_solver *s) {
     cudaEventDestroy(e.b);
   }
   for (auto e : s->event_pool) cudaEventDestroy(e);
+  if (s->graph) cudaGraphExecDestroy(s->graph);
   for (void *p : s->allocs) cudaFree(p);
   if (s->nccl.comm && s->nccl.destroy) s->nccl.destroy(s->nccl.comm);
   if (s->nccl.lib) dlclose(s->nccl.lib);
@@ -366,6 +376,10 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   s->device = o->device;
   s->record_mm = o->record_mm != 0;
   s->profile = o->profile != 0;
+  {
+    const char *g = getenv("FDOG_GRAPHS");  // experiment knob: FDOG_GRAPHS=0 disables graph replay
+    s->use_graphs = !(g && g[0] == '0');
+  }
   s->rank = P.rank;
   s->world = P.world;
   s->clamp = o->clamp > 0 ? o->clamp : 1e4 * (1.0 + P.max_abs_cost);  // A5
@@ -599,6 +613,44 @@ fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
     set_error("omega %g outside (0, 1]", omega);
     return FDOG_EINVAL;
   }
+  // CUDA graph of one iteration: used when the passes alternate normally, no
+  // per-kernel events are requested and there is no NCCL exchange
+  const bool graphs = s->use_graphs && !s->profile && s->world == 1 && s->dist_state == 0 && n_iter > 0;
+  if (graphs) {
+    if (!s->graph || s->graph_omega != omega || s->graph_cur != s->cur) {
+      if (s->graph) {
+        cudaGraphExecDestroy(s->graph);
+        s->graph = nullptr;
+      }
+      const int cur0 = s->cur, ds0 = s->dist_state;
+      const int64_t passes0 = s->passes, launches0 = s->launches;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+      fdog_status st = do_pass(s, true, omega);
+      if (!st) st = do_pass(s, false, omega);
+      cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+      if (st) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      e = cudaGraphInstantiate(&s->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+      s->graph_omega = omega;
+      s->graph_cur = cur0;
+      s->graph_launches = s->launches - launches0;
+      s->cur = cur0;  // capture recorded the work without running it
+      s->dist_state = ds0;
+      s->passes = passes0;
+      s->launches = launches0;
+    }
+    for (int32_t t = 0; t < n_iter; ++t) CK(cudaGraphLaunch(s->graph, s->stream), "cudaGraphLaunch");
+    s->launches += s->graph_launches * n_iter;
+    s->passes += 2 * (int64_t)n_iter;
+    s->dist_state = 0;
+    return FDOG_OK;
+  }
   for (int32_t t = 0; t < n_iter; ++t) {
     fdog_status st = do_pass(s, true, omega);
     if (st) return st;
@@ -738,6 +790,16 @@ fdog_status fdog_profile(fdog_solver *s, fdog_kernel_time *out, int32_t cap, int
     ++k;
   }
   *n = k;
+  return FDOG_OK;
+}
+
+fdog_status fdog_profile_enable(fdog_solver *s, int32_t on) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  s->profile = on != 0;
   return FDOG_OK;
 }
 
