@@ -1,0 +1,103 @@
+"""Summarise a round's ncu captures into profiles/ (committed evidence).
+
+usage: python scripts/summarize_ncu.py TAG [bench.json]
+  reads gpurun_out/launches_TAG.csv (launch list, gpu__time_duration) and
+  gpurun_out/prof_TAG.ncu-rep (--set full capture); writes
+  profiles/TAG_launches.csv, profiles/TAG_ncu_summary.md and updates
+  profiles/sweep_traffic.json (dram bytes per sweep launch, for bench.py).
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+tag = sys.argv[1]
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+out = os.path.join(root, "profiles")
+os.makedirs(out, exist_ok=True)
+lines = []
+
+# launch list
+lp = os.path.join(root, "gpurun_out", f"launches_{tag}.csv")
+if os.path.exists(lp):
+    txt = "".join(l for l in open(lp) if not l.startswith("=="))
+    rows = list(csv.DictReader(io.StringIO(txt)))
+    with open(os.path.join(out, f"{tag}_launches.csv"), "w") as f:
+        f.write("id,kernel,grid,block,gpu__time_duration_ns\n")
+        for r in rows:
+            f.write(f"{r['ID']},\"{r['Kernel Name'][:80]}\",\"{r['Grid Size']}\",\"{r['Block Size']}\",{r['Metric Value']}\n")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows:
+        k = r["Kernel Name"].split("(")[0].replace("void ", "")
+        agg[k][0] += 1
+        agg[k][1] += float(r["Metric Value"])
+    tot = sum(v[1] for v in agg.values())
+    lines.append(f"## Launch list ({lp.split('/')[-1]}; ncu gpu__time_duration.sum, --clock-control none, cold-cache serialised)\n")
+    lines.append("| kernel | launches | total us | mean us | share |\n|---|---|---|---|---|")
+    for k, (n, ns) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        lines.append(f"| `{k}` | {n} | {ns/1e3:.1f} | {ns/n/1e3:.2f} | {ns/tot:.3f} |")
+    lines.append("")
+
+# full capture
+rp = os.path.join(root, "gpurun_out", f"prof_{tag}.ncu-rep")
+traffic = {}
+if os.path.exists(rp):
+    raw = subprocess.run(["ncu", "-i", rp, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    hdr = rr[0]
+    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+            "sm__cycles_active.avg", "sm__cycles_elapsed.avg", "smsp__inst_executed.sum",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "launch__grid_size", "launch__block_size"]
+    lines.append(f"## ncu --set full ({rp.split('/')[-1]})\n")
+    lines.append("| kernel | " + " | ".join(w for w in want) + " |")
+    lines.append("|---|" + "---|" * len(want))
+    units = rr[1]
+    for row in rr[2:]:
+        d = dict(zip(hdr, row))
+        u = dict(zip(hdr, units))
+        name = d["Kernel Name"].split("(")[0].replace("void ", "")
+        vals = []
+        for w in want:
+            vals.append(f"{d.get(w, '')} {u.get(w, '')}".strip())
+        lines.append(f"| `{name}` | " + " | ".join(vals) + " |")
+        if "sweep_kernel<float, 0" in name or "sweep_kernel<float, 1" in name:
+            def mb(w):
+                v = float(d[w])
+                return v * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}.get(u[w], 1)
+            traffic.setdefault(name, []).append(mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"))
+    lines.append("")
+    # stall reasons per kernel
+    lines.append("### warp stall reasons (cycles per issued instruction)\n")
+    for row in rr[2:]:
+        d = dict(zip(hdr, row))
+        name = d["Kernel Name"].split("(")[0].replace("void ", "")
+        st = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""): float(v)
+              for k, v in d.items() if k.startswith("smsp__average_warps_issue_stalled_")
+              and k.endswith("per_issue_active.ratio") and v not in ("", "n/a")}
+        top = sorted(st.items(), key=lambda x: -x[1])[:6]
+        lines.append(f"- `{name}`: " + ", ".join(f"{k} {v:.2f}" for k, v in top))
+    lines.append("")
+
+if len(sys.argv) > 2 and os.path.exists(sys.argv[2]):
+    b = json.load(open(sys.argv[2]))
+    lines.insert(0, f"Bench line of the same round ({sys.argv[2].split('/')[-1]}): value {b['value']:.4g} {b['unit']}, "
+                    f"{b['ms_per_step']*1e3:.1f} us/step, roofline frac {b['roofline']['frac']:.3f} "
+                    f"({b['roofline']['achieved']:.0f} of {b['roofline']['peak']} GB/s {b['roofline']['peak_kind']}), "
+                    f"kernel shares {json.dumps({k: round(v, 3) for k, v in b['kernel_share'].items()})}\n")
+lines.insert(0, f"# ncu summary, {tag}\n")
+with open(os.path.join(out, f"{tag}_ncu_summary.md"), "w") as f:
+    f.write("\n".join(lines) + "\n")
+if traffic:
+    tp = os.path.join(out, "sweep_traffic.json")
+    cur = json.load(open(tp)) if os.path.exists(tp) else {}
+    allv = [v for vs in traffic.values() for v in vs]
+    cur["gm_worms_like(seed=0,n=500,K=10,knn=30)/fp32"] = sum(allv) / len(allv)
+    cur["_note"] = f"dram__bytes_read.sum + dram__bytes_write.sum per sweep launch, ncu --set full, round tag {tag}"
+    json.dump(cur, open(tp, "w"), indent=1)
+print("\n".join(lines))
