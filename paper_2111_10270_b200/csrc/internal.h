@@ -2,6 +2,7 @@
 // Not part of the ABI; include/fastdog.h is.
 #pragma once
 #include <cstdint>
+#include <vector_types.h>
 #include <string>
 #include <vector>
 
@@ -104,12 +105,14 @@ struct Plan {
   std::vector<int32_t> slot_var;    // padded device slots: variable or -1
   std::vector<int64_t> canon_slot;  // canonical local slot -> device slot
   std::vector<int32_t> canon_con, canon_pos;
-  std::vector<int32_t> var_list;    // variables with local slots, by first device slot
+  std::vector<int32_t> var_list;    // CSR part of the averaging: variables by first device slot
   std::vector<int64_t> var_ptr;     // CSR over var_list
   std::vector<int32_t> var_slots;   // device slots, j ascending within a variable
   std::vector<int32_t> var_xidx;    // per var_list entry: index into shared_vars or -1
   std::vector<int32_t> shared_vars; // ascending global ids exchanged with other ranks
   std::vector<int32_t> deg_list;    // |J_i| (global) per var_list entry
+  std::vector<int32_t> ell;         // ELL part: slot pairs (second -1 if |J_i| = 1)
+  int64_t n_vars_local = 0;         // variables with local slots (ELL + CSR)
   std::vector<int32_t> x_local;     // per shared var: index into var_list or -1
   std::vector<int32_t> x_deg;       // per shared var: |J_i| (global)
 
@@ -141,8 +144,7 @@ struct SweepArgs {
   void *delta_out;       // T*: per slot avg_i in, delta out (in place)
   void *m0, *m1;         // T*, recorded min-marginals (may be null)
   double omega, clamp;
-  double *lb_part;       // per tile
-  double *lb_out;        // final (written by the last CTA)
+  double *lb_part;       // per tile bound contribution (reduced by lb_reduce_kernel)
   unsigned int *done_counter;
   unsigned int *tile_counter;  // dynamic tile scheduler (reset by the last CTA)
   int32_t max_nodes, max_w, max_hops;  // over all tiles (direct-mode scratch)
@@ -153,14 +155,18 @@ struct SweepArgs {
 };
 
 struct AvgArgs {
-  int32_t n;                 // entries of var_list
-  const int64_t *var_ptr;    // CSR over var_list
+  int32_t n_ell;             // variables in the ELL part (|J_i| <= 2, not exchanged)
+  const int2 *ell;           // their slot pairs (y = -1 if |J_i| = 1)
+  int32_t n;                 // variables in the CSR part
+  int32_t group;             // lanes per CSR variable (power of two <= 32)
+  const int64_t *var_ptr;    // CSR over the CSR part
   const int32_t *var_slots;  // device slots, ascending j within a variable
   const int32_t *var_xidx;   // may be null (world == 1)
-  const int32_t *deg_l;      // |J_i| (global) per var_list entry
+  const int32_t *deg_l;      // |J_i| (global) per CSR entry
   const void *delta_bar;     // T*: delta of the last pass
   void *avg_slot;            // T*: avg_i written into every slot of i (the other delta buffer)
   void *xbuf;                // T* partial sums of shared variables (may be null)
+  unsigned int *tile_counter;  // sweep scheduler counter, reset here for the next sweep
 };
 
 // returns the cudaError_t as int
@@ -171,6 +177,7 @@ int launch_avg(int precision, const AvgArgs &a, void *stream);
 int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,
                       void *stream);
 int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, void *stream);
+int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream);
 int launch_fill(int precision, int64_t n, void *dst, double value, void *stream);
 
 }  // namespace fdog

@@ -58,33 +58,37 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Last CTA reduces the per-tile bound partials in a fixed order (deterministic
-// for any tile-to-warp assignment): thread q sums the contiguous chunk q of
-// lb_part with independent L2 loads, then a fixed-shape block reduction.
-__device__ void reduce_lb_last_cta(const double *lb_part, int n, double *out, unsigned int *counter,
-                                   unsigned int *tile_counter) {
+// The last CTA of a sweep resets the scheduler counters for the next launch.
+__device__ void last_cta_reset(unsigned int *counter, unsigned int *tile_counter) {
   __shared__ bool is_last;
-  __shared__ double red[32];
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     unsigned prev = atomicAdd(counter, 1u);
     is_last = (prev == gridDim.x - 1);
+    if (is_last) {
+      *counter = 0u;
+      *tile_counter = 0u;
+    }
   }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
+}
+
+// Bound of the last pass (A7): the per-tile partials summed in a fixed order
+// (deterministic for any tile-to-warp assignment); one CTA, launched on demand
+// by fdog_lower_bound.
+__global__ void __launch_bounds__(1024) lb_reduce_kernel(const double *__restrict__ lb_part, int n, double *out) {
+  __shared__ double red[32];
   const int chunk = (n + blockDim.x - 1) / blockDim.x;
   const int q0 = threadIdx.x * chunk, q1 = min(n, q0 + chunk);
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int q = q0;
   for (; q + 3 < q1; q += 4) {
-    s0 += __ldcg(lb_part + q);
-    s1 += __ldcg(lb_part + q + 1);
-    s2 += __ldcg(lb_part + q + 2);
-    s3 += __ldcg(lb_part + q + 3);
+    s0 += lb_part[q];
+    s1 += lb_part[q + 1];
+    s2 += lb_part[q + 2];
+    s3 += lb_part[q + 3];
   }
-  for (; q < q1; ++q) s0 += __ldcg(lb_part + q);
+  for (; q < q1; ++q) s0 += lb_part[q];
   double s = (s0 + s1) + (s2 + s3);
   s = warp_sum(s);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -93,11 +97,7 @@ __device__ void reduce_lb_last_cta(const double *lb_part, int n, double *out, un
   if (warp == 0) {
     double v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
     v = warp_sum(v);
-    if (lane == 0) {
-      *out = v;
-      *counter = 0u;
-      *tile_counter = 0u;
-    }
+    if (lane == 0) *out = v;
   }
 }
 
@@ -487,6 +487,9 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   // so the atomic's round trip overlaps the tile's work
   auto claim_issue = [&]() -> int { return lane == 0 ? (int)atomicAdd(a.tile_counter, 1u) : 0; };
   auto claim_get = [&](int raw) -> int { return __shfl_sync(0xffffffffu, raw, 0); };
+  // pipeline per warp: the claim for the tile after next is in flight, the
+  // next tile's descriptor is loaded and its TMA stage loads are issued, while
+  // the current tile is processed
   uint32_t phase = 0;  // bit b = parity of bar[b]
   int b = 0;
   int t = claim();
@@ -496,16 +499,20 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     if ((d.kind & 2) && lane == 0) issue_stage<T, MODE>(a, d, stage_at<T>(sbuf0, d), &bar[0]);
   }
   int tn = t < a.n_tiles ? claim() : a.n_tiles;
+  TileDesc dn;
+  if (tn < a.n_tiles) dn = a.tiles[tn];
+  int raw_nn = tn < a.n_tiles ? claim_issue() : 0;
   while (t < a.n_tiles) {
-    TileDesc dn;
     const bool has_next = tn < a.n_tiles;
-    if (has_next) dn = a.tiles[tn];
     const int bn = a.NB > 1 ? (b ^ 1) : 0;
     if (a.NB > 1 && has_next && (dn.kind & 2) && lane == 0) {
       bulk_wait_read_all();  // the bulk stores issued from stage bn have read their source
       issue_stage<T, MODE>(a, dn, stage_at<T>(bn ? sbuf1 : sbuf0, dn), &bar[bn]);
     }
-    const int tnn_raw = has_next ? claim_issue() : 0;
+    const int tnn = has_next ? claim_get(raw_nn) : a.n_tiles;
+    TileDesc dnn;
+    if (tnn < a.n_tiles) dnn = a.tiles[tnn];  // used one tile later
+    raw_nn = tnn < a.n_tiles ? claim_issue() : 0;
     const int L = d.lanes;
     const bool active = lane < L;
     const bool valid = lane < d.n_lanes;
@@ -560,55 +567,80 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     }
     t = tn;
     d = dn;
-    tn = has_next ? claim_get(tnn_raw) : a.n_tiles;
+    tn = tnn;
+    dn = dnn;
     b = bn;
   }
   if (lane == 0) bulk_wait_read_all();  // shared memory must outlive the TMA stores' reads
   __syncwarp();
-  reduce_lb_last_cta(a.lb_part, a.n_tiles, a.lb_out, a.done_counter, a.tile_counter);
+  last_cta_reset(a.done_counter, a.tile_counter);
 }
 
-// Deferred averaging (A1): one thread per variable of the local list.
-// avg_i = (sum over the slots of i, in CSR order = ascending j, of delta_bar) /
-// |J_i| is written into every slot of i of the OTHER delta buffer, where the
-// next sweep reads it (and overwrites it with its own delta).
+// Deferred averaging (A1).  avg_i = (sum over the slots of i, in
+// ascending j, of delta_bar) / |J_i| is written into every slot of i of the
+// OTHER delta buffer, where the next sweep reads it (and overwrites it with its
+// own delta).  Threads [0, ceil(n_ell/2)) take two ELL variables each (slot
+// pair inline, |J_i| <= 2); the remaining threads take one CSR variable each.
+// Thread 0 also resets the sweep's tile counter.
 template <typename T>
 __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
-  T *__restrict__ xbuf = reinterpret_cast<T *>(a.xbuf);
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= a.n) return;
-  const int64_t p0 = __ldg(a.var_ptr + q), p1 = __ldg(a.var_ptr + q + 1);
-  const int x = a.var_xidx ? __ldg(a.var_xidx + q) : -1;
-  const int deg = __ldg(a.deg_l + q);
-  if (p1 - p0 == 2) {
-    const int sa = __ldg(a.var_slots + p0), sb = __ldg(a.var_slots + p0 + 1);
-    const T s = __ldg(db + sa) + __ldg(db + sb);
-    if (x >= 0) {
-      xbuf[x] = s;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid == 0) *a.tile_counter = 0u;
+  const int n_ell_thr = (((a.n_ell + 1) >> 1) + 31) & ~31;  // whole warps
+  if (tid < n_ell_thr) {
+    if (2 * tid >= a.n_ell) return;
+    const int q = 2 * tid;
+    const int2 p0 = __ldg(a.ell + q);
+    const int2 p1 = q + 1 < a.n_ell ? __ldg(a.ell + q + 1) : make_int2(-1, -1);
+    const T x0 = __ldg(db + p0.x);
+    const T y0 = p0.y >= 0 ? __ldg(db + p0.y) : T(0);
+    const T x1 = p1.x >= 0 ? __ldg(db + p1.x) : T(0);
+    const T y1 = p1.y >= 0 ? __ldg(db + p1.y) : T(0);
+    if (p0.y >= 0) {
+      const T v = (x0 + y0) / T(2);
+      out[p0.x] = v;
+      out[p0.y] = v;
     } else {
-      const T v = s / T(deg);
-      out[sa] = v;
-      out[sb] = v;
+      out[p0.x] = x0;  // |J_i| = 1: the average is the value itself
+    }
+    if (p1.x >= 0) {
+      if (p1.y >= 0) {
+        const T v = (x1 + y1) / T(2);
+        out[p1.x] = v;
+        out[p1.y] = v;
+      } else {
+        out[p1.x] = x1;
+      }
     }
     return;
   }
-  T s = T(0);
-  int64_t p = p0;
-  for (; p + 1 < p1; p += 2) {
-    const int sa = __ldg(a.var_slots + p), sb = __ldg(a.var_slots + p + 1);
-    const T va = __ldg(db + sa), vb = __ldg(db + sb);
-    s += va;
-    s += vb;
+  // CSR part: a group of G lanes per variable; lane j sums slots j, j+G, ...
+  // in order, then a fixed-shape shuffle tree combines the lanes (deterministic)
+  const int G = a.group;
+  const int gt = tid - n_ell_thr;
+  const int q = gt / G, j = gt % G;
+  const bool on = q < a.n;
+  T *__restrict__ xbuf = reinterpret_cast<T *>(a.xbuf);
+  int64_t p0 = 0, p1 = 0;
+  if (on) {
+    p0 = __ldg(a.var_ptr + q);
+    p1 = __ldg(a.var_ptr + q + 1);
   }
-  if (p < p1) s += __ldg(db + __ldg(a.var_slots + p));
+  T s = T(0);
+  for (int64_t p = p0 + j; p < p1; p += G) s += __ldg(db + __ldg(a.var_slots + p));
+  // the group is G consecutive lanes of one warp (G divides 32, threads of
+  // the CSR part start at a multiple of 32: n_ell_thr is rounded up)
+  for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+  if (!on) return;
+  const int x = a.var_xidx ? __ldg(a.var_xidx + q) : -1;
   if (x >= 0) {
-    xbuf[x] = s;
+    if (j == 0) xbuf[x] = s;
     return;
   }
-  const T v = s / T(deg);
-  for (p = p0; p < p1; ++p) out[__ldg(a.var_slots + p)] = v;
+  const T v = s / T(__ldg(a.deg_l + q));
+  for (int64_t p = p0 + j; p < p1; p += G) out[__ldg(a.var_slots + p)] = v;
 }
 
 // Shared variables after the NCCL exchange: average and scatter into the local slots.
@@ -676,7 +708,8 @@ static int grid_for(int64_t n, int block) {
 
 int launch_avg(int precision, const AvgArgs &a, void *stream) {
   const int block = 256;
-  const int grid = (int)std::max<int64_t>(1, ((int64_t)a.n + block - 1) / block);
+  const int64_t threads = (int64_t)((((a.n_ell + 1) / 2) + 31) & ~31) + (int64_t)a.n * a.group;
+  const int grid = (int)std::max<int64_t>(1, (threads + block - 1) / block);
   if (precision == 64)
     avg_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(a);
   else
@@ -702,6 +735,11 @@ int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, voi
     add_deferred_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, (double *)lambda, (double *)delta);
   else
     add_deferred_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, (float *)lambda, (float *)delta);
+  return (int)cudaGetLastError();
+}
+
+int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream) {
+  lb_reduce_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(lb_part, n, out);
   return (int)cudaGetLastError();
 }
 

@@ -666,6 +666,30 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     for (size_t q = 0; q < P.shared_vars.size(); ++q) xpos[P.shared_vars[q]] = (int32_t)q;
     for (size_t q = 0; q < P.var_list.size(); ++q) P.var_xidx[q] = xpos[P.var_list[q]];
   }
+  // averaging layout: variables with <= 2 local slots that are not exchanged
+  // keep their slot pair inline (ELL, one 8-byte load); the rest stay in CSR
+  {
+    std::vector<int32_t> csr_list, csr_slots, csr_x;
+    std::vector<int64_t> csr_ptr(1, 0);
+    P.ell.clear();
+    for (size_t q = 0; q < P.var_list.size(); ++q) {
+      const int64_t a = P.var_ptr[q], b = P.var_ptr[q + 1];
+      if (b - a <= 2 && P.var_xidx[q] < 0) {
+        P.ell.push_back(P.var_slots[a]);
+        P.ell.push_back(b - a == 2 ? P.var_slots[a + 1] : -1);
+      } else {
+        csr_list.push_back(P.var_list[q]);
+        csr_x.push_back(P.var_xidx[q]);
+        for (int64_t p = a; p < b; ++p) csr_slots.push_back(P.var_slots[p]);
+        csr_ptr.push_back((int64_t)csr_slots.size());
+      }
+    }
+    P.n_vars_local = (int64_t)P.var_list.size();
+    P.var_list.swap(csr_list);
+    P.var_ptr.swap(csr_ptr);
+    P.var_slots.swap(csr_slots);
+    P.var_xidx.swap(csr_x);
+  }
   P.deg_list.resize(P.var_list.size());
   for (size_t q = 0; q < P.var_list.size(); ++q) P.deg_list[q] = P.deg_global[P.var_list[q]];
   P.x_local.assign(P.shared_vars.size(), -1);
@@ -737,7 +761,7 @@ fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out) {
   out->nodes = P.n_nodes;
   out->arcs = 2 * P.n_nodes;
   out->slots = P.n_slots;
-  out->vars_local = (int64_t)P.var_list.size();
+  out->vars_local = P.n_vars_local;
   out->vars_shared = 0;
   for (int32_t x : P.var_xidx) out->vars_shared += x >= 0;
   int64_t fv = 0;

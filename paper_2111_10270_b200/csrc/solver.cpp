@@ -44,9 +44,9 @@ struct Nccl {
   nccl_comm comm = nullptr;
 };
 
-enum KernelId { kKSweepFwd = 0, kKSweepBwd, kKEnergy, kKAvg, kKAvgFinish, kKAllreduce, kKAddDeferred, kKFill, kKCount };
+enum KernelId { kKSweepFwd = 0, kKSweepBwd, kKEnergy, kKAvg, kKAvgFinish, kKAllreduce, kKAddDeferred, kKFill, kKLbReduce, kKCount };
 const char *kKernelNames[kKCount] = {"sweep_forward", "sweep_backward", "sweep_energy", "avg", "avg_finish",
-                                     "nccl_allreduce", "add_deferred", "fill"};
+                                     "nccl_allreduce", "add_deferred", "fill", "lb_reduce"};
 
 struct EventRec {
   int kernel;
@@ -85,6 +85,9 @@ struct fdog_solver {
   void *d_delta[2] = {nullptr, nullptr};
   void *d_m0 = nullptr, *d_m1 = nullptr;
   int32_t *d_var_slots = nullptr, *d_var_xidx = nullptr, *d_deg_list = nullptr;
+  int2 *d_ell = nullptr;
+  int32_t n_ell = 0, csr_group = 1;
+  bool lb_dirty = false;  // per-tile partials not reduced yet
   int64_t *d_var_ptr = nullptr;
   double *d_lb_part = nullptr, *d_lb = nullptr;
   unsigned int *d_counter = nullptr;
@@ -200,7 +203,6 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   a.omega = omega;
   a.clamp = s->clamp;
   a.lb_part = s->d_lb_part;
-  a.lb_out = s->d_lb;
   a.done_counter = s->d_counter;
   a.tile_counter = s->d_counter + 1;
   a.max_nodes = s->max_nodes;
@@ -219,12 +221,17 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
     e = launch_sweep(s->precision, mode, rec, a, s->grid, s->block, s->smem, s->stream);
   }
   if (e) return cuda_fail((cudaError_t)e, "sweep launch");
+  s->lb_dirty = true;
   return FDOG_OK;
 }
 
 fdog_status run_avg(fdog_solver *s) {
   AvgArgs a{};
+  a.n_ell = s->n_ell;
+  a.ell = s->d_ell;
+  a.tile_counter = s->d_counter + 1;
   a.n = s->n_varlist;
+  a.group = s->csr_group;
   a.var_ptr = s->d_var_ptr;
   a.var_slots = s->d_var_slots;
   a.var_xidx = s->world > 1 ? s->d_var_xidx : nullptr;
@@ -448,6 +455,17 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   if ((st = upload(s, &s->d_var_slots, P.var_slots))) return st;
   if ((st = upload(s, &s->d_var_xidx, P.var_xidx))) return st;
   if ((st = upload(s, &s->d_deg_list, P.deg_list))) return st;
+  {
+    std::vector<int2> ell(P.ell.size() / 2);
+    for (size_t q = 0; q < ell.size(); ++q) ell[q] = make_int2(P.ell[2 * q], P.ell[2 * q + 1]);
+    s->n_ell = (int32_t)ell.size();
+    int64_t maxdeg = 1;
+    for (size_t q = 0; q + 1 < P.var_ptr.size(); ++q) maxdeg = std::max<int64_t>(maxdeg, P.var_ptr[q + 1] - P.var_ptr[q]);
+    // lanes per CSR variable: about four slots per lane for the widest variable
+    s->csr_group = 1;
+    while (s->csr_group < 32 && 4 * s->csr_group < maxdeg) s->csr_group *= 2;
+    if ((st = upload(s, &s->d_ell, ell))) return st;
+  }
   if ((st = upload(s, &s->d_x_local, P.x_local))) return st;
   if ((st = upload(s, &s->d_x_deg, P.x_deg))) return st;
   const size_t slot_bytes = (size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz;
@@ -649,6 +667,7 @@ fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
     s->launches += s->graph_launches * n_iter;
     s->passes += 2 * (int64_t)n_iter;
     s->dist_state = 0;
+    s->lb_dirty = true;  // the replayed sweeps wrote new per-tile partials
     return FDOG_OK;
   }
   for (int32_t t = 0; t < n_iter; ++t) {
@@ -664,6 +683,15 @@ fdog_status fdog_lower_bound(fdog_solver *s, double *out) {
   if (!s || !out) {
     set_error("null argument");
     return FDOG_EINVAL;
+  }
+  if (s->lb_dirty) {
+    int e;
+    {
+      Timed t(s, kKLbReduce);
+      e = launch_lb_reduce(s->d_lb_part, s->n_tiles, s->d_lb, s->stream);
+    }
+    if (e) return cuda_fail((cudaError_t)e, "lb_reduce launch");
+    s->lb_dirty = false;
   }
   double v = 0.0;
   CK(cudaMemcpyAsync(&v, s->d_lb, sizeof(double), cudaMemcpyDeviceToHost, s->stream), "D2H");

@@ -202,7 +202,7 @@ def test_graph_replay_matches_direct_launches(monkeypatch):
     g1 = F.Solver(p, precision=32)
     monkeypatch.setenv("FDOG_GRAPHS", "0")
     g2 = F.Solver(p, precision=32)
-    for n, om in ((3, 0.5), (2, 0.3), (1, 0.5)):
+    for n, om in ((3, 0.5), (2, 0.3), (1, 0.5), (1, 0.5)):
         g1.iterate(n, om); g2.iterate(n, om)
         assert np.array_equal(g1.lam(), g2.lam()) and g1.lower_bound() == g2.lower_bound()
     g1.pass_(True, 0.5); g2.pass_(True, 0.5)      # odd parity, then graphs again
