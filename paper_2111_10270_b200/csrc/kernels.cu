@@ -58,21 +58,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// The last CTA of a sweep resets the scheduler counters for the next launch.
-__device__ void last_cta_reset(unsigned int *counter, unsigned int *tile_counter) {
-  __shared__ bool is_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned prev = atomicAdd(counter, 1u);
-    is_last = (prev == gridDim.x - 1);
-    if (is_last) {
-      *counter = 0u;
-      *tile_counter = 0u;
-    }
-  }
-}
-
 // Bound of the last pass (A7): the per-tile partials summed in a fixed order
 // (deterministic for any tile-to-warp assignment); one CTA, launched on demand
 // by fdog_lower_bound.
@@ -475,33 +460,28 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   }
   __syncwarp();
 
-  // dynamic tile scheduler: lane 0 claims tiles from a global counter (reset by
-  // the last CTA); claims run one tile ahead so the atomic's latency overlaps
-  // the current tile
-  auto claim = [&]() -> int {
-    int x = 0;
-    if (lane == 0) x = (int)atomicAdd(a.tile_counter, 1u);
-    return __shfl_sync(0xffffffffu, x, 0);
-  };
-  // split claim: lane 0 issues the atomic, the broadcast happens one tile later
-  // so the atomic's round trip overlaps the tile's work
+  // tile schedule: warp w takes tiles w and w + W statically (tiles are sorted
+  // by decreasing cost); later tiles are claimed from a global counter (reset
+  // before every sweep), one claim in flight two tiles ahead of its use
+  const int W = gridDim.x * wpb;
   auto claim_issue = [&]() -> int { return lane == 0 ? (int)atomicAdd(a.tile_counter, 1u) : 0; };
-  auto claim_get = [&](int raw) -> int { return __shfl_sync(0xffffffffu, raw, 0); };
+  auto claim_get = [&](int raw) -> int { return 2 * W + __shfl_sync(0xffffffffu, raw, 0); };
   // pipeline per warp: the claim for the tile after next is in flight, the
   // next tile's descriptor is loaded and its TMA stage loads are issued, while
   // the current tile is processed
   uint32_t phase = 0;  // bit b = parity of bar[b]
   int b = 0;
-  int t = claim();
+  int t = gwarp;
   TileDesc d;
   if (t < a.n_tiles) {
     d = a.tiles[t];
     if ((d.kind & 2) && lane == 0) issue_stage<T, MODE>(a, d, stage_at<T>(sbuf0, d), &bar[0]);
   }
-  int tn = t < a.n_tiles ? claim() : a.n_tiles;
+  int tn = gwarp + W < a.n_tiles ? gwarp + W : a.n_tiles;
   TileDesc dn;
   if (tn < a.n_tiles) dn = a.tiles[tn];
-  int raw_nn = tn < a.n_tiles ? claim_issue() : 0;
+  int raw_nn = (tn < a.n_tiles && 2 * W < a.n_tiles) ? claim_issue() : 0;
+  bool pending = tn < a.n_tiles && 2 * W < a.n_tiles;  // a claim is in flight
   while (t < a.n_tiles) {
     const bool has_next = tn < a.n_tiles;
     const int bn = a.NB > 1 ? (b ^ 1) : 0;
@@ -509,10 +489,15 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
       bulk_wait_read_all();  // the bulk stores issued from stage bn have read their source
       issue_stage<T, MODE>(a, dn, stage_at<T>(bn ? sbuf1 : sbuf0, dn), &bar[bn]);
     }
-    const int tnn = has_next ? claim_get(raw_nn) : a.n_tiles;
+    int tnn = a.n_tiles;
+    if (pending) {
+      tnn = claim_get(raw_nn);
+      if (tnn > a.n_tiles) tnn = a.n_tiles;
+    }
     TileDesc dnn;
     if (tnn < a.n_tiles) dnn = a.tiles[tnn];  // used one tile later
-    raw_nn = tnn < a.n_tiles ? claim_issue() : 0;
+    pending = tnn < a.n_tiles;
+    raw_nn = pending ? claim_issue() : 0;
     const int L = d.lanes;
     const bool active = lane < L;
     const bool valid = lane < d.n_lanes;
@@ -573,7 +558,6 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   }
   if (lane == 0) bulk_wait_read_all();  // shared memory must outlive the TMA stores' reads
   __syncwarp();
-  last_cta_reset(a.done_counter, a.tile_counter);
 }
 
 // Deferred averaging (A1).  avg_i = (sum over the slots of i, in

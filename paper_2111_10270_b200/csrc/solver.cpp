@@ -214,8 +214,12 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   a.dist = s->d_dist;
   a.scratch = s->d_scratch;
   a.scratch_stride = s->scratch_stride;
-  const bool rec = s->record_mm && mode != kEnergy;
+  const bool rec = s->record_mm && (mode == kForward || mode == kBackward);
   int e;
+  if (mode != kForward && mode != kBackward) {
+    // not preceded by avg_kernel: reset the dynamic tile counter here
+    CK(cudaMemsetAsync(s->d_counter + 1, 0, sizeof(unsigned int), s->stream), "memset");
+  }
   {
     Timed t(s, mode == kForward ? kKSweepFwd : mode == kBackward ? kKSweepBwd : kKEnergy);
     e = launch_sweep(s->precision, mode, rec, a, s->grid, s->block, s->smem, s->stream);
