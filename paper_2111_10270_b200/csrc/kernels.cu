@@ -291,57 +291,75 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
 // marginalisation rows of the BASELINE workloads).  Same arithmetic and the
 // same D / va conventions as process_bdd, with the per-partition values of the
 // sweep direction in registers and no loops over nodes.
-template <typename T>
-__device__ __forceinline__ void push2(T x, int r, T &a0, T &a1) {
-  if (r == 0) a0 = fmin(a0, x);
-  if (r == 1) a1 = fmin(a1, x);
-}
-
-template <typename T, int MODE, bool REC>
-__device__ __forceinline__ double process_bdd_w2(const int K, const int32_t *ho, const uint32_t *tp, const int ts,
-                                                 const int L, T *lam, T *va, T *D, const bool valid, const T omega,
+template <typename T, int MODE, bool REC, int LC>
+__device__ __forceinline__ double process_bdd_w2(const int K, const int32_t *ho, const uint32_t *tp, const int ts_rt,
+                                                 const int L_rt, T *lam, T *va, T *D, const bool valid, const T omega,
                                                  const T clamp, T *m0g, T *m1g) {
+  // LC = 32: full shared-topology tile, compile-time strides (shifts and
+  // immediate shared-memory offsets); LC = 0: runtime lane count / stride
+  const int L = LC ? LC : L_rt;
+  const int ts = LC ? 1 : ts_rt;
   const T inf = t_inf<T>();
   double acc = 0.0;
+  auto finish = [&](int h, T l, T m0, T m1r) -> T {
+    const T m1 = l + m1r;  // P:312
+    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+    const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);  // P:641
+    if (valid) {
+      lam[h * L] = lam_new;
+      va[h * L] = delta;
+      if (REC) {
+        m0g[h * L] = m0;
+        m1g[h * L] = m1;
+      }
+      acc += (double)fmin(delta, T(0));
+    } else {
+      va[h * L] = T(0);
+    }
+    return lam_new;
+  };
   if (MODE == kForward) {
     T c0 = T(0), c1 = inf;  // shp(r, .) of the (up to) two nodes of P_h
+    int n0 = ho[0];
 #pragma unroll 1
-    for (int h = 0; h < K; ++h) {
-      const int n0 = ho[h], n1 = ho[h + 1];
+    for (int h = 0; h < K - 1; ++h) {
+      const int n1 = ho[h + 1];
       const uint32_t e0 = tp[n0 * ts];
       const int lo0 = (int)(e0 & 0xFFFFu), hi0 = (int)(e0 >> 16);
       D[n0 * L] = c0;  // shp(v, T) of P_h is no longer needed: keep shp(r, v)
       T m0 = c0 + D[lo0 * L], m1r = c0 + D[hi0 * L];
-      T nl0 = inf, nl1 = inf, nh0 = inf, nh1 = inf;
-      push2(c0, lo0 - n1, nl0, nl1);
-      push2(c0, hi0 - n1, nh0, nh1);
+      // relaxation into P_{h+1} (nodes n1, n1 + 1); other targets are bottom
+      T nl0 = lo0 == n1 ? c0 : inf, nl1 = lo0 == n1 + 1 ? c0 : inf;
+      T nh0 = hi0 == n1 ? c0 : inf, nh1 = hi0 == n1 + 1 ? c0 : inf;
       if (n1 - n0 > 1) {
         const uint32_t e1 = tp[(n0 + 1) * ts];
         const int lo1 = (int)(e1 & 0xFFFFu), hi1 = (int)(e1 >> 16);
         D[(n0 + 1) * L] = c1;
         m0 = fmin(m0, c1 + D[lo1 * L]);
         m1r = fmin(m1r, c1 + D[hi1 * L]);
-        push2(c1, lo1 - n1, nl0, nl1);
-        push2(c1, hi1 - n1, nh0, nh1);
+        if (lo1 == n1) nl0 = fmin(nl0, c1);
+        if (lo1 == n1 + 1) nl1 = fmin(nl1, c1);
+        if (hi1 == n1) nh0 = fmin(nh0, c1);
+        if (hi1 == n1 + 1) nh1 = fmin(nh1, c1);
       }
-      const T l = lam[h * L];
-      const T m1 = l + m1r;
-      const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
-      const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
-      if (valid) {
-        lam[h * L] = lam_new;
-        va[h * L] = delta;
-        if (REC) {
-          m0g[h * L] = m0;
-          m1g[h * L] = m1;
-        }
-        acc += (double)fmin(delta, T(0));
-      } else {
-        va[h * L] = T(0);
-      }
+      const T lam_new = finish(h, lam[h * L], m0, m1r);
       c0 = fmin(nl0, nh0 + lam_new);  // A4: 1-arcs priced with the updated lambda_h
       c1 = fmin(nl1, nh1 + lam_new);
-      if (h == K - 1 && valid) acc += (double)fmin(m0, lam_new + m1r);  // E^j
+      n0 = n1;
+    }
+    {  // last partition: successors are terminals (sentinels of D)
+      const int h = K - 1;
+      const uint32_t e0 = tp[n0 * ts];
+      D[n0 * L] = c0;
+      T m0 = c0 + D[(e0 & 0xFFFFu) * L], m1r = c0 + D[(e0 >> 16) * L];
+      if (ho[K] - n0 > 1) {
+        const uint32_t e1 = tp[(n0 + 1) * ts];
+        D[(n0 + 1) * L] = c1;
+        m0 = fmin(m0, c1 + D[(e1 & 0xFFFFu) * L]);
+        m1r = fmin(m1r, c1 + D[(e1 >> 16) * L]);
+      }
+      const T lam_new = finish(h, lam[h * L], m0, m1r);
+      if (valid) acc += (double)fmin(m0, lam_new + m1r);  // E^j at the updated lambda
     }
     return acc;
   }
@@ -363,21 +381,7 @@ __device__ __forceinline__ double process_bdd_w2(const int K, const int32_t *ho,
       m0 = fmin(m0, f1 + a1);
       m1r = fmin(m1r, f1 + b1);
     }
-    const T l = lam[h * L];
-    const T m1 = l + m1r;
-    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
-    const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
-    if (valid) {
-      lam[h * L] = lam_new;
-      va[h * L] = delta;
-      if (REC) {
-        m0g[h * L] = m0;
-        m1g[h * L] = m1;
-      }
-      acc += (double)fmin(delta, T(0));
-    } else {
-      va[h * L] = T(0);
-    }
+    const T lam_new = finish(h, lam[h * L], m0, m1r);
     D[n0 * L] = fmin(a0, lam_new + b0);  // shp(v, T) with the updated lambda_h
     if (two) D[(n0 + 1) * L] = fmin(a1, lam_new + b1);
   }
@@ -513,9 +517,12 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
         T *R = reinterpret_cast<T *>(rbase) + lane;
         T *m0p = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
         T *m1p = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
-        if (kUpd && d.max_w <= 2)
-          acc = process_bdd_w2<T, MODE, REC>(K, s.hop, tp, (d.kind & 1) ? L : 1, L, s.lam + lane, s.va + lane,
-                                             s.dist + lane, valid, omega, clamp, m0p, m1p);
+        if (kUpd && d.max_w <= 2 && L == 32 && !(d.kind & 1))
+          acc = process_bdd_w2<T, MODE, REC, 32>(K, s.hop, tp, 1, 32, s.lam + lane, s.va + lane, s.dist + lane, valid,
+                                                 omega, clamp, m0p, m1p);
+        else if (kUpd && d.max_w <= 2)
+          acc = process_bdd_w2<T, MODE, REC, 0>(K, s.hop, tp, (d.kind & 1) ? L : 1, L, s.lam + lane, s.va + lane,
+                                                s.dist + lane, valid, omega, clamp, m0p, m1p);
         else
           acc = process_bdd<T, MODE, REC>(K, d.nodes, s.hop, tp, (d.kind & 1) ? L : 1, L, s.lam + lane, s.va + lane,
                                           s.dist + lane, R, d.max_w, valid, omega, clamp, m0p, m1p);
