@@ -181,15 +181,21 @@ def run_gpu(args):
         if world == 1:
             raise SystemExit(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes")
     torch.cuda.set_device(local)
-    uid = None
     nccl_lib = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        import nvidia.nccl  # namespace package: the torch-bundled NCCL
+        nccl_lib = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+
+    def new_uid():
+        # a fresh ncclUniqueId per communicator, broadcast through torch.distributed
+        if world == 1:
+            return None
         obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-        import nvidia.nccl
-        nccl_lib = os.path.join(os.path.dirname(nvidia.nccl.__file__), "lib", "libnccl.so.2")
+        return obj[0]
+
+    uid = new_uid()
     stream = torch.cuda.Stream()  # a real stream (the legacy default stream's handle is 0)
     torch.cuda.set_stream(stream)
     problem = _workload(args.workload)
@@ -276,12 +282,13 @@ def run_gpu(args):
     # e2e through the public API with host buffers (fresh solver; upload inside)
     e2e = None
     if not args.no_e2e:
+        uid2 = new_uid()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         s2 = F.Solver(plan=plan, precision=prec, device=local, rank=rank, world=world,
-                      nccl_unique_id=uid, nccl_library=nccl_lib, stream=stream.cuda_stream)
+                      nccl_unique_id=uid2, nccl_library=nccl_lib, stream=stream.cuda_stream)
         for _ in range(args.steps):
             s2.iterate(1, OMEGA)
             s2.lower_bound()  # D2H of the step's result (8 bytes)

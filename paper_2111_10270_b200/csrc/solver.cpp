@@ -503,12 +503,12 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   }
   if ((st = alloc(s, &s->d_xbuf, (size_t)std::max<int32_t>(s->n_shared, 1) * s->tsz))) return st;
   if ((st = alloc(s, (void **)&s->d_lb_part, (size_t)std::max(s->n_tiles, 1) * sizeof(double)))) return st;
-  if ((st = alloc(s, (void **)&s->d_lb, sizeof(double)))) return st;
+  if ((st = alloc(s, (void **)&s->d_lb, 2 * sizeof(double)))) return st;
   if ((st = alloc(s, (void **)&s->d_counter, 2 * sizeof(unsigned int)))) return st;
   if ((st = alloc(s, &s->d_scratch, s->n_direct ? (size_t)s->grid * (s->block / 32) * s->scratch_stride * s->tsz : 16)))
     return st;
   CK(cudaMemsetAsync(s->d_counter, 0, 2 * sizeof(unsigned int), s->stream), "memset");
-  CK(cudaMemsetAsync(s->d_lb, 0, sizeof(double), s->stream), "memset");
+  CK(cudaMemsetAsync(s->d_lb, 0, 2 * sizeof(double), s->stream), "memset");
   CK(cudaMemsetAsync(s->d_delta[0], 0, slot_bytes, s->stream), "memset");
   CK(cudaMemsetAsync(s->d_delta[1], 0, slot_bytes, s->stream), "memset");
   if (s->record_mm) {
@@ -703,7 +703,7 @@ fdog_status fdog_lower_bound(fdog_solver *s, double *out) {
   double tot = v + s->free_term;
   if (s->world > 1) {
     // scalar allreduce of the per-rank partials (fp64)
-    double *d = (double *)s->d_lb_part;  // scratch: reuse slot 0 after the sync above
+    double *d = s->d_lb + 1;  // scratch slot for the cross-rank sum
     CK(cudaMemcpyAsync(d, &tot, sizeof(double), cudaMemcpyHostToDevice, s->stream), "H2D");
     int r = s->nccl.allreduce(d, d, 1, kNcclFloat64, kNcclSum, s->nccl.comm, s->stream);
     if (r) {
