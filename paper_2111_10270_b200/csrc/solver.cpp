@@ -243,6 +243,8 @@ fdog_status run_avg(fdog_solver *s) {
   a.delta_bar = s->d_delta[s->cur];
   a.avg_slot = s->d_delta[s->cur ^ 1];
   a.xbuf = s->d_xbuf;
+  if (s->world > 1 && s->n_shared > 0)  // entries of variables this rank does not hold contribute 0
+    CK(cudaMemsetAsync(s->d_xbuf, 0, (size_t)s->n_shared * s->tsz, s->stream), "memset");
   int e;
   {
     Timed t(s, kKAvg);
