@@ -132,6 +132,23 @@ void fdog_destroy(fdog_solver *s);
 fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega);
 /* One pass only: forward (1, ascending) or backward (0). */
 fdog_status fdog_pass(fdog_solver *s, int32_t forward, double omega);
+/* External exchange (world > 1 with nccl_unique_id == NULL): the caller sums
+ * the exchange vectors across ranks itself (e.g. torch.distributed, or several
+ * rank solvers in one process).  A pass is then two calls:
+ *   fdog_pass_begin  -- deferred averaging; this rank's partial sums of the
+ *                       exchanged variables are in the exchange vector;
+ *   (caller: exchange vector <- sum over ranks, via fdog_exchange_read/write)
+ *   fdog_pass_end    -- averages of the exchanged variables + the sweep.
+ * fdog_iterate returns FDOG_ESTATE in this mode, and fdog_lower_bound returns
+ * this rank's part of the bound (the caller sums it). */
+fdog_status fdog_pass_begin(fdog_solver *s, int32_t forward, double omega);
+fdog_status fdog_pass_end(fdog_solver *s, int32_t forward, double omega);
+/* Number of exchanged variables (identical on every rank), and host copies of
+ * the exchange vector (fdog_plan_shared_vars order) as double. */
+fdog_status fdog_exchange_size(const fdog_solver *s, int64_t *n);
+fdog_status fdog_exchange_read(fdog_solver *s, double *out, int64_t len);
+fdog_status fdog_exchange_write(fdog_solver *s, const double *in, int64_t len);
+
 /* Lower bound of the last completed pass (A7): sum_j E^j(lambda^j) +
  * sum_slots min(delta_bar, 0) + sum_free min(c_i, 0); summed over ranks.
  * Synchronises the stream. */

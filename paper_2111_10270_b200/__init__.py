@@ -61,7 +61,8 @@ EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdo
            "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_lower_bound",
            "fdog_finalize", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
            "fdog_get_deferred", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
-           "fdog_profile", "fdog_profile_reset", "fdog_profile_enable", "fdog_last_error", "fdog_version"]
+           "fdog_profile", "fdog_profile_reset", "fdog_profile_enable", "fdog_pass_begin", "fdog_pass_end",
+           "fdog_exchange_size", "fdog_exchange_read", "fdog_exchange_write", "fdog_last_error", "fdog_version"]
 
 _lib = None
 
@@ -102,6 +103,11 @@ def load():
         "fdog_profile": ([P, P, i32, P], C.c_int),
         "fdog_profile_reset": ([P], C.c_int),
         "fdog_profile_enable": ([P, i32], C.c_int),
+        "fdog_pass_begin": ([P, i32, dbl], C.c_int),
+        "fdog_pass_end": ([P, i32, dbl], C.c_int),
+        "fdog_exchange_size": ([P, P], C.c_int),
+        "fdog_exchange_read": ([P, P, i64], C.c_int),
+        "fdog_exchange_write": ([P, P, i64], C.c_int),
         "fdog_last_error": ([], C.c_char_p),
         "fdog_version": ([], C.c_int32),
     }
@@ -306,6 +312,23 @@ class Solver:
 
     def profile_reset(self):
         _check(self._lib.fdog_profile_reset(self._h), "fdog_profile_reset")
+
+    def pass_begin(self, forward: bool, omega: float = 0.5):
+        _check(self._lib.fdog_pass_begin(self._h, 1 if forward else 0, float(omega)), "fdog_pass_begin")
+
+    def pass_end(self, forward: bool, omega: float = 0.5):
+        _check(self._lib.fdog_pass_end(self._h, 1 if forward else 0, float(omega)), "fdog_pass_end")
+
+    def exchange_read(self):
+        n = C.c_int64()
+        _check(self._lib.fdog_exchange_size(self._h, C.byref(n)), "fdog_exchange_size")
+        out = np.empty(max(n.value, 1), np.float64)
+        _check(self._lib.fdog_exchange_read(self._h, _ptr(out), n.value), "fdog_exchange_read")
+        return out[:n.value]
+
+    def exchange_write(self, x):
+        a = np.ascontiguousarray(x, dtype=np.float64)
+        _check(self._lib.fdog_exchange_write(self._h, _ptr(a), a.size), "fdog_exchange_write")
 
     def profile_enable(self, on: bool):
         _check(self._lib.fdog_profile_enable(self._h, 1 if on else 0), "fdog_profile_enable")

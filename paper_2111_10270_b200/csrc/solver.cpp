@@ -65,6 +65,7 @@ struct fdog_solver {
   bool profile = false;
   double clamp = 0.0;
   int rank = 0, world = 1;
+  bool external = false;  // world > 1 without NCCL: the caller performs the exchange
 
   // host copies needed by getters
   std::vector<int64_t> canon_slot;
@@ -229,7 +230,21 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   return FDOG_OK;
 }
 
-fdog_status run_avg(fdog_solver *s) {
+AvgArgs avg_args(fdog_solver *s);
+
+fdog_status run_avg_finish(fdog_solver *s) {
+  if (s->world <= 1 || s->n_shared <= 0) return FDOG_OK;
+  AvgArgs a = avg_args(s);
+  int e;
+  {
+    Timed t(s, kKAvgFinish);
+    e = launch_avg_finish(s->precision, a, s->n_shared, s->d_x_local, s->d_x_deg, s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "avg_finish launch");
+  return FDOG_OK;
+}
+
+AvgArgs avg_args(fdog_solver *s) {
   AvgArgs a{};
   a.n_ell = s->n_ell;
   a.ell = s->d_ell;
@@ -243,6 +258,11 @@ fdog_status run_avg(fdog_solver *s) {
   a.delta_bar = s->d_delta[s->cur];
   a.avg_slot = s->d_delta[s->cur ^ 1];
   a.xbuf = s->d_xbuf;
+  return a;
+}
+
+fdog_status run_avg(fdog_solver *s) {
+  AvgArgs a = avg_args(s);
   if (s->world > 1 && s->n_shared > 0)  // entries of variables this rank does not hold contribute 0
     CK(cudaMemsetAsync(s->d_xbuf, 0, (size_t)s->n_shared * s->tsz, s->stream), "memset");
   int e;
@@ -251,7 +271,7 @@ fdog_status run_avg(fdog_solver *s) {
     e = launch_avg(s->precision, a, s->stream);
   }
   if (e) return cuda_fail((cudaError_t)e, "avg launch");
-  if (s->world > 1 && s->n_shared > 0) {
+  if (s->world > 1 && s->n_shared > 0 && !s->external) {
     int r;
     {
       Timed t(s, kKAllreduce);
@@ -263,29 +283,34 @@ fdog_status run_avg(fdog_solver *s) {
       set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(r) : "error");
       return FDOG_ENCCL;
     }
-    {
-      Timed t(s, kKAvgFinish);
-      e = launch_avg_finish(s->precision, a, s->n_shared, s->d_x_local, s->d_x_deg, s->stream);
-    }
-    if (e) return cuda_fail((cudaError_t)e, "avg_finish launch");
+    return run_avg_finish(s);
   }
   return FDOG_OK;
 }
 
-fdog_status do_pass(fdog_solver *s, bool forward, double omega) {
+// stage 0: conversions + averaging (partials of the exchanged variables in
+// xbuf); stage 1: exchanged averages + sweep + swap.  do_pass runs both.
+fdog_status pass_stage(fdog_solver *s, bool forward, double omega, int stage) {
   fdog_status st;
-  // the pass needs the distances of the opposite direction; after
-  // an unusual call sequence recompute them first
-  if (forward && s->dist_state != 0 && (st = run_sweep(s, kEnergy, omega))) return st;
-  if (!forward && s->dist_state != 1 && (st = run_sweep(s, kCfr, omega))) return st;
-  st = run_avg(s);
-  if (st) return st;
+  if (stage == 0) {
+    // the pass needs the distances of the opposite direction;
+    // after an unusual call sequence recompute them first
+    if (forward && s->dist_state != 0 && (st = run_sweep(s, kEnergy, omega))) return st;
+    if (!forward && s->dist_state != 1 && (st = run_sweep(s, kCfr, omega))) return st;
+    return run_avg(s);
+  }
+  if (s->external && (st = run_avg_finish(s))) return st;
   st = run_sweep(s, forward ? kForward : kBackward, omega);
   if (st) return st;
   s->dist_state = forward ? 1 : 0;
   s->cur ^= 1;  // mbar <- m
   s->passes++;
   return FDOG_OK;
+}
+
+fdog_status do_pass(fdog_solver *s, bool forward, double omega) {
+  fdog_status st = pass_stage(s, forward, omega, 0);
+  return st ? st : pass_stage(s, forward, omega, 1);
 }
 
 fdog_status energy(fdog_solver *s) {
@@ -529,7 +554,8 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
     CK(cudaMemcpyAsync(s->d_lambda, lam.data(), slot_bytes, cudaMemcpyHostToDevice, s->stream), "H2D");
     CK(cudaStreamSynchronize(s->stream), "sync");
   }
-  if (s->world > 1 && (st = init_nccl(s, o))) return st;
+  s->external = s->world > 1 && !o->nccl_unique_id;
+  if (s->world > 1 && !s->external && (st = init_nccl(s, o))) return st;
 
   // algorithmic bytes per launch: per node 2 T (distance read +
   // write) + 4 B topology for per-lane-topology tiles; per slot 4 T (lambda
@@ -621,6 +647,10 @@ fdog_status fdog_pass(fdog_solver *s, int32_t forward, double omega) {
     set_error("null solver");
     return FDOG_EINVAL;
   }
+  if (s->external) {
+    set_error("external-exchange mode: use fdog_pass_begin / fdog_pass_end");
+    return FDOG_ESTATE;
+  }
   if (!(omega > 0.0 && omega <= 1.0)) {
     set_error("omega %g outside (0, 1]", omega);
     return FDOG_EINVAL;
@@ -628,10 +658,77 @@ fdog_status fdog_pass(fdog_solver *s, int32_t forward, double omega) {
   return do_pass(s, forward != 0, omega);
 }
 
+fdog_status fdog_pass_begin(fdog_solver *s, int32_t forward, double omega) {
+  if (!s || !(omega > 0.0 && omega <= 1.0)) {
+    set_error("null solver or omega outside (0, 1]");
+    return FDOG_EINVAL;
+  }
+  if (!s->external) {
+    set_error("fdog_pass_begin needs the external-exchange mode (world > 1, no NCCL id)");
+    return FDOG_ESTATE;
+  }
+  return pass_stage(s, forward != 0, omega, 0);
+}
+
+fdog_status fdog_pass_end(fdog_solver *s, int32_t forward, double omega) {
+  if (!s || !(omega > 0.0 && omega <= 1.0)) {
+    set_error("null solver or omega outside (0, 1]");
+    return FDOG_EINVAL;
+  }
+  if (!s->external) {
+    set_error("fdog_pass_end needs the external-exchange mode (world > 1, no NCCL id)");
+    return FDOG_ESTATE;
+  }
+  return pass_stage(s, forward != 0, omega, 1);
+}
+
+fdog_status fdog_exchange_size(const fdog_solver *s, int64_t *n) {
+  if (!s || !n) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  *n = s->n_shared;
+  return FDOG_OK;
+}
+
+fdog_status fdog_exchange_read(fdog_solver *s, double *out, int64_t len) {
+  if (!s || (len > 0 && !out) || len < s->n_shared) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  if (s->n_shared == 0) return FDOG_OK;
+  std::vector<unsigned char> buf((size_t)s->n_shared * s->tsz);
+  CK(cudaMemcpyAsync(buf.data(), s->d_xbuf, buf.size(), cudaMemcpyDeviceToHost, s->stream), "D2H");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  for (int32_t q = 0; q < s->n_shared; ++q)
+    out[q] = s->precision == 64 ? ((double *)buf.data())[q] : (double)((float *)buf.data())[q];
+  return FDOG_OK;
+}
+
+fdog_status fdog_exchange_write(fdog_solver *s, const double *in, int64_t len) {
+  if (!s || (len > 0 && !in) || len != s->n_shared) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  if (s->n_shared == 0) return FDOG_OK;
+  std::vector<unsigned char> buf((size_t)s->n_shared * s->tsz);
+  for (int32_t q = 0; q < s->n_shared; ++q) {
+    if (s->precision == 64) ((double *)buf.data())[q] = in[q];
+    else ((float *)buf.data())[q] = (float)in[q];
+  }
+  CK(cudaMemcpyAsync(s->d_xbuf, buf.data(), buf.size(), cudaMemcpyHostToDevice, s->stream), "H2D");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  return FDOG_OK;
+}
+
 fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
   if (!s || n_iter < 0) {
     set_error("null solver or negative n_iter");
     return FDOG_EINVAL;
+  }
+  if (s->external) {
+    set_error("external-exchange mode: use fdog_pass_begin / fdog_pass_end");
+    return FDOG_ESTATE;
   }
   if (!(omega > 0.0 && omega <= 1.0)) {
     set_error("omega %g outside (0, 1]", omega);
@@ -703,7 +800,7 @@ fdog_status fdog_lower_bound(fdog_solver *s, double *out) {
   CK(cudaMemcpyAsync(&v, s->d_lb, sizeof(double), cudaMemcpyDeviceToHost, s->stream), "D2H");
   CK(cudaStreamSynchronize(s->stream), "sync");
   double tot = v + s->free_term;
-  if (s->world > 1) {
+  if (s->world > 1 && !s->external) {
     // scalar allreduce of the per-rank partials (fp64)
     double *d = s->d_lb + 1;  // scratch slot for the cross-rank sum
     CK(cudaMemcpyAsync(d, &tot, sizeof(double), cudaMemcpyHostToDevice, s->stream), "H2D");
