@@ -88,6 +88,7 @@ typedef struct {
   int64_t staged_tiles;  /* tiles staged on chip by TMA (the rest run from global)    */
   int32_t sweep_grid, sweep_block; /* persistent sweep launch configuration           */
   int64_t sweep_smem_per_warp;     /* bytes of shared memory per warp                 */
+  int32_t sweep_streaming;         /* 1: passes use the streaming sweep kernel        */
 } fdog_stats_t;
 
 typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */

@@ -172,6 +172,7 @@ struct AvgArgs {
 // returns the cudaError_t as int
 int launch_sweep(int precision, int mode, bool record, const SweepArgs &a, int grid, int block,
                  size_t smem, void *stream);
+int launch_sweep_stream(int precision, int mode, bool record, const SweepArgs &a, void *stream);
 int sweep_occupancy(int precision, int mode, bool record, int block, size_t smem, int *blocks_per_sm);
 int launch_avg(int precision, const AvgArgs &a, void *stream);
 int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,

@@ -573,6 +573,157 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
 // own delta).  Threads [0, ceil(n_ell/2)) take two ELL variables each (slot
 // pair inline, |J_i| <= 2); the remaining threads take one CSR variable each.
 // Thread 0 also resets the sweep's tile counter.
+// ---------------------------------------------------------------------------
+// Streaming sweep for narrow tiles (every partition <= 2 nodes): one warp per
+// tile, no shared memory.  Each lane streams its BDD partition by partition
+// straight from global memory -- per partition one coalesced 128-byte access
+// per array (lambda, avg/delta, the two distances) -- with the loads of the
+// next two partitions in flight (software pipeline), so occupancy is bounded
+// by registers only.  Same arithmetic and D/va conventions as process_bdd_w2.
+template <typename T>
+struct HopSet {
+  int n0, n1, n2;   // P_h = [n0, n1), P_{h+1} = [n1, n2)
+  uint32_t e0, e1;  // topology of the (up to) two nodes of P_h
+  T l, av;          // lambda_h, avg_i (in va)
+  T x0, x1;         // forward: shp(., T) of P_{h+1};  backward: shp(r, .) of P_h
+};
+
+template <typename T, int MODE>
+__device__ __forceinline__ void load_hop(HopSet<T> &s, int h, int K, const int32_t *ho, const uint32_t *tp, int ts,
+                                         int L, const T *lam, const T *va, const T *D) {
+  const T inf = t_inf<T>();
+  s.n0 = __ldg(ho + h);
+  s.n1 = __ldg(ho + h + 1);
+  s.n2 = h + 1 < K ? __ldg(ho + h + 2) : s.n1;
+  s.e0 = __ldg(tp + s.n0 * ts);
+  s.e1 = s.n1 - s.n0 > 1 ? __ldg(tp + (s.n0 + 1) * ts) : 0u;
+  s.l = lam[h * L];
+  s.av = va[h * L];
+  if (MODE == kForward) {
+    s.x0 = h + 1 < K ? D[s.n1 * L] : inf;
+    s.x1 = (h + 1 < K && s.n2 - s.n1 > 1) ? D[(s.n1 + 1) * L] : inf;
+  } else {
+    s.x0 = D[s.n0 * L];
+    s.x1 = s.n1 - s.n0 > 1 ? D[(s.n0 + 1) * L] : inf;
+  }
+}
+
+// successor value: top, bottom, or a node of the next partition (held in
+// registers).  The sentinels are tested first: on the last partition
+// n1 == nodes == top.
+template <typename T>
+__device__ __forceinline__ T succ(int code, int n1, int top, T v0, T v1) {
+  const T inf = t_inf<T>();
+  return code == top ? T(0) : code > top ? inf : code == n1 ? v0 : code == n1 + 1 ? v1 : inf;
+}
+
+template <typename T, int MODE, bool REC>
+__global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= a.n_tiles) return;  // whole warps
+  const TileDesc d = a.tiles[t];
+  const int L = d.lanes, K = d.K;
+  const bool valid = lane < d.n_lanes;
+  double acc = 0.0;
+  if (lane < L) {
+    const int32_t *ho = a.hop_off + d.hop_base;
+    const int ts = (d.kind & 1) ? L : 1;
+    const uint32_t *tp = a.topo + d.topo_base + ((d.kind & 1) ? lane : 0);
+    T *lam = reinterpret_cast<T *>(a.lambda) + d.slot_base + lane;
+    T *va = reinterpret_cast<T *>(a.delta_out) + d.slot_base + lane;
+    T *D = reinterpret_cast<T *>(a.dist) + d.dist_base + lane;
+    T *m0g = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
+    T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
+    const T inf = t_inf<T>();
+    const T omega = T(a.omega), clamp = T(a.clamp);
+    const int top = d.nodes;
+    auto finish = [&](int h, T l, T av, T m0, T m1r) -> T {
+      const T m1 = l + m1r;
+      const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+      const T lam_new = add_rn(sub_rn(l, delta), av);
+      if (valid) {
+        lam[h * L] = lam_new;
+        va[h * L] = delta;
+        if (REC) {
+          m0g[h * L] = m0;
+          m1g[h * L] = m1;
+        }
+        acc += (double)fmin(delta, T(0));
+      } else {
+        va[h * L] = T(0);
+      }
+      return lam_new;
+    };
+    HopSet<T> s0, s1, s2;
+    if (MODE == kForward) {
+      load_hop<T, MODE>(s0, 0, K, ho, tp, ts, L, lam, va, D);
+      if (K > 1) load_hop<T, MODE>(s1, 1, K, ho, tp, ts, L, lam, va, D);
+      T c0 = T(0), c1 = inf;  // shp(r, .) of P_h
+#pragma unroll 1
+      for (int h = 0; h < K; ++h) {
+        if (h + 2 < K) load_hop<T, MODE>(s2, h + 2, K, ho, tp, ts, L, lam, va, D);
+        const int n0 = s0.n0, n1 = s0.n1;
+        const int lo0 = (int)(s0.e0 & 0xFFFFu), hi0 = (int)(s0.e0 >> 16);
+        D[n0 * L] = c0;  // keep shp(r, v) (P:315-316 reuse for the backward pass)
+        T m0 = c0 + succ(lo0, n1, top, s0.x0, s0.x1), m1r = c0 + succ(hi0, n1, top, s0.x0, s0.x1);
+        T nl0 = lo0 == n1 ? c0 : inf, nl1 = lo0 == n1 + 1 ? c0 : inf;
+        T nh0 = hi0 == n1 ? c0 : inf, nh1 = hi0 == n1 + 1 ? c0 : inf;
+        if (n1 - n0 > 1) {
+          const int lo1 = (int)(s0.e1 & 0xFFFFu), hi1 = (int)(s0.e1 >> 16);
+          D[(n0 + 1) * L] = c1;
+          m0 = fmin(m0, c1 + succ(lo1, n1, top, s0.x0, s0.x1));
+          m1r = fmin(m1r, c1 + succ(hi1, n1, top, s0.x0, s0.x1));
+          if (lo1 == n1) nl0 = fmin(nl0, c1);
+          if (lo1 == n1 + 1) nl1 = fmin(nl1, c1);
+          if (hi1 == n1) nh0 = fmin(nh0, c1);
+          if (hi1 == n1 + 1) nh1 = fmin(nh1, c1);
+        }
+        const T lam_new = finish(h, s0.l, s0.av, m0, m1r);
+        if (h == K - 1) {
+          if (valid) acc += (double)fmin(m0, lam_new + m1r);  // E^j at the updated lambda
+        } else {
+          c0 = fmin(nl0, nh0 + lam_new);  // A4
+          c1 = fmin(nl1, nh1 + lam_new);
+        }
+        s0 = s1;
+        s1 = s2;
+      }
+    } else {
+      load_hop<T, MODE>(s0, K - 1, K, ho, tp, ts, L, lam, va, D);
+      if (K > 1) load_hop<T, MODE>(s1, K - 2, K, ho, tp, ts, L, lam, va, D);
+      T ct0 = inf, ct1 = inf;  // shp(., T) of P_{h+1}
+#pragma unroll 1
+      for (int h = K - 1; h >= 0; --h) {
+        if (h >= 2) load_hop<T, MODE>(s2, h - 2, K, ho, tp, ts, L, lam, va, D);
+        const int n0 = s0.n0, n1 = s0.n1;
+        const int lo0 = (int)(s0.e0 & 0xFFFFu), hi0 = (int)(s0.e0 >> 16);
+        const T a0 = succ(lo0, n1, top, ct0, ct1), b0 = succ(hi0, n1, top, ct0, ct1);
+        T m0 = s0.x0 + a0, m1r = s0.x0 + b0;
+        T a1 = inf, b1 = inf;
+        const bool two = n1 - n0 > 1;
+        if (two) {
+          const int lo1 = (int)(s0.e1 & 0xFFFFu), hi1 = (int)(s0.e1 >> 16);
+          a1 = succ(lo1, n1, top, ct0, ct1);
+          b1 = succ(hi1, n1, top, ct0, ct1);
+          m0 = fmin(m0, s0.x1 + a1);
+          m1r = fmin(m1r, s0.x1 + b1);
+        }
+        const T lam_new = finish(h, s0.l, s0.av, m0, m1r);
+        ct0 = fmin(a0, lam_new + b0);  // shp(v, T) with the updated lambda_h
+        ct1 = two ? fmin(a1, lam_new + b1) : inf;
+        D[n0 * L] = ct0;
+        if (two) D[(n0 + 1) * L] = ct1;
+        s0 = s1;
+        s1 = s2;
+      }
+      if (valid) acc += (double)ct0;  // E^j = shp(r, T)
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) a.lb_part[t] = acc;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
@@ -681,6 +832,19 @@ int sweep_occupancy(int precision, int mode, bool rec, int block, size_t smem, i
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
+}
+
+template <typename T>
+static const void *stream_fn(int mode, bool rec) {
+  if (mode == kForward) return rec ? (const void *)sweep_stream_kernel<T, kForward, true> : (const void *)sweep_stream_kernel<T, kForward, false>;
+  return rec ? (const void *)sweep_stream_kernel<T, kBackward, true> : (const void *)sweep_stream_kernel<T, kBackward, false>;
+}
+
+int launch_sweep_stream(int precision, int mode, bool rec, const SweepArgs &a, void *stream) {
+  const void *f = precision == 64 ? stream_fn<double>(mode, rec) : stream_fn<float>(mode, rec);
+  void *args[] = {(void *)&a};
+  const int grid = (a.n_tiles + 3) / 4;
+  return (int)cudaLaunchKernel(f, dim3(grid > 0 ? grid : 1), dim3(128), args, 0, (cudaStream_t)stream);
 }
 
 int launch_sweep(int precision, int mode, bool rec, const SweepArgs &a, int grid, int block, size_t smem,

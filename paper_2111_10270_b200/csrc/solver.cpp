@@ -66,6 +66,7 @@ struct fdog_solver {
   double clamp = 0.0;
   int rank = 0, world = 1;
   bool external = false;  // world > 1 without NCCL: the caller performs the exchange
+  bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
 
   // host copies needed by getters
   std::vector<int64_t> canon_slot;
@@ -223,7 +224,10 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   }
   {
     Timed t(s, mode == kForward ? kKSweepFwd : mode == kBackward ? kKSweepBwd : kKEnergy);
-    e = launch_sweep(s->precision, mode, rec, a, s->grid, s->block, s->smem, s->stream);
+    if (s->stream_mode && (mode == kForward || mode == kBackward))
+      e = launch_sweep_stream(s->precision, mode, rec, a, s->stream);
+    else
+      e = launch_sweep(s->precision, mode, rec, a, s->grid, s->block, s->smem, s->stream);
   }
   if (e) return cuda_fail((cudaError_t)e, "sweep launch");
   s->lb_dirty = true;
@@ -462,6 +466,22 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   s->NB = P.NB;
   s->warp_bytes = (size_t)warp_bytes(P.SB, P.DB, P.NB);
   s->n_direct = P.direct_tiles;
+  {
+    // all tiles narrow: the passes stream from global memory (no staging)
+    bool narrow = true;
+    for (const auto &d : tiles) narrow = narrow && d.max_w <= 2;
+    // the TMA-staged kernel wins while enough warps fit per SM; long BDDs (whole
+    // tiles too large to stage for >= 8 warps per SM) stream instead
+    const size_t sm_bytes = (size_t)prop.sharedMemPerMultiprocessor - 4096;
+    const bool staged_ok = sm_bytes / std::max<size_t>(s->warp_bytes, 1) >= 8;
+    const char *m = getenv("FDOG_SWEEP");  // experiment knob: "tma" or "stream"
+    const bool forced = m && (m[0] == 's' || m[0] == 't');
+    s->stream_mode = narrow && (forced ? m[0] == 's' : !staged_ok);
+    if (m && m[0] == 's' && !narrow) {
+      set_error("FDOG_SWEEP=stream needs every partition <= 2 nodes wide");
+      return FDOG_EINVAL;
+    }
+  }
   int warps = (int)std::max<size_t>(1, std::min<size_t>(4, (size_t)prop.sharedMemPerBlockOptin / s->warp_bytes));
   s->block = warps * 32;
   s->smem = (size_t)warps * s->warp_bytes;
@@ -594,6 +614,7 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   s->st.sweep_grid = s->grid;
   s->st.sweep_block = s->block;
   s->st.sweep_smem_per_warp = (int64_t)s->warp_bytes;
+  s->st.sweep_streaming = s->stream_mode ? 1 : 0;
 
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;

@@ -214,6 +214,21 @@ def test_graph_replay_matches_direct_launches(monkeypatch):
     assert "sweep_forward" in g1.profile()
 
 
+@pytest.mark.parametrize("mode", ["tma", "stream"])
+@pytest.mark.parametrize("name,make", [
+    ("gm", lambda: synth.gm_worms_like(13, n_src=70, k_cand=6, knn=8)),
+    ("mrf", lambda: synth.mrf_potts(13, H=9, W=11, L=4)),
+    ("qap", lambda: synth.qap(13, n=8)),
+    ("lap", lambda: synth.lap(synth.LAP4_LITERAL)),
+])
+def test_both_sweep_kernels(oracle_mod, monkeypatch, mode, name, make):
+    """The TMA-staged sweep and the streaming sweep (chosen per problem by
+    default) both match the oracle pass by pass, fp64."""
+    monkeypatch.setenv("FDOG_SWEEP", mode)
+    g, _ = _compare_pass_by_pass(make(), oracle_mod, passes=6)
+    assert g.stats()["sweep_streaming"] == (1 if mode == "stream" else 0)
+
+
 def test_errors_and_state():
     p = synth.spec_two_constraint()
     g = F.Solver(p, precision=64)
