@@ -292,8 +292,34 @@ def qap(seed=0, n=50) -> Problem:
     return rb.build(ybase + P * n * (n - 1), cost, f"qap(seed={seed},n={n})")
 
 
+def _grouped_rows(rb, det, var, extra_vars, extra_coefs, rel, rhs):
+    """One row per detection: its incident variables (coef 1) plus extra columns."""
+    order = np.lexsort((var, det))
+    det, var = det[order], var[order]
+    nd = extra_vars.shape[0]
+    counts = np.bincount(det, minlength=nd)
+    starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    for ln in np.unique(counts):
+        dets = np.flatnonzero(counts == ln)
+        if ln:
+            pos = starts[dets][:, None] + np.arange(ln)[None, :]
+            inc = var[pos]
+        else:
+            inc = np.zeros((dets.size, 0), dtype=np.int64)
+        v = np.concatenate([inc, extra_vars[dets]], axis=1)
+        c = np.concatenate([np.ones((dets.size, ln)), np.broadcast_to(extra_coefs, (dets.size, extra_coefs.size))], axis=1)
+        rb.add(v, c, rel, rhs)
+
+
 def celltrack(seed=0, frames=100, dets=2150, n_trans=5, n_div=3, excl_pairs=None) -> Problem:
-    """Cell tracking shaped like 'Cell tracking - large' (detection / conservation / exclusion)."""
+    """Cell tracking shaped like 'Cell tracking - large' (detection / conservation / exclusion).
+
+    Per detection d: x_d (cost U[-10,1)), appearance a_d and disappearance e_d
+    (U[5,20)); per detection and frame, transitions to its n_trans nearest
+    detections of the next frame (cost 5*dist/max + U[0,4)) and divisions into
+    pairs of those (U[2,8)).  Rows: incoming sum(in) + a_d - x_d = 0, outgoing
+    sum(out) + e_d - x_d = 0, and x_u + x_w <= 1 on random pairs per frame.
+    """
     rng = np.random.default_rng(seed)
     if excl_pairs is None:
         excl_pairs = dets // 2
@@ -301,45 +327,43 @@ def celltrack(seed=0, frames=100, dets=2150, n_trans=5, n_div=3, excl_pairs=None
     pos = rng.uniform(0, 1, size=(T, Dn, 2))
     nd = T * Dn
     did = np.arange(nd).reshape(T, Dn)
-    # variable layout: x_d [nd], a_d [nd], e_d [nd], transitions, divisions
     x0, a0, e0 = 0, nd, 2 * nd
     nv = 3 * nd
     cost = [rng.uniform(-10, 1, size=nd), rng.uniform(5, 20, size=nd), rng.uniform(5, 20, size=nd)]
-    out_vars = [[] for _ in range(nd)]
-    in_vars = [[] for _ in range(nd)]
+    pairs = [(0, 1), (0, 2), (1, 2)][:n_div]
+    in_det, in_var, out_det, out_var = [], [], [], []
     for t in range(T - 1):
-        d = np.linalg.norm(pos[t][:, None, :] - pos[t + 1][None, :, :], axis=2)
-        nbr = np.argsort(d, axis=1, kind="stable")[:, :n_trans]
+        d = np.sqrt(((pos[t][:, None, :] - pos[t + 1][None, :, :]) ** 2).sum(-1))
+        sel = np.argpartition(d, n_trans, axis=1)[:, :n_trans]
+        sel.sort(axis=1)  # ties in distance are broken by index (deterministic)
+        nbr = np.take_along_axis(sel, np.argsort(np.take_along_axis(d, sel, axis=1), axis=1, kind="stable"), axis=1)
         tc = 5.0 * np.take_along_axis(d, nbr, axis=1) / max(d.max(), 1e-9) + rng.uniform(0, 4, size=nbr.shape)
         tv = nv + np.arange(Dn * n_trans).reshape(Dn, n_trans)
         nv += Dn * n_trans
         cost.append(tc.ravel())
-        # divisions: pairs of transition targets (0,1), (0,2), (1,2)
-        pairs = [(0, 1), (0, 2), (1, 2)][:n_div]
         dv = nv + np.arange(Dn * len(pairs)).reshape(Dn, len(pairs))
         nv += Dn * len(pairs)
         cost.append(rng.uniform(2, 8, size=Dn * len(pairs)))
-        for i in range(Dn):
-            src = did[t, i]
-            for q in range(n_trans):
-                tgt = did[t + 1, nbr[i, q]]
-                out_vars[src].append(tv[i, q]); in_vars[tgt].append(tv[i, q])
-            for q, (u, w) in enumerate(pairs):
-                out_vars[src].append(dv[i, q])
-                in_vars[did[t + 1, nbr[i, u]]].append(dv[i, q])
-                in_vars[did[t + 1, nbr[i, w]]].append(dv[i, q])
-    rows = []
-    for d in range(nd):
-        # incoming: sum in + a_d - x_d = 0 ; outgoing: sum out + e_d - x_d = 0
-        rows.append((in_vars[d] + [a0 + d, x0 + d], [1] * len(in_vars[d]) + [1, -1], EQ, 0))
-        rows.append((out_vars[d] + [e0 + d, x0 + d], [1] * len(out_vars[d]) + [1, -1], EQ, 0))
+        src = np.repeat(did[t], n_trans)
+        out_det.append(src); out_var.append(tv.ravel())
+        in_det.append(did[t + 1][nbr].ravel()); in_var.append(tv.ravel())
+        out_det.append(np.repeat(did[t], len(pairs))); out_var.append(dv.ravel())
+        for q, (u, w) in enumerate(pairs):
+            in_det.append(did[t + 1][nbr[:, u]]); in_var.append(dv[:, q])
+            in_det.append(did[t + 1][nbr[:, w]]); in_var.append(dv[:, q])
+    cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)
+    rb = RowBuilder()
+    xd = np.arange(nd)
+    _grouped_rows(rb, cat(in_det), cat(in_var), np.stack([a0 + xd, x0 + xd], 1), np.array([1, -1]), EQ, 0)
+    _grouped_rows(rb, cat(out_det), cat(out_var), np.stack([e0 + xd, x0 + xd], 1), np.array([1, -1]), EQ, 0)
+    ex = []
     for t in range(T):
         pr = rng.choice(Dn, size=(excl_pairs, 2))
         pr = pr[pr[:, 0] != pr[:, 1]]
-        for u, w in pr:
-            rows.append(([did[t, u], did[t, w]], [1, 1], LE, 1))
-    cost = np.concatenate(cost)
-    return from_rows(nv, cost, rows, f"celltrack(seed={seed},{frames}x{dets})")
+        ex.append(did[t][pr])
+    ex = np.concatenate(ex)
+    rb.add(ex, np.ones(ex.shape), LE, 1)
+    return rb.build(nv, np.concatenate(cost), f"celltrack(seed={seed},{frames}x{dets})")
 
 
 def thin_hop(seed=0, k=10_000) -> Problem:
