@@ -725,37 +725,41 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
 }
 
 template <typename T>
+__device__ __forceinline__ void ell_store(T *out, int2 p, T x, T y) {
+  if (p.x < 0) return;
+  if (p.y >= 0) {
+    const T v = (x + y) / T(2);
+    out[p.x] = v;
+    out[p.y] = v;
+  } else {
+    out[p.x] = x;  // |J_i| = 1: the average is the value itself
+  }
+}
+
+template <typename T>
 __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (tid == 0) *a.tile_counter = 0u;
-  const int n_ell_thr = (((a.n_ell + 1) >> 1) + 31) & ~31;  // whole warps
+  // ELL part: four variables per thread (tid, tid + N, tid + 2N, tid + 3N, so
+  // every load of a warp stays coalesced), all eight gathers issued before use
+  const int n_ell_thr = (((a.n_ell + 3) >> 2) + 31) & ~31;  // whole warps
   if (tid < n_ell_thr) {
-    if (2 * tid >= a.n_ell) return;
-    const int q = 2 * tid;
-    const int2 p0 = __ldg(a.ell + q);
-    const int2 p1 = q + 1 < a.n_ell ? __ldg(a.ell + q + 1) : make_int2(-1, -1);
-    const T x0 = __ldg(db + p0.x);
-    const T y0 = p0.y >= 0 ? __ldg(db + p0.y) : T(0);
-    const T x1 = p1.x >= 0 ? __ldg(db + p1.x) : T(0);
-    const T y1 = p1.y >= 0 ? __ldg(db + p1.y) : T(0);
-    if (p0.y >= 0) {
-      const T v = (x0 + y0) / T(2);
-      out[p0.x] = v;
-      out[p0.y] = v;
-    } else {
-      out[p0.x] = x0;  // |J_i| = 1: the average is the value itself
+    int2 p[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = tid + u * n_ell_thr;
+      p[u] = q < a.n_ell ? __ldg(a.ell + q) : make_int2(-1, -1);
     }
-    if (p1.x >= 0) {
-      if (p1.y >= 0) {
-        const T v = (x1 + y1) / T(2);
-        out[p1.x] = v;
-        out[p1.y] = v;
-      } else {
-        out[p1.x] = x1;
-      }
+    T x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[u] = p[u].x >= 0 ? __ldg(db + p[u].x) : T(0);
+      y[u] = p[u].y >= 0 ? __ldg(db + p[u].y) : T(0);
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ell_store(out, p[u], x[u], y[u]);
     return;
   }
   // CSR part: a group of G lanes per variable; lane j sums slots j, j+G, ...
@@ -863,7 +867,7 @@ static int grid_for(int64_t n, int block) {
 
 int launch_avg(int precision, const AvgArgs &a, void *stream) {
   const int block = 256;
-  const int64_t threads = (int64_t)((((a.n_ell + 1) / 2) + 31) & ~31) + (int64_t)a.n * a.group;
+  const int64_t threads = (int64_t)((((a.n_ell + 3) / 4) + 31) & ~31) + (int64_t)a.n * a.group;
   const int grid = (int)std::max<int64_t>(1, (threads + block - 1) / block);
   if (precision == 64)
     avg_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(a);
