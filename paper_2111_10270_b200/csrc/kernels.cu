@@ -52,6 +52,11 @@ __device__ __forceinline__ T mm_difference(T m1, T m0, T clamp) {
   return sub_rn(m1, m0);
 }
 
+// ---- Programmatic dependent launch: a kernel launched with the PDL attribute
+// may start while its predecessor drains; it waits here before reading the
+// predecessor's outputs (or touching the tile counter it resets).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -63,6 +68,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // by fdog_lower_bound.
 __global__ void __launch_bounds__(1024) lb_reduce_kernel(const double *__restrict__ lb_part, int n, double *out) {
   __shared__ double red[32];
+  pdl_wait();
   const int chunk = (n + blockDim.x - 1) / blockDim.x;
   const int q0 = threadIdx.x * chunk, q1 = min(n, q0 + chunk);
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -468,6 +474,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   // by decreasing cost); later tiles are claimed from a global counter (reset
   // before every sweep), one claim in flight two tiles ahead of its use
   const int W = gridDim.x * wpb;
+  pdl_wait();
   auto claim_issue = [&]() -> int { return lane == 0 ? (int)atomicAdd(a.tile_counter, 1u) : 0; };
   auto claim_get = [&](int raw) -> int { return 2 * W + __shfl_sync(0xffffffffu, raw, 0); };
   // pipeline per warp: the claim for the tile after next is in flight, the
@@ -626,6 +633,7 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
   const int L = d.lanes, K = d.K;
   const bool valid = lane < d.n_lanes;
   double acc = 0.0;
+  pdl_wait();
   if (lane < L) {
     const int32_t *ho = a.hop_off + d.hop_base;
     const int ts = (d.kind & 1) ? L : 1;
@@ -741,6 +749,7 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
   if (tid == 0) *a.tile_counter = 0u;
   // ELL part: four variables per thread (tid, tid + N, tid + 2N, tid + 3N, so
   // every load of a warp stays coalesced), all eight gathers issued before use
@@ -838,6 +847,21 @@ int sweep_occupancy(int precision, int mode, bool rec, int block, size_t smem, i
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
 }
 
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute
+static int launch_pdl(const void *f, dim3 grid, dim3 block, size_t smem, void *stream, void **args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelExC(&cfg, f, args);
+}
+
 template <typename T>
 static const void *stream_fn(int mode, bool rec) {
   if (mode == kForward) return rec ? (const void *)sweep_stream_kernel<T, kForward, true> : (const void *)sweep_stream_kernel<T, kForward, false>;
@@ -848,14 +872,14 @@ int launch_sweep_stream(int precision, int mode, bool rec, const SweepArgs &a, v
   const void *f = precision == 64 ? stream_fn<double>(mode, rec) : stream_fn<float>(mode, rec);
   void *args[] = {(void *)&a};
   const int grid = (a.n_tiles + 3) / 4;
-  return (int)cudaLaunchKernel(f, dim3(grid > 0 ? grid : 1), dim3(128), args, 0, (cudaStream_t)stream);
+  return launch_pdl(f, dim3(grid > 0 ? grid : 1), dim3(128), 0, stream, args);
 }
 
 int launch_sweep(int precision, int mode, bool rec, const SweepArgs &a, int grid, int block, size_t smem,
                  void *stream) {
   const void *f = sweep_ptr(precision, mode, rec);
   void *args[] = {(void *)&a};
-  return (int)cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, (cudaStream_t)stream);
+  return launch_pdl(f, dim3(grid), dim3(block), smem, stream, args);
 }
 
 static int grid_for(int64_t n, int block) {
@@ -869,11 +893,9 @@ int launch_avg(int precision, const AvgArgs &a, void *stream) {
   const int block = 256;
   const int64_t threads = (int64_t)((((a.n_ell + 3) / 4) + 31) & ~31) + (int64_t)a.n * a.group;
   const int grid = (int)std::max<int64_t>(1, (threads + block - 1) / block);
-  if (precision == 64)
-    avg_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(a);
-  else
-    avg_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(a);
-  return (int)cudaGetLastError();
+  void *args[] = {(void *)&a};
+  const void *f = precision == 64 ? (const void *)avg_kernel<double> : (const void *)avg_kernel<float>;
+  return launch_pdl(f, dim3(grid), dim3(block), 0, stream, args);
 }
 
 int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,
@@ -898,8 +920,8 @@ int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, voi
 }
 
 int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream) {
-  lb_reduce_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(lb_part, n, out);
-  return (int)cudaGetLastError();
+  void *args[] = {(void *)&lb_part, (void *)&n, (void *)&out};
+  return launch_pdl((const void *)lb_reduce_kernel, dim3(1), dim3(1024), 0, stream, args);
 }
 
 int launch_fill(int precision, int64_t n, void *dst, double value, void *stream) {
