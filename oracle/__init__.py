@@ -19,7 +19,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
-_ERRORS = {1: "invalid argument", 2: "infeasible constraint", 3: "out of memory", 6: "bad state"}
+_ERRORS = {1: "invalid argument", 2: "infeasible constraint", 3: "out of memory", 6: "bad state",
+           7: "no consensus within max_rounds"}
 
 
 class OracleError(RuntimeError):
@@ -68,6 +69,9 @@ def _load():
         lib.oracle_bdd_get.argtypes = [P, C.c_int32, P, P, P, P]
         lib.oracle_total_nodes.argtypes = [P, P]
         lib.oracle_num_threads.argtypes = [P]
+        lib.oracle_primal_step.argtypes = [P, C.c_int32, C.c_double, C.c_uint64, P, P]
+        lib.oracle_round_primal.argtypes = [P, C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_uint64,
+                                            C.c_double, P, P]
         _lib = lib
     return _lib
 
@@ -105,6 +109,7 @@ class Oracle:
         self._h = h
         self._lib = lib
         self.n_cons = int(problem.n_cons)
+        self.n_vars = int(problem.n_vars)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -183,6 +188,22 @@ class Oracle:
         self._chk(self._lib.oracle_bdd_get(self._h, int(j), _ptr(vars_), _ptr(hs), _ptr(lo), _ptr(hi)),
                   "bdd_get")
         return vars_[:k.value], hs, lo[:n.value], hi[:n.value]
+
+    def primal_step(self, round_: int, delta: float, seed: int = 0):
+        """One classification + perturbation step of Alg. 2; returns (conflicts, x)."""
+        x = np.zeros(max(self.n_vars, 1), np.uint8)
+        nc = C.c_int64()
+        self._chk(self._lib.oracle_primal_step(self._h, int(round_), float(delta), int(seed), C.byref(nc),
+                                               _ptr(x)), "primal_step")
+        return nc.value, x[:self.n_vars]
+
+    def round_primal(self, delta0=1.0, alpha=1.2, inner=5, max_rounds=100, seed=0, omega=0.5):
+        """Alg. 2; returns (x, rounds); raises OracleError(7) without consensus."""
+        x = np.zeros(max(self.n_vars, 1), np.uint8)
+        r = C.c_int32()
+        self._chk(self._lib.oracle_round_primal(self._h, float(delta0), float(alpha), int(inner), int(max_rounds),
+                                                int(seed), float(omega), _ptr(x), C.byref(r)), "round_primal")
+        return x[:self.n_vars], r.value
 
     def hop_widths(self, j: int):
         _, hs, _, _ = self.bdd(j)

@@ -658,3 +658,113 @@ int oracle_total_nodes(const oracle_solver *s, int64_t *out) {
 }
 
 int oracle_num_threads(const oracle_solver *s) { return s ? s->n_threads : 0; }
+
+/* ------------------------------------------------------------------ */
+/* Alg. "Perturbation Primal Rounding"                     */
+
+/* Counter-based uniform in [0, 1): splitmix64 of (seed, round, i).  Both sides
+ * (oracle and product) implement this same generator, so they draw the same r
+ * (Alg. 2 "Sample r uniformly from [-delta, delta]"). */
+static double primal_uniform(uint64_t seed, int64_t round, int64_t i) {
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + (uint64_t)round * 0xBF58476D1CE4E5B9ull +
+               (uint64_t)i * 0x94D049BB133111EBull + 1ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+/* sign of m1 - m0 with the clamp of A5 */
+static int mm_sign(double m1, double m0, double clamp) {
+  double d = mm_difference(m1, m0, clamp);
+  return (d > 0) - (d < 0);
+}
+
+/* One classification + perturbation step of Alg. 2 over the min-marginals
+ * recorded in the last pass.  Returns the number of undecided variables
+ * (subproblems not all strictly favouring one value -- the loop guard, P:204,
+ * read with P:193/P:197, reading R1); perturbs lambda only if that number is > 0.  x (length n_vars, may be NULL) receives the
+ * labeling read off the signs: 1 if m1 < m0 in every subproblem, else 0;
+ * free variables x_i = [c_i < 0]. */
+int oracle_primal_step(oracle_solver *s, int32_t round, double delta, uint64_t seed, int64_t *conflicts,
+                       uint8_t *x) {
+  if (!s || !conflicts) return O_EINVAL;
+  if (s->passes == 0) return O_ESTATE;
+  int64_t nc = 0;
+  for (int32_t i = 0; i < s->n_vars; ++i) {
+    int64_t a = s->var_ptr[i], b = s->var_ptr[i + 1];
+    if (a == b) {
+      if (x) x[i] = s->cost[i] < 0;
+      continue;
+    }
+    int pos = 1, neg = 1, zero = 1;
+    for (int64_t q = a; q < b; ++q) {
+      int sg = mm_sign(s->m1[s->var_slots[q]], s->m0[s->var_slots[q]], s->clamp);
+      pos &= sg > 0;
+      neg &= sg < 0;
+      zero &= sg == 0;
+    }
+    if (x) x[i] = (uint8_t)neg;
+    /* undecided unless every subproblem strictly favours the same value:
+     * P:193 "agree and favor a single variable", P:197 ties are perturbed
+     * (reading R1); the literal guard of P:204 would stop on ties */
+    (void)zero;
+    if (!(pos || neg)) nc++;
+  }
+  *conflicts = nc;
+  if (nc == 0) return O_OK;
+  for (int32_t i = 0; i < s->n_vars; ++i) {
+    int64_t a = s->var_ptr[i], b = s->var_ptr[i + 1];
+    if (a == b) continue;
+    int pos = 1, neg = 1, zero = 1;
+    double dsum = 0.0; /* d_i = sum_j (m1_ij - m0_ij), clamped (A5) */
+    for (int64_t q = a; q < b; ++q) {
+      int64_t sl = s->var_slots[q];
+      int sg = mm_sign(s->m1[sl], s->m0[sl], s->clamp);
+      pos &= sg > 0;
+      neg &= sg < 0;
+      zero &= sg == 0;
+      dsum += mm_difference(s->m1[sl], s->m0[sl], s->clamp);
+    }
+    double r = delta * (2.0 * primal_uniform(seed, round, i) - 1.0); /* r ~ U[-delta, delta] */
+    double step;
+    if (pos) step = delta;
+    else if (neg) step = -delta;
+    else if (zero) step = r * delta;
+    else step = (double)((dsum > 0) - (dsum < 0)) * fabs(r) * delta;
+    for (int64_t q = a; q < b; ++q) s->lambda[s->var_slots[q]] += step;
+  }
+  /* lambda changed: stored distances must be recomputed before the next pass */
+  s->ctt_ok = s->cfr_ok = 0;
+  return O_OK;
+}
+
+/* Alg. 2 driver: while some variable's min-marginals disagree in sign,
+ * perturb (delta, then delta *= alpha) and reoptimise with `inner`
+ * iterations of Alg. 1.  On success x holds the labeling, *rounds the
+ * number of perturbation rounds; returns 7 if max_rounds is exhausted. */
+int oracle_round_primal(oracle_solver *s, double delta0, double alpha, int32_t inner, int32_t max_rounds,
+                        uint64_t seed, double omega, uint8_t *x, int32_t *rounds) {
+  if (!s || !x || !rounds || !(delta0 > 0) || !(alpha >= 1) || inner < 1 || max_rounds < 0) return O_EINVAL;
+  if (s->passes == 0) {
+    int rc = oracle_iterate(s, inner, omega);
+    if (rc) return rc;
+  }
+  double delta = delta0;
+  for (int32_t round = 0;; ++round) {
+    int64_t nc = 0;
+    int rc = oracle_primal_step(s, round, delta, seed, &nc, x);
+    if (rc) return rc;
+    if (nc == 0) {
+      *rounds = round;
+      return O_OK;
+    }
+    if (round + 1 > max_rounds) {
+      *rounds = round;
+      return 7;
+    }
+    delta *= alpha;
+    rc = oracle_iterate(s, inner, omega);
+    if (rc) return rc;
+  }
+}

@@ -13,7 +13,7 @@
  * (A1..A16, same labels as SURVEY.md §8(c)).
  *
  * Error codes: 0 ok, 1 invalid argument, 2 infeasible constraint,
- *              3 out of memory, 6 bad state.
+ *              3 out of memory, 6 bad state, 7 rounding without consensus.
  */
 #ifndef FASTDOG_ORACLE_H
 #define FASTDOG_ORACLE_H
@@ -78,6 +78,18 @@ int oracle_bdd_size(const oracle_solver *s, int32_t j, int32_t *k, int32_t *n_no
 int oracle_bdd_get(const oracle_solver *s, int32_t j, int32_t *vars, int32_t *hop_start,
                    int32_t *lo, int32_t *hi);
 int oracle_total_nodes(const oracle_solver *s, int64_t *out);
+
+/* Alg. "Perturbation Primal Rounding", reading of DESIGN.md §3:
+ * signs of the min-marginals recorded in the last pass; r ~ U[-delta, delta]
+ * from the counter-based generator splitmix64(seed, round, i).
+ * oracle_primal_step: one classification (+ perturbation if any variable's
+ * subproblems disagree); *conflicts = number of such variables; x = labeling.
+ * oracle_round_primal: the full loop with `inner` Alg.-1 iterations per round;
+ * returns 7 when max_rounds perturbation rounds did not reach consensus. */
+int oracle_primal_step(oracle_solver *s, int32_t round, double delta, uint64_t seed, int64_t *conflicts,
+                       uint8_t *x);
+int oracle_round_primal(oracle_solver *s, double delta0, double alpha, int32_t inner, int32_t max_rounds,
+                        uint64_t seed, double omega, uint8_t *x, int32_t *rounds);
 int oracle_num_threads(const oracle_solver *s);
 
 #ifdef __cplusplus
