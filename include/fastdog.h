@@ -36,7 +36,8 @@ typedef enum {
   FDOG_ECUDA = 4,       /* CUDA runtime error (message in fdog_last_error)          */
   FDOG_ENCCL = 5,       /* NCCL error (multi-GPU)                                   */
   FDOG_ESTATE = 6,      /* call not valid in this state (e.g. min_marginals w/o record_mm) */
-  FDOG_ETOOBIG = 7      /* a BDD exceeds the kernels' on-chip limits                */
+  FDOG_ETOOBIG = 7,     /* a BDD exceeds the kernels' on-chip limits                */
+  FDOG_ENOSOLUTION = 8  /* primal rounding: no consensus within max_rounds           */
 } fdog_status;
 
 /* Binary program (BP) P:555-565 in the row form of Example ILP P:567-577.
@@ -185,6 +186,37 @@ fdog_status fdog_profile_reset(fdog_solver *s);
  * fdog_iterate launches kernels one by one; with events off (and world == 1)
  * it replays a CUDA graph of one iteration. */
 fdog_status fdog_profile_enable(fdog_solver *s, int32_t on);
+
+/* ---- primal rounding: Alg. "Perturbation Primal Rounding" --
+ * Signs of m1 - m0 are read from the min-marginals of the last pass
+ * (delta_bar = omega * clamp(m1 - m0)).  The loop runs while some variable is
+ * undecided -- its subproblems do not all strictly favour one value (reading
+ * R1) -- perturbing lambda per variable by +delta / -delta /
+ * r*delta / sign(d_i)|r|delta, r ~ U[-delta, delta] from the
+ * counter-based generator splitmix64(seed, round, i), delta *= alpha,
+ * then `inner` iterations of Alg. 1.  Defaults delta0 = 1.0,
+ * alpha = 1.2, inner = 5, max_rounds = 100, omega = 0.5.  world == 1. */
+typedef struct {
+  double delta0;
+  double alpha;
+  int32_t inner;
+  int32_t max_rounds;
+  uint64_t seed;
+  double omega;
+  int32_t keep_state;  /* 0: restore the dual state (lambda, delta_bar, bound) afterwards */
+} fdog_primal_options;
+void fdog_default_primal_options(fdog_primal_options *opts);
+/* One classification (+ perturbation when *undecided > 0) step.  x: length
+ * n_vars host array receiving x_i = 1 iff m1 < m0 in every subproblem
+ * (free variables: x_i = [c_i < 0]). */
+fdog_status fdog_primal_step(fdog_solver *s, int32_t round, double delta, uint64_t seed, int64_t *undecided,
+                             uint8_t *x, int64_t len);
+/* The full rounding loop.  On success x is a labeling that satisfies every
+ * constraint (checked on the host), *objective = <c, x>, *rounds = the number
+ * of perturbation rounds.  FDOG_ENOSOLUTION: no consensus within max_rounds
+ * (x holds the last labeling). */
+fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, uint8_t *x, int64_t len,
+                              int32_t *rounds, double *objective);
 
 const char *fdog_last_error(void);
 int32_t fdog_version(void);

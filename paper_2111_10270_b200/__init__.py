@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfastdog.so")
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EINFEASIBLE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE",
-          7: "ETOOBIG"}
+          7: "ETOOBIG", 8: "ENOSOLUTION"}
 
 
 class FastdogError(RuntimeError):
@@ -52,6 +52,11 @@ class Stats(C.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class PrimalOptions(C.Structure):
+    _fields_ = [("delta0", C.c_double), ("alpha", C.c_double), ("inner", C.c_int32), ("max_rounds", C.c_int32),
+                ("seed", C.c_uint64), ("omega", C.c_double), ("keep_state", C.c_int32)]
+
+
 class KernelTime(C.Structure):
     _fields_ = [("name", C.c_char_p), ("ms", C.c_double), ("launches", C.c_int64),
                 ("bytes_per_launch", C.c_double)]
@@ -63,7 +68,8 @@ EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdo
            "fdog_finalize", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
            "fdog_get_deferred", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
            "fdog_profile", "fdog_profile_reset", "fdog_profile_enable", "fdog_pass_begin", "fdog_pass_end",
-           "fdog_exchange_size", "fdog_exchange_read", "fdog_exchange_write", "fdog_last_error", "fdog_version"]
+           "fdog_exchange_size", "fdog_exchange_read", "fdog_exchange_write", "fdog_default_primal_options",
+           "fdog_primal_step", "fdog_round_primal", "fdog_last_error", "fdog_version"]
 
 _lib = None
 
@@ -109,6 +115,9 @@ def load():
         "fdog_exchange_size": ([P, P], C.c_int),
         "fdog_exchange_read": ([P, P, i64], C.c_int),
         "fdog_exchange_write": ([P, P, i64], C.c_int),
+        "fdog_default_primal_options": ([P], None),
+        "fdog_primal_step": ([P, i32, dbl, C.c_uint64, P, P, i64], C.c_int),
+        "fdog_round_primal": ([P, P, P, i64, P, P], C.c_int),
         "fdog_last_error": ([], C.c_char_p),
         "fdog_version": ([], C.c_int32),
     }
@@ -239,6 +248,7 @@ class Solver:
             _check(lib.fdog_create(C.byref(pa.struct), C.byref(self._opts), C.byref(h)), "fdog_create")
         self._h = h
         self.precision = precision
+        self.n_vars = int(plan._pa.struct.n_vars) if plan is not None else int(problem.n_vars)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -330,6 +340,29 @@ class Solver:
     def exchange_write(self, x):
         a = np.ascontiguousarray(x, dtype=np.float64)
         _check(self._lib.fdog_exchange_write(self._h, _ptr(a), a.size), "fdog_exchange_write")
+
+    def primal_step(self, round_: int, delta: float, seed: int = 0):
+        """One classification (+ perturbation) step of Alg. 2: (undecided, x)."""
+        n = self.n_vars
+        x = np.zeros(max(n, 1), np.uint8)
+        u = C.c_int64()
+        _check(self._lib.fdog_primal_step(self._h, int(round_), float(delta), int(seed), C.byref(u), _ptr(x), n),
+               "fdog_primal_step")
+        return u.value, x[:n]
+
+    def round_primal(self, delta0=1.0, alpha=1.2, inner=5, max_rounds=100, seed=0, omega=0.5, keep_state=False):
+        """Alg. 2: returns (x, rounds, objective); FastdogError(8) without consensus."""
+        o = PrimalOptions()
+        self._lib.fdog_default_primal_options(C.byref(o))
+        o.delta0, o.alpha, o.inner, o.max_rounds = float(delta0), float(alpha), int(inner), int(max_rounds)
+        o.seed, o.omega, o.keep_state = int(seed), float(omega), int(bool(keep_state))
+        n = self.n_vars
+        x = np.zeros(max(n, 1), np.uint8)
+        r = C.c_int32()
+        obj = C.c_double()
+        _check(self._lib.fdog_round_primal(self._h, C.byref(o), _ptr(x), n, C.byref(r), C.byref(obj)),
+               "fdog_round_primal")
+        return x[:n], r.value, obj.value
 
     def profile_enable(self, on: bool):
         _check(self._lib.fdog_profile_enable(self._h, 1 if on else 0), "fdog_profile_enable")

@@ -112,6 +112,10 @@ struct Plan {
   std::vector<int32_t> shared_vars; // ascending global ids exchanged with other ranks
   std::vector<int32_t> deg_list;    // |J_i| (global) per var_list entry
   std::vector<int32_t> ell;         // ELL part: slot pairs (second -1 if |J_i| = 1)
+  std::vector<int32_t> ell_var;     // ELL part: the variables
+  std::vector<int32_t> col_coef;    // copy of the rows (feasibility checks of primal labelings)
+  std::vector<int8_t> rel;
+  std::vector<int64_t> rhs;
   int64_t n_vars_local = 0;         // variables with local slots (ELL + CSR)
   std::vector<int32_t> x_local;     // per shared var: index into var_list or -1
   std::vector<int32_t> x_deg;       // per shared var: |J_i| (global)
@@ -169,6 +173,23 @@ struct AvgArgs {
   unsigned int *tile_counter;  // sweep scheduler counter, reset here for the next sweep
 };
 
+struct PrimalArgs {
+  int32_t n_ell, n_csr;
+  const int2 *ell;
+  const int32_t *ell_var;     // variable of each ELL entry
+  const int32_t *csr_var;     // variable of each CSR entry
+  const int64_t *var_ptr;
+  const int32_t *var_slots;
+  const void *delta_bar;      // T*
+  void *lambda;               // T*
+  uint8_t *x;                 // per variable
+  unsigned long long *undecided;
+  int32_t mode;               // 0 classify, 1 perturb
+  int32_t round;
+  double delta;
+  uint64_t seed;
+};
+
 // returns the cudaError_t as int
 int launch_sweep(int precision, int mode, bool record, const SweepArgs &a, int grid, int block,
                  size_t smem, void *stream);
@@ -179,6 +200,7 @@ int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const i
                       void *stream);
 int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, void *stream);
 int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream);
+int launch_primal(int precision, const PrimalArgs &a, void *stream);
 int launch_fill(int precision, int64_t n, void *dst, double value, void *stream);
 
 }  // namespace fdog

@@ -799,6 +799,70 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
 }
 
 // Shared variables after the NCCL exchange: average and scatter into the local slots.
+// ---------------------------------------------------------------------------
+// Alg. "Perturbation Primal Rounding", one kernel per step.
+// Thread per variable (ELL part: slot pair inline; CSR part: slot list).  The
+// signs of m1 - m0 are those of delta_bar = omega * clamp(m1 - m0) of the last
+// pass.  mode 0: classify -> x (1 iff m1 < m0 in every subproblem) and the
+// count of undecided variables (reading R1); mode 1: perturbation of lambda.
+__device__ __forceinline__ double primal_uniform(uint64_t seed, int64_t round, int64_t i) {
+  // splitmix64(seed, round, i) -> [0, 1); the oracle implements the same generator
+  uint64_t z = seed * 0x9E3779B97F4A7C15ull + (uint64_t)round * 0xBF58476D1CE4E5B9ull +
+               (uint64_t)i * 0x94D049BB133111EBull + 1ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) primal_kernel(const PrimalArgs a) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= a.n_ell + a.n_csr) return;
+  const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
+  int i, s0 = -1, s1 = -1;
+  int64_t p0 = 0, p1 = 0;
+  if (q < a.n_ell) {
+    const int2 pr = a.ell[q];
+    i = a.ell_var[q];
+    s0 = pr.x;
+    s1 = pr.y;
+  } else {
+    const int c = q - a.n_ell;
+    i = a.csr_var[c];
+    p0 = a.var_ptr[c];
+    p1 = a.var_ptr[c + 1];
+  }
+  auto slot_at = [&](int64_t u) -> int { return q < a.n_ell ? (u == 0 ? s0 : s1) : a.var_slots[p0 + u]; };
+  const int64_t deg = q < a.n_ell ? (s1 >= 0 ? 2 : 1) : p1 - p0;
+  bool pos = true, neg = true, zero = true;
+  double dsum = 0.0;  // sign of d_i = sum_j (m1 - m0) = sign of sum_j delta_bar (omega > 0)
+  for (int64_t u = 0; u < deg; ++u) {
+    const T v = db[slot_at(u)];
+    pos = pos && v > T(0);
+    neg = neg && v < T(0);
+    zero = zero && v == T(0);
+    dsum += (double)v;
+  }
+  if (a.mode == 0) {
+    a.x[i] = neg ? 1 : 0;
+    if (!(pos || neg)) atomicAdd(a.undecided, 1ull);
+    return;
+  }
+  const double delta = a.delta;
+  const double r = delta * (2.0 * primal_uniform(a.seed, a.round, i) - 1.0);  // r ~ U[-delta, delta]
+  double step;
+  if (pos) step = delta;
+  else if (neg) step = -delta;
+  else if (zero) step = r * delta;
+  else step = (double)((dsum > 0) - (dsum < 0)) * fabs(r) * delta;
+  T *__restrict__ lam = reinterpret_cast<T *>(a.lambda);
+  for (int64_t u = 0; u < deg; ++u) {
+    const int s = slot_at(u);
+    lam[s] = (T)((double)lam[s] + step);
+  }
+}
+
 template <typename T>
 __global__ void avg_finish_kernel(const AvgArgs a, int32_t n_shared, const int32_t *__restrict__ xlocal,
                                   const int32_t *__restrict__ deg_x) {
@@ -916,6 +980,17 @@ int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, voi
     add_deferred_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, (double *)lambda, (double *)delta);
   else
     add_deferred_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, (float *)lambda, (float *)delta);
+  return (int)cudaGetLastError();
+}
+
+int launch_primal(int precision, const PrimalArgs &a, void *stream) {
+  const int n = a.n_ell + a.n_csr;
+  if (n <= 0) return 0;
+  const int block = 256, grid = (n + block - 1) / block;
+  if (precision == 64)
+    primal_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(a);
+  else
+    primal_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(a);
   return (int)cudaGetLastError();
 }
 

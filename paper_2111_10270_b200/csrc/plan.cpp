@@ -250,6 +250,9 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   if (p->n_cons == 0) P.row_ptr.assign(1, 0);
   const int64_t nnz = P.row_ptr.back();
   P.col_var.assign(p->col_var, p->col_var + nnz);
+  P.col_coef.assign(p->col_coef, p->col_coef + nnz);
+  P.rel.assign(p->rel, p->rel + p->n_cons);
+  P.rhs.assign(p->rhs, p->rhs + p->n_cons);
 
   // rows with no variable: feasible (dropped) or infeasible (error)
   for (int32_t j = 0; j < p->n_cons; ++j)
@@ -672,11 +675,13 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     std::vector<int32_t> csr_list, csr_slots, csr_x;
     std::vector<int64_t> csr_ptr(1, 0);
     P.ell.clear();
+    P.ell_var.clear();
     for (size_t q = 0; q < P.var_list.size(); ++q) {
       const int64_t a = P.var_ptr[q], b = P.var_ptr[q + 1];
       if (b - a <= 2 && P.var_xidx[q] < 0) {
         P.ell.push_back(P.var_slots[a]);
         P.ell.push_back(b - a == 2 ? P.var_slots[a + 1] : -1);
+        P.ell_var.push_back(P.var_list[q]);
       } else {
         csr_list.push_back(P.var_list[q]);
         csr_x.push_back(P.var_xidx[q]);

@@ -44,9 +44,9 @@ struct Nccl {
   nccl_comm comm = nullptr;
 };
 
-enum KernelId { kKSweepFwd = 0, kKSweepBwd, kKEnergy, kKAvg, kKAvgFinish, kKAllreduce, kKAddDeferred, kKFill, kKLbReduce, kKCount };
+enum KernelId { kKSweepFwd = 0, kKSweepBwd, kKEnergy, kKAvg, kKAvgFinish, kKAllreduce, kKAddDeferred, kKFill, kKLbReduce, kKPrimal, kKCount };
 const char *kKernelNames[kKCount] = {"sweep_forward", "sweep_backward", "sweep_energy", "avg", "avg_finish",
-                                     "nccl_allreduce", "add_deferred", "fill", "lb_reduce"};
+                                     "nccl_allreduce", "add_deferred", "fill", "lb_reduce", "primal"};
 
 struct EventRec {
   int kernel;
@@ -89,6 +89,17 @@ struct fdog_solver {
   int32_t *d_var_slots = nullptr, *d_var_xidx = nullptr, *d_deg_list = nullptr;
   int2 *d_ell = nullptr;
   int32_t n_ell = 0, csr_group = 1;
+  // primal rounding
+  int32_t *d_ell_var = nullptr, *d_csr_var = nullptr;
+  uint8_t *d_x = nullptr;
+  unsigned long long *d_undecided = nullptr;
+  std::vector<int64_t> h_row_ptr;
+  std::vector<int32_t> h_col_var, h_col_coef;
+  std::vector<int8_t> h_rel;
+  std::vector<int64_t> h_rhs;
+  std::vector<double> h_cost;
+  std::vector<int32_t> h_deg;
+  int64_t n_dist = 0;
   bool lb_dirty = false;  // per-tile partials not reduced yet
   int64_t *d_var_ptr = nullptr;
   double *d_lb_part = nullptr, *d_lb = nullptr;
@@ -506,6 +517,18 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   if ((st = upload(s, &s->d_var_slots, P.var_slots))) return st;
   if ((st = upload(s, &s->d_var_xidx, P.var_xidx))) return st;
   if ((st = upload(s, &s->d_deg_list, P.deg_list))) return st;
+  if ((st = upload(s, &s->d_ell_var, P.ell_var))) return st;
+  if ((st = upload(s, &s->d_csr_var, P.var_list))) return st;
+  if ((st = alloc(s, (void **)&s->d_x, (size_t)std::max<int64_t>(P.n_vars, 1)))) return st;
+  if ((st = alloc(s, (void **)&s->d_undecided, sizeof(unsigned long long)))) return st;
+  s->h_row_ptr = P.row_ptr;
+  s->h_col_var = P.col_var;
+  s->h_col_coef = P.col_coef;
+  s->h_rel = P.rel;
+  s->h_rhs = P.rhs;
+  s->h_cost = P.cost;
+  s->h_deg = P.deg_global;
+  s->n_dist = P.n_dist;
   {
     std::vector<int2> ell(P.ell.size() / 2);
     for (size_t q = 0; q < ell.size(); ++q) ell[q] = make_int2(P.ell[2 * q], P.ell[2 * q + 1]);
@@ -624,7 +647,194 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
 
 }  // namespace
 
+namespace {
+
+PrimalArgs primal_args(fdog_solver *s, int mode, int32_t round, double delta, uint64_t seed) {
+  PrimalArgs a{};
+  a.n_ell = s->n_ell;
+  a.n_csr = s->n_varlist;
+  a.ell = s->d_ell;
+  a.ell_var = s->d_ell_var;
+  a.csr_var = s->d_csr_var;
+  a.var_ptr = s->d_var_ptr;
+  a.var_slots = s->d_var_slots;
+  a.delta_bar = s->d_delta[s->cur];
+  a.lambda = s->d_lambda;
+  a.x = s->d_x;
+  a.undecided = s->d_undecided;
+  a.mode = mode;
+  a.round = round;
+  a.delta = delta;
+  a.seed = seed;
+  return a;
+}
+
+fdog_status primal_step_impl(fdog_solver *s, int32_t round, double delta, uint64_t seed, int64_t *undecided,
+                             uint8_t *x) {
+  CK(cudaMemsetAsync(s->d_undecided, 0, sizeof(unsigned long long), s->stream), "memset");
+  int e;
+  {
+    Timed t(s, kKPrimal);
+    e = launch_primal(s->precision, primal_args(s, 0, round, delta, seed), s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "primal classify");
+  unsigned long long u = 0;
+  CK(cudaMemcpyAsync(&u, s->d_undecided, sizeof u, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  if (x && s->n_vars > 0) CK(cudaMemcpyAsync(x, s->d_x, (size_t)s->n_vars, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  if (x)
+    for (int64_t i = 0; i < s->n_vars; ++i)
+      if (s->h_deg[i] == 0) x[i] = s->h_cost[i] < 0;  // free variables (A13)
+  *undecided = (int64_t)u;
+  if (u == 0) return FDOG_OK;
+  {
+    Timed t(s, kKPrimal);
+    e = launch_primal(s->precision, primal_args(s, 1, round, delta, seed), s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "primal perturb");
+  s->dist_state = 2;  // lambda changed: distances are recomputed before the next pass
+  return FDOG_OK;
+}
+
+bool labeling_feasible(const fdog_solver *s, const uint8_t *x, int64_t *bad_row) {
+  const int64_t m = (int64_t)s->h_rel.size();
+  for (int64_t j = 0; j < m; ++j) {
+    int64_t acc = 0;
+    for (int64_t q = s->h_row_ptr[j]; q < s->h_row_ptr[j + 1]; ++q) acc += (int64_t)s->h_col_coef[q] * x[s->h_col_var[q]];
+    const int8_t r = s->h_rel[j];
+    const bool ok = r < 0 ? acc <= s->h_rhs[j] : r > 0 ? acc >= s->h_rhs[j] : acc == s->h_rhs[j];
+    if (!ok) {
+      *bad_row = j;
+      return false;
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
 extern "C" {
+
+void fdog_default_primal_options(fdog_primal_options *o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof *o);
+  o->delta0 = 1.0;
+  o->alpha = 1.2;
+  o->inner = 5;
+  o->max_rounds = 100;
+  o->omega = 0.5;
+}
+
+fdog_status fdog_primal_step(fdog_solver *s, int32_t round, double delta, uint64_t seed, int64_t *undecided,
+                             uint8_t *x, int64_t len) {
+  if (!s || !undecided || (x && len < s->n_vars)) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  if (s->world > 1) {
+    set_error("primal rounding is single-GPU in this version");
+    return FDOG_ESTATE;
+  }
+  if (s->passes == 0) {
+    set_error("primal rounding needs the min-marginals of at least one pass");
+    return FDOG_ESTATE;
+  }
+  return primal_step_impl(s, round, delta, seed, undecided, x);
+}
+
+fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, uint8_t *x, int64_t len,
+                              int32_t *rounds, double *objective) {
+  if (!s || !x || !rounds || !objective || len < s->n_vars) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  fdog_primal_options def;
+  fdog_default_primal_options(&def);
+  const fdog_primal_options *o = opts ? opts : &def;
+  if (!(o->delta0 > 0) || !(o->alpha >= 1) || o->inner < 1 || o->max_rounds < 0 || !(o->omega > 0 && o->omega <= 1)) {
+    set_error("invalid primal options");
+    return FDOG_EINVAL;
+  }
+  if (s->world > 1) {
+    set_error("primal rounding is single-GPU in this version");
+    return FDOG_ESTATE;
+  }
+  fdog_status st;
+  // snapshot of the dual state (restored unless keep_state)
+  const size_t sb = (size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz;
+  const size_t db = (size_t)std::max<int64_t>(s->n_dist, 1) * s->tsz;
+  std::vector<void *> snap;
+  auto cleanup = [&]() {
+    for (void *p : snap) cudaFree(p);
+  };
+  const int cur0 = s->cur, ds0 = s->dist_state;
+  const int64_t passes0 = s->passes;
+  const bool dirty0 = s->lb_dirty;
+  const size_t pb = (size_t)std::max(s->n_tiles, 1) * sizeof(double), lbb = 2 * sizeof(double);
+  if (!o->keep_state) {
+    void *p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    const size_t sz[6] = {sb, sb, sb, db, pb, lbb};
+    void *src[6] = {s->d_lambda, s->d_delta[0], s->d_delta[1], s->d_dist, s->d_lb_part, s->d_lb};
+    for (int q = 0; q < 6; ++q) {
+      cudaError_t e = cudaMalloc(&p[q], sz[q]);
+      if (e != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e, "cudaMalloc (primal snapshot)");
+      }
+      snap.push_back(p[q]);
+      e = cudaMemcpyAsync(p[q], src[q], sz[q], cudaMemcpyDeviceToDevice, s->stream);
+      if (e != cudaSuccess) {
+        cleanup();
+        return cuda_fail(e, "snapshot");
+      }
+    }
+  }
+  auto restore = [&]() -> fdog_status {
+    if (o->keep_state) return FDOG_OK;
+    void *dst[6] = {s->d_lambda, s->d_delta[0], s->d_delta[1], s->d_dist, s->d_lb_part, s->d_lb};
+    const size_t sz[6] = {sb, sb, sb, db, pb, lbb};
+    for (int q = 0; q < 6; ++q) CK(cudaMemcpyAsync(dst[q], snap[q], sz[q], cudaMemcpyDeviceToDevice, s->stream), "restore");
+    CK(cudaStreamSynchronize(s->stream), "sync");
+    s->cur = cur0;
+    s->dist_state = ds0;
+    s->passes = passes0;
+    s->lb_dirty = dirty0;
+    return FDOG_OK;
+  };
+  if (s->passes == 0 && (st = fdog_iterate(s, o->inner, o->omega))) {
+    restore();
+    cleanup();
+    return st;
+  }
+  double delta = o->delta0;
+  int32_t round = 0;
+  for (;; ++round) {
+    int64_t und = 0;
+    if ((st = primal_step_impl(s, round, delta, o->seed, &und, x))) break;
+    if (und == 0) break;
+    if (round + 1 > o->max_rounds) {
+      set_error("primal rounding: %lld undecided variables after %d rounds", (long long)und, round);
+      st = FDOG_ENOSOLUTION;
+      break;
+    }
+    delta *= o->alpha;
+    if ((st = fdog_iterate(s, o->inner, o->omega))) break;
+  }
+  *rounds = round;
+  double obj = 0.0;
+  for (int64_t i = 0; i < s->n_vars; ++i) obj += x[i] ? s->h_cost[i] : 0.0;
+  *objective = obj;
+  fdog_status rs = restore();
+  cleanup();
+  if (st) return st;
+  if (rs) return rs;
+  int64_t bad = -1;
+  if (!labeling_feasible(s, x, &bad)) {
+    set_error("internal: labeling with all variables decided violates row %lld", (long long)bad);
+    return FDOG_ESTATE;
+  }
+  return FDOG_OK;
+}
 
 fdog_status fdog_create_from_plan(const fdog_plan *plan, const fdog_options *opts, fdog_solver **out) {
   if (!plan || !out) {
