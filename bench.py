@@ -200,7 +200,7 @@ def run_gpu(args):
     torch.cuda.set_stream(stream)
     problem = _workload(args.workload)
     t0 = time.perf_counter()
-    plan = F.Plan(problem, rank=rank, world=world)
+    plan = F.Plan(problem, rank=rank, world=world, precision=64 if args.fp64 else 32)
     plan_s = time.perf_counter() - t0
     prec = 64 if args.fp64 else 32
     solver = F.Solver(plan=plan, precision=prec, device=local, profile=False, rank=rank, world=world,
@@ -306,6 +306,33 @@ def run_gpu(args):
                "includes": "device allocation + H2D upload of the packed plan, K x (iterate(1) + "
                            "lower_bound D2H), get_lambda D2H"}
 
+    # time-to-LB (BASELINE metric): target = fp64 bound after 1000
+    # iterations; fp32 solver from scratch, bound sampled every 10 iterations
+    # (the D2H read of the bound is inside the timed interval)
+    ttl = None
+    if not args.no_ttl and world == 1:
+        plan64 = F.Plan(problem, precision=64)
+        ref = F.Solver(plan=plan64, precision=64, device=local, stream=stream.cuda_stream)
+        lb0_64 = ref.lower_bound()
+        ref.iterate(1000, OMEGA)
+        target = ref.lower_bound()
+        ref.close()
+        thr = lb0_64 + 0.99 * (target - lb0_64)
+        s3 = F.Solver(plan=plan, precision=prec, device=local, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        its, cur_lb = 0, s3.lower_bound()
+        while cur_lb < thr and its < 1000:
+            s3.iterate(10, OMEGA)
+            its += 10
+            cur_lb = s3.lower_bound()
+        el = time.perf_counter() - t0
+        s3.close()
+        ttl = {"seconds": el, "iterations": its, "reached": bool(cur_lb >= thr), "lb0": lb0_64,
+               "target_lb_1000_fp64": target, "threshold": thr, "lb": cur_lb,
+               "definition": "wall time from the first iterate until LB >= LB0 + 0.99 (LB*_1000 - LB0), "
+                             "bound sampled every 10 iterations"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = _cpu_baseline(problem, 2 * 2 * st["nodes"], budget_s=args.cpu_budget)
@@ -337,6 +364,7 @@ def run_gpu(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,
+            "time_to_lb": ttl,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -354,6 +382,7 @@ def main():
     ap.add_argument("--fp64", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ttl", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3:

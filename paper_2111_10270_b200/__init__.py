@@ -179,10 +179,10 @@ def make_options(precision=32, device=0, clamp=0.0, record_mm=False, profile=Fal
 class Plan:
     """Host-side compiled + packed problem (no GPU needed)."""
 
-    def __init__(self, problem, rank=0, world=1, host_threads=0):
+    def __init__(self, problem, rank=0, world=1, host_threads=0, precision=32):
         lib = load()
         self._pa = _ProblemArrays(problem)
-        self._opts = make_options(rank=rank, world=world, host_threads=host_threads)
+        self._opts = make_options(precision=precision, rank=rank, world=world, host_threads=host_threads)
         h = C.c_void_p()
         _check(lib.fdog_plan_create(C.byref(self._pa.struct), C.byref(self._opts), C.byref(h)),
                "fdog_plan_create")
