@@ -154,6 +154,7 @@ struct SweepArgs {
   int32_t max_nodes, max_w, max_hops;  // over all tiles (direct-mode scratch)
   void *dist;               // T*, per-node distances (store design)
   int32_t SB, DB, NB;       // per-warp stage-buffer / relaxation budgets (bytes), stage buffers
+  int32_t static_sched;     // 1: round-robin tiles only (no dynamic claims)
   void *scratch;            // T*, [warps][scratch_stride] for direct tiles
   int64_t scratch_stride;   // elements per warp
 };

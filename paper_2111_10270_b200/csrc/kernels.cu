@@ -491,8 +491,8 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   int tn = gwarp + W < a.n_tiles ? gwarp + W : a.n_tiles;
   TileDesc dn;
   if (tn < a.n_tiles) dn = a.tiles[tn];
-  int raw_nn = (tn < a.n_tiles && 2 * W < a.n_tiles) ? claim_issue() : 0;
-  bool pending = tn < a.n_tiles && 2 * W < a.n_tiles;  // a claim is in flight
+  bool pending = !a.static_sched && tn < a.n_tiles && 2 * W < a.n_tiles;  // a claim is in flight
+  int raw_nn = pending ? claim_issue() : 0;
   while (t < a.n_tiles) {
     const bool has_next = tn < a.n_tiles;
     const int bn = a.NB > 1 ? (b ^ 1) : 0;
@@ -501,13 +501,15 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
       issue_stage<T, MODE>(a, dn, stage_at<T>(bn ? sbuf1 : sbuf0, dn), &bar[bn]);
     }
     int tnn = a.n_tiles;
-    if (pending) {
+    if (a.static_sched) {
+      tnn = tn + W < a.n_tiles ? tn + W : a.n_tiles;
+    } else if (pending) {
       tnn = claim_get(raw_nn);
       if (tnn > a.n_tiles) tnn = a.n_tiles;
     }
     TileDesc dnn;
     if (tnn < a.n_tiles) dnn = a.tiles[tnn];  // used one tile later
-    pending = tnn < a.n_tiles;
+    pending = !a.static_sched && tnn < a.n_tiles;
     raw_nn = pending ? claim_issue() : 0;
     const int L = d.lanes;
     const bool active = lane < L;

@@ -67,6 +67,7 @@ struct fdog_solver {
   int rank = 0, world = 1;
   bool external = false;  // world > 1 without NCCL: the caller performs the exchange
   bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
+  int32_t static_sched = 0;  // TMA sweep: round-robin tiles only
 
   // host copies needed by getters
   std::vector<int64_t> canon_slot;
@@ -225,6 +226,7 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   a.DB = s->DB;
   a.NB = s->NB;
   a.dist = s->d_dist;
+  a.static_sched = s->static_sched;
   a.scratch = s->d_scratch;
   a.scratch_stride = s->scratch_stride;
   const bool rec = s->record_mm && (mode == kForward || mode == kBackward);
@@ -506,6 +508,15 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
     }
   const int64_t want = ((int64_t)s->n_tiles + warps - 1) / warps;
   s->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)prop.multiProcessorCount * bps));
+  {
+    // few tiles per warp: a plain round-robin over the cost-sorted tiles
+    // (claims would sit on the critical path); many tiles per warp: dynamic
+    // claims balance the load
+    const char *sc = getenv("FDOG_SCHED");  // experiment knob: "static" or "dynamic"
+    const int64_t warps_total = (int64_t)s->grid * warps;
+    if (sc && (sc[0] == 's' || sc[0] == 'd')) s->static_sched = sc[0] == 's';
+    else s->static_sched = s->n_tiles <= 4 * warps_total;
+  }
   s->scratch_stride = (int64_t)relax_slots(s->max_w) * 32;
 
   fdog_status st;
