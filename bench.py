@@ -298,7 +298,7 @@ def run_gpu(args):
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        up = s2.stats()["device_bytes"]
+        up = s2.stats()["h2d_bytes"]
         s2.close()
         e2e = {"value": arcs_total * 2 * args.steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(up / args.steps),

@@ -90,6 +90,7 @@ typedef struct {
   int32_t sweep_grid, sweep_block; /* persistent sweep launch configuration           */
   int64_t sweep_smem_per_warp;     /* bytes of shared memory per warp                 */
   int32_t sweep_streaming;         /* 1: passes use the streaming sweep kernel        */
+  int64_t h2d_bytes;               /* host->device bytes copied by create             */
 } fdog_stats_t;
 
 typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */

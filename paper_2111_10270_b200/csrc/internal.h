@@ -85,6 +85,25 @@ FDOG_HD int relax_slots(int W) { return 3 * (W + 1); }
 FDOG_HD int relax_bytes(int tsz, int W, int L) { return r16(relax_slots(W) * L * tsz); }
 FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (16 + NB * SB + DB + 127) & ~127; }
 
+// One contiguous device image of everything a solver uploads (built by the
+// plan, untimed; pinned host memory when a CUDA device is present), so that
+// creating a solver is one allocation and one host->device copy.
+enum ImageSection {
+  kImTiles = 0, kImHopOff, kImTopo, kImSlotVar, kImVarPtr, kImVarSlots, kImVarXidx, kImDegList, kImEll, kImEllVar,
+  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImCount
+};
+
+struct HostImage {
+  unsigned char *data = nullptr;
+  size_t bytes = 0;
+  bool pinned = false;
+  size_t off[kImCount] = {0};
+  HostImage() = default;
+  HostImage(const HostImage &) = delete;
+  HostImage &operator=(const HostImage &) = delete;
+  ~HostImage();
+};
+
 struct Plan {
   int32_t n_vars = 0, n_cons = 0, rank = 0, world = 1;
   std::vector<double> cost;
@@ -125,6 +144,8 @@ struct Plan {
   int64_t n_dist = 0;               // elements of the distance array
   int64_t direct_tiles = 0;
 
+  HostImage image;                  // device image (see ImageSection)
+
   int64_t n_nodes = 0;              // real (unpadded) nodes on this rank
   int64_t n_slots = 0;              // real slots
   int64_t tiles_shared = 0;
@@ -134,6 +155,7 @@ struct Plan {
 // host-side helpers implemented in plan.cpp
 void set_error(const char *fmt, ...);
 fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &plan);
+fdog_status build_image(Plan &plan);
 
 // ---- device launchers (kernels.cu) -------------------------------------
 enum SweepMode { kForward = 0, kBackward = 1, kEnergy = 2, kCfr = 3 };

@@ -15,9 +15,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <unordered_map>
+
+#include <cuda_runtime.h>
 
 #include "internal.h"
 
@@ -705,6 +708,92 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   return FDOG_OK;
 }
 
+HostImage::~HostImage() {
+  if (!data) return;
+  if (pinned) cudaFreeHost(data);
+  else free(data);
+}
+
+// Lay out every uploaded array in one buffer (256-byte aligned sections),
+// including the initial lambda_i^j = c_i / |J_i| (A9; fp64, rounded once
+// to the build precision) and the distance array with its sentinels (0 for
+// top, +inf for bottom, never overwritten).
+fdog_status build_image(Plan &P) {
+  const int tsz = P.precision == 64 ? 8 : 4;
+  size_t sz[kImCount];
+  sz[kImTiles] = P.tiles.size() * sizeof(TileDesc);
+  sz[kImHopOff] = P.hop_off.size() * 4;
+  sz[kImTopo] = P.topo.size() * 4;
+  sz[kImSlotVar] = P.slot_var.size() * 4;
+  sz[kImVarPtr] = P.var_ptr.size() * 8;
+  sz[kImVarSlots] = P.var_slots.size() * 4;
+  sz[kImVarXidx] = P.var_xidx.size() * 4;
+  sz[kImDegList] = P.deg_list.size() * 4;
+  sz[kImEll] = P.ell.size() * 4;
+  sz[kImEllVar] = P.ell_var.size() * 4;
+  sz[kImCsrVar] = P.var_list.size() * 4;
+  sz[kImXLocal] = P.x_local.size() * 4;
+  sz[kImXDeg] = P.x_deg.size() * 4;
+  sz[kImLambda0] = P.slot_var.size() * tsz;
+  sz[kImDist0] = (size_t)P.n_dist * tsz;
+  size_t at = 0;
+  for (int q = 0; q < kImCount; ++q) {
+    P.image.off[q] = at;
+    at += (std::max<size_t>(sz[q], 1) + 255) & ~(size_t)255;
+  }
+  P.image.bytes = at;
+  void *mem = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && cudaMallocHost(&mem, at) == cudaSuccess) {
+    P.image.pinned = true;
+  } else {
+    cudaGetLastError();  // no device (host-only use): pageable memory
+    mem = malloc(at);
+    if (!mem) {
+      set_error("host out of memory (device image, %zu bytes)", at);
+      return FDOG_ENOMEM;
+    }
+  }
+  P.image.data = (unsigned char *)mem;
+  memset(P.image.data, 0, at);
+  auto put = [&](int q, const void *src) {
+    if (sz[q]) memcpy(P.image.data + P.image.off[q], src, sz[q]);
+  };
+  put(kImTiles, P.tiles.data());
+  put(kImHopOff, P.hop_off.data());
+  put(kImTopo, P.topo.data());
+  put(kImSlotVar, P.slot_var.data());
+  put(kImVarPtr, P.var_ptr.data());
+  put(kImVarSlots, P.var_slots.data());
+  put(kImVarXidx, P.var_xidx.data());
+  put(kImDegList, P.deg_list.data());
+  put(kImEll, P.ell.data());
+  put(kImEllVar, P.ell_var.data());
+  put(kImCsrVar, P.var_list.data());
+  put(kImXLocal, P.x_local.data());
+  put(kImXDeg, P.x_deg.data());
+  unsigned char *lam = P.image.data + P.image.off[kImLambda0];
+  for (size_t q = 0; q < P.slot_var.size(); ++q) {
+    const int32_t i = P.slot_var[q];
+    const double v = i >= 0 ? P.cost[i] / (double)P.deg_global[i] : 0.0;
+    if (tsz == 8) ((double *)lam)[q] = v;
+    else ((float *)lam)[q] = (float)v;
+  }
+  unsigned char *dist = P.image.data + P.image.off[kImDist0];
+  for (const auto &d : P.tiles)
+    for (int l = 0; l < d.lanes; ++l) {
+      const size_t top = (size_t)(d.dist_base + (int64_t)d.nodes * d.lanes + l), bot = top + d.lanes;
+      if (tsz == 8) {
+        ((double *)dist)[top] = 0.0;
+        ((double *)dist)[bot] = INFINITY;
+      } else {
+        ((float *)dist)[top] = 0.0f;
+        ((float *)dist)[bot] = INFINITY;
+      }
+    }
+  return FDOG_OK;
+}
+
 }  // namespace fdog
 
 // ---------------------------------------------------------------------------
@@ -713,7 +802,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
 using namespace fdog;
 
 struct fdog_plan {
-  Plan p;
+  std::shared_ptr<Plan> sp = std::make_shared<Plan>();
+  Plan &p = *sp;
 };
 
 extern "C" {
@@ -738,6 +828,7 @@ fdog_status fdog_plan_create(const fdog_problem *p, const fdog_options *opts, fd
   try {
     auto *pl = new fdog_plan();
     fdog_status st = build_plan(p, opts, pl->p);
+    if (st == FDOG_OK) st = build_image(pl->p);
     if (st != FDOG_OK) {
       delete pl;
       return st;
@@ -780,6 +871,7 @@ fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out) {
   out->max_width = P.max_width;
   out->staged_tiles = (int64_t)P.tiles.size() - P.direct_tiles;
   out->sweep_smem_per_warp = warp_bytes(P.SB, P.DB, P.NB);
+  out->h2d_bytes = (int64_t)P.image.bytes;
   return FDOG_OK;
 }
 
@@ -850,5 +942,5 @@ fdog_status fdog_plan_shared_vars(const fdog_plan *plan, int32_t *vars, int64_t 
 
 // accessor for solver.cpp
 namespace fdog {
-const Plan &plan_of(const fdog_plan *p) { return p->p; }
+std::shared_ptr<const Plan> plan_of(const fdog_plan *p) { return p->sp; }
 }

@@ -12,12 +12,13 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "internal.h"
 
 namespace fdog {
-const Plan &plan_of(const fdog_plan *p);
+std::shared_ptr<const Plan> plan_of(const fdog_plan *p);
 }
 
 using namespace fdog;
@@ -70,8 +71,8 @@ struct fdog_solver {
   int32_t static_sched = 0;  // TMA sweep: round-robin tiles only
 
   // host copies needed by getters
-  std::vector<int64_t> canon_slot;
-  std::vector<int32_t> canon_con, canon_pos;
+  // host-side data shared with the plan (no copy; kept alive by the solver)
+  std::shared_ptr<const Plan> plan;
   double free_term = 0.0;
   int64_t n_dev_slots = 0;
   int32_t n_tiles = 0, n_varlist = 0, n_shared = 0;
@@ -94,13 +95,8 @@ struct fdog_solver {
   int32_t *d_ell_var = nullptr, *d_csr_var = nullptr;
   uint8_t *d_x = nullptr;
   unsigned long long *d_undecided = nullptr;
-  std::vector<int64_t> h_row_ptr;
-  std::vector<int32_t> h_col_var, h_col_coef;
-  std::vector<int8_t> h_rel;
-  std::vector<int64_t> h_rhs;
-  std::vector<double> h_cost;
-  std::vector<int32_t> h_deg;
   int64_t n_dist = 0;
+  int64_t upload_bytes = 0;  // host->device bytes of create
   bool lb_dirty = false;  // per-tile partials not reduced yet
   int64_t *d_var_ptr = nullptr;
   double *d_lb_part = nullptr, *d_lb = nullptr;
@@ -157,7 +153,7 @@ fdog_status upload(fdog_solver *s, V **dst, const std::vector<V> &src, size_t mi
   void *p = nullptr;
   CK(cudaMalloc(&p, n * sizeof(V)), "cudaMalloc");
   s->allocs.push_back(p);
-  s->st.device_bytes += (int64_t)(n * sizeof(V));
+  s->st.device_bytes += (int64_t)(n * sizeof(V));  // (legacy helper)
   if (!src.empty()) CK(cudaMemcpyAsync(p, src.data(), src.size() * sizeof(V), cudaMemcpyHostToDevice, s->stream), "H2D");
   *dst = (V *)p;
   return FDOG_OK;
@@ -353,7 +349,7 @@ void free_solver(fdog_solver *s) {
 }
 
 fdog_status fetch_slots(fdog_solver *s, const void *dev, double *out, int64_t len) {
-  const int64_t n = (int64_t)s->canon_slot.size();
+  const int64_t n = (int64_t)s->plan->canon_slot.size();
   if (!out || len < n) {
     set_error("output length %lld < %lld slots", (long long)len, (long long)n);
     return FDOG_EINVAL;
@@ -363,16 +359,16 @@ fdog_status fetch_slots(fdog_solver *s, const void *dev, double *out, int64_t le
   CK(cudaStreamSynchronize(s->stream), "sync");
   if (s->precision == 64) {
     const double *b = (const double *)buf.data();
-    for (int64_t q = 0; q < n; ++q) out[q] = b[s->canon_slot[q]];
+    for (int64_t q = 0; q < n; ++q) out[q] = b[s->plan->canon_slot[q]];
   } else {
     const float *b = (const float *)buf.data();
-    for (int64_t q = 0; q < n; ++q) out[q] = (double)b[s->canon_slot[q]];
+    for (int64_t q = 0; q < n; ++q) out[q] = (double)b[s->plan->canon_slot[q]];
   }
   return FDOG_OK;
 }
 
 fdog_status put_slots(fdog_solver *s, void *dev, const double *in, int64_t len) {
-  const int64_t n = (int64_t)s->canon_slot.size();
+  const int64_t n = (int64_t)s->plan->canon_slot.size();
   if (len != n) {
     set_error("input length %lld != %lld slots", (long long)len, (long long)n);
     return FDOG_EINVAL;
@@ -382,10 +378,10 @@ fdog_status put_slots(fdog_solver *s, void *dev, const double *in, int64_t len) 
   CK(cudaStreamSynchronize(s->stream), "sync");
   if (s->precision == 64) {
     double *b = (double *)buf.data();
-    for (int64_t q = 0; q < n; ++q) b[s->canon_slot[q]] = in[q];
+    for (int64_t q = 0; q < n; ++q) b[s->plan->canon_slot[q]] = in[q];
   } else {
     float *b = (float *)buf.data();
-    for (int64_t q = 0; q < n; ++q) b[s->canon_slot[q]] = (float)in[q];
+    for (int64_t q = 0; q < n; ++q) b[s->plan->canon_slot[q]] = (float)in[q];
   }
   CK(cudaMemcpyAsync(dev, buf.data(), (size_t)s->n_dev_slots * s->tsz, cudaMemcpyHostToDevice, s->stream), "H2D");
   CK(cudaStreamSynchronize(s->stream), "sync");
@@ -421,7 +417,9 @@ fdog_status init_nccl(fdog_solver *s, const fdog_options *o) {
   return FDOG_OK;
 }
 
-fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
+fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o, fdog_solver *s) {
+  s->plan = plan;
+  const Plan &P = *plan;
   s->precision = o->precision == 64 ? 64 : 32;
   if (o->precision != 32 && o->precision != 64) {
     set_error("precision must be 32 or 64");
@@ -451,9 +449,6 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
     CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     s->own_stream = true;
   }
-  s->canon_slot = P.canon_slot;
-  s->canon_con = P.canon_con;
-  s->canon_pos = P.canon_pos;
   s->free_term = P.rank == 0 ? P.free_term : 0.0;
   s->n_dev_slots = (int64_t)P.slot_var.size();
   s->n_tiles = (int32_t)P.tiles.size();
@@ -467,8 +462,12 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   // launch configuration: persistent grid of warps; per-warp shared-memory
   // budget chosen so that >= 16 warps fit per SM; tiles within the budget are
   // staged through TMA (kind bit 2), the rest run directly from global memory
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, s->device), "cudaGetDeviceProperties");
+  struct {
+    int smem_sm, smem_block, sms;
+  } prop;
+  CK(cudaDeviceGetAttribute(&prop.smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, s->device), "attr");
+  CK(cudaDeviceGetAttribute(&prop.smem_block, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device), "attr");
+  CK(cudaDeviceGetAttribute(&prop.sms, cudaDevAttrMultiProcessorCount, s->device), "attr");
   std::vector<TileDesc> tiles = P.tiles;
   if (P.precision != s->precision) {
     set_error("plan packed for fp%d, solver asked for fp%d", P.precision, s->precision);
@@ -485,7 +484,7 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
     for (const auto &d : tiles) narrow = narrow && d.max_w <= 2;
     // the TMA-staged kernel wins while enough warps fit per SM; long BDDs (whole
     // tiles too large to stage for >= 8 warps per SM) stream instead
-    const size_t sm_bytes = (size_t)prop.sharedMemPerMultiprocessor - 4096;
+    const size_t sm_bytes = (size_t)prop.smem_sm - 4096;
     const bool staged_ok = sm_bytes / std::max<size_t>(s->warp_bytes, 1) >= 8;
     const char *m = getenv("FDOG_SWEEP");  // experiment knob: "tma" or "stream"
     const bool forced = m && (m[0] == 's' || m[0] == 't');
@@ -495,7 +494,7 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
       return FDOG_EINVAL;
     }
   }
-  int warps = (int)std::max<size_t>(1, std::min<size_t>(4, (size_t)prop.sharedMemPerBlockOptin / s->warp_bytes));
+  int warps = (int)std::max<size_t>(1, std::min<size_t>(4, (size_t)prop.smem_block / s->warp_bytes));
   s->block = warps * 32;
   s->smem = (size_t)warps * s->warp_bytes;
   int bps = 1;
@@ -507,7 +506,7 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
       if (mode == kForward && rec == (int)s->record_mm) bps = std::max(1, b);
     }
   const int64_t want = ((int64_t)s->n_tiles + warps - 1) / warps;
-  s->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)prop.multiProcessorCount * bps));
+  s->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)prop.sms * bps));
   {
     // few tiles per warp: a plain round-robin over the cost-sorted tiles
     // (claims would sit on the critical path); many tiles per warp: dynamic
@@ -520,94 +519,75 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   s->scratch_stride = (int64_t)relax_slots(s->max_w) * 32;
 
   fdog_status st;
-  if ((st = upload(s, &s->d_tiles, tiles))) return st;
-  if ((st = upload(s, &s->d_hop_off, P.hop_off))) return st;
-  if ((st = upload(s, &s->d_topo, P.topo))) return st;
-  if ((st = upload(s, &s->d_slot_var, P.slot_var))) return st;
-  if ((st = upload(s, &s->d_var_ptr, P.var_ptr))) return st;
-  if ((st = upload(s, &s->d_var_slots, P.var_slots))) return st;
-  if ((st = upload(s, &s->d_var_xidx, P.var_xidx))) return st;
-  if ((st = upload(s, &s->d_deg_list, P.deg_list))) return st;
-  if ((st = upload(s, &s->d_ell_var, P.ell_var))) return st;
-  if ((st = upload(s, &s->d_csr_var, P.var_list))) return st;
-  if ((st = alloc(s, (void **)&s->d_x, (size_t)std::max<int64_t>(P.n_vars, 1)))) return st;
-  if ((st = alloc(s, (void **)&s->d_undecided, sizeof(unsigned long long)))) return st;
-  s->h_row_ptr = P.row_ptr;
-  s->h_col_var = P.col_var;
-  s->h_col_coef = P.col_coef;
-  s->h_rel = P.rel;
-  s->h_rhs = P.rhs;
-  s->h_cost = P.cost;
-  s->h_deg = P.deg_global;
   s->n_dist = P.n_dist;
+  s->n_ell = (int32_t)(P.ell.size() / 2);
   {
-    std::vector<int2> ell(P.ell.size() / 2);
-    for (size_t q = 0; q < ell.size(); ++q) ell[q] = make_int2(P.ell[2 * q], P.ell[2 * q + 1]);
-    s->n_ell = (int32_t)ell.size();
     int64_t maxdeg = 1;
     for (size_t q = 0; q + 1 < P.var_ptr.size(); ++q) maxdeg = std::max<int64_t>(maxdeg, P.var_ptr[q + 1] - P.var_ptr[q]);
     // lanes per CSR variable: about four slots per lane for the widest variable
     s->csr_group = 1;
     while (s->csr_group < 32 && 4 * s->csr_group < maxdeg) s->csr_group *= 2;
-    if ((st = upload(s, &s->d_ell, ell))) return st;
   }
-  if ((st = upload(s, &s->d_x_local, P.x_local))) return st;
-  if ((st = upload(s, &s->d_x_deg, P.x_deg))) return st;
+  // one device allocation: the plan's image (one host->device copy) followed
+  // by the runtime buffers (zeroed)
   const size_t slot_bytes = (size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz;
-  if ((st = alloc(s, &s->d_lambda, slot_bytes))) return st;
-  if ((st = alloc(s, &s->d_delta[0], slot_bytes))) return st;
-  if ((st = alloc(s, &s->d_delta[1], slot_bytes))) return st;
+  const HostImage &im = P.image;
+  if (!im.data) {
+    set_error("plan has no device image");
+    return FDOG_ESTATE;
+  }
+  size_t rt = 0;
+  auto carve = [&](size_t bytes) {
+    const size_t at = rt;
+    rt += (std::max<size_t>(bytes, 16) + 255) & ~(size_t)255;
+    return at;
+  };
+  const size_t o_delta0 = carve(slot_bytes), o_delta1 = carve(slot_bytes);
+  const size_t o_m0 = s->record_mm ? carve(slot_bytes) : 0, o_m1 = s->record_mm ? carve(slot_bytes) : 0;
+  const size_t o_xbuf = carve((size_t)std::max<int32_t>(s->n_shared, 1) * s->tsz);
+  const size_t o_lbp = carve((size_t)std::max(s->n_tiles, 1) * sizeof(double));
+  const size_t o_lb = carve(2 * sizeof(double));
+  const size_t o_ctr = carve(2 * sizeof(unsigned int));
+  const size_t o_scr = carve(s->n_direct ? (size_t)s->grid * (s->block / 32) * s->scratch_stride * s->tsz : 16);
+  const size_t o_x = carve((size_t)std::max<int64_t>(P.n_vars, 1));
+  const size_t o_und = carve(sizeof(unsigned long long));
+  unsigned char *base = nullptr;
+  CK(cudaMalloc((void **)&base, im.bytes + rt), "cudaMalloc");
+  s->allocs.push_back(base);
+  s->st.device_bytes = (int64_t)(im.bytes + rt);
+  s->upload_bytes = (int64_t)im.bytes;
+  CK(cudaMemcpyAsync(base, im.data, im.bytes, cudaMemcpyHostToDevice, s->stream), "H2D");
+  CK(cudaMemsetAsync(base + im.bytes, 0, rt, s->stream), "memset");
+  auto sec = [&](int q) { return (void *)(base + im.off[q]); };
+  s->d_tiles = (TileDesc *)sec(kImTiles);
+  s->d_hop_off = (int32_t *)sec(kImHopOff);
+  s->d_topo = (uint32_t *)sec(kImTopo);
+  s->d_slot_var = (int32_t *)sec(kImSlotVar);
+  s->d_var_ptr = (int64_t *)sec(kImVarPtr);
+  s->d_var_slots = (int32_t *)sec(kImVarSlots);
+  s->d_var_xidx = (int32_t *)sec(kImVarXidx);
+  s->d_deg_list = (int32_t *)sec(kImDegList);
+  s->d_ell = (int2 *)sec(kImEll);
+  s->d_ell_var = (int32_t *)sec(kImEllVar);
+  s->d_csr_var = (int32_t *)sec(kImCsrVar);
+  s->d_x_local = (int32_t *)sec(kImXLocal);
+  s->d_x_deg = (int32_t *)sec(kImXDeg);
+  s->d_lambda = sec(kImLambda0);
+  s->d_dist = sec(kImDist0);
+  unsigned char *r = base + im.bytes;
+  s->d_delta[0] = r + o_delta0;
+  s->d_delta[1] = r + o_delta1;
   if (s->record_mm) {
-    if ((st = alloc(s, &s->d_m0, slot_bytes))) return st;
-    if ((st = alloc(s, &s->d_m1, slot_bytes))) return st;
+    s->d_m0 = r + o_m0;
+    s->d_m1 = r + o_m1;
   }
-  {
-    // per-node distances; the two sentinel slots per lane hold shp(T, T) = 0 and
-    // bottom = +inf and are never overwritten
-    const size_t nd = (size_t)std::max<int64_t>(P.n_dist, 1);
-    std::vector<unsigned char> buf(nd * s->tsz, 0);
-    for (const auto &d : tiles)
-      for (int l = 0; l < d.lanes; ++l) {
-        const size_t top = (size_t)(d.dist_base + (int64_t)d.nodes * d.lanes + l);
-        const size_t bot = top + d.lanes;
-        if (s->precision == 64) {
-          ((double *)buf.data())[top] = 0.0;
-          ((double *)buf.data())[bot] = INFINITY;
-        } else {
-          ((float *)buf.data())[top] = 0.0f;
-          ((float *)buf.data())[bot] = INFINITY;
-        }
-      }
-    if ((st = alloc(s, &s->d_dist, nd * s->tsz))) return st;
-    CK(cudaMemcpyAsync(s->d_dist, buf.data(), nd * s->tsz, cudaMemcpyHostToDevice, s->stream), "H2D");
-    CK(cudaStreamSynchronize(s->stream), "sync");
-  }
-  if ((st = alloc(s, &s->d_xbuf, (size_t)std::max<int32_t>(s->n_shared, 1) * s->tsz))) return st;
-  if ((st = alloc(s, (void **)&s->d_lb_part, (size_t)std::max(s->n_tiles, 1) * sizeof(double)))) return st;
-  if ((st = alloc(s, (void **)&s->d_lb, 2 * sizeof(double)))) return st;
-  if ((st = alloc(s, (void **)&s->d_counter, 2 * sizeof(unsigned int)))) return st;
-  if ((st = alloc(s, &s->d_scratch, s->n_direct ? (size_t)s->grid * (s->block / 32) * s->scratch_stride * s->tsz : 16)))
-    return st;
-  CK(cudaMemsetAsync(s->d_counter, 0, 2 * sizeof(unsigned int), s->stream), "memset");
-  CK(cudaMemsetAsync(s->d_lb, 0, 2 * sizeof(double), s->stream), "memset");
-  CK(cudaMemsetAsync(s->d_delta[0], 0, slot_bytes, s->stream), "memset");
-  CK(cudaMemsetAsync(s->d_delta[1], 0, slot_bytes, s->stream), "memset");
-  if (s->record_mm) {
-    CK(cudaMemsetAsync(s->d_m0, 0, slot_bytes, s->stream), "memset");
-    CK(cudaMemsetAsync(s->d_m1, 0, slot_bytes, s->stream), "memset");
-  }
-  // lambda_i^j = c_i / |J_i| (A9) computed on the host in fp64, rounded once
-  {
-    std::vector<unsigned char> lam(slot_bytes, 0);
-    for (size_t q = 0; q < P.slot_var.size(); ++q) {
-      int32_t i = P.slot_var[q];
-      double v = i >= 0 ? P.cost[i] / (double)P.deg_global[i] : 0.0;
-      if (s->precision == 64) ((double *)lam.data())[q] = v;
-      else ((float *)lam.data())[q] = (float)v;
-    }
-    CK(cudaMemcpyAsync(s->d_lambda, lam.data(), slot_bytes, cudaMemcpyHostToDevice, s->stream), "H2D");
-    CK(cudaStreamSynchronize(s->stream), "sync");
-  }
+  s->d_xbuf = r + o_xbuf;
+  s->d_lb_part = (double *)(r + o_lbp);
+  s->d_lb = (double *)(r + o_lb);
+  s->d_counter = (unsigned int *)(r + o_ctr);
+  s->d_scratch = r + o_scr;
+  s->d_x = (uint8_t *)(r + o_x);
+  s->d_undecided = (unsigned long long *)(r + o_und);
   s->external = s->world > 1 && !o->nccl_unique_id;
   if (s->world > 1 && !s->external && (st = init_nccl(s, o))) return st;
 
@@ -649,6 +629,7 @@ fdog_status create_impl(const Plan &P, const fdog_options *o, fdog_solver *s) {
   s->st.sweep_block = s->block;
   s->st.sweep_smem_per_warp = (int64_t)s->warp_bytes;
   s->st.sweep_streaming = s->stream_mode ? 1 : 0;
+  s->st.h2d_bytes = s->upload_bytes;
 
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;
@@ -695,7 +676,7 @@ fdog_status primal_step_impl(fdog_solver *s, int32_t round, double delta, uint64
   CK(cudaStreamSynchronize(s->stream), "sync");
   if (x)
     for (int64_t i = 0; i < s->n_vars; ++i)
-      if (s->h_deg[i] == 0) x[i] = s->h_cost[i] < 0;  // free variables (A13)
+      if (s->plan->deg_global[i] == 0) x[i] = s->plan->cost[i] < 0;  // free variables (A13)
   *undecided = (int64_t)u;
   if (u == 0) return FDOG_OK;
   {
@@ -708,12 +689,12 @@ fdog_status primal_step_impl(fdog_solver *s, int32_t round, double delta, uint64
 }
 
 bool labeling_feasible(const fdog_solver *s, const uint8_t *x, int64_t *bad_row) {
-  const int64_t m = (int64_t)s->h_rel.size();
+  const int64_t m = (int64_t)s->plan->rel.size();
   for (int64_t j = 0; j < m; ++j) {
     int64_t acc = 0;
-    for (int64_t q = s->h_row_ptr[j]; q < s->h_row_ptr[j + 1]; ++q) acc += (int64_t)s->h_col_coef[q] * x[s->h_col_var[q]];
-    const int8_t r = s->h_rel[j];
-    const bool ok = r < 0 ? acc <= s->h_rhs[j] : r > 0 ? acc >= s->h_rhs[j] : acc == s->h_rhs[j];
+    for (int64_t q = s->plan->row_ptr[j]; q < s->plan->row_ptr[j + 1]; ++q) acc += (int64_t)s->plan->col_coef[q] * x[s->plan->col_var[q]];
+    const int8_t r = s->plan->rel[j];
+    const bool ok = r < 0 ? acc <= s->plan->rhs[j] : r > 0 ? acc >= s->plan->rhs[j] : acc == s->plan->rhs[j];
     if (!ok) {
       *bad_row = j;
       return false;
@@ -833,7 +814,7 @@ fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, u
   }
   *rounds = round;
   double obj = 0.0;
-  for (int64_t i = 0; i < s->n_vars; ++i) obj += x[i] ? s->h_cost[i] : 0.0;
+  for (int64_t i = 0; i < s->n_vars; ++i) obj += x[i] ? s->plan->cost[i] : 0.0;
   *objective = obj;
   fdog_status rs = restore();
   cleanup();
@@ -1077,17 +1058,17 @@ fdog_status fdog_num_slots(const fdog_solver *s, int64_t *out) {
     set_error("null argument");
     return FDOG_EINVAL;
   }
-  *out = (int64_t)s->canon_slot.size();
+  *out = (int64_t)s->plan->canon_slot.size();
   return FDOG_OK;
 }
 
 fdog_status fdog_slot_index(const fdog_solver *s, int32_t *con, int32_t *pos, int64_t len) {
-  if (!s || !con || !pos || len < (int64_t)s->canon_slot.size()) {
+  if (!s || !con || !pos || len < (int64_t)s->plan->canon_slot.size()) {
     set_error("bad argument");
     return FDOG_EINVAL;
   }
-  std::copy(s->canon_con.begin(), s->canon_con.end(), con);
-  std::copy(s->canon_pos.begin(), s->canon_pos.end(), pos);
+  std::copy(s->plan->canon_con.begin(), s->plan->canon_con.end(), con);
+  std::copy(s->plan->canon_pos.begin(), s->plan->canon_pos.end(), pos);
   return FDOG_OK;
 }
 
