@@ -90,7 +90,7 @@ FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (16 + NB * SB + DB + 127
 // creating a solver is one allocation and one host->device copy.
 enum ImageSection {
   kImTiles = 0, kImHopOff, kImTopo, kImSlotVar, kImVarPtr, kImVarSlots, kImVarXidx, kImDegList, kImEll, kImEllVar,
-  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImCount
+  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImCount
 };
 
 struct HostImage {
@@ -132,6 +132,8 @@ struct Plan {
   std::vector<int32_t> deg_list;    // |J_i| (global) per var_list entry
   std::vector<int32_t> ell;         // ELL part: slot pairs (second -1 if |J_i| = 1)
   std::vector<int32_t> ell_var;     // ELL part: the variables
+  std::vector<int32_t> ell4;        // ELL-4 part (|J_i| = 3, 4): slot quads, -1 padded
+  std::vector<int32_t> ell4_var;
   std::vector<int32_t> col_coef;    // copy of the rows (feasibility checks of primal labelings)
   std::vector<int8_t> rel;
   std::vector<int64_t> rhs;
@@ -184,6 +186,8 @@ struct SweepArgs {
 struct AvgArgs {
   int32_t n_ell;             // variables in the ELL part (|J_i| <= 2, not exchanged)
   const int2 *ell;           // their slot pairs (y = -1 if |J_i| = 1)
+  int32_t n_ell4;            // variables in the ELL-4 part (|J_i| = 3, 4, not exchanged)
+  const int4 *ell4;          // their slot quads (-1 padded)
   int32_t n;                 // variables in the CSR part
   int32_t group;             // lanes per CSR variable (power of two <= 32)
   const int64_t *var_ptr;    // CSR over the CSR part
@@ -197,9 +201,11 @@ struct AvgArgs {
 };
 
 struct PrimalArgs {
-  int32_t n_ell, n_csr;
+  int32_t n_ell, n_ell4, n_csr;
   const int2 *ell;
   const int32_t *ell_var;     // variable of each ELL entry
+  const int4 *ell4;
+  const int32_t *ell4_var;
   const int32_t *csr_var;     // variable of each CSR entry
   const int64_t *var_ptr;
   const int32_t *var_slots;

@@ -773,10 +773,29 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
     for (int u = 0; u < 4; ++u) ell_store(out, p[u], x[u], y[u]);
     return;
   }
+  // ELL-4 part (|J_i| = 3 or 4): one variable per thread, slot quad inline,
+  // summed in ascending j
+  const int n_ell4_thr = (a.n_ell4 + 31) & ~31;
+  if (tid < n_ell_thr + n_ell4_thr) {
+    const int q = tid - n_ell_thr;
+    if (q >= a.n_ell4) return;
+    const int4 p = __ldg(a.ell4 + q);
+    const T x0 = __ldg(db + p.x), x1 = __ldg(db + p.y), x2 = __ldg(db + p.z);
+    const T x3 = p.w >= 0 ? __ldg(db + p.w) : T(0);
+    T s = x0 + x1;
+    s += x2;
+    if (p.w >= 0) s += x3;
+    const T v = s / T(p.w >= 0 ? 4 : 3);
+    out[p.x] = v;
+    out[p.y] = v;
+    out[p.z] = v;
+    if (p.w >= 0) out[p.w] = v;
+    return;
+  }
   // CSR part: a group of G lanes per variable; lane j sums slots j, j+G, ...
   // in order, then a fixed-shape shuffle tree combines the lanes (deterministic)
   const int G = a.group;
-  const int gt = tid - n_ell_thr;
+  const int gt = tid - n_ell_thr - n_ell4_thr;
   const int q = gt / G, j = gt % G;
   const bool on = q < a.n;
   T *__restrict__ xbuf = reinterpret_cast<T *>(a.xbuf);
@@ -820,23 +839,33 @@ __device__ __forceinline__ double primal_uniform(uint64_t seed, int64_t round, i
 template <typename T>
 __global__ void __launch_bounds__(256) primal_kernel(const PrimalArgs a) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= a.n_ell + a.n_csr) return;
+  if (q >= a.n_ell + a.n_ell4 + a.n_csr) return;
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
-  int i, s0 = -1, s1 = -1;
-  int64_t p0 = 0, p1 = 0;
-  if (q < a.n_ell) {
+  int i, sl[4] = {-1, -1, -1, -1};
+  int64_t p0 = 0, p1 = 0, deg;
+  const int kind = q < a.n_ell ? 0 : q < a.n_ell + a.n_ell4 ? 1 : 2;
+  if (kind == 0) {
     const int2 pr = a.ell[q];
     i = a.ell_var[q];
-    s0 = pr.x;
-    s1 = pr.y;
+    sl[0] = pr.x;
+    sl[1] = pr.y;
+    deg = pr.y >= 0 ? 2 : 1;
+  } else if (kind == 1) {
+    const int4 pr = a.ell4[q - a.n_ell];
+    i = a.ell4_var[q - a.n_ell];
+    sl[0] = pr.x;
+    sl[1] = pr.y;
+    sl[2] = pr.z;
+    sl[3] = pr.w;
+    deg = pr.w >= 0 ? 4 : 3;
   } else {
-    const int c = q - a.n_ell;
+    const int c = q - a.n_ell - a.n_ell4;
     i = a.csr_var[c];
     p0 = a.var_ptr[c];
     p1 = a.var_ptr[c + 1];
+    deg = p1 - p0;
   }
-  auto slot_at = [&](int64_t u) -> int { return q < a.n_ell ? (u == 0 ? s0 : s1) : a.var_slots[p0 + u]; };
-  const int64_t deg = q < a.n_ell ? (s1 >= 0 ? 2 : 1) : p1 - p0;
+  auto slot_at = [&](int64_t u) -> int { return kind < 2 ? sl[u] : a.var_slots[p0 + u]; };
   bool pos = true, neg = true, zero = true;
   double dsum = 0.0;  // sign of d_i = sum_j (m1 - m0) = sign of sum_j delta_bar (omega > 0)
   for (int64_t u = 0; u < deg; ++u) {
@@ -957,7 +986,8 @@ static int grid_for(int64_t n, int block) {
 
 int launch_avg(int precision, const AvgArgs &a, void *stream) {
   const int block = 256;
-  const int64_t threads = (int64_t)((((a.n_ell + 3) / 4) + 31) & ~31) + (int64_t)a.n * a.group;
+  const int64_t threads = (int64_t)((((a.n_ell + 3) / 4) + 31) & ~31) + (int64_t)((a.n_ell4 + 31) & ~31) +
+                          (int64_t)a.n * a.group;
   const int grid = (int)std::max<int64_t>(1, (threads + block - 1) / block);
   void *args[] = {(void *)&a};
   const void *f = precision == 64 ? (const void *)avg_kernel<double> : (const void *)avg_kernel<float>;
@@ -986,7 +1016,7 @@ int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, voi
 }
 
 int launch_primal(int precision, const PrimalArgs &a, void *stream) {
-  const int n = a.n_ell + a.n_csr;
+  const int n = a.n_ell + a.n_ell4 + a.n_csr;
   if (n <= 0) return 0;
   const int block = 256, grid = (n + block - 1) / block;
   if (precision == 64)

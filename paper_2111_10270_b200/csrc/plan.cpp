@@ -679,12 +679,17 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     std::vector<int64_t> csr_ptr(1, 0);
     P.ell.clear();
     P.ell_var.clear();
+    P.ell4.clear();
+    P.ell4_var.clear();
     for (size_t q = 0; q < P.var_list.size(); ++q) {
       const int64_t a = P.var_ptr[q], b = P.var_ptr[q + 1];
       if (b - a <= 2 && P.var_xidx[q] < 0) {
         P.ell.push_back(P.var_slots[a]);
         P.ell.push_back(b - a == 2 ? P.var_slots[a + 1] : -1);
         P.ell_var.push_back(P.var_list[q]);
+      } else if (b - a <= 4 && P.var_xidx[q] < 0) {
+        for (int64_t u = 0; u < 4; ++u) P.ell4.push_back(a + u < b ? P.var_slots[a + u] : -1);
+        P.ell4_var.push_back(P.var_list[q]);
       } else {
         csr_list.push_back(P.var_list[q]);
         csr_x.push_back(P.var_xidx[q]);
@@ -732,6 +737,8 @@ fdog_status build_image(Plan &P) {
   sz[kImEll] = P.ell.size() * 4;
   sz[kImEllVar] = P.ell_var.size() * 4;
   sz[kImCsrVar] = P.var_list.size() * 4;
+  sz[kImEll4] = P.ell4.size() * 4;
+  sz[kImEll4Var] = P.ell4_var.size() * 4;
   sz[kImXLocal] = P.x_local.size() * 4;
   sz[kImXDeg] = P.x_deg.size() * 4;
   sz[kImLambda0] = P.slot_var.size() * tsz;
@@ -770,6 +777,8 @@ fdog_status build_image(Plan &P) {
   put(kImEll, P.ell.data());
   put(kImEllVar, P.ell_var.data());
   put(kImCsrVar, P.var_list.data());
+  put(kImEll4, P.ell4.data());
+  put(kImEll4Var, P.ell4_var.data());
   put(kImXLocal, P.x_local.data());
   put(kImXDeg, P.x_deg.data());
   unsigned char *lam = P.image.data + P.image.off[kImLambda0];

@@ -90,7 +90,9 @@ struct fdog_solver {
   void *d_m0 = nullptr, *d_m1 = nullptr;
   int32_t *d_var_slots = nullptr, *d_var_xidx = nullptr, *d_deg_list = nullptr;
   int2 *d_ell = nullptr;
-  int32_t n_ell = 0, csr_group = 1;
+  int4 *d_ell4 = nullptr;
+  int32_t *d_ell4_var = nullptr;
+  int32_t n_ell = 0, n_ell4 = 0, csr_group = 1;
   // primal rounding
   int32_t *d_ell_var = nullptr, *d_csr_var = nullptr;
   uint8_t *d_x = nullptr;
@@ -261,6 +263,8 @@ AvgArgs avg_args(fdog_solver *s) {
   AvgArgs a{};
   a.n_ell = s->n_ell;
   a.ell = s->d_ell;
+  a.n_ell4 = s->n_ell4;
+  a.ell4 = s->d_ell4;
   a.tile_counter = s->d_counter + 1;
   a.n = s->n_varlist;
   a.group = s->csr_group;
@@ -521,6 +525,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   fdog_status st;
   s->n_dist = P.n_dist;
   s->n_ell = (int32_t)(P.ell.size() / 2);
+  s->n_ell4 = (int32_t)(P.ell4.size() / 4);
   {
     int64_t maxdeg = 1;
     for (size_t q = 0; q + 1 < P.var_ptr.size(); ++q) maxdeg = std::max<int64_t>(maxdeg, P.var_ptr[q + 1] - P.var_ptr[q]);
@@ -569,6 +574,8 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_deg_list = (int32_t *)sec(kImDegList);
   s->d_ell = (int2 *)sec(kImEll);
   s->d_ell_var = (int32_t *)sec(kImEllVar);
+  s->d_ell4 = (int4 *)sec(kImEll4);
+  s->d_ell4_var = (int32_t *)sec(kImEll4Var);
   s->d_csr_var = (int32_t *)sec(kImCsrVar);
   s->d_x_local = (int32_t *)sec(kImXLocal);
   s->d_x_deg = (int32_t *)sec(kImXDeg);
@@ -644,9 +651,12 @@ namespace {
 PrimalArgs primal_args(fdog_solver *s, int mode, int32_t round, double delta, uint64_t seed) {
   PrimalArgs a{};
   a.n_ell = s->n_ell;
+  a.n_ell4 = s->n_ell4;
   a.n_csr = s->n_varlist;
   a.ell = s->d_ell;
   a.ell_var = s->d_ell_var;
+  a.ell4 = s->d_ell4;
+  a.ell4_var = s->d_ell4_var;
   a.csr_var = s->d_csr_var;
   a.var_ptr = s->d_var_ptr;
   a.var_slots = s->d_var_slots;
