@@ -112,6 +112,9 @@ fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out);
 fdog_status fdog_plan_bdd(const fdog_plan *plan, int32_t j, int32_t *k, int32_t *n_nodes,
                           int32_t *hop_start, int32_t *lo, int32_t *hi, int32_t cap_hops,
                           int32_t cap_nodes);
+/* Device slot of every canonical slot (j ascending, h ascending) of this rank
+ * (layout inspection; len >= the rank's slot count). */
+fdog_status fdog_plan_slot_map(const fdog_plan *plan, int64_t *dev_slot, int64_t len);
 /* Global row -> owning rank for every row (length n_cons). */
 fdog_status fdog_plan_owner(const fdog_plan *plan, int32_t *owner, int64_t len);
 /* Ascending global indices of the variables exchanged between ranks (held by

@@ -62,7 +62,7 @@ class KernelTime(C.Structure):
                 ("bytes_per_launch", C.c_double)]
 
 
-EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdog_plan_stats",
+EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdog_plan_stats", "fdog_plan_slot_map",
            "fdog_plan_bdd", "fdog_plan_owner", "fdog_plan_shared_vars", "fdog_create",
            "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_lower_bound",
            "fdog_finalize", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
@@ -92,6 +92,7 @@ def load():
         "fdog_plan_stats": ([P, P], C.c_int),
         "fdog_plan_bdd": ([P, i32, P, P, P, P, P, i32, i32], C.c_int),
         "fdog_plan_owner": ([P, P, i64], C.c_int),
+        "fdog_plan_slot_map": ([P, P, i64], C.c_int),
         "fdog_plan_shared_vars": ([P, P, i64, P], C.c_int),
         "fdog_create": ([P, P, C.POINTER(P)], C.c_int),
         "fdog_create_from_plan": ([P, P, C.POINTER(P)], C.c_int),
@@ -214,6 +215,13 @@ class Plan:
         _check(self._lib.fdog_plan_bdd(self._h, int(j), C.byref(k), C.byref(n), _ptr(hs), _ptr(lo),
                                        _ptr(hi), k.value, n.value), "fdog_plan_bdd")
         return hs, lo[:n.value], hi[:n.value]
+
+    def slot_map(self):
+        """Device slot of every canonical slot (j ascending, h ascending)."""
+        n = self.stats()["slots"]
+        out = np.empty(max(n, 1), np.int64)
+        _check(self._lib.fdog_plan_slot_map(self._h, _ptr(out), out.size), "fdog_plan_slot_map")
+        return out[:n]
 
     def owner(self):
         o = np.empty(max(self.n_cons, 1), np.int32)

@@ -230,6 +230,5 @@ int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const i
 int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, void *stream);
 int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream);
 int launch_primal(int precision, const PrimalArgs &a, void *stream);
-int launch_fill(int precision, int64_t n, void *dst, double value, void *stream);
 
 }  // namespace fdog

@@ -915,11 +915,6 @@ __global__ void add_deferred_kernel(int64_t n, T *__restrict__ lambda, T *__rest
   }
 }
 
-template <typename T>
-__global__ void fill_kernel(int64_t n, T *__restrict__ dst, T v) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-    dst[q] = v;
-}
 
 // ---------------------------------------------------------------- launchers
 
@@ -1031,14 +1026,5 @@ int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream
   return launch_pdl((const void *)lb_reduce_kernel, dim3(1), dim3(1024), 0, stream, args);
 }
 
-int launch_fill(int precision, int64_t n, void *dst, double value, void *stream) {
-  if (n <= 0) return 0;
-  const int block = 256, grid = grid_for(n, block);
-  if (precision == 64)
-    fill_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, (double *)dst, value);
-  else
-    fill_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, (float *)dst, (float)value);
-  return (int)cudaGetLastError();
-}
 
 }  // namespace fdog

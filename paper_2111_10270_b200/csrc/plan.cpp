@@ -922,6 +922,15 @@ fdog_status fdog_plan_bdd(const fdog_plan *plan, int32_t j, int32_t *k, int32_t 
   return FDOG_OK;
 }
 
+fdog_status fdog_plan_slot_map(const fdog_plan *plan, int64_t *dev_slot, int64_t len) {
+  if (!plan || !dev_slot || len < (int64_t)plan->p.canon_slot.size()) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  std::copy(plan->p.canon_slot.begin(), plan->p.canon_slot.end(), dev_slot);
+  return FDOG_OK;
+}
+
 fdog_status fdog_plan_owner(const fdog_plan *plan, int32_t *owner, int64_t len) {
   if (!plan || !owner || len < plan->p.n_cons) {
     set_error("bad argument");

@@ -45,9 +45,9 @@ struct Nccl {
   nccl_comm comm = nullptr;
 };
 
-enum KernelId { kKSweepFwd = 0, kKSweepBwd, kKEnergy, kKAvg, kKAvgFinish, kKAllreduce, kKAddDeferred, kKFill, kKLbReduce, kKPrimal, kKCount };
+enum KernelId { kKSweepFwd = 0, kKSweepBwd, kKEnergy, kKAvg, kKAvgFinish, kKAllreduce, kKAddDeferred, kKLbReduce, kKPrimal, kKCount };
 const char *kKernelNames[kKCount] = {"sweep_forward", "sweep_backward", "sweep_energy", "avg", "avg_finish",
-                                     "nccl_allreduce", "add_deferred", "fill", "lb_reduce", "primal"};
+                                     "nccl_allreduce", "add_deferred", "lb_reduce", "primal"};
 
 struct EventRec {
   int kernel;
@@ -148,27 +148,6 @@ fdog_status cuda_fail(cudaError_t e, const char *what) {
     cudaError_t e__ = (cudaError_t)(call);             \
     if (e__ != cudaSuccess) return cuda_fail(e__, what); \
   } while (0)
-
-template <typename V>
-fdog_status upload(fdog_solver *s, V **dst, const std::vector<V> &src, size_t min_elems = 1) {
-  size_t n = std::max(src.size(), min_elems);
-  void *p = nullptr;
-  CK(cudaMalloc(&p, n * sizeof(V)), "cudaMalloc");
-  s->allocs.push_back(p);
-  s->st.device_bytes += (int64_t)(n * sizeof(V));  // (legacy helper)
-  if (!src.empty()) CK(cudaMemcpyAsync(p, src.data(), src.size() * sizeof(V), cudaMemcpyHostToDevice, s->stream), "H2D");
-  *dst = (V *)p;
-  return FDOG_OK;
-}
-
-fdog_status alloc(fdog_solver *s, void **dst, size_t bytes) {
-  void *p = nullptr;
-  CK(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc");
-  s->allocs.push_back(p);
-  s->st.device_bytes += (int64_t)bytes;
-  *dst = p;
-  return FDOG_OK;
-}
 
 cudaEvent_t get_event(fdog_solver *s) {
   if (!s->event_pool.empty()) {
