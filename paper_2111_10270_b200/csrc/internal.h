@@ -55,9 +55,9 @@ struct TileDesc {
   int32_t nodes;    // nodes per lane (hop_off[hop_base + K])
   int32_t max_w;    // widest partition of the tile
   int32_t lanes;    // L
-  int32_t pad_;
+  int32_t pad_[3];  // 64 bytes: fetched as four 16-byte cp.async chunks
 };
-static_assert(sizeof(TileDesc) == 56, "TileDesc layout");
+static_assert(sizeof(TileDesc) == 64, "TileDesc layout");
 
 #if defined(__CUDACC__)
 #define FDOG_HD __host__ __device__ __forceinline__
@@ -67,10 +67,11 @@ static_assert(sizeof(TileDesc) == 56, "TileDesc layout");
 
 // Shared-memory layout of one warp (identical on host and device):
 //   [0, 16)                   two mbarriers
-//   [16, 16 + SB)             stage buffer 0: lambda | avg->delta | distances D[nodes + 2][L] |
+//   [16, 256)                 ring of three tile descriptors (current, next, next-but-one)
+//   [256, 256 + SB)           stage buffer 0: lambda | avg->delta | distances D[nodes + 2][L] |
 //                             topology | partition offsets
-//   [16 + SB, 16 + 2 SB)      stage buffer 1 (NB = 2 only)
-//   [16 + NB SB, + DB)        relaxation buffers R[3 (W + 1)][L]
+//   [256 + SB, 256 + 2 SB)    stage buffer 1 (NB = 2 only)
+//   [256 + NB SB, + DB)       relaxation buffers R[3 (W + 1)][L]
 FDOG_HD int r16(int bytes) { return (bytes + 15) & ~15; }
 FDOG_HD int stage_lam_bytes(int tsz, int K, int L) { return r16(K * L * tsz); }
 FDOG_HD int stage_va_bytes(int tsz, int K, int L) { return r16(K * L * tsz); }
@@ -83,7 +84,8 @@ FDOG_HD int stage_bytes(int tsz, int kind, int K, int nodes, int L) {
 }
 FDOG_HD int relax_slots(int W) { return 3 * (W + 1); }
 FDOG_HD int relax_bytes(int tsz, int W, int L) { return r16(relax_slots(W) * L * tsz); }
-FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (16 + NB * SB + DB + 127) & ~127; }
+constexpr int kWarpHeader = 256;
+FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (kWarpHeader + NB * SB + DB + 127) & ~127; }
 
 // One contiguous device image of everything a solver uploads (built by the
 // plan, untimed; pinned host memory when a CUDA device is present), so that

@@ -444,6 +444,15 @@ __device__ __forceinline__ void issue_stage(const SweepArgs &a, const TileDesc &
 // two stage buffers the next tile's TMA loads are in flight while the current
 // one is processed.  lambda, delta and the distances go back with TMA bulk
 // stores.
+// cp.async of one 64-byte tile descriptor into shared memory (lanes 0-3)
+__device__ __forceinline__ void fetch_desc(TileDesc *dst, const TileDesc *src, int lane) {
+  if (lane < 4)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(reinterpret_cast<char *>(dst) + 16 * lane)),
+                 "l"(reinterpret_cast<const char *>(src) + 16 * lane)
+                 : "memory");
+  cp_async_commit();
+}
+
 template <typename T, int MODE, bool REC>
 __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   constexpr bool kUpd = MODE == kForward || MODE == kBackward;
@@ -452,10 +461,11 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   const int warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
   unsigned char *wbase = smem_raw + (size_t)warp * warp_bytes(a.SB, a.DB, a.NB);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(wbase);  // bar[0], bar[1]
-  unsigned char *const sbuf0 = wbase + 16;
-  unsigned char *const sbuf1 = wbase + 16 + (a.NB > 1 ? a.SB : 0);
-  unsigned char *const rbase = wbase + 16 + a.NB * a.SB;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(wbase);          // bar[0], bar[1]
+  TileDesc *ring = reinterpret_cast<TileDesc *>(wbase + 64);    // 3 descriptors
+  unsigned char *const sbuf0 = wbase + kWarpHeader;
+  unsigned char *const sbuf1 = wbase + kWarpHeader + (a.NB > 1 ? a.SB : 0);
+  unsigned char *const rbase = wbase + kWarpHeader + a.NB * a.SB;
 
   T *__restrict__ lambda = reinterpret_cast<T *>(a.lambda);
   T *__restrict__ delta_out = reinterpret_cast<T *>(a.delta_out);
@@ -468,32 +478,33 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
-  __syncwarp();
-
   // tile schedule: warp w takes tiles w and w + W statically (tiles are sorted
   // by decreasing cost); later tiles are claimed from a global counter (reset
-  // before every sweep), one claim in flight two tiles ahead of its use
+  // before every sweep) unless static_sched
   const int W = gridDim.x * wpb;
+  int t = gwarp;
+  int tn = gwarp + W < a.n_tiles ? gwarp + W : a.n_tiles;
+  // descriptors are constant: fetch them before waiting for the predecessor
+  if (t < a.n_tiles) fetch_desc(&ring[0], a.tiles + t, lane);
+  if (tn < a.n_tiles) fetch_desc(&ring[1], a.tiles + tn, lane);
   pdl_wait();
   auto claim_issue = [&]() -> int { return lane == 0 ? (int)atomicAdd(a.tile_counter, 1u) : 0; };
   auto claim_get = [&](int raw) -> int { return 2 * W + __shfl_sync(0xffffffffu, raw, 0); };
-  // pipeline per warp: the claim for the tile after next is in flight, the
-  // next tile's descriptor is loaded and its TMA stage loads are issued, while
-  // the current tile is processed
+  // pipeline per warp: while tile t is processed, the TMA stage loads of the
+  // next tile are in flight, the descriptor of the one after is being fetched
+  // (cp.async), and (dynamic schedule) the claim for the tile after that.
   uint32_t phase = 0;  // bit b = parity of bar[b]
-  int b = 0;
-  int t = gwarp;
-  TileDesc d;
-  if (t < a.n_tiles) {
-    d = a.tiles[t];
-    if ((d.kind & 2) && lane == 0) issue_stage<T, MODE>(a, d, stage_at<T>(sbuf0, d), &bar[0]);
-  }
-  int tn = gwarp + W < a.n_tiles ? gwarp + W : a.n_tiles;
-  TileDesc dn;
-  if (tn < a.n_tiles) dn = a.tiles[tn];
+  int b = 0, rc = 0;   // stage buffer and ring slot of the current tile
+  cp_async_wait_all();
+  __syncwarp();
+  if (t < a.n_tiles && (ring[0].kind & 2) && lane == 0)
+    issue_stage<T, MODE>(a, ring[0], stage_at<T>(sbuf0, ring[0]), &bar[0]);
   bool pending = !a.static_sched && tn < a.n_tiles && 2 * W < a.n_tiles;  // a claim is in flight
   int raw_nn = pending ? claim_issue() : 0;
   while (t < a.n_tiles) {
+    const TileDesc &d = ring[rc];
+    const TileDesc &dn = ring[rc == 2 ? 0 : rc + 1];
+    TileDesc &dnn = ring[rc == 0 ? 2 : rc - 1];
     const bool has_next = tn < a.n_tiles;
     const int bn = a.NB > 1 ? (b ^ 1) : 0;
     if (a.NB > 1 && has_next && (dn.kind & 2) && lane == 0) {
@@ -507,8 +518,8 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
       tnn = claim_get(raw_nn);
       if (tnn > a.n_tiles) tnn = a.n_tiles;
     }
-    TileDesc dnn;
-    if (tnn < a.n_tiles) dnn = a.tiles[tnn];  // used one tile later
+    __syncwarp();  // every lane has read dnn's slot (it held the previous tile)
+    if (tnn < a.n_tiles) fetch_desc(&dnn, a.tiles + tnn, lane);  // used one tile later
     pending = !a.static_sched && tnn < a.n_tiles;
     raw_nn = pending ? claim_issue() : 0;
     const int L = d.lanes;
@@ -561,15 +572,15 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     }
     acc = warp_sum(acc);
     if (lane == 0) a.lb_part[t] = acc;
+    cp_async_wait_all();  // the descriptor of the tile after next has landed
     __syncwarp();
     if (a.NB == 1 && has_next && (dn.kind & 2) && lane == 0) {
       bulk_wait_read_all();  // single stage buffer: its stores must have read it
       issue_stage<T, MODE>(a, dn, stage_at<T>(sbuf0, dn), &bar[0]);
     }
     t = tn;
-    d = dn;
     tn = tnn;
-    dn = dnn;
+    rc = rc == 2 ? 0 : rc + 1;
     b = bn;
   }
   if (lane == 0) bulk_wait_read_all();  // shared memory must outlive the TMA stores' reads
