@@ -61,6 +61,7 @@ def _load():
         lib.oracle_lower_bound.argtypes = [P, P]
         lib.oracle_dual_energy.argtypes = [P, P]
         lib.oracle_finalize.argtypes = [P]
+        lib.oracle_finalize_avg.argtypes = [P]
         lib.oracle_num_slots.argtypes = [P, P]
         for f in ("oracle_get_lambda", "oracle_get_deferred", "oracle_set_lambda"):
             getattr(lib, f).argtypes = [P, P, C.c_int64]
@@ -142,8 +143,9 @@ class Oracle:
         self._chk(self._lib.oracle_dual_energy(self._h, C.byref(x)), "dual_energy")
         return x.value
 
-    def finalize(self):
-        self._chk(self._lib.oracle_finalize(self._h), "finalize")
+    def finalize(self, averaged: bool = False):
+        fn = self._lib.oracle_finalize_avg if averaged else self._lib.oracle_finalize
+        self._chk(fn(self._h), "finalize")
 
     def num_slots(self) -> int:
         x = C.c_int64()

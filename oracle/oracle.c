@@ -589,6 +589,29 @@ int oracle_finalize(oracle_solver *s) {
   return O_OK;
 }
 
+/* Final correction read as "a min-marginal averaging step" (reading
+ * A11 alternative): lambda_i^j += (1/|J_i|) sum_k delta_bar_ik, delta_bar = 0.
+ * Dual feasible like the per-slot form: sum_j [lambda + avg] = c_i. */
+int oracle_finalize_avg(oracle_solver *s) {
+  if (!s) return O_EINVAL;
+  for (int32_t i = 0; i < s->n_vars; ++i) {
+    int64_t deg = s->var_ptr[i + 1] - s->var_ptr[i];
+    if (deg == 0) continue;
+    double sum = 0.0;
+    for (int64_t q = s->var_ptr[i]; q < s->var_ptr[i + 1]; ++q) sum += s->delta_bar[s->var_slots[q]];
+    double avg = sum / (double)deg;
+    for (int64_t q = s->var_ptr[i]; q < s->var_ptr[i + 1]; ++q) s->lambda[s->var_slots[q]] += avg;
+  }
+  for (int64_t q = 0; q < s->n_slots; ++q) s->delta_bar[q] = 0.0;
+  for (int32_t j = 0; j < s->n_cons; ++j) {
+    backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+    forward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
+  }
+  s->lb = raw_energy(s);
+  s->ctt_ok = s->cfr_ok = 1;
+  return O_OK;
+}
+
 int oracle_num_slots(const oracle_solver *s, int64_t *out) {
   if (!s || !out) return O_EINVAL;
   *out = s->n_slots;

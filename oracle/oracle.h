@@ -61,6 +61,8 @@ int oracle_dual_energy(const oracle_solver *s, double *out);
 /* Final correction P:650-652: lambda += delta_bar (per slot), delta_bar = 0,
  * recompute cost_to_terminal. */
 int oracle_finalize(oracle_solver *s);
+/* Averaged final correction (P:673 prose; A11 alternative). */
+int oracle_finalize_avg(oracle_solver *s);
 
 /* Slots in canonical order (j ascending, hop ascending). */
 int oracle_num_slots(const oracle_solver *s, int64_t *out);

@@ -65,7 +65,7 @@ class KernelTime(C.Structure):
 EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdog_plan_stats", "fdog_plan_slot_map",
            "fdog_plan_bdd", "fdog_plan_owner", "fdog_plan_shared_vars", "fdog_create",
            "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_lower_bound",
-           "fdog_finalize", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
+           "fdog_finalize", "fdog_finalize_averaged", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
            "fdog_get_deferred", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
            "fdog_profile", "fdog_profile_reset", "fdog_profile_enable", "fdog_pass_begin", "fdog_pass_end",
            "fdog_exchange_size", "fdog_exchange_read", "fdog_exchange_write", "fdog_default_primal_options",
@@ -101,6 +101,7 @@ def load():
         "fdog_pass": ([P, i32, dbl], C.c_int),
         "fdog_lower_bound": ([P, P], C.c_int),
         "fdog_finalize": ([P], C.c_int),
+        "fdog_finalize_averaged": ([P], C.c_int),
         "fdog_num_slots": ([P, P], C.c_int),
         "fdog_slot_index": ([P, P, P, i64], C.c_int),
         "fdog_get_lambda": ([P, P, i64], C.c_int),
@@ -276,8 +277,12 @@ class Solver:
         _check(self._lib.fdog_lower_bound(self._h, C.byref(x)), "fdog_lower_bound")
         return x.value
 
-    def finalize(self):
-        _check(self._lib.fdog_finalize(self._h), "fdog_finalize")
+    def finalize(self, averaged: bool = False):
+        """P:650-652 per-slot correction, or the averaged reading of P:673."""
+        if averaged:
+            _check(self._lib.fdog_finalize_averaged(self._h), "fdog_finalize_averaged")
+        else:
+            _check(self._lib.fdog_finalize(self._h), "fdog_finalize")
 
     def num_slots(self) -> int:
         x = C.c_int64()

@@ -1042,6 +1042,29 @@ fdog_status fdog_finalize(fdog_solver *s) {
   return energy(s);
 }
 
+fdog_status fdog_finalize_averaged(fdog_solver *s) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  if (s->external) {
+    set_error("fdog_finalize_averaged needs world == 1 or the NCCL exchange");
+    return FDOG_ESTATE;
+  }
+  // the averaging kernel (+ exchange) writes avg_i into every slot of the other
+  // delta buffer; lambda += that buffer, then both buffers are zero
+  fdog_status st = run_avg(s);
+  if (st) return st;
+  int e;
+  {
+    Timed t(s, kKAddDeferred);
+    e = launch_add_deferred(s->precision, s->n_dev_slots, s->d_lambda, s->d_delta[s->cur ^ 1], s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "add_deferred");
+  CK(cudaMemsetAsync(s->d_delta[s->cur], 0, (size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz, s->stream), "memset");
+  return energy(s);
+}
+
 fdog_status fdog_num_slots(const fdog_solver *s, int64_t *out) {
   if (!s || !out) {
     set_error("null argument");

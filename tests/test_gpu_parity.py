@@ -156,6 +156,22 @@ def test_finalize_feasible(oracle_mod):
     assert g.lower_bound() == pytest.approx(o.lower_bound(), rel=1e-9, abs=1e-9)
 
 
+def test_finalize_averaged(oracle_mod):
+    """Averaged final correction (P:673 prose) vs the oracle; feasible afterwards."""
+    p = synth.gm_worms_like(15, n_src=50, k_cand=5, knn=6)
+    g = F.Solver(p, precision=64)
+    o = oracle_mod.Oracle(p)
+    g.iterate(5, 0.5); o.iterate(5, 0.5)
+    g.pass_(True, 0.5); o.pass_(True, 0.5)
+    g.finalize(averaged=True); o.finalize(averaged=True)
+    s = _s(p)
+    assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s
+    assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+    assert np.all(g.deferred() == 0)
+    g.iterate(2, 0.5); o.iterate(2, 0.5)
+    assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+
+
 def test_edge_cases(oracle_mod):
     # no constraints: bound = sum min(c, 0)
     p = synth.from_rows(3, [-1.0, 2.0, -0.5], [])

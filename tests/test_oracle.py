@@ -224,6 +224,23 @@ def test_prop1_invariants_random(oracle_mod, omega):
     assert checked >= 40
 
 
+def test_averaged_finalize_feasible(oracle_mod):
+    """Averaged final correction (P:673 prose): sum_j lambda_i^j = c_i afterwards,
+    and its bound is a valid lower bound (<= OPT)."""
+    for seed in range(30):
+        p = synth.random_ilp(6000 + seed, n=10, m=6, kmax=6)
+        opt = bf.solve_exhaustive(p)
+        if opt is None:
+            continue
+        o = oracle_mod.Oracle(p)
+        o.iterate(4, 0.5)
+        o.pass_(True, 0.5)
+        o.finalize(averaged=True)
+        assert _feasibility_residual(p, o.lam(), np.zeros(o.num_slots())) < 1e-9
+        assert o.lower_bound() <= opt + 1e-9
+        assert np.all(o.deferred() == 0)
+
+
 def test_single_constraint_is_exact(oracle_mod):
     """m = 1: the dual is the subproblem itself, so LB = OPT from init and stays."""
     for seed in range(20):
