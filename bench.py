@@ -48,6 +48,8 @@ def _workload(name):
         return synth.mrf_potts(0)
     if name == "qap50":
         return synth.qap(0, 50)
+    if name == "qap128":
+        return synth.qap(0, 128)
     if name == "celltrack":
         return synth.celltrack(0)
     if name == "lap4":

@@ -465,10 +465,11 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     // all tiles narrow: the passes stream from global memory (no staging)
     bool narrow = true;
     for (const auto &d : tiles) narrow = narrow && d.max_w <= 2;
-    // the TMA-staged kernel wins while enough warps fit per SM; long BDDs (whole
-    // tiles too large to stage for >= 8 warps per SM) stream instead
+    // the TMA-staged kernel wins while every tile is staged and enough warps fit
+    // per SM; long BDDs (tiles too large to stage, or only for < 8 warps per SM)
+    // stream instead
     const size_t sm_bytes = (size_t)prop.smem_sm - 4096;
-    const bool staged_ok = sm_bytes / std::max<size_t>(s->warp_bytes, 1) >= 8;
+    const bool staged_ok = sm_bytes / std::max<size_t>(s->warp_bytes, 1) >= 8 && s->n_direct == 0;
     const char *m = getenv("FDOG_SWEEP");  // experiment knob: "tma" or "stream"
     const bool forced = m && (m[0] == 's' || m[0] == 't');
     s->stream_mode = narrow && (forced ? m[0] == 's' : !staged_ok);
