@@ -54,6 +54,8 @@ def _workload(name):
         return synth.celltrack(0)
     if name == "lap4":
         return synth.lap_random(4, 0)
+    if name == "thin_hop":
+        return synth.thin_hop(0)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -352,6 +354,7 @@ def run_gpu(args):
                        "l2": "flushed before every timed step (256 MB write + 256 MB read, untimed)",
                        "plan_s": round(plan_s, 3)},
             "iters_per_s": iters_s,
+            "per_hop_latency_ns": (1e6 * sw_ms / sw_n / st["max_hops"]) if sw_n else None,
             "lower_bound": {"initial": lb0, "after": lb, "iterations": args.warmup + args.steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "sweep_forward+sweep_backward",

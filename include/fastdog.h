@@ -91,6 +91,9 @@ typedef struct {
   int64_t sweep_smem_per_warp;     /* bytes of shared memory per warp                 */
   int32_t sweep_streaming;         /* 1: passes use the streaming sweep kernel        */
   int64_t h2d_bytes;               /* host->device bytes copied by create             */
+  int32_t fused_small;             /* 1: fdog_iterate runs all its iterations in one
+                                      single-CTA launch (small narrow problems);
+                                      2: same, state resident in shared memory         */
 } fdog_stats_t;
 
 typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */

@@ -757,13 +757,19 @@ __device__ __forceinline__ void ell_store(T *out, int2 p, T x, T y) {
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
+// load through the read-only path (kernel-lifetime constant data) or a plain
+// load (data written earlier in the same kernel: the fused small-problem path)
+template <bool NC, typename V>
+__device__ __forceinline__ V ld(const V *p) {
+  if (NC) return __ldg(p);
+  return *p;
+}
+
+// NC: delta_bar is read-only for the kernel's lifetime (the standalone kernel)
+template <typename T, bool NC>
+__device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  pdl_wait();
-  if (tid == 0) *a.tile_counter = 0u;
   // ELL part: four variables per thread (tid, tid + N, tid + 2N, tid + 3N, so
   // every load of a warp stays coalesced), all eight gathers issued before use
   const int n_ell_thr = (((a.n_ell + 3) >> 2) + 31) & ~31;  // whole warps
@@ -777,8 +783,8 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
     T x[4], y[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      x[u] = p[u].x >= 0 ? __ldg(db + p[u].x) : T(0);
-      y[u] = p[u].y >= 0 ? __ldg(db + p[u].y) : T(0);
+      x[u] = p[u].x >= 0 ? ld<NC>(db + p[u].x) : T(0);
+      y[u] = p[u].y >= 0 ? ld<NC>(db + p[u].y) : T(0);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) ell_store(out, p[u], x[u], y[u]);
@@ -791,8 +797,8 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
     const int q = tid - n_ell_thr;
     if (q >= a.n_ell4) return;
     const int4 p = __ldg(a.ell4 + q);
-    const T x0 = __ldg(db + p.x), x1 = __ldg(db + p.y), x2 = __ldg(db + p.z);
-    const T x3 = p.w >= 0 ? __ldg(db + p.w) : T(0);
+    const T x0 = ld<NC>(db + p.x), x1 = ld<NC>(db + p.y), x2 = ld<NC>(db + p.z);
+    const T x3 = p.w >= 0 ? ld<NC>(db + p.w) : T(0);
     T s = x0 + x1;
     s += x2;
     if (p.w >= 0) s += x3;
@@ -816,7 +822,7 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
     p1 = __ldg(a.var_ptr + q + 1);
   }
   T s = T(0);
-  for (int64_t p = p0 + j; p < p1; p += G) s += __ldg(db + __ldg(a.var_slots + p));
+  for (int64_t p = p0 + j; p < p1; p += G) s += ld<NC>(db + __ldg(a.var_slots + p));
   // the group is G consecutive lanes of one warp (G divides 32, threads of
   // the CSR part start at a multiple of 32: n_ell_thr is rounded up)
   for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
@@ -828,6 +834,96 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
   }
   const T v = s / T(__ldg(a.deg_l + q));
   for (int64_t p = p0 + j; p < p1; p += G) out[__ldg(a.var_slots + p)] = v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
+  if (tid == 0) *a.tile_counter = 0u;
+  avg_body<T, true>(a, tid);
+}
+
+// threads the averaging needs (whole warps per section)
+__host__ __device__ __forceinline__ int64_t avg_threads(const AvgArgs &a) {
+  return (int64_t)((((a.n_ell + 3) / 4) + 31) & ~31) + (int64_t)((a.n_ell4 + 31) & ~31) + (int64_t)a.n * a.group;
+}
+
+// ---------------------------------------------------------------------------
+// Small problems (every tile narrow, few tiles): one CTA runs n iterations in a
+// single launch -- averaging and sweep phases separated by __syncthreads
+// instead of kernel boundaries (latency path, e.g. BASELINE configs[0]).
+// Same device code as the standalone kernels; data stays in global memory
+// (L1/L2 resident at these sizes).  cur0 = parity of delta_bar on entry.
+template <typename T, bool REC>
+__global__ void __launch_bounds__(1024) fused_small_kernel(const SweepArgs sa, const AvgArgs aa, int32_t n_iter,
+                                                           int64_t n_slots, int64_t n_dist, int32_t resident) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T *const g_dbar = const_cast<T *>(reinterpret_cast<const T *>(aa.delta_bar));  // delta[cur] on entry
+  T *const g_va = reinterpret_cast<T *>(aa.avg_slot);
+  T *const g_lambda = reinterpret_cast<T *>(sa.lambda);
+  T *const g_dist = reinterpret_cast<T *>(sa.dist);
+  T *dbar = g_dbar, *va_all = g_va, *lambda = g_lambda, *gdist = g_dist;
+  const T omega = T(sa.omega), clamp = T(sa.clamp);
+  extern __shared__ __align__(16) unsigned char fsm[];
+  pdl_wait();
+  if (resident) {
+    // the whole mutable state (lambda, both delta buffers, distances) fits in
+    // shared memory: same absolute indices, shared-memory latency per hop
+    T *sl = reinterpret_cast<T *>(fsm), *s0 = sl + n_slots, *s1 = s0 + n_slots, *sd = s1 + n_slots;
+    for (int64_t i = threadIdx.x; i < n_slots; i += blockDim.x) {
+      sl[i] = g_lambda[i];
+      s0[i] = g_dbar[i];
+      s1[i] = g_va[i];
+    }
+    for (int64_t i = threadIdx.x; i < n_dist; i += blockDim.x) sd[i] = g_dist[i];
+    __syncthreads();
+    lambda = sl;
+    dbar = s0;
+    va_all = s1;
+    gdist = sd;
+  }
+  const int64_t na = avg_threads(aa);
+  for (int it = 0; it < 2 * n_iter; ++it) {
+    AvgArgs a = aa;
+    a.delta_bar = dbar;
+    a.avg_slot = va_all;
+    for (int64_t base = 0; base < na; base += blockDim.x) avg_body<T, false>(a, (int)(base + threadIdx.x));
+    __syncthreads();
+    for (int t = warp; t < sa.n_tiles; t += nw) {
+      const TileDesc d = sa.tiles[t];
+      const int L = d.lanes;
+      const bool valid = lane < d.n_lanes;
+      double acc = 0.0;
+      if (lane < L) {
+        const int64_t sb = d.slot_base + lane;
+        const uint32_t *tp = (d.kind & 1) ? sa.topo + d.topo_base + lane : sa.topo + d.topo_base;
+        const int ts = (d.kind & 1) ? L : 1;
+        T *m0p = REC ? reinterpret_cast<T *>(sa.m0) + sb : nullptr;
+        T *m1p = REC ? reinterpret_cast<T *>(sa.m1) + sb : nullptr;
+        if (it % 2 == 0)
+          acc = process_bdd_w2<T, kForward, REC, 0>(d.K, sa.hop_off + d.hop_base, tp, ts, L, lambda + sb, va_all + sb,
+                                                    gdist + d.dist_base + lane, valid, omega, clamp, m0p, m1p);
+        else
+          acc = process_bdd_w2<T, kBackward, REC, 0>(d.K, sa.hop_off + d.hop_base, tp, ts, L, lambda + sb, va_all + sb,
+                                                     gdist + d.dist_base + lane, valid, omega, clamp, m0p, m1p);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) sa.lb_part[t] = acc;
+    }
+    __syncthreads();
+    T *const t = dbar;  // mbar <- m
+    dbar = va_all;
+    va_all = t;
+  }
+  if (resident) {  // an even number of swaps: dbar / va_all are s0 / s1 again
+    for (int64_t i = threadIdx.x; i < n_slots; i += blockDim.x) {
+      g_lambda[i] = lambda[i];
+      g_dbar[i] = dbar[i];
+      g_va[i] = va_all[i];
+    }
+    for (int64_t i = threadIdx.x; i < n_dist; i += blockDim.x) g_dist[i] = gdist[i];
+  }
 }
 
 // Shared variables after the NCCL exchange: average and scatter into the local slots.
@@ -992,8 +1088,7 @@ static int grid_for(int64_t n, int block) {
 
 int launch_avg(int precision, const AvgArgs &a, void *stream) {
   const int block = 256;
-  const int64_t threads = (int64_t)((((a.n_ell + 3) / 4) + 31) & ~31) + (int64_t)((a.n_ell4 + 31) & ~31) +
-                          (int64_t)a.n * a.group;
+  const int64_t threads = avg_threads(a);
   const int grid = (int)std::max<int64_t>(1, (threads + block - 1) / block);
   void *args[] = {(void *)&a};
   const void *f = precision == 64 ? (const void *)avg_kernel<double> : (const void *)avg_kernel<float>;
@@ -1030,6 +1125,19 @@ int launch_primal(int precision, const PrimalArgs &a, void *stream) {
   else
     primal_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(a);
   return (int)cudaGetLastError();
+}
+
+int launch_fused_small(int precision, bool rec, const SweepArgs &sa, const AvgArgs &aa, int32_t n_iter,
+                       int64_t n_slots, int64_t n_dist, size_t smem, void *stream) {
+  int32_t resident = smem > 0 ? 1 : 0;
+  void *args[] = {(void *)&sa, (void *)&aa, (void *)&n_iter, (void *)&n_slots, (void *)&n_dist, (void *)&resident};
+  const void *f = precision == 64 ? (rec ? (const void *)fused_small_kernel<double, true> : (const void *)fused_small_kernel<double, false>)
+                                  : (rec ? (const void *)fused_small_kernel<float, true> : (const void *)fused_small_kernel<float, false>);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return launch_pdl(f, dim3(1), dim3(1024), smem, stream, args);
 }
 
 int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream) {

@@ -126,6 +126,8 @@ struct fdog_solver {
   int graph_cur = -1;
   int64_t graph_launches = 0;
   bool use_graphs = true;
+  bool use_fused = false;  // small problems: all iterations in one single-CTA launch
+  size_t fused_smem = 0;   // > 0: its state is shared-memory resident
 
   Nccl nccl;
   std::vector<EventRec> events;
@@ -180,7 +182,29 @@ struct Timed {
   }
 };
 
+SweepArgs sweep_args(fdog_solver *s, double omega);
+
 fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
+  SweepArgs a = sweep_args(s, omega);
+  const bool rec = s->record_mm && (mode == kForward || mode == kBackward);
+  int e;
+  if (mode != kForward && mode != kBackward) {
+    // not preceded by avg_kernel: reset the dynamic tile counter here
+    CK(cudaMemsetAsync(s->d_counter + 1, 0, sizeof(unsigned int), s->stream), "memset");
+  }
+  {
+    Timed t(s, mode == kForward ? kKSweepFwd : mode == kBackward ? kKSweepBwd : kKEnergy);
+    if (s->stream_mode && (mode == kForward || mode == kBackward))
+      e = launch_sweep_stream(s->precision, mode, rec, a, s->stream);
+    else
+      e = launch_sweep(s->precision, mode, rec, a, s->grid, s->block, s->smem, s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "sweep launch");
+  s->lb_dirty = true;
+  return FDOG_OK;
+}
+
+SweepArgs sweep_args(fdog_solver *s, double omega) {
   SweepArgs a{};
   a.tiles = s->d_tiles;
   a.n_tiles = s->n_tiles;
@@ -204,24 +228,7 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   a.NB = s->NB;
   a.dist = s->d_dist;
   a.static_sched = s->static_sched;
-  a.scratch = s->d_scratch;
-  a.scratch_stride = s->scratch_stride;
-  const bool rec = s->record_mm && (mode == kForward || mode == kBackward);
-  int e;
-  if (mode != kForward && mode != kBackward) {
-    // not preceded by avg_kernel: reset the dynamic tile counter here
-    CK(cudaMemsetAsync(s->d_counter + 1, 0, sizeof(unsigned int), s->stream), "memset");
-  }
-  {
-    Timed t(s, mode == kForward ? kKSweepFwd : mode == kBackward ? kKSweepBwd : kKEnergy);
-    if (s->stream_mode && (mode == kForward || mode == kBackward))
-      e = launch_sweep_stream(s->precision, mode, rec, a, s->stream);
-    else
-      e = launch_sweep(s->precision, mode, rec, a, s->grid, s->block, s->smem, s->stream);
-  }
-  if (e) return cuda_fail((cudaError_t)e, "sweep launch");
-  s->lb_dirty = true;
-  return FDOG_OK;
+  return a;
 }
 
 AvgArgs avg_args(fdog_solver *s);
@@ -473,6 +480,14 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     const char *m = getenv("FDOG_SWEEP");  // experiment knob: "tma" or "stream"
     const bool forced = m && (m[0] == 's' || m[0] == 't');
     s->stream_mode = narrow && (forced ? m[0] == 's' : !staged_ok);
+    // tiny instances (BASELINE configs[0]) are launch-latency bound: one CTA
+    // runs every iteration of an fdog_iterate call (fused_small_kernel)
+    const char *fz = getenv("FDOG_FUSED");  // experiment knob: 0 / 1
+    const bool small = tiles.size() <= 64 && P.n_slots <= (1 << 15);
+    s->use_fused = narrow && P.world == 1 && (fz ? fz[0] == '1' : small);
+    const size_t fbytes = (size_t)(3 * (int64_t)P.slot_var.size() + P.n_dist) * s->tsz;
+    const char *fr = getenv("FDOG_FUSED_SMEM");  // experiment knob: 0 keeps the state in global memory
+    s->fused_smem = (fbytes <= (size_t)prop.smem_block && !(fr && fr[0] == '0')) ? fbytes : 0;
     if (m && m[0] == 's' && !narrow) {
       set_error("FDOG_SWEEP=stream needs every partition <= 2 nodes wide");
       return FDOG_EINVAL;
@@ -617,6 +632,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->st.sweep_smem_per_warp = (int64_t)s->warp_bytes;
   s->st.sweep_streaming = s->stream_mode ? 1 : 0;
   s->st.h2d_bytes = s->upload_bytes;
+  s->st.fused_small = s->use_fused ? (s->fused_smem ? 2 : 1) : 0;
 
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;
@@ -946,6 +962,18 @@ fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
   if (!(omega > 0.0 && omega <= 1.0)) {
     set_error("omega %g outside (0, 1]", omega);
     return FDOG_EINVAL;
+  }
+  if (s->use_fused && !s->profile && s->world == 1 && s->dist_state == 0 && n_iter > 0) {
+    // 2 n_iter passes in one launch; delta_bar ends in the same buffer
+    const SweepArgs sa = sweep_args(s, omega);
+    const AvgArgs aa = avg_args(s);
+    const int e = launch_fused_small(s->precision, s->record_mm, sa, aa, n_iter, s->n_dev_slots, s->n_dist,
+                                     s->fused_smem, s->stream);
+    if (e) return cuda_fail((cudaError_t)e, "fused launch");
+    s->launches += 1;
+    s->passes += 2 * (int64_t)n_iter;
+    s->lb_dirty = true;
+    return FDOG_OK;
   }
   // CUDA graph of one iteration: used when the passes alternate normally, no
   // per-kernel events are requested and there is no NCCL exchange

@@ -214,6 +214,7 @@ def test_graph_replay_matches_direct_launches(monkeypatch):
     """fdog_iterate's CUDA-graph replay gives bit-identical results to launching
     the kernels one by one (same kernels, same order, deterministic reductions)."""
     p = synth.gm_worms_like(9, n_src=60, k_cand=6, knn=6)
+    monkeypatch.setenv("FDOG_FUSED", "0")
     monkeypatch.setenv("FDOG_GRAPHS", "1")
     g1 = F.Solver(p, precision=32)
     monkeypatch.setenv("FDOG_GRAPHS", "0")
@@ -228,6 +229,48 @@ def test_graph_replay_matches_direct_launches(monkeypatch):
     g1.iterate(1, 0.5); g2.iterate(1, 0.5)
     assert np.array_equal(g1.lam(), g2.lam())
     assert "sweep_forward" in g1.profile()
+
+
+@pytest.mark.parametrize("resident", ["0", "1"])
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("name,make", [
+    ("lap", lambda: synth.lap(synth.LAP4_LITERAL)),
+    ("lap_random", lambda: synth.lap_random(9, 5)),
+    ("gm", lambda: synth.gm_worms_like(21, n_src=50, k_cand=5, knn=6)),
+    ("mrf", lambda: synth.mrf_potts(21, H=7, W=9, L=3)),
+    ("ct", lambda: synth.celltrack(21, frames=3, dets=30)),
+])
+def test_fused_small_path(oracle_mod, monkeypatch, resident, precision, name, make):
+    """Small narrow problems run every iteration of fdog_iterate in one
+    single-CTA launch (fused_small_kernel; state in global memory, or copied
+    into shared memory when it fits).  Same arithmetic as the per-pass
+    kernels: bit-identical lambda, delta_bar, min-marginals and bound, and the
+    oracle's iterates within the fp64 tolerance."""
+    p = make()
+    monkeypatch.setenv("FDOG_FUSED_SMEM", resident)
+    monkeypatch.setenv("FDOG_FUSED", "1")
+    gf = F.Solver(p, precision=precision, record_mm=True)
+    monkeypatch.setenv("FDOG_FUSED", "0")
+    gd = F.Solver(p, precision=precision, record_mm=True)
+    assert gf.stats()["fused_small"] >= 1 and gd.stats()["fused_small"] == 0
+    if resident == "0":
+        assert gf.stats()["fused_small"] == 1
+    o = oracle_mod.Oracle(p)
+    for n, om in ((1, 0.5), (3, 0.3), (2, 0.5)):
+        l0 = gf.stats()["launches"]
+        gf.iterate(n, om); gd.iterate(n, om); o.iterate(n, om)
+        assert gf.stats()["launches"] == l0 + 1
+        assert np.array_equal(gf.lam(), gd.lam()) and np.array_equal(gf.deferred(), gd.deferred())
+        m_f, m_d = gf.min_marginals(), gd.min_marginals()
+        assert np.array_equal(m_f[0], m_d[0]) and np.array_equal(m_f[1], m_d[1])
+        assert gf.lower_bound() == gd.lower_bound()
+    if precision == 64:
+        s = _s(p)
+        assert np.max(np.abs(gf.lam() - o.lam())) <= 1e-9 * s * 10
+        assert abs(gf.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+    gf.pass_(True, 0.5); gd.pass_(True, 0.5)      # odd parity, then fused again
+    gf.iterate(2, 0.5); gd.iterate(2, 0.5)
+    assert np.array_equal(gf.lam(), gd.lam()) and gf.lower_bound() == gd.lower_bound()
 
 
 @pytest.mark.parametrize("mode", ["tma", "stream"])
