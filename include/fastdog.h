@@ -94,6 +94,8 @@ typedef struct {
   int32_t fused_small;             /* 1: fdog_iterate runs all its iterations in one
                                       single-CTA launch (small narrow problems);
                                       2: same, state resident in shared memory         */
+  int32_t sweep_recompute;         /* 1: the passes recompute the opposite-direction
+                                      distances on chip (no per-node HBM traffic)     */
 } fdog_stats_t;
 
 typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */

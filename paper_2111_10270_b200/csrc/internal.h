@@ -40,6 +40,10 @@ struct Shape {
 //          with (bottom, bottom) nodes;
 //   kind bit 1 set: staged through shared memory by TMA (fits the per-warp
 //          budget); clear: processed from global memory (L = 32).
+//   kind bit 2 set ("arc-mask tile", staged shared-topology tiles of shapes
+//          whose partitions have <= 2 nodes): the stage holds the shape's hop
+//          records (HopRec, at recs + 16 * rec_base) instead of topology and
+//          partition offsets; the sweeps use the branch-free min-plus form.
 // Topology entries are absolute child indices within the tile (s^0 in the low
 // 16 bits, s^1 in the high 16 bits), top = nodes, bottom = nodes + 1.
 // Partition offsets of the tile: hop_off[hop_base + h], h = 0..K.
@@ -55,7 +59,8 @@ struct TileDesc {
   int32_t nodes;    // nodes per lane (hop_off[hop_base + K])
   int32_t max_w;    // widest partition of the tile
   int32_t lanes;    // L
-  int32_t pad_[3];  // 64 bytes: fetched as four 16-byte cp.async chunks
+  int32_t rec_base; // kind bit 2: first hop record, in 16-byte units of Plan::recs
+  int32_t pad_[2];  // 64 bytes: fetched as four 16-byte cp.async chunks
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc layout");
 
@@ -72,15 +77,35 @@ static_assert(sizeof(TileDesc) == 64, "TileDesc layout");
 //                             topology | partition offsets
 //   [256 + SB, 256 + 2 SB)    stage buffer 1 (NB = 2 only)
 //   [256 + NB SB, + DB)       relaxation buffers R[3 (W + 1)][L]
+// Recompute design (Plan::rc, narrow tiles only): the stage buffers hold no
+// distances (lambda | avg->delta | topology | partition offsets), and the DB
+// region is the lane-private distance scratch D[nodes + 2][L].
 FDOG_HD int r16(int bytes) { return (bytes + 15) & ~15; }
 FDOG_HD int stage_lam_bytes(int tsz, int K, int L) { return r16(K * L * tsz); }
 FDOG_HD int stage_va_bytes(int tsz, int K, int L) { return r16(K * L * tsz); }
 FDOG_HD int stage_dist_bytes(int tsz, int nodes, int L) { return r16((nodes + 2) * L * tsz); }
 FDOG_HD int stage_topo_bytes(int kind, int nodes, int L) { return r16(((kind & 1) ? nodes * L : nodes) * 4); }
 FDOG_HD int stage_hop_bytes(int K) { return r16((K + 1) * 4); }
+// Hop record of an arc-mask tile (one per partition P_h of a shape whose
+// partitions have <= 2 nodes), T = build precision:
+//   A[0..3]  0-arc masks, A[4..7] 1-arc masks, entry 2 i + j = 0 if the arc
+//            out of node i of P_h ends in node j of P_{h+1}, else +inf.  For
+//            the last partition, j = 0 is the terminal top (bottom is never a
+//            target: arcs to bottom are +inf in every column);
+//   n0, n1   first node of P_h and of P_{h+1} (n1 = nodes = top on the last
+//            partition), so D[n1 + j] is the distance of target j -- on the
+//            last partition the sentinels (0 for top, +inf).
+//   w2       1 if P_h has two nodes.
+FDOG_HD int rec_bytes(int tsz) { return 8 * tsz + 16; }
+FDOG_HD int stage_tail_bytes(int tsz, int kind, int K, int nodes, int L) {
+  return (kind & 4) ? r16(K * rec_bytes(tsz)) : stage_topo_bytes(kind, nodes, L) + stage_hop_bytes(K);
+}
 FDOG_HD int stage_bytes(int tsz, int kind, int K, int nodes, int L) {
-  return stage_lam_bytes(tsz, K, L) + stage_va_bytes(tsz, K, L) +
-         stage_dist_bytes(tsz, nodes, L) + stage_topo_bytes(kind, nodes, L) + stage_hop_bytes(K);
+  return stage_lam_bytes(tsz, K, L) + stage_va_bytes(tsz, K, L) + stage_dist_bytes(tsz, nodes, L) +
+         stage_tail_bytes(tsz, kind, K, nodes, L);
+}
+FDOG_HD int stage_bytes_rc(int tsz, int kind, int K, int nodes, int L) {
+  return stage_lam_bytes(tsz, K, L) + stage_va_bytes(tsz, K, L) + stage_tail_bytes(tsz, kind, K, nodes, L);
 }
 FDOG_HD int relax_slots(int W) { return 3 * (W + 1); }
 FDOG_HD int relax_bytes(int tsz, int W, int L) { return r16(relax_slots(W) * L * tsz); }
@@ -92,7 +117,7 @@ FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (kWarpHeader + NB * SB +
 // creating a solver is one allocation and one host->device copy.
 enum ImageSection {
   kImTiles = 0, kImHopOff, kImTopo, kImSlotVar, kImVarPtr, kImVarSlots, kImVarXidx, kImDegList, kImEll, kImEllVar,
-  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImCount
+  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImRecs, kImCount
 };
 
 struct HostImage {
@@ -123,6 +148,7 @@ struct Plan {
   std::vector<TileDesc> tiles;
   std::vector<int32_t> hop_off;
   std::vector<uint32_t> topo;       // lo | hi << 16
+  std::vector<unsigned char> recs;  // hop records of arc-mask shapes (build precision, 16-byte units)
   std::vector<int32_t> slot_var;    // padded device slots: variable or -1
   std::vector<int64_t> canon_slot;  // canonical local slot -> device slot
   std::vector<int32_t> canon_con, canon_pos;
@@ -145,6 +171,7 @@ struct Plan {
 
   // per-warp shared-memory budget the tiles were packed for (precision-specific)
   int32_t precision = 32, SB = 0, DB = 0, NB = 2;
+  bool rc = false;                  // recompute design: tiles packed for sweep_kernel<..., RC>
   int64_t n_dist = 0;               // elements of the distance array
   int64_t direct_tiles = 0;
 
@@ -169,6 +196,7 @@ struct SweepArgs {
   int32_t n_tiles;
   const int32_t *hop_off;
   const uint32_t *topo;
+  const unsigned char *recs;  // hop records of arc-mask tiles
   const int32_t *slot_var;
   void *lambda;          // T*
   void *delta_out;       // T*: per slot avg_i in, delta out (in place)
@@ -222,10 +250,11 @@ struct PrimalArgs {
 };
 
 // returns the cudaError_t as int
-int launch_sweep(int precision, int mode, bool record, const SweepArgs &a, int grid, int block,
+// rc: recompute design (sweep_kernel<..., RC = true>; plan packed with Plan::rc)
+int launch_sweep(int precision, int mode, bool record, bool rc, const SweepArgs &a, int grid, int block,
                  size_t smem, void *stream);
 int launch_sweep_stream(int precision, int mode, bool record, const SweepArgs &a, void *stream);
-int sweep_occupancy(int precision, int mode, bool record, int block, size_t smem, int *blocks_per_sm);
+int sweep_occupancy(int precision, int mode, bool record, bool rc, int block, size_t smem, int *blocks_per_sm);
 int launch_avg(int precision, const AvgArgs &a, void *stream);
 int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,
                       void *stream);

@@ -395,6 +395,340 @@ __device__ __forceinline__ double process_bdd_w2(const int K, const int32_t *ho,
   return acc;
 }
 
+// successor value: top, bottom, or a node of the next partition (held in
+// registers).  The sentinels are tested first: on the last partition
+// n1 == nodes == top.
+template <typename T>
+__device__ __forceinline__ T succ(int code, int n1, int top, T v0, T v1) {
+  const T inf = t_inf<T>();
+  return code == top ? T(0) : code > top ? inf : code == n1 ? v0 : code == n1 + 1 ? v1 : inf;
+}
+
+// Recompute design, narrow tiles (every partition <= 2 nodes).
+// The distances of the opposite direction are not kept in HBM: phase 1
+// recomputes them on chip from the current lambda -- shp(v, T) for a forward
+// pass, shp(r, v) for a backward pass -- into the
+// lane's column of the per-warp scratch D (two sentinel slots: D[top] = 0,
+// D[bottom] = +inf).  Because lambda has not changed since the previous pass
+// computed them, they are bit-identical to the stored distances of P:315-316.
+// Phase 2 is the pass with updates; its own-direction distances
+// are carried in registers.  HBM traffic per pass: lambda read + write, the
+// average read, delta write -- nothing per node.
+template <typename T, int MODE, bool REC, int LC>
+__device__ __forceinline__ double process_rc_w2(const int K, const int top, const int32_t *ho, const uint32_t *tp,
+                                                const int ts_rt, const int L_rt, T *lam, T *va, T *D,
+                                                const bool valid, const T omega, const T clamp, T *m0g, T *m1g) {
+  const int L = LC ? LC : L_rt;
+  const int ts = LC ? 1 : ts_rt;
+  const T inf = t_inf<T>();
+  double acc = 0.0;
+  auto finish = [&](int h, T l, T m0, T m1r) -> T {
+    const T m1 = l + m1r;
+    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+    const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
+    if (valid) {
+      lam[h * L] = lam_new;
+      va[h * L] = delta;
+      if (REC) {
+        m0g[h * L] = m0;
+        m1g[h * L] = m1;
+      }
+      acc += (double)fmin(delta, T(0));
+    } else {
+      va[h * L] = T(0);
+    }
+    return lam_new;
+  };
+  if (MODE == kForward) {
+    {  // phase 1: shp(v, T) for every node under the current lambda
+      T x0 = inf, x1 = inf;  // shp(., T) of P_{h+1}
+#pragma unroll 1
+      for (int h = K - 1; h >= 0; --h) {
+        const int n0 = ho[h], n1 = ho[h + 1];
+        const uint32_t e0 = tp[n0 * ts];
+        const T l = lam[h * L];
+        const T ct0 = fmin(succ((int)(e0 & 0xFFFFu), n1, top, x0, x1), l + succ((int)(e0 >> 16), n1, top, x0, x1));
+        T ct1 = inf;
+        if (n1 - n0 > 1) {
+          const uint32_t e1 = tp[(n0 + 1) * ts];
+          ct1 = fmin(succ((int)(e1 & 0xFFFFu), n1, top, x0, x1), l + succ((int)(e1 >> 16), n1, top, x0, x1));
+          D[(n0 + 1) * L] = ct1;
+        }
+        D[n0 * L] = ct0;
+        x0 = ct0;
+        x1 = ct1;
+      }
+    }
+    // phase 2: forward pass with updates; shp(r, .) of P_h in registers
+    T c0 = T(0), c1 = inf;
+    int n0 = ho[0];
+#pragma unroll 1
+    for (int h = 0; h < K; ++h) {
+      const int n1 = ho[h + 1];
+      const uint32_t e0 = tp[n0 * ts];
+      const int lo0 = (int)(e0 & 0xFFFFu), hi0 = (int)(e0 >> 16);
+      T m0 = c0 + D[lo0 * L], m1r = c0 + D[hi0 * L];
+      T nl0 = lo0 == n1 ? c0 : inf, nl1 = lo0 == n1 + 1 ? c0 : inf;
+      T nh0 = hi0 == n1 ? c0 : inf, nh1 = hi0 == n1 + 1 ? c0 : inf;
+      if (n1 - n0 > 1) {
+        const uint32_t e1 = tp[(n0 + 1) * ts];
+        const int lo1 = (int)(e1 & 0xFFFFu), hi1 = (int)(e1 >> 16);
+        m0 = fmin(m0, c1 + D[lo1 * L]);
+        m1r = fmin(m1r, c1 + D[hi1 * L]);
+        if (lo1 == n1) nl0 = fmin(nl0, c1);
+        if (lo1 == n1 + 1) nl1 = fmin(nl1, c1);
+        if (hi1 == n1) nh0 = fmin(nh0, c1);
+        if (hi1 == n1 + 1) nh1 = fmin(nh1, c1);
+      }
+      const T lam_new = finish(h, lam[h * L], m0, m1r);
+      if (h == K - 1) {
+        if (valid) acc += (double)fmin(m0, lam_new + m1r);  // E^j at the updated lambda
+      } else {
+        c0 = fmin(nl0, nh0 + lam_new);  // A4: 1-arcs priced with the updated lambda_h
+        c1 = fmin(nl1, nh1 + lam_new);
+      }
+      n0 = n1;
+    }
+    return acc;
+  }
+  // kBackward.  Phase 1: shp(r, v) for every node under the current lambda
+  // (P:319-324, 1-arcs out of P_h priced with lambda_h, reading A4).
+  {
+    T c0 = T(0), c1 = inf;
+    int n0 = ho[0];
+#pragma unroll 1
+    for (int h = 0; h < K - 1; ++h) {
+      const int n1 = ho[h + 1];
+      const uint32_t e0 = tp[n0 * ts];
+      const int lo0 = (int)(e0 & 0xFFFFu), hi0 = (int)(e0 >> 16);
+      D[n0 * L] = c0;
+      T nl0 = lo0 == n1 ? c0 : inf, nl1 = lo0 == n1 + 1 ? c0 : inf;
+      T nh0 = hi0 == n1 ? c0 : inf, nh1 = hi0 == n1 + 1 ? c0 : inf;
+      if (n1 - n0 > 1) {
+        const uint32_t e1 = tp[(n0 + 1) * ts];
+        const int lo1 = (int)(e1 & 0xFFFFu), hi1 = (int)(e1 >> 16);
+        D[(n0 + 1) * L] = c1;
+        if (lo1 == n1) nl0 = fmin(nl0, c1);
+        if (lo1 == n1 + 1) nl1 = fmin(nl1, c1);
+        if (hi1 == n1) nh0 = fmin(nh0, c1);
+        if (hi1 == n1 + 1) nh1 = fmin(nh1, c1);
+      }
+      const T l = lam[h * L];
+      c0 = fmin(nl0, nh0 + l);
+      c1 = fmin(nl1, nh1 + l);
+      n0 = n1;
+    }
+    D[n0 * L] = c0;
+    if (ho[K] - n0 > 1) D[(n0 + 1) * L] = c1;
+  }
+  // phase 2: backward pass with updates; shp(., T) of P_{h+1} in registers
+  T ct0 = inf, ct1 = inf;
+#pragma unroll 1
+  for (int h = K - 1; h >= 0; --h) {
+    const int n0 = ho[h], n1 = ho[h + 1];
+    const uint32_t e0 = tp[n0 * ts];
+    const bool two = n1 - n0 > 1;
+    const T f0 = D[n0 * L];
+    const T a0 = succ((int)(e0 & 0xFFFFu), n1, top, ct0, ct1), b0 = succ((int)(e0 >> 16), n1, top, ct0, ct1);
+    T m0 = f0 + a0, m1r = f0 + b0;
+    T a1 = inf, b1 = inf;
+    if (two) {
+      const uint32_t e1 = tp[(n0 + 1) * ts];
+      const T f1 = D[(n0 + 1) * L];
+      a1 = succ((int)(e1 & 0xFFFFu), n1, top, ct0, ct1);
+      b1 = succ((int)(e1 >> 16), n1, top, ct0, ct1);
+      m0 = fmin(m0, f1 + a1);
+      m1r = fmin(m1r, f1 + b1);
+    }
+    const T lam_new = finish(h, lam[h * L], m0, m1r);
+    ct0 = fmin(a0, lam_new + b0);  // shp(v, T) with the updated lambda_h
+    ct1 = two ? fmin(a1, lam_new + b1) : inf;
+  }
+  if (valid) acc += (double)ct0;  // E^j = shp(r, T)
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
+// Arc-mask form of a narrow hop (tiles with kind bit 2; HopRec in internal.h).
+// With the 0/+inf arc masks A of partition P_h, the hop is branch-free
+// min-plus arithmetic over the (up to) two nodes i of P_h and the two targets
+// j of P_{h+1} (or top on the last partition):
+//   a_i = min_j (A0[i][j] + x_j),  b_i = min_j (A1[i][j] + x_j)
+//     (x = shp(., T) of P_{h+1}: the distance of node i's 0-/1-successor),
+//   m^0 = min_i (c_i + a_i),  m^1 = lambda_h + min_i (c_i + b_i),
+//   shp(v_i, T) = min(a_i, lambda_h + b_i),
+//   shp(r, v_j) = min_i min(c_i + A0[i][j], lambda_h + (c_i + A1[i][j])) (A4),
+// with c = shp(r, .) of P_h.  Adding a 0 mask is exact and +inf masks
+// absorb, so every value is bit-identical to the topology-walking form
+// (process_bdd_w2).  The loops prefetch the next partition's record, lambda,
+// average and distances while the current one is computed.
+template <typename T>
+struct __align__(16) HopRec {
+  T A[8];
+  int32_t n0, n1, w2, pad;
+};
+static_assert(sizeof(HopRec<float>) == 48 && sizeof(HopRec<double>) == 80, "HopRec layout (internal.h rec_bytes)");
+
+template <typename T>
+__device__ __forceinline__ void arc_mins(const HopRec<T> &r, T x0, T x1, T &a0, T &a1, T &b0, T &b1) {
+  a0 = fmin(r.A[0] + x0, r.A[1] + x1);
+  a1 = fmin(r.A[2] + x0, r.A[3] + x1);
+  b0 = fmin(r.A[4] + x0, r.A[5] + x1);
+  b1 = fmin(r.A[6] + x0, r.A[7] + x1);
+}
+template <typename T>
+__device__ __forceinline__ void arc_relax(const HopRec<T> &r, T c0, T c1, T lam, T &o0, T &o1) {
+  o0 = fmin(fmin(c0 + r.A[0], c1 + r.A[2]), lam + fmin(c0 + r.A[4], c1 + r.A[6]));
+  o1 = fmin(fmin(c0 + r.A[1], c1 + r.A[3]), lam + fmin(c0 + r.A[5], c1 + r.A[7]));
+}
+
+// dual update of one slot (A5, A10); returns the new lambda_h
+template <typename T, bool REC>
+__device__ __forceinline__ T mask_finish(T *lam, T *va, int hL, T l, T av, T m0, T m1r, bool valid, T omega, T clamp,
+                                         T *m0g, T *m1g, double &acc) {
+  const T m1 = l + m1r;
+  const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+  const T lam_new = add_rn(sub_rn(l, delta), av);
+  if (valid) {
+    lam[hL] = lam_new;
+    va[hL] = delta;
+    if (REC) {
+      m0g[hL] = m0;
+      m1g[hL] = m1;
+    }
+    acc += (double)fmin(delta, T(0));
+  } else {
+    va[hL] = T(0);
+  }
+  return lam_new;
+}
+
+// shp(v, T) of every node under the current lambda (no update); returns
+// shp(r, T) = E^j.  (kEnergy; phase 1 of a recompute forward pass.)
+template <typename T, int LC>
+__device__ __forceinline__ T mask_ctt(const int K, const HopRec<T> *rec, const int L_rt, const T *lam, T *D) {
+  const int L = LC ? LC : L_rt;
+  T x0 = T(0), x1 = t_inf<T>();
+  HopRec<T> r = rec[K - 1];
+  T l = lam[(K - 1) * L];
+#pragma unroll 1
+  for (int h = K - 1; h >= 0; --h) {
+    const int hn = h > 0 ? h - 1 : 0;
+    const HopRec<T> rn = rec[hn];
+    const T ln = lam[hn * L];
+    T a0, a1, b0, b1;
+    arc_mins(r, x0, x1, a0, a1, b0, b1);
+    x0 = fmin(a0, l + b0);
+    x1 = fmin(a1, l + b1);
+    D[r.n0 * L] = x0;
+    if (r.w2) D[(r.n0 + 1) * L] = x1;
+    r = rn;
+    l = ln;
+  }
+  return x0;
+}
+
+// shp(r, v) of every node under the current lambda (no update); returns
+// shp(r, T) = E^j.  (kCfr; phase 1 of a recompute backward pass.)
+template <typename T, int LC>
+__device__ __forceinline__ T mask_cfr(const int K, const HopRec<T> *rec, const int L_rt, const T *lam, T *D) {
+  const int L = LC ? LC : L_rt;
+  T c0 = T(0), c1 = t_inf<T>();
+  HopRec<T> r = rec[0];
+  T l = lam[0];
+#pragma unroll 1
+  for (int h = 0; h < K; ++h) {
+    const int hn = h + 1 < K ? h + 1 : h;
+    const HopRec<T> rn = rec[hn];
+    const T ln = lam[hn * L];
+    D[r.n0 * L] = c0;
+    if (r.w2) D[(r.n0 + 1) * L] = c1;
+    arc_relax(r, c0, c1, l, c0, c1);
+    r = rn;
+    l = ln;
+  }
+  return c0;  // after the last partition: the relaxation into top
+}
+
+// forward pass with updates.  D holds shp(v, T) (stored by the
+// previous backward pass, or recomputed by mask_ctt); STORE: D of P_h is
+// overwritten with shp(r, v) for the next backward pass (P:315-316 reuse).
+template <typename T, bool STORE, bool REC, int LC>
+__device__ __forceinline__ double mask_forward(const int K, const HopRec<T> *rec, const int L_rt, T *lam, T *va,
+                                               T *D, const bool valid, const T omega, const T clamp, T *m0g,
+                                               T *m1g) {
+  const int L = LC ? LC : L_rt;
+  double acc = 0.0;
+  T c0 = T(0), c1 = t_inf<T>();
+  HopRec<T> r = rec[0];
+  T l = lam[0], av = va[0];
+  T x0 = D[r.n1 * L], x1 = D[(r.n1 + 1) * L];
+#pragma unroll 1
+  for (int h = 0; h < K; ++h) {
+    const int hn = h + 1 < K ? h + 1 : h;
+    const HopRec<T> rn = rec[hn];
+    const T ln = lam[hn * L], avn = va[hn * L];
+    const T x0n = D[rn.n1 * L], x1n = D[(rn.n1 + 1) * L];
+    if (STORE) {
+      D[r.n0 * L] = c0;
+      if (r.w2) D[(r.n0 + 1) * L] = c1;
+    }
+    T a0, a1, b0, b1;
+    arc_mins(r, x0, x1, a0, a1, b0, b1);
+    const T m0 = fmin(c0 + a0, c1 + a1);
+    const T m1r = fmin(c0 + b0, c1 + b1);
+    const T lam_new = mask_finish<T, REC>(lam, va, h * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
+    arc_relax(r, c0, c1, lam_new, c0, c1);  // A4: 1-arcs priced with the updated lambda_h
+    r = rn;
+    l = ln;
+    av = avn;
+    x0 = x0n;
+    x1 = x1n;
+  }
+  if (valid) acc += (double)c0;  // E^j = shp(r, T) at the updated lambda
+  return acc;
+}
+
+// backward pass with updates.  D holds shp(r, v) (stored by the
+// forward pass, or recomputed by mask_cfr); STORE: D of P_h is overwritten
+// with shp(v, T) for the next forward pass.
+template <typename T, bool STORE, bool REC, int LC>
+__device__ __forceinline__ double mask_backward(const int K, const HopRec<T> *rec, const int L_rt, T *lam, T *va,
+                                                T *D, const bool valid, const T omega, const T clamp, T *m0g,
+                                                T *m1g) {
+  const int L = LC ? LC : L_rt;
+  double acc = 0.0;
+  T x0 = T(0), x1 = t_inf<T>();  // shp(., T) of P_{h+1}; the last partition's targets: top
+  HopRec<T> r = rec[K - 1];
+  T l = lam[(K - 1) * L], av = va[(K - 1) * L];
+  T f0 = D[r.n0 * L], f1 = D[(r.n0 + 1) * L];
+#pragma unroll 1
+  for (int h = K - 1; h >= 0; --h) {
+    const int hn = h > 0 ? h - 1 : 0;
+    const HopRec<T> rn = rec[hn];
+    const T ln = lam[hn * L], avn = va[hn * L];
+    const T f0n = D[rn.n0 * L], f1n = D[(rn.n0 + 1) * L];
+    T a0, a1, b0, b1;
+    arc_mins(r, x0, x1, a0, a1, b0, b1);
+    const T m0 = fmin(f0 + a0, f1 + a1);
+    const T m1r = fmin(f0 + b0, f1 + b1);
+    const T lam_new = mask_finish<T, REC>(lam, va, h * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
+    x0 = fmin(a0, lam_new + b0);  // shp(v, T) with the updated lambda_h
+    x1 = fmin(a1, lam_new + b1);
+    if (STORE) {
+      D[r.n0 * L] = x0;
+      if (r.w2) D[(r.n0 + 1) * L] = x1;
+    }
+    r = rn;
+    l = ln;
+    av = avn;
+    f0 = f0n;
+    f1 = f1n;
+  }
+  if (valid) acc += (double)x0;  // E^j = shp(r, T)
+  return acc;
+}
+
 // Stage buffer of one tile (layout: internal.h).
 template <typename T>
 struct Stage {
@@ -405,7 +739,8 @@ struct Stage {
   int32_t *hop;
 };
 
-template <typename T>
+// RC: recompute design, no distances in the stage buffer (internal.h)
+template <typename T, bool RC>
 __device__ __forceinline__ Stage<T> stage_at(unsigned char *base, const TileDesc &d) {
   constexpr int tsz = sizeof(T);
   Stage<T> s;
@@ -414,8 +749,8 @@ __device__ __forceinline__ Stage<T> stage_at(unsigned char *base, const TileDesc
   p += stage_lam_bytes(tsz, d.K, d.lanes);
   s.va = reinterpret_cast<T *>(p);
   p += stage_va_bytes(tsz, d.K, d.lanes);
-  s.dist = reinterpret_cast<T *>(p);
-  p += stage_dist_bytes(tsz, d.nodes, d.lanes);
+  s.dist = RC ? nullptr : reinterpret_cast<T *>(p);
+  if (!RC) p += stage_dist_bytes(tsz, d.nodes, d.lanes);
   s.topo = reinterpret_cast<uint32_t *>(p);
   p += stage_topo_bytes(d.kind, d.nodes, d.lanes);
   s.hop = reinterpret_cast<int32_t *>(p);
@@ -424,20 +759,25 @@ __device__ __forceinline__ Stage<T> stage_at(unsigned char *base, const TileDesc
 
 // One lane issues the TMA bulk copies of a tile's lambda, variables, topology
 // and partition offsets; completion is counted on the stage's mbarrier.
-template <typename T, int MODE>
+template <typename T, int MODE, bool RC>
 __device__ __forceinline__ void issue_stage(const SweepArgs &a, const TileDesc &d, const Stage<T> &s, uint64_t *bar) {
   const bool upd = MODE == kForward || MODE == kBackward;
   const uint32_t lam_b = (uint32_t)d.K * d.lanes * sizeof(T);
   const uint32_t va_b = upd ? lam_b : 0u;
-  const uint32_t dist_b = (uint32_t)(d.nodes + 2) * d.lanes * sizeof(T);
-  const uint32_t topo_b = (uint32_t)stage_topo_bytes(d.kind, d.nodes, d.lanes);
-  const uint32_t hop_b = (uint32_t)stage_hop_bytes(d.K);
+  const uint32_t dist_b = RC ? 0u : (uint32_t)(d.nodes + 2) * d.lanes * sizeof(T);
+  const bool masks = d.kind & 4;  // hop records instead of topology + partition offsets
+  const uint32_t topo_b = masks ? (uint32_t)(d.K * rec_bytes((int)sizeof(T))) : (uint32_t)stage_topo_bytes(d.kind, d.nodes, d.lanes);
+  const uint32_t hop_b = masks ? 0u : (uint32_t)stage_hop_bytes(d.K);
   mbar_expect_tx(bar, lam_b + va_b + dist_b + topo_b + hop_b);
   bulk_g2s(s.lam, reinterpret_cast<const T *>(a.lambda) + d.slot_base, lam_b, bar);
   if (va_b) bulk_g2s(s.va, reinterpret_cast<const T *>(a.delta_out) + d.slot_base, va_b, bar);
-  bulk_g2s(s.dist, reinterpret_cast<const T *>(a.dist) + d.dist_base, dist_b, bar);
-  bulk_g2s(s.topo, a.topo + d.topo_base, topo_b, bar);
-  bulk_g2s(s.hop, a.hop_off + d.hop_base, hop_b, bar);
+  if (!RC) bulk_g2s(s.dist, reinterpret_cast<const T *>(a.dist) + d.dist_base, dist_b, bar);
+  if (masks) {
+    bulk_g2s(s.topo, a.recs + 16 * (int64_t)d.rec_base, topo_b, bar);
+  } else {
+    bulk_g2s(s.topo, a.topo + d.topo_base, topo_b, bar);
+    bulk_g2s(s.hop, a.hop_off + d.hop_base, hop_b, bar);
+  }
 }
 
 // One pass over all tiles.  Persistent warps claim tiles dynamically; with
@@ -453,7 +793,10 @@ __device__ __forceinline__ void fetch_desc(TileDesc *dst, const TileDesc *src, i
   cp_async_commit();
 }
 
-template <typename T, int MODE, bool REC>
+// RC: recompute design (narrow tiles, every tile staged): the stage buffers
+// hold lambda, averages, topology and partition offsets only; the distances
+// live in a per-warp scratch column per lane (the DB region) and never touch HBM.
+template <typename T, int MODE, bool REC, bool RC>
 __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   constexpr bool kUpd = MODE == kForward || MODE == kBackward;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -498,7 +841,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   cp_async_wait_all();
   __syncwarp();
   if (t < a.n_tiles && (ring[0].kind & 2) && lane == 0)
-    issue_stage<T, MODE>(a, ring[0], stage_at<T>(sbuf0, ring[0]), &bar[0]);
+    issue_stage<T, MODE, RC>(a, ring[0], stage_at<T, RC>(sbuf0, ring[0]), &bar[0]);
   bool pending = !a.static_sched && tn < a.n_tiles && 2 * W < a.n_tiles;  // a claim is in flight
   int raw_nn = pending ? claim_issue() : 0;
   while (t < a.n_tiles) {
@@ -509,7 +852,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     const int bn = a.NB > 1 ? (b ^ 1) : 0;
     if (a.NB > 1 && has_next && (dn.kind & 2) && lane == 0) {
       bulk_wait_read_all();  // the bulk stores issued from stage bn have read their source
-      issue_stage<T, MODE>(a, dn, stage_at<T>(bn ? sbuf1 : sbuf0, dn), &bar[bn]);
+      issue_stage<T, MODE, RC>(a, dn, stage_at<T, RC>(bn ? sbuf1 : sbuf0, dn), &bar[bn]);
     }
     int tnn = a.n_tiles;
     if (a.static_sched) {
@@ -529,10 +872,83 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     double acc = 0.0;
     if (d.kind & 2) {
       // staged tile: everything on chip
-      const Stage<T> s = stage_at<T>(b ? sbuf1 : sbuf0, d);
+      const Stage<T> s = stage_at<T, RC>(b ? sbuf1 : sbuf0, d);
       mbar_wait(&bar[b], (phase >> b) & 1u);
       phase ^= 1u << b;
-      if (active) {
+      if (d.kind & 4) {
+        // arc-mask tile (narrow shape, shared topology)
+        if (active) {
+          const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(s.topo);
+          T *D = RC ? reinterpret_cast<T *>(rbase) + lane : s.dist + lane;
+          if (RC) {
+            D[d.nodes * L] = T(0);              // top
+            D[(d.nodes + 1) * L] = t_inf<T>();  // bottom
+          }
+          T *m0p = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
+          T *m1p = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
+          T *lm = s.lam + lane, *vp = s.va + lane;
+          if (L == 32) {
+            if (MODE == kEnergy) {
+              const T e = mask_ctt<T, 32>(K, rec, 32, lm, D);
+              acc = valid ? (double)e : 0.0;
+            } else if (MODE == kCfr) {
+              const T e = mask_cfr<T, 32>(K, rec, 32, lm, D);
+              acc = valid ? (double)e : 0.0;
+            } else if (MODE == kForward) {
+              if (RC) mask_ctt<T, 32>(K, rec, 32, lm, D);
+              acc = mask_forward<T, !RC, REC, 32>(K, rec, 32, lm, vp, D, valid, omega, clamp, m0p, m1p);
+            } else {
+              if (RC) mask_cfr<T, 32>(K, rec, 32, lm, D);
+              acc = mask_backward<T, !RC, REC, 32>(K, rec, 32, lm, vp, D, valid, omega, clamp, m0p, m1p);
+            }
+          } else {
+            if (MODE == kEnergy) {
+              const T e = mask_ctt<T, 0>(K, rec, L, lm, D);
+              acc = valid ? (double)e : 0.0;
+            } else if (MODE == kCfr) {
+              const T e = mask_cfr<T, 0>(K, rec, L, lm, D);
+              acc = valid ? (double)e : 0.0;
+            } else if (MODE == kForward) {
+              if (RC) mask_ctt<T, 0>(K, rec, L, lm, D);
+              acc = mask_forward<T, !RC, REC, 0>(K, rec, L, lm, vp, D, valid, omega, clamp, m0p, m1p);
+            } else {
+              if (RC) mask_cfr<T, 0>(K, rec, L, lm, D);
+              acc = mask_backward<T, !RC, REC, 0>(K, rec, L, lm, vp, D, valid, omega, clamp, m0p, m1p);
+            }
+          }
+        }
+      } else if (RC) {
+        if (active) {
+          T *D = reinterpret_cast<T *>(rbase) + lane;  // this lane's distance column
+          D[d.nodes * L] = T(0);                      // top
+          D[(d.nodes + 1) * L] = t_inf<T>();          // bottom
+          const uint32_t *tp = (d.kind & 1) ? s.topo + lane : s.topo;
+          const int ts = (d.kind & 1) ? L : 1;
+          T *m0p = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
+          T *m1p = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
+          if (MODE == kEnergy) {
+            // sum_j E^j(lambda): shp(v, T) under the current lambda
+            const int32_t *ho = s.hop;
+#pragma unroll 1
+            for (int h = K - 1; h >= 0; --h) {
+              const T l = s.lam[h * L + lane];
+              const int n1 = ho[h + 1];
+#pragma unroll 1
+              for (int n = ho[h]; n < n1; ++n) {
+                const uint32_t e = tp[n * ts];
+                D[n * L] = fmin(D[(e & 0xFFFFu) * L], l + D[(e >> 16) * L]);
+              }
+            }
+            acc = valid ? (double)D[0] : 0.0;
+          } else if (L == 32 && !(d.kind & 1)) {
+            acc = process_rc_w2<T, MODE, REC, 32>(K, d.nodes, s.hop, tp, 1, 32, s.lam + lane, s.va + lane, D, valid,
+                                                  omega, clamp, m0p, m1p);
+          } else {
+            acc = process_rc_w2<T, MODE, REC, 0>(K, d.nodes, s.hop, tp, ts, L, s.lam + lane, s.va + lane, D, valid,
+                                                 omega, clamp, m0p, m1p);
+          }
+        }
+      } else if (active) {
         const uint32_t *tp = (d.kind & 1) ? s.topo + lane : s.topo;
         T *R = reinterpret_cast<T *>(rbase) + lane;
         T *m0p = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
@@ -555,7 +971,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
           bulk_s2g(lambda + d.slot_base, s.lam, bytes);
           bulk_s2g(delta_out + d.slot_base, s.va, bytes);
         }
-        bulk_s2g(gdist + d.dist_base, s.dist, (uint32_t)(d.nodes + 2) * L * sizeof(T));
+        if (!RC) bulk_s2g(gdist + d.dist_base, s.dist, (uint32_t)(d.nodes + 2) * L * sizeof(T));
         bulk_commit();
       }
     } else {
@@ -576,7 +992,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     __syncwarp();
     if (a.NB == 1 && has_next && (dn.kind & 2) && lane == 0) {
       bulk_wait_read_all();  // single stage buffer: its stores must have read it
-      issue_stage<T, MODE>(a, dn, stage_at<T>(sbuf0, dn), &bar[0]);
+      issue_stage<T, MODE, RC>(a, dn, stage_at<T, RC>(sbuf0, dn), &bar[0]);
     }
     t = tn;
     tn = tnn;
@@ -628,15 +1044,6 @@ __device__ __forceinline__ void load_hop(HopSet<T> &s, int h, int K, const int32
   }
 }
 
-// successor value: top, bottom, or a node of the next partition (held in
-// registers).  The sentinels are tested first: on the last partition
-// n1 == nodes == top.
-template <typename T>
-__device__ __forceinline__ T succ(int code, int n1, int top, T v0, T v1) {
-  const T inf = t_inf<T>();
-  return code == top ? T(0) : code > top ? inf : code == n1 ? v0 : code == n1 + 1 ? v1 : inf;
-}
-
 template <typename T, int MODE, bool REC>
 __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
   const int lane = threadIdx.x & 31;
@@ -647,7 +1054,24 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
   const bool valid = lane < d.n_lanes;
   double acc = 0.0;
   pdl_wait();
-  if (lane < L) {
+  if ((d.kind & 4) && lane < L) {
+    // arc-mask tile: the same min-plus loops as the staged kernel, on global
+    // memory (records are warp-uniform loads through L1)
+    const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(a.recs + 16 * (int64_t)d.rec_base);
+    T *lam = reinterpret_cast<T *>(a.lambda) + d.slot_base + lane;
+    T *va = reinterpret_cast<T *>(a.delta_out) + d.slot_base + lane;
+    T *D = reinterpret_cast<T *>(a.dist) + d.dist_base + lane;
+    T *m0g = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
+    T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
+    const T omega = T(a.omega), clamp = T(a.clamp);
+    if (L == 32) {
+      acc = MODE == kForward ? mask_forward<T, true, REC, 32>(K, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g)
+                             : mask_backward<T, true, REC, 32>(K, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g);
+    } else {
+      acc = MODE == kForward ? mask_forward<T, true, REC, 0>(K, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g)
+                             : mask_backward<T, true, REC, 0>(K, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g);
+    }
+  } else if (lane < L) {
     const int32_t *ho = a.hop_off + d.hop_base;
     const int ts = (d.kind & 1) ? L : 1;
     const uint32_t *tp = a.topo + d.topo_base + ((d.kind & 1) ? lane : 0);
@@ -1025,20 +1449,24 @@ __global__ void add_deferred_kernel(int64_t n, T *__restrict__ lambda, T *__rest
 
 // ---------------------------------------------------------------- launchers
 
-template <typename T>
+template <typename T, bool RC>
 static const void *sweep_fn(int mode, bool rec) {
-  if (mode == kForward) return rec ? (const void *)sweep_kernel<T, kForward, true> : (const void *)sweep_kernel<T, kForward, false>;
-  if (mode == kBackward) return rec ? (const void *)sweep_kernel<T, kBackward, true> : (const void *)sweep_kernel<T, kBackward, false>;
-  if (mode == kCfr) return (const void *)sweep_kernel<T, kCfr, false>;
-  return (const void *)sweep_kernel<T, kEnergy, false>;
+  if (mode == kForward)
+    return rec ? (const void *)sweep_kernel<T, kForward, true, RC> : (const void *)sweep_kernel<T, kForward, false, RC>;
+  if (mode == kBackward)
+    return rec ? (const void *)sweep_kernel<T, kBackward, true, RC> : (const void *)sweep_kernel<T, kBackward, false, RC>;
+  if (mode == kCfr) return RC ? nullptr : (const void *)sweep_kernel<T, kCfr, false, false>;
+  return (const void *)sweep_kernel<T, kEnergy, false, RC>;
 }
 
-static const void *sweep_ptr(int precision, int mode, bool rec) {
-  return precision == 64 ? sweep_fn<double>(mode, rec) : sweep_fn<float>(mode, rec);
+static const void *sweep_ptr(int precision, int mode, bool rec, bool rc) {
+  if (precision == 64) return rc ? sweep_fn<double, true>(mode, rec) : sweep_fn<double, false>(mode, rec);
+  return rc ? sweep_fn<float, true>(mode, rec) : sweep_fn<float, false>(mode, rec);
 }
 
-int sweep_occupancy(int precision, int mode, bool rec, int block, size_t smem, int *blocks_per_sm) {
-  const void *f = sweep_ptr(precision, mode, rec);
+int sweep_occupancy(int precision, int mode, bool rec, bool rc, int block, size_t smem, int *blocks_per_sm) {
+  const void *f = sweep_ptr(precision, mode, rec, rc);
+  if (!f) return 0;
   cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
@@ -1072,9 +1500,10 @@ int launch_sweep_stream(int precision, int mode, bool rec, const SweepArgs &a, v
   return launch_pdl(f, dim3(grid > 0 ? grid : 1), dim3(128), 0, stream, args);
 }
 
-int launch_sweep(int precision, int mode, bool rec, const SweepArgs &a, int grid, int block, size_t smem,
+int launch_sweep(int precision, int mode, bool rec, bool rc, const SweepArgs &a, int grid, int block, size_t smem,
                  void *stream) {
-  const void *f = sweep_ptr(precision, mode, rec);
+  const void *f = sweep_ptr(precision, mode, rec, rc);
+  if (!f) return (int)cudaErrorInvalidValue;
   void *args[] = {(void *)&a};
   return launch_pdl(f, dim3(grid), dim3(block), smem, stream, args);
 }

@@ -230,6 +230,42 @@ static uint32_t abs_code(uint16_t rel, int32_t next, int32_t nodes) {
   return uint32_t(next + rel);
 }
 
+// Hop records of a shape whose partitions have <= 2 nodes (layout:
+// internal.h HopRec): per partition the 0-/1-arc masks (0 where the arc out of
+// node i of P_h ends in node j of P_{h+1}, or in top on the last partition;
+// +inf otherwise, including every arc to bottom), n0, n1 and w2.
+static void append_recs(const Shape &S, int tsz, std::vector<unsigned char> &out) {
+  for (int32_t h = 0; h < S.k; ++h) {
+    double A[8];
+    for (double &a : A) a = INFINITY;
+    const int32_t w = S.hop_start[h + 1] - S.hop_start[h];
+    for (int32_t i = 0; i < w; ++i) {
+      const int32_t n = S.hop_start[h] + i;
+      for (int beta = 0; beta < 2; ++beta) {
+        const uint32_t code = beta ? S.hi[n] : S.lo[n];
+        if (code == kBot) continue;
+        const int j = code == kTop ? 0 : (int)code;  // top only on the last partition
+        A[4 * beta + 2 * i + j] = 0.0;
+      }
+    }
+    const size_t at = out.size();
+    out.resize(at + (size_t)rec_bytes(tsz), 0);
+    unsigned char *r = out.data() + at;
+    for (int q = 0; q < 8; ++q) {
+      if (tsz == 8) {
+        const double v = A[q];
+        memcpy(r + 8 * q, &v, 8);
+      } else {
+        const float v = (float)A[q];
+        memcpy(r + 4 * q, &v, 4);
+      }
+    }
+    const int32_t tail[4] = {S.hop_start[h], S.hop_start[h + 1], w == 2 ? 1 : 0, 0};
+    memcpy(r + 8 * tsz, tail, 16);
+  }
+  out.resize((out.size() + 15) & ~(size_t)15, 0);
+}
+
 fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   fdog_status st = validate(p);
   if (st) return st;
@@ -367,55 +403,6 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     const char *nb = getenv("FDOG_NBUF");  // experiment knob: stage buffers per warp (1 or 2)
     P.NB = (nb && atoi(nb) == 1) ? 1 : 2;
   }
-  auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB) {
-    return stage_bytes(tsz, kind, K, nodes, L) <= SB && relax_bytes(tsz, W, L) <= DB;
-  };
-  auto lanes_for = [&](int kind, int K, int nodes, int W, int SB, int DB) {
-    for (int L = 32; L >= 4; L /= 2)
-      if (fits(kind, K, nodes, W, L, SB, DB)) return L;
-    return 0;
-  };
-  {
-    int maxW = 1;
-    for (size_t s = 0; s < P.shapes.size(); ++s)
-      if (!by_shape[s].empty()) maxW = std::max(maxW, P.shapes[s].max_w);
-    const int DB = relax_bytes(tsz, std::min(maxW, 64), 32);
-    const int cands[] = {6, 7, 8, 9, 10, 11, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 72, 96, 112};
-    double best = 1e300;
-    int bestSB = 0;
-    for (int kb : cands) {
-      const int SB = ((kb * 1024 - 16 - DB) / P.NB) & ~15;
-      if (SB <= 0) continue;
-      double chain = 0, instr = 0;
-      int usedSB = 16;
-      for (size_t s = 0; s < P.shapes.size(); ++s) {
-        if (by_shape[s].empty()) continue;
-        const Shape &S = P.shapes[s];
-        int L = lanes_for(0, S.k, S.nodes(), S.max_w, SB, DB);
-        double pen = 1.0;
-        if (L == 0) {  // direct from global memory: latency-bound
-          L = 32;
-          pen = 10.0;
-        } else {
-          usedSB = std::max(usedSB, stage_bytes(tsz, 0, S.k, S.nodes(), L));
-        }
-        const double tiles = std::ceil((double)by_shape[s].size() / L);
-        chain += pen * tiles * (50.0 * S.nodes() + 120.0 * S.k + (P.NB == 1 ? 1500.0 : 0.0));
-        instr += tiles * (20.0 * S.nodes() + 35.0 * S.k);
-      }
-      const int wb = warp_bytes(usedSB, DB, P.NB);
-      const double warps = std::min(32.0, std::floor(226.0 * 1024 / wb));
-      if (warps < 1) continue;
-      const double t = std::max(chain / (148.0 * warps), instr / (148.0 * 2.0));
-      if (t < best * 0.98) {
-        best = t;
-        bestSB = usedSB;
-      }
-    }
-    P.SB = std::max(bestSB, 64);
-    P.DB = DB;
-  }
-
   struct PendingTile {
     int kind;                    // bit 0 per-lane topology, bit 1 staged
     int32_t shape;               // kind 0
@@ -423,88 +410,176 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     std::vector<int32_t> rows;   // lanes
     int64_t cost;
   };
-  std::vector<PendingTile> pend;
-  std::vector<int32_t> pool;  // rows for per-lane tiles
-  for (size_t s = 0; s < P.shapes.size(); ++s) {
-    auto &rows = by_shape[s];
-    const Shape &S = P.shapes[s];
-    int L = lanes_for(0, S.k, S.nodes(), S.max_w, P.SB, P.DB);
-    const bool staged = L > 0;
-    if (!staged) L = 32;
-    size_t full = rows.size() / L * L;
-    for (size_t q = 0; q < full; q += L) {
+  // pack(rc): budget + tiles for the store design (rc = false) or the
+  // recompute design (rc = true, narrow shapes only); returns the tiles in
+  // launch order
+  auto pack = [&](bool rc) {
+    std::vector<PendingTile> pend;
+    auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB) {
+      if (rc) return stage_bytes_rc(tsz, kind, K, nodes, L) <= SB && stage_dist_bytes(tsz, nodes, L) <= DB;
+      return stage_bytes(tsz, kind, K, nodes, L) <= SB && relax_bytes(tsz, W, L) <= DB;
+    };
+    auto lanes_for = [&](int kind, int K, int nodes, int W, int SB, int DB) {
+      for (int L = 32; L >= 4; L /= 2)
+        if (fits(kind, K, nodes, W, L, SB, DB)) return L;
+      return 0;
+    };
+    {
+      int maxW = 1;
+      for (size_t s = 0; s < P.shapes.size(); ++s)
+        if (!by_shape[s].empty()) maxW = std::max(maxW, P.shapes[s].max_w);
+      // store design: DB holds the relaxation buffers of the widest partition;
+      // recompute design: DB = SB holds the distance scratch (for partitions of
+      // <= 2 nodes the distances of a tile are about as large as its stage)
+      const int DB0 = relax_bytes(tsz, std::min(maxW, 64), 32);
+      const int cands[] = {6, 7, 8, 9, 10, 11, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 72, 96, 112};
+      double best = 1e300;
+      int bestSB = 0, bestDB = DB0;
+      for (int kb : cands) {
+        const int SB = rc ? ((kb * 1024 - 16) / (P.NB + 1)) & ~15 : ((kb * 1024 - 16 - DB0) / P.NB) & ~15;
+        const int DB = rc ? SB : DB0;
+        if (SB <= 0) continue;
+        double chain = 0, instr = 0;
+        int usedSB = 16, usedDB = 16;
+        for (size_t s = 0; s < P.shapes.size(); ++s) {
+          if (by_shape[s].empty()) continue;
+          const Shape &S = P.shapes[s];
+          const int k0 = S.max_w <= 2 ? 4 : 0;  // arc-mask tiles for narrow shapes
+          int L = lanes_for(k0, S.k, S.nodes(), S.max_w, SB, DB);
+          double pen = 1.0;
+          if (L == 0) {  // direct from global memory: latency-bound
+            L = 32;
+            pen = 10.0;
+          } else {
+            usedSB = std::max(usedSB, rc ? stage_bytes_rc(tsz, k0, S.k, S.nodes(), L) : stage_bytes(tsz, k0, S.k, S.nodes(), L));
+            if (rc) usedDB = std::max(usedDB, stage_dist_bytes(tsz, S.nodes(), L));
+          }
+          const double tiles = std::ceil((double)by_shape[s].size() / L);
+          // per-tile sequential chain and issued instructions (the recompute
+          // design adds the on-chip distance pass)
+          const double cn = rc ? 70.0 : 50.0, ck = rc ? 160.0 : 120.0, in = rc ? 30.0 : 20.0, ik = rc ? 50.0 : 35.0;
+          chain += pen * tiles * (cn * S.nodes() + ck * S.k + (P.NB == 1 ? 1500.0 : 0.0));
+          instr += tiles * (in * S.nodes() + ik * S.k);
+        }
+        if (!rc) usedDB = DB;
+        const int wb = warp_bytes(usedSB, usedDB, P.NB);
+        const double warps = std::min(32.0, std::floor(226.0 * 1024 / wb));
+        if (warps < 1) continue;
+        const double t = std::max(chain / (148.0 * warps), instr / (148.0 * 2.0));
+        if (t < best * 0.98) {
+          best = t;
+          bestSB = usedSB;
+          bestDB = usedDB;
+        }
+      }
+      P.SB = std::max(bestSB, 64);
+      P.DB = rc ? std::max(bestDB, 64) : DB0;
+    }
+
+    std::vector<int32_t> pool;  // rows for per-lane tiles
+    for (size_t s = 0; s < P.shapes.size(); ++s) {
+      auto &rows = by_shape[s];
+      const Shape &S = P.shapes[s];
+      const int k0 = S.max_w <= 2 ? 4 : 0;
+      int L = lanes_for(k0, S.k, S.nodes(), S.max_w, P.SB, P.DB);
+      const bool staged = L > 0;
+      if (!staged) L = 32;
+      size_t full = rows.size() / L * L;
+      for (size_t q = 0; q < full; q += L) {
+        PendingTile t;
+        t.kind = (staged ? 2 : 0) | k0;  // records also serve the streaming kernel
+        t.shape = (int32_t)s;
+        t.L = L;
+        t.rows.assign(rows.begin() + q, rows.begin() + q + L);
+        t.cost = (int64_t)S.nodes() + S.k;
+        pend.push_back(std::move(t));
+      }
+      pool.insert(pool.end(), rows.begin() + full, rows.end());
+    }
+    // per-lane tiles: same K within a tile; similar shapes adjacent
+    std::stable_sort(pool.begin(), pool.end(), [&](int32_t x, int32_t y) {
+      const Shape &a = P.shapes[P.row_shape[x]], &b = P.shapes[P.row_shape[y]];
+      if (a.k != b.k) return a.k < b.k;
+      if (a.nodes() != b.nodes()) return a.nodes() < b.nodes();
+      return P.row_shape[x] < P.row_shape[y];
+    });
+    auto padded = [&](const std::vector<int32_t> &rows, size_t n, int *nodes, int *W) {
+      const int K = P.shapes[P.row_shape[rows[0]]].k;
+      std::vector<int32_t> w(K, 0);
+      for (size_t q = 0; q < n; ++q) {
+        const Shape &S = P.shapes[P.row_shape[rows[q]]];
+        for (int h = 0; h < K; ++h) w[h] = std::max(w[h], S.hop_start[h + 1] - S.hop_start[h]);
+      }
+      *nodes = 0;
+      *W = 1;
+      for (int h = 0; h < K; ++h) {
+        *nodes += w[h];
+        *W = std::max(*W, w[h]);
+      }
+    };
+    for (size_t q = 0; q < pool.size();) {
+      const int K = P.shapes[P.row_shape[pool[q]]].k;
+      std::vector<int32_t> rows;
+      while (q < pool.size() && rows.size() < (size_t)kLanes && P.shapes[P.row_shape[pool[q]]].k == K)
+        rows.push_back(pool[q++]);
+      // largest lane count whose padded tile fits the budget
+      int L = 0, nodes = 0, W = 1;
+      for (int Lc = 32; Lc >= 4; Lc /= 2) {
+        size_t n = std::min(rows.size(), (size_t)Lc);
+        padded(rows, n, &nodes, &W);
+        if (fits(1, K, nodes, W, Lc, P.SB, P.DB)) {
+          L = Lc;
+          break;
+        }
+      }
       PendingTile t;
-      t.kind = staged ? 2 : 0;
-      t.shape = (int32_t)s;
-      t.L = L;
-      t.rows.assign(rows.begin() + q, rows.begin() + q + L);
-      t.cost = (int64_t)S.nodes() + S.k;
+      t.shape = -1;
+      if (L == 0) {
+        t.kind = 1;  // direct
+        t.L = 32;
+      } else {
+        t.kind = 3;
+        t.L = L;
+        if (rows.size() > (size_t)L) {  // give the surplus back to the pool
+          q -= rows.size() - L;
+          rows.resize(L);
+        }
+      }
+      t.rows = rows;
+      int c = 0;
+      for (int32_t j : t.rows) c = std::max(c, P.shapes[P.row_shape[j]].nodes());
+      t.cost = c + K;
       pend.push_back(std::move(t));
     }
-    pool.insert(pool.end(), rows.begin() + full, rows.end());
-  }
-  // per-lane tiles: same K within a tile; similar shapes adjacent
-  std::stable_sort(pool.begin(), pool.end(), [&](int32_t x, int32_t y) {
-    const Shape &a = P.shapes[P.row_shape[x]], &b = P.shapes[P.row_shape[y]];
-    if (a.k != b.k) return a.k < b.k;
-    if (a.nodes() != b.nodes()) return a.nodes() < b.nodes();
-    return P.row_shape[x] < P.row_shape[y];
-  });
-  auto padded = [&](const std::vector<int32_t> &rows, size_t n, int *nodes, int *W) {
-    const int K = P.shapes[P.row_shape[rows[0]]].k;
-    std::vector<int32_t> w(K, 0);
-    for (size_t q = 0; q < n; ++q) {
-      const Shape &S = P.shapes[P.row_shape[rows[q]]];
-      for (int h = 0; h < K; ++h) w[h] = std::max(w[h], S.hop_start[h + 1] - S.hop_start[h]);
-    }
-    *nodes = 0;
-    *W = 1;
-    for (int h = 0; h < K; ++h) {
-      *nodes += w[h];
-      *W = std::max(*W, w[h]);
-    }
+    // direct tiles first (slowest), then expensive tiles, so the dynamic
+    // scheduler does not leave them for the tail
+    std::stable_sort(pend.begin(), pend.end(), [](const PendingTile &a, const PendingTile &b) {
+      const bool da = !(a.kind & 2), db = !(b.kind & 2);
+      if (da != db) return da;
+      return a.cost * 32 / a.L > b.cost * 32 / b.L;
+    });
+
+    return pend;
   };
-  for (size_t q = 0; q < pool.size();) {
-    const int K = P.shapes[P.row_shape[pool[q]]].k;
-    std::vector<int32_t> rows;
-    while (q < pool.size() && rows.size() < (size_t)kLanes && P.shapes[P.row_shape[pool[q]]].k == K)
-      rows.push_back(pool[q++]);
-    // largest lane count whose padded tile fits the budget
-    int L = 0, nodes = 0, W = 1;
-    for (int Lc = 32; Lc >= 4; Lc /= 2) {
-      size_t n = std::min(rows.size(), (size_t)Lc);
-      padded(rows, n, &nodes, &W);
-      if (fits(1, K, nodes, W, Lc, P.SB, P.DB)) {
-        L = Lc;
-        break;
-      }
+  bool narrow = true;
+  for (size_t s = 0; s < P.shapes.size(); ++s)
+    if (!by_shape[s].empty()) narrow = narrow && P.shapes[s].max_w <= 2;
+  // design choice (experiment knobs: FDOG_SWEEP = rc | tma | stream; FDOG_FUSED)
+  const char *sw = getenv("FDOG_SWEEP");
+  const char *fz = getenv("FDOG_FUSED");
+  bool rc = narrow && !(sw && (sw[0] == 't' || sw[0] == 's')) && !(fz && fz[0] == '1');
+  std::vector<PendingTile> pend = pack(rc);
+  if (rc) {
+    bool direct = false;
+    for (const auto &t : pend) direct = direct || !(t.kind & 2);
+    // small problems run the fused single-CTA path (store design, solver.cpp)
+    const bool small = pend.size() <= 64 && P.n_slots <= (1 << 15) && P.world == 1 && !(fz && fz[0] == '0');
+    if (direct || (small && !(sw && sw[0] == 'r'))) {
+      rc = false;
+      pend = pack(false);
     }
-    PendingTile t;
-    t.shape = -1;
-    if (L == 0) {
-      t.kind = 1;  // direct
-      t.L = 32;
-    } else {
-      t.kind = 3;
-      t.L = L;
-      if (rows.size() > (size_t)L) {  // give the surplus back to the pool
-        q -= rows.size() - L;
-        rows.resize(L);
-      }
-    }
-    t.rows = rows;
-    int c = 0;
-    for (int32_t j : t.rows) c = std::max(c, P.shapes[P.row_shape[j]].nodes());
-    t.cost = c + K;
-    pend.push_back(std::move(t));
   }
-  // direct tiles first (slowest), then expensive tiles, so the dynamic
-  // scheduler does not leave them for the tail
-  std::stable_sort(pend.begin(), pend.end(), [](const PendingTile &a, const PendingTile &b) {
-    const bool da = !(a.kind & 2), db = !(b.kind & 2);
-    if (da != db) return da;
-    return a.cost * 32 / a.L > b.cost * 32 / b.L;
-  });
+  P.rc = rc;
 
   P.tiles.clear();
   P.hop_off.clear();
@@ -515,6 +590,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   P.max_tile_nodes = 0;
   std::vector<int64_t> shape_topo(P.shapes.size(), -1);
   std::vector<int32_t> shape_hop(P.shapes.size(), -1);
+  std::vector<int64_t> shape_rec(P.shapes.size(), -1);
+  P.recs.clear();
   // device slot of (row j, hop h): row_slot[j] + h * row_L[j]
   std::vector<int64_t> row_slot(p->n_cons, -1);
   std::vector<int32_t> row_L(p->n_cons, 32);
@@ -545,6 +622,17 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       }
       d.topo_base = shape_topo[t.shape];
       d.hop_base = shape_hop[t.shape];
+      if (t.kind & 4) {
+        if (shape_rec[t.shape] < 0) {
+          shape_rec[t.shape] = (int64_t)(P.recs.size() / 16);
+          append_recs(S0, tsz, P.recs);
+        }
+        if (shape_rec[t.shape] > 0x7fffffffLL) {
+          set_error("hop record table exceeds 32 GiB");
+          return FDOG_ETOOBIG;
+        }
+        d.rec_base = (int32_t)shape_rec[t.shape];
+      }
       d.nodes = S0.nodes();
       d.max_w = S0.max_w;
       P.tiles_shared++;
@@ -743,6 +831,7 @@ fdog_status build_image(Plan &P) {
   sz[kImXDeg] = P.x_deg.size() * 4;
   sz[kImLambda0] = P.slot_var.size() * tsz;
   sz[kImDist0] = (size_t)P.n_dist * tsz;
+  sz[kImRecs] = P.recs.size();
   size_t at = 0;
   for (int q = 0; q < kImCount; ++q) {
     P.image.off[q] = at;
@@ -781,6 +870,7 @@ fdog_status build_image(Plan &P) {
   put(kImEll4Var, P.ell4_var.data());
   put(kImXLocal, P.x_local.data());
   put(kImXDeg, P.x_deg.data());
+  put(kImRecs, P.recs.data());
   unsigned char *lam = P.image.data + P.image.off[kImLambda0];
   for (size_t q = 0; q < P.slot_var.size(); ++q) {
     const int32_t i = P.slot_var[q];

@@ -68,6 +68,7 @@ struct fdog_solver {
   int rank = 0, world = 1;
   bool external = false;  // world > 1 without NCCL: the caller performs the exchange
   bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
+  bool rc = false;           // recompute design (Plan::rc): no distance traffic, no dist_state
   int32_t static_sched = 0;  // TMA sweep: round-robin tiles only
 
   // host copies needed by getters
@@ -114,6 +115,7 @@ struct fdog_solver {
   size_t smem = 0;
   int32_t SB = 0, DB = 0, NB = 2;
   size_t warp_bytes = 0;
+  const unsigned char *d_recs = nullptr;
   void *d_dist = nullptr;
   int dist_state = 0;  // 0: distances hold shp(v, T); 1: shp(r, v)
   int64_t n_direct = 0, scratch_stride = 0;
@@ -197,7 +199,7 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
     if (s->stream_mode && (mode == kForward || mode == kBackward))
       e = launch_sweep_stream(s->precision, mode, rec, a, s->stream);
     else
-      e = launch_sweep(s->precision, mode, rec, a, s->grid, s->block, s->smem, s->stream);
+      e = launch_sweep(s->precision, mode, rec, s->rc, a, s->grid, s->block, s->smem, s->stream);
   }
   if (e) return cuda_fail((cudaError_t)e, "sweep launch");
   s->lb_dirty = true;
@@ -210,6 +212,7 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.n_tiles = s->n_tiles;
   a.hop_off = s->d_hop_off;
   a.topo = s->d_topo;
+  a.recs = s->d_recs;
   a.slot_var = s->d_slot_var;
   a.lambda = s->d_lambda;
   a.delta_out = s->d_delta[s->cur ^ 1];  // avg_i in (avg_kernel), delta out
@@ -228,6 +231,8 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.NB = s->NB;
   a.dist = s->d_dist;
   a.static_sched = s->static_sched;
+  a.scratch = s->d_scratch;  // relaxation buffers of direct (unstaged) tiles
+  a.scratch_stride = s->scratch_stride;
   return a;
 }
 
@@ -298,8 +303,9 @@ fdog_status pass_stage(fdog_solver *s, bool forward, double omega, int stage) {
   if (stage == 0) {
     // the pass needs the distances of the opposite direction;
     // after an unusual call sequence recompute them first
-    if (forward && s->dist_state != 0 && (st = run_sweep(s, kEnergy, omega))) return st;
-    if (!forward && s->dist_state != 1 && (st = run_sweep(s, kCfr, omega))) return st;
+    // (the recompute design derives them inside the pass)
+    if (!s->rc && forward && s->dist_state != 0 && (st = run_sweep(s, kEnergy, omega))) return st;
+    if (!s->rc && !forward && s->dist_state != 1 && (st = run_sweep(s, kCfr, omega))) return st;
     return run_avg(s);
   }
   if (s->external && (st = run_avg_finish(s))) return st;
@@ -466,6 +472,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->SB = P.SB;
   s->DB = P.DB;
   s->NB = P.NB;
+  s->rc = P.rc;
   s->warp_bytes = (size_t)warp_bytes(P.SB, P.DB, P.NB);
   s->n_direct = P.direct_tiles;
   {
@@ -479,12 +486,12 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     const bool staged_ok = sm_bytes / std::max<size_t>(s->warp_bytes, 1) >= 8 && s->n_direct == 0;
     const char *m = getenv("FDOG_SWEEP");  // experiment knob: "tma" or "stream"
     const bool forced = m && (m[0] == 's' || m[0] == 't');
-    s->stream_mode = narrow && (forced ? m[0] == 's' : !staged_ok);
+    s->stream_mode = !s->rc && narrow && (forced ? m[0] == 's' : !staged_ok);
     // tiny instances (BASELINE configs[0]) are launch-latency bound: one CTA
     // runs every iteration of an fdog_iterate call (fused_small_kernel)
     const char *fz = getenv("FDOG_FUSED");  // experiment knob: 0 / 1
     const bool small = tiles.size() <= 64 && P.n_slots <= (1 << 15);
-    s->use_fused = narrow && P.world == 1 && (fz ? fz[0] == '1' : small);
+    s->use_fused = !s->rc && narrow && P.world == 1 && (fz ? fz[0] == '1' : small);
     const size_t fbytes = (size_t)(3 * (int64_t)P.slot_var.size() + P.n_dist) * s->tsz;
     const char *fr = getenv("FDOG_FUSED_SMEM");  // experiment knob: 0 keeps the state in global memory
     s->fused_smem = (fbytes <= (size_t)prop.smem_block && !(fr && fr[0] == '0')) ? fbytes : 0;
@@ -500,7 +507,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   for (int mode = 0; mode < 4; ++mode)
     for (int rec = 0; rec < 2; ++rec) {
       int b = 0;
-      int e = sweep_occupancy(s->precision, mode, rec && mode != kEnergy, s->block, s->smem, &b);
+      int e = sweep_occupancy(s->precision, mode, rec && mode != kEnergy, s->rc, s->block, s->smem, &b);
       if (e) return cuda_fail((cudaError_t)e, "occupancy");
       if (mode == kForward && rec == (int)s->record_mm) bps = std::max(1, b);
     }
@@ -562,6 +569,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_tiles = (TileDesc *)sec(kImTiles);
   s->d_hop_off = (int32_t *)sec(kImHopOff);
   s->d_topo = (uint32_t *)sec(kImTopo);
+  s->d_recs = (const unsigned char *)sec(kImRecs);
   s->d_slot_var = (int32_t *)sec(kImSlotVar);
   s->d_var_ptr = (int64_t *)sec(kImVarPtr);
   s->d_var_slots = (int32_t *)sec(kImVarSlots);
@@ -603,8 +611,10 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     for (const auto &d : tiles)
       if (d.kind & 1) lane_topo += 4.0 * d.nodes * d.n_lanes;
     const double rec = s->record_mm ? 2 * T : 0.0;
-    s->bytes[kKSweepFwd] = s->bytes[kKSweepBwd] = nodes * 2 * T + lane_topo + slots * (4 * T + rec);
-    s->bytes[kKEnergy] = nodes * 2 * T + lane_topo + slots * T;
+    // (recompute design: no per-node distance traffic)
+    const double dist = s->rc ? 0.0 : nodes * 2 * T;
+    s->bytes[kKSweepFwd] = s->bytes[kKSweepBwd] = dist + lane_topo + slots * (4 * T + rec);
+    s->bytes[kKEnergy] = dist + lane_topo + slots * T;
     // averaging: per slot the slot index, the delta gather and the average scatter;
     // per variable the CSR pointer and |J_i|
     s->bytes[kKAvg] = slots * (4 + 2 * T) + nv * (8 + 4);
@@ -633,6 +643,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->st.sweep_streaming = s->stream_mode ? 1 : 0;
   s->st.h2d_bytes = s->upload_bytes;
   s->st.fused_small = s->use_fused ? (s->fused_smem ? 2 : 1) : 0;
+  s->st.sweep_recompute = s->rc ? 1 : 0;
 
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;
@@ -977,7 +988,7 @@ fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
   }
   // CUDA graph of one iteration: used when the passes alternate normally, no
   // per-kernel events are requested and there is no NCCL exchange
-  const bool graphs = s->use_graphs && !s->profile && s->world == 1 && s->dist_state == 0 && n_iter > 0;
+  const bool graphs = s->use_graphs && !s->profile && s->world == 1 && (s->rc || s->dist_state == 0) && n_iter > 0;
   if (graphs) {
     if (!s->graph || s->graph_omega != omega || s->graph_cur != s->cur) {
       if (s->graph) {

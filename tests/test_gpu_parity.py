@@ -273,19 +273,71 @@ def test_fused_small_path(oracle_mod, monkeypatch, resident, precision, name, ma
     assert np.array_equal(gf.lam(), gd.lam()) and gf.lower_bound() == gd.lower_bound()
 
 
-@pytest.mark.parametrize("mode", ["tma", "stream"])
-@pytest.mark.parametrize("name,make", [
+_SWEEP_CASES = [
     ("gm", lambda: synth.gm_worms_like(13, n_src=70, k_cand=6, knn=8)),
     ("mrf", lambda: synth.mrf_potts(13, H=9, W=11, L=4)),
     ("qap", lambda: synth.qap(13, n=8)),
+    ("ct", lambda: synth.celltrack(13, frames=4, dets=40)),
     ("lap", lambda: synth.lap(synth.LAP4_LITERAL)),
-])
-def test_both_sweep_kernels(oracle_mod, monkeypatch, mode, name, make):
-    """The TMA-staged sweep and the streaming sweep (chosen per problem by
-    default) both match the oracle pass by pass, fp64."""
+]
+
+
+@pytest.mark.parametrize("mode", ["rc", "tma", "stream"])
+@pytest.mark.parametrize("name,make", _SWEEP_CASES)
+def test_all_sweep_kernels(oracle_mod, monkeypatch, mode, name, make):
+    """The three sweep designs -- recompute (the default for narrow problems:
+    distances of the opposite direction rebuilt on chip), TMA-staged store and
+    streaming store -- each match the oracle pass by pass, fp64."""
     monkeypatch.setenv("FDOG_SWEEP", mode)
     g, _ = _compare_pass_by_pass(make(), oracle_mod, passes=6)
-    assert g.stats()["sweep_streaming"] == (1 if mode == "stream" else 0)
+    st = g.stats()
+    assert st["sweep_streaming"] == (1 if mode == "stream" else 0)
+    assert st["sweep_recompute"] == (1 if mode == "rc" else 0)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("name,make", _SWEEP_CASES[:4])
+def test_recompute_equals_store_bitwise(monkeypatch, precision, name, make):
+    """The recomputed distances equal the stored ones exactly (lambda has not
+    changed since the previous pass computed them, same operations in the same
+    order), so the recompute and store designs give bit-identical iterates --
+    including after unusual pass orders, finalize and set_state.  (The bound
+    is a sum of per-tile partials in tile order: equal up to summation order.)"""
+    p = make()
+    gs = {}
+    for mode in ("rc", "tma", "stream"):
+        monkeypatch.setenv("FDOG_SWEEP", mode)
+        monkeypatch.setenv("FDOG_FUSED", "0")
+        gs[mode] = F.Solver(p, precision=precision, record_mm=True)
+    assert gs["rc"].stats()["sweep_recompute"] == 1
+    def lb_close(a, b):  # the per-tile partials are summed in tile order, and
+        return abs(a - b) <= 1e-12 * (1 + abs(b))  # the two designs pack tiles differently
+    lb0 = {m: g.lower_bound() for m, g in gs.items()}
+    assert lb_close(lb0["rc"], lb0["tma"]) and lb_close(lb0["stream"], lb0["tma"])
+    steps = [("it", 3, 0.5), ("pass", True, 0.5), ("pass", True, 0.3), ("pass", False, 0.5),
+             ("pass", False, 0.5), ("it", 2, 0.4), ("fin",), ("it", 2, 0.5)]
+    for st in steps:
+        for g in gs.values():
+            if st[0] == "it":
+                g.iterate(st[1], st[2])
+            elif st[0] == "pass":
+                g.pass_(st[1], st[2])
+            else:
+                g.finalize()
+        ref = gs["tma"]
+        for m in ("rc", "stream"):
+            g = gs[m]
+            assert np.array_equal(g.lam(), ref.lam()), (m, st)
+            assert np.array_equal(g.deferred(), ref.deferred()), (m, st)
+            assert lb_close(g.lower_bound(), ref.lower_bound()), (m, st)
+            if st[0] != "fin":
+                a, b = g.min_marginals(), ref.min_marginals()
+                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (m, st)
+    lam, dl = gs["tma"].lam(), gs["tma"].deferred()
+    for g in gs.values():
+        g.set_state(lam, dl)
+        g.iterate(1, 0.5)
+    assert np.array_equal(gs["rc"].lam(), gs["tma"].lam())
 
 
 def test_errors_and_state():
