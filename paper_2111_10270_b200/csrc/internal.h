@@ -44,6 +44,8 @@ struct Shape {
 //          whose partitions have <= 2 nodes): the stage holds the shape's hop
 //          records (HopRec, at recs + 16 * rec_base) instead of topology and
 //          partition offsets; the sweeps use the branch-free min-plus form.
+//   kind bit 3 set (with bit 2): every partition but the first and the last
+//          is a chain hop (HopRec type 1); the sweeps fold those hops.
 // Topology entries are absolute child indices within the tile (s^0 in the low
 // 16 bits, s^1 in the high 16 bits), top = nodes, bottom = nodes + 1.
 // Partition offsets of the tile: hop_off[hop_base + h], h = 0..K.
@@ -96,6 +98,8 @@ FDOG_HD int stage_hop_bytes(int K) { return r16((K + 1) * 4); }
 //            partition), so D[n1 + j] is the distance of target j -- on the
 //            last partition the sentinels (0 for top, +inf).
 //   w2       1 if P_h has two nodes.
+//   type     0 generic; 1..3 a specialised pattern (plan.cpp append_recs,
+//            kernels.cu hop_type): the kernels then skip the masks.
 FDOG_HD int rec_bytes(int tsz) { return 8 * tsz + 16; }
 FDOG_HD int stage_tail_bytes(int tsz, int kind, int K, int nodes, int L) {
   return (kind & 4) ? r16(K * rec_bytes(tsz)) : stage_topo_bytes(kind, nodes, L) + stage_hop_bytes(K);

@@ -1,26 +1,34 @@
 // kernels.cu -- sm_100a kernels of the deferred min-marginal averaging hot path.
 //
-//   sweep_kernel<T, MODE, REC>   one pass (forward P:627-645 / backward P:647-648)
-//                                over all BDD tiles; MODE kEnergy = sum_j E^j only.
-//   avg_kernel<T>                deferred averaging avg_i = mean_{k in J_i} delta_bar_ik
-//                                (P:641 second term, readings A1/A10).
-//   avg_finish_kernel<T>         shared variables after the NCCL exchange.
-//   add_deferred_kernel<T>       final correction lambda += delta_bar.
+//   sweep_kernel<T, MODE, REC, RC> one pass (forward P:627-645 / backward P:647-648)
+//                                  over all BDD tiles, TMA-staged; MODE kEnergy =
+//                                  sum_j E^j only, kCfr = shp(r, .) only.
+//   sweep_stream_kernel<T, MODE, REC> the same pass streamed from global memory
+//                                  (store design, narrow tiles; FDOG_SWEEP=stream).
+//   avg_kernel<T>                  deferred averaging avg_i = mean_{k in J_i} delta_bar_ik
+//                                  (P:641 second term, readings A1/A10).
+//   avg_finish_kernel<T>           shared variables after the NCCL exchange.
+//   add_deferred_kernel<T>         final correction lambda += delta_bar.
+//   fused_small_kernel<T, REC>     every iteration of a small problem in one CTA.
+//   primal_kernel<T>               Alg. 2 classify / perturb steps.
 //
-// Thread mapping: one warp per tile of 32 BDDs, one BDD per
+// Thread mapping: one warp per tile of L <= 32 BDDs, one BDD per
 // lane.  Each lane walks its BDD's partitions sequentially (the hop recursion
-// P:317-342 is sequential); all distances live in the lane's private column
-// of shared memory ([node][lane] layout: conflict-free, no cross-lane
-// communication, no atomics, no barriers inside a pass).  The distances of the
-// opposite direction are RECOMPUTED on chip at the start of every pass from
-// the current lambda (they equal the stored distances of P:315-316 exactly,
-// because lambda has not changed since they were computed), so HBM traffic is
-// topology + per-slot data only.
+// P:317-342 is sequential); distances live in the lane's private column of
+// shared memory ([node][lane] layout: conflict-free, no cross-lane
+// communication, no atomics, no barriers inside a pass).  Two designs for the
+// distances of the opposite direction:
+//   * recompute (RC, default for narrow problems): rebuilt on chip at the start
+//     of every pass from the current lambda -- equal to the stored distances of
+//     P:315-316 exactly, since lambda has not changed since they were computed
+//     -- so HBM traffic is per-slot data only;
+//   * store: kept in HBM per node and converted in place by each pass.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -565,9 +573,15 @@ __device__ __forceinline__ double process_rc_w2(const int K, const int top, cons
 template <typename T>
 struct __align__(16) HopRec {
   T A[8];
-  int32_t n0, n1, w2, pad;
+  int32_t n0, n1, w2, type;
 };
 static_assert(sizeof(HopRec<float>) == 48 && sizeof(HopRec<double>) == 80, "HopRec layout (internal.h rec_bytes)");
+
+// The record's 16-byte tail (n0, n1, w2, type), one vector load.
+template <typename T>
+__device__ __forceinline__ int4 hop_tail(const HopRec<T> *r) {
+  return *reinterpret_cast<const int4 *>(&r->n0);
+}
 
 template <typename T>
 __device__ __forceinline__ void arc_mins(const HopRec<T> &r, T x0, T x1, T &a0, T &a1, T &b0, T &b1) {
@@ -576,15 +590,77 @@ __device__ __forceinline__ void arc_mins(const HopRec<T> &r, T x0, T x1, T &a0, 
   b0 = fmin(r.A[4] + x0, r.A[5] + x1);
   b1 = fmin(r.A[6] + x0, r.A[7] + x1);
 }
+
+// Hop types (plan.cpp append_recs): the masks of type 1..3 are fixed, so the
+// general expressions fold to the ones below (exactly: a 0 mask adds nothing,
+// an +inf mask drops the term).  The type is warp-uniform in a tile.
+//   1 chain: 0-arcs 0->0, 1->1; 1-arc 1->0     (a = (x0, x1), b = (inf, x0))
+//   2 root : one node; 0-arc ->0, 1-arc ->1    (a0 = x0, b0 = x1)
+//   3 join : 0-arc 0->0; 1-arc 1->0            (a = (x0, inf), b = (inf, x0))
+// m^0 = min_i (c_i + a_i), m^1 - lambda = min_i (c_i + b_i); c = shp(r, .) of
+// P_h in a forward pass, the stored/recomputed shp(r, .) in a backward pass.
 template <typename T>
-__device__ __forceinline__ void arc_relax(const HopRec<T> &r, T c0, T c1, T lam, T &o0, T &o1) {
-  o0 = fmin(fmin(c0 + r.A[0], c1 + r.A[2]), lam + fmin(c0 + r.A[4], c1 + r.A[6]));
-  o1 = fmin(fmin(c0 + r.A[1], c1 + r.A[3]), lam + fmin(c0 + r.A[5], c1 + r.A[7]));
+__device__ __forceinline__ void hop_mm(const int type, const HopRec<T> *rp, T x0, T x1, T c0, T c1, T &m0, T &m1r) {
+  if (type == 1) {
+    m0 = fmin(c0 + x0, c1 + x1);
+    m1r = c1 + x0;
+  } else if (type == 2) {
+    m0 = c0 + x0;
+    m1r = c0 + x1;
+  } else if (type == 3) {
+    m0 = c0 + x0;
+    m1r = c1 + x0;
+  } else {
+    const HopRec<T> r = *rp;
+    T a0, a1, b0, b1;
+    arc_mins(r, x0, x1, a0, a1, b0, b1);
+    m0 = fmin(c0 + a0, c1 + a1);
+    m1r = fmin(c0 + b0, c1 + b1);
+  }
+}
+// shp(v_i, T) = min(a_i, lambda + b_i)
+template <typename T>
+__device__ __forceinline__ void hop_ctt(const int type, const HopRec<T> *rp, T x0, T x1, T lam, T &o0, T &o1) {
+  if (type == 1) {
+    o0 = x0;
+    o1 = fmin(x1, lam + x0);
+  } else if (type == 2) {
+    o0 = fmin(x0, lam + x1);
+    o1 = t_inf<T>();
+  } else if (type == 3) {
+    o0 = x0;
+    o1 = lam + x0;
+  } else {
+    const HopRec<T> r = *rp;
+    T a0, a1, b0, b1;
+    arc_mins(r, x0, x1, a0, a1, b0, b1);
+    o0 = fmin(a0, lam + b0);
+    o1 = fmin(a1, lam + b1);
+  }
+}
+// shp(r, v_j) of P_{h+1} = min over arcs into v_j of c_i (+ lambda on 1-arcs)
+// (reading A4)
+template <typename T>
+__device__ __forceinline__ void hop_relax(const int type, const HopRec<T> *rp, T c0, T c1, T lam, T &o0, T &o1) {
+  if (type == 1) {
+    o0 = fmin(c0, lam + c1);
+    o1 = c1;
+  } else if (type == 2) {
+    o0 = c0;
+    o1 = lam + c0;
+  } else if (type == 3) {
+    o0 = fmin(c0, lam + c1);
+    o1 = t_inf<T>();
+  } else {
+    const HopRec<T> r = *rp;
+    o0 = fmin(fmin(c0 + r.A[0], c1 + r.A[2]), lam + fmin(c0 + r.A[4], c1 + r.A[6]));
+    o1 = fmin(fmin(c0 + r.A[1], c1 + r.A[3]), lam + fmin(c0 + r.A[5], c1 + r.A[7]));
+  }
 }
 
 // dual update of one slot (A5, A10); returns the new lambda_h
 template <typename T, bool REC>
-__device__ __forceinline__ T mask_finish(T *lam, T *va, int hL, T l, T av, T m0, T m1r, bool valid, T omega, T clamp,
+__device__ __forceinline__ T mask_finish(T *lam, T *va, uint32_t hL, T l, T av, T m0, T m1r, bool valid, T omega, T clamp,
                                          T *m0g, T *m1g, double &acc) {
   const T m1 = l + m1r;
   const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
@@ -603,50 +679,72 @@ __device__ __forceinline__ T mask_finish(T *lam, T *va, int hL, T l, T av, T m0,
   return lam_new;
 }
 
+// Loops over the partitions.  Tiles with kind bit 3 ("chain tiles") have
+// type-1 (chain) hops everywhere but the first and the last partition: those
+// two run the general masks, the middle ones the folded chain expressions --
+// no per-hop type dispatch on the dependent chain.  Other tiles run the
+// general masks throughout.  Every loop prefetches the next partition's record
+// tail, lambda, average and distances before computing the current one.
+template <bool B>
+using Bool = std::integral_constant<bool, B>;
+
 // shp(v, T) of every node under the current lambda (no update); returns
 // shp(r, T) = E^j.  (kEnergy; phase 1 of a recompute forward pass.)
 template <typename T, int LC>
-__device__ __forceinline__ T mask_ctt(const int K, const HopRec<T> *rec, const int L_rt, const T *lam, T *D) {
-  const int L = LC ? LC : L_rt;
+__device__ __forceinline__ T mask_ctt(const int K, const bool chain, const HopRec<T> *rec, const int L_rt,
+                                      const T *lam, T *D) {
+  const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   T x0 = T(0), x1 = t_inf<T>();
-  HopRec<T> r = rec[K - 1];
+  int4 tl = hop_tail(rec + K - 1);
   T l = lam[(K - 1) * L];
-#pragma unroll 1
-  for (int h = K - 1; h >= 0; --h) {
-    const int hn = h > 0 ? h - 1 : 0;
-    const HopRec<T> rn = rec[hn];
+  auto step = [&](auto ch, int h) {
+    const uint32_t hn = h > 0 ? h - 1 : 0;
+    const int4 tn = hop_tail(rec + hn);
     const T ln = lam[hn * L];
-    T a0, a1, b0, b1;
-    arc_mins(r, x0, x1, a0, a1, b0, b1);
-    x0 = fmin(a0, l + b0);
-    x1 = fmin(a1, l + b1);
-    D[r.n0 * L] = x0;
-    if (r.w2) D[(r.n0 + 1) * L] = x1;
-    r = rn;
+    hop_ctt(decltype(ch)::value ? 1 : 0, rec + (uint32_t)h, x0, x1, l, x0, x1);
+    D[tl.x * L] = x0;
+    if (tl.z) D[(tl.x + 1) * L] = x1;
+    tl = tn;
     l = ln;
+  };
+  int h = K - 1;
+  if (chain) {
+    if (h > 0) step(Bool<false>(), h--);
+#pragma unroll 1
+    for (; h > 0; --h) step(Bool<true>(), h);
   }
+#pragma unroll 1
+  for (; h >= 0; --h) step(Bool<false>(), h);
   return x0;
 }
 
 // shp(r, v) of every node under the current lambda (no update); returns
 // shp(r, T) = E^j.  (kCfr; phase 1 of a recompute backward pass.)
 template <typename T, int LC>
-__device__ __forceinline__ T mask_cfr(const int K, const HopRec<T> *rec, const int L_rt, const T *lam, T *D) {
-  const int L = LC ? LC : L_rt;
+__device__ __forceinline__ T mask_cfr(const int K, const bool chain, const HopRec<T> *rec, const int L_rt,
+                                      const T *lam, T *D) {
+  const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   T c0 = T(0), c1 = t_inf<T>();
-  HopRec<T> r = rec[0];
+  int4 tl = hop_tail(rec);
   T l = lam[0];
-#pragma unroll 1
-  for (int h = 0; h < K; ++h) {
-    const int hn = h + 1 < K ? h + 1 : h;
-    const HopRec<T> rn = rec[hn];
+  auto step = [&](auto ch, int h) {
+    const uint32_t hn = h + 1 < K ? h + 1 : h;
+    const int4 tn = hop_tail(rec + hn);
     const T ln = lam[hn * L];
-    D[r.n0 * L] = c0;
-    if (r.w2) D[(r.n0 + 1) * L] = c1;
-    arc_relax(r, c0, c1, l, c0, c1);
-    r = rn;
+    D[tl.x * L] = c0;
+    if (tl.z) D[(tl.x + 1) * L] = c1;
+    hop_relax(decltype(ch)::value ? 1 : 0, rec + (uint32_t)h, c0, c1, l, c0, c1);
+    tl = tn;
     l = ln;
+  };
+  int h = 0;
+  if (chain) {
+    if (h < K - 1) step(Bool<false>(), h++);
+#pragma unroll 1
+    for (; h < K - 1; ++h) step(Bool<true>(), h);
   }
+#pragma unroll 1
+  for (; h < K; ++h) step(Bool<false>(), h);
   return c0;  // after the last partition: the relaxation into top
 }
 
@@ -654,37 +752,43 @@ __device__ __forceinline__ T mask_cfr(const int K, const HopRec<T> *rec, const i
 // previous backward pass, or recomputed by mask_ctt); STORE: D of P_h is
 // overwritten with shp(r, v) for the next backward pass (P:315-316 reuse).
 template <typename T, bool STORE, bool REC, int LC>
-__device__ __forceinline__ double mask_forward(const int K, const HopRec<T> *rec, const int L_rt, T *lam, T *va,
-                                               T *D, const bool valid, const T omega, const T clamp, T *m0g,
-                                               T *m1g) {
-  const int L = LC ? LC : L_rt;
+__device__ __forceinline__ double mask_forward(const int K, const bool chain, const HopRec<T> *rec, const int L_rt,
+                                               T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
+                                               T *m0g, T *m1g) {
+  const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   double acc = 0.0;
   T c0 = T(0), c1 = t_inf<T>();
-  HopRec<T> r = rec[0];
+  int4 tl = hop_tail(rec);
   T l = lam[0], av = va[0];
-  T x0 = D[r.n1 * L], x1 = D[(r.n1 + 1) * L];
-#pragma unroll 1
-  for (int h = 0; h < K; ++h) {
-    const int hn = h + 1 < K ? h + 1 : h;
-    const HopRec<T> rn = rec[hn];
+  T x0 = D[tl.y * L], x1 = D[(tl.y + 1) * L];
+  auto step = [&](auto ch, int h) {
+    constexpr int ty = decltype(ch)::value ? 1 : 0;
+    const uint32_t hn = h + 1 < K ? h + 1 : h;
+    const int4 tn = hop_tail(rec + hn);
     const T ln = lam[hn * L], avn = va[hn * L];
-    const T x0n = D[rn.n1 * L], x1n = D[(rn.n1 + 1) * L];
+    const T x0n = D[tn.y * L], x1n = D[(tn.y + 1) * L];
     if (STORE) {
-      D[r.n0 * L] = c0;
-      if (r.w2) D[(r.n0 + 1) * L] = c1;
+      D[tl.x * L] = c0;
+      if (tl.z) D[(tl.x + 1) * L] = c1;
     }
-    T a0, a1, b0, b1;
-    arc_mins(r, x0, x1, a0, a1, b0, b1);
-    const T m0 = fmin(c0 + a0, c1 + a1);
-    const T m1r = fmin(c0 + b0, c1 + b1);
-    const T lam_new = mask_finish<T, REC>(lam, va, h * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
-    arc_relax(r, c0, c1, lam_new, c0, c1);  // A4: 1-arcs priced with the updated lambda_h
-    r = rn;
+    T m0, m1r;
+    hop_mm(ty, rec + (uint32_t)h, x0, x1, c0, c1, m0, m1r);
+    const T lam_new = mask_finish<T, REC>(lam, va, (uint32_t)h * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
+    hop_relax(ty, rec + (uint32_t)h, c0, c1, lam_new, c0, c1);  // A4: 1-arcs priced with the updated lambda_h
+    tl = tn;
     l = ln;
     av = avn;
     x0 = x0n;
     x1 = x1n;
+  };
+  int h = 0;
+  if (chain) {
+    if (h < K - 1) step(Bool<false>(), h++);
+#pragma unroll 1
+    for (; h < K - 1; ++h) step(Bool<true>(), h);
   }
+#pragma unroll 1
+  for (; h < K; ++h) step(Bool<false>(), h);
   if (valid) acc += (double)c0;  // E^j = shp(r, T) at the updated lambda
   return acc;
 }
@@ -693,38 +797,46 @@ __device__ __forceinline__ double mask_forward(const int K, const HopRec<T> *rec
 // forward pass, or recomputed by mask_cfr); STORE: D of P_h is overwritten
 // with shp(v, T) for the next forward pass.
 template <typename T, bool STORE, bool REC, int LC>
-__device__ __forceinline__ double mask_backward(const int K, const HopRec<T> *rec, const int L_rt, T *lam, T *va,
-                                                T *D, const bool valid, const T omega, const T clamp, T *m0g,
-                                                T *m1g) {
-  const int L = LC ? LC : L_rt;
+__device__ __forceinline__ double mask_backward(const int K, const bool chain, const HopRec<T> *rec, const int L_rt,
+                                                T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
+                                                T *m0g, T *m1g) {
+  const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
+  const T inf = t_inf<T>();
   double acc = 0.0;
-  T x0 = T(0), x1 = t_inf<T>();  // shp(., T) of P_{h+1}; the last partition's targets: top
-  HopRec<T> r = rec[K - 1];
+  T x0 = T(0), x1 = inf;  // shp(., T) of P_{h+1}; the last partition's targets: top
+  int4 tl = hop_tail(rec + K - 1);
   T l = lam[(K - 1) * L], av = va[(K - 1) * L];
-  T f0 = D[r.n0 * L], f1 = D[(r.n0 + 1) * L];
-#pragma unroll 1
-  for (int h = K - 1; h >= 0; --h) {
-    const int hn = h > 0 ? h - 1 : 0;
-    const HopRec<T> rn = rec[hn];
+  // (a one-node partition's second entry is not read: in global memory the
+  // load would alias the store of the partition above)
+  T f0 = D[tl.x * L], f1 = tl.z ? D[(tl.x + 1) * L] : inf;
+  auto step = [&](auto ch, int h) {
+    constexpr int ty = decltype(ch)::value ? 1 : 0;
+    const uint32_t hn = h > 0 ? h - 1 : 0;
+    const int4 tn = hop_tail(rec + hn);
     const T ln = lam[hn * L], avn = va[hn * L];
-    const T f0n = D[rn.n0 * L], f1n = D[(rn.n0 + 1) * L];
-    T a0, a1, b0, b1;
-    arc_mins(r, x0, x1, a0, a1, b0, b1);
-    const T m0 = fmin(f0 + a0, f1 + a1);
-    const T m1r = fmin(f0 + b0, f1 + b1);
-    const T lam_new = mask_finish<T, REC>(lam, va, h * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
-    x0 = fmin(a0, lam_new + b0);  // shp(v, T) with the updated lambda_h
-    x1 = fmin(a1, lam_new + b1);
+    const T f0n = D[tn.x * L], f1n = tn.z ? D[(tn.x + 1) * L] : inf;
+    T m0, m1r;
+    hop_mm(ty, rec + (uint32_t)h, x0, x1, f0, f1, m0, m1r);
+    const T lam_new = mask_finish<T, REC>(lam, va, (uint32_t)h * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
+    hop_ctt(ty, rec + (uint32_t)h, x0, x1, lam_new, x0, x1);  // shp(v, T) with the updated lambda_h
     if (STORE) {
-      D[r.n0 * L] = x0;
-      if (r.w2) D[(r.n0 + 1) * L] = x1;
+      D[tl.x * L] = x0;
+      if (tl.z) D[(tl.x + 1) * L] = x1;
     }
-    r = rn;
+    tl = tn;
     l = ln;
     av = avn;
     f0 = f0n;
     f1 = f1n;
+  };
+  int h = K - 1;
+  if (chain) {
+    if (h > 0) step(Bool<false>(), h--);
+#pragma unroll 1
+    for (; h > 0; --h) step(Bool<true>(), h);
   }
+#pragma unroll 1
+  for (; h >= 0; --h) step(Bool<false>(), h);
   if (valid) acc += (double)x0;  // E^j = shp(r, T)
   return acc;
 }
@@ -879,6 +991,7 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
         // arc-mask tile (narrow shape, shared topology)
         if (active) {
           const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(s.topo);
+          const bool chain = d.kind & 8;
           T *D = RC ? reinterpret_cast<T *>(rbase) + lane : s.dist + lane;
           if (RC) {
             D[d.nodes * L] = T(0);              // top
@@ -889,31 +1002,31 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
           T *lm = s.lam + lane, *vp = s.va + lane;
           if (L == 32) {
             if (MODE == kEnergy) {
-              const T e = mask_ctt<T, 32>(K, rec, 32, lm, D);
+              const T e = mask_ctt<T, 32>(K, chain, rec, 32, lm, D);
               acc = valid ? (double)e : 0.0;
             } else if (MODE == kCfr) {
-              const T e = mask_cfr<T, 32>(K, rec, 32, lm, D);
+              const T e = mask_cfr<T, 32>(K, chain, rec, 32, lm, D);
               acc = valid ? (double)e : 0.0;
             } else if (MODE == kForward) {
-              if (RC) mask_ctt<T, 32>(K, rec, 32, lm, D);
-              acc = mask_forward<T, !RC, REC, 32>(K, rec, 32, lm, vp, D, valid, omega, clamp, m0p, m1p);
+              if (RC) mask_ctt<T, 32>(K, chain, rec, 32, lm, D);
+              acc = mask_forward<T, !RC, REC, 32>(K, chain, rec, 32, lm, vp, D, valid, omega, clamp, m0p, m1p);
             } else {
-              if (RC) mask_cfr<T, 32>(K, rec, 32, lm, D);
-              acc = mask_backward<T, !RC, REC, 32>(K, rec, 32, lm, vp, D, valid, omega, clamp, m0p, m1p);
+              if (RC) mask_cfr<T, 32>(K, chain, rec, 32, lm, D);
+              acc = mask_backward<T, !RC, REC, 32>(K, chain, rec, 32, lm, vp, D, valid, omega, clamp, m0p, m1p);
             }
           } else {
             if (MODE == kEnergy) {
-              const T e = mask_ctt<T, 0>(K, rec, L, lm, D);
+              const T e = mask_ctt<T, 0>(K, chain, rec, L, lm, D);
               acc = valid ? (double)e : 0.0;
             } else if (MODE == kCfr) {
-              const T e = mask_cfr<T, 0>(K, rec, L, lm, D);
+              const T e = mask_cfr<T, 0>(K, chain, rec, L, lm, D);
               acc = valid ? (double)e : 0.0;
             } else if (MODE == kForward) {
-              if (RC) mask_ctt<T, 0>(K, rec, L, lm, D);
-              acc = mask_forward<T, !RC, REC, 0>(K, rec, L, lm, vp, D, valid, omega, clamp, m0p, m1p);
+              if (RC) mask_ctt<T, 0>(K, chain, rec, L, lm, D);
+              acc = mask_forward<T, !RC, REC, 0>(K, chain, rec, L, lm, vp, D, valid, omega, clamp, m0p, m1p);
             } else {
-              if (RC) mask_cfr<T, 0>(K, rec, L, lm, D);
-              acc = mask_backward<T, !RC, REC, 0>(K, rec, L, lm, vp, D, valid, omega, clamp, m0p, m1p);
+              if (RC) mask_cfr<T, 0>(K, chain, rec, L, lm, D);
+              acc = mask_backward<T, !RC, REC, 0>(K, chain, rec, L, lm, vp, D, valid, omega, clamp, m0p, m1p);
             }
           }
         }
@@ -1058,6 +1171,7 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
     // arc-mask tile: the same min-plus loops as the staged kernel, on global
     // memory (records are warp-uniform loads through L1)
     const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(a.recs + 16 * (int64_t)d.rec_base);
+    const bool chain = d.kind & 8;
     T *lam = reinterpret_cast<T *>(a.lambda) + d.slot_base + lane;
     T *va = reinterpret_cast<T *>(a.delta_out) + d.slot_base + lane;
     T *D = reinterpret_cast<T *>(a.dist) + d.dist_base + lane;
@@ -1065,11 +1179,11 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
     T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
     const T omega = T(a.omega), clamp = T(a.clamp);
     if (L == 32) {
-      acc = MODE == kForward ? mask_forward<T, true, REC, 32>(K, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g)
-                             : mask_backward<T, true, REC, 32>(K, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g);
+      acc = MODE == kForward ? mask_forward<T, true, REC, 32>(K, chain, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g)
+                             : mask_backward<T, true, REC, 32>(K, chain, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g);
     } else {
-      acc = MODE == kForward ? mask_forward<T, true, REC, 0>(K, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g)
-                             : mask_backward<T, true, REC, 0>(K, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g);
+      acc = MODE == kForward ? mask_forward<T, true, REC, 0>(K, chain, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g)
+                             : mask_backward<T, true, REC, 0>(K, chain, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g);
     }
   } else if (lane < L) {
     const int32_t *ho = a.hop_off + d.hop_base;
@@ -1245,8 +1359,24 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {
     p0 = __ldg(a.var_ptr + q);
     p1 = __ldg(a.var_ptr + q + 1);
   }
+  // lane j sums slots p0 + j, p0 + j + G, ... in ascending order; four at a
+  // time, all index loads and then all gathers issued before the adds (two
+  // dependent memory round trips per four slots instead of two per slot)
   T s = T(0);
-  for (int64_t p = p0 + j; p < p1; p += G) s += ld<NC>(db + __ldg(a.var_slots + p));
+  for (int64_t base = p0 + j; base < p1; base += 4 * (int64_t)G) {
+    int32_t q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t p = base + (int64_t)u * G;
+      q[u] = p < p1 ? __ldg(a.var_slots + p) : -1;
+    }
+    T v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = q[u] >= 0 ? ld<NC>(db + q[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (q[u] >= 0) s += v[u];
+  }
   // the group is G consecutive lanes of one warp (G divides 32, threads of
   // the CSR part start at a multiple of 32: n_ell_thr is rounded up)
   for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);

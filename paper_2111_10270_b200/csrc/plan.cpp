@@ -8,6 +8,7 @@
 //     DESIGN.md §5 (partition-contiguous per BDD, made tile-local),
 //     slot arrays, CSR variable -> slots (J_i).
 #include <algorithm>
+#include <initializer_list>
 #include <atomic>
 #include <climits>
 #include <cmath>
@@ -230,24 +231,51 @@ static uint32_t abs_code(uint16_t rel, int32_t next, int32_t nodes) {
   return uint32_t(next + rel);
 }
 
-// Hop records of a shape whose partitions have <= 2 nodes (layout:
-// internal.h HopRec): per partition the 0-/1-arc masks (0 where the arc out of
-// node i of P_h ends in node j of P_{h+1}, or in top on the last partition;
-// +inf otherwise, including every arc to bottom), n0, n1 and w2.
+// Arc masks of partition h of a shape whose partitions have <= 2 nodes:
+// A[4 beta + 2 i + j] = 0 if the beta-arc out of node i of P_h ends in node j
+// of P_{h+1} (or in top on the last partition), +inf otherwise (including
+// every arc to bottom).  Returns the hop type (internal.h HopRec): 1 chain
+// (0-arcs 0->0, 1->1; 1-arc 1->0), 2 root (one node; ->0, ->1), 3 join
+// (0-arc 0->0; 1-arc 1->0), 0 anything else.
+static int hop_masks(const Shape &S, int32_t h, double A[8]) {
+  for (int q = 0; q < 8; ++q) A[q] = INFINITY;
+  const int32_t w = S.hop_start[h + 1] - S.hop_start[h];
+  for (int32_t i = 0; i < w; ++i) {
+    const int32_t n = S.hop_start[h] + i;
+    for (int beta = 0; beta < 2; ++beta) {
+      const uint32_t code = beta ? S.hi[n] : S.lo[n];
+      if (code == kBot) continue;
+      const int j = code == kTop ? 0 : (int)code;  // top only on the last partition
+      A[4 * beta + 2 * i + j] = 0.0;
+    }
+  }
+  auto is = [&](std::initializer_list<int> zeros) {
+    for (int q = 0; q < 8; ++q) {
+      bool z = false;
+      for (int t : zeros) z = z || t == q;
+      if (z != (A[q] == 0.0)) return false;
+    }
+    return true;
+  };
+  return (w == 2 && is({0, 3, 6})) ? 1 : (w == 1 && is({0, 5})) ? 2 : (w == 2 && is({0, 6})) ? 3 : 0;
+}
+
+// kind bit 3: every partition but the first and the last is a chain hop
+static bool chain_shape(const Shape &S) {
+  if (S.max_w > 2) return false;
+  double A[8];
+  for (int32_t h = 1; h + 1 < S.k; ++h)
+    if (hop_masks(S, h, A) != 1) return false;
+  return true;
+}
+
+// Hop records (layout: internal.h HopRec) of a shape whose partitions have
+// <= 2 nodes, in the build precision.
 static void append_recs(const Shape &S, int tsz, std::vector<unsigned char> &out) {
   for (int32_t h = 0; h < S.k; ++h) {
     double A[8];
-    for (double &a : A) a = INFINITY;
+    const int32_t type = hop_masks(S, h, A);
     const int32_t w = S.hop_start[h + 1] - S.hop_start[h];
-    for (int32_t i = 0; i < w; ++i) {
-      const int32_t n = S.hop_start[h] + i;
-      for (int beta = 0; beta < 2; ++beta) {
-        const uint32_t code = beta ? S.hi[n] : S.lo[n];
-        if (code == kBot) continue;
-        const int j = code == kTop ? 0 : (int)code;  // top only on the last partition
-        A[4 * beta + 2 * i + j] = 0.0;
-      }
-    }
     const size_t at = out.size();
     out.resize(at + (size_t)rec_bytes(tsz), 0);
     unsigned char *r = out.data() + at;
@@ -260,7 +288,7 @@ static void append_recs(const Shape &S, int tsz, std::vector<unsigned char> &out
         memcpy(r + 4 * q, &v, 4);
       }
     }
-    const int32_t tail[4] = {S.hop_start[h], S.hop_start[h + 1], w == 2 ? 1 : 0, 0};
+    const int32_t tail[4] = {S.hop_start[h], S.hop_start[h + 1], w == 2 ? 1 : 0, type};
     memcpy(r + 8 * tsz, tail, 16);
   }
   out.resize((out.size() + 15) & ~(size_t)15, 0);
@@ -399,10 +427,10 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // warps vs. issued instructions over the SMs.
   const int tsz = (o && o->precision == 64) ? 8 : 4;
   P.precision = tsz * 8;
-  {
-    const char *nb = getenv("FDOG_NBUF");  // experiment knob: stage buffers per warp (1 or 2)
-    P.NB = (nb && atoi(nb) == 1) ? 1 : 2;
-  }
+  // stage buffers per warp: the recompute design runs single-buffered (more
+  // resident warps hide the TMA latency; measured faster on every BASELINE
+  // workload), the store design double-buffered.  FDOG_NBUF = 1 | 2 overrides.
+  const char *nbuf = getenv("FDOG_NBUF");
   struct PendingTile {
     int kind;                    // bit 0 per-lane topology, bit 1 staged
     int32_t shape;               // kind 0
@@ -415,6 +443,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // launch order
   auto pack = [&](bool rc) {
     std::vector<PendingTile> pend;
+    P.NB = nbuf ? (atoi(nbuf) == 1 ? 1 : 2) : (rc ? 1 : 2);
     auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB) {
       if (rc) return stage_bytes_rc(tsz, kind, K, nodes, L) <= SB && stage_dist_bytes(tsz, nodes, L) <= DB;
       return stage_bytes(tsz, kind, K, nodes, L) <= SB && relax_bytes(tsz, W, L) <= DB;
@@ -487,7 +516,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       size_t full = rows.size() / L * L;
       for (size_t q = 0; q < full; q += L) {
         PendingTile t;
-        t.kind = (staged ? 2 : 0) | k0;  // records also serve the streaming kernel
+        t.kind = (staged ? 2 : 0) | k0 | (k0 && chain_shape(S) ? 8 : 0);  // records also serve the streaming kernel
         t.shape = (int32_t)s;
         t.L = L;
         t.rows.assign(rows.begin() + q, rows.begin() + q + L);

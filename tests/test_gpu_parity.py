@@ -251,6 +251,7 @@ def test_fused_small_path(oracle_mod, monkeypatch, resident, precision, name, ma
     monkeypatch.setenv("FDOG_FUSED", "1")
     gf = F.Solver(p, precision=precision, record_mm=True)
     monkeypatch.setenv("FDOG_FUSED", "0")
+    monkeypatch.setenv("FDOG_SWEEP", "tma")  # same (store-design) tile packing as the fused path
     gd = F.Solver(p, precision=precision, record_mm=True)
     assert gf.stats()["fused_small"] >= 1 and gd.stats()["fused_small"] == 0
     if resident == "0":
