@@ -909,7 +909,7 @@ __device__ __forceinline__ void fetch_desc(TileDesc *dst, const TileDesc *src, i
 // hold lambda, averages, topology and partition offsets only; the distances
 // live in a per-warp scratch column per lane (the DB region) and never touch HBM.
 template <typename T, int MODE, bool REC, bool RC>
-__global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   constexpr bool kUpd = MODE == kForward || MODE == kBackward;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -1116,12 +1116,6 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   __syncwarp();
 }
 
-// Deferred averaging (P:641, A1).  avg_i = (sum over the slots of i, in
-// ascending j, of delta_bar) / |J_i| is written into every slot of i of the
-// OTHER delta buffer, where the next sweep reads it (and overwrites it with its
-// own delta).  Threads [0, ceil(n_ell/2)) take two ELL variables each (slot
-// pair inline, |J_i| <= 2); the remaining threads take one CSR variable each.
-// Thread 0 also resets the sweep's tile counter.
 // ---------------------------------------------------------------------------
 // Streaming sweep for narrow tiles (every partition <= 2 nodes): one warp per
 // tile, no shared memory.  Each lane streams its BDD partition by partition
@@ -1303,6 +1297,15 @@ __device__ __forceinline__ V ld(const V *p) {
   return *p;
 }
 
+// Deferred averaging (P:641, A1).  avg_i = (sum over the slots of i, in
+// ascending j, of delta_bar) / |J_i| is written into every slot of i of the
+// OTHER delta buffer, where the next sweep reads it (and overwrites it with its
+// own delta).  Three sections of whole warps: ELL pairs (|J_i| <= 2, four
+// variables per thread), ELL-4 quads (|J_i| = 3, 4), CSR groups (the rest and
+// every exchanged variable).  avg_kernel's thread 0 also resets the sweep's
+// tile counter.  (A slot-parallel variant of the ELL section -- every slot
+// gathering its partner's delta_bar, coalesced writes -- measured 1.5-2.3x
+// slower: the partner gathers lose the locality of the first slot.)
 // NC: delta_bar is read-only for the kernel's lifetime (the standalone kernel)
 template <typename T, bool NC>
 __device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {

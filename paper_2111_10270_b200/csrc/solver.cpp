@@ -500,7 +500,9 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
       return FDOG_EINVAL;
     }
   }
-  int warps = (int)std::max<size_t>(1, std::min<size_t>(4, (size_t)prop.smem_block / s->warp_bytes));
+  const char *wpb = getenv("FDOG_WPB");  // experiment knob: warps per sweep CTA (default 4, max 16)
+  const size_t wmax = wpb ? std::max(1, std::min(16, atoi(wpb))) : 4;
+  int warps = (int)std::max<size_t>(1, std::min<size_t>(wmax, (size_t)prop.smem_block / s->warp_bytes));
   s->block = warps * 32;
   s->smem = (size_t)warps * s->warp_bytes;
   int bps = 1;
