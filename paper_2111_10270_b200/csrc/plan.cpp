@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <initializer_list>
 #include <atomic>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -294,7 +295,20 @@ static void append_recs(const Shape &S, int tsz, std::vector<unsigned char> &out
   out.resize((out.size() + 15) & ~(size_t)15, 0);
 }
 
+// FDOG_PLAN_TRACE=1: per-phase wall times of build_plan on stderr
+struct PhaseTimer {
+  bool on = getenv("FDOG_PLAN_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char *what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[plan] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
+
 fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
+  PhaseTimer tm;
   fdog_status st = validate(p);
   if (st) return st;
   const int world = o ? std::max(1, o->world) : 1;
@@ -332,6 +346,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       }
     }
 
+  tm.mark("copy + validate");
   shard_rows(p, world, P.owner);
   // global |J_i| and the free-variable term (A13)
   P.deg_global.assign(p->n_vars, 0);
@@ -340,6 +355,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   for (int32_t i = 0; i < p->n_vars; ++i)
     if (P.deg_global[i] == 0 && P.cost[i] < 0) P.free_term += P.cost[i];
 
+  tm.mark("shard + degrees");
   // local rows, dedupe by signature, compile unique signatures in parallel
   P.row_shape.assign(p->n_cons, -1);
   P.local_rows.clear();
@@ -404,6 +420,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     }
   }
 
+  tm.mark("dedupe + compile");
   // ---------------------------------------------------------------- packing
   P.max_hops = 0;
   P.max_width = 0;
@@ -590,6 +607,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
 
     return pend;
   };
+  tm.mark("group by shape");
   bool narrow = true;
   for (size_t s = 0; s < P.shapes.size(); ++s)
     if (!by_shape[s].empty()) narrow = narrow && P.shapes[s].max_w <= 2;
@@ -610,6 +628,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   }
   P.rc = rc;
 
+  tm.mark("budget + tile packing");
   P.tiles.clear();
   P.hop_off.clear();
   P.topo.clear();
@@ -728,34 +747,42 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     set_error("more than 2^31 device slots on one rank");
     return FDOG_ETOOBIG;
   }
+  tm.mark("tile emission");
   // canonical slots and CSR variable -> device slots (j ascending, A1)
   P.canon_slot.clear();
   P.canon_con.clear();
   P.canon_pos.clear();
   std::vector<int64_t> cnt(p->n_vars + 1, 0);
-  for (int32_t j : P.local_rows) {
-    int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
-    for (int32_t h = 0; h < k; ++h) {
-      P.canon_slot.push_back(row_slot[j] + (int64_t)h * row_L[j]);
-      P.canon_con.push_back(j);
-      P.canon_pos.push_back(h);
-      cnt[P.col_var[P.row_ptr[j] + h]]++;
+  P.canon_slot.resize((size_t)P.n_slots);
+  P.canon_con.resize((size_t)P.n_slots);
+  P.canon_pos.resize((size_t)P.n_slots);
+  {
+    size_t q = 0;
+    for (int32_t j : P.local_rows) {
+      const int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
+      const int32_t *vars = P.col_var.data() + P.row_ptr[j];
+      for (int32_t h = 0; h < k; ++h, ++q) {
+        P.canon_slot[q] = row_slot[j] + (int64_t)h * row_L[j];
+        P.canon_con[q] = j;
+        P.canon_pos[q] = h;
+        cnt[vars[h]]++;
+      }
     }
   }
+  tm.mark("canonical slots + CSR");
   // variables in the order of their first device slot, so that neighbouring
   // averaging threads gather and scatter neighbouring slots (the tile layout
   // puts consecutive rows of a shape in consecutive lanes)
+  // (one walk over the device slots in order: a variable is listed where it
+  // first occurs -- the order of a sort by first device slot, without the sort)
   P.var_list.clear();
   {
-    std::vector<int64_t> first(p->n_vars, INT64_MAX);
-    for (size_t q = 0; q < P.canon_slot.size(); ++q) {
-      int32_t i = P.col_var[P.row_ptr[P.canon_con[q]] + P.canon_pos[q]];
-      first[i] = std::min(first[i], P.canon_slot[q]);
-    }
-    for (int32_t i = 0; i < p->n_vars; ++i)
-      if (cnt[i]) P.var_list.push_back(i);
-    std::stable_sort(P.var_list.begin(), P.var_list.end(),
-                     [&](int32_t x, int32_t y) { return first[x] < first[y]; });
+    std::vector<char> seen(p->n_vars, 0);
+    for (int32_t i : P.slot_var)
+      if (i >= 0 && !seen[i]) {
+        seen[i] = 1;
+        P.var_list.push_back(i);
+      }
   }
   P.var_ptr.assign(1, 0);
   std::vector<int64_t> where(p->n_vars, -1);
@@ -769,6 +796,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     int32_t i = P.col_var[P.row_ptr[j] + P.canon_pos[q]];
     P.var_slots[where[i]++] = (int32_t)P.canon_slot[q];
   }
+  tm.mark("variable order");
   // shared variables: held by this rank and by another one
   P.shared_vars.clear();
   P.var_xidx.assign(P.var_list.size(), -1);
@@ -789,6 +817,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     for (size_t q = 0; q < P.shared_vars.size(); ++q) xpos[P.shared_vars[q]] = (int32_t)q;
     for (size_t q = 0; q < P.var_list.size(); ++q) P.var_xidx[q] = xpos[P.var_list[q]];
   }
+  tm.mark("shared variables");
   // averaging layout: variables with <= 2 local slots that are not exchanged
   // keep their slot pair inline (ELL, one 8-byte load); the rest stay in CSR
   {
@@ -827,6 +856,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   for (size_t q = 0; q < P.var_list.size(); ++q)
     if (P.var_xidx[q] >= 0) P.x_local[P.var_xidx[q]] = (int32_t)q;
   for (size_t q = 0; q < P.shared_vars.size(); ++q) P.x_deg[q] = P.deg_global[P.shared_vars[q]];
+  tm.mark("averaging layout");
   return FDOG_OK;
 }
 
@@ -841,6 +871,7 @@ HostImage::~HostImage() {
 // to the build precision) and the distance array with its sentinels (0 for
 // top, +inf for bottom, never overwritten).
 fdog_status build_image(Plan &P) {
+  PhaseTimer tm;
   const int tsz = P.precision == 64 ? 8 : 4;
   size_t sz[kImCount];
   sz[kImTiles] = P.tiles.size() * sizeof(TileDesc);
@@ -919,6 +950,7 @@ fdog_status build_image(Plan &P) {
         ((float *)dist)[bot] = INFINITY;
       }
     }
+  tm.mark("device image");
   return FDOG_OK;
 }
 
