@@ -121,7 +121,7 @@ FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (kWarpHeader + NB * SB +
 // creating a solver is one allocation and one host->device copy.
 enum ImageSection {
   kImTiles = 0, kImHopOff, kImTopo, kImSlotVar, kImVarPtr, kImVarSlots, kImVarXidx, kImDegList, kImEll, kImEllVar,
-  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImRecs, kImCount
+  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImRecs, kImCanon, kImCount
 };
 
 struct HostImage {
@@ -268,5 +268,7 @@ int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream
 int launch_fused_small(int precision, bool record, const SweepArgs &sa, const AvgArgs &aa, int32_t n_iter,
                        int64_t n_slots, int64_t n_dist, size_t smem, void *stream);
 int launch_primal(int precision, const PrimalArgs &a, void *stream);
+// out[q] = src[canon[q]], q < n: per-slot state in canonical (j, h) order
+int launch_gather_canon(int precision, int64_t n, const int32_t *canon, const void *src, void *out, void *stream);
 
 }  // namespace fdog

@@ -1597,10 +1597,21 @@ static const void *sweep_ptr(int precision, int mode, bool rec, bool rc) {
   return rc ? sweep_fn<float, true>(mode, rec) : sweep_fn<float, false>(mode, rec);
 }
 
+// The dynamic shared-memory limit is a per-function attribute shared by every
+// solver in the process: raise it to the device maximum (never lower it to one
+// solver's need, which would break a concurrent solver with a larger budget).
+static cudaError_t allow_max_smem(const void *f) {
+  int dev = 0, mx = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  return e;
+}
+
 int sweep_occupancy(int precision, int mode, bool rec, bool rc, int block, size_t smem, int *blocks_per_sm) {
   const void *f = sweep_ptr(precision, mode, rec, rc);
   if (!f) return 0;
-  cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = allow_max_smem(f);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, smem);
 }
@@ -1696,10 +1707,27 @@ int launch_fused_small(int precision, bool rec, const SweepArgs &sa, const AvgAr
   const void *f = precision == 64 ? (rec ? (const void *)fused_small_kernel<double, true> : (const void *)fused_small_kernel<double, false>)
                                   : (rec ? (const void *)fused_small_kernel<float, true> : (const void *)fused_small_kernel<float, false>);
   if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = allow_max_smem(f);
     if (e != cudaSuccess) return (int)e;
   }
   return launch_pdl(f, dim3(1), dim3(1024), smem, stream, args);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gather_canon_kernel(int64_t n, const int32_t *__restrict__ canon,
+                                                          const T *__restrict__ src, T *__restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = src[canon[q]];
+}
+
+int launch_gather_canon(int precision, int64_t n, const int32_t *canon, const void *src, void *out, void *stream) {
+  if (n <= 0) return 0;
+  const int block = 256, grid = grid_for(n, block);
+  if (precision == 64)
+    gather_canon_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, canon, (const double *)src, (double *)out);
+  else
+    gather_canon_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, canon, (const float *)src, (float *)out);
+  return (int)cudaGetLastError();
 }
 
 int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream) {

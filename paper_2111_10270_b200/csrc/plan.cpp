@@ -614,7 +614,16 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // design choice (experiment knobs: FDOG_SWEEP = rc | tma | stream; FDOG_FUSED)
   const char *sw = getenv("FDOG_SWEEP");
   const char *fz = getenv("FDOG_FUSED");
-  bool rc = narrow && !(sw && (sw[0] == 't' || sw[0] == 's')) && !(fz && fz[0] == '1');
+  // The recompute design halves the HBM bytes of a pass at ~30 % more
+  // instructions.  When the store design's per-pass working set (distances +
+  // slot data) stays resident in the 126 MB L2 across the four kernels of an
+  // iteration, the bytes are cheap and the instructions are not: keep the
+  // store design there (measured: GM-worms-like, 73 MB, store 4 % faster;
+  // CellTrack 160 MB / QAP50 195 MB / MRF 2.2 GB, recompute 6-27 % faster).
+  const double store_bytes = (double)P.n_nodes * 2 * tsz + (double)P.n_slots * 4 * tsz;
+  const bool l2_resident = store_bytes <= 0.75 * 126e6;
+  bool rc = narrow && !(sw && (sw[0] == 't' || sw[0] == 's')) && !(fz && fz[0] == '1') &&
+            (!l2_resident || (sw && sw[0] == 'r'));
   std::vector<PendingTile> pend = pack(rc);
   if (rc) {
     bool direct = false;
@@ -892,6 +901,7 @@ fdog_status build_image(Plan &P) {
   sz[kImLambda0] = P.slot_var.size() * tsz;
   sz[kImDist0] = (size_t)P.n_dist * tsz;
   sz[kImRecs] = P.recs.size();
+  sz[kImCanon] = P.canon_slot.size() * 4;
   size_t at = 0;
   for (int q = 0; q < kImCount; ++q) {
     P.image.off[q] = at;
@@ -931,6 +941,10 @@ fdog_status build_image(Plan &P) {
   put(kImXLocal, P.x_local.data());
   put(kImXDeg, P.x_deg.data());
   put(kImRecs, P.recs.data());
+  {
+    int32_t *cs = (int32_t *)(P.image.data + P.image.off[kImCanon]);
+    for (size_t q = 0; q < P.canon_slot.size(); ++q) cs[q] = (int32_t)P.canon_slot[q];
+  }
   unsigned char *lam = P.image.data + P.image.off[kImLambda0];
   for (size_t q = 0; q < P.slot_var.size(); ++q) {
     const int32_t i = P.slot_var[q];

@@ -116,6 +116,8 @@ struct fdog_solver {
   int32_t SB = 0, DB = 0, NB = 2;
   size_t warp_bytes = 0;
   const unsigned char *d_recs = nullptr;
+  const int32_t *d_canon = nullptr;  // canonical slot -> device slot
+  void *d_canon_out = nullptr;       // getters' staging buffer (T per canonical slot)
   void *d_dist = nullptr;
   int dist_state = 0;  // 0: distances hold shp(v, T); 1: shp(r, v)
   int64_t n_direct = 0, scratch_stride = 0;
@@ -350,15 +352,21 @@ fdog_status fetch_slots(fdog_solver *s, const void *dev, double *out, int64_t le
     set_error("output length %lld < %lld slots", (long long)len, (long long)n);
     return FDOG_EINVAL;
   }
-  std::vector<unsigned char> buf((size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz);
-  CK(cudaMemcpyAsync(buf.data(), dev, (size_t)s->n_dev_slots * s->tsz, cudaMemcpyDeviceToHost, s->stream), "D2H");
-  CK(cudaStreamSynchronize(s->stream), "sync");
+  if (n == 0) return FDOG_OK;
+  // canonical (j, h) order on the device (gather kernel), then one contiguous
+  // copy: straight into the caller's buffer in fp64, through a host buffer
+  // (sequential widening) in fp32
+  const int e = launch_gather_canon(s->precision, n, s->d_canon, dev, s->d_canon_out, s->stream);
+  if (e) return cuda_fail((cudaError_t)e, "gather launch");
+  s->launches++;
   if (s->precision == 64) {
-    const double *b = (const double *)buf.data();
-    for (int64_t q = 0; q < n; ++q) out[q] = b[s->plan->canon_slot[q]];
+    CK(cudaMemcpyAsync(out, s->d_canon_out, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s->stream), "D2H");
+    CK(cudaStreamSynchronize(s->stream), "sync");
   } else {
-    const float *b = (const float *)buf.data();
-    for (int64_t q = 0; q < n; ++q) out[q] = (double)b[s->plan->canon_slot[q]];
+    std::vector<float> buf((size_t)n);
+    CK(cudaMemcpyAsync(buf.data(), s->d_canon_out, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, s->stream), "D2H");
+    CK(cudaStreamSynchronize(s->stream), "sync");
+    for (int64_t q = 0; q < n; ++q) out[q] = (double)buf[q];
   }
   return FDOG_OK;
 }
@@ -562,6 +570,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   const size_t o_scr = carve(s->n_direct ? (size_t)s->grid * (s->block / 32) * s->scratch_stride * s->tsz : 16);
   const size_t o_x = carve((size_t)std::max<int64_t>(P.n_vars, 1));
   const size_t o_und = carve(sizeof(unsigned long long));
+  const size_t o_canon = carve((size_t)std::max<size_t>(P.canon_slot.size(), 1) * s->tsz);
   unsigned char *base = nullptr;
   CK(cudaMalloc((void **)&base, im.bytes + rt), "cudaMalloc");
   s->allocs.push_back(base);
@@ -574,6 +583,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_hop_off = (int32_t *)sec(kImHopOff);
   s->d_topo = (uint32_t *)sec(kImTopo);
   s->d_recs = (const unsigned char *)sec(kImRecs);
+  s->d_canon = (const int32_t *)sec(kImCanon);
   s->d_slot_var = (int32_t *)sec(kImSlotVar);
   s->d_var_ptr = (int64_t *)sec(kImVarPtr);
   s->d_var_slots = (int32_t *)sec(kImVarSlots);
@@ -602,6 +612,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_scratch = r + o_scr;
   s->d_x = (uint8_t *)(r + o_x);
   s->d_undecided = (unsigned long long *)(r + o_und);
+  s->d_canon_out = r + o_canon;
   s->external = s->world > 1 && !o->nccl_unique_id;
   if (s->world > 1 && !s->external && (st = init_nccl(s, o))) return st;
 

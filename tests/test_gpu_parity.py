@@ -391,3 +391,24 @@ def test_full_size_gm_fp64_sampled(oracle_mod):
     a, b = g.lam(), o.lam()
     assert np.max(np.abs(a - b) - 1e-9 * np.abs(b)) <= 1e-9 * s
     assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+
+
+def test_concurrent_solvers_with_different_budgets(oracle_mod):
+    """Several solvers alive in one process with different per-warp shared-memory
+    budgets and sweep designs (the dynamic shared-memory limit is a
+    per-function attribute shared by all of them): interleaved passes, each
+    still matches its own oracle."""
+    probs = [synth.gm_worms_like(31, n_src=50, k_cand=6, knn=6), synth.qap(31, n=7),
+             synth.mrf_potts(31, H=8, W=9, L=5), synth.random_ilp(31, n=30, m=40, kmax=9, coef=4)]
+    gs = [F.Solver(p, precision=64) for p in probs]
+    os_ = [oracle_mod.Oracle(p) for p in probs]
+    budgets = {g.stats()["sweep_smem_per_warp"] for g in gs}
+    assert len(budgets) > 1
+    for t in range(4):
+        for g, o in zip(gs, os_):
+            g.pass_(t % 2 == 0, 0.5)
+            o.pass_(t % 2 == 0, 0.5)
+    for g, o, p in zip(gs, os_, probs):
+        s = _s(p)
+        assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s
+        assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
