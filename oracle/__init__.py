@@ -58,6 +58,8 @@ def _load():
         lib.oracle_destroy.restype = None
         lib.oracle_pass.argtypes = [P, C.c_int, C.c_double]
         lib.oracle_iterate.argtypes = [P, C.c_int, C.c_double]
+        lib.oracle_pass_seq.argtypes = [P, C.c_int, C.c_double]
+        lib.oracle_iterate_seq.argtypes = [P, C.c_int, C.c_double]
         lib.oracle_lower_bound.argtypes = [P, P]
         lib.oracle_dual_energy.argtypes = [P, P]
         lib.oracle_finalize.argtypes = [P]
@@ -132,6 +134,13 @@ class Oracle:
 
     def iterate(self, n: int, omega: float = 0.5):
         self._chk(self._lib.oracle_iterate(self._h, int(n), float(omega)), "iterate")
+
+    def pass_seq(self, forward: bool, omega: float = 0.5):
+        """Non-deferred (sequential) min-marginal averaging pass."""
+        self._chk(self._lib.oracle_pass_seq(self._h, 1 if forward else 0, float(omega)), "pass_seq")
+
+    def iterate_seq(self, n: int, omega: float = 0.5):
+        self._chk(self._lib.oracle_iterate_seq(self._h, int(n), float(omega)), "iterate_seq")
 
     def lower_bound(self) -> float:
         x = C.c_double()

@@ -60,6 +60,7 @@ struct oracle_solver {
   obdd *bdd;
   int64_t n_slots;
   int32_t *slot_var;   /* i of slot (j, h)                         */
+  int32_t *slot_bdd;   /* j of slot (j, h)                         */
   double *lambda;      /* lambda_i^j per slot                      */
   double *delta_bar;   /* omega * d of the last pass (deferred)    */
   double *delta_new;   /* this pass                                */
@@ -384,7 +385,7 @@ static void free_solver(oracle_solver *s) {
       free(s->bdd[j].cfr); free(s->bdd[j].ctt);
     }
   }
-  free(s->bdd); free(s->cost); free(s->slot_var); free(s->lambda); free(s->delta_bar);
+  free(s->bdd); free(s->cost); free(s->slot_var); free(s->slot_bdd); free(s->lambda); free(s->delta_bar);
   free(s->delta_new); free(s->m0); free(s->m1); free(s->var_ptr); free(s->var_slots);
   free(s->avg); free(s->energy);
   free(s);
@@ -456,6 +457,7 @@ int oracle_create(const oracle_problem *p, double clamp, int n_threads, oracle_s
   {
     int64_t S = s->n_slots ? s->n_slots : 1;
     s->slot_var = (int32_t *)malloc((size_t)S * sizeof(int32_t));
+    s->slot_bdd = (int32_t *)malloc((size_t)S * sizeof(int32_t));
     s->lambda = (double *)malloc((size_t)S * sizeof(double));
     s->delta_bar = (double *)calloc((size_t)S, sizeof(double));
     s->delta_new = (double *)calloc((size_t)S, sizeof(double));
@@ -464,7 +466,7 @@ int oracle_create(const oracle_problem *p, double clamp, int n_threads, oracle_s
     s->var_ptr = (int64_t *)calloc((size_t)p->n_vars + 1, sizeof(int64_t));
     s->var_slots = (int64_t *)malloc((size_t)S * sizeof(int64_t));
     s->avg = (double *)calloc((size_t)(p->n_vars ? p->n_vars : 1), sizeof(double));
-    if (!s->slot_var || !s->lambda || !s->delta_bar || !s->delta_new || !s->m0 || !s->m1 ||
+    if (!s->slot_var || !s->slot_bdd || !s->lambda || !s->delta_bar || !s->delta_new || !s->m0 || !s->m1 ||
         !s->var_ptr || !s->var_slots || !s->avg)
       goto fail;
   }
@@ -472,6 +474,7 @@ int oracle_create(const oracle_problem *p, double clamp, int n_threads, oracle_s
     for (int32_t h = 0; h < s->bdd[j].k; ++h) {
       int32_t i = s->bdd[j].vars[h];
       s->slot_var[s->bdd[j].slot0 + h] = i;
+      s->slot_bdd[s->bdd[j].slot0 + h] = j;
       s->var_ptr[i + 1]++;
     }
   for (int32_t i = 0; i < p->n_vars; ++i) s->var_ptr[i + 1] += s->var_ptr[i];
@@ -547,6 +550,101 @@ int oracle_pass(oracle_solver *s, int forward, double omega) {
   s->passes++;
   s->ctt_ok = !forward; /* a forward pass leaves shp(r,v) valid, a backward pass shp(v,T) */
   s->cfr_ok = forward;
+  return O_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* Non-deferred min-marginal averaging ("If mbar <- m, then    */
+/* (dual_update) matches the update from [lange2021efficient]"; the      */
+/* sequential scheme the deferral replaces).                  */
+/*                                                                       */
+/* Variables are visited one at a time, in ascending (forward) or        */
+/* descending (backward) global index.  At variable i every subproblem   */
+/* j in J_i computes m_ij at its current lambda^j (via P:312),    */
+/* then all of them update at once:                                      */
+/*   lambda_i^j <- lambda_i^j - omega d_ij + (1/|J_i|) sum_k omega d_ik   */
+/* (the update of Alg. parallel-mma line 'lambda-update' with mbar = m;  */
+/* d = clamp(m1 - m0), A5).  Each BDD orders its variables ascending     */
+/* (A12), so BDD j reaches hop h exactly when variable I_j[h] is visited */
+/* and the incremental shortest paths of P:315-342 apply unchanged.      */
+/* sum_j lambda_i^j = c_i after every variable, so no deferred term       */
+/* remains (delta_bar = 0) and sum_j E^j is the bound.                   */
+int oracle_pass_seq(oracle_solver *s, int forward, double omega) {
+  if (!s) return O_EINVAL;
+  if (!(omega > 0.0 && omega <= 1.0)) return O_EINVAL; /* A14 */
+  /* a pending deferred correction is not part of this scheme */
+  for (int64_t q = 0; q < s->n_slots; ++q)
+    if (s->delta_bar[q] != 0.0) return O_ESTATE;
+  if (forward && !s->ctt_ok)
+    for (int32_t q = 0; q < s->n_cons; ++q) backward_dp(&s->bdd[q], s->lambda + s->bdd[q].slot0);
+  if (!forward && !s->cfr_ok)
+    for (int32_t q = 0; q < s->n_cons; ++q) forward_dp(&s->bdd[q], s->lambda + s->bdd[q].slot0);
+  double *dl = s->delta_new; /* omega * d_ij of the current variable's slots */
+  for (int32_t t = 0; t < s->n_vars; ++t) {
+    const int32_t i = forward ? t : s->n_vars - 1 - t;
+    const int64_t q0 = s->var_ptr[i], q1 = s->var_ptr[i + 1];
+    if (q0 == q1) continue;
+    /* min-marginals of i in every j in J_i (ascending j) */
+    for (int64_t q = q0; q < q1; ++q) {
+      const int64_t slot = s->var_slots[q];
+      obdd *d = &s->bdd[s->slot_bdd[slot]];
+      double *lam = s->lambda + d->slot0;
+      const int32_t h = (int32_t)(slot - d->slot0);
+      if (forward) {
+        if (h == 0) {
+          d->cfr[0] = 0.0; /* shp(r, r) */
+        } else {
+          /* shp(r, v), v in P_h, from P_{h-1} with the updated lambda_{h-1} (A4) */
+          for (int32_t v = d->hop_start[h]; v < d->hop_start[h + 1]; ++v) {
+            double best = INFINITY;
+            for (int32_t u = d->hop_start[h - 1]; u < d->hop_start[h]; ++u) {
+              if (d->lo[u] == v && d->cfr[u] < best) best = d->cfr[u];
+              if (d->hi[u] == v && d->cfr[u] + lam[h - 1] < best) best = d->cfr[u] + lam[h - 1];
+            }
+            d->cfr[v] = best;
+          }
+        }
+      }
+      double m0, m1;
+      min_marginals_at(d, lam, h, &m0, &m1);
+      s->m0[slot] = m0;
+      s->m1[slot] = m1;
+      dl[slot] = omega * mm_difference(m1, m0, s->clamp);
+    }
+    /* the averaging of the same min-marginals (j ascending, A1) */
+    double sum = 0.0;
+    for (int64_t q = q0; q < q1; ++q) sum += dl[s->var_slots[q]];
+    const double avg = sum / (double)(q1 - q0);
+    for (int64_t q = q0; q < q1; ++q) {
+      const int64_t slot = s->var_slots[q];
+      obdd *d = &s->bdd[s->slot_bdd[slot]];
+      double *lam = s->lambda + d->slot0;
+      const int32_t h = (int32_t)(slot - d->slot0);
+      lam[h] = lam[h] - dl[slot] + avg;
+      if (!forward) /* shp(v, T), v in P_h, with the updated lambda_h */
+        for (int32_t v = d->hop_start[h]; v < d->hop_start[h + 1]; ++v) {
+          double a = ctt_of(d, d->lo[v]);
+          double b = lam[h] + ctt_of(d, d->hi[v]);
+          d->ctt[v] = a < b ? a : b;
+        }
+    }
+  }
+  for (int64_t q = 0; q < s->n_slots; ++q) s->delta_bar[q] = 0.0;
+  s->lb = raw_energy(s);
+  s->passes++;
+  s->ctt_ok = !forward;
+  s->cfr_ok = forward;
+  return O_OK;
+}
+
+int oracle_iterate_seq(oracle_solver *s, int n_iter, double omega) {
+  if (!s || n_iter < 0) return O_EINVAL;
+  for (int t = 0; t < n_iter; ++t) {
+    int rc = oracle_pass_seq(s, 1, omega);
+    if (rc) return rc;
+    rc = oracle_pass_seq(s, 0, omega);
+    if (rc) return rc;
+  }
   return O_OK;
 }
 

@@ -53,6 +53,13 @@ void oracle_destroy(oracle_solver *s);
 int oracle_pass(oracle_solver *s, int forward, double omega);
 /* n_iter x (forward pass, backward pass). */
 int oracle_iterate(oracle_solver *s, int n_iter, double omega);
+/* Non-deferred variant ([lange2021efficient]): variables visited
+ * one at a time in ascending (forward) / descending (backward) global order;
+ * all j in J_i compute m_ij, then lambda_i^j <- lambda_i^j - omega d_ij +
+ * mean_k omega d_ik.  Needs delta_bar = 0 (fresh, finalized, or after another
+ * _seq pass; else 6).  Leaves delta_bar = 0; the bound is sum_j E^j. */
+int oracle_pass_seq(oracle_solver *s, int forward, double omega);
+int oracle_iterate_seq(oracle_solver *s, int n_iter, double omega);
 /* Lifted lower bound (A7) of the last completed pass, or sum_j E^j at init /
  * after finalize. */
 int oracle_lower_bound(const oracle_solver *s, double *out);
