@@ -143,6 +143,18 @@ void fdog_destroy(fdog_solver *s);
 fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega);
 /* One pass only: forward (1, ascending) or backward (0). */
 fdog_status fdog_pass(fdog_solver *s, int32_t forward, double omega);
+/* Non-deferred (sequential) min-marginal averaging, P:660-661 ("if mbar <- m,
+ * (dual_update) matches the update from [lange2021efficient]"):
+ * variables are visited in ascending (forward) / descending (backward) global
+ * order; at variable i every j in J_i computes m_ij at its current lambda^j and
+ * all update at once, lambda_i^j += -omega d_ij + mean_k omega d_ik.  Run as a
+ * level schedule (variables of one level share no BDD): one kernel per level,
+ * the schedule built on the first call.  Single-GPU (FDOG_ESTATE if world > 1);
+ * needs delta_bar = 0 (fresh solver, after fdog_finalize, or after another _seq
+ * pass; else FDOG_ESTATE).  Leaves delta_bar = 0 and lower_bound = sum_j E^j.
+ * fdog_iterate_seq: n x (forward, backward). */
+fdog_status fdog_pass_seq(fdog_solver *s, int32_t forward, double omega);
+fdog_status fdog_iterate_seq(fdog_solver *s, int32_t n_iter, double omega);
 /* External exchange (world > 1 with nccl_unique_id == NULL): the caller sums
  * the exchange vectors across ranks itself (e.g. torch.distributed, or several
  * rank solvers in one process).  A pass is then two calls:

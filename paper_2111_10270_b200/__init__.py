@@ -65,7 +65,8 @@ class KernelTime(C.Structure):
 
 EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdog_plan_stats", "fdog_plan_slot_map",
            "fdog_plan_bdd", "fdog_plan_owner", "fdog_plan_shared_vars", "fdog_create",
-           "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_lower_bound",
+           "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_pass_seq", "fdog_iterate_seq",
+           "fdog_lower_bound",
            "fdog_finalize", "fdog_finalize_averaged", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
            "fdog_get_deferred", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
            "fdog_profile", "fdog_profile_reset", "fdog_profile_enable", "fdog_pass_begin", "fdog_pass_end",
@@ -100,6 +101,8 @@ def load():
         "fdog_destroy": ([P], None),
         "fdog_iterate": ([P, i32, dbl], C.c_int),
         "fdog_pass": ([P, i32, dbl], C.c_int),
+        "fdog_pass_seq": ([P, i32, dbl], C.c_int),
+        "fdog_iterate_seq": ([P, i32, dbl], C.c_int),
         "fdog_lower_bound": ([P, P], C.c_int),
         "fdog_finalize": ([P], C.c_int),
         "fdog_finalize_averaged": ([P], C.c_int),
@@ -272,6 +275,13 @@ class Solver:
 
     def pass_(self, forward: bool, omega: float = 0.5):
         _check(self._lib.fdog_pass(self._h, 1 if forward else 0, float(omega)), "fdog_pass")
+
+    def pass_seq(self, forward: bool, omega: float = 0.5):
+        """Non-deferred (sequential) min-marginal averaging pass."""
+        _check(self._lib.fdog_pass_seq(self._h, 1 if forward else 0, float(omega)), "fdog_pass_seq")
+
+    def iterate_seq(self, n: int, omega: float = 0.5):
+        _check(self._lib.fdog_iterate_seq(self._h, int(n), float(omega)), "fdog_iterate_seq")
 
     def lower_bound(self) -> float:
         x = C.c_double()

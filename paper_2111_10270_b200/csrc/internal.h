@@ -253,6 +253,31 @@ struct PrimalArgs {
   uint64_t seed;
 };
 
+// Non-deferred (sequential) min-marginal averaging: one
+// kernel per level of the variable schedule (solver.cpp seq_schedule); thread
+// q in [q0, q1) handles the q-th variable of the pass order and all its slots.
+struct SeqArgs {
+  const TileDesc *tiles;
+  const int32_t *hop_off;
+  const uint32_t *topo;
+  const int32_t *slot_tile;   // device slot -> tile
+  const int64_t *ptr;         // per pass-order variable: its slots [ptr[q], ptr[q+1]) in slots
+  const int32_t *slots;       // device slots, j ascending within a variable
+  void *lambda;               // T*
+  void *dist;                 // T*, store-design distances (shp(v,T) before a forward pass, shp(r,v) before a backward one)
+  void *delta;                // T*, scratch: omega * d per slot
+  void *m0, *m1;              // T*, recorded min-marginals (may be null)
+  double *e_lane;             // per (tile, lane): E^j, written at the BDD's last visited partition
+  double omega, clamp;
+  int32_t forward;
+};
+int launch_seq_level(int precision, bool record, const SeqArgs &a, int64_t q0, int64_t q1, void *stream);
+// per tile: lb_part[t] = sum over the tile's valid lanes of e_lane (fixed order)
+int launch_seq_bound(const TileDesc *tiles, int32_t n_tiles, const double *e_lane, double *lb_part, void *stream);
+// store-design distances of every BDD from the current lambda, in global memory:
+// forward = 0: shp(v, T) (before a forward pass); 1: shp(r, v) (before a backward pass)
+int launch_dist_dp(int precision, const SeqArgs &a, int32_t n_tiles, int32_t forward, void *stream);
+
 // returns the cudaError_t as int
 // rc: recompute design (sweep_kernel<..., RC = true>; plan packed with Plan::rc)
 int launch_sweep(int precision, int mode, bool record, bool rc, const SweepArgs &a, int grid, int block,

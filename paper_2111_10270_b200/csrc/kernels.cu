@@ -1580,6 +1580,171 @@ __global__ void add_deferred_kernel(int64_t n, T *__restrict__ lambda, T *__rest
 }
 
 
+// ---------------------------------------------------------------------------
+// Non-deferred min-marginal averaging (oracle_pass_seq).  The
+// variables of a pass are ordered by a level schedule (solver.cpp): a
+// variable's level is one more than the largest level of its predecessor in
+// any of its BDDs, so variables of one level share no BDD and can be updated
+// together -- the same result as visiting them one by one in ascending
+// (descending) index.  Thread q handles one variable: the min-marginals in
+// every j in J_i (store-design distances in global memory), their
+// average, the dual update, and the advance of each BDD by one partition
+// (forward: shp(r, .) of P_{h+1}, P:319-324 with A4; backward: shp(., T) of
+// P_h).  Generic in the partition width.
+struct SeqLoc {
+  int32_t h, lane, L, K, nodes;
+  const int32_t *ho;   // partition offsets of the tile
+  const uint32_t *tp;  // topology of node n at tp[n * ts]
+  int32_t ts;
+  int64_t dbase;       // distance of node n: dist[dbase + n * L]
+};
+
+__device__ __forceinline__ SeqLoc seq_locate(const SeqArgs &a, int32_t ds, int32_t &t) {
+  t = __ldg(a.slot_tile + ds);
+  const TileDesc &d = a.tiles[t];
+  SeqLoc l;
+  l.L = d.lanes;
+  const int64_t off = ds - d.slot_base;
+  l.h = (int32_t)(off / l.L);
+  l.lane = (int32_t)(off - (int64_t)l.h * l.L);
+  l.K = d.K;
+  l.nodes = d.nodes;
+  l.ho = a.hop_off + d.hop_base;
+  l.ts = (d.kind & 1) ? l.L : 1;
+  l.tp = a.topo + d.topo_base + ((d.kind & 1) ? l.lane : 0);
+  l.dbase = d.dist_base + l.lane;
+  return l;
+}
+
+template <typename T, bool REC>
+__global__ void __launch_bounds__(128) seq_level_kernel(const SeqArgs a, int64_t q0, int64_t q1) {
+  const int64_t q = q0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= q1) return;
+  T *__restrict__ lam = reinterpret_cast<T *>(a.lambda);
+  T *__restrict__ D = reinterpret_cast<T *>(a.dist);
+  T *__restrict__ dl = reinterpret_cast<T *>(a.delta);
+  const T omega = T(a.omega), clamp = T(a.clamp), inf = t_inf<T>();
+  const int64_t p0 = a.ptr[q], p1 = a.ptr[q + 1];
+  // min-marginals of the variable in every j in J_i (ascending j)
+  T sum = T(0);
+  for (int64_t p = p0; p < p1; ++p) {
+    const int32_t ds = a.slots[p];
+    int32_t t;
+    const SeqLoc l = seq_locate(a, ds, t);
+    const int n0 = l.ho[l.h], n1 = l.ho[l.h + 1];
+    if (a.forward && l.h == 0) D[l.dbase] = T(0);  // shp(r, r)
+    T m0 = inf, m1r = inf;
+    for (int n = n0; n < n1; ++n) {
+      const uint32_t e = l.tp[(int64_t)n * l.ts];
+      const T c = D[l.dbase + (int64_t)n * l.L];
+      m0 = fmin(m0, c + D[l.dbase + (int64_t)(e & 0xFFFFu) * l.L]);
+      m1r = fmin(m1r, c + D[l.dbase + (int64_t)(e >> 16) * l.L]);
+    }
+    const T lv = lam[ds];
+    const T m1 = lv + m1r;
+    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+    dl[ds] = delta;
+    if (REC) {
+      reinterpret_cast<T *>(a.m0)[ds] = m0;
+      reinterpret_cast<T *>(a.m1)[ds] = m1;
+    }
+    sum += delta;
+  }
+  const T avg = sum / T(p1 - p0);
+  // update every slot, then advance its BDD by one partition
+  for (int64_t p = p0; p < p1; ++p) {
+    const int32_t ds = a.slots[p];
+    int32_t t;
+    const SeqLoc l = seq_locate(a, ds, t);
+    const T lam_new = add_rn(sub_rn(lam[ds], dl[ds]), avg);
+    lam[ds] = lam_new;
+    const int n0 = l.ho[l.h], n1 = l.ho[l.h + 1];
+    if (a.forward) {
+      if (l.h + 1 < l.K) {
+        const int n2 = l.ho[l.h + 2];
+        for (int v = n1; v < n2; ++v) {
+          T best = inf;
+          for (int n = n0; n < n1; ++n) {
+            const uint32_t e = l.tp[(int64_t)n * l.ts];
+            const T c = D[l.dbase + (int64_t)n * l.L];
+            if ((int)(e & 0xFFFFu) == v) best = fmin(best, c);
+            if ((int)(e >> 16) == v) best = fmin(best, c + lam_new);
+          }
+          D[l.dbase + (int64_t)v * l.L] = best;
+        }
+      } else {
+        // last partition: E^j = shp(r, T) at the updated lambda
+        T e_j = inf;
+        for (int n = n0; n < n1; ++n) {
+          const uint32_t e = l.tp[(int64_t)n * l.ts];
+          const T c = D[l.dbase + (int64_t)n * l.L];
+          e_j = fmin(e_j, fmin(c + D[l.dbase + (int64_t)(e & 0xFFFFu) * l.L],
+                               c + lam_new + D[l.dbase + (int64_t)(e >> 16) * l.L]));
+        }
+        a.e_lane[(int64_t)t * 32 + l.lane] = (double)e_j;
+      }
+    } else {
+      for (int n = n0; n < n1; ++n) {
+        const uint32_t e = l.tp[(int64_t)n * l.ts];
+        D[l.dbase + (int64_t)n * l.L] = fmin(D[l.dbase + (int64_t)(e & 0xFFFFu) * l.L],
+                                             lam_new + D[l.dbase + (int64_t)(e >> 16) * l.L]);
+      }
+      if (l.h == 0) a.e_lane[(int64_t)t * 32 + l.lane] = (double)D[l.dbase];  // E^j = shp(r, T)
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) seq_bound_kernel(const TileDesc *tiles, int32_t n_tiles,
+                                                        const double *e_lane, double *lb_part) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_tiles) return;
+  const int nl = tiles[t].n_lanes;
+  double s = 0.0;
+  for (int l = 0; l < nl; ++l) s += e_lane[(int64_t)t * 32 + l];
+  lb_part[t] = s;
+}
+
+// one thread per (tile, lane): the store-design distances from the current lambda
+template <typename T>
+__global__ void __launch_bounds__(256) dist_dp_kernel(const SeqArgs a, int32_t n_tiles, int32_t forward) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int32_t t = (int32_t)(g >> 5), lane = (int32_t)(g & 31);
+  if (t >= n_tiles) return;
+  const TileDesc &d = a.tiles[t];
+  if (lane >= d.lanes) return;
+  const int L = d.lanes, K = d.K;
+  const int32_t *ho = a.hop_off + d.hop_base;
+  const int ts = (d.kind & 1) ? L : 1;
+  const uint32_t *tp = a.topo + d.topo_base + ((d.kind & 1) ? lane : 0);
+  T *D = reinterpret_cast<T *>(a.dist) + d.dist_base + lane;
+  const T *lam = reinterpret_cast<const T *>(a.lambda) + d.slot_base + lane;
+  const T inf = t_inf<T>();
+  if (!forward) {  // shp(v, T)
+    for (int h = K - 1; h >= 0; --h) {
+      const T l = lam[(int64_t)h * L];
+      for (int n = ho[h]; n < ho[h + 1]; ++n) {
+        const uint32_t e = tp[(int64_t)n * ts];
+        D[(int64_t)n * L] = fmin(D[(int64_t)(e & 0xFFFFu) * L], l + D[(int64_t)(e >> 16) * L]);
+      }
+    }
+  } else {  // shp(r, v), P:319-324 (A4)
+    D[0] = T(0);
+    for (int h = 0; h + 1 < K; ++h) {
+      const T l = lam[(int64_t)h * L];
+      for (int v = ho[h + 1]; v < ho[h + 2]; ++v) {
+        T best = inf;
+        for (int n = ho[h]; n < ho[h + 1]; ++n) {
+          const uint32_t e = tp[(int64_t)n * ts];
+          const T c = D[(int64_t)n * L];
+          if ((int)(e & 0xFFFFu) == v) best = fmin(best, c);
+          if ((int)(e >> 16) == v) best = fmin(best, c + l);
+        }
+        D[(int64_t)v * L] = best;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 
 template <typename T, bool RC>
@@ -1727,6 +1892,38 @@ int launch_gather_canon(int precision, int64_t n, const int32_t *canon, const vo
     gather_canon_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, canon, (const double *)src, (double *)out);
   else
     gather_canon_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, canon, (const float *)src, (float *)out);
+  return (int)cudaGetLastError();
+}
+
+int launch_seq_level(int precision, bool record, const SeqArgs &a, int64_t q0, int64_t q1, void *stream) {
+  if (q1 <= q0) return 0;
+  const int block = 128;
+  const unsigned grid = (unsigned)((q1 - q0 + block - 1) / block);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (precision == 64) {
+    if (record) seq_level_kernel<double, true><<<grid, block, 0, st>>>(a, q0, q1);
+    else seq_level_kernel<double, false><<<grid, block, 0, st>>>(a, q0, q1);
+  } else {
+    if (record) seq_level_kernel<float, true><<<grid, block, 0, st>>>(a, q0, q1);
+    else seq_level_kernel<float, false><<<grid, block, 0, st>>>(a, q0, q1);
+  }
+  return (int)cudaGetLastError();
+}
+
+int launch_seq_bound(const TileDesc *tiles, int32_t n_tiles, const double *e_lane, double *lb_part, void *stream) {
+  if (n_tiles <= 0) return 0;
+  seq_bound_kernel<<<(n_tiles + 255) / 256, 256, 0, (cudaStream_t)stream>>>(tiles, n_tiles, e_lane, lb_part);
+  return (int)cudaGetLastError();
+}
+
+int launch_dist_dp(int precision, const SeqArgs &a, int32_t n_tiles, int32_t forward, void *stream) {
+  if (n_tiles <= 0) return 0;
+  const int64_t threads = (int64_t)n_tiles * 32;
+  const unsigned grid = (unsigned)((threads + 255) / 256);
+  if (precision == 64)
+    dist_dp_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(a, n_tiles, forward);
+  else
+    dist_dp_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(a, n_tiles, forward);
   return (int)cudaGetLastError();
 }
 

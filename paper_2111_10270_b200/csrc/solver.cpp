@@ -69,6 +69,14 @@ struct fdog_solver {
   bool external = false;  // world > 1 without NCCL: the caller performs the exchange
   bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
   bool rc = false;           // recompute design (Plan::rc): no distance traffic, no dist_state
+  bool dbar_zero = true;     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
+  // non-deferred variant (fdog_pass_seq): level schedule, built on first use
+  bool seq_ready = false;
+  std::vector<int64_t> seq_lvl[2];        // [backward, forward]: level boundaries in pass order
+  int64_t *d_seq_ptr[2] = {nullptr, nullptr};
+  int32_t *d_seq_slots[2] = {nullptr, nullptr};
+  int32_t *d_slot_tile = nullptr;
+  double *d_e_lane = nullptr;
   int32_t static_sched = 0;  // TMA sweep: round-robin tiles only
 
   // host copies needed by getters
@@ -313,9 +321,10 @@ fdog_status pass_stage(fdog_solver *s, bool forward, double omega, int stage) {
   if (s->external && (st = run_avg_finish(s))) return st;
   st = run_sweep(s, forward ? kForward : kBackward, omega);
   if (st) return st;
-  s->dist_state = forward ? 1 : 0;
+  s->dist_state = s->rc ? 2 : (forward ? 1 : 0);  // (the recompute design keeps no distances in HBM)
   s->cur ^= 1;  // mbar <- m
   s->passes++;
+  s->dbar_zero = false;
   return FDOG_OK;
 }
 
@@ -326,8 +335,142 @@ fdog_status do_pass(fdog_solver *s, bool forward, double omega) {
 
 fdog_status energy(fdog_solver *s) {
   fdog_status st = run_sweep(s, kEnergy, 0.5);
-  if (!st) s->dist_state = 0;
+  if (!st) s->dist_state = s->rc ? 2 : 0;
   return st;
+}
+
+// ---- non-deferred variant ---------------------------
+// Level schedule of one pass direction: level(i) = 1 + max over the rows of i
+// of the level of i's predecessor (forward: the previous variable of the row;
+// backward: the next one).  Variables of one level share no BDD, so a level is
+// one kernel launch and the pass equals visiting the variables one by one.
+fdog_status seq_schedule(fdog_solver *s) {
+  if (s->seq_ready) return FDOG_OK;
+  const Plan &P = *s->plan;
+  const int64_t S = (int64_t)P.canon_slot.size();
+  const int32_t n = P.n_vars;
+  // per variable: canonical slots, j ascending
+  std::vector<int64_t> vptr(n + 1, 0);
+  for (int64_t q = 0; q < S; ++q) vptr[P.col_var[P.row_ptr[P.canon_con[q]] + P.canon_pos[q]] + 1]++;
+  for (int32_t i = 0; i < n; ++i) vptr[i + 1] += vptr[i];
+  std::vector<int64_t> vq(S), fill(vptr.begin(), vptr.end() - 1);
+  for (int64_t q = 0; q < S; ++q) vq[fill[P.col_var[P.row_ptr[P.canon_con[q]] + P.canon_pos[q]]]++] = q;
+  std::vector<int32_t> slot_tile(std::max<int64_t>(s->n_dev_slots, 1), 0);
+  for (int32_t t = 0; t < (int32_t)P.tiles.size(); ++t) {
+    const TileDesc &d = P.tiles[t];
+    for (int64_t x = 0; x < (int64_t)d.K * d.lanes; ++x) slot_tile[d.slot_base + x] = t;
+  }
+  const size_t bytes = slot_tile.size() * 4 + 2 * ((size_t)(n + 1) * 8 + (size_t)std::max<int64_t>(S, 1) * 4) +
+                       (size_t)std::max(s->n_tiles, 1) * 32 * 8 + 8 * 256;  // + alignment of six sections
+  unsigned char *base = nullptr;
+  CK(cudaMalloc((void **)&base, bytes), "cudaMalloc (seq schedule)");
+  s->allocs.push_back(base);
+  size_t at = 0;
+  auto carve = [&](size_t b) {
+    unsigned char *p = base + at;
+    at += (b + 255) & ~(size_t)255;
+    return p;
+  };
+  s->d_slot_tile = (int32_t *)carve(slot_tile.size() * 4);
+  CK(cudaMemcpyAsync(s->d_slot_tile, slot_tile.data(), slot_tile.size() * 4, cudaMemcpyHostToDevice, s->stream), "H2D");
+  for (int dir = 0; dir < 2; ++dir) {
+    const bool fwd = dir == 1;
+    std::vector<int32_t> lvl(n, -1);
+    int32_t nl = 0;
+    for (int32_t t = 0; t < n; ++t) {
+      const int32_t i = fwd ? t : n - 1 - t;
+      if (vptr[i] == vptr[i + 1]) continue;
+      int32_t L = 0;
+      for (int64_t x = vptr[i]; x < vptr[i + 1]; ++x) {
+        const int64_t q = vq[x];
+        const int32_t j = P.canon_con[q], pos = P.canon_pos[q];
+        const int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
+        const int32_t nb = fwd ? pos - 1 : pos + 1;  // the row's neighbour visited before i
+        if (nb >= 0 && nb < k) L = std::max(L, lvl[P.col_var[P.row_ptr[j] + nb]] + 1);
+      }
+      lvl[i] = L;
+      nl = std::max(nl, L + 1);
+    }
+    // pass order: by level, then variable (counting sort)
+    std::vector<int64_t> cnt(nl + 1, 0);
+    for (int32_t i = 0; i < n; ++i)
+      if (lvl[i] >= 0) cnt[lvl[i] + 1]++;
+    for (int32_t l = 0; l < nl; ++l) cnt[l + 1] += cnt[l];
+    s->seq_lvl[dir] = cnt;
+    std::vector<int32_t> order(cnt[nl]);
+    std::vector<int64_t> f(cnt.begin(), cnt.end() - 1);
+    for (int32_t i = 0; i < n; ++i)
+      if (lvl[i] >= 0) order[f[lvl[i]]++] = i;
+    std::vector<int64_t> ptr(order.size() + 1, 0);
+    std::vector<int32_t> slots;
+    slots.reserve(S);
+    for (size_t o = 0; o < order.size(); ++o) {
+      const int32_t i = order[o];
+      for (int64_t x = vptr[i]; x < vptr[i + 1]; ++x) slots.push_back((int32_t)P.canon_slot[vq[x]]);
+      ptr[o + 1] = (int64_t)slots.size();
+    }
+    s->d_seq_ptr[dir] = (int64_t *)carve(ptr.size() * 8);
+    s->d_seq_slots[dir] = (int32_t *)carve(std::max<size_t>(slots.size(), 1) * 4);
+    CK(cudaMemcpyAsync(s->d_seq_ptr[dir], ptr.data(), ptr.size() * 8, cudaMemcpyHostToDevice, s->stream), "H2D");
+    if (!slots.empty())
+      CK(cudaMemcpyAsync(s->d_seq_slots[dir], slots.data(), slots.size() * 4, cudaMemcpyHostToDevice, s->stream), "H2D");
+    CK(cudaStreamSynchronize(s->stream), "sync");  // host vectors go out of scope
+  }
+  s->d_e_lane = (double *)carve((size_t)std::max(s->n_tiles, 1) * 32 * 8);
+  CK(cudaMemsetAsync(s->d_e_lane, 0, (size_t)std::max(s->n_tiles, 1) * 32 * 8, s->stream), "memset");
+  s->seq_ready = true;
+  return FDOG_OK;
+}
+
+SeqArgs seq_args(fdog_solver *s, bool forward, double omega) {
+  SeqArgs a{};
+  a.tiles = s->d_tiles;
+  a.hop_off = s->d_hop_off;
+  a.topo = s->d_topo;
+  a.slot_tile = s->d_slot_tile;
+  a.ptr = s->d_seq_ptr[forward ? 1 : 0];
+  a.slots = s->d_seq_slots[forward ? 1 : 0];
+  a.lambda = s->d_lambda;
+  a.dist = s->d_dist;
+  a.delta = s->d_delta[s->cur ^ 1];  // scratch; delta_bar (d_delta[cur]) stays 0
+  a.m0 = s->record_mm ? s->d_m0 : nullptr;
+  a.m1 = s->record_mm ? s->d_m1 : nullptr;
+  a.e_lane = s->d_e_lane;
+  a.omega = omega;
+  a.clamp = s->clamp;
+  a.forward = forward ? 1 : 0;
+  return a;
+}
+
+fdog_status do_pass_seq(fdog_solver *s, bool forward, double omega) {
+  fdog_status st = seq_schedule(s);
+  if (st) return st;
+  SeqArgs a = seq_args(s, forward, omega);
+  int e;
+  // store-design distances of the opposite direction
+  if (forward ? s->dist_state != 0 : s->dist_state != 1) {
+    Timed t(s, kKEnergy);
+    e = launch_dist_dp(s->precision, a, s->n_tiles, forward ? 0 : 1, s->stream);
+    if (e) return cuda_fail((cudaError_t)e, "dist_dp launch");
+  }
+  const std::vector<int64_t> &lv = s->seq_lvl[forward ? 1 : 0];
+  {
+    Timed t(s, forward ? kKSweepFwd : kKSweepBwd);
+    for (size_t l = 0; l + 1 < lv.size(); ++l) {
+      e = launch_seq_level(s->precision, s->record_mm, a, lv[l], lv[l + 1], s->stream);
+      if (e) return cuda_fail((cudaError_t)e, "seq level launch");
+      s->launches++;
+    }
+    s->launches--;  // (Timed counts one)
+  }
+  e = launch_seq_bound(s->d_tiles, s->n_tiles, s->d_e_lane, s->d_lb_part, s->stream);
+  if (e) return cuda_fail((cudaError_t)e, "seq bound launch");
+  s->launches++;
+  s->dist_state = forward ? 1 : 0;
+  s->passes++;
+  s->dbar_zero = true;
+  s->lb_dirty = true;
+  return FDOG_OK;
 }
 
 void free_solver(fdog_solver *s) {
@@ -793,7 +936,7 @@ fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, u
   };
   const int cur0 = s->cur, ds0 = s->dist_state;
   const int64_t passes0 = s->passes;
-  const bool dirty0 = s->lb_dirty;
+  const bool dirty0 = s->lb_dirty, dz0 = s->dbar_zero;
   const size_t pb = (size_t)std::max(s->n_tiles, 1) * sizeof(double), lbb = 2 * sizeof(double);
   if (!o->keep_state) {
     void *p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -823,6 +966,7 @@ fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, u
     s->dist_state = ds0;
     s->passes = passes0;
     s->lb_dirty = dirty0;
+    s->dbar_zero = dz0;
     return FDOG_OK;
   };
   if (s->passes == 0 && (st = fdog_iterate(s, o->inner, o->omega))) {
@@ -911,6 +1055,39 @@ fdog_status fdog_pass(fdog_solver *s, int32_t forward, double omega) {
     return FDOG_EINVAL;
   }
   return do_pass(s, forward != 0, omega);
+}
+
+fdog_status fdog_pass_seq(fdog_solver *s, int32_t forward, double omega) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  if (!(omega > 0.0 && omega <= 1.0)) {
+    set_error("omega %g outside (0, 1]", omega);
+    return FDOG_EINVAL;
+  }
+  if (s->world > 1) {
+    set_error("the non-deferred variant is single-GPU");
+    return FDOG_ESTATE;
+  }
+  if (!s->dbar_zero) {
+    set_error("a deferred correction is pending: fdog_finalize first");
+    return FDOG_ESTATE;
+  }
+  return do_pass_seq(s, forward != 0, omega);
+}
+
+fdog_status fdog_iterate_seq(fdog_solver *s, int32_t n_iter, double omega) {
+  if (!s || n_iter < 0) {
+    set_error("null solver or negative n_iter");
+    return FDOG_EINVAL;
+  }
+  for (int32_t t = 0; t < n_iter; ++t) {
+    fdog_status st = fdog_pass_seq(s, 1, omega);
+    if (!st) st = fdog_pass_seq(s, 0, omega);
+    if (st) return st;
+  }
+  return FDOG_OK;
 }
 
 fdog_status fdog_pass_begin(fdog_solver *s, int32_t forward, double omega) {
@@ -1094,6 +1271,7 @@ fdog_status fdog_finalize(fdog_solver *s) {
     e = launch_add_deferred(s->precision, s->n_dev_slots, s->d_lambda, s->d_delta[s->cur], s->stream);
   }
   if (e) return cuda_fail((cudaError_t)e, "add_deferred");
+  s->dbar_zero = true;
   return energy(s);
 }
 
@@ -1117,6 +1295,7 @@ fdog_status fdog_finalize_averaged(fdog_solver *s) {
   }
   if (e) return cuda_fail((cudaError_t)e, "add_deferred");
   CK(cudaMemsetAsync(s->d_delta[s->cur], 0, (size_t)std::max<int64_t>(s->n_dev_slots, 1) * s->tsz, s->stream), "memset");
+  s->dbar_zero = true;
   return energy(s);
 }
 
@@ -1176,6 +1355,11 @@ fdog_status fdog_set_state(fdog_solver *s, const double *lambda, const double *d
   fdog_status st;
   if (lambda && (st = put_slots(s, s->d_lambda, lambda, len))) return st;
   if (delta && (st = put_slots(s, s->d_delta[s->cur], delta, len))) return st;
+  if (delta) {
+    bool z = true;
+    for (int64_t q = 0; q < len && z; ++q) z = delta[q] == 0.0;
+    s->dbar_zero = z;
+  }
   return energy(s);
 }
 
