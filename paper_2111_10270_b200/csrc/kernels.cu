@@ -1616,43 +1616,51 @@ __device__ __forceinline__ SeqLoc seq_locate(const SeqArgs &a, int32_t ds, int32
   return l;
 }
 
+// one warp per variable, lane k handles slots k, k + 32, ... of it (every slot
+// of a high-degree variable in parallel); the sum over J_i is accumulated in
+// ascending j by one lane (shuffles), as the oracle does
 template <typename T, bool REC>
 __global__ void __launch_bounds__(128) seq_level_kernel(const SeqArgs a, int64_t q0, int64_t q1) {
-  const int64_t q = q0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= q1) return;
+  const int64_t q = q0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= q1) return;  // whole warps
   T *__restrict__ lam = reinterpret_cast<T *>(a.lambda);
   T *__restrict__ D = reinterpret_cast<T *>(a.dist);
   T *__restrict__ dl = reinterpret_cast<T *>(a.delta);
   const T omega = T(a.omega), clamp = T(a.clamp), inf = t_inf<T>();
   const int64_t p0 = a.ptr[q], p1 = a.ptr[q + 1];
-  // min-marginals of the variable in every j in J_i (ascending j)
+  // min-marginals of the variable in every j in J_i
   T sum = T(0);
-  for (int64_t p = p0; p < p1; ++p) {
-    const int32_t ds = a.slots[p];
-    int32_t t;
-    const SeqLoc l = seq_locate(a, ds, t);
-    const int n0 = l.ho[l.h], n1 = l.ho[l.h + 1];
-    if (a.forward && l.h == 0) D[l.dbase] = T(0);  // shp(r, r)
-    T m0 = inf, m1r = inf;
-    for (int n = n0; n < n1; ++n) {
-      const uint32_t e = l.tp[(int64_t)n * l.ts];
-      const T c = D[l.dbase + (int64_t)n * l.L];
-      m0 = fmin(m0, c + D[l.dbase + (int64_t)(e & 0xFFFFu) * l.L]);
-      m1r = fmin(m1r, c + D[l.dbase + (int64_t)(e >> 16) * l.L]);
+  for (int64_t c0 = p0; c0 < p1; c0 += 32) {
+    const int64_t p = c0 + lane;
+    T delta = T(0);
+    if (p < p1) {
+      const int32_t ds = a.slots[p];
+      int32_t t;
+      const SeqLoc l = seq_locate(a, ds, t);
+      const int n0 = l.ho[l.h], n1 = l.ho[l.h + 1];
+      if (a.forward && l.h == 0) D[l.dbase] = T(0);  // shp(r, r)
+      T m0 = inf, m1r = inf;
+      for (int n = n0; n < n1; ++n) {
+        const uint32_t e = l.tp[(int64_t)n * l.ts];
+        const T c = D[l.dbase + (int64_t)n * l.L];
+        m0 = fmin(m0, c + D[l.dbase + (int64_t)(e & 0xFFFFu) * l.L]);
+        m1r = fmin(m1r, c + D[l.dbase + (int64_t)(e >> 16) * l.L]);
+      }
+      const T m1 = lam[ds] + m1r;
+      delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+      dl[ds] = delta;
+      if (REC) {
+        reinterpret_cast<T *>(a.m0)[ds] = m0;
+        reinterpret_cast<T *>(a.m1)[ds] = m1;
+      }
     }
-    const T lv = lam[ds];
-    const T m1 = lv + m1r;
-    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
-    dl[ds] = delta;
-    if (REC) {
-      reinterpret_cast<T *>(a.m0)[ds] = m0;
-      reinterpret_cast<T *>(a.m1)[ds] = m1;
-    }
-    sum += delta;
+    const int cnt = p1 - c0 < 32 ? (int)(p1 - c0) : 32;
+    for (int k = 0; k < cnt; ++k) sum += __shfl_sync(0xffffffffu, delta, k);  // ascending j
   }
   const T avg = sum / T(p1 - p0);
   // update every slot, then advance its BDD by one partition
-  for (int64_t p = p0; p < p1; ++p) {
+  for (int64_t p = p0 + lane; p < p1; p += 32) {
     const int32_t ds = a.slots[p];
     int32_t t;
     const SeqLoc l = seq_locate(a, ds, t);
@@ -1897,8 +1905,8 @@ int launch_gather_canon(int precision, int64_t n, const int32_t *canon, const vo
 
 int launch_seq_level(int precision, bool record, const SeqArgs &a, int64_t q0, int64_t q1, void *stream) {
   if (q1 <= q0) return 0;
-  const int block = 128;
-  const unsigned grid = (unsigned)((q1 - q0 + block - 1) / block);
+  const int block = 128;  // four variables (warps) per block
+  const unsigned grid = (unsigned)((q1 - q0 + 3) / 4);
   cudaStream_t st = (cudaStream_t)stream;
   if (precision == 64) {
     if (record) seq_level_kernel<double, true><<<grid, block, 0, st>>>(a, q0, q1);

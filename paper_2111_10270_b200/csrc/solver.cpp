@@ -134,6 +134,10 @@ struct fdog_solver {
   // one captured iteration (avg, forward, avg, backward), keyed by omega and
   // the parity of the delta buffers; replayed by fdog_iterate
   cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t seq_graph = nullptr;  // one iteration of the non-deferred variant
+  double seq_graph_omega = 0.0;
+  int seq_graph_cur = -1;  // the graph's scratch is d_delta[cur ^ 1] of capture time
+  int64_t seq_graph_launches = 0;
   double graph_omega = 0.0;
   int graph_cur = -1;
   int64_t graph_launches = 0;
@@ -482,6 +486,7 @@ void free_solver(fdog_solver *s) {
   }
   for (auto e : s->event_pool) cudaEventDestroy(e);
   if (s->graph) cudaGraphExecDestroy(s->graph);
+  if (s->seq_graph) cudaGraphExecDestroy(s->seq_graph);
   for (void *p : s->allocs) cudaFree(p);
   if (s->nccl.comm && s->nccl.destroy) s->nccl.destroy(s->nccl.comm);
   if (s->nccl.lib) dlclose(s->nccl.lib);
@@ -1082,11 +1087,54 @@ fdog_status fdog_iterate_seq(fdog_solver *s, int32_t n_iter, double omega) {
     set_error("null solver or negative n_iter");
     return FDOG_EINVAL;
   }
-  for (int32_t t = 0; t < n_iter; ++t) {
-    fdog_status st = fdog_pass_seq(s, 1, omega);
-    if (!st) st = fdog_pass_seq(s, 0, omega);
-    if (st) return st;
+  if (n_iter == 0) return FDOG_OK;
+  fdog_status st = fdog_pass_seq(s, 1, omega);  // validates the state; builds the schedule
+  if (!st) st = fdog_pass_seq(s, 0, omega);
+  if (st || n_iter == 1) return st;
+  // the remaining iterations replay a CUDA graph of one (forward, backward)
+  // iteration: hundreds of small level kernels, launch-latency bound otherwise
+  // (the distances are in the state a forward pass expects after a backward one)
+  if (!s->use_graphs || s->profile) {
+    for (int32_t t = 1; t < n_iter; ++t) {
+      st = fdog_pass_seq(s, 1, omega);
+      if (!st) st = fdog_pass_seq(s, 0, omega);
+      if (st) return st;
+    }
+    return FDOG_OK;
   }
+  if (!s->seq_graph || s->seq_graph_omega != omega || s->seq_graph_cur != s->cur) {
+    if (s->seq_graph) {
+      cudaGraphExecDestroy(s->seq_graph);
+      s->seq_graph = nullptr;
+    }
+    const int ds0 = s->dist_state;
+    const int64_t passes0 = s->passes, launches0 = s->launches;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    st = do_pass_seq(s, true, omega);
+    if (!st) st = do_pass_seq(s, false, omega);
+    cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+    if (st) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&s->seq_graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    s->seq_graph_omega = omega;
+    s->seq_graph_cur = s->cur;
+    s->seq_graph_launches = s->launches - launches0;
+    s->dist_state = ds0;  // capture recorded the work without running it
+    s->passes = passes0;
+    s->launches = launches0;
+  }
+  for (int32_t t = 1; t < n_iter; ++t) CK(cudaGraphLaunch(s->seq_graph, s->stream), "cudaGraphLaunch");
+  s->launches += s->seq_graph_launches * (n_iter - 1);
+  s->passes += 2 * (int64_t)(n_iter - 1);
+  s->dist_state = 0;
+  s->dbar_zero = true;
+  s->lb_dirty = true;
   return FDOG_OK;
 }
 

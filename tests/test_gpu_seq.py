@@ -102,3 +102,21 @@ def test_seq_fp32_bound(oracle_mod):
     o.iterate_seq(20, 0.5)
     g.iterate_seq(20, 0.5)
     assert abs(g.lower_bound() - o.lower_bound()) <= 1e-4 * abs(o.lower_bound())
+
+
+def test_seq_graph_replay_matches_direct(monkeypatch):
+    """fdog_iterate_seq replays a CUDA graph of one iteration after the first:
+    bit-identical to launching every level kernel directly, also after a
+    deferred pass + finalize flipped the delta buffers in between."""
+    p = synth.gm_worms_like(47, n_src=60, k_cand=5, knn=6)
+    monkeypatch.setenv("FDOG_GRAPHS", "1")
+    g1 = F.Solver(p, precision=32)
+    monkeypatch.setenv("FDOG_GRAPHS", "0")
+    g2 = F.Solver(p, precision=32)
+    for g in (g1, g2):
+        g.iterate_seq(4, 0.5)
+        g.pass_(True, 0.5)
+        g.finalize()
+        g.iterate_seq(3, 0.5)
+    assert np.array_equal(g1.lam(), g2.lam()) and g1.lower_bound() == g2.lower_bound()
+    assert np.all(g1.deferred() == 0.0)
