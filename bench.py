@@ -280,6 +280,18 @@ def run_gpu(args):
             traffic = json.load(open(tpath)).get(problem.name + f"/fp{prec}")
         except Exception:
             traffic = None
+    # SURVEY §8(d) byte models of one sweep launch (per pass: store 16 B/node +
+    # 20 B/slot, minimal/recompute 8 B/node + 20 B/slot, fp32), the same launch
+    # time: the bandwidth a design moving those bytes would need (bytes_per_launch
+    # above is what this build's design actually moves)
+    survey_models = None
+    if sw_n and prec == 32:
+        t_l = sw_ms / sw_n * 1e-3
+        store_b = 16.0 * st["nodes"] + 20.0 * st["slots"]
+        min_b = 8.0 * st["nodes"] + 20.0 * st["slots"]
+        survey_models = {"store_bytes": store_b, "min_bytes": min_b,
+                         "store_gbs": store_b / t_l / 1e9, "min_gbs": min_b / t_l / 1e9,
+                         "store_frac": store_b / t_l / 1e9 / peak, "min_frac": min_b / t_l / 1e9 / peak}
     step_total_ms = sum(v["ms"] for v in prof.values())
     shares = {k: v["ms"] / step_total_ms for k, v in prof.items()} if step_total_ms else {}
 
@@ -392,7 +404,9 @@ def run_gpu(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "sweep_forward+sweep_backward",
                          "bytes_per_launch": sw_bytes, "peak_kind": peak_kind,
-                         "launch_us": 1e3 * sw_ms / sw_n if sw_n else None},
+                         "launch_us": 1e3 * sw_ms / sw_n if sw_n else None,
+                         "design": "recompute" if st.get("sweep_recompute") else "store",
+                         "survey_models": survey_models},
             "kernel_share": shares,
             "ms_per_step_profiled": float(sum(ms_prof)) / args.steps,
             "solver_stats": {k: st[k] for k in ("tiles", "tiles_shared_topology", "staged_tiles", "sweep_grid",
