@@ -89,7 +89,8 @@ typedef struct {
   int64_t staged_tiles;  /* tiles staged on chip by TMA (the rest run from global)    */
   int32_t sweep_grid, sweep_block; /* persistent sweep launch configuration           */
   int64_t sweep_smem_per_warp;     /* bytes of shared memory per warp                 */
-  int32_t sweep_streaming;         /* 1: passes use the streaming sweep kernel        */
+  int32_t sweep_streaming;         /* 1: passes use the streaming sweep kernel;
+                                      2: the chunked kernel (rows too long to stage)    */
   int64_t h2d_bytes;               /* host->device bytes copied by create             */
   int32_t fused_small;             /* 1: fdog_iterate runs all its iterations in one
                                       single-CTA launch (small narrow problems);

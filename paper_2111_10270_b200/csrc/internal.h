@@ -232,6 +232,7 @@ struct AvgArgs {
   void *avg_slot;            // T*: avg_i written into every slot of i (the other delta buffer)
   void *xbuf;                // T* partial sums of shared variables (may be null)
   unsigned int *tile_counter;  // sweep scheduler counter, reset here for the next sweep
+  int32_t ell_v;             // ELL variables per thread (1, 2, 4 or 8; the fused path uses 4)
 };
 
 struct PrimalArgs {
@@ -283,6 +284,8 @@ int launch_dist_dp(int precision, const SeqArgs &a, int32_t n_tiles, int32_t for
 int launch_sweep(int precision, int mode, bool record, bool rc, const SweepArgs &a, int grid, int block,
                  size_t smem, void *stream);
 int launch_sweep_stream(int precision, int mode, bool record, const SweepArgs &a, void *stream);
+// chunked walk of rows too long to stage whole (store design; every tile an arc-mask tile)
+int launch_sweep_chunk(int precision, int mode, bool record, const SweepArgs &a, void *stream);
 int sweep_occupancy(int precision, int mode, bool record, bool rc, int block, size_t smem, int *blocks_per_sm);
 int launch_avg(int precision, const AvgArgs &a, void *stream);
 int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,

@@ -1123,6 +1123,241 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
 // per array (lambda, avg/delta, the two distances) -- with the loads of the
 // next two partitions in flight (software pipeline), so occupancy is bounded
 // by registers only.  Same arithmetic and D/va conventions as process_bdd_w2.
+// Forward / backward pass over partitions [hb, he) of a K-partition BDD whose
+// lambda, averages and hop records are given from partition hb on (chunk
+// buffers) and whose distances hold rows from node r0 on; the recursion state
+// (c forward, x backward) is carried in and out.  The same prefetching loops
+// and hop arithmetic as mask_forward / mask_backward (store design).
+template <typename T, bool REC, int LC>
+__device__ __forceinline__ void mask_forward_range(const int hb, const int he, const int K, const bool chain,
+                                                   const HopRec<T> *rec, const int L_rt, T *lam, T *va, T *D,
+                                                   const int r0, const bool valid, const T omega, const T clamp,
+                                                   T *m0g, T *m1g, T &c0, T &c1, double &acc) {
+  const uint32_t L = LC ? LC : L_rt;
+  int4 tl = hop_tail(rec);
+  T l = lam[0], av = va[0];
+  T x0 = D[(uint32_t)(tl.y - r0) * L], x1 = D[(uint32_t)(tl.y + 1 - r0) * L];
+  auto step = [&](auto ch, int h) {
+    constexpr int ty = decltype(ch)::value ? 1 : 0;
+    const uint32_t i = h - hb, in = h + 1 < he ? i + 1 : i;
+    const int4 tn = hop_tail(rec + in);
+    const T ln = lam[in * L], avn = va[in * L];
+    const T x0n = D[(uint32_t)(tn.y - r0) * L], x1n = D[(uint32_t)(tn.y + 1 - r0) * L];
+    D[(uint32_t)(tl.x - r0) * L] = c0;  // keep shp(r, v) for the backward pass
+    if (tl.z) D[(uint32_t)(tl.x + 1 - r0) * L] = c1;
+    T m0, m1r;
+    hop_mm(ty, rec + i, x0, x1, c0, c1, m0, m1r);
+    const T lam_new = mask_finish<T, REC>(lam, va, i * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
+    hop_relax(ty, rec + i, c0, c1, lam_new, c0, c1);
+    tl = tn;
+    l = ln;
+    av = avn;
+    x0 = x0n;
+    x1 = x1n;
+  };
+  int h = hb;
+  if (chain) {
+    if (h == 0 && h < he) step(Bool<false>(), h++);
+    const int hm = min(he, K - 1);
+#pragma unroll 1
+    for (; h < hm; ++h) step(Bool<true>(), h);
+  }
+#pragma unroll 1
+  for (; h < he; ++h) step(Bool<false>(), h);
+}
+
+template <typename T, bool REC, int LC>
+__device__ __forceinline__ void mask_backward_range(const int hb, const int he, const int K, const bool chain,
+                                                    const HopRec<T> *rec, const int L_rt, T *lam, T *va, T *D,
+                                                    const int r0, const bool valid, const T omega, const T clamp,
+                                                    T *m0g, T *m1g, T &x0, T &x1, double &acc) {
+  const uint32_t L = LC ? LC : L_rt;
+  const T inf = t_inf<T>();
+  const uint32_t top = he - 1 - hb;
+  int4 tl = hop_tail(rec + top);
+  T l = lam[top * L], av = va[top * L];
+  T f0 = D[(uint32_t)(tl.x - r0) * L], f1 = tl.z ? D[(uint32_t)(tl.x + 1 - r0) * L] : inf;
+  auto step = [&](auto ch, int h) {
+    constexpr int ty = decltype(ch)::value ? 1 : 0;
+    const uint32_t i = h - hb, in = h > hb ? i - 1 : i;
+    const int4 tn = hop_tail(rec + in);
+    const T ln = lam[in * L], avn = va[in * L];
+    const T f0n = D[(uint32_t)(tn.x - r0) * L], f1n = tn.z ? D[(uint32_t)(tn.x + 1 - r0) * L] : inf;
+    T m0, m1r;
+    hop_mm(ty, rec + i, x0, x1, f0, f1, m0, m1r);
+    const T lam_new = mask_finish<T, REC>(lam, va, i * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
+    hop_ctt(ty, rec + i, x0, x1, lam_new, x0, x1);  // shp(v, T) with the updated lambda_h
+    D[(uint32_t)(tl.x - r0) * L] = x0;
+    if (tl.z) D[(uint32_t)(tl.x + 1 - r0) * L] = x1;
+    tl = tn;
+    l = ln;
+    av = avn;
+    f0 = f0n;
+    f1 = f1n;
+  };
+  int h = he - 1;
+  if (chain) {
+    if (h == K - 1 && h >= hb) step(Bool<false>(), h--);
+    const int hm = max(hb, 1);
+#pragma unroll 1
+    for (; h >= hm; --h) step(Bool<true>(), h);
+  }
+#pragma unroll 1
+  for (; h >= hb; --h) step(Bool<false>(), h);
+}
+
+// ---------------------------------------------------------------------------
+// Chunked sweep for rows too long to stage whole (store design, arc-mask
+// tiles; e.g. SURVEY §8(d)'s thin-hop microbench, one BDD of 10^4 partitions,
+// and QAP n=128): one warp per tile walks the partitions in chunks of kChunk.
+// A chunk's lambda, averages, hop records and distance rows are staged into
+// the warp's shared memory by TMA bulk copies, double-buffered (the next
+// chunk's loads are in flight while the current one is computed at
+// shared-memory latency); lambda, delta and the chunk's own distance rows go
+// back by TMA bulk stores.  The hop recursion carries its state (shp(r, .) of
+// the current partition forward, shp(., T) of the partition above backward)
+// in registers across chunks.  Same arithmetic as mask_forward /
+// mask_backward (store design).  Chunks never overlap in what they write, and
+// a chunk reads only distance rows no earlier chunk of the pass writes.
+constexpr int kChunk = 32;
+
+template <typename T>
+__host__ __device__ __forceinline__ int chunk_rows() { return 2 * (kChunk + 1) + 3; }  // <= 2 nodes per partition
+template <typename T>
+__host__ __device__ __forceinline__ int chunk_stage_bytes() {
+  return 2 * kChunk * 32 * (int)sizeof(T) + kChunk * (8 * (int)sizeof(T) + 16) + chunk_rows<T>() * 32 * (int)sizeof(T);
+}
+template <typename T>
+__host__ __device__ __forceinline__ int chunk_warp_bytes() { return (128 + 2 * chunk_stage_bytes<T>() + 127) & ~127; }
+
+struct ChunkSpan {
+  int h0, h1, r0, rown, rend;  // hops [h0, h1); rows [r0, rend) loaded, [r0, rown) written back
+};
+
+template <typename T, int MODE>
+__device__ __forceinline__ ChunkSpan chunk_span(const TileDesc &d, const HopRec<T> *grec, int c) {
+  ChunkSpan sp;
+  sp.h0 = c * kChunk;
+  sp.h1 = min(d.K, sp.h0 + kChunk);
+  sp.r0 = __ldg(&grec[sp.h0].n0);
+  sp.rown = __ldg(&grec[sp.h1 - 1].n1);  // first node after the chunk (= nodes on the last)
+  // forward: also the next partition (its distances are the successors'
+  // shp(., T); the last chunk's are the sentinels), +1 row so the second node
+  // read of a one-node next partition (masked out) stays a defined value
+  sp.rend = MODE == kForward ? min(d.nodes + 2, (sp.h1 < d.K ? __ldg(&grec[sp.h1].n1) : d.nodes + 2) + 1) : sp.rown;
+  return sp;
+}
+
+template <typename T>
+struct ChunkStage {
+  T *lam, *va, *D;
+  HopRec<T> *rec;
+};
+template <typename T>
+__device__ __forceinline__ ChunkStage<T> chunk_stage_at(unsigned char *p) {
+  ChunkStage<T> st;
+  st.lam = reinterpret_cast<T *>(p);
+  st.va = st.lam + kChunk * 32;
+  st.rec = reinterpret_cast<HopRec<T> *>(st.va + kChunk * 32);
+  st.D = reinterpret_cast<T *>(st.rec + kChunk);
+  return st;
+}
+
+template <typename T>
+__device__ __forceinline__ void chunk_issue(const ChunkStage<T> &st, const ChunkSpan &sp, int L, const T *glam,
+                                            const T *gva, const HopRec<T> *grec, const T *gD, uint64_t *bar) {
+  const int nh = sp.h1 - sp.h0;
+  const uint32_t lb = (uint32_t)nh * L * sizeof(T), rb = (uint32_t)nh * sizeof(HopRec<T>);
+  const uint32_t db = (uint32_t)(sp.rend - sp.r0) * L * sizeof(T);
+  mbar_expect_tx(bar, 2 * lb + rb + db);
+  bulk_g2s(st.lam, glam + (int64_t)sp.h0 * L, lb, bar);
+  bulk_g2s(st.va, gva + (int64_t)sp.h0 * L, lb, bar);
+  bulk_g2s(st.rec, grec + sp.h0, rb, bar);
+  bulk_g2s(st.D, gD + (int64_t)sp.r0 * L, db, bar);
+}
+
+template <typename T, int MODE, bool REC>
+__global__ void __launch_bounds__(128) sweep_chunk_kernel(const SweepArgs a) {
+  extern __shared__ __align__(128) unsigned char csm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (t >= a.n_tiles) return;  // whole warps
+  unsigned char *wb = csm + (size_t)warp * chunk_warp_bytes<T>();
+  uint64_t *bar = reinterpret_cast<uint64_t *>(wb);  // bar[0], bar[1]
+  unsigned char *sb[2] = {wb + 128, wb + 128 + chunk_stage_bytes<T>()};
+  const TileDesc d = a.tiles[t];
+  const int L = d.lanes, K = d.K;
+  const bool valid = lane < d.n_lanes, active = lane < L;
+  const bool chain = d.kind & 8;
+  const HopRec<T> *grec = reinterpret_cast<const HopRec<T> *>(a.recs + 16 * (int64_t)d.rec_base);
+  T *glam = reinterpret_cast<T *>(a.lambda) + d.slot_base;
+  T *gva = reinterpret_cast<T *>(a.delta_out) + d.slot_base;
+  T *gD = reinterpret_cast<T *>(a.dist) + d.dist_base;
+  T *m0g = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
+  T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
+  const T omega = T(a.omega), clamp = T(a.clamp), inf = t_inf<T>();
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  pdl_wait();
+  const int nch = (K + kChunk - 1) / kChunk;
+  auto chunk_of = [&](int ci) { return MODE == kForward ? ci : nch - 1 - ci; };
+  if (lane == 0) chunk_issue(chunk_stage_at<T>(sb[0]), chunk_span<T, MODE>(d, grec, chunk_of(0)), L, glam, gva, grec, gD, &bar[0]);
+  uint32_t phase = 0;
+  double acc = 0.0;
+  T c0 = T(0), c1 = inf;  // forward: shp(r, .) of the current partition
+  T x0 = T(0), x1 = inf;  // backward: shp(., T) of the partition above
+  for (int ci = 0; ci < nch; ++ci) {
+    const int b = ci & 1;
+    const ChunkSpan sp = chunk_span<T, MODE>(d, grec, chunk_of(ci));
+    if (ci + 1 < nch && lane == 0) {
+      bulk_wait_read_all();  // the stores of chunk ci - 1 (same buffer as ci + 1) have read it
+      chunk_issue(chunk_stage_at<T>(sb[b ^ 1]), chunk_span<T, MODE>(d, grec, chunk_of(ci + 1)), L, glam, gva, grec, gD,
+                  &bar[b ^ 1]);
+    }
+    const ChunkStage<T> st = chunk_stage_at<T>(sb[b]);
+    mbar_wait(&bar[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+    const int h0 = sp.h0, h1 = sp.h1, r0 = sp.r0;
+    if (active) {
+      T *lam = st.lam + lane, *va = st.va + lane, *D = st.D + lane;
+      T *m0c = REC ? m0g + (int64_t)h0 * L : nullptr;  // recorded min-marginals, chunk-relative
+      T *m1c = REC ? m1g + (int64_t)h0 * L : nullptr;
+      if (L == 32) {
+        if (MODE == kForward)
+          mask_forward_range<T, REC, 32>(h0, h1, K, chain, st.rec, 32, lam, va, D, r0, valid, omega, clamp, m0c, m1c,
+                                         c0, c1, acc);
+        else
+          mask_backward_range<T, REC, 32>(h0, h1, K, chain, st.rec, 32, lam, va, D, r0, valid, omega, clamp, m0c,
+                                          m1c, x0, x1, acc);
+      } else {
+        if (MODE == kForward)
+          mask_forward_range<T, REC, 0>(h0, h1, K, chain, st.rec, L, lam, va, D, r0, valid, omega, clamp, m0c, m1c,
+                                        c0, c1, acc);
+        else
+          mask_backward_range<T, REC, 0>(h0, h1, K, chain, st.rec, L, lam, va, D, r0, valid, omega, clamp, m0c, m1c,
+                                         x0, x1, acc);
+      }
+    }
+    fence_proxy_async();  // lanes' shared-memory writes -> visible to the TMA stores
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t lb = (uint32_t)(h1 - h0) * L * sizeof(T);
+      bulk_s2g(glam + (int64_t)h0 * L, st.lam, lb);
+      bulk_s2g(gva + (int64_t)h0 * L, st.va, lb);
+      bulk_s2g(gD + (int64_t)r0 * L, st.D, (uint32_t)(sp.rown - r0) * L * sizeof(T));  // the chunk's own partitions
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait_read_all();  // shared memory must outlive the TMA stores' reads
+  if (valid) acc += (double)(MODE == kForward ? c0 : x0);  // E^j = shp(r, T)
+  acc = warp_sum(acc);
+  if (lane == 0) a.lb_part[t] = acc;
+}
+
 template <typename T>
 struct HopSet {
   int n0, n1, n2;   // P_h = [n0, n1), P_{h+1} = [n1, n2)
@@ -1307,28 +1542,30 @@ __device__ __forceinline__ V ld(const V *p) {
 // gathering its partner's delta_bar, coalesced writes -- measured 1.5-2.3x
 // slower: the partner gathers lose the locality of the first slot.)
 // NC: delta_bar is read-only for the kernel's lifetime (the standalone kernel)
-template <typename T, bool NC>
+// V: ELL variables per thread (tid, tid + N, ..., tid + (V-1) N: every load of
+// a warp stays coalesced, all 2V gathers in flight before the first use)
+template <typename T, bool NC, int V = 4>
 __device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
   // ELL part: four variables per thread (tid, tid + N, tid + 2N, tid + 3N, so
   // every load of a warp stays coalesced), all eight gathers issued before use
-  const int n_ell_thr = (((a.n_ell + 3) >> 2) + 31) & ~31;  // whole warps
+  const int n_ell_thr = (((a.n_ell + V - 1) / V) + 31) & ~31;  // whole warps
   if (tid < n_ell_thr) {
-    int2 p[4];
+    int2 p[V];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < V; ++u) {
       const int q = tid + u * n_ell_thr;
       p[u] = q < a.n_ell ? __ldg(a.ell + q) : make_int2(-1, -1);
     }
-    T x[4], y[4];
+    T x[V], y[V];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < V; ++u) {
       x[u] = p[u].x >= 0 ? ld<NC>(db + p[u].x) : T(0);
       y[u] = p[u].y >= 0 ? ld<NC>(db + p[u].y) : T(0);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) ell_store(out, p[u], x[u], y[u]);
+    for (int u = 0; u < V; ++u) ell_store(out, p[u], x[u], y[u]);
     return;
   }
   // ELL-4 part (|J_i| = 3 or 4): one variable per thread, slot quad inline,
@@ -1398,12 +1635,16 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
   if (tid == 0) *a.tile_counter = 0u;
-  avg_body<T, true>(a, tid);
+  if (a.ell_v == 8) avg_body<T, true, 8>(a, tid);
+  else if (a.ell_v == 2) avg_body<T, true, 2>(a, tid);
+  else if (a.ell_v == 1) avg_body<T, true, 1>(a, tid);
+  else avg_body<T, true, 4>(a, tid);
 }
 
 // threads the averaging needs (whole warps per section)
 __host__ __device__ __forceinline__ int64_t avg_threads(const AvgArgs &a) {
-  return (int64_t)((((a.n_ell + 3) / 4) + 31) & ~31) + (int64_t)((a.n_ell4 + 31) & ~31) + (int64_t)a.n * a.group;
+  const int v = (a.ell_v == 8 || a.ell_v == 2 || a.ell_v == 1) ? a.ell_v : 4;
+  return (int64_t)((((a.n_ell + v - 1) / v) + 31) & ~31) + (int64_t)((a.n_ell4 + 31) & ~31) + (int64_t)a.n * a.group;
 }
 
 // ---------------------------------------------------------------------------
@@ -1440,9 +1681,11 @@ __global__ void __launch_bounds__(1024) fused_small_kernel(const SweepArgs sa, c
     va_all = s1;
     gdist = sd;
   }
-  const int64_t na = avg_threads(aa);
+  AvgArgs a4 = aa;
+  a4.ell_v = 4;  // avg_body's default V below
+  const int64_t na = avg_threads(a4);
   for (int it = 0; it < 2 * n_iter; ++it) {
-    AvgArgs a = aa;
+    AvgArgs a = a4;
     a.delta_bar = dbar;
     a.avg_slot = va_all;
     for (int64_t base = 0; base < na; base += blockDim.x) avg_body<T, false>(a, (int)(base + threadIdx.x));
@@ -1815,6 +2058,23 @@ int launch_sweep_stream(int precision, int mode, bool rec, const SweepArgs &a, v
   void *args[] = {(void *)&a};
   const int grid = (a.n_tiles + 3) / 4;
   return launch_pdl(f, dim3(grid > 0 ? grid : 1), dim3(128), 0, stream, args);
+}
+
+template <typename T>
+static const void *chunk_fn(int mode, bool rec) {
+  if (mode == kForward) return rec ? (const void *)sweep_chunk_kernel<T, kForward, true> : (const void *)sweep_chunk_kernel<T, kForward, false>;
+  return rec ? (const void *)sweep_chunk_kernel<T, kBackward, true> : (const void *)sweep_chunk_kernel<T, kBackward, false>;
+}
+
+int launch_sweep_chunk(int precision, int mode, bool rec, const SweepArgs &a, void *stream) {
+  const void *f = precision == 64 ? chunk_fn<double>(mode, rec) : chunk_fn<float>(mode, rec);
+  const size_t wbytes = (size_t)(precision == 64 ? chunk_warp_bytes<double>() : chunk_warp_bytes<float>());
+  const int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (227 * 1024) / wbytes));  // warps per CTA
+  const cudaError_t e = allow_max_smem(f);
+  if (e != cudaSuccess) return (int)e;
+  void *args[] = {(void *)&a};
+  const int grid = (a.n_tiles + wpb - 1) / wpb;
+  return launch_pdl(f, dim3(grid > 0 ? grid : 1), dim3(32 * wpb), (size_t)wpb * wbytes, stream, args);
 }
 
 int launch_sweep(int precision, int mode, bool rec, bool rc, const SweepArgs &a, int grid, int block, size_t smem,

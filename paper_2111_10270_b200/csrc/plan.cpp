@@ -530,13 +530,17 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       int L = lanes_for(k0, S.k, S.nodes(), S.max_w, P.SB, P.DB);
       const bool staged = L > 0;
       if (!staged) L = 32;
+      // (rows too long to stage, of a narrow shape: the last tile keeps the
+      // shape's records even if partly filled -- the chunked path walks them;
+      // other leftovers are pooled into per-lane-topology tiles)
       size_t full = rows.size() / L * L;
+      if (!staged && k0) full = rows.size();
       for (size_t q = 0; q < full; q += L) {
         PendingTile t;
         t.kind = (staged ? 2 : 0) | k0 | (k0 && chain_shape(S) ? 8 : 0);  // records also serve the streaming kernel
         t.shape = (int32_t)s;
         t.L = L;
-        t.rows.assign(rows.begin() + q, rows.begin() + q + L);
+        t.rows.assign(rows.begin() + q, rows.begin() + std::min(rows.size(), q + L));
         t.cost = (int64_t)S.nodes() + S.k;
         pend.push_back(std::move(t));
       }

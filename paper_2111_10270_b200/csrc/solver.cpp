@@ -68,8 +68,10 @@ struct fdog_solver {
   int rank = 0, world = 1;
   bool external = false;  // world > 1 without NCCL: the caller performs the exchange
   bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
+  bool chunk_mode = false;   // ... or sweep_chunk_kernel (every tile an arc-mask tile)
   bool rc = false;           // recompute design (Plan::rc): no distance traffic, no dist_state
-  bool dbar_zero = true;     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
+  bool dbar_zero = true;
+  int32_t ell_v = 4;         // averaging: ELL variables per thread (experiment knob FDOG_AVG_V)     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
   // non-deferred variant (fdog_pass_seq): level schedule, built on first use
   bool seq_ready = false;
   std::vector<int64_t> seq_lvl[2];        // [backward, forward]: level boundaries in pass order
@@ -210,7 +212,9 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
   }
   {
     Timed t(s, mode == kForward ? kKSweepFwd : mode == kBackward ? kKSweepBwd : kKEnergy);
-    if (s->stream_mode && (mode == kForward || mode == kBackward))
+    if (s->chunk_mode && (mode == kForward || mode == kBackward))
+      e = launch_sweep_chunk(s->precision, mode, rec, a, s->stream);
+    else if (s->stream_mode && (mode == kForward || mode == kBackward))
       e = launch_sweep_stream(s->precision, mode, rec, a, s->stream);
     else
       e = launch_sweep(s->precision, mode, rec, s->rc, a, s->grid, s->block, s->smem, s->stream);
@@ -271,6 +275,7 @@ AvgArgs avg_args(fdog_solver *s) {
   a.n_ell4 = s->n_ell4;
   a.ell4 = s->d_ell4;
   a.tile_counter = s->d_counter + 1;
+  a.ell_v = s->ell_v;
   a.n = s->n_varlist;
   a.group = s->csr_group;
   a.var_ptr = s->d_var_ptr;
@@ -629,6 +634,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->DB = P.DB;
   s->NB = P.NB;
   s->rc = P.rc;
+  if (const char *av = getenv("FDOG_AVG_V")) s->ell_v = atoi(av);
   s->warp_bytes = (size_t)warp_bytes(P.SB, P.DB, P.NB);
   s->n_direct = P.direct_tiles;
   {
@@ -643,10 +649,16 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     const char *m = getenv("FDOG_SWEEP");  // experiment knob: "tma" or "stream"
     const bool forced = m && (m[0] == 's' || m[0] == 't');
     s->stream_mode = !s->rc && narrow && (forced ? m[0] == 's' : !staged_ok);
+    // rows too long to stage: walk them in chunks through shared memory when
+    // every tile carries hop records (FDOG_CHUNK=0 keeps the streaming kernel)
+    bool masks = true;
+    for (const auto &d : tiles) masks = masks && (d.kind & 4);
+    const char *ck = getenv("FDOG_CHUNK");
+    s->chunk_mode = s->stream_mode && masks && !(forced && m[0] == 's') && !(ck && ck[0] == '0');
     // tiny instances (BASELINE configs[0]) are launch-latency bound: one CTA
     // runs every iteration of an fdog_iterate call (fused_small_kernel)
     const char *fz = getenv("FDOG_FUSED");  // experiment knob: 0 / 1
-    const bool small = tiles.size() <= 64 && P.n_slots <= (1 << 15);
+    const bool small = tiles.size() <= 64 && P.n_slots <= (1 << 15) && P.direct_tiles == 0;  // (long rows: chunked kernel)
     s->use_fused = !s->rc && narrow && P.world == 1 && (fz ? fz[0] == '1' : small);
     const size_t fbytes = (size_t)(3 * (int64_t)P.slot_var.size() + P.n_dist) * s->tsz;
     const char *fr = getenv("FDOG_FUSED_SMEM");  // experiment knob: 0 keeps the state in global memory
@@ -803,7 +815,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->st.sweep_grid = s->grid;
   s->st.sweep_block = s->block;
   s->st.sweep_smem_per_warp = (int64_t)s->warp_bytes;
-  s->st.sweep_streaming = s->stream_mode ? 1 : 0;
+  s->st.sweep_streaming = s->chunk_mode ? 2 : s->stream_mode ? 1 : 0;
   s->st.h2d_bytes = s->upload_bytes;
   s->st.fused_small = s->use_fused ? (s->fused_smem ? 2 : 1) : 0;
   s->st.sweep_recompute = s->rc ? 1 : 0;

@@ -412,3 +412,30 @@ def test_concurrent_solvers_with_different_budgets(oracle_mod):
         s = _s(p)
         assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s
         assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+
+
+def _long_rows(seed, n=2560, rows=7):
+    """Rows too long to stage whole: one-hot / at-most-one rows over 900-2400
+    of n variables (several rows share a shape, so tiles hold several lanes),
+    plus short rows, so every variable is shared."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for r in range(rows):
+        k = [900, 900, 2400, 1500, 900, 2400, 1500][r % 7]
+        v = np.sort(rng.choice(n, size=k, replace=False))
+        out.append((v, np.ones(k), synth.EQ if r % 2 else synth.LE, 1))
+    for q in range(0, n - 1, 2):
+        out.append((np.array([q, q + 1]), np.ones(2), synth.LE, 1))
+    return synth.from_rows(n, rng.uniform(-1, 1, size=n).round(3), out, f"long_rows({seed})")
+
+
+@pytest.mark.parametrize("chunk", ["1", "0"])
+def test_long_rows_chunked(oracle_mod, monkeypatch, chunk):
+    """Rows too long to stage whole run the chunked kernel (partitions walked
+    through shared memory in chunks, state carried across chunks) -- or the
+    streaming kernel with FDOG_CHUNK=0; both match the oracle pass by pass, fp64.
+    Includes the thin-hop microbench's single 3000-partition row."""
+    monkeypatch.setenv("FDOG_CHUNK", chunk)
+    for p in (_long_rows(3), synth.thin_hop(5, k=3000)):
+        g, _ = _compare_pass_by_pass(p, oracle_mod, passes=4)
+        assert g.stats()["sweep_streaming"] == (2 if chunk == "1" else 1)
