@@ -1568,23 +1568,38 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {
     for (int u = 0; u < V; ++u) ell_store(out, p[u], x[u], y[u]);
     return;
   }
-  // ELL-4 part (|J_i| = 3 or 4): one variable per thread, slot quad inline,
-  // summed in ascending j
-  const int n_ell4_thr = (a.n_ell4 + 31) & ~31;
+  // ELL-4 part (|J_i| = 3 or 4): two variables per thread (q, q + N; loads of
+  // a warp stay coalesced), slot quads inline, all gathers in flight before
+  // the sums, each summed in ascending j
+  const int n_ell4_thr = (((a.n_ell4 + 1) >> 1) + 31) & ~31;
   if (tid < n_ell_thr + n_ell4_thr) {
     const int q = tid - n_ell_thr;
-    if (q >= a.n_ell4) return;
-    const int4 p = __ldg(a.ell4 + q);
-    const T x0 = ld<NC>(db + p.x), x1 = ld<NC>(db + p.y), x2 = ld<NC>(db + p.z);
-    const T x3 = p.w >= 0 ? ld<NC>(db + p.w) : T(0);
-    T s = x0 + x1;
-    s += x2;
-    if (p.w >= 0) s += x3;
-    const T v = s / T(p.w >= 0 ? 4 : 3);
-    out[p.x] = v;
-    out[p.y] = v;
-    out[p.z] = v;
-    if (p.w >= 0) out[p.w] = v;
+    int4 p[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int qq = q + u * n_ell4_thr;
+      p[u] = qq < a.n_ell4 ? __ldg(a.ell4 + qq) : make_int4(-1, -1, -1, -1);
+    }
+    T x[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      x[u][0] = p[u].x >= 0 ? ld<NC>(db + p[u].x) : T(0);
+      x[u][1] = p[u].x >= 0 ? ld<NC>(db + p[u].y) : T(0);
+      x[u][2] = p[u].x >= 0 ? ld<NC>(db + p[u].z) : T(0);
+      x[u][3] = p[u].w >= 0 ? ld<NC>(db + p[u].w) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (p[u].x < 0) continue;
+      T s = x[u][0] + x[u][1];
+      s += x[u][2];
+      if (p[u].w >= 0) s += x[u][3];
+      const T v = s / T(p[u].w >= 0 ? 4 : 3);
+      out[p[u].x] = v;
+      out[p[u].y] = v;
+      out[p[u].z] = v;
+      if (p[u].w >= 0) out[p[u].w] = v;
+    }
     return;
   }
   // CSR part: a group of G lanes per variable; lane j sums slots j, j+G, ...
@@ -1644,7 +1659,8 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
 // threads the averaging needs (whole warps per section)
 __host__ __device__ __forceinline__ int64_t avg_threads(const AvgArgs &a) {
   const int v = (a.ell_v == 8 || a.ell_v == 2 || a.ell_v == 1) ? a.ell_v : 4;
-  return (int64_t)((((a.n_ell + v - 1) / v) + 31) & ~31) + (int64_t)((a.n_ell4 + 31) & ~31) + (int64_t)a.n * a.group;
+  return (int64_t)((((a.n_ell + v - 1) / v) + 31) & ~31) + (int64_t)((((a.n_ell4 + 1) >> 1) + 31) & ~31) +
+         (int64_t)a.n * a.group;
 }
 
 // ---------------------------------------------------------------------------
