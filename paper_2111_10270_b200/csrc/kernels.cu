@@ -50,14 +50,16 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 
-// m1 - m0 with an infinite side replaced by +-clamp (reading A5).
+// m1 - m0 with an infinite side replaced by +-clamp (reading A5): the IEEE
+// difference is +inf exactly when m1 is infinite, -inf when m0 is, finite
+// otherwise (both infinite -- NaN -- only on padding lanes, whose results are
+// discarded), so one test of |m1 - m0| and a copysign give the reading.
+__device__ __forceinline__ float copysign_t(float c, float s) { return copysignf(c, s); }
+__device__ __forceinline__ double copysign_t(double c, double s) { return copysign(c, s); }
 template <typename T>
 __device__ __forceinline__ T mm_difference(T m1, T m0, T clamp) {
-  const bool i1 = isinf(m1), i0 = isinf(m0);
-  if (i1 && i0) return T(0);  // only on padding lanes
-  if (i1) return clamp;
-  if (i0) return -clamp;
-  return sub_rn(m1, m0);
+  const T d = sub_rn(m1, m0);
+  return fabs(d) < t_inf<T>() ? d : copysign_t(clamp, d);
 }
 
 // ---- Programmatic dependent launch: a kernel launched with the PDL attribute
