@@ -46,6 +46,8 @@ struct Shape {
 //          partition offsets; the sweeps use the branch-free min-plus form.
 //   kind bit 3 set (with bit 2): every partition but the first and the last
 //          is a chain hop (HopRec type 1); the sweeps fold those hops.
+//   kind bit 4 set (with bit 3): the first partition is a root hop (type 2)
+//          and the last a join into top (type 3); folded as well.
 // Topology entries are absolute child indices within the tile (s^0 in the low
 // 16 bits, s^1 in the high 16 bits), top = nodes, bottom = nodes + 1.
 // Partition offsets of the tile: hop_off[hop_base + h], h = 0..K.

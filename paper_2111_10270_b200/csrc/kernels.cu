@@ -687,13 +687,13 @@ __device__ __forceinline__ T mask_finish(T *lam, T *va, uint32_t hL, T l, T av, 
 // no per-hop type dispatch on the dependent chain.  Other tiles run the
 // general masks throughout.  Every loop prefetches the next partition's record
 // tail, lambda, average and distances before computing the current one.
-template <bool B>
-using Bool = std::integral_constant<bool, B>;
+template <int N>
+using Ty = std::integral_constant<int, N>;  // compile-time hop type (hop_mm)
 
 // shp(v, T) of every node under the current lambda (no update); returns
 // shp(r, T) = E^j.  (kEnergy; phase 1 of a recompute forward pass.)
 template <typename T, int LC>
-__device__ __forceinline__ T mask_ctt(const int K, const bool chain, const HopRec<T> *rec, const int L_rt,
+__device__ __forceinline__ T mask_ctt(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
                                       const T *lam, T *D) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   T x0 = T(0), x1 = t_inf<T>();
@@ -703,27 +703,31 @@ __device__ __forceinline__ T mask_ctt(const int K, const bool chain, const HopRe
     const uint32_t hn = h > 0 ? h - 1 : 0;
     const int4 tn = hop_tail(rec + hn);
     const T ln = lam[hn * L];
-    hop_ctt(decltype(ch)::value ? 1 : 0, rec + (uint32_t)h, x0, x1, l, x0, x1);
+    hop_ctt(decltype(ch)::value, rec + (uint32_t)h, x0, x1, l, x0, x1);
     D[tl.x * L] = x0;
     if (tl.z) D[(tl.x + 1) * L] = x1;
     tl = tn;
     l = ln;
   };
   int h = K - 1;
-  if (chain) {
-    if (h > 0) step(Bool<false>(), h--);
+  if (chain) {  // bit 0: chain middle; bit 1: join last, root first
+    if (h > 0) {
+      if (chain & 2) step(Ty<3>(), h--);
+      else step(Ty<0>(), h--);
+    }
 #pragma unroll 1
-    for (; h > 0; --h) step(Bool<true>(), h);
+    for (; h > 0; --h) step(Ty<1>(), h);
+    if ((chain & 2) && h >= 0) step(Ty<2>(), h--);
   }
 #pragma unroll 1
-  for (; h >= 0; --h) step(Bool<false>(), h);
+  for (; h >= 0; --h) step(Ty<0>(), h);
   return x0;
 }
 
 // shp(r, v) of every node under the current lambda (no update); returns
 // shp(r, T) = E^j.  (kCfr; phase 1 of a recompute backward pass.)
 template <typename T, int LC>
-__device__ __forceinline__ T mask_cfr(const int K, const bool chain, const HopRec<T> *rec, const int L_rt,
+__device__ __forceinline__ T mask_cfr(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
                                       const T *lam, T *D) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   T c0 = T(0), c1 = t_inf<T>();
@@ -735,18 +739,22 @@ __device__ __forceinline__ T mask_cfr(const int K, const bool chain, const HopRe
     const T ln = lam[hn * L];
     D[tl.x * L] = c0;
     if (tl.z) D[(tl.x + 1) * L] = c1;
-    hop_relax(decltype(ch)::value ? 1 : 0, rec + (uint32_t)h, c0, c1, l, c0, c1);
+    hop_relax(decltype(ch)::value, rec + (uint32_t)h, c0, c1, l, c0, c1);
     tl = tn;
     l = ln;
   };
   int h = 0;
-  if (chain) {
-    if (h < K - 1) step(Bool<false>(), h++);
+  if (chain) {  // bit 0: chain middle; bit 1: root first, join last (kind bits 3, 4)
+    if (h < K - 1) {
+      if (chain & 2) step(Ty<2>(), h++);
+      else step(Ty<0>(), h++);
+    }
 #pragma unroll 1
-    for (; h < K - 1; ++h) step(Bool<true>(), h);
+    for (; h < K - 1; ++h) step(Ty<1>(), h);
+    if ((chain & 2) && h < K) step(Ty<3>(), h++);
   }
 #pragma unroll 1
-  for (; h < K; ++h) step(Bool<false>(), h);
+  for (; h < K; ++h) step(Ty<0>(), h);
   return c0;  // after the last partition: the relaxation into top
 }
 
@@ -754,7 +762,7 @@ __device__ __forceinline__ T mask_cfr(const int K, const bool chain, const HopRe
 // previous backward pass, or recomputed by mask_ctt); STORE: D of P_h is
 // overwritten with shp(r, v) for the next backward pass (P:315-316 reuse).
 template <typename T, bool STORE, bool REC, int LC>
-__device__ __forceinline__ double mask_forward(const int K, const bool chain, const HopRec<T> *rec, const int L_rt,
+__device__ __forceinline__ double mask_forward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
                                                T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
                                                T *m0g, T *m1g) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
@@ -764,7 +772,7 @@ __device__ __forceinline__ double mask_forward(const int K, const bool chain, co
   T l = lam[0], av = va[0];
   T x0 = D[tl.y * L], x1 = D[(tl.y + 1) * L];
   auto step = [&](auto ch, int h) {
-    constexpr int ty = decltype(ch)::value ? 1 : 0;
+    constexpr int ty = decltype(ch)::value;
     const uint32_t hn = h + 1 < K ? h + 1 : h;
     const int4 tn = hop_tail(rec + hn);
     const T ln = lam[hn * L], avn = va[hn * L];
@@ -784,13 +792,17 @@ __device__ __forceinline__ double mask_forward(const int K, const bool chain, co
     x1 = x1n;
   };
   int h = 0;
-  if (chain) {
-    if (h < K - 1) step(Bool<false>(), h++);
+  if (chain) {  // bit 0: chain middle; bit 1: root first, join last (kind bits 3, 4)
+    if (h < K - 1) {
+      if (chain & 2) step(Ty<2>(), h++);
+      else step(Ty<0>(), h++);
+    }
 #pragma unroll 1
-    for (; h < K - 1; ++h) step(Bool<true>(), h);
+    for (; h < K - 1; ++h) step(Ty<1>(), h);
+    if ((chain & 2) && h < K) step(Ty<3>(), h++);
   }
 #pragma unroll 1
-  for (; h < K; ++h) step(Bool<false>(), h);
+  for (; h < K; ++h) step(Ty<0>(), h);
   if (valid) acc += (double)c0;  // E^j = shp(r, T) at the updated lambda
   return acc;
 }
@@ -799,7 +811,7 @@ __device__ __forceinline__ double mask_forward(const int K, const bool chain, co
 // forward pass, or recomputed by mask_cfr); STORE: D of P_h is overwritten
 // with shp(v, T) for the next forward pass.
 template <typename T, bool STORE, bool REC, int LC>
-__device__ __forceinline__ double mask_backward(const int K, const bool chain, const HopRec<T> *rec, const int L_rt,
+__device__ __forceinline__ double mask_backward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
                                                 T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
                                                 T *m0g, T *m1g) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
@@ -812,7 +824,7 @@ __device__ __forceinline__ double mask_backward(const int K, const bool chain, c
   // load would alias the store of the partition above)
   T f0 = D[tl.x * L], f1 = tl.z ? D[(tl.x + 1) * L] : inf;
   auto step = [&](auto ch, int h) {
-    constexpr int ty = decltype(ch)::value ? 1 : 0;
+    constexpr int ty = decltype(ch)::value;
     const uint32_t hn = h > 0 ? h - 1 : 0;
     const int4 tn = hop_tail(rec + hn);
     const T ln = lam[hn * L], avn = va[hn * L];
@@ -832,13 +844,17 @@ __device__ __forceinline__ double mask_backward(const int K, const bool chain, c
     f1 = f1n;
   };
   int h = K - 1;
-  if (chain) {
-    if (h > 0) step(Bool<false>(), h--);
+  if (chain) {  // bit 0: chain middle; bit 1: join last, root first
+    if (h > 0) {
+      if (chain & 2) step(Ty<3>(), h--);
+      else step(Ty<0>(), h--);
+    }
 #pragma unroll 1
-    for (; h > 0; --h) step(Bool<true>(), h);
+    for (; h > 0; --h) step(Ty<1>(), h);
+    if ((chain & 2) && h >= 0) step(Ty<2>(), h--);
   }
 #pragma unroll 1
-  for (; h >= 0; --h) step(Bool<false>(), h);
+  for (; h >= 0; --h) step(Ty<0>(), h);
   if (valid) acc += (double)x0;  // E^j = shp(r, T)
   return acc;
 }
@@ -993,7 +1009,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
         // arc-mask tile (narrow shape, shared topology)
         if (active) {
           const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(s.topo);
-          const bool chain = d.kind & 8;
+          const int chain = ((d.kind & 8) ? 1 : 0) | ((d.kind & 16) ? 2 : 0);
           T *D = RC ? reinterpret_cast<T *>(rbase) + lane : s.dist + lane;
           if (RC) {
             D[d.nodes * L] = T(0);              // top
@@ -1131,7 +1147,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
 // (c forward, x backward) is carried in and out.  The same prefetching loops
 // and hop arithmetic as mask_forward / mask_backward (store design).
 template <typename T, bool REC, int LC>
-__device__ __forceinline__ void mask_forward_range(const int hb, const int he, const int K, const bool chain,
+__device__ __forceinline__ void mask_forward_range(const int hb, const int he, const int K, const int chain,
                                                    const HopRec<T> *rec, const int L_rt, T *lam, T *va, T *D,
                                                    const int r0, const bool valid, const T omega, const T clamp,
                                                    T *m0g, T *m1g, T &c0, T &c1, double &acc) {
@@ -1140,7 +1156,7 @@ __device__ __forceinline__ void mask_forward_range(const int hb, const int he, c
   T l = lam[0], av = va[0];
   T x0 = D[(uint32_t)(tl.y - r0) * L], x1 = D[(uint32_t)(tl.y + 1 - r0) * L];
   auto step = [&](auto ch, int h) {
-    constexpr int ty = decltype(ch)::value ? 1 : 0;
+    constexpr int ty = decltype(ch)::value;
     const uint32_t i = h - hb, in = h + 1 < he ? i + 1 : i;
     const int4 tn = hop_tail(rec + in);
     const T ln = lam[in * L], avn = va[in * L];
@@ -1159,17 +1175,21 @@ __device__ __forceinline__ void mask_forward_range(const int hb, const int he, c
   };
   int h = hb;
   if (chain) {
-    if (h == 0 && h < he) step(Bool<false>(), h++);
+    if (h == 0 && h < he && K > 1) {
+      if (chain & 2) step(Ty<2>(), h++);
+      else step(Ty<0>(), h++);
+    }
     const int hm = min(he, K - 1);
 #pragma unroll 1
-    for (; h < hm; ++h) step(Bool<true>(), h);
+    for (; h < hm; ++h) step(Ty<1>(), h);
+    if ((chain & 2) && h == K - 1 && h < he) step(Ty<3>(), h++);
   }
 #pragma unroll 1
-  for (; h < he; ++h) step(Bool<false>(), h);
+  for (; h < he; ++h) step(Ty<0>(), h);
 }
 
 template <typename T, bool REC, int LC>
-__device__ __forceinline__ void mask_backward_range(const int hb, const int he, const int K, const bool chain,
+__device__ __forceinline__ void mask_backward_range(const int hb, const int he, const int K, const int chain,
                                                     const HopRec<T> *rec, const int L_rt, T *lam, T *va, T *D,
                                                     const int r0, const bool valid, const T omega, const T clamp,
                                                     T *m0g, T *m1g, T &x0, T &x1, double &acc) {
@@ -1180,7 +1200,7 @@ __device__ __forceinline__ void mask_backward_range(const int hb, const int he, 
   T l = lam[top * L], av = va[top * L];
   T f0 = D[(uint32_t)(tl.x - r0) * L], f1 = tl.z ? D[(uint32_t)(tl.x + 1 - r0) * L] : inf;
   auto step = [&](auto ch, int h) {
-    constexpr int ty = decltype(ch)::value ? 1 : 0;
+    constexpr int ty = decltype(ch)::value;
     const uint32_t i = h - hb, in = h > hb ? i - 1 : i;
     const int4 tn = hop_tail(rec + in);
     const T ln = lam[in * L], avn = va[in * L];
@@ -1199,13 +1219,17 @@ __device__ __forceinline__ void mask_backward_range(const int hb, const int he, 
   };
   int h = he - 1;
   if (chain) {
-    if (h == K - 1 && h >= hb) step(Bool<false>(), h--);
+    if (h == K - 1 && h >= hb && K > 1) {
+      if (chain & 2) step(Ty<3>(), h--);
+      else step(Ty<0>(), h--);
+    }
     const int hm = max(hb, 1);
 #pragma unroll 1
-    for (; h >= hm; --h) step(Bool<true>(), h);
+    for (; h >= hm; --h) step(Ty<1>(), h);
+    if ((chain & 2) && h == 0 && h >= hb) step(Ty<2>(), h--);
   }
 #pragma unroll 1
-  for (; h >= hb; --h) step(Bool<false>(), h);
+  for (; h >= hb; --h) step(Ty<0>(), h);
 }
 
 // ---------------------------------------------------------------------------
@@ -1290,7 +1314,7 @@ __global__ void __launch_bounds__(128) sweep_chunk_kernel(const SweepArgs a) {
   const TileDesc d = a.tiles[t];
   const int L = d.lanes, K = d.K;
   const bool valid = lane < d.n_lanes, active = lane < L;
-  const bool chain = d.kind & 8;
+  const int chain = ((d.kind & 8) ? 1 : 0) | ((d.kind & 16) ? 2 : 0);
   const HopRec<T> *grec = reinterpret_cast<const HopRec<T> *>(a.recs + 16 * (int64_t)d.rec_base);
   T *glam = reinterpret_cast<T *>(a.lambda) + d.slot_base;
   T *gva = reinterpret_cast<T *>(a.delta_out) + d.slot_base;
@@ -1402,7 +1426,7 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
     // arc-mask tile: the same min-plus loops as the staged kernel, on global
     // memory (records are warp-uniform loads through L1)
     const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(a.recs + 16 * (int64_t)d.rec_base);
-    const bool chain = d.kind & 8;
+    const int chain = ((d.kind & 8) ? 1 : 0) | ((d.kind & 16) ? 2 : 0);
     T *lam = reinterpret_cast<T *>(a.lambda) + d.slot_base + lane;
     T *va = reinterpret_cast<T *>(a.delta_out) + d.slot_base + lane;
     T *D = reinterpret_cast<T *>(a.dist) + d.dist_base + lane;

@@ -270,6 +270,14 @@ static bool chain_shape(const Shape &S) {
   return true;
 }
 
+// kind bit 4 (with bit 3): the first partition is a root hop (type 2) and the
+// last a join into top (type 3) -- every hop of the shape is then folded
+static bool ends_shape(const Shape &S) {
+  if (S.max_w > 2 || S.k < 2) return false;
+  double A[8];
+  return hop_masks(S, 0, A) == 2 && hop_masks(S, S.k - 1, A) == 3;
+}
+
 // Hop records (layout: internal.h HopRec) of a shape whose partitions have
 // <= 2 nodes, in the build precision.
 static void append_recs(const Shape &S, int tsz, std::vector<unsigned char> &out) {
@@ -537,7 +545,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       if (!staged && k0) full = rows.size();
       for (size_t q = 0; q < full; q += L) {
         PendingTile t;
-        t.kind = (staged ? 2 : 0) | k0 | (k0 && chain_shape(S) ? 8 : 0);  // records also serve the streaming kernel
+        const bool ch = k0 && chain_shape(S);
+        t.kind = (staged ? 2 : 0) | k0 | (ch ? 8 : 0) | (ch && ends_shape(S) ? 16 : 0);  // records also serve the streaming kernel
         t.shape = (int32_t)s;
         t.L = L;
         t.rows.assign(rows.begin() + q, rows.begin() + std::min(rows.size(), q + L));
