@@ -690,18 +690,28 @@ __device__ __forceinline__ T mask_finish(T *lam, T *va, uint32_t hL, T l, T av, 
 template <int N>
 using Ty = std::integral_constant<int, N>;  // compile-time hop type (hop_mm)
 
+// Record tail (n0, n1, w2, type) of partition h (records given from partition
+// hb on).  ENDS (kind bit 4): every hop folded, and the partition sizes are
+// 1, 2, 2, ..., 2 -- P_0 = {0}, P_h = {2h - 1, 2h}, top = 2K - 1 -- so the
+// tail is arithmetic and the records are never read.
+template <bool ENDS, typename T>
+__device__ __forceinline__ int4 tail_of(const HopRec<T> *rec, int h, int hb = 0) {
+  if (ENDS) return make_int4(h ? 2 * h - 1 : 0, 2 * h + 1, h ? 1 : 0, 0);
+  return hop_tail(rec + (h - hb));
+}
+
 // shp(v, T) of every node under the current lambda (no update); returns
 // shp(r, T) = E^j.  (kEnergy; phase 1 of a recompute forward pass.)
-template <typename T, int LC>
-__device__ __forceinline__ T mask_ctt(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+template <typename T, int LC, bool ENDS>
+__device__ __forceinline__ T mask_ctt_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
                                       const T *lam, T *D) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   T x0 = T(0), x1 = t_inf<T>();
-  int4 tl = hop_tail(rec + K - 1);
+  int4 tl = tail_of<ENDS>(rec, K - 1);
   T l = lam[(K - 1) * L];
   auto step = [&](auto ch, int h) {
     const uint32_t hn = h > 0 ? h - 1 : 0;
-    const int4 tn = hop_tail(rec + hn);
+    const int4 tn = tail_of<ENDS>(rec, hn);
     const T ln = lam[hn * L];
     hop_ctt(decltype(ch)::value, rec + (uint32_t)h, x0, x1, l, x0, x1);
     D[tl.x * L] = x0;
@@ -724,18 +734,25 @@ __device__ __forceinline__ T mask_ctt(const int K, const int chain, const HopRec
   return x0;
 }
 
+template <typename T, int LC>
+__device__ __forceinline__ T mask_ctt(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+                                      const T *lam, T *D) {
+  if (chain & 2) return mask_ctt_impl<T, LC, true>(K, chain, rec, L_rt, lam, D);
+  return mask_ctt_impl<T, LC, false>(K, chain, rec, L_rt, lam, D);
+}
+
 // shp(r, v) of every node under the current lambda (no update); returns
 // shp(r, T) = E^j.  (kCfr; phase 1 of a recompute backward pass.)
-template <typename T, int LC>
-__device__ __forceinline__ T mask_cfr(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+template <typename T, int LC, bool ENDS>
+__device__ __forceinline__ T mask_cfr_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
                                       const T *lam, T *D) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   T c0 = T(0), c1 = t_inf<T>();
-  int4 tl = hop_tail(rec);
+  int4 tl = tail_of<ENDS>(rec, 0);
   T l = lam[0];
   auto step = [&](auto ch, int h) {
     const uint32_t hn = h + 1 < K ? h + 1 : h;
-    const int4 tn = hop_tail(rec + hn);
+    const int4 tn = tail_of<ENDS>(rec, hn);
     const T ln = lam[hn * L];
     D[tl.x * L] = c0;
     if (tl.z) D[(tl.x + 1) * L] = c1;
@@ -758,23 +775,30 @@ __device__ __forceinline__ T mask_cfr(const int K, const int chain, const HopRec
   return c0;  // after the last partition: the relaxation into top
 }
 
+template <typename T, int LC>
+__device__ __forceinline__ T mask_cfr(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+                                      const T *lam, T *D) {
+  if (chain & 2) return mask_cfr_impl<T, LC, true>(K, chain, rec, L_rt, lam, D);
+  return mask_cfr_impl<T, LC, false>(K, chain, rec, L_rt, lam, D);
+}
+
 // forward pass with updates.  D holds shp(v, T) (stored by the
 // previous backward pass, or recomputed by mask_ctt); STORE: D of P_h is
 // overwritten with shp(r, v) for the next backward pass (P:315-316 reuse).
-template <typename T, bool STORE, bool REC, int LC>
-__device__ __forceinline__ double mask_forward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+template <typename T, bool STORE, bool REC, int LC, bool ENDS>
+__device__ __forceinline__ double mask_forward_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
                                                T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
                                                T *m0g, T *m1g) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   double acc = 0.0;
   T c0 = T(0), c1 = t_inf<T>();
-  int4 tl = hop_tail(rec);
+  int4 tl = tail_of<ENDS>(rec, 0);
   T l = lam[0], av = va[0];
   T x0 = D[tl.y * L], x1 = D[(tl.y + 1) * L];
   auto step = [&](auto ch, int h) {
     constexpr int ty = decltype(ch)::value;
     const uint32_t hn = h + 1 < K ? h + 1 : h;
-    const int4 tn = hop_tail(rec + hn);
+    const int4 tn = tail_of<ENDS>(rec, hn);
     const T ln = lam[hn * L], avn = va[hn * L];
     const T x0n = D[tn.y * L], x1n = D[(tn.y + 1) * L];
     if (STORE) {
@@ -807,18 +831,26 @@ __device__ __forceinline__ double mask_forward(const int K, const int chain, con
   return acc;
 }
 
+template <typename T, bool STORE, bool REC, int LC>
+__device__ __forceinline__ double mask_forward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+                                               T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
+                                               T *m0g, T *m1g) {
+  if (chain & 2) return mask_forward_impl<T, STORE, REC, LC, true>(K, chain, rec, L_rt, lam, va, D, valid, omega, clamp, m0g, m1g);
+  return mask_forward_impl<T, STORE, REC, LC, false>(K, chain, rec, L_rt, lam, va, D, valid, omega, clamp, m0g, m1g);
+}
+
 // backward pass with updates.  D holds shp(r, v) (stored by the
 // forward pass, or recomputed by mask_cfr); STORE: D of P_h is overwritten
 // with shp(v, T) for the next forward pass.
-template <typename T, bool STORE, bool REC, int LC>
-__device__ __forceinline__ double mask_backward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+template <typename T, bool STORE, bool REC, int LC, bool ENDS>
+__device__ __forceinline__ double mask_backward_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
                                                 T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
                                                 T *m0g, T *m1g) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   const T inf = t_inf<T>();
   double acc = 0.0;
   T x0 = T(0), x1 = inf;  // shp(., T) of P_{h+1}; the last partition's targets: top
-  int4 tl = hop_tail(rec + K - 1);
+  int4 tl = tail_of<ENDS>(rec, K - 1);
   T l = lam[(K - 1) * L], av = va[(K - 1) * L];
   // (a one-node partition's second entry is not read: in global memory the
   // load would alias the store of the partition above)
@@ -826,7 +858,7 @@ __device__ __forceinline__ double mask_backward(const int K, const int chain, co
   auto step = [&](auto ch, int h) {
     constexpr int ty = decltype(ch)::value;
     const uint32_t hn = h > 0 ? h - 1 : 0;
-    const int4 tn = hop_tail(rec + hn);
+    const int4 tn = tail_of<ENDS>(rec, hn);
     const T ln = lam[hn * L], avn = va[hn * L];
     const T f0n = D[tn.x * L], f1n = tn.z ? D[(tn.x + 1) * L] : inf;
     T m0, m1r;
@@ -857,6 +889,14 @@ __device__ __forceinline__ double mask_backward(const int K, const int chain, co
   for (; h >= 0; --h) step(Ty<0>(), h);
   if (valid) acc += (double)x0;  // E^j = shp(r, T)
   return acc;
+}
+
+template <typename T, bool STORE, bool REC, int LC>
+__device__ __forceinline__ double mask_backward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+                                                T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
+                                                T *m0g, T *m1g) {
+  if (chain & 2) return mask_backward_impl<T, STORE, REC, LC, true>(K, chain, rec, L_rt, lam, va, D, valid, omega, clamp, m0g, m1g);
+  return mask_backward_impl<T, STORE, REC, LC, false>(K, chain, rec, L_rt, lam, va, D, valid, omega, clamp, m0g, m1g);
 }
 
 // Stage buffer of one tile (layout: internal.h).
@@ -896,14 +936,16 @@ __device__ __forceinline__ void issue_stage(const SweepArgs &a, const TileDesc &
   const uint32_t va_b = upd ? lam_b : 0u;
   const uint32_t dist_b = RC ? 0u : (uint32_t)(d.nodes + 2) * d.lanes * sizeof(T);
   const bool masks = d.kind & 4;  // hop records instead of topology + partition offsets
-  const uint32_t topo_b = masks ? (uint32_t)(d.K * rec_bytes((int)sizeof(T))) : (uint32_t)stage_topo_bytes(d.kind, d.nodes, d.lanes);
+  // (fully folded tiles, kind bit 4, never read their records)
+  const uint32_t topo_b = masks ? ((d.kind & 16) ? 0u : (uint32_t)(d.K * rec_bytes((int)sizeof(T))))
+                                : (uint32_t)stage_topo_bytes(d.kind, d.nodes, d.lanes);
   const uint32_t hop_b = masks ? 0u : (uint32_t)stage_hop_bytes(d.K);
   mbar_expect_tx(bar, lam_b + va_b + dist_b + topo_b + hop_b);
   bulk_g2s(s.lam, reinterpret_cast<const T *>(a.lambda) + d.slot_base, lam_b, bar);
   if (va_b) bulk_g2s(s.va, reinterpret_cast<const T *>(a.delta_out) + d.slot_base, va_b, bar);
   if (!RC) bulk_g2s(s.dist, reinterpret_cast<const T *>(a.dist) + d.dist_base, dist_b, bar);
   if (masks) {
-    bulk_g2s(s.topo, a.recs + 16 * (int64_t)d.rec_base, topo_b, bar);
+    if (topo_b) bulk_g2s(s.topo, a.recs + 16 * (int64_t)d.rec_base, topo_b, bar);
   } else {
     bulk_g2s(s.topo, a.topo + d.topo_base, topo_b, bar);
     bulk_g2s(s.hop, a.hop_off + d.hop_base, hop_b, bar);
@@ -1146,19 +1188,19 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
 // buffers) and whose distances hold rows from node r0 on; the recursion state
 // (c forward, x backward) is carried in and out.  The same prefetching loops
 // and hop arithmetic as mask_forward / mask_backward (store design).
-template <typename T, bool REC, int LC>
-__device__ __forceinline__ void mask_forward_range(const int hb, const int he, const int K, const int chain,
+template <typename T, bool REC, int LC, bool ENDS>
+__device__ __forceinline__ void mask_forward_range_impl(const int hb, const int he, const int K, const int chain,
                                                    const HopRec<T> *rec, const int L_rt, T *lam, T *va, T *D,
                                                    const int r0, const bool valid, const T omega, const T clamp,
                                                    T *m0g, T *m1g, T &c0, T &c1, double &acc) {
   const uint32_t L = LC ? LC : L_rt;
-  int4 tl = hop_tail(rec);
+  int4 tl = tail_of<ENDS>(rec, hb, hb);
   T l = lam[0], av = va[0];
   T x0 = D[(uint32_t)(tl.y - r0) * L], x1 = D[(uint32_t)(tl.y + 1 - r0) * L];
   auto step = [&](auto ch, int h) {
     constexpr int ty = decltype(ch)::value;
     const uint32_t i = h - hb, in = h + 1 < he ? i + 1 : i;
-    const int4 tn = hop_tail(rec + in);
+    const int4 tn = tail_of<ENDS>(rec, hb + (int)in, hb);
     const T ln = lam[in * L], avn = va[in * L];
     const T x0n = D[(uint32_t)(tn.y - r0) * L], x1n = D[(uint32_t)(tn.y + 1 - r0) * L];
     D[(uint32_t)(tl.x - r0) * L] = c0;  // keep shp(r, v) for the backward pass
@@ -1189,20 +1231,29 @@ __device__ __forceinline__ void mask_forward_range(const int hb, const int he, c
 }
 
 template <typename T, bool REC, int LC>
-__device__ __forceinline__ void mask_backward_range(const int hb, const int he, const int K, const int chain,
+__device__ __forceinline__ void mask_forward_range(const int hb, const int he, const int K, const int chain,
+                                                   const HopRec<T> *rec, const int L_rt, T *lam, T *va, T *D,
+                                                   const int r0, const bool valid, const T omega, const T clamp,
+                                                   T *m0g, T *m1g, T &c0, T &c1, double &acc) {
+  if (chain & 2) return mask_forward_range_impl<T, REC, LC, true>(hb, he, K, chain, rec, L_rt, lam, va, D, r0, valid, omega, clamp, m0g, m1g, c0, c1, acc);
+  return mask_forward_range_impl<T, REC, LC, false>(hb, he, K, chain, rec, L_rt, lam, va, D, r0, valid, omega, clamp, m0g, m1g, c0, c1, acc);
+}
+
+template <typename T, bool REC, int LC, bool ENDS>
+__device__ __forceinline__ void mask_backward_range_impl(const int hb, const int he, const int K, const int chain,
                                                     const HopRec<T> *rec, const int L_rt, T *lam, T *va, T *D,
                                                     const int r0, const bool valid, const T omega, const T clamp,
                                                     T *m0g, T *m1g, T &x0, T &x1, double &acc) {
   const uint32_t L = LC ? LC : L_rt;
   const T inf = t_inf<T>();
   const uint32_t top = he - 1 - hb;
-  int4 tl = hop_tail(rec + top);
+  int4 tl = tail_of<ENDS>(rec, hb + (int)top, hb);
   T l = lam[top * L], av = va[top * L];
   T f0 = D[(uint32_t)(tl.x - r0) * L], f1 = tl.z ? D[(uint32_t)(tl.x + 1 - r0) * L] : inf;
   auto step = [&](auto ch, int h) {
     constexpr int ty = decltype(ch)::value;
     const uint32_t i = h - hb, in = h > hb ? i - 1 : i;
-    const int4 tn = hop_tail(rec + in);
+    const int4 tn = tail_of<ENDS>(rec, hb + (int)in, hb);
     const T ln = lam[in * L], avn = va[in * L];
     const T f0n = D[(uint32_t)(tn.x - r0) * L], f1n = tn.z ? D[(uint32_t)(tn.x + 1 - r0) * L] : inf;
     T m0, m1r;
@@ -1230,6 +1281,15 @@ __device__ __forceinline__ void mask_backward_range(const int hb, const int he, 
   }
 #pragma unroll 1
   for (; h >= hb; --h) step(Ty<0>(), h);
+}
+
+template <typename T, bool REC, int LC>
+__device__ __forceinline__ void mask_backward_range(const int hb, const int he, const int K, const int chain,
+                                                    const HopRec<T> *rec, const int L_rt, T *lam, T *va, T *D,
+                                                    const int r0, const bool valid, const T omega, const T clamp,
+                                                    T *m0g, T *m1g, T &x0, T &x1, double &acc) {
+  if (chain & 2) return mask_backward_range_impl<T, REC, LC, true>(hb, he, K, chain, rec, L_rt, lam, va, D, r0, valid, omega, clamp, m0g, m1g, x0, x1, acc);
+  return mask_backward_range_impl<T, REC, LC, false>(hb, he, K, chain, rec, L_rt, lam, va, D, r0, valid, omega, clamp, m0g, m1g, x0, x1, acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -1291,14 +1351,15 @@ __device__ __forceinline__ ChunkStage<T> chunk_stage_at(unsigned char *p) {
 
 template <typename T>
 __device__ __forceinline__ void chunk_issue(const ChunkStage<T> &st, const ChunkSpan &sp, int L, const T *glam,
-                                            const T *gva, const HopRec<T> *grec, const T *gD, uint64_t *bar) {
+                                            const T *gva, const HopRec<T> *grec, const T *gD, uint64_t *bar,
+                                            bool folded) {
   const int nh = sp.h1 - sp.h0;
-  const uint32_t lb = (uint32_t)nh * L * sizeof(T), rb = (uint32_t)nh * sizeof(HopRec<T>);
+  const uint32_t lb = (uint32_t)nh * L * sizeof(T), rb = folded ? 0u : (uint32_t)nh * sizeof(HopRec<T>);
   const uint32_t db = (uint32_t)(sp.rend - sp.r0) * L * sizeof(T);
   mbar_expect_tx(bar, 2 * lb + rb + db);
   bulk_g2s(st.lam, glam + (int64_t)sp.h0 * L, lb, bar);
   bulk_g2s(st.va, gva + (int64_t)sp.h0 * L, lb, bar);
-  bulk_g2s(st.rec, grec + sp.h0, rb, bar);
+  if (rb) bulk_g2s(st.rec, grec + sp.h0, rb, bar);
   bulk_g2s(st.D, gD + (int64_t)sp.r0 * L, db, bar);
 }
 
@@ -1331,7 +1392,7 @@ __global__ void __launch_bounds__(128) sweep_chunk_kernel(const SweepArgs a) {
   pdl_wait();
   const int nch = (K + kChunk - 1) / kChunk;
   auto chunk_of = [&](int ci) { return MODE == kForward ? ci : nch - 1 - ci; };
-  if (lane == 0) chunk_issue(chunk_stage_at<T>(sb[0]), chunk_span<T, MODE>(d, grec, chunk_of(0)), L, glam, gva, grec, gD, &bar[0]);
+  if (lane == 0) chunk_issue(chunk_stage_at<T>(sb[0]), chunk_span<T, MODE>(d, grec, chunk_of(0)), L, glam, gva, grec, gD, &bar[0], d.kind & 16);
   uint32_t phase = 0;
   double acc = 0.0;
   T c0 = T(0), c1 = inf;  // forward: shp(r, .) of the current partition
@@ -1342,7 +1403,7 @@ __global__ void __launch_bounds__(128) sweep_chunk_kernel(const SweepArgs a) {
     if (ci + 1 < nch && lane == 0) {
       bulk_wait_read_all();  // the stores of chunk ci - 1 (same buffer as ci + 1) have read it
       chunk_issue(chunk_stage_at<T>(sb[b ^ 1]), chunk_span<T, MODE>(d, grec, chunk_of(ci + 1)), L, glam, gva, grec, gD,
-                  &bar[b ^ 1]);
+                  &bar[b ^ 1], d.kind & 16);
     }
     const ChunkStage<T> st = chunk_stage_at<T>(sb[b]);
     mbar_wait(&bar[b], (phase >> b) & 1u);

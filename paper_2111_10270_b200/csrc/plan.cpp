@@ -466,9 +466,9 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // pack(rc): budget + tiles for the store design (rc = false) or the
   // recompute design (rc = true, narrow shapes only); returns the tiles in
   // launch order
-  auto pack = [&](bool rc) {
+  auto pack = [&](bool rc, int nb) {
     std::vector<PendingTile> pend;
-    P.NB = nbuf ? (atoi(nbuf) == 1 ? 1 : 2) : (rc ? 1 : 2);
+    P.NB = nbuf ? (atoi(nbuf) == 1 ? 1 : 2) : nb;
     auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB) {
       if (rc) return stage_bytes_rc(tsz, kind, K, nodes, L) <= SB && stage_dist_bytes(tsz, nodes, L) <= DB;
       return stage_bytes(tsz, kind, K, nodes, L) <= SB && relax_bytes(tsz, W, L) <= DB;
@@ -637,7 +637,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   const bool l2_resident = store_bytes <= 0.75 * 126e6;
   bool rc = narrow && !(sw && (sw[0] == 't' || sw[0] == 's')) && !(fz && fz[0] == '1') &&
             (!l2_resident || (sw && sw[0] == 'r'));
-  std::vector<PendingTile> pend = pack(rc);
+  std::vector<PendingTile> pend = pack(rc, rc ? 1 : 2);
   if (rc) {
     bool direct = false;
     for (const auto &t : pend) direct = direct || !(t.kind & 2);
@@ -645,7 +645,12 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     const bool small = pend.size() <= 64 && P.n_slots <= (1 << 15) && P.world == 1 && !(fz && fz[0] == '0');
     if (direct || (small && !(sw && sw[0] == 'r'))) {
       rc = false;
-      pend = pack(false);
+      pend = pack(false, 2);
+    } else if (warp_bytes(P.SB, P.DB, 1) <= 8192) {
+      // short rows: single-buffered warps finish a tile faster than its TMA
+      // stage arrives -- double-buffer (measured: MRF 287 -> 248 us per sweep;
+      // CellTrack / QAP50, whose stages are larger, stay single-buffered)
+      pend = pack(true, 2);
     }
   }
   P.rc = rc;
