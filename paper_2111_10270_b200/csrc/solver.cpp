@@ -775,6 +775,13 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_canon_out = r + o_canon;
   s->external = s->world > 1 && !o->nccl_unique_id;
   if (s->world > 1 && !s->external && (st = init_nccl(s, o))) return st;
+  // FDOG_NCCL_SELF=1 (test knob): a one-rank NCCL communicator for world == 1,
+  // so the bound's allreduce goes through the same dlopen'ed NCCL calls as a
+  // multi-GPU run (tests/test_gpu_parity.py::test_nccl_one_rank_communicator)
+  if (s->world == 1 && o->nccl_unique_id) {
+    const char *ns = getenv("FDOG_NCCL_SELF");
+    if (ns && ns[0] == '1' && (st = init_nccl(s, o))) return st;
+  }
 
   // algorithmic bytes per launch: per node 2 T (distance read +
   // write) + 4 B topology for per-lane-topology tiles; per slot 4 T (lambda
@@ -1304,7 +1311,7 @@ fdog_status fdog_lower_bound(fdog_solver *s, double *out) {
   CK(cudaMemcpyAsync(&v, s->d_lb, sizeof(double), cudaMemcpyDeviceToHost, s->stream), "D2H");
   CK(cudaStreamSynchronize(s->stream), "sync");
   double tot = v + s->free_term;
-  if (s->world > 1 && !s->external) {
+  if ((s->world > 1 && !s->external) || s->nccl.comm) {
     // scalar allreduce of the per-rank partials (fp64)
     double *d = s->d_lb + 1;  // scratch slot for the cross-rank sum
     CK(cudaMemcpyAsync(d, &tot, sizeof(double), cudaMemcpyHostToDevice, s->stream), "H2D");

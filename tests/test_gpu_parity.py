@@ -439,3 +439,23 @@ def test_long_rows_chunked(oracle_mod, monkeypatch, chunk):
     for p in (_long_rows(3), synth.thin_hop(5, k=3000)):
         g, _ = _compare_pass_by_pass(p, oracle_mod, passes=4)
         assert g.stats()["sweep_streaming"] == (2 if chunk == "1" else 1)
+
+
+def test_nccl_one_rank_communicator(monkeypatch):
+    """The NCCL path of a multi-GPU run (dlopen of the torch-bundled libnccl,
+    ncclCommInitRank with a torch-generated unique id, ncclAllReduce on the
+    solver's stream, ncclCommDestroy) on a one-rank communicator: the bound's
+    allreduce over one rank is the identity."""
+    import os
+    import torch
+    import nvidia.nccl
+    lib = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+    p = synth.gm_worms_like(51, n_src=40, k_cand=5, knn=6)
+    monkeypatch.setenv("FDOG_NCCL_SELF", "1")
+    g = F.Solver(p, precision=64, nccl_unique_id=torch.cuda.nccl.unique_id(), nccl_library=lib)
+    monkeypatch.setenv("FDOG_NCCL_SELF", "0")
+    h = F.Solver(p, precision=64)
+    for _ in range(3):
+        g.iterate(1, 0.5); h.iterate(1, 0.5)
+        assert g.lower_bound() == h.lower_bound()
+    g.close()
