@@ -2298,6 +2298,28 @@ int launch_dist_dp(int precision, const SeqArgs &a, int32_t n_tiles, int32_t for
   return (int)cudaGetLastError();
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) dist_sentinel_kernel(const TileDesc *tiles, int32_t n_tiles, T *dist) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int32_t t = (int32_t)(g >> 5), lane = (int32_t)(g & 31);
+  if (t >= n_tiles) return;
+  const TileDesc &d = tiles[t];
+  if (lane >= d.lanes) return;
+  T *top = dist + d.dist_base + (int64_t)d.nodes * d.lanes + lane;
+  top[0] = T(0);
+  top[d.lanes] = t_inf<T>();
+}
+
+int launch_dist_sentinels(int precision, const TileDesc *tiles, int32_t n_tiles, void *dist, void *stream) {
+  if (n_tiles <= 0) return 0;
+  const unsigned grid = (unsigned)(((int64_t)n_tiles * 32 + 255) / 256);
+  if (precision == 64)
+    dist_sentinel_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(tiles, n_tiles, (double *)dist);
+  else
+    dist_sentinel_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(tiles, n_tiles, (float *)dist);
+  return (int)cudaGetLastError();
+}
+
 int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream) {
   void *args[] = {(void *)&lb_part, (void *)&n, (void *)&out};
   return launch_pdl((const void *)lb_reduce_kernel, dim3(1), dim3(1024), 0, stream, args);

@@ -895,8 +895,9 @@ HostImage::~HostImage() {
 
 // Lay out every uploaded array in one buffer (256-byte aligned sections),
 // including the initial lambda_i^j = c_i / |J_i| (A9; fp64, rounded once
-// to the build precision) and the distance array with its sentinels (0 for
-// top, +inf for bottom, never overwritten).
+// to the build precision).  The distance array is not uploaded: the solver
+// allocates it and writes its sentinels on the device (0 for top, +inf for
+// bottom, never overwritten); the first energy sweep fills the rest.
 fdog_status build_image(Plan &P) {
   PhaseTimer tm;
   const int tsz = P.precision == 64 ? 8 : 4;
@@ -904,7 +905,7 @@ fdog_status build_image(Plan &P) {
   sz[kImTiles] = P.tiles.size() * sizeof(TileDesc);
   sz[kImHopOff] = P.hop_off.size() * 4;
   sz[kImTopo] = P.topo.size() * 4;
-  sz[kImSlotVar] = P.slot_var.size() * 4;
+  sz[kImSlotVar] = 0;  // (host-side only: no kernel reads it)
   sz[kImVarPtr] = P.var_ptr.size() * 8;
   sz[kImVarSlots] = P.var_slots.size() * 4;
   sz[kImVarXidx] = P.var_xidx.size() * 4;
@@ -917,7 +918,7 @@ fdog_status build_image(Plan &P) {
   sz[kImXLocal] = P.x_local.size() * 4;
   sz[kImXDeg] = P.x_deg.size() * 4;
   sz[kImLambda0] = P.slot_var.size() * tsz;
-  sz[kImDist0] = (size_t)P.n_dist * tsz;
+  sz[kImDist0] = 0;  // (allocated and initialised on the device, solver.cpp)
   sz[kImRecs] = P.recs.size();
   sz[kImCanon] = P.canon_slot.size() * 4;
   size_t at = 0;
@@ -946,7 +947,6 @@ fdog_status build_image(Plan &P) {
   put(kImTiles, P.tiles.data());
   put(kImHopOff, P.hop_off.data());
   put(kImTopo, P.topo.data());
-  put(kImSlotVar, P.slot_var.data());
   put(kImVarPtr, P.var_ptr.data());
   put(kImVarSlots, P.var_slots.data());
   put(kImVarXidx, P.var_xidx.data());
@@ -970,18 +970,6 @@ fdog_status build_image(Plan &P) {
     if (tsz == 8) ((double *)lam)[q] = v;
     else ((float *)lam)[q] = (float)v;
   }
-  unsigned char *dist = P.image.data + P.image.off[kImDist0];
-  for (const auto &d : P.tiles)
-    for (int l = 0; l < d.lanes; ++l) {
-      const size_t top = (size_t)(d.dist_base + (int64_t)d.nodes * d.lanes + l), bot = top + d.lanes;
-      if (tsz == 8) {
-        ((double *)dist)[top] = 0.0;
-        ((double *)dist)[bot] = INFINITY;
-      } else {
-        ((float *)dist)[top] = 0.0f;
-        ((float *)dist)[bot] = INFINITY;
-      }
-    }
   tm.mark("device image");
   return FDOG_OK;
 }

@@ -231,7 +231,7 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.hop_off = s->d_hop_off;
   a.topo = s->d_topo;
   a.recs = s->d_recs;
-  a.slot_var = s->d_slot_var;
+  a.slot_var = nullptr;  // (not uploaded)
   a.lambda = s->d_lambda;
   a.delta_out = s->d_delta[s->cur ^ 1];  // avg_i in (avg_kernel), delta out
   a.m0 = s->d_m0;
@@ -731,6 +731,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   const size_t o_x = carve((size_t)std::max<int64_t>(P.n_vars, 1));
   const size_t o_und = carve(sizeof(unsigned long long));
   const size_t o_canon = carve((size_t)std::max<size_t>(P.canon_slot.size(), 1) * s->tsz);
+  const size_t o_dist = carve((size_t)std::max<int64_t>(P.n_dist, 1) * s->tsz);
   unsigned char *base = nullptr;
   CK(cudaMalloc((void **)&base, im.bytes + rt), "cudaMalloc");
   s->allocs.push_back(base);
@@ -744,7 +745,6 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_topo = (uint32_t *)sec(kImTopo);
   s->d_recs = (const unsigned char *)sec(kImRecs);
   s->d_canon = (const int32_t *)sec(kImCanon);
-  s->d_slot_var = (int32_t *)sec(kImSlotVar);
   s->d_var_ptr = (int64_t *)sec(kImVarPtr);
   s->d_var_slots = (int32_t *)sec(kImVarSlots);
   s->d_var_xidx = (int32_t *)sec(kImVarXidx);
@@ -757,7 +757,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_x_local = (int32_t *)sec(kImXLocal);
   s->d_x_deg = (int32_t *)sec(kImXDeg);
   s->d_lambda = sec(kImLambda0);
-  s->d_dist = sec(kImDist0);
+  s->d_dist = nullptr;  // runtime region below
   unsigned char *r = base + im.bytes;
   s->d_delta[0] = r + o_delta0;
   s->d_delta[1] = r + o_delta1;
@@ -773,6 +773,12 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_x = (uint8_t *)(r + o_x);
   s->d_undecided = (unsigned long long *)(r + o_und);
   s->d_canon_out = r + o_canon;
+  s->d_dist = r + o_dist;
+  {
+    // the distances' sentinels (top 0, bottom +inf) of every tile lane
+    const int e = launch_dist_sentinels(s->precision, s->d_tiles, s->n_tiles, s->d_dist, s->stream);
+    if (e) return cuda_fail((cudaError_t)e, "sentinel launch");
+  }
   s->external = s->world > 1 && !o->nccl_unique_id;
   if (s->world > 1 && !s->external && (st = init_nccl(s, o))) return st;
   // FDOG_NCCL_SELF=1 (test knob): a one-rank NCCL communicator for world == 1,
