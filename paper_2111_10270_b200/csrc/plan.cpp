@@ -489,7 +489,10 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       const int cands[] = {6, 7, 8, 9, 10, 11, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 72, 96, 112};
       double best = 1e300;
       int bestSB = 0, bestDB = DB0;
-      for (int kb : cands) {
+      const char *mk = getenv("FDOG_MAXKB");  // experiment knob: largest per-warp budget (KB) the model may pick
+    const int maxkb = mk ? atoi(mk) : 1 << 30;
+    for (int kb : cands) {
+      if (kb > maxkb) continue;
         const int SB = rc ? ((kb * 1024 - 16) / (P.NB + 1)) & ~15 : ((kb * 1024 - 16 - DB0) / P.NB) & ~15;
         const int DB = rc ? SB : DB0;
         if (SB <= 0) continue;
@@ -503,7 +506,9 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
           double pen = 1.0;
           if (L == 0) {  // direct from global memory: latency-bound
             L = 32;
-            pen = 10.0;
+            // (the recompute design cannot run direct tiles at all: a budget
+            // that leaves any is a fallback to the store design)
+            pen = rc ? 1e6 : 10.0;
           } else {
             usedSB = std::max(usedSB, rc ? stage_bytes_rc(tsz, k0, S.k, S.nodes(), L) : stage_bytes(tsz, k0, S.k, S.nodes(), L));
             if (rc) usedDB = std::max(usedDB, stage_dist_bytes(tsz, S.nodes(), L));
@@ -1099,6 +1104,30 @@ fdog_status fdog_plan_slot_map(const fdog_plan *plan, int64_t *dev_slot, int64_t
     return FDOG_EINVAL;
   }
   std::copy(plan->p.canon_slot.begin(), plan->p.canon_slot.end(), dev_slot);
+  return FDOG_OK;
+}
+
+fdog_status fdog_plan_tiles(const fdog_plan *plan, int32_t *desc, int64_t cap, int64_t *n) {
+  if (!plan || !n) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  const auto &T = plan->p.tiles;
+  *n = (int64_t)T.size();
+  if (!desc) return FDOG_OK;
+  if (cap < *n) {
+    set_error("capacity %lld < %lld tiles", (long long)cap, (long long)*n);
+    return FDOG_EINVAL;
+  }
+  for (size_t t = 0; t < T.size(); ++t) {
+    int32_t *o = desc + 6 * t;
+    o[0] = T[t].kind;
+    o[1] = T[t].K;
+    o[2] = T[t].lanes;
+    o[3] = T[t].n_lanes;
+    o[4] = T[t].nodes;
+    o[5] = (int32_t)(T[t].slot_base / std::max(1, T[t].lanes) < 0 ? 0 : 0);
+  }
   return FDOG_OK;
 }
 
