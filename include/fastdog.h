@@ -121,6 +121,11 @@ fdog_status fdog_plan_bdd(const fdog_plan *plan, int32_t j, int32_t *k, int32_t 
 /* Device slot of every canonical slot (j ascending, h ascending) of this rank
  * (layout inspection; len >= the rank's slot count). */
 fdog_status fdog_plan_slot_map(const fdog_plan *plan, int64_t *dev_slot, int64_t len);
+/* Tile descriptors for inspection: 6 values per tile (kind bits -- 0 per-lane
+ * topology, 1 staged, 2 arc-mask records, 3 chain middle, 4 root/join ends --,
+ * partitions K, lanes L, valid lanes, nodes per lane, first device slot);
+ * *n = number of tiles; desc may be NULL to query *n; cap in tiles. */
+fdog_status fdog_plan_tiles(const fdog_plan *plan, int64_t *desc, int64_t cap, int64_t *n);
 /* Global row -> owning rank for every row (length n_cons). */
 fdog_status fdog_plan_owner(const fdog_plan *plan, int32_t *owner, int64_t len);
 /* Ascending global indices of the variables exchanged between ranks (held by

@@ -1107,7 +1107,7 @@ fdog_status fdog_plan_slot_map(const fdog_plan *plan, int64_t *dev_slot, int64_t
   return FDOG_OK;
 }
 
-fdog_status fdog_plan_tiles(const fdog_plan *plan, int32_t *desc, int64_t cap, int64_t *n) {
+fdog_status fdog_plan_tiles(const fdog_plan *plan, int64_t *desc, int64_t cap, int64_t *n) {
   if (!plan || !n) {
     set_error("bad argument");
     return FDOG_EINVAL;
@@ -1120,13 +1120,13 @@ fdog_status fdog_plan_tiles(const fdog_plan *plan, int32_t *desc, int64_t cap, i
     return FDOG_EINVAL;
   }
   for (size_t t = 0; t < T.size(); ++t) {
-    int32_t *o = desc + 6 * t;
+    int64_t *o = desc + 6 * t;
     o[0] = T[t].kind;
     o[1] = T[t].K;
     o[2] = T[t].lanes;
     o[3] = T[t].n_lanes;
     o[4] = T[t].nodes;
-    o[5] = (int32_t)(T[t].slot_base / std::max(1, T[t].lanes) < 0 ? 0 : 0);
+    o[5] = T[t].slot_base;
   }
   return FDOG_OK;
 }

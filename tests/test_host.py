@@ -177,3 +177,53 @@ def test_sharder_and_shared_index(world):
     # balance by row length
     nnz = np.array([sum(len(p.row(j)[0]) for j in np.flatnonzero(owner == r)) for r in range(world)])
     assert nnz.max() <= 1.1 * nnz.mean() + 64
+
+
+def _pattern(hs, lo, hi, h):
+    """Arc targets of partition h: per node (lo, hi) as 'next j' / 'T' / 'B'."""
+    n1 = hs[h + 1]
+    out = []
+    for n in range(hs[h], n1):
+        out.append(tuple("B" if c == -1 else "T" if c == -2 else int(c - n1) for c in (lo[n], hi[n])))
+    return out
+
+
+@pytest.mark.parametrize("name,make", [
+    ("gm", lambda: synth.gm_worms_like(3, n_src=60, k_cand=5, knn=6)),
+    ("mrf", lambda: synth.mrf_potts(3, H=8, W=9, L=4)),
+    ("qap", lambda: synth.qap(3, n=7)),
+    ("ct", lambda: synth.celltrack(3, frames=4, dets=30)),
+    ("thin", lambda: synth.thin_hop(3, k=2000)),  # too long to stage: a partly filled records tile
+])
+def test_hop_record_classes(name, make):
+    """Tile kind bits the kernels rely on, re-derived from each row's compiled
+    BDD: arc-mask tiles (bit 2) have partitions of <= 2 nodes; chain tiles
+    (bit 3) have the chain pattern 0->0, 1->1 (0-arcs), 1->0 (1-arc) in every
+    middle partition; root/join tiles (bit 4) have a one-node root with arcs
+    to nodes 0 / 1, partition sizes 1, 2, ..., 2 (node indices 2h-1, 2h: the
+    folded kernels compute them) and a last partition joining into top."""
+    p = make()
+    pl = F.Plan(p, precision=32)
+    tiles = pl.tiles()
+    smap = pl.slot_map()
+    nonempty = np.diff(p.row_ptr) > 0
+    first = {int(smap[p.row_ptr[j]]): j for j in range(p.n_cons) if nonempty[j]}
+    seen = 0
+    for kind, K, L, nl, nodes, base in tiles:
+        if not kind & 4:
+            assert not kind & 24
+            continue
+        for lane in range(nl):
+            j = first[int(base + lane)]
+            hs, lo, hi = pl.bdd(j)
+            assert len(hs) - 1 == K and np.all(np.diff(hs) <= 2)
+            if kind & 8:
+                for h in range(1, K - 1):
+                    assert _pattern(hs, lo, hi, h) == [(0, "B"), (1, 0)], (name, j, h)
+            if kind & 16:
+                assert kind & 8 and K >= 2
+                assert list(np.diff(hs)) == [1] + [2] * (K - 1) and hs[-1] == 2 * K - 1 == nodes
+                assert _pattern(hs, lo, hi, 0) == [(0, 1)]
+                assert _pattern(hs, lo, hi, K - 1) == [("T", "B"), ("B", "T")]
+            seen += 1
+    assert seen > 0
