@@ -1625,9 +1625,10 @@ __device__ __forceinline__ V ld(const V *p) {
 // own delta).  Three sections of whole warps: ELL pairs (|J_i| <= 2, four
 // variables per thread), ELL-4 quads (|J_i| = 3, 4), CSR groups (the rest and
 // every exchanged variable).  avg_kernel's thread 0 also resets the sweep's
-// tile counter.  (A slot-parallel variant of the ELL section -- every slot
-// gathering its partner's delta_bar, coalesced writes -- measured 1.5-2.3x
-// slower: the partner gathers lose the locality of the first slot.)
+// tile counter.  (Measured slower: a slot-parallel ELL section -- every slot
+// gathering its partner's delta_bar, coalesced writes -- 1.5-2.3x, the
+// partner gathers lose the locality of the first slot; consecutive instead of
+// strided variables per thread (FDOG_AVG_LOCAL=1) 1.1-1.4x.)
 // NC: delta_bar is read-only for the kernel's lifetime (the standalone kernel)
 // V: ELL variables per thread (tid, tid + N, ..., tid + (V-1) N: every load of
 // a warp stays coalesced, all 2V gathers in flight before the first use)
@@ -1642,7 +1643,7 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {
     int2 p[V];
 #pragma unroll
     for (int u = 0; u < V; ++u) {
-      const int q = tid + u * n_ell_thr;
+      const int q = a.ell_local ? tid * V + u : tid + u * n_ell_thr;
       p[u] = q < a.n_ell ? __ldg(a.ell + q) : make_int2(-1, -1);
     }
     T x[V], y[V];
@@ -1664,7 +1665,7 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {
     int4 p[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const int qq = q + u * n_ell4_thr;
+      const int qq = a.ell_local ? q * 2 + u : q + u * n_ell4_thr;
       p[u] = qq < a.n_ell4 ? __ldg(a.ell4 + qq) : make_int4(-1, -1, -1, -1);
     }
     T x[2][4];

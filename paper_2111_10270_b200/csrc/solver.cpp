@@ -71,7 +71,8 @@ struct fdog_solver {
   bool chunk_mode = false;   // ... or sweep_chunk_kernel (every tile an arc-mask tile)
   bool rc = false;           // recompute design (Plan::rc): no distance traffic, no dist_state
   bool dbar_zero = true;
-  int32_t ell_v = 4;         // averaging: ELL variables per thread (experiment knob FDOG_AVG_V)     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
+  int32_t ell_v = 4;         // averaging: ELL variables per thread (experiment knob FDOG_AVG_V)
+  int32_t ell_local = 0;     // averaging: consecutive variables per thread (experiment knob FDOG_AVG_LOCAL)     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
   // non-deferred variant (fdog_pass_seq): level schedule, built on first use
   bool seq_ready = false;
   std::vector<int64_t> seq_lvl[2];        // [backward, forward]: level boundaries in pass order
@@ -276,6 +277,7 @@ AvgArgs avg_args(fdog_solver *s) {
   a.ell4 = s->d_ell4;
   a.tile_counter = s->d_counter + 1;
   a.ell_v = s->ell_v;
+  a.ell_local = s->ell_local;
   a.n = s->n_varlist;
   a.group = s->csr_group;
   a.var_ptr = s->d_var_ptr;
@@ -635,6 +637,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->NB = P.NB;
   s->rc = P.rc;
   if (const char *av = getenv("FDOG_AVG_V")) s->ell_v = atoi(av);
+  if (const char *al = getenv("FDOG_AVG_LOCAL")) s->ell_local = atoi(al) ? 1 : 0;
   s->warp_bytes = (size_t)warp_bytes(P.SB, P.DB, P.NB);
   s->n_direct = P.direct_tiles;
   {
