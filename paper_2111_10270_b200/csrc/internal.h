@@ -302,6 +302,7 @@ int launch_primal(int precision, const PrimalArgs &a, void *stream);
 // top / bottom sentinel slots (0 / +inf) of every tile lane's distance column
 int launch_dist_sentinels(int precision, const TileDesc *tiles, int32_t n_tiles, void *dist, void *stream);
 // out[q] = src[canon[q]], q < n: per-slot state in canonical (j, h) order
-int launch_gather_canon(int precision, int64_t n, const int32_t *canon, const void *src, void *out, void *stream);
+int launch_gather_canon(int precision, int64_t n, const int32_t *canon, const void *src, void *out, int widen,
+                        void *stream);
 
 }  // namespace fdog

@@ -2250,20 +2250,25 @@ int launch_fused_small(int precision, bool rec, const SweepArgs &sa, const AvgAr
   return launch_pdl(f, dim3(1), dim3(1024), smem, stream, args);
 }
 
-template <typename T>
+template <typename T, typename O>
 __global__ void __launch_bounds__(256) gather_canon_kernel(int64_t n, const int32_t *__restrict__ canon,
-                                                          const T *__restrict__ src, T *__restrict__ out) {
+                                                          const T *__restrict__ src, O *__restrict__ out) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-    out[q] = src[canon[q]];
+    out[q] = (O)src[canon[q]];
 }
 
-int launch_gather_canon(int precision, int64_t n, const int32_t *canon, const void *src, void *out, void *stream) {
+// out: T per slot, or fp64 per slot (widen = 1)
+int launch_gather_canon(int precision, int64_t n, const int32_t *canon, const void *src, void *out, int widen,
+                        void *stream) {
   if (n <= 0) return 0;
   const int block = 256, grid = grid_for(n, block);
+  cudaStream_t st = (cudaStream_t)stream;
   if (precision == 64)
-    gather_canon_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, canon, (const double *)src, (double *)out);
+    gather_canon_kernel<double, double><<<grid, block, 0, st>>>(n, canon, (const double *)src, (double *)out);
+  else if (widen)
+    gather_canon_kernel<float, double><<<grid, block, 0, st>>>(n, canon, (const float *)src, (double *)out);
   else
-    gather_canon_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, canon, (const float *)src, (float *)out);
+    gather_canon_kernel<float, float><<<grid, block, 0, st>>>(n, canon, (const float *)src, (float *)out);
   return (int)cudaGetLastError();
 }
 
