@@ -62,11 +62,20 @@ def test_round_primal_random(oracle_mod):
     assert tried >= 20 and ok >= 0.9 * tried, (ok, tried)
 
 
-def test_round_primal_workloads(oracle_mod):
+@pytest.mark.parametrize("mode", ["", "rc", "tma"])
+def test_round_primal_workloads(oracle_mod, monkeypatch, mode):
+    """Every sweep design (default choice, recompute, TMA store) under the
+    rounding loop's snapshot / perturb / iterate / restore sequence."""
+    if mode:
+        monkeypatch.setenv("FDOG_SWEEP", mode)
     for p in (synth.gm_worms_like(14, n_src=40, k_cand=4, knn=4), synth.mrf_potts(14, H=6, W=7, L=3),
               synth.lap(synth.LAP4_LITERAL)):
         g = F.Solver(p, precision=32)
         g.iterate(30, 0.5)
         lb = g.lower_bound()
+        lam = g.lam()
         x, rounds, obj = g.round_primal(seed=1, max_rounds=200)
         assert _feasible(p, x) and obj >= lb - 1e-3 * max(1.0, abs(lb))
+        assert np.array_equal(g.lam(), lam) and g.lower_bound() == lb  # state restored
+        g.iterate(2, 0.5)  # and the solver continues from it
+        assert g.lower_bound() >= lb - 1e-5 * max(1.0, abs(lb))
