@@ -126,6 +126,10 @@ fdog_status fdog_plan_slot_map(const fdog_plan *plan, int64_t *dev_slot, int64_t
  * partitions K, lanes L, valid lanes, nodes per lane, first device slot);
  * *n = number of tiles; desc may be NULL to query *n; cap in tiles. */
 fdog_status fdog_plan_tiles(const fdog_plan *plan, int64_t *desc, int64_t cap, int64_t *n);
+/* 64-bit FNV-1a digest of every packed array and the device image (plans
+ * are deterministic: the same problem and options give the same digest for
+ * any host thread count). */
+fdog_status fdog_plan_digest(const fdog_plan *plan, uint64_t *out);
 /* Global row -> owning rank for every row (length n_cons). */
 fdog_status fdog_plan_owner(const fdog_plan *plan, int32_t *owner, int64_t len);
 /* Ascending global indices of the variables exchanged between ranks (held by

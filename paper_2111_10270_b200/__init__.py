@@ -64,7 +64,7 @@ class KernelTime(C.Structure):
 
 
 EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdog_plan_stats", "fdog_plan_slot_map",
-           "fdog_plan_tiles",
+           "fdog_plan_tiles", "fdog_plan_digest",
            "fdog_plan_bdd", "fdog_plan_owner", "fdog_plan_shared_vars", "fdog_create",
            "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_pass_seq", "fdog_iterate_seq",
            "fdog_lower_bound",
@@ -97,6 +97,7 @@ def load():
         "fdog_plan_owner": ([P, P, i64], C.c_int),
         "fdog_plan_slot_map": ([P, P, i64], C.c_int),
         "fdog_plan_tiles": ([P, P, i64, P], C.c_int),
+        "fdog_plan_digest": ([P, P], C.c_int),
         "fdog_plan_shared_vars": ([P, P, i64, P], C.c_int),
         "fdog_create": ([P, P, C.POINTER(P)], C.c_int),
         "fdog_create_from_plan": ([P, P, C.POINTER(P)], C.c_int),
@@ -229,6 +230,12 @@ class Plan:
         out = np.empty(max(n, 1), np.int64)
         _check(self._lib.fdog_plan_slot_map(self._h, _ptr(out), out.size), "fdog_plan_slot_map")
         return out[:n]
+
+    def digest(self) -> int:
+        """FNV-1a digest of the packed arrays and the device image."""
+        x = C.c_uint64()
+        _check(self._lib.fdog_plan_digest(self._h, C.byref(x)), "fdog_plan_digest")
+        return x.value
 
     def tiles(self):
         """Tile descriptors [n, 6]: kind bits, K, lanes, valid lanes, nodes per lane, first device slot."""

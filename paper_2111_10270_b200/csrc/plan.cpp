@@ -8,6 +8,7 @@
 //     DESIGN.md §5 (partition-contiguous per BDD, made tile-local),
 //     slot arrays, CSR variable -> slots (J_i).
 #include <algorithm>
+#include <array>
 #include <initializer_list>
 #include <atomic>
 #include <chrono>
@@ -301,6 +302,31 @@ static void append_recs(const Shape &S, int tsz, std::vector<unsigned char> &out
     memcpy(r + 8 * tsz, tail, 16);
   }
   out.resize((out.size() + 15) & ~(size_t)15, 0);
+}
+
+// ---- host parallelism of the packing phases.  Work over [0, n) is split into
+// a fixed number of contiguous chunks (par_chunks); every step below writes a
+// result that does not depend on the chunking, so plans are identical for
+// any thread count.
+static int par_chunks(int64_t n, int threads) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(threads, (n + (1 << 16) - 1) >> 16));
+}
+template <typename F>
+static void par_for(int64_t n, int threads, F f) {  // f(chunk, begin, end)
+  const int T = par_chunks(n, threads);
+  if (T == 1) {
+    f(0, (int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; ++t) pool.emplace_back([&f, t, T, n] { f(t, n * t / T, n * (t + 1) / T); });
+  f(0, (int64_t)0, n / T);
+  for (auto &th : pool) th.join();
+}
+static inline void atomic_min32(int32_t *p, int32_t v) {
+  int32_t cur = __atomic_load_n(p, __ATOMIC_RELAXED);
+  while (v < cur && !__atomic_compare_exchange_n(p, &cur, v, true, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+  }
 }
 
 // FDOG_PLAN_TRACE=1: per-phase wall times of build_plan on stderr
@@ -789,44 +815,101 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   P.canon_con.resize((size_t)P.n_slots);
   P.canon_pos.resize((size_t)P.n_slots);
   {
-    size_t q = 0;
-    for (int32_t j : P.local_rows) {
-      const int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
-      const int32_t *vars = P.col_var.data() + P.row_ptr[j];
-      for (int32_t h = 0; h < k; ++h, ++q) {
-        P.canon_slot[q] = row_slot[j] + (int64_t)h * row_L[j];
-        P.canon_con[q] = j;
-        P.canon_pos[q] = h;
-        cnt[vars[h]]++;
-      }
+    const int64_t nr = (int64_t)P.local_rows.size();
+    std::vector<int64_t> q0(nr + 1, 0);  // first canonical slot of each local row
+    for (int64_t r = 0; r < nr; ++r) {
+      const int32_t j = P.local_rows[r];
+      q0[r + 1] = q0[r] + (P.row_ptr[j + 1] - P.row_ptr[j]);
     }
+    par_for(nr, threads, [&](int, int64_t r0, int64_t r1) {
+      for (int64_t r = r0; r < r1; ++r) {
+        const int32_t j = P.local_rows[r];
+        const int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
+        const int32_t *vars = P.col_var.data() + P.row_ptr[j];
+        for (int32_t h = 0; h < k; ++h) {
+          const int64_t q = q0[r] + h;
+          P.canon_slot[q] = row_slot[j] + (int64_t)h * row_L[j];
+          P.canon_con[q] = j;
+          P.canon_pos[q] = h;
+          __atomic_fetch_add(&cnt[vars[h]], 1, __ATOMIC_RELAXED);
+        }
+      }
+    });
   }
   tm.mark("canonical slots + CSR");
   // variables in the order of their first device slot, so that neighbouring
   // averaging threads gather and scatter neighbouring slots (the tile layout
-  // puts consecutive rows of a shape in consecutive lanes)
-  // (one walk over the device slots in order: a variable is listed where it
-  // first occurs -- the order of a sort by first device slot, without the sort)
+  // puts consecutive rows of a shape in consecutive lanes): each variable's
+  // first device slot (atomic min), then the device slots that are a first
+  // occurrence, compacted in device-slot order -- the order of a sort by first
+  // device slot, without the sort
   P.var_list.clear();
   {
-    std::vector<char> seen(p->n_vars, 0);
-    for (int32_t i : P.slot_var)
-      if (i >= 0 && !seen[i]) {
-        seen[i] = 1;
-        P.var_list.push_back(i);
-      }
+    const int64_t ns = (int64_t)P.slot_var.size();
+    std::vector<int32_t> first(p->n_vars, INT32_MAX);  // (device slots < 2^31, checked above)
+    par_for(ns, threads, [&](int, int64_t a, int64_t b) {
+      for (int64_t d = a; d < b; ++d)
+        if (P.slot_var[d] >= 0) atomic_min32(&first[P.slot_var[d]], (int32_t)d);
+    });
+    const int T = par_chunks(ns, threads);
+    std::vector<int64_t> cc(T + 1, 0);
+    auto is_first = [&](int64_t d) { return P.slot_var[d] >= 0 && first[P.slot_var[d]] == d; };
+    par_for(ns, threads, [&](int c, int64_t a, int64_t b) {
+      int64_t m = 0;
+      for (int64_t d = a; d < b; ++d) m += is_first(d);
+      cc[c + 1] = m;
+    });
+    for (int c = 0; c < T; ++c) cc[c + 1] += cc[c];
+    P.var_list.resize(cc[T]);
+    par_for(ns, threads, [&](int c, int64_t a, int64_t b) {
+      int64_t o = cc[c];
+      for (int64_t d = a; d < b; ++d)
+        if (is_first(d)) P.var_list[o++] = P.slot_var[d];
+    });
   }
-  P.var_ptr.assign(1, 0);
+  // CSR over var_list: prefix of the local degrees
   std::vector<int64_t> where(p->n_vars, -1);
-  for (int32_t i : P.var_list) {
-    where[i] = P.var_ptr.back();
-    P.var_ptr.push_back(P.var_ptr.back() + cnt[i]);
+  {
+    const int64_t nv = (int64_t)P.var_list.size();
+    const int T = par_chunks(nv, threads);
+    std::vector<int64_t> cs(T + 1, 0);
+    par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
+      int64_t m = 0;
+      for (int64_t k = a; k < b; ++k) m += cnt[P.var_list[k]];
+      cs[c + 1] = m;
+    });
+    for (int c = 0; c < T; ++c) cs[c + 1] += cs[c];
+    P.var_ptr.resize(nv + 1);
+    P.var_ptr[nv] = cs[T];
+    par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
+      int64_t o = cs[c];
+      for (int64_t k = a; k < b; ++k) {
+        P.var_ptr[k] = o;
+        where[P.var_list[k]] = o;
+        o += cnt[P.var_list[k]];
+      }
+    });
   }
-  P.var_slots.assign(P.var_ptr.back(), -1);
-  for (size_t q = 0; q < P.canon_slot.size(); ++q) {
-    int32_t j = P.canon_con[q];
-    int32_t i = P.col_var[P.row_ptr[j] + P.canon_pos[q]];
-    P.var_slots[where[i]++] = (int32_t)P.canon_slot[q];
+  // fill: canonical slot indices claimed with an atomic cursor per variable,
+  // then each variable's (short) list sorted -- ascending canonical index is
+  // ascending j (A1) -- and mapped to device slots
+  {
+    const int64_t nq = (int64_t)P.canon_slot.size();
+    std::vector<int32_t> tq((size_t)std::max<int64_t>(nq, 1));
+    par_for(nq, threads, [&](int, int64_t a, int64_t b) {
+      for (int64_t q = a; q < b; ++q) {
+        const int32_t i = P.col_var[P.row_ptr[P.canon_con[q]] + P.canon_pos[q]];
+        tq[__atomic_fetch_add(&where[i], 1, __ATOMIC_RELAXED)] = (int32_t)q;
+      }
+    });
+    P.var_slots.assign(P.var_ptr.back(), -1);
+    par_for((int64_t)P.var_list.size(), threads, [&](int, int64_t a, int64_t b) {
+      for (int64_t k = a; k < b; ++k) {
+        const int64_t p0 = P.var_ptr[k], p1 = P.var_ptr[k + 1];
+        std::sort(tq.begin() + p0, tq.begin() + p1);
+        for (int64_t x = p0; x < p1; ++x) P.var_slots[x] = (int32_t)P.canon_slot[tq[x]];
+      }
+    });
   }
   tm.mark("variable order");
   // shared variables: held by this rank and by another one
@@ -851,31 +934,58 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   }
   tm.mark("shared variables");
   // averaging layout: variables with <= 2 local slots that are not exchanged
-  // keep their slot pair inline (ELL, one 8-byte load); the rest stay in CSR
+  // keep their slot pair inline (ELL, one 8-byte load), with 3-4 the slot quad
+  // (ELL-4); the rest stay in CSR.  (Per chunk counts, then the fill.)
   {
-    std::vector<int32_t> csr_list, csr_slots, csr_x;
-    std::vector<int64_t> csr_ptr(1, 0);
-    P.ell.clear();
-    P.ell_var.clear();
-    P.ell4.clear();
-    P.ell4_var.clear();
-    for (size_t q = 0; q < P.var_list.size(); ++q) {
-      const int64_t a = P.var_ptr[q], b = P.var_ptr[q + 1];
-      if (b - a <= 2 && P.var_xidx[q] < 0) {
-        P.ell.push_back(P.var_slots[a]);
-        P.ell.push_back(b - a == 2 ? P.var_slots[a + 1] : -1);
-        P.ell_var.push_back(P.var_list[q]);
-      } else if (b - a <= 4 && P.var_xidx[q] < 0) {
-        for (int64_t u = 0; u < 4; ++u) P.ell4.push_back(a + u < b ? P.var_slots[a + u] : -1);
-        P.ell4_var.push_back(P.var_list[q]);
-      } else {
-        csr_list.push_back(P.var_list[q]);
-        csr_x.push_back(P.var_xidx[q]);
-        for (int64_t p = a; p < b; ++p) csr_slots.push_back(P.var_slots[p]);
-        csr_ptr.push_back((int64_t)csr_slots.size());
+    const int64_t nv = (int64_t)P.var_list.size();
+    auto cat = [&](int64_t q) {
+      const int64_t d = P.var_ptr[q + 1] - P.var_ptr[q];
+      return P.var_xidx[q] >= 0 ? 2 : d <= 2 ? 0 : d <= 4 ? 1 : 2;
+    };
+    const int T = par_chunks(nv, threads);
+    std::vector<std::array<int64_t, 4>> cc(T + 1, {0, 0, 0, 0});  // ell, ell4, csr vars, csr slots
+    par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
+      std::array<int64_t, 4> m = {0, 0, 0, 0};
+      for (int64_t q = a; q < b; ++q) {
+        const int k = cat(q);
+        m[k]++;
+        if (k == 2) m[3] += P.var_ptr[q + 1] - P.var_ptr[q];
       }
-    }
-    P.n_vars_local = (int64_t)P.var_list.size();
+      cc[c + 1] = m;
+    });
+    for (int c = 0; c < T; ++c)
+      for (int u = 0; u < 4; ++u) cc[c + 1][u] += cc[c][u];
+    const auto &tot = cc[T];
+    P.ell.assign(2 * tot[0], -1);
+    P.ell_var.resize(tot[0]);
+    P.ell4.assign(4 * tot[1], -1);
+    P.ell4_var.resize(tot[1]);
+    std::vector<int32_t> csr_list(tot[2]), csr_slots(tot[3]), csr_x(tot[2]);
+    std::vector<int64_t> csr_ptr(tot[2] + 1, 0);
+    csr_ptr[tot[2]] = tot[3];
+    par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
+      std::array<int64_t, 4> o = cc[c];
+      for (int64_t q = a; q < b; ++q) {
+        const int64_t p0 = P.var_ptr[q], p1 = P.var_ptr[q + 1];
+        switch (cat(q)) {
+          case 0:
+            P.ell[2 * o[0]] = P.var_slots[p0];
+            if (p1 - p0 == 2) P.ell[2 * o[0] + 1] = P.var_slots[p0 + 1];
+            P.ell_var[o[0]++] = P.var_list[q];
+            break;
+          case 1:
+            for (int64_t u = 0; u < p1 - p0; ++u) P.ell4[4 * o[1] + u] = P.var_slots[p0 + u];
+            P.ell4_var[o[1]++] = P.var_list[q];
+            break;
+          default:
+            csr_list[o[2]] = P.var_list[q];
+            csr_x[o[2]] = P.var_xidx[q];
+            csr_ptr[o[2]++] = o[3];
+            for (int64_t x = p0; x < p1; ++x) csr_slots[o[3]++] = P.var_slots[x];
+        }
+      }
+    });
+    P.n_vars_local = nv;
     P.var_list.swap(csr_list);
     P.var_ptr.swap(csr_ptr);
     P.var_slots.swap(csr_slots);
@@ -1104,6 +1214,46 @@ fdog_status fdog_plan_slot_map(const fdog_plan *plan, int64_t *dev_slot, int64_t
     return FDOG_EINVAL;
   }
   std::copy(plan->p.canon_slot.begin(), plan->p.canon_slot.end(), dev_slot);
+  return FDOG_OK;
+}
+
+fdog_status fdog_plan_digest(const fdog_plan *plan, uint64_t *out) {
+  if (!plan || !out) {
+    set_error("bad argument");
+    return FDOG_EINVAL;
+  }
+  const Plan &P = plan->p;
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](const void *data, size_t bytes) {
+    const unsigned char *c = (const unsigned char *)data;
+    for (size_t q = 0; q < bytes; ++q) {
+      h ^= c[q];
+      h *= 1099511628211ull;
+    }
+  };
+  auto vec = [&](const auto &v) {
+    const uint64_t n = v.size();
+    mix(&n, 8);
+    if (n) mix(v.data(), n * sizeof(v[0]));
+  };
+  vec(P.tiles);
+  vec(P.hop_off);
+  vec(P.topo);
+  vec(P.recs);
+  vec(P.slot_var);
+  vec(P.canon_slot);
+  vec(P.var_list);
+  vec(P.var_ptr);
+  vec(P.var_slots);
+  vec(P.var_xidx);
+  vec(P.deg_list);
+  vec(P.ell);
+  vec(P.ell_var);
+  vec(P.ell4);
+  vec(P.ell4_var);
+  vec(P.shared_vars);
+  if (P.image.data) mix(P.image.data, P.image.bytes);
+  *out = h;
   return FDOG_OK;
 }
 

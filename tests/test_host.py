@@ -227,3 +227,19 @@ def test_hop_record_classes(name, make):
                 assert _pattern(hs, lo, hi, K - 1) == [("T", "B"), ("B", "T")]
             seen += 1
     assert seen > 0
+
+
+@pytest.mark.parametrize("name,make", [
+    ("gm", lambda: synth.gm_worms_like(5)),                 # 2.3 M slots: many 64 K chunks
+    ("mrf", lambda: synth.mrf_potts(5, H=60, W=80, L=8)),
+    ("ct", lambda: synth.celltrack(5, frames=30, dets=600)),
+    ("wide", lambda: synth.random_ilp(5, n=60, m=200, kmax=10, coef=4)),
+])
+def test_plan_deterministic_across_threads(name, make):
+    """The parallel packing phases (chunks of 64 K items) give byte-identical
+    plans -- every packed array and the device image -- for 1, 3 and 8 host
+    threads."""
+    p = make()
+    d = {t: F.Plan(p, precision=32, host_threads=t).digest() for t in (1, 3, 8)}
+    assert d[1] == d[3] == d[8]
+    assert F.Plan(p, precision=64, host_threads=1).digest() == F.Plan(p, precision=64, host_threads=8).digest()
