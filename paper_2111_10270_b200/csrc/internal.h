@@ -177,6 +177,7 @@ struct Plan {
 
   // per-warp shared-memory budget the tiles were packed for (precision-specific)
   int32_t precision = 32, SB = 0, DB = 0, NB = 2;
+  int32_t host_threads = 1;         // threads of the host packing phases
   bool rc = false;                  // recompute design: tiles packed for sweep_kernel<..., RC>
   int64_t n_dist = 0;               // elements of the distance array
   int64_t direct_tiles = 0;

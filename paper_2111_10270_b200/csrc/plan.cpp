@@ -42,6 +42,32 @@ void set_error(const char *fmt, ...) {
 
 const char *last_error() { return g_err.c_str(); }
 
+// ---- host parallelism of the packing phases.  Work over [0, n) is split into
+// a fixed number of contiguous chunks (par_chunks); every step below writes a
+// result that does not depend on the chunking, so plans are identical for
+// any thread count.
+static int par_chunks(int64_t n, int threads) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(threads, (n + (1 << 16) - 1) >> 16));
+}
+template <typename F>
+static void par_for(int64_t n, int threads, F f) {  // f(chunk, begin, end)
+  const int T = par_chunks(n, threads);
+  if (T == 1) {
+    f(0, (int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; ++t) pool.emplace_back([&f, t, T, n] { f(t, n * t / T, n * (t + 1) / T); });
+  f(0, (int64_t)0, n / T);
+  for (auto &th : pool) th.join();
+}
+static inline void atomic_min32(int32_t *p, int32_t v) {
+  int32_t cur = __atomic_load_n(p, __ATOMIC_RELAXED);
+  while (v < cur && !__atomic_compare_exchange_n(p, &cur, v, true, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+  }
+}
+
+
 // ---------------------------------------------------------------------------
 // Compiler B.
 //
@@ -156,7 +182,7 @@ static uint64_t signature_hash(int32_t k, const int32_t *a, int8_t rel, int64_t 
   return h;
 }
 
-static fdog_status validate(const fdog_problem *p) {
+static fdog_status validate(const fdog_problem *p, int threads) {
   if (!p || p->n_vars < 0 || p->n_cons < 0) {
     set_error("null problem or negative sizes");
     return FDOG_EINVAL;
@@ -169,7 +195,22 @@ static fdog_status validate(const fdog_problem *p) {
     set_error("row_ptr[0] must be 0");
     return FDOG_EINVAL;
   }
-  for (int32_t j = 0; j < p->n_cons; ++j) {
+  // parallel scan for the first bad row; the messages below come from it
+  int32_t first_bad = p->n_cons;
+  par_for(p->n_cons, threads, [&](int, int64_t j0, int64_t j1) {
+    for (int64_t j = j0; j < j1; ++j) {
+      const int64_t a = p->row_ptr[j], b = p->row_ptr[j + 1];
+      bool bad = b < a || b - a > 0x7fffffff || p->rel[j] < -1 || p->rel[j] > 1;
+      for (int64_t q = a; q < b && !bad; ++q)
+        bad = p->col_var[q] < 0 || p->col_var[q] >= p->n_vars || p->col_coef[q] == 0 ||
+              (q > a && p->col_var[q] <= p->col_var[q - 1]);
+      if (bad) {
+        atomic_min32(&first_bad, (int32_t)j);
+        return;
+      }
+    }
+  });
+  for (int32_t j = first_bad; j < p->n_cons; ++j) {
     int64_t a = p->row_ptr[j], b = p->row_ptr[j + 1];
     if (b < a || b - a > 0x7fffffff) {
       set_error("row %d: bad row_ptr", j);
@@ -304,31 +345,6 @@ static void append_recs(const Shape &S, int tsz, std::vector<unsigned char> &out
   out.resize((out.size() + 15) & ~(size_t)15, 0);
 }
 
-// ---- host parallelism of the packing phases.  Work over [0, n) is split into
-// a fixed number of contiguous chunks (par_chunks); every step below writes a
-// result that does not depend on the chunking, so plans are identical for
-// any thread count.
-static int par_chunks(int64_t n, int threads) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(threads, (n + (1 << 16) - 1) >> 16));
-}
-template <typename F>
-static void par_for(int64_t n, int threads, F f) {  // f(chunk, begin, end)
-  const int T = par_chunks(n, threads);
-  if (T == 1) {
-    f(0, (int64_t)0, n);
-    return;
-  }
-  std::vector<std::thread> pool;
-  for (int t = 1; t < T; ++t) pool.emplace_back([&f, t, T, n] { f(t, n * t / T, n * (t + 1) / T); });
-  f(0, (int64_t)0, n / T);
-  for (auto &th : pool) th.join();
-}
-static inline void atomic_min32(int32_t *p, int32_t v) {
-  int32_t cur = __atomic_load_n(p, __ATOMIC_RELAXED);
-  while (v < cur && !__atomic_compare_exchange_n(p, &cur, v, true, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
-  }
-}
-
 // FDOG_PLAN_TRACE=1: per-phase wall times of build_plan on stderr
 struct PhaseTimer {
   bool on = getenv("FDOG_PLAN_TRACE") != nullptr;
@@ -343,7 +359,9 @@ struct PhaseTimer {
 
 fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   PhaseTimer tm;
-  fdog_status st = validate(p);
+  int threads = o && o->host_threads > 0 ? o->host_threads : (int)std::thread::hardware_concurrency();
+  threads = std::max(1, std::min(threads, 64));
+  fdog_status st = validate(p, threads);
   if (st) return st;
   const int world = o ? std::max(1, o->world) : 1;
   const int rank = o ? o->rank : 0;
@@ -351,8 +369,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     set_error("rank %d outside [0, %d)", rank, world);
     return FDOG_EINVAL;
   }
-  int threads = o && o->host_threads > 0 ? o->host_threads : (int)std::thread::hardware_concurrency();
-  threads = std::max(1, std::min(threads, 64));
+  P.host_threads = threads;
 
   P.n_vars = p->n_vars;
   P.n_cons = p->n_cons;
@@ -364,8 +381,12 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   P.row_ptr.assign(p->row_ptr, p->row_ptr + p->n_cons + 1);
   if (p->n_cons == 0) P.row_ptr.assign(1, 0);
   const int64_t nnz = P.row_ptr.back();
-  P.col_var.assign(p->col_var, p->col_var + nnz);
-  P.col_coef.assign(p->col_coef, p->col_coef + nnz);
+  P.col_var.resize(nnz);
+  P.col_coef.resize(nnz);
+  par_for(nnz, threads, [&](int, int64_t a, int64_t b) {
+    memcpy(P.col_var.data() + a, p->col_var + a, (b - a) * sizeof(int32_t));
+    memcpy(P.col_coef.data() + a, p->col_coef + a, (b - a) * sizeof(int32_t));
+  });
   P.rel.assign(p->rel, p->rel + p->n_cons);
   P.rhs.assign(p->rhs, p->rhs + p->n_cons);
 
@@ -384,7 +405,9 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   shard_rows(p, world, P.owner);
   // global |J_i| and the free-variable term (A13)
   P.deg_global.assign(p->n_vars, 0);
-  for (int64_t q = 0; q < nnz; ++q) P.deg_global[p->col_var[q]]++;
+  par_for(nnz, threads, [&](int, int64_t a, int64_t b) {
+    for (int64_t q = a; q < b; ++q) __atomic_fetch_add(&P.deg_global[p->col_var[q]], 1, __ATOMIC_RELAXED);
+  });
   P.free_term = 0.0;
   for (int32_t i = 0; i < p->n_vars; ++i)
     if (P.deg_global[i] == 0 && P.cost[i] < 0) P.free_term += P.cost[i];
@@ -1044,10 +1067,14 @@ fdog_status build_image(Plan &P) {
   P.image.bytes = at;
   void *mem = nullptr;
   int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && cudaMallocHost(&mem, at) == cudaSuccess) {
+  // pinned memory makes the one host->device copy fast, but pinning costs
+  // more than it saves for multi-GB images (FDOG_PIN_MB: the limit, MB)
+  const char *pm = getenv("FDOG_PIN_MB");
+  const size_t pin_max = (size_t)(pm ? atoll(pm) : 256) << 20;
+  if (at <= pin_max && cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && cudaMallocHost(&mem, at) == cudaSuccess) {
     P.image.pinned = true;
   } else {
-    cudaGetLastError();  // no device (host-only use): pageable memory
+    cudaGetLastError();  // no device (host-only use) or a large image: pageable memory
     mem = malloc(at);
     if (!mem) {
       set_error("host out of memory (device image, %zu bytes)", at);
@@ -1055,36 +1082,47 @@ fdog_status build_image(Plan &P) {
     }
   }
   P.image.data = (unsigned char *)mem;
-  memset(P.image.data, 0, at);
-  auto put = [&](int q, const void *src) {
-    if (sz[q]) memcpy(P.image.data + P.image.off[q], src, sz[q]);
-  };
-  put(kImTiles, P.tiles.data());
-  put(kImHopOff, P.hop_off.data());
-  put(kImTopo, P.topo.data());
-  put(kImVarPtr, P.var_ptr.data());
-  put(kImVarSlots, P.var_slots.data());
-  put(kImVarXidx, P.var_xidx.data());
-  put(kImDegList, P.deg_list.data());
-  put(kImEll, P.ell.data());
-  put(kImEllVar, P.ell_var.data());
-  put(kImCsrVar, P.var_list.data());
-  put(kImEll4, P.ell4.data());
-  put(kImEll4Var, P.ell4_var.data());
-  put(kImXLocal, P.x_local.data());
-  put(kImXDeg, P.x_deg.data());
-  put(kImRecs, P.recs.data());
+  const int threads = P.host_threads;
+  // each section: its bytes, then zeros up to the next 256-byte boundary
+  const void *src[kImCount] = {};
+  src[kImTiles] = P.tiles.data();
+  src[kImHopOff] = P.hop_off.data();
+  src[kImTopo] = P.topo.data();
+  src[kImVarPtr] = P.var_ptr.data();
+  src[kImVarSlots] = P.var_slots.data();
+  src[kImVarXidx] = P.var_xidx.data();
+  src[kImDegList] = P.deg_list.data();
+  src[kImEll] = P.ell.data();
+  src[kImEllVar] = P.ell_var.data();
+  src[kImCsrVar] = P.var_list.data();
+  src[kImEll4] = P.ell4.data();
+  src[kImEll4Var] = P.ell4_var.data();
+  src[kImXLocal] = P.x_local.data();
+  src[kImXDeg] = P.x_deg.data();
+  src[kImRecs] = P.recs.data();
+  for (int q = 0; q < kImCount; ++q) {
+    const size_t end = q + 1 < kImCount ? P.image.off[q + 1] : at;
+    memset(P.image.data + P.image.off[q] + sz[q], 0, end - P.image.off[q] - sz[q]);
+    if (!src[q] || !sz[q]) continue;
+    unsigned char *dst = P.image.data + P.image.off[q];
+    const unsigned char *sp = (const unsigned char *)src[q];
+    par_for((int64_t)sz[q], threads, [&](int, int64_t a, int64_t b) { memcpy(dst + a, sp + a, b - a); });
+  }
   {
     int32_t *cs = (int32_t *)(P.image.data + P.image.off[kImCanon]);
-    for (size_t q = 0; q < P.canon_slot.size(); ++q) cs[q] = (int32_t)P.canon_slot[q];
+    par_for((int64_t)P.canon_slot.size(), threads, [&](int, int64_t a, int64_t b) {
+      for (int64_t q = a; q < b; ++q) cs[q] = (int32_t)P.canon_slot[q];
+    });
   }
   unsigned char *lam = P.image.data + P.image.off[kImLambda0];
-  for (size_t q = 0; q < P.slot_var.size(); ++q) {
-    const int32_t i = P.slot_var[q];
-    const double v = i >= 0 ? P.cost[i] / (double)P.deg_global[i] : 0.0;
-    if (tsz == 8) ((double *)lam)[q] = v;
-    else ((float *)lam)[q] = (float)v;
-  }
+  par_for((int64_t)P.slot_var.size(), threads, [&](int, int64_t a, int64_t b) {
+    for (int64_t q = a; q < b; ++q) {
+      const int32_t i = P.slot_var[q];
+      const double v = i >= 0 ? P.cost[i] / (double)P.deg_global[i] : 0.0;
+      if (tsz == 8) ((double *)lam)[q] = v;
+      else ((float *)lam)[q] = (float)v;
+    }
+  });
   tm.mark("device image");
   return FDOG_OK;
 }
