@@ -66,6 +66,9 @@ __device__ __forceinline__ T mm_difference(T m1, T m0, T clamp) {
 // may start while its predecessor drains; it waits here before reading the
 // predecessor's outputs (or touching the tile counter it resets).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// (An early griddepcontrol.launch_dependents at the end of each sweep warp's
+// tile loop was measured: no gain on GM / CellTrack / QAP50, MRF sweeps 15 %
+// slower -- the dependent grid's resident CTAs get in the sweep's way.)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
