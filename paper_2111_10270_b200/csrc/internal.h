@@ -190,6 +190,11 @@ struct Plan {
   int32_t max_hops = 0, max_width = 0, max_tile_nodes = 0;
 };
 
+// compiler B on the GPU (compile_gpu.cu): every shape's k, coef, rel, rhs in,
+// hop_start / lo / hi / max_w out -- identical to the host compiler;
+// FDOG_ETOOBIG when a shape exceeds the GPU scratch bound (compile on the host)
+fdog_status gpu_compile_shapes(std::vector<Shape> &shapes, int device);
+
 // host-side helpers implemented in plan.cpp
 void set_error(const char *fmt, ...);
 fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &plan);

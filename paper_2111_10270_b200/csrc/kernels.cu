@@ -182,7 +182,7 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
       m1g[h * L] = m1;
     }
   };
-  if (MODE == kEnergy) {
+  if constexpr (MODE == kEnergy) {
     // shp(v, T) for all nodes under the current lambda
 #pragma unroll 1
     for (int h = K - 1; h >= 0; --h) {
@@ -196,7 +196,7 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
     }
     return valid ? (double)D[0] : 0.0;  // E^j = shp(r, T)
   }
-  if (MODE == kCfr) {
+  if constexpr (MODE == kCfr) {
     // shp(r, v) for all nodes under the current lambda, relaxed
     // through the R buffers (no writes into the sentinels)
     T *cur = R, *nlo = R + (rw + 1) * L, *nhi = R + 2 * (rw + 1) * L;
@@ -229,7 +229,7 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
     }
     return acc;
   }
-  if (MODE == kForward) {
+  if constexpr (MODE == kForward) {
     // forward pass with updates (Alg. forward_pass_mm): D holds
     // shp(v, T) from the previous pass, valid for P_{h+1} at hop h;
     // R holds shp(r, .) of P_h (cur) and the 0-/1-arc relaxations into P_{h+1}
@@ -275,34 +275,36 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
     }
     return acc;
   }
-  // MODE == kBackward (Alg. backward_pass_mm): D holds shp(r, v)
-  // from the forward pass, valid for P_h at hop h; shp(v, T) of P_{h+1} was
-  // written into D by the previous hop of this pass.
+  if constexpr (MODE == kBackward) {
+    // MODE == kBackward (Alg. backward_pass_mm): D holds shp(r, v)
+    // from the forward pass, valid for P_h at hop h; shp(v, T) of P_{h+1} was
+    // written into D by the previous hop of this pass.
 #pragma unroll 1
-  for (int h = K - 1; h >= 0; --h) {
-    const int n0 = ho[h], n1 = ho[h + 1];
-    T m0 = inf, m1r = inf;
+    for (int h = K - 1; h >= 0; --h) {
+      const int n0 = ho[h], n1 = ho[h + 1];
+      T m0 = inf, m1r = inf;
 #pragma unroll 1
-    for (int n = n0; n < n1; ++n) {
-      const uint32_t e = tp[n * ts];
-      const T cf = D[n * L];
-      m0 = fmin(m0, cf + D[(e & 0xFFFFu) * L]);
-      m1r = fmin(m1r, cf + D[(e >> 16) * L]);
+      for (int n = n0; n < n1; ++n) {
+        const uint32_t e = tp[n * ts];
+        const T cf = D[n * L];
+        m0 = fmin(m0, cf + D[(e & 0xFFFFu) * L]);
+        m1r = fmin(m1r, cf + D[(e >> 16) * L]);
+      }
+      const T l = lam[h * L];
+      const T m1 = l + m1r;
+      const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+      const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
+      emit(h, lam_new, delta, m0, m1);
+      if (valid) acc += (double)fmin(delta, T(0));
+      // shp(v, T), v in P_h, with the updated lambda_h
+#pragma unroll 1
+      for (int n = n0; n < n1; ++n) {
+        const uint32_t e = tp[n * ts];
+        D[n * L] = fmin(D[(e & 0xFFFFu) * L], lam_new + D[(e >> 16) * L]);
+      }
     }
-    const T l = lam[h * L];
-    const T m1 = l + m1r;
-    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
-    const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
-    emit(h, lam_new, delta, m0, m1);
-    if (valid) acc += (double)fmin(delta, T(0));
-    // shp(v, T), v in P_h, with the updated lambda_h
-#pragma unroll 1
-    for (int n = n0; n < n1; ++n) {
-      const uint32_t e = tp[n * ts];
-      D[n * L] = fmin(D[(e & 0xFFFFu) * L], lam_new + D[(e >> 16) * L]);
-    }
+    if (valid) acc += (double)D[0];  // E^j = shp(r, T)
   }
-  if (valid) acc += (double)D[0];  // E^j = shp(r, T)
   return acc;
 }
 
@@ -337,7 +339,7 @@ __device__ __forceinline__ double process_bdd_w2(const int K, const int32_t *ho,
     }
     return lam_new;
   };
-  if (MODE == kForward) {
+  if constexpr (MODE == kForward) {
     T c0 = T(0), c1 = inf;  // shp(r, .) of the (up to) two nodes of P_h
     int n0 = ho[0];
 #pragma unroll 1
@@ -382,29 +384,31 @@ __device__ __forceinline__ double process_bdd_w2(const int K, const int32_t *ho,
     }
     return acc;
   }
-  // kBackward
+  if constexpr (MODE == kBackward) {
+    // kBackward
 #pragma unroll 1
-  for (int h = K - 1; h >= 0; --h) {
-    const int n0 = ho[h], n1 = ho[h + 1];
-    const uint32_t e0 = tp[n0 * ts];
-    const T f0 = D[n0 * L];
-    const T a0 = D[(e0 & 0xFFFFu) * L], b0 = D[(e0 >> 16) * L];
-    T m0 = f0 + a0, m1r = f0 + b0;
-    T a1 = inf, b1 = inf;
-    const bool two = n1 - n0 > 1;
-    if (two) {
-      const uint32_t e1 = tp[(n0 + 1) * ts];
-      const T f1 = D[(n0 + 1) * L];
-      a1 = D[(e1 & 0xFFFFu) * L];
-      b1 = D[(e1 >> 16) * L];
-      m0 = fmin(m0, f1 + a1);
-      m1r = fmin(m1r, f1 + b1);
+    for (int h = K - 1; h >= 0; --h) {
+      const int n0 = ho[h], n1 = ho[h + 1];
+      const uint32_t e0 = tp[n0 * ts];
+      const T f0 = D[n0 * L];
+      const T a0 = D[(e0 & 0xFFFFu) * L], b0 = D[(e0 >> 16) * L];
+      T m0 = f0 + a0, m1r = f0 + b0;
+      T a1 = inf, b1 = inf;
+      const bool two = n1 - n0 > 1;
+      if (two) {
+        const uint32_t e1 = tp[(n0 + 1) * ts];
+        const T f1 = D[(n0 + 1) * L];
+        a1 = D[(e1 & 0xFFFFu) * L];
+        b1 = D[(e1 >> 16) * L];
+        m0 = fmin(m0, f1 + a1);
+        m1r = fmin(m1r, f1 + b1);
+      }
+      const T lam_new = finish(h, lam[h * L], m0, m1r);
+      D[n0 * L] = fmin(a0, lam_new + b0);  // shp(v, T) with the updated lambda_h
+      if (two) D[(n0 + 1) * L] = fmin(a1, lam_new + b1);
     }
-    const T lam_new = finish(h, lam[h * L], m0, m1r);
-    D[n0 * L] = fmin(a0, lam_new + b0);  // shp(v, T) with the updated lambda_h
-    if (two) D[(n0 + 1) * L] = fmin(a1, lam_new + b1);
+    if (valid) acc += (double)D[0];  // E^j = shp(r, T)
   }
-  if (valid) acc += (double)D[0];  // E^j = shp(r, T)
   return acc;
 }
 
@@ -452,7 +456,7 @@ __device__ __forceinline__ double process_rc_w2(const int K, const int top, cons
     }
     return lam_new;
   };
-  if (MODE == kForward) {
+  if constexpr (MODE == kForward) {
     {  // phase 1: shp(v, T) for every node under the current lambda
       T x0 = inf, x1 = inf;  // shp(., T) of P_{h+1}
 #pragma unroll 1

@@ -446,7 +446,26 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     }
     P.row_shape[j] = id;
   }
-  {
+  // FDOG_GPU_COMPILE=1: compile the distinct shapes on the GPU (compile_gpu.cu,
+  // identical results); falls back to the host compiler when a shape's
+  // suffix-sum sets may exceed the GPU scratch bound or no device is present
+  bool compiled = false;
+  if (const char *gc = getenv("FDOG_GPU_COMPILE"); gc && gc[0] == '1') {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+      const int dev = o ? o->device : 0;
+      const fdog_status r = gpu_compile_shapes(P.shapes, dev >= 0 && dev < ndev ? dev : 0);
+      if (r == FDOG_EINFEASIBLE) {
+        set_error("a constraint has an empty feasible set");
+        return r;
+      }
+      if (r == FDOG_ECUDA) return r;
+      compiled = r == FDOG_OK;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  if (!compiled) {
     std::atomic<int64_t> next{0};
     std::atomic<int> bad{0};
     std::mutex mu;
