@@ -206,6 +206,10 @@ fdog_status fdog_min_marginals(fdog_solver *s, double *m0, double *m1, int64_t l
 /* Overwrite (lambda, delta_bar) -- checkpoint/resume; either may be NULL. */
 fdog_status fdog_set_state(fdog_solver *s, const double *lambda, const double *delta, int64_t len);
 fdog_status fdog_stats(const fdog_solver *s, fdog_stats_t *out);
+/* Debug (solver created with FDOG_TRACE=1): per warp of the TMA-staged sweep,
+ * {start, end (globaltimer ns), tiles processed, SM id} of the last sweep;
+ * *n = warps (0 without tracing); cap in warps. */
+fdog_status fdog_debug_trace(fdog_solver *s, uint64_t *out, int64_t cap, int64_t *n);
 
 /* Per-kernel device time (opts.profile = 1): names[i] (static strings),
  * total milliseconds and launch counts since the last reset.  Synchronises. */

@@ -64,7 +64,7 @@ class KernelTime(C.Structure):
 
 
 EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdog_plan_stats", "fdog_plan_slot_map",
-           "fdog_plan_tiles", "fdog_plan_digest",
+           "fdog_plan_tiles", "fdog_plan_digest", "fdog_debug_trace",
            "fdog_plan_bdd", "fdog_plan_owner", "fdog_plan_shared_vars", "fdog_create",
            "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_pass_seq", "fdog_iterate_seq",
            "fdog_lower_bound",
@@ -98,6 +98,7 @@ def load():
         "fdog_plan_slot_map": ([P, P, i64], C.c_int),
         "fdog_plan_tiles": ([P, P, i64, P], C.c_int),
         "fdog_plan_digest": ([P, P], C.c_int),
+        "fdog_debug_trace": ([P, P, i64, P], C.c_int),
         "fdog_plan_shared_vars": ([P, P, i64, P], C.c_int),
         "fdog_create": ([P, P, C.POINTER(P)], C.c_int),
         "fdog_create_from_plan": ([P, P, C.POINTER(P)], C.c_int),
@@ -292,6 +293,14 @@ class Solver:
 
     def pass_(self, forward: bool, omega: float = 0.5):
         _check(self._lib.fdog_pass(self._h, 1 if forward else 0, float(omega)), "fdog_pass")
+
+    def debug_trace(self):
+        """[warps, 4]: start / end (ns), tiles, SM of the last TMA-staged sweep (FDOG_TRACE=1)."""
+        n = C.c_int64()
+        _check(self._lib.fdog_debug_trace(self._h, None, 0, C.byref(n)), "fdog_debug_trace")
+        out = np.zeros((max(n.value, 1), 4), np.uint64)
+        _check(self._lib.fdog_debug_trace(self._h, _ptr(out), n.value, C.byref(n)), "fdog_debug_trace")
+        return out[:n.value]
 
     def pass_seq(self, forward: bool, omega: float = 0.5):
         """Non-deferred (sequential) min-marginal averaging pass."""

@@ -1010,6 +1010,9 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   if (t < a.n_tiles) fetch_desc(&ring[0], a.tiles + t, lane);
   if (tn < a.n_tiles) fetch_desc(&ring[1], a.tiles + tn, lane);
   pdl_wait();
+  unsigned long long t_start = 0;
+  int n_done = 0;
+  if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   auto claim_issue = [&]() -> int { return lane == 0 ? (int)atomicAdd(a.tile_counter, 1u) : 0; };
   auto claim_get = [&](int raw) -> int { return 2 * W + __shfl_sync(0xffffffffu, raw, 0); };
   // pipeline per warp: while tile t is processed, the TMA stage loads of the
@@ -1178,6 +1181,18 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
     tn = tnn;
     rc = rc == 2 ? 0 : rc + 1;
     b = bn;
+    ++n_done;
+  }
+  if (a.trace && lane == 0) {
+    unsigned long long t_end, smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(*reinterpret_cast<unsigned *>(&smid)));
+    smid &= 0xffffffffull;
+    unsigned long long *o = a.trace + 4 * (size_t)gwarp;
+    o[0] = t_start;
+    o[1] = t_end;
+    o[2] = (unsigned long long)n_done;
+    o[3] = smid;
   }
   if (lane == 0) bulk_wait_read_all();  // shared memory must outlive the TMA stores' reads
   __syncwarp();

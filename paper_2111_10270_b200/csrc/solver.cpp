@@ -134,6 +134,7 @@ struct fdog_solver {
   int dist_state = 0;  // 0: distances hold shp(v, T); 1: shp(r, v)
   int64_t n_direct = 0, scratch_stride = 0;
   void *d_scratch = nullptr;
+  unsigned long long *d_trace = nullptr;  // FDOG_TRACE=1: per-warp sweep timeline of the last sweep
 
   // one captured iteration (avg, forward, avg, backward), keyed by omega and
   // the parity of the delta buffers; replayed by fdog_iterate
@@ -251,6 +252,7 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.NB = s->NB;
   a.dist = s->d_dist;
   a.static_sched = s->static_sched;
+  a.trace = s->d_trace;
   a.scratch = s->d_scratch;  // relaxation buffers of direct (unstaged) tiles
   a.scratch_stride = s->scratch_stride;
   return a;
@@ -699,6 +701,10 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     const int64_t warps_total = (int64_t)s->grid * warps;
     if (sc && (sc[0] == 's' || sc[0] == 'd')) s->static_sched = sc[0] == 's';
     else s->static_sched = s->n_tiles <= (s->rc ? 1 : 4) * warps_total;
+    // (A balanced static grid -- every warp exactly ceil(tiles / warps) tiles --
+    // was measured on QAP50: 6 % slower.  Warps' finish times spread over 2x
+    // either way: a grid that is not a multiple of the SM count leaves SMs
+    // with different warp counts, i.e. different per-tile times.)
   }
   s->scratch_stride = (int64_t)relax_slots(s->max_w) * 32;
 
@@ -779,6 +785,12 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_x = (uint8_t *)(r + o_x);
   s->d_undecided = (unsigned long long *)(r + o_und);
   s->d_canon_out = r + o_canon;
+  if (const char *tr = getenv("FDOG_TRACE"); tr && tr[0] == '1') {
+    void *p = nullptr;
+    CK(cudaMalloc(&p, (size_t)s->grid * (s->block / 32) * 4 * 8), "cudaMalloc (trace)");
+    s->allocs.push_back(p);
+    s->d_trace = (unsigned long long *)p;
+  }
   s->d_dist = r + o_dist;
   {
     // the distances' sentinels (top 0, bottom +inf) of every tile lane
@@ -1440,6 +1452,22 @@ fdog_status fdog_set_state(fdog_solver *s, const double *lambda, const double *d
     s->dbar_zero = z;
   }
   return energy(s);
+}
+
+fdog_status fdog_debug_trace(fdog_solver *s, uint64_t *out, int64_t cap, int64_t *n) {
+  if (!s || !n) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  *n = s->d_trace ? (int64_t)s->grid * (s->block / 32) : 0;
+  if (!out || !s->d_trace) return FDOG_OK;
+  if (cap < *n) {
+    set_error("capacity %lld < %lld warps", (long long)cap, (long long)*n);
+    return FDOG_EINVAL;
+  }
+  CK(cudaMemcpyAsync(out, s->d_trace, (size_t)*n * 32, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  return FDOG_OK;
 }
 
 fdog_status fdog_stats(const fdog_solver *s, fdog_stats_t *out) {
