@@ -243,6 +243,7 @@ struct AvgArgs {
   unsigned int *tile_counter;  // sweep scheduler counter, reset here for the next sweep
   int32_t ell_v;             // ELL variables per thread (1, 2, 4 or 8; the fused path uses 4)
   int32_t ell_local;         // 1: a thread's ELL variables are consecutive (else strided by the thread count)
+  int32_t csr_first;         // 1: the CSR section takes the first threads (else the last)
 };
 
 struct PrimalArgs {

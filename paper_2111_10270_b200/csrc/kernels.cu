@@ -1654,10 +1654,73 @@ __device__ __forceinline__ V ld(const V *p) {
 // NC: delta_bar is read-only for the kernel's lifetime (the standalone kernel)
 // V: ELL variables per thread (tid, tid + N, ..., tid + (V-1) N: every load of
 // a warp stays coalesced, all 2V gathers in flight before the first use)
-template <typename T, bool NC, int V = 4>
-__device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {
+// CSR part: a group of G lanes per variable (gt = thread index inside the part);
+// lane j sums slots j, j+G, ... in order, then a fixed-shape shuffle tree
+// combines the lanes (deterministic)
+template <typename T, bool NC>
+__device__ __forceinline__ void avg_csr(const AvgArgs &a, const int gt) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
+  const int G = a.group;
+  const int q = gt / G, j = gt % G;
+  const bool on = q < a.n;
+  T *__restrict__ xbuf = reinterpret_cast<T *>(a.xbuf);
+  int64_t p0 = 0, p1 = 0;
+  if (on) {
+    p0 = __ldg(a.var_ptr + q);
+    p1 = __ldg(a.var_ptr + q + 1);
+  }
+  // lane j sums slots p0 + j, p0 + j + G, ... in ascending order; four at a
+  // time, all index loads and then all gathers issued before the adds (two
+  // dependent memory round trips per four slots instead of two per slot)
+  T s = T(0);
+  for (int64_t base = p0 + j; base < p1; base += 4 * (int64_t)G) {
+    int32_t q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t p = base + (int64_t)u * G;
+      q[u] = p < p1 ? __ldg(a.var_slots + p) : -1;
+    }
+    T v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = q[u] >= 0 ? ld<NC>(db + q[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (q[u] >= 0) s += v[u];
+  }
+  // the group is G consecutive lanes of one warp (G divides 32, the CSR part
+  // starts at a multiple of 32 threads: the sections are rounded up)
+  for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+  if (!on) return;
+  const int x = a.var_xidx ? __ldg(a.var_xidx + q) : -1;
+  if (x >= 0) {
+    if (j == 0) xbuf[x] = s;
+    return;
+  }
+  const T v = s / T(__ldg(a.deg_l + q));
+  for (int64_t p = p0 + j; p < p1; p += G) out[__ldg(a.var_slots + p)] = v;
+}
+
+// threads of the CSR part (whole warps)
+__host__ __device__ __forceinline__ int64_t avg_csr_threads(const AvgArgs &a) {
+  return ((int64_t)a.n * a.group + 31) & ~(int64_t)31;
+}
+
+template <typename T, bool NC, int V = 4>
+__device__ __forceinline__ void avg_body(const AvgArgs &a, int tid) {
+  const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
+  T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
+  // csr_first: the CSR part (the longest dependent chains: offsets, slots,
+  // gathers, shuffle tree, slots again, stores) takes the lowest block
+  // indices, so it is dispatched in the first wave instead of forming the tail
+  if (a.csr_first) {
+    const int64_t nc = avg_csr_threads(a);
+    if (tid < nc) {
+      avg_csr<T, NC>(a, tid);
+      return;
+    }
+    tid -= (int)nc;
+  }
   // ELL part: four variables per thread (tid, tid + N, tid + 2N, tid + 3N, so
   // every load of a warp stays coalesced), all eight gathers issued before use
   const int n_ell_thr = (((a.n_ell + V - 1) / V) + 31) & ~31;  // whole warps
@@ -1712,47 +1775,8 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, const int tid) {
     }
     return;
   }
-  // CSR part: a group of G lanes per variable; lane j sums slots j, j+G, ...
-  // in order, then a fixed-shape shuffle tree combines the lanes (deterministic)
-  const int G = a.group;
-  const int gt = tid - n_ell_thr - n_ell4_thr;
-  const int q = gt / G, j = gt % G;
-  const bool on = q < a.n;
-  T *__restrict__ xbuf = reinterpret_cast<T *>(a.xbuf);
-  int64_t p0 = 0, p1 = 0;
-  if (on) {
-    p0 = __ldg(a.var_ptr + q);
-    p1 = __ldg(a.var_ptr + q + 1);
-  }
-  // lane j sums slots p0 + j, p0 + j + G, ... in ascending order; four at a
-  // time, all index loads and then all gathers issued before the adds (two
-  // dependent memory round trips per four slots instead of two per slot)
-  T s = T(0);
-  for (int64_t base = p0 + j; base < p1; base += 4 * (int64_t)G) {
-    int32_t q[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t p = base + (int64_t)u * G;
-      q[u] = p < p1 ? __ldg(a.var_slots + p) : -1;
-    }
-    T v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = q[u] >= 0 ? ld<NC>(db + q[u]) : T(0);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (q[u] >= 0) s += v[u];
-  }
-  // the group is G consecutive lanes of one warp (G divides 32, threads of
-  // the CSR part start at a multiple of 32: n_ell_thr is rounded up)
-  for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-  if (!on) return;
-  const int x = a.var_xidx ? __ldg(a.var_xidx + q) : -1;
-  if (x >= 0) {
-    if (j == 0) xbuf[x] = s;
-    return;
-  }
-  const T v = s / T(__ldg(a.deg_l + q));
-  for (int64_t p = p0 + j; p < p1; p += G) out[__ldg(a.var_slots + p)] = v;
+  if (a.csr_first) return;  // (past the last section: padding threads)
+  avg_csr<T, NC>(a, tid - n_ell_thr - n_ell4_thr);
 }
 
 template <typename T>
@@ -1770,7 +1794,7 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
 __host__ __device__ __forceinline__ int64_t avg_threads(const AvgArgs &a) {
   const int v = (a.ell_v == 8 || a.ell_v == 2 || a.ell_v == 1) ? a.ell_v : 4;
   return (int64_t)((((a.n_ell + v - 1) / v) + 31) & ~31) + (int64_t)((((a.n_ell4 + 1) >> 1) + 31) & ~31) +
-         (int64_t)a.n * a.group;
+         avg_csr_threads(a);
 }
 
 // ---------------------------------------------------------------------------

@@ -73,6 +73,7 @@ struct fdog_solver {
   bool dbar_zero = true;
   int32_t ell_v = 4;         // averaging: ELL variables per thread (experiment knob FDOG_AVG_V)
   int32_t ell_local = 0;     // averaging: consecutive variables per thread (experiment knob FDOG_AVG_LOCAL)
+  int32_t csr_first = 1;     // averaging: CSR section in the first blocks (experiment knob FDOG_AVG_CSR_FIRST)
   bool get_direct = true;    // getters: widen to fp64 on the device, one D2H (FDOG_GET_DIRECT=0: host widening)     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
   // non-deferred variant (fdog_pass_seq): level schedule, built on first use
   bool seq_ready = false;
@@ -281,6 +282,7 @@ AvgArgs avg_args(fdog_solver *s) {
   a.tile_counter = s->d_counter + 1;
   a.ell_v = s->ell_v;
   a.ell_local = s->ell_local;
+  a.csr_first = s->csr_first;
   a.n = s->n_varlist;
   a.group = s->csr_group;
   a.var_ptr = s->d_var_ptr;
@@ -642,6 +644,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->rc = P.rc;
   if (const char *av = getenv("FDOG_AVG_V")) s->ell_v = atoi(av);
   if (const char *al = getenv("FDOG_AVG_LOCAL")) s->ell_local = atoi(al) ? 1 : 0;
+  if (const char *cf = getenv("FDOG_AVG_CSR_FIRST")) s->csr_first = atoi(cf) ? 1 : 0;
   if (const char *gd = getenv("FDOG_GET_DIRECT")) s->get_direct = gd[0] == '1';
   s->warp_bytes = (size_t)warp_bytes(P.SB, P.DB, P.NB);
   s->n_direct = P.direct_tiles;
