@@ -67,8 +67,9 @@ __device__ __forceinline__ T mm_difference(T m1, T m0, T clamp) {
 // predecessor's outputs (or touching the tile counter it resets).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // (An early griddepcontrol.launch_dependents at the end of each sweep warp's
-// tile loop was measured: no gain on GM / CellTrack / QAP50, MRF sweeps 15 %
-// slower -- the dependent grid's resident CTAs get in the sweep's way.)
+// tile loop (SweepArgs::pdl_early) only pays with few tiles per warp, where the
+// averaging grid's CTAs prefetch their slot indices during the sweep's tail;
+// with many (MRF) the dependent CTAs get in the sweep's way: 15 % slower.)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -1183,6 +1184,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
     b = bn;
     ++n_done;
   }
+  if (a.pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.trace && lane == 0) {
     unsigned long long t_end, smid;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -1657,7 +1659,7 @@ __device__ __forceinline__ V ld(const V *p) {
 // CSR part: a group of G lanes per variable (gt = thread index inside the part);
 // lane j sums slots j, j+G, ... in order, then a fixed-shape shuffle tree
 // combines the lanes (deterministic)
-template <typename T, bool NC>
+template <typename T, bool NC, bool PRE = false>
 __device__ __forceinline__ void avg_csr(const AvgArgs &a, const int gt) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
@@ -1670,6 +1672,7 @@ __device__ __forceinline__ void avg_csr(const AvgArgs &a, const int gt) {
     p0 = __ldg(a.var_ptr + q);
     p1 = __ldg(a.var_ptr + q + 1);
   }
+  if (PRE) pdl_wait();
   // lane j sums slots p0 + j, p0 + j + G, ... in ascending order; four at a
   // time, all index loads and then all gathers issued before the adds (two
   // dependent memory round trips per four slots instead of two per slot)
@@ -1706,7 +1709,10 @@ __host__ __device__ __forceinline__ int64_t avg_csr_threads(const AvgArgs &a) {
   return ((int64_t)a.n * a.group + 31) & ~(int64_t)31;
 }
 
-template <typename T, bool NC, int V = 4>
+// PRE: the standalone kernel launched behind a sweep (PDL): the constant index
+// loads of a thread are issued before griddepcontrol.wait, the gathers of
+// delta_bar after it
+template <typename T, bool NC, int V = 4, bool PRE = false>
 __device__ __forceinline__ void avg_body(const AvgArgs &a, int tid) {
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
@@ -1716,7 +1722,7 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, int tid) {
   if (a.csr_first) {
     const int64_t nc = avg_csr_threads(a);
     if (tid < nc) {
-      avg_csr<T, NC>(a, tid);
+      avg_csr<T, NC, PRE>(a, tid);
       return;
     }
     tid -= (int)nc;
@@ -1731,6 +1737,7 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, int tid) {
       const int q = a.ell_local ? tid * V + u : tid + u * n_ell_thr;
       p[u] = q < a.n_ell ? __ldg(a.ell + q) : make_int2(-1, -1);
     }
+    if (PRE) pdl_wait();
     T x[V], y[V];
 #pragma unroll
     for (int u = 0; u < V; ++u) {
@@ -1753,6 +1760,7 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, int tid) {
       const int qq = a.ell_local ? q * 2 + u : q + u * n_ell4_thr;
       p[u] = qq < a.n_ell4 ? __ldg(a.ell4 + qq) : make_int4(-1, -1, -1, -1);
     }
+    if (PRE) pdl_wait();
     T x[2][4];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -1776,18 +1784,20 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, int tid) {
     return;
   }
   if (a.csr_first) return;  // (past the last section: padding threads)
-  avg_csr<T, NC>(a, tid - n_ell_thr - n_ell4_thr);
+  avg_csr<T, NC, PRE>(a, tid - n_ell_thr - n_ell4_thr);
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  pdl_wait();
-  if (tid == 0) *a.tile_counter = 0u;
-  if (a.ell_v == 8) avg_body<T, true, 8>(a, tid);
-  else if (a.ell_v == 2) avg_body<T, true, 2>(a, tid);
-  else if (a.ell_v == 1) avg_body<T, true, 1>(a, tid);
-  else avg_body<T, true, 4>(a, tid);
+  if (tid == 0) {
+    pdl_wait();  // the sweep before has finished with the counter
+    *a.tile_counter = 0u;
+  }
+  if (a.ell_v == 8) avg_body<T, true, 8, true>(a, tid);
+  else if (a.ell_v == 2) avg_body<T, true, 2, true>(a, tid);
+  else if (a.ell_v == 1) avg_body<T, true, 1, true>(a, tid);
+  else avg_body<T, true, 4, true>(a, tid);
 }
 
 // threads the averaging needs (whole warps per section)

@@ -83,6 +83,7 @@ struct fdog_solver {
   int32_t *d_slot_tile = nullptr;
   double *d_e_lane = nullptr;
   int32_t static_sched = 0;  // TMA sweep: round-robin tiles only
+  int32_t pdl_early = 0;     // sweep warps release the averaging grid when their tiles are done
 
   // host copies needed by getters
   // host-side data shared with the plan (no copy; kept alive by the solver)
@@ -253,6 +254,7 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.NB = s->NB;
   a.dist = s->d_dist;
   a.static_sched = s->static_sched;
+  a.pdl_early = s->pdl_early;
   a.trace = s->d_trace;
   a.scratch = s->d_scratch;  // relaxation buffers of direct (unstaged) tiles
   a.scratch_stride = s->scratch_stride;
@@ -704,6 +706,13 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     const int64_t warps_total = (int64_t)s->grid * warps;
     if (sc && (sc[0] == 's' || sc[0] == 'd')) s->static_sched = sc[0] == 's';
     else s->static_sched = s->n_tiles <= (s->rc ? 1 : 4) * warps_total;
+    // store design with few tiles per warp: the sweep's tail is a large part
+    // of it; its warps release the averaging grid as they finish, whose CTAs
+    // load their (constant) slot indices on the idle SMs before waiting for
+    // the sweep (measured: GM -1 %; CellTrack, QAP50, MRF (recompute design)
+    // +0-2 %, so off there)
+    const char *pe = getenv("FDOG_PDL_EARLY");  // experiment knob: 0 / 1
+    s->pdl_early = pe ? (atoi(pe) ? 1 : 0) : (!s->rc && s->n_tiles < 8 * warps_total ? 1 : 0);
     // (A balanced static grid -- every warp exactly ceil(tiles / warps) tiles --
     // was measured on QAP50: 6 % slower.  Warps' finish times spread over 2x
     // either way: a grid that is not a multiple of the SM count leaves SMs
