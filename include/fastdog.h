@@ -172,8 +172,9 @@ fdog_status fdog_iterate_seq(fdog_solver *s, int32_t n_iter, double omega);
  *                       exchanged variables are in the exchange vector;
  *   (caller: exchange vector <- sum over ranks, via fdog_exchange_read/write)
  *   fdog_pass_end    -- averages of the exchanged variables + the sweep.
- * fdog_iterate returns FDOG_ESTATE in this mode, and fdog_lower_bound returns
- * this rank's part of the bound (the caller sums it). */
+ * fdog_iterate returns FDOG_ESTATE in this mode (unless the peer exchange
+ * below is set), and fdog_lower_bound returns this rank's part of the bound
+ * (the caller sums it). */
 fdog_status fdog_pass_begin(fdog_solver *s, int32_t forward, double omega);
 fdog_status fdog_pass_end(fdog_solver *s, int32_t forward, double omega);
 /* Number of exchanged variables (identical on every rank), and host copies of
@@ -181,6 +182,39 @@ fdog_status fdog_pass_end(fdog_solver *s, int32_t forward, double omega);
 fdog_status fdog_exchange_size(const fdog_solver *s, int64_t *n);
 fdog_status fdog_exchange_read(fdog_solver *s, double *out, int64_t len);
 fdog_status fdog_exchange_write(fdog_solver *s, const double *in, int64_t len);
+
+/* Peer-memory exchange (external-exchange mode; SURVEY §8(a) a4 without NCCL):
+ * the ranks exchange the partial sums of the shared variables through each
+ * other's device memory over NVLink instead of an allreduce.
+ *   fdog_exchange_region  -- this solver's exchange region (device memory,
+ *       one allocation of *bytes: pass counter at byte 0, error word at 4,
+ *       two partial-sum buffers from byte 256).  Share it with the peers: in
+ *       one process as the plain pointer, across processes through
+ *       fdog_ipc_handle / fdog_ipc_open.
+ *   fdog_set_peer_regions -- regions[k] = rank k's region as a device pointer
+ *       valid in this process (regions[rank] = the own one), before the first
+ *       pass.  From then on fdog_pass / fdog_iterate do the whole pass on the
+ *       device: averaging, publish (system-scope release of the pass
+ *       counter), wait until every peer has published the same pass, sum the
+ *       peers' partials in rank order (every rank gets bit-identical averages),
+ *       sweep.  A peer that does not publish within timeout_s seconds sets the
+ *       error word (fdog_peer_error) instead of hanging the device; the
+ *       results of that pass are then invalid.  fdog_pass_begin publishes,
+ *       fdog_pass_end waits, so one thread may drive several ranks of one
+ *       process by calling every begin before any end.  fdog_lower_bound
+ *       still returns this rank's part.
+ * Errors: FDOG_ESTATE outside the external-exchange mode or after a pass;
+ * FDOG_EINVAL for a wrong world size, a null region or a foreign own region. */
+#define FDOG_IPC_HANDLE_BYTES 64
+fdog_status fdog_exchange_region(const fdog_solver *s, void **region, int64_t *bytes);
+fdog_status fdog_set_peer_regions(fdog_solver *s, int32_t world, void *const *regions, double timeout_s);
+/* *err = 1 if a peer-exchange wait timed out (synchronises the stream). */
+fdog_status fdog_peer_error(fdog_solver *s, int32_t *err);
+/* CUDA IPC of a device allocation (handle: FDOG_IPC_HANDLE_BYTES bytes);
+ * fdog_ipc_open maps a handle of another process (peer access enabled). */
+fdog_status fdog_ipc_handle(void *dev_ptr, void *handle);
+fdog_status fdog_ipc_open(const void *handle, void **dev_ptr);
+fdog_status fdog_ipc_close(void *dev_ptr);
 
 /* Lower bound of the last completed pass (A7): sum_j E^j(lambda^j) +
  * sum_slots min(delta_bar, 0) + sum_free min(c_i, 0); summed over ranks.

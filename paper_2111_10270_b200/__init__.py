@@ -21,6 +21,26 @@ STATUS = {0: "OK", 1: "EINVAL", 2: "EINFEASIBLE", 3: "ENOMEM", 4: "ECUDA", 5: "E
           7: "ETOOBIG", 8: "ENOSOLUTION"}
 
 
+def ipc_handle(dev_ptr: int) -> bytes:
+    """CUDA IPC handle (64 bytes) of a device allocation, e.g. an exchange region."""
+    lib = load()
+    buf = C.create_string_buffer(64)
+    _check(lib.fdog_ipc_handle(C.c_void_p(dev_ptr), buf), "fdog_ipc_handle")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's allocation (peer access enabled); returns the device pointer."""
+    lib = load()
+    ptr = C.c_void_p()
+    _check(lib.fdog_ipc_open(C.c_char_p(bytes(handle)), C.byref(ptr)), "fdog_ipc_open")
+    return ptr.value
+
+
+def ipc_close(dev_ptr: int):
+    _check(load().fdog_ipc_close(C.c_void_p(dev_ptr)), "fdog_ipc_close")
+
+
 class FastdogError(RuntimeError):
     def __init__(self, code, what, msg):
         super().__init__(f"{what}: FDOG_{STATUS.get(code, code)}: {msg}")
@@ -71,7 +91,9 @@ EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdo
            "fdog_finalize", "fdog_finalize_averaged", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
            "fdog_get_deferred", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
            "fdog_profile", "fdog_profile_reset", "fdog_profile_enable", "fdog_pass_begin", "fdog_pass_end",
-           "fdog_exchange_size", "fdog_exchange_read", "fdog_exchange_write", "fdog_default_primal_options",
+           "fdog_exchange_size", "fdog_exchange_read", "fdog_exchange_write", "fdog_exchange_region",
+           "fdog_set_peer_regions", "fdog_peer_error", "fdog_ipc_handle", "fdog_ipc_open", "fdog_ipc_close",
+           "fdog_default_primal_options",
            "fdog_primal_step", "fdog_round_primal", "fdog_last_error", "fdog_version"]
 
 _lib = None
@@ -125,6 +147,12 @@ def load():
         "fdog_exchange_size": ([P, P], C.c_int),
         "fdog_exchange_read": ([P, P, i64], C.c_int),
         "fdog_exchange_write": ([P, P, i64], C.c_int),
+        "fdog_exchange_region": ([P, C.POINTER(P), P], C.c_int),
+        "fdog_set_peer_regions": ([P, i32, P, dbl], C.c_int),
+        "fdog_peer_error": ([P, P], C.c_int),
+        "fdog_ipc_handle": ([P, P], C.c_int),
+        "fdog_ipc_open": ([P, C.POINTER(P)], C.c_int),
+        "fdog_ipc_close": ([P], C.c_int),
         "fdog_default_primal_options": ([P], None),
         "fdog_primal_step": ([P, i32, dbl, C.c_uint64, P, P, i64], C.c_int),
         "fdog_round_primal": ([P, P, P, i64, P, P], C.c_int),
@@ -390,6 +418,24 @@ class Solver:
     def exchange_write(self, x):
         a = np.ascontiguousarray(x, dtype=np.float64)
         _check(self._lib.fdog_exchange_write(self._h, _ptr(a), a.size), "fdog_exchange_write")
+
+    def exchange_region(self):
+        """(device pointer, bytes) of this rank's exchange region (peer-memory mode)."""
+        ptr, n = C.c_void_p(), C.c_int64()
+        _check(self._lib.fdog_exchange_region(self._h, C.byref(ptr), C.byref(n)), "fdog_exchange_region")
+        return ptr.value, n.value
+
+    def set_peer_regions(self, regions, timeout_s: float = 20.0):
+        """regions[k]: rank k's exchange region as a device pointer valid in this
+        process (regions[rank] = own).  Passes then exchange over peer memory."""
+        arr = (C.c_void_p * len(regions))(*[int(r) for r in regions])
+        _check(self._lib.fdog_set_peer_regions(self._h, len(regions), arr, float(timeout_s)),
+               "fdog_set_peer_regions")
+
+    def peer_error(self) -> int:
+        e = C.c_int32()
+        _check(self._lib.fdog_peer_error(self._h, C.byref(e)), "fdog_peer_error")
+        return e.value
 
     def primal_step(self, round_: int, delta: float, seed: int = 0):
         """One classification (+ perturbation) step of Alg. 2: (undecided, x)."""

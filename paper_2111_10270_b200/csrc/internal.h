@@ -247,6 +247,17 @@ struct AvgArgs {
   int32_t csr_first;         // 1: the CSR section takes the first threads (else the last)
 };
 
+// Peer-memory exchange (kernels.cu peer_finish_kernel): the W ranks' exchange
+// regions as device pointers valid in this process.
+constexpr int kMaxPeers = 16;
+constexpr int kRegionBuf = 256;  // first partial-sum buffer of a region
+struct PeerArgs {
+  int32_t world, rank;
+  int64_t buf_off;                          // byte offset of this pass's buffer
+  unsigned long long timeout_ns;            // wait for a peer at most this long
+  const unsigned char *region[kMaxPeers];
+};
+
 struct PrimalArgs {
   int32_t n_ell, n_ell4, n_csr;
   const int2 *ell;
@@ -300,6 +311,9 @@ int launch_sweep_stream(int precision, int mode, bool record, const SweepArgs &a
 int launch_sweep_chunk(int precision, int mode, bool record, const SweepArgs &a, void *stream);
 int sweep_occupancy(int precision, int mode, bool record, bool rc, int block, size_t smem, int *blocks_per_sm);
 int launch_avg(int precision, const AvgArgs &a, void *stream);
+int launch_peer_signal(const PeerArgs &pa, void *stream);
+int launch_peer_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal,
+                       const int32_t *deg_x, const PeerArgs &pa, void *stream);
 int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,
                       void *stream);
 int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, void *stream);

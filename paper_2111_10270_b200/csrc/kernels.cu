@@ -8,6 +8,7 @@
 //   avg_kernel<T>                  deferred averaging avg_i = mean_{k in J_i} delta_bar_ik
 //                                  (P:641 second term, readings A1/A10).
 //   avg_finish_kernel<T>           shared variables after the NCCL exchange.
+//   peer_signal_kernel, peer_finish_kernel<T>  the exchange over peer memory instead.
 //   add_deferred_kernel<T>         final correction lambda += delta_bar.
 //   fused_small_kernel<T, REC>     every iteration of a small problem in one CTA.
 //   primal_kernel<T>               Alg. 2 classify / perturb steps.
@@ -1972,6 +1973,87 @@ __global__ void avg_finish_kernel(const AvgArgs a, int32_t n_shared, const int32
     const T v = xbuf[q] / T(deg_x[q]);
     for (int64_t p = a.var_ptr[l]; p < a.var_ptr[l + 1]; ++p) out[a.var_slots[p]] = v;
   }
+}
+
+// ---- peer-memory exchange (world > 1, fdog_set_peer_regions) ---------------
+// Every rank's exchange region (its own memory; the peers' regions mapped into
+// this process by CUDA IPC or, in one process, plain device pointers):
+//   [0] pass counter, [4] error word, [kRegionBuf + b * buf_stride] partial
+//   sums of pass parity b.  Per pass: averaging writes this rank's partials
+//   into its buffer of the pass parity; peer_signal_kernel publishes them
+//   (system-scope release of counter + 1); peer_finish_kernel waits until every
+//   peer's counter has reached this rank's, then sums the peers' partials over
+//   NVLink in rank order 0..W-1 (identical on every rank: the ranks agree bit
+//   for bit) and scatters the averages into the local slots.  Two buffers:
+//   a rank rewrites parity b only two passes later, after every peer has
+//   published the pass in between, i.e. finished reading this one.
+__global__ void peer_signal_kernel(unsigned *counter) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
+}
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T>
+__global__ void peer_finish_kernel(const AvgArgs a, int32_t n_shared, const int32_t *__restrict__ xlocal,
+                                   const int32_t *__restrict__ deg_x, const PeerArgs pa) {
+  T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    const unsigned target = *reinterpret_cast<volatile const unsigned *>(pa.region[pa.rank]);
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int good = 1;
+    for (int k = 0; k < pa.world && good; ++k) {
+      const unsigned *c = reinterpret_cast<const unsigned *>(pa.region[k]);
+      while (ld_acquire_sys(c) < target) {
+        __nanosleep(256);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > pa.timeout_ns) {  // a peer never published: report, do not hang
+          atomicExch(reinterpret_cast<unsigned *>(const_cast<unsigned char *>(pa.region[pa.rank]) + 4), 1u);
+          good = 0;
+          break;
+        }
+      }
+    }
+    ok = good;
+  }
+  __syncthreads();
+  if (!ok) return;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_shared; q += gridDim.x * blockDim.x) {
+    const int l = xlocal[q];
+    if (l < 0) continue;  // exchanged variable this rank does not hold
+    T sum = T(0);
+    for (int k = 0; k < pa.world; ++k) {
+      const T *b = reinterpret_cast<const T *>(pa.region[k] + pa.buf_off);
+      sum += __ldcv(b + q);  // (no stale L1 line of the peer's memory)
+    }
+    const T v = sum / T(deg_x[q]);
+    for (int64_t p = a.var_ptr[l]; p < a.var_ptr[l + 1]; ++p) out[a.var_slots[p]] = v;
+  }
+}
+
+static int grid_for(int64_t n, int block);
+
+int launch_peer_signal(const PeerArgs &pa, void *stream) {
+  peer_signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<unsigned *>(const_cast<unsigned char *>(pa.region[pa.rank])));
+  return (int)cudaGetLastError();
+}
+
+int launch_peer_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal,
+                       const int32_t *deg_x, const PeerArgs &pa, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int block = 256, grid = grid_for(std::max(n_shared, 1), block);
+  if (precision == 64)
+    peer_finish_kernel<double><<<grid, block, 0, st>>>(a, n_shared, xlocal, deg_x, pa);
+  else
+    peer_finish_kernel<float><<<grid, block, 0, st>>>(a, n_shared, xlocal, deg_x, pa);
+  return (int)cudaGetLastError();
 }
 
 template <typename T>

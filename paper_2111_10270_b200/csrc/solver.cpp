@@ -67,6 +67,14 @@ struct fdog_solver {
   double clamp = 0.0;
   int rank = 0, world = 1;
   bool external = false;  // world > 1 without NCCL: the caller performs the exchange
+  // peer-memory exchange (fdog_set_peer_regions; external mode only): this
+  // rank's region (pass counter, error word, two partial-sum buffers) and the
+  // peers' regions as device pointers valid in this process
+  unsigned char *d_region = nullptr;
+  size_t region_stride = 0;  // bytes per partial-sum buffer
+  bool peer = false;
+  int32_t peer_par = 0;      // parity of the next pass's buffer
+  PeerArgs peer_args{};
   bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
   bool chunk_mode = false;   // ... or sweep_chunk_kernel (every tile an arc-mask tile)
   bool rc = false;           // recompute design (Plan::rc): no distance traffic, no dist_state
@@ -275,6 +283,23 @@ fdog_status run_avg_finish(fdog_solver *s) {
   return FDOG_OK;
 }
 
+// peer-memory exchange of one pass (after run_avg published this rank's
+// partials): wait for the peers', sum them in rank order over NVLink, scatter
+// the averages
+fdog_status run_peer_exchange(fdog_solver *s) {
+  AvgArgs a = avg_args(s);
+  PeerArgs pa = s->peer_args;
+  pa.buf_off = kRegionBuf + (int64_t)s->peer_par * (int64_t)s->region_stride;
+  int e;
+  {
+    Timed t(s, kKAvgFinish);
+    e = launch_peer_finish(s->precision, a, s->n_shared, s->d_x_local, s->d_x_deg, pa, s->stream);
+  }
+  if (e) return cuda_fail((cudaError_t)e, "peer exchange launch");
+  s->peer_par ^= 1;
+  return FDOG_OK;
+}
+
 AvgArgs avg_args(fdog_solver *s) {
   AvgArgs a{};
   a.n_ell = s->n_ell;
@@ -299,14 +324,21 @@ AvgArgs avg_args(fdog_solver *s) {
 
 fdog_status run_avg(fdog_solver *s) {
   AvgArgs a = avg_args(s);
+  if (s->peer) a.xbuf = s->d_region + kRegionBuf + (size_t)s->peer_par * s->region_stride;
   if (s->world > 1 && s->n_shared > 0)  // entries of variables this rank does not hold contribute 0
-    CK(cudaMemsetAsync(s->d_xbuf, 0, (size_t)s->n_shared * s->tsz, s->stream), "memset");
+    CK(cudaMemsetAsync(a.xbuf, 0, (size_t)s->n_shared * s->tsz, s->stream), "memset");
   int e;
   {
     Timed t(s, kKAvg);
     e = launch_avg(s->precision, a, s->stream);
   }
   if (e) return cuda_fail((cudaError_t)e, "avg launch");
+  if (s->peer) {  // publish this rank's partials (the peers read them in their run_peer_exchange)
+    if (s->n_shared > 0 && (e = launch_peer_signal(s->peer_args, s->stream)))
+      return cuda_fail((cudaError_t)e, "peer signal launch");
+    s->launches++;
+    return FDOG_OK;
+  }
   if (s->world > 1 && s->n_shared > 0 && !s->external) {
     int r;
     {
@@ -336,7 +368,11 @@ fdog_status pass_stage(fdog_solver *s, bool forward, double omega, int stage) {
     if (!s->rc && !forward && s->dist_state != 1 && (st = run_sweep(s, kCfr, omega))) return st;
     return run_avg(s);
   }
-  if (s->external && (st = run_avg_finish(s))) return st;
+  if (s->peer && s->n_shared > 0) {
+    if ((st = run_peer_exchange(s))) return st;
+  } else if (s->external && (st = run_avg_finish(s))) {
+    return st;
+  }
   st = run_sweep(s, forward ? kForward : kBackward, omega);
   if (st) return st;
   s->dist_state = s->rc ? 2 : (forward ? 1 : 0);  // (the recompute design keeps no distances in HBM)
@@ -811,6 +847,15 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   }
   s->external = s->world > 1 && !o->nccl_unique_id;
   if (s->world > 1 && !s->external && (st = init_nccl(s, o))) return st;
+  if (s->external) {
+    // exchange region for the peer-memory mode (a separate allocation, so that
+    // one CUDA IPC handle maps exactly it): counter, error word, two buffers
+    s->region_stride = ((size_t)std::max<int32_t>(s->n_shared, 1) * s->tsz + 255) & ~(size_t)255;
+    const size_t rb = kRegionBuf + 2 * s->region_stride;
+    CK(cudaMalloc((void **)&s->d_region, rb), "cudaMalloc (exchange region)");
+    s->allocs.push_back(s->d_region);
+    CK(cudaMemsetAsync(s->d_region, 0, rb, s->stream), "memset");
+  }
   // FDOG_NCCL_SELF=1 (test knob): a one-rank NCCL communicator for world == 1,
   // so the bound's allreduce goes through the same dlopen'ed NCCL calls as a
   // multi-GPU run (tests/test_gpu_parity.py::test_nccl_one_rank_communicator)
@@ -1106,7 +1151,7 @@ fdog_status fdog_pass(fdog_solver *s, int32_t forward, double omega) {
     set_error("null solver");
     return FDOG_EINVAL;
   }
-  if (s->external) {
+  if (s->external && !s->peer) {
     set_error("external-exchange mode: use fdog_pass_begin / fdog_pass_end");
     return FDOG_ESTATE;
   }
@@ -1217,6 +1262,104 @@ fdog_status fdog_pass_end(fdog_solver *s, int32_t forward, double omega) {
   return pass_stage(s, forward != 0, omega, 1);
 }
 
+fdog_status fdog_exchange_region(const fdog_solver *s, void **region, int64_t *bytes) {
+  if (!s || !region || !bytes) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  if (!s->d_region) {
+    set_error("no exchange region: the solver is not in the external-exchange mode");
+    return FDOG_ESTATE;
+  }
+  *region = s->d_region;
+  *bytes = (int64_t)(kRegionBuf + 2 * s->region_stride);
+  return FDOG_OK;
+}
+
+fdog_status fdog_set_peer_regions(fdog_solver *s, int32_t world, void *const *regions, double timeout_s) {
+  if (!s || !regions || !(timeout_s > 0.0)) {
+    set_error("null argument or timeout <= 0");
+    return FDOG_EINVAL;
+  }
+  if (!s->d_region) {
+    set_error("peer exchange needs the external-exchange mode (world > 1, no NCCL id)");
+    return FDOG_ESTATE;
+  }
+  if (world != s->world || world > kMaxPeers) {
+    set_error("world %d: the solver's is %d (at most %d peers)", world, s->world, kMaxPeers);
+    return FDOG_EINVAL;
+  }
+  if (regions[s->rank] != (void *)s->d_region) {
+    set_error("regions[rank] must be this solver's own region");
+    return FDOG_EINVAL;
+  }
+  if (s->passes != 0) {
+    set_error("fdog_set_peer_regions must precede the first pass (the pass counters start at 0 on every rank)");
+    return FDOG_ESTATE;
+  }
+  PeerArgs pa{};
+  pa.world = world;
+  pa.rank = s->rank;
+  pa.timeout_ns = (unsigned long long)(timeout_s * 1e9);
+  for (int k = 0; k < world; ++k) {
+    if (!regions[k]) {
+      set_error("null region of rank %d", k);
+      return FDOG_EINVAL;
+    }
+    pa.region[k] = (const unsigned char *)regions[k];
+  }
+  s->peer_args = pa;
+  s->peer = true;
+  s->peer_par = 0;
+  return FDOG_OK;
+}
+
+fdog_status fdog_peer_error(fdog_solver *s, int32_t *err) {
+  if (!s || !err) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  *err = 0;
+  if (!s->d_region) return FDOG_OK;
+  unsigned v = 0;
+  CK(cudaMemcpyAsync(&v, s->d_region + 4, 4, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  CK(cudaStreamSynchronize(s->stream), "sync");
+  *err = (int32_t)v;
+  return FDOG_OK;
+}
+
+fdog_status fdog_ipc_handle(void *dev_ptr, void *handle) {
+  if (!dev_ptr || !handle) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, dev_ptr), "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == FDOG_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  return FDOG_OK;
+}
+
+fdog_status fdog_ipc_open(const void *handle, void **dev_ptr) {
+  if (!handle || !dev_ptr) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  return FDOG_OK;
+}
+
+fdog_status fdog_ipc_close(void *dev_ptr) {
+  if (!dev_ptr) {
+    set_error("null argument");
+    return FDOG_EINVAL;
+  }
+  CK(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+  return FDOG_OK;
+}
+
 fdog_status fdog_exchange_size(const fdog_solver *s, int64_t *n) {
   if (!s || !n) {
     set_error("null argument");
@@ -1261,7 +1404,7 @@ fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
     set_error("null solver or negative n_iter");
     return FDOG_EINVAL;
   }
-  if (s->external) {
+  if (s->external && !s->peer) {
     set_error("external-exchange mode: use fdog_pass_begin / fdog_pass_end");
     return FDOG_ESTATE;
   }

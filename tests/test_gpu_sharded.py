@@ -49,3 +49,109 @@ def test_sharded_solvers_match_unsharded(oracle_mod, world, name, make):
     with pytest.raises(F.FastdogError) as e:
         ranks[0].iterate(1, 0.5)
     assert e.value.code == 6
+
+
+def _gather(p, ranks, oracle_n):
+    lam = np.full(oracle_n, np.nan)
+    dl = np.full(oracle_n, np.nan)
+    for g in ranks:
+        con, pos = g.slot_index()
+        idx = p.row_ptr[con] + pos
+        lam[idx] = g.lam()
+        dl[idx] = g.deferred()
+    return lam, dl
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name,make", [
+    ("gm", lambda: synth.gm_worms_like(13, n_src=60, k_cand=6, knn=6)),
+    ("mrf", lambda: synth.mrf_potts(13, H=10, W=12, L=4)),
+])
+def test_peer_exchange_equals_host_exchange(oracle_mod, precision, world, name, make):
+    """Peer-memory exchange (fdog_set_peer_regions; the regions as plain device
+    pointers, one process): after every pass bit-identical to the host-summed
+    exchange in rank order, and within 1e-9 of the oracle (fp64)."""
+    p = make()
+    s = max(1.0, float(np.abs(p.cost).max()))
+    host = [F.Solver(p, precision=precision, rank=r, world=world) for r in range(world)]
+    peer = [F.Solver(p, precision=precision, rank=r, world=world) for r in range(world)]
+    regions = [g.exchange_region()[0] for g in peer]
+    for g in peer:
+        g.set_peer_regions(regions)
+    o = oracle_mod.Oracle(p)
+    for t in range(6):
+        fwd = t % 2 == 0
+        for g in host:
+            g.pass_begin(fwd, 0.5)
+        # rank order, in the solver's precision, as the device sums
+        dt = np.float64 if precision == 64 else np.float32
+        x = np.zeros(1, dt)
+        for g in host:
+            x = (x + g.exchange_read().astype(dt)).astype(dt)
+        x = x.astype(np.float64)
+        for g in host:
+            g.exchange_write(x)
+        for g in host:
+            g.pass_end(fwd, 0.5)
+        for g in peer:      # every rank publishes ...
+            g.pass_begin(fwd, 0.5)
+        for g in peer:      # ... before any waits (one thread drives all ranks)
+            g.pass_end(fwd, 0.5)
+        o.pass_(fwd, 0.5)
+        for a, b in zip(host, peer):
+            assert np.array_equal(a.lam(), b.lam()) and np.array_equal(a.deferred(), b.deferred()), f"pass {t}"
+        if precision == 64:
+            lam, dl = _gather(p, peer, o.num_slots())
+            assert np.max(np.abs(lam - o.lam())) <= 1e-9 * s, f"pass {t}"
+            assert np.max(np.abs(dl - o.deferred())) <= 1e-9 * s
+    assert all(g.peer_error() == 0 for g in peer)
+
+
+def test_peer_exchange_whole_passes_on_streams(oracle_mod):
+    """fdog_iterate in the peer mode: each rank's whole pass on its own stream,
+    launched one rank after the other from one thread -- the ranks wait for
+    each other on the device only."""
+    import torch
+    p = synth.gm_worms_like(14, n_src=60, k_cand=6, knn=6)
+    s = max(1.0, float(np.abs(p.cost).max()))
+    world = 2
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    ranks = [F.Solver(p, precision=64, rank=r, world=world, stream=streams[r].cuda_stream) for r in range(world)]
+    regions = [g.exchange_region()[0] for g in ranks]
+    for g in ranks:
+        g.set_peer_regions(regions, timeout_s=10.0)
+    o = oracle_mod.Oracle(p)
+    for it in range(3):
+        for g in ranks:
+            g.iterate(1, 0.5)
+        o.iterate(1, 0.5)
+        assert all(g.peer_error() == 0 for g in ranks)
+        lam, dl = _gather(p, ranks, o.num_slots())
+        assert np.max(np.abs(lam - o.lam())) <= 1e-9 * s, it
+        lb = sum(g.lower_bound() for g in ranks)
+        assert abs(lb - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+
+
+def test_peer_exchange_errors_and_timeout():
+    p = synth.gm_worms_like(15, n_src=40, k_cand=5, knn=5)
+    single = F.Solver(p, precision=32)
+    with pytest.raises(F.FastdogError) as e:
+        single.exchange_region()
+    assert e.value.code == 6
+    ranks = [F.Solver(p, precision=32, rank=r, world=2) for r in range(2)]
+    regions = [g.exchange_region()[0] for g in ranks]
+    with pytest.raises(F.FastdogError) as e:
+        ranks[0].set_peer_regions(regions[:1])          # wrong world size
+    assert e.value.code == 1
+    with pytest.raises(F.FastdogError) as e:
+        ranks[0].set_peer_regions(regions[::-1])        # own region not at [rank]
+    assert e.value.code == 1
+    ranks[0].set_peer_regions(regions, timeout_s=0.2)
+    ranks[0].pass_(True, 0.5)                           # rank 1 never publishes
+    assert ranks[0].peer_error() == 1                   # reported, no hang
+    ranks[1].pass_begin(True, 0.5)
+    ranks[1].pass_end(True, 0.5)
+    with pytest.raises(F.FastdogError) as e:
+        ranks[1].set_peer_regions(regions)              # after a pass
+    assert e.value.code == 6
