@@ -184,22 +184,57 @@ def run_gpu(args):
     if world != args.gpus and not (world == 1 and args.gpus == 1):
         if world == 1:
             raise SystemExit(f"--gpus {args.gpus} needs torchrun with {args.gpus} processes")
+    peer = args.exchange == "peer" and world > 1
+    # FDOG_SAME_DEVICE=1 (test knob, peer exchange only): every rank on GPU 0
+    if peer and os.environ.get("FDOG_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     nccl_lib = None
-    if world > 1:
+    if world > 1 and peer:
+        # the shared variables go through peer memory (CUDA IPC); the plumbing
+        # (handles, barriers, timing max) through gloo
+        dist.init_process_group("gloo")
+    elif world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         import nvidia.nccl  # namespace package: the torch-bundled NCCL
         nccl_lib = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+    tdev = "cpu" if peer else "cuda"  # tensors of the plumbing collectives
+
+    opened = []
+
+    def make_solver(plan_, prec_):
+        s_ = F.Solver(plan=plan_, precision=prec_, device=local, rank=rank, world=world,
+                      nccl_unique_id=new_uid(), nccl_library=nccl_lib, stream=stream.cuda_stream)
+        if peer:
+            own, _ = s_.exchange_region()
+            hs = [None] * world
+            dist.all_gather_object(hs, F.ipc_handle(own))
+            regions = []
+            for k, h in enumerate(hs):
+                if k == rank:
+                    regions.append(own)
+                else:
+                    regions.append(F.ipc_open(h))
+                    opened.append(regions[-1])
+            s_.set_peer_regions(regions)
+        return s_
+
+    def global_lb(s_):
+        v = s_.lower_bound()
+        if peer:  # each rank holds its part of the bound (fdog_lower_bound)
+            t_ = torch.tensor([v], dtype=torch.float64)
+            dist.all_reduce(t_)
+            v = float(t_.item())
+        return v
 
     def new_uid():
         # a fresh ncclUniqueId per communicator, broadcast through torch.distributed
-        if world == 1:
+        if world == 1 or peer:
             return None
         obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         return obj[0]
 
-    uid = new_uid()
     stream = torch.cuda.Stream()  # a real stream (the legacy default stream's handle is 0)
     torch.cuda.set_stream(stream)
     problem = _workload(args.workload)
@@ -207,16 +242,15 @@ def run_gpu(args):
     plan = F.Plan(problem, rank=rank, world=world, precision=64 if args.fp64 else 32)
     plan_s = time.perf_counter() - t0
     prec = 64 if args.fp64 else 32
-    solver = F.Solver(plan=plan, precision=prec, device=local, profile=False, rank=rank, world=world,
-                      nccl_unique_id=uid, nccl_library=nccl_lib, stream=stream.cuda_stream)
+    solver = make_solver(plan, prec)
     st = solver.stats()
     arcs_local = st["arcs"]
     arcs_total = arcs_local
     if world > 1:
-        t = torch.tensor([arcs_local], dtype=torch.int64, device="cuda")
+        t = torch.tensor([arcs_local], dtype=torch.int64, device=tdev)
         dist.all_reduce(t)
         arcs_total = int(t.item())
-    lb0 = solver.lower_bound()
+    lb0 = global_lb(solver)
     # L2 flush between timed steps: write 256 MB (> 126 MB L2), then read another
     # 256 MB so the dirty lines are written back before the timed interval starts
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -253,7 +287,7 @@ def run_gpu(args):
     clocks = sampler.stop()
     tot_ms = float(sum(ms))
     if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     launches = solver.stats()["launches"] - launches0
@@ -264,7 +298,7 @@ def run_gpu(args):
     ms_prof = timed_steps()
     prof = solver.profile()
     solver.profile_enable(False)
-    lb = solver.lower_bound()
+    lb = global_lb(solver)
 
     # roofline of the dominant kernel (the two sweeps share one code path)
     peak, peak_kind = _peaks()
@@ -298,23 +332,24 @@ def run_gpu(args):
     # e2e through the public API with host buffers (fresh solver; upload inside)
     e2e = None
     if not args.no_e2e:
-        uid2 = new_uid()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        s2 = F.Solver(plan=plan, precision=prec, device=local, rank=rank, world=world,
-                      nccl_unique_id=uid2, nccl_library=nccl_lib, stream=stream.cuda_stream)
+        s2 = make_solver(plan, prec)
         for _ in range(args.steps):
             s2.iterate(1, OMEGA)
             s2.lower_bound()  # D2H of the step's result (8 bytes)
         lam = s2.lam()
         el = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            t = torch.tensor([el], dtype=torch.float64, device=tdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         up = s2.stats()["h2d_bytes"]
+        if peer:  # no rank frees its region while a peer may still read it
+            torch.cuda.synchronize()
+            dist.barrier()
         s2.close()
         e2e = {"value": arcs_total * 2 * args.steps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(up / args.steps),
@@ -395,7 +430,7 @@ def run_gpu(args):
             "dtype": "f64" if prec == 64 else "f32", "data": "synthetic",
             "config": {"workload": problem.name, "bdds": st["bdds"], "nodes": st["nodes"],
                        "arcs": st["arcs"], "slots": st["slots"], "vars": problem.n_vars,
-                       "omega": OMEGA, "parallelism": f"bdd-shard{world}",
+                       "omega": OMEGA, "parallelism": f"bdd-shard{world}" + ("-peer" if peer else ""),
                        "l2": "flushed before every timed step (256 MB write + 256 MB read, untimed)",
                        "plan_s": round(plan_s, 3)},
             "iters_per_s": iters_s,
@@ -421,6 +456,13 @@ def run_gpu(args):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if peer:
+        torch.cuda.synchronize()
+        dist.barrier()
+        for r_ in opened:
+            F.ipc_close(r_)
+        dist.barrier()
+        solver.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -433,6 +475,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="gm_worms_like")
     ap.add_argument("--fp64", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: shared variables by ncclAllReduce or through peer memory (CUDA IPC)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttl", action="store_true")
