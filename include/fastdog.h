@@ -225,7 +225,8 @@ fdog_status fdog_lower_bound(fdog_solver *s, double *out);
 fdog_status fdog_finalize(fdog_solver *s);
 /* Final correction read as "a min-marginal averaging step" (P:673 prose, the
  * alternative of reading A11): lambda_i^j += (1/|J_i|) sum_k delta_bar_ik,
- * delta_bar = 0.  Also dual feasible.  world == 1 or NCCL mode. */
+ * delta_bar = 0.  Also dual feasible.  world == 1, NCCL or peer-memory mode
+ * (a collective: every rank calls it). */
 fdog_status fdog_finalize_averaged(fdog_solver *s);
 
 fdog_status fdog_num_slots(const fdog_solver *s, int64_t *out);

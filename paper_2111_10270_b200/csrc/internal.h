@@ -312,6 +312,7 @@ int launch_sweep_chunk(int precision, int mode, bool record, const SweepArgs &a,
 int sweep_occupancy(int precision, int mode, bool record, bool rc, int block, size_t smem, int *blocks_per_sm);
 int launch_avg(int precision, const AvgArgs &a, void *stream);
 int launch_peer_signal(const PeerArgs &pa, void *stream);
+int preload_kernels(int precision);
 int launch_peer_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal,
                        const int32_t *deg_x, const PeerArgs &pa, void *stream);
 int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const int32_t *xlocal, const int32_t *deg_x,

@@ -2319,6 +2319,34 @@ int launch_sweep_chunk(int precision, int mode, bool rec, const SweepArgs &a, vo
   return launch_pdl(f, dim3(grid > 0 ? grid : 1), dim3(32 * wpb), (size_t)wpb * wbytes, stream, args);
 }
 
+// Load every kernel a pass, a finalize or a bound can launch (CUDA lazy
+// loading would otherwise load a kernel at its first launch, and loading waits
+// for the device: with a peer-exchange kernel spinning on a rank that the same
+// host thread has not launched yet, that first launch would never return).
+int preload_kernels(int precision) {
+  cudaFuncAttributes at;
+  auto load = [&](const void *f) { return f ? cudaFuncGetAttributes(&at, f) : cudaSuccess; };
+  cudaError_t e = cudaSuccess;
+  for (int mode = 0; mode < 4 && e == cudaSuccess; ++mode)
+    for (int rec = 0; rec < 2 && e == cudaSuccess; ++rec)
+      for (int rc = 0; rc < 2 && e == cudaSuccess; ++rc) {
+        e = load(sweep_ptr(precision, mode, rec != 0, rc != 0));
+        if (e == cudaSuccess && !rc)
+          e = load(precision == 64 ? stream_fn<double>(mode, rec != 0) : stream_fn<float>(mode, rec != 0));
+        if (e == cudaSuccess && !rc)
+          e = load(precision == 64 ? chunk_fn<double>(mode, rec != 0) : chunk_fn<float>(mode, rec != 0));
+      }
+  const bool d = precision == 64;
+  const void *fs[] = {d ? (const void *)avg_kernel<double> : (const void *)avg_kernel<float>,
+                      d ? (const void *)avg_finish_kernel<double> : (const void *)avg_finish_kernel<float>,
+                      d ? (const void *)peer_finish_kernel<double> : (const void *)peer_finish_kernel<float>,
+                      d ? (const void *)add_deferred_kernel<double> : (const void *)add_deferred_kernel<float>,
+                      (const void *)peer_signal_kernel, (const void *)lb_reduce_kernel};
+  for (const void *f : fs)
+    if (e == cudaSuccess) e = load(f);
+  return (int)e;
+}
+
 int launch_sweep(int precision, int mode, bool rec, bool rc, const SweepArgs &a, int grid, int block, size_t smem,
                  void *stream) {
   const void *f = sweep_ptr(precision, mode, rec, rc);

@@ -1297,6 +1297,10 @@ fdog_status fdog_set_peer_regions(fdog_solver *s, int32_t world, void *const *re
     set_error("fdog_set_peer_regions must precede the first pass (the pass counters start at 0 on every rank)");
     return FDOG_ESTATE;
   }
+  {
+    const int e = preload_kernels(s->precision);
+    if (e) return cuda_fail((cudaError_t)e, "kernel preload");
+  }
   PeerArgs pa{};
   pa.world = world;
   pa.rank = s->rank;
@@ -1526,14 +1530,15 @@ fdog_status fdog_finalize_averaged(fdog_solver *s) {
     set_error("null solver");
     return FDOG_EINVAL;
   }
-  if (s->external) {
-    set_error("fdog_finalize_averaged needs world == 1 or the NCCL exchange");
+  if (s->external && !s->peer) {
+    set_error("fdog_finalize_averaged needs world == 1, the NCCL or the peer-memory exchange");
     return FDOG_ESTATE;
   }
   // the averaging kernel (+ exchange) writes avg_i into every slot of the other
   // delta buffer; lambda += that buffer, then both buffers are zero
   fdog_status st = run_avg(s);
   if (st) return st;
+  if (s->peer && s->n_shared > 0 && (st = run_peer_exchange(s))) return st;
   int e;
   {
     Timed t(s, kKAddDeferred);

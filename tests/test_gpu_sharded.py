@@ -131,6 +131,16 @@ def test_peer_exchange_whole_passes_on_streams(oracle_mod):
         assert np.max(np.abs(lam - o.lam())) <= 1e-9 * s, it
         lb = sum(g.lower_bound() for g in ranks)
         assert abs(lb - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+    # averaged final correction (A11 prose reading) through the peer exchange
+    for g in ranks:
+        g.finalize(averaged=True)
+    o.finalize(averaged=True)
+    assert all(g.peer_error() == 0 for g in ranks)
+    lam, dl = _gather(p, ranks, o.num_slots())
+    assert np.max(np.abs(lam - o.lam())) <= 1e-9 * s
+    assert np.all(dl == 0.0)
+    lb = sum(g.lower_bound() for g in ranks)
+    assert abs(lb - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
 
 
 def test_peer_exchange_errors_and_timeout():
