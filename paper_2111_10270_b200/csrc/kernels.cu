@@ -1015,8 +1015,12 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   unsigned long long t_start = 0;
   int n_done = 0;
   if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-  auto claim_issue = [&]() -> int { return lane == 0 ? (int)atomicAdd(a.tile_counter, 1u) : 0; };
+  // claims take claim_batch consecutive tiles per atomic (many small tiles:
+  // one counter serialises the claims of every warp)
+  const int CB = a.claim_batch > 1 ? a.claim_batch : 1;
+  auto claim_issue = [&]() -> int { return lane == 0 ? (int)atomicAdd(a.tile_counter, (unsigned)CB) : 0; };
   auto claim_get = [&](int raw) -> int { return 2 * W + __shfl_sync(0xffffffffu, raw, 0); };
+  int bnext = 0, bend = 0;  // the rest of the current batch (warp-uniform)
   // pipeline per warp: while tile t is processed, the TMA stage loads of the
   // next tile are in flight, the descriptor of the one after is being fetched
   // (cp.async), and (dynamic schedule) the claim for the tile after that.
@@ -1041,14 +1045,20 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
     int tnn = a.n_tiles;
     if (a.static_sched) {
       tnn = tn + W < a.n_tiles ? tn + W : a.n_tiles;
-    } else if (pending) {
-      tnn = claim_get(raw_nn);
-      if (tnn > a.n_tiles) tnn = a.n_tiles;
+    } else {
+      if (bnext >= bend && pending) {
+        bnext = claim_get(raw_nn);
+        bend = bnext + CB < a.n_tiles ? bnext + CB : a.n_tiles;
+        pending = false;
+      }
+      if (bnext < bend) tnn = bnext++;
     }
     __syncwarp();  // every lane has read dnn's slot (it held the previous tile)
     if (tnn < a.n_tiles) fetch_desc(&dnn, a.tiles + tnn, lane);  // used one tile later
-    pending = !a.static_sched && tnn < a.n_tiles;
-    raw_nn = pending ? claim_issue() : 0;
+    if (!a.static_sched && !pending && bnext >= bend && tnn < a.n_tiles) {
+      pending = true;  // the next batch's claim, in flight while this one is used
+      raw_nn = claim_issue();
+    }
     const int L = d.lanes;
     const bool active = lane < L;
     const bool valid = lane < d.n_lanes;

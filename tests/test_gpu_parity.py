@@ -371,6 +371,33 @@ def test_stage_buffers_bitwise(oracle_mod, monkeypatch, mode, name, make):
     assert np.array_equal(gs[0].lam(), gs[1].lam())
 
 
+def test_tile_schedules_bitwise(monkeypatch):
+    """Static round-robin, dynamic claims of one tile and batched claims of
+    several tiles per atomic give bit-identical iterates and bounds (a BDD's
+    arithmetic does not depend on the warp that runs it; the bound sums the
+    per-tile partials in tile order).  One warp per CTA, so every warp runs
+    several tiles and the batches are exercised."""
+    p = synth.mrf_potts(5, H=100, W=100, L=8)
+    monkeypatch.setenv("FDOG_WPB", "1")
+    gs = {}
+    for name, env in (("static", {"FDOG_SCHED": "static"}), ("claim1", {"FDOG_SCHED": "dynamic", "FDOG_CLAIM": "1"}),
+                      ("claim3", {"FDOG_SCHED": "dynamic", "FDOG_CLAIM": "3"})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        gs[name] = F.Solver(p, precision=32)
+        for k in env:
+            monkeypatch.delenv(k)
+    st = gs["claim3"].stats()
+    assert st["tiles"] > 2 * st["sweep_grid"]
+    for g in gs.values():
+        g.iterate(3, 0.5)
+        g.pass_(True, 0.5)
+    ref = gs["static"]
+    for g in gs.values():
+        assert np.array_equal(g.lam(), ref.lam()) and np.array_equal(g.deferred(), ref.deferred())
+        assert g.lower_bound() == ref.lower_bound()
+
+
 def test_errors_and_state():
     p = synth.spec_two_constraint()
     g = F.Solver(p, precision=64)
