@@ -1663,7 +1663,9 @@ __device__ __forceinline__ V ld(const V *p) {
 // tile counter.  (Measured slower: a slot-parallel ELL section -- every slot
 // gathering its partner's delta_bar, coalesced writes -- 1.5-2.3x, the
 // partner gathers lose the locality of the first slot; consecutive instead of
-// strided variables per thread (FDOG_AVG_LOCAL=1) 1.1-1.4x.)
+// strided variables per thread (FDOG_AVG_LOCAL=1) 1.1-1.4x; pairs re-ordered
+// by the 2^b-slot bucket of their smaller slot, then the larger, b = 4..14:
+// within 1 %.)
 // NC: delta_bar is read-only for the kernel's lifetime (the standalone kernel)
 // V: ELL variables per thread (tid, tid + N, ..., tid + (V-1) N: every load of
 // a warp stays coalesced, all 2V gathers in flight before the first use)
