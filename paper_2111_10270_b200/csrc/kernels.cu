@@ -2116,6 +2116,10 @@ __device__ __forceinline__ SeqLoc seq_locate(const SeqArgs &a, int32_t ds, int32
 // one warp per variable, lane k handles slots k, k + 32, ... of it (every slot
 // of a high-degree variable in parallel); the sum over J_i is accumulated in
 // ascending j by one lane (shuffles), as the oracle does
+// (Measured slower: the whole pass as one cooperative launch with a grid
+// barrier between levels, 148-592 CTAs of 16 warps looping over a level's
+// variables -- GM 7.7-8.6 ms per iteration against 5.4 for the CUDA graph of
+// per-level launches, one warp per variable.)
 template <typename T, bool REC>
 __global__ void __launch_bounds__(128) seq_level_kernel(const SeqArgs a, int64_t q0, int64_t q1) {
   const int64_t q = q0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
