@@ -1007,7 +1007,15 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   // before every sweep) unless static_sched
   const int W = gridDim.x * wpb;
   int t = gwarp;
-  int tn = gwarp + W < a.n_tiles ? gwarp + W : a.n_tiles;
+  // static rounds alternate direction (round r takes tile r W + w for even r,
+  // r W + W - 1 - w for odd r): the warp with the costliest tile of one round
+  // gets the cheapest of the next (cost-sorted tiles; a.snake)
+  auto sidx = [&](int r) -> int {
+    const long long i = (long long)r * W + ((a.snake && (r & 1)) ? W - 1 - gwarp : gwarp);
+    return i < a.n_tiles ? (int)i : a.n_tiles;
+  };
+  int rnd = 1;  // static round of tn
+  int tn = sidx(1);
   // descriptors are constant: fetch them before waiting for the predecessor
   if (t < a.n_tiles) fetch_desc(&ring[0], a.tiles + t, lane);
   if (tn < a.n_tiles) fetch_desc(&ring[1], a.tiles + tn, lane);
@@ -1044,7 +1052,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
     }
     int tnn = a.n_tiles;
     if (a.static_sched) {
-      tnn = tn + W < a.n_tiles ? tn + W : a.n_tiles;
+      tnn = sidx(++rnd);
     } else {
       if (bnext >= bend && pending) {
         bnext = claim_get(raw_nn);
