@@ -329,33 +329,43 @@ def run_gpu(args):
     step_total_ms = sum(v["ms"] for v in prof.values())
     shares = {k: v["ms"] / step_total_ms for k, v in prof.items()} if step_total_ms else {}
 
-    # e2e through the public API with host buffers (fresh solver; upload inside)
+    # e2e through the public API with host buffers (fresh solver; upload inside).
+    # Three complete runs, each with its own solver; the median is reported and
+    # every run is listed (single runs showed rare 5-10x outliers on fresh boxes)
     e2e = None
     if not args.no_e2e:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        s2 = make_solver(plan, prec)
-        for _ in range(args.steps):
-            s2.iterate(1, OMEGA)
-            s2.lower_bound()  # D2H of the step's result (8 bytes)
-        lam = s2.lam()
-        el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], dtype=torch.float64, device=tdev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
-        up = s2.stats()["h2d_bytes"]
-        if peer:  # no rank frees its region while a peer may still read it
+        runs, parts = [], []
+        for _rep in range(3):
             torch.cuda.synchronize()
-            dist.barrier()
-        s2.close()
-        e2e = {"value": arcs_total * 2 * args.steps / el, "unit": UNIT,
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            s2 = make_solver(plan, prec)
+            t1 = time.perf_counter()
+            for _ in range(args.steps):
+                s2.iterate(1, OMEGA)
+                s2.lower_bound()  # D2H of the step's result (8 bytes)
+            t2 = time.perf_counter()
+            lam = s2.lam()
+            el = time.perf_counter() - t0
+            if world > 1:
+                t = torch.tensor([el], dtype=torch.float64, device=tdev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                el = float(t.item())
+            up = s2.stats()["h2d_bytes"]
+            if peer:  # no rank frees its region while a peer may still read it
+                torch.cuda.synchronize()
+                dist.barrier()
+            s2.close()
+            runs.append(arcs_total * 2 * args.steps / el)
+            parts.append({"create_ms": 1e3 * (t1 - t0), "steps_ms": 1e3 * (t2 - t1),
+                          "get_lambda_ms": 1e3 * (el - (t2 - t0)) if world == 1 else None})
+        e2e = {"value": statistics.median(runs), "unit": UNIT,
                "h2d_bytes_per_step": int(up / args.steps),
                "d2h_bytes_per_step": int(8 + lam.nbytes / args.steps),
-               "includes": "device allocation + H2D upload of the packed plan, K x (iterate(1) + "
-                           "lower_bound D2H), get_lambda D2H"}
+               "runs": runs, "parts": parts,
+               "includes": "per run: device allocation + H2D upload of the packed plan, K x (iterate(1) + "
+                           "lower_bound D2H), get_lambda D2H; value = median of the runs"}
 
     # time-to-LB (BASELINE metric): target = fp64 bound after 1000
     # iterations; fp32 solver from scratch, bound sampled every 10 iterations
