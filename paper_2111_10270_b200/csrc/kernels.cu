@@ -1002,9 +1002,10 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
-  // tile schedule: warp w takes tiles w and w + W statically (tiles are sorted
-  // by decreasing cost); later tiles are claimed from a global counter (reset
-  // before every sweep) unless static_sched
+  // tile schedule (tiles sorted by decreasing cost): warp w takes its tiles of
+  // the first two static rounds; later tiles are claimed from a global counter
+  // (reset before every sweep, claims start at 2 W), or static_sched: every
+  // round static
   const int W = gridDim.x * wpb;
   int t = gwarp;
   // static rounds alternate direction (round r takes tile r W + w for even r,
