@@ -203,8 +203,15 @@ fdog_status fdog_exchange_write(fdog_solver *s, const double *in, int64_t len);
  *       fdog_pass_end waits, so one thread may drive several ranks of one
  *       process by calling every begin before any end.  fdog_lower_bound
  *       still returns this rank's part.
+ * Ownership: the region belongs to the solver and is freed by fdog_destroy;
+ * a rank may destroy its solver only after every peer has finished its last
+ * pass (e.g. a barrier), and an importer closes its mappings with
+ * fdog_ipc_close.  fdog_set_peer_regions also loads every kernel a pass can
+ * launch (a lazy first-launch load would wait for the device, where a peer's
+ * kernel may be spinning).
  * Errors: FDOG_ESTATE outside the external-exchange mode or after a pass;
- * FDOG_EINVAL for a wrong world size, a null region or a foreign own region. */
+ * FDOG_EINVAL for a wrong world size (at most 16), a null region or a foreign
+ * own region. */
 #define FDOG_IPC_HANDLE_BYTES 64
 fdog_status fdog_exchange_region(const fdog_solver *s, void **region, int64_t *bytes);
 fdog_status fdog_set_peer_regions(fdog_solver *s, int32_t world, void *const *regions, double timeout_s);
