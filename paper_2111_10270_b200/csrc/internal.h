@@ -224,6 +224,7 @@ struct SweepArgs {
   int32_t pdl_early;        // 1: griddepcontrol.launch_dependents after a warp's last tile
   int32_t claim_batch;      // dynamic schedule: tiles per claim (>= 1)
   int32_t snake;            // static rounds alternate direction
+  int32_t spread;           // static tiles spread over CTAs (SMs) first
   void *scratch;            // T*, [warps][scratch_stride] for direct tiles
   unsigned long long *trace;  // debug (FDOG_TRACE=1): per warp {start, end, tiles, smid}, else null
   int64_t scratch_stride;   // elements per warp

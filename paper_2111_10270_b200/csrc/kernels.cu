@@ -1007,12 +1007,16 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   // (reset before every sweep, claims start at 2 W), or static_sched: every
   // round static
   const int W = gridDim.x * wpb;
-  int t = gwarp;
+  // schedule index: consecutive (i.e. the costliest) static tiles go to the
+  // same warp slot of consecutive CTAs, i.e. to different SMs, instead of
+  // filling one CTA's warps first (FDOG_SPREAD=0: the CTA-major order)
+  const int sw = a.spread ? warp * (int)gridDim.x + (int)blockIdx.x : gwarp;
+  int t = sw;
   // static rounds alternate direction (round r takes tile r W + w for even r,
   // r W + W - 1 - w for odd r): the warp with the costliest tile of one round
   // gets the cheapest of the next (cost-sorted tiles; a.snake)
   auto sidx = [&](int r) -> int {
-    const long long i = (long long)r * W + ((a.snake && (r & 1)) ? W - 1 - gwarp : gwarp);
+    const long long i = (long long)r * W + ((a.snake && (r & 1)) ? W - 1 - sw : sw);
     return i < a.n_tiles ? (int)i : a.n_tiles;
   };
   int rnd = 1;  // static round of tn

@@ -94,6 +94,7 @@ struct fdog_solver {
   int32_t pdl_early = 0;     // sweep warps release the averaging grid when their tiles are done
   int32_t claim_batch = 1;   // dynamic schedule: tiles per atomic claim
   int32_t snake = 1;         // static rounds alternate direction (FDOG_SNAKE=0: all ascending)
+  int32_t spread = 1;        // static tiles over CTAs first (FDOG_SPREAD=0: CTA-major)
 
   // host copies needed by getters
   // host-side data shared with the plan (no copy; kept alive by the solver)
@@ -267,6 +268,7 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.pdl_early = s->pdl_early;
   a.claim_batch = s->claim_batch;
   a.snake = s->snake;
+  a.spread = s->spread;
   a.trace = s->d_trace;
   a.scratch = s->d_scratch;  // relaxation buffers of direct (unstaged) tiles
   a.scratch_stride = s->scratch_stride;
@@ -756,6 +758,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     // warp, sweeps 282 -> 219 us with 2-4 tiles per claim, 8: 226, 16: 235;
     // CellTrack, 9.5 per warp, 39.5 -> 38.8 us with 2)
     if (const char *sn = getenv("FDOG_SNAKE")) s->snake = atoi(sn) ? 1 : 0;  // experiment knob
+    if (const char *sp = getenv("FDOG_SPREAD")) s->spread = atoi(sp) ? 1 : 0;  // experiment knob
     const char *cb = getenv("FDOG_CLAIM");  // experiment knob: tiles per claim
     const int64_t tpw = s->n_tiles / std::max<int64_t>(warps_total, 1);
     s->claim_batch = cb ? std::max(1, atoi(cb)) : (tpw >= 32 ? 4 : tpw >= 8 ? 2 : 1);
