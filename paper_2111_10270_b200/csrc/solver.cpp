@@ -94,7 +94,7 @@ struct fdog_solver {
   int32_t pdl_early = 0;     // sweep warps release the averaging grid when their tiles are done
   int32_t claim_batch = 1;   // dynamic schedule: tiles per atomic claim
   int32_t snake = 1;         // static rounds alternate direction (FDOG_SNAKE=0: all ascending)
-  int32_t spread = 1;        // static tiles over CTAs first (FDOG_SPREAD=0: CTA-major)
+  int32_t spread = 0;        // FDOG_SPREAD=1: static tiles over CTAs first (measured: no gain, QAP50 +3 %)
 
   // host copies needed by getters
   // host-side data shared with the plan (no copy; kept alive by the solver)
