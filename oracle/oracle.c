@@ -746,7 +746,11 @@ int oracle_set_lambda(oracle_solver *s, const double *lambda, int64_t len) {
     backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
     forward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
   }
-  s->lb = raw_energy(s);
+  /* delta_bar is untouched: the lifted bound (A7) keeps its outstanding
+   * sum_slots min(delta_bar, 0) term (zero when delta_bar = 0) */
+  double neg = 0.0;
+  for (int64_t q = 0; q < s->n_slots; ++q) neg += s->delta_bar[q] < 0 ? s->delta_bar[q] : 0.0;
+  s->lb = raw_energy(s) + neg;
   s->ctt_ok = s->cfr_ok = 1;
   return O_OK;
 }

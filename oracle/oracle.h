@@ -78,6 +78,9 @@ int oracle_get_lambda(const oracle_solver *s, double *out, int64_t len);
 int oracle_get_deferred(const oracle_solver *s, double *out, int64_t len);
 /* m0, m1 recorded during the last pass (+inf where infeasible). */
 int oracle_min_marginals(const oracle_solver *s, double *m0, double *m1, int64_t len);
+/* Overwrite lambda (canonical order); delta_bar is kept.  Recomputes both
+ * distance directions from the definition; the bound
+ * becomes sum_j E^j(lambda) + sum min(delta_bar, 0) + free term (A7). */
 int oracle_set_lambda(oracle_solver *s, const double *lambda, int64_t len);
 
 /* BDD inspection (for the path-set / closed-form pins). */
