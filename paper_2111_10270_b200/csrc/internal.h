@@ -322,6 +322,9 @@ int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const i
                       void *stream);
 int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, void *stream);
 int launch_lb_reduce(const double *lb_part, int32_t n, double *out, void *stream);
+// lb_part[t] += sum over tile t's slots of min(delta_bar, 0) (the A7 term after an energy sweep)
+int launch_lb_deferred(int precision, const TileDesc *tiles, int32_t n_tiles, const void *delta, double *lb_part,
+                       void *stream);
 // smem > 0: the mutable state is copied into that many bytes of shared memory
 int launch_fused_small(int precision, bool record, const SweepArgs &sa, const AvgArgs &aa, int32_t n_iter,
                        int64_t n_slots, int64_t n_dist, size_t smem, void *stream);

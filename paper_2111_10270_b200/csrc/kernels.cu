@@ -2089,6 +2089,22 @@ __global__ void add_deferred_kernel(int64_t n, T *__restrict__ lambda, T *__rest
   }
 }
 
+// The outstanding deferred term of the lifted bound (A7), sum over a tile's
+// slots of min(delta_bar, 0), added to the tile's partial after an energy
+// sweep (fdog_set_state with a non-zero delta_bar).  One warp per tile;
+// padding slots hold 0.
+template <typename T>
+__global__ void __launch_bounds__(256) lb_deferred_kernel(const TileDesc *__restrict__ tiles, int32_t n_tiles,
+                                                          const T *__restrict__ delta, double *__restrict__ lb_part) {
+  const int lane = threadIdx.x & 31;
+  const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (t >= n_tiles) return;
+  const TileDesc d = tiles[t];
+  double acc = 0.0;
+  for (int64_t q = lane; q < (int64_t)d.K * d.lanes; q += 32) acc += (double)fmin(delta[d.slot_base + q], T(0));
+  acc = warp_sum(acc);
+  if (lane == 0) lb_part[t] += acc;
+}
 
 // ---------------------------------------------------------------------------
 // Non-deferred min-marginal averaging (oracle_pass_seq).  The
@@ -2418,6 +2434,17 @@ int launch_add_deferred(int precision, int64_t n, void *lambda, void *delta, voi
     add_deferred_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, (double *)lambda, (double *)delta);
   else
     add_deferred_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, (float *)lambda, (float *)delta);
+  return (int)cudaGetLastError();
+}
+
+int launch_lb_deferred(int precision, const TileDesc *tiles, int32_t n_tiles, const void *delta, double *lb_part,
+                       void *stream) {
+  if (n_tiles <= 0) return 0;
+  const int block = 256, grid = (int)(((int64_t)n_tiles * 32 + block - 1) / block);
+  if (precision == 64)
+    lb_deferred_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(tiles, n_tiles, (const double *)delta, lb_part);
+  else
+    lb_deferred_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(tiles, n_tiles, (const float *)delta, lb_part);
   return (int)cudaGetLastError();
 }
 

@@ -78,11 +78,11 @@ struct fdog_solver {
   bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
   bool chunk_mode = false;   // ... or sweep_chunk_kernel (every tile an arc-mask tile)
   bool rc = false;           // recompute design (Plan::rc): no distance traffic, no dist_state
-  bool dbar_zero = true;
+  bool dbar_zero = true;     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
   int32_t ell_v = 4;         // averaging: ELL variables per thread (experiment knob FDOG_AVG_V)
   int32_t ell_local = 0;     // averaging: consecutive variables per thread (experiment knob FDOG_AVG_LOCAL)
   int32_t csr_first = 1;     // averaging: CSR section in the first blocks (experiment knob FDOG_AVG_CSR_FIRST)
-  bool get_direct = true;    // getters: widen to fp64 on the device, one D2H (FDOG_GET_DIRECT=0: host widening)     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
+  bool get_direct = true;    // getters: widen to fp64 on the device, one D2H (FDOG_GET_DIRECT=0: host widening)
   // non-deferred variant (fdog_pass_seq): level schedule, built on first use
   bool seq_ready = false;
   std::vector<int64_t> seq_lvl[2];        // [backward, forward]: level boundaries in pass order
@@ -1058,18 +1058,26 @@ fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, u
   const int64_t passes0 = s->passes;
   const bool dirty0 = s->lb_dirty, dz0 = s->dbar_zero;
   const size_t pb = (size_t)std::max(s->n_tiles, 1) * sizeof(double), lbb = 2 * sizeof(double);
+  // (with record_mm also the min-marginals, so fdog_min_marginals after the
+  // rounding returns those of the restored state's last pass)
+  std::vector<void *> live = {s->d_lambda, s->d_delta[0], s->d_delta[1], s->d_dist, s->d_lb_part, s->d_lb};
+  std::vector<size_t> sz = {sb, sb, sb, db, pb, lbb};
+  if (s->record_mm) {
+    live.push_back(s->d_m0);
+    live.push_back(s->d_m1);
+    sz.push_back(sb);
+    sz.push_back(sb);
+  }
   if (!o->keep_state) {
-    void *p[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    const size_t sz[6] = {sb, sb, sb, db, pb, lbb};
-    void *src[6] = {s->d_lambda, s->d_delta[0], s->d_delta[1], s->d_dist, s->d_lb_part, s->d_lb};
-    for (int q = 0; q < 6; ++q) {
-      cudaError_t e = cudaMalloc(&p[q], sz[q]);
+    for (size_t q = 0; q < live.size(); ++q) {
+      void *pq = nullptr;
+      cudaError_t e = cudaMalloc(&pq, sz[q]);
       if (e != cudaSuccess) {
         cleanup();
         return cuda_fail(e, "cudaMalloc (primal snapshot)");
       }
-      snap.push_back(p[q]);
-      e = cudaMemcpyAsync(p[q], src[q], sz[q], cudaMemcpyDeviceToDevice, s->stream);
+      snap.push_back(pq);
+      e = cudaMemcpyAsync(pq, live[q], sz[q], cudaMemcpyDeviceToDevice, s->stream);
       if (e != cudaSuccess) {
         cleanup();
         return cuda_fail(e, "snapshot");
@@ -1078,9 +1086,8 @@ fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, u
   }
   auto restore = [&]() -> fdog_status {
     if (o->keep_state) return FDOG_OK;
-    void *dst[6] = {s->d_lambda, s->d_delta[0], s->d_delta[1], s->d_dist, s->d_lb_part, s->d_lb};
-    const size_t sz[6] = {sb, sb, sb, db, pb, lbb};
-    for (int q = 0; q < 6; ++q) CK(cudaMemcpyAsync(dst[q], snap[q], sz[q], cudaMemcpyDeviceToDevice, s->stream), "restore");
+    for (size_t q = 0; q < live.size(); ++q)
+      CK(cudaMemcpyAsync(live[q], snap[q], sz[q], cudaMemcpyDeviceToDevice, s->stream), "restore");
     CK(cudaStreamSynchronize(s->stream), "sync");
     s->cur = cur0;
     s->dist_state = ds0;
@@ -1441,6 +1448,7 @@ fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
     s->launches += 1;
     s->passes += 2 * (int64_t)n_iter;
     s->lb_dirty = true;
+    s->dbar_zero = false;
     return FDOG_OK;
   }
   // CUDA graph of one iteration: used when the passes alternate normally, no
@@ -1480,6 +1488,7 @@ fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
     s->passes += 2 * (int64_t)n_iter;
     s->dist_state = 0;
     s->lb_dirty = true;  // the replayed sweeps wrote new per-tile partials
+    s->dbar_zero = false;
     return FDOG_OK;
   }
   for (int32_t t = 0; t < n_iter; ++t) {
@@ -1626,7 +1635,14 @@ fdog_status fdog_set_state(fdog_solver *s, const double *lambda, const double *d
     for (int64_t q = 0; q < len && z; ++q) z = delta[q] == 0.0;
     s->dbar_zero = z;
   }
-  return energy(s);
+  if ((st = energy(s))) return st;
+  if (!s->dbar_zero) {
+    // the lifted bound (A7) keeps the outstanding sum_slots min(delta_bar, 0)
+    Timed t(s, kKLbReduce);
+    const int e = launch_lb_deferred(s->precision, s->d_tiles, s->n_tiles, s->d_delta[s->cur], s->d_lb_part, s->stream);
+    if (e) return cuda_fail((cudaError_t)e, "lb_deferred launch");
+  }
+  return FDOG_OK;
 }
 
 fdog_status fdog_debug_trace(fdog_solver *s, uint64_t *out, int64_t cap, int64_t *n) {

@@ -79,3 +79,18 @@ def test_round_primal_workloads(oracle_mod, monkeypatch, mode):
         assert np.array_equal(g.lam(), lam) and g.lower_bound() == lb  # state restored
         g.iterate(2, 0.5)  # and the solver continues from it
         assert g.lower_bound() >= lb - 1e-5 * max(1.0, abs(lb))
+
+
+def test_round_primal_restores_min_marginals():
+    """keep_state = 0 restores the recorded min-marginals too (record_mm), so
+    fdog_min_marginals after the rounding returns those of the restored last pass."""
+    p = synth.gm_worms_like(15, n_src=30, k_cand=4, knn=4)
+    g = F.Solver(p, precision=64, record_mm=True)
+    g.iterate(10, 0.5)
+    m0, m1 = g.min_marginals()
+    try:
+        g.round_primal(seed=3, max_rounds=200)
+    except F.FastdogError as e:   # no consensus: the state is restored all the same
+        assert e.code == 8
+    a0, a1 = g.min_marginals()
+    assert np.array_equal(a0, m0) and np.array_equal(a1, m1)

@@ -94,6 +94,32 @@ def test_seq_state_errors():
     assert e.value.code == 1
 
 
+def test_seq_state_errors_after_iterate(monkeypatch):
+    """The pending-correction guard also holds after fdog_iterate's fused
+    single-CTA launch and after a graph-replayed iterate that follows a finalize
+    (the replay path must mark delta_bar as pending too)."""
+    p = synth.spec_two_constraint()
+    monkeypatch.setenv("FDOG_FUSED", "1")
+    g = F.Solver(p, precision=64)
+    assert g.stats()["fused_small"] >= 1
+    g.iterate(2, 0.5)
+    with pytest.raises(F.FastdogError) as e:
+        g.pass_seq(True, 0.5)
+    assert e.value.code == 6
+    g.finalize()
+    g.pass_seq(True, 0.5)
+    monkeypatch.setenv("FDOG_FUSED", "0")
+    monkeypatch.setenv("FDOG_SWEEP", "tma")
+    h = F.Solver(p, precision=64)
+    assert h.stats()["fused_small"] == 0
+    h.iterate(2, 0.5)            # captures the graph
+    h.finalize()
+    h.iterate(2, 0.5)            # replays it
+    with pytest.raises(F.FastdogError) as e:
+        h.pass_seq(True, 0.5)
+    assert e.value.code == 6
+
+
 def test_seq_fp32_bound(oracle_mod):
     """fp32 build: the bound after 20 sequential iterations within 1e-4 relative."""
     p = synth.gm_worms_like(45, n_src=80, k_cand=6, knn=8)
