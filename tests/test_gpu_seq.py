@@ -98,7 +98,7 @@ def test_seq_state_errors_after_iterate(monkeypatch):
     """The pending-correction guard also holds after fdog_iterate's fused
     single-CTA launch and after a graph-replayed iterate that follows a finalize
     (the replay path must mark delta_bar as pending too)."""
-    p = synth.spec_two_constraint()
+    p = synth.lap(synth.LAP4_LITERAL)  # narrow (partitions <= 2 nodes): fused-eligible
     monkeypatch.setenv("FDOG_FUSED", "1")
     g = F.Solver(p, precision=64)
     assert g.stats()["fused_small"] >= 1
