@@ -67,6 +67,11 @@ typedef struct {
   const char *nccl_library; /* path of libnccl.so.2 to dlopen (NULL: default)   */
   void *stream;             /* cudaStream_t to run on; NULL: solver-owned stream */
   int32_t host_threads;     /* threads for host BDD compilation (<= 0: all)    */
+  const int32_t *row_owner; /* optional (world > 1): rank of every row, length
+                               n_cons, identical on every rank; NULL: the
+                               locality-aware sharder (bundles of rows joined by
+                               |J_i| = 2 variables, ordered by their shared
+                               variables, cut by BDD node count) */
 } fdog_options;
 
 /* Sizes of this rank's part of the problem. */
@@ -107,7 +112,7 @@ void fdog_default_options(fdog_options *opts);
 /* ---- host setup (no GPU needed) -------------------------------------- */
 /* Compile every row of this rank's shard into a quasi-reduced ordered BDD
  * (host compiler "B") and pack them into
- * the device layout.  Only opts->rank, world, host_threads are read. */
+ * the device layout.  Only opts->rank, world, host_threads, row_owner are read. */
 fdog_status fdog_plan_create(const fdog_problem *p, const fdog_options *opts, fdog_plan **out);
 void fdog_plan_destroy(fdog_plan *plan);
 fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out);

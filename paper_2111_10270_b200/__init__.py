@@ -57,7 +57,8 @@ class Options(C.Structure):
     _fields_ = [("precision", C.c_int32), ("device", C.c_int32), ("clamp", C.c_double),
                 ("record_mm", C.c_int32), ("profile", C.c_int32), ("rank", C.c_int32),
                 ("world", C.c_int32), ("nccl_unique_id", C.c_void_p), ("nccl_library", C.c_char_p),
-                ("stream", C.c_void_p), ("host_threads", C.c_int32)]
+                ("stream", C.c_void_p), ("host_threads", C.c_int32),
+                ("row_owner", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -192,7 +193,7 @@ class _ProblemArrays:
 
 
 def make_options(precision=32, device=0, clamp=0.0, record_mm=False, profile=False, rank=0, world=1,
-                 nccl_unique_id=None, nccl_library=None, stream=None, host_threads=0):
+                 nccl_unique_id=None, nccl_library=None, stream=None, host_threads=0, row_owner=None):
     lib = load()
     o = Options()
     lib.fdog_default_options(C.byref(o))
@@ -211,16 +212,21 @@ def make_options(precision=32, device=0, clamp=0.0, record_mm=False, profile=Fal
     o.nccl_library = o._lib
     o.stream = stream
     o.host_threads = int(host_threads)
+    o._owner = None
+    if row_owner is not None:
+        o._owner = np.ascontiguousarray(row_owner, dtype=np.int32)
+        o.row_owner = o._owner.ctypes.data
     return o
 
 
 class Plan:
     """Host-side compiled + packed problem (no GPU needed)."""
 
-    def __init__(self, problem, rank=0, world=1, host_threads=0, precision=32):
+    def __init__(self, problem, rank=0, world=1, host_threads=0, precision=32, row_owner=None):
         lib = load()
         self._pa = _ProblemArrays(problem)
-        self._opts = make_options(precision=precision, rank=rank, world=world, host_threads=host_threads)
+        self._opts = make_options(precision=precision, rank=rank, world=world, host_threads=host_threads,
+                                  row_owner=row_owner)
         h = C.c_void_p()
         _check(lib.fdog_plan_create(C.byref(self._pa.struct), C.byref(self._opts), C.byref(h)),
                "fdog_plan_create")
@@ -293,11 +299,11 @@ class Solver:
 
     def __init__(self, problem=None, *, plan: Plan | None = None, precision=32, device=0, clamp=0.0,
                  record_mm=False, profile=False, rank=0, world=1, nccl_unique_id=None,
-                 nccl_library=None, stream=None, host_threads=0):
+                 nccl_library=None, stream=None, host_threads=0, row_owner=None):
         lib = load()
         self._lib = lib
         self._opts = make_options(precision, device, clamp, record_mm, profile, rank, world,
-                                  nccl_unique_id, nccl_library, stream, host_threads)
+                                  nccl_unique_id, nccl_library, stream, host_threads, row_owner)
         h = C.c_void_p()
         if plan is not None:
             _check(lib.fdog_create_from_plan(plan._h, C.byref(self._opts), C.byref(h)),

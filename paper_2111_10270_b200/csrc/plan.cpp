@@ -243,17 +243,94 @@ static fdog_status validate(const fdog_problem *p, int threads) {
   return FDOG_OK;
 }
 
-// Contiguous row ranges with (approximately) equal total row length.
-static void shard_rows(const fdog_problem *p, int world, std::vector<int32_t> &owner) {
+// Locality-aware sharder.  The only coupling
+// between BDDs is the per-variable average of P:641, so the exchange vector is
+// the set of variables whose subproblems land on more than one rank.
+//  1. Bundles: rows joined by a variable held by exactly two rows (|J_i| = 2:
+//     an MRF edge's or a QAP pair's y variables) are united
+//     (union-find; the root of a component is its smallest row).  Such a
+//     variable is never exchanged if its bundle stays on one rank.
+//  2. A bundle heavier than total / (4 world) nodes (e.g. cell tracking, where
+//     transitions chain every frame to the next) is dissolved into its rows.
+//  3. Units (bundles or dissolved rows) are ordered by a locality key: for a
+//     bundle the smallest index of its variables with |J_i| != 2 (the
+//     variables it shares with other bundles -- pixels, QAP assignment
+//     variables, graph-matching labels); for a dissolved row its smallest
+//     variable index.  Ties: the unit's smallest row.
+//  4. The ordered units are cut into `world` ranges of equal BDD node count
+//     (the rank whose share contains a unit's midpoint owns it).
+// Deterministic: every rank derives the same map from the same problem.
+static void shard_rows(const fdog_problem *p, int world, const std::vector<int32_t> &deg,
+                       const std::vector<int64_t> &weight, std::vector<int32_t> &owner) {
   owner.assign(p->n_cons, 0);
   if (world <= 1 || p->n_cons == 0) return;
-  const int64_t total = p->row_ptr[p->n_cons];
-  for (int32_t j = 0; j < p->n_cons; ++j) {
-    // the rank whose share contains the row's midpoint
-    int64_t mid2 = p->row_ptr[j] + p->row_ptr[j + 1];  // 2 * midpoint
-    int64_t r = total > 0 ? (mid2 * world) / (2 * total) : 0;
-    owner[j] = (int32_t)std::min<int64_t>(std::max<int64_t>(r, 0), world - 1);
+  const int32_t m = p->n_cons;
+  std::vector<int32_t> parent(m);
+  for (int32_t j = 0; j < m; ++j) parent[j] = j;
+  auto find = [&](int32_t x) {
+    while (parent[x] != x) {
+      parent[x] = parent[parent[x]];
+      x = parent[x];
+    }
+    return x;
+  };
+  {
+    std::vector<int32_t> first(p->n_vars, -1);
+    for (int32_t j = 0; j < m; ++j)
+      for (int64_t q = p->row_ptr[j]; q < p->row_ptr[j + 1]; ++q) {
+        const int32_t i = p->col_var[q];
+        if (deg[i] != 2) continue;
+        if (first[i] < 0) {
+          first[i] = j;
+          continue;
+        }
+        int32_t a = find(first[i]), b = find(j);
+        if (a == b) continue;
+        if (a > b) std::swap(a, b);
+        parent[b] = a;  // the smaller row is the root
+      }
   }
+  std::vector<int32_t> root(m);
+  std::vector<int64_t> compw(m, 0);
+  int64_t total = 0;
+  for (int32_t j = 0; j < m; ++j) {
+    root[j] = find(j);
+    compw[root[j]] += weight[j];
+    total += weight[j];
+  }
+  if (total <= 0) return;
+  const int64_t cap = std::max<int64_t>(1, total / (4 * (int64_t)world));
+  // unit of each row, and per unit: key, weight (unit ids are row indices)
+  std::vector<int32_t> unit(m);
+  std::vector<int64_t> kext(m, INT64_MAX), kall(m, INT64_MAX), uw(m, 0);
+  for (int32_t j = 0; j < m; ++j) {
+    const bool dissolve = compw[root[j]] > cap;
+    const int32_t u = dissolve ? j : root[j];
+    unit[j] = u;
+    uw[u] += weight[j];
+    for (int64_t q = p->row_ptr[j]; q < p->row_ptr[j + 1]; ++q) {
+      const int32_t i = p->col_var[q];
+      kall[u] = std::min<int64_t>(kall[u], i);
+      if (!dissolve && deg[i] != 2) kext[u] = std::min<int64_t>(kext[u], i);
+    }
+  }
+  std::vector<int32_t> units;
+  for (int32_t j = 0; j < m; ++j)
+    if (unit[j] == j) units.push_back(j);
+  auto key = [&](int32_t u) { return kext[u] != INT64_MAX ? kext[u] : kall[u]; };
+  std::sort(units.begin(), units.end(), [&](int32_t a, int32_t b) {
+    const int64_t ka = key(a), kb = key(b);
+    return ka != kb ? ka < kb : a < b;
+  });
+  std::vector<int32_t> rank_of(m, 0);
+  int64_t acc = 0;
+  for (int32_t u : units) {
+    const int64_t mid2 = 2 * acc + uw[u];  // 2 * midpoint
+    const int64_t r = (mid2 * world) / (2 * total);
+    rank_of[u] = (int32_t)std::min<int64_t>(std::max<int64_t>(r, 0), world - 1);
+    acc += uw[u];
+  }
+  for (int32_t j = 0; j < m; ++j) owner[j] = rank_of[unit[j]];
 }
 
 // Pad a 4-byte array to a multiple of 16 bytes: every tile's topology and
@@ -402,7 +479,6 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     }
 
   tm.mark("copy + validate");
-  shard_rows(p, world, P.owner);
   // global |J_i| and the free-variable term (A13)
   P.deg_global.assign(p->n_vars, 0);
   par_for(nnz, threads, [&](int, int64_t a, int64_t b) {
@@ -412,17 +488,16 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   for (int32_t i = 0; i < p->n_vars; ++i)
     if (P.deg_global[i] == 0 && P.cost[i] < 0) P.free_term += P.cost[i];
 
-  tm.mark("shard + degrees");
-  // local rows, dedupe by signature, compile unique signatures in parallel
+  tm.mark("degrees");
+  // dedupe every non-empty row by signature (the sharder weighs rows by node
+  // count, so with world > 1 all shapes are compiled, not only local ones)
   P.row_shape.assign(p->n_cons, -1);
   P.local_rows.clear();
   std::unordered_map<uint64_t, std::vector<int32_t>> sig;
   for (int32_t j = 0; j < p->n_cons; ++j) {
-    if (P.owner[j] != rank) continue;
     int64_t a = p->row_ptr[j];
     int32_t k = (int32_t)(p->row_ptr[j + 1] - a);
     if (k == 0) continue;
-    P.local_rows.push_back(j);
     const int32_t *c = p->col_coef + a;
     uint64_t h = signature_hash(k, c, p->rel[j], p->rhs[j]);
     auto &cands = sig[h];
@@ -497,6 +572,25 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   }
 
   tm.mark("dedupe + compile");
+  if (o && o->row_owner && world > 1) {  // caller-supplied row -> rank map
+    P.owner.assign(o->row_owner, o->row_owner + p->n_cons);
+    for (int32_t j = 0; j < p->n_cons; ++j)
+      if (P.owner[j] < 0 || P.owner[j] >= world) {
+        set_error("row_owner[%d] = %d outside [0, %d)", j, P.owner[j], world);
+        return FDOG_EINVAL;
+      }
+  } else {
+    std::vector<int64_t> wt(p->n_cons, 0);
+    for (int32_t j = 0; j < p->n_cons; ++j)
+      if (P.row_shape[j] >= 0) wt[j] = P.shapes[P.row_shape[j]].nodes();
+    shard_rows(p, world, P.deg_global, wt, P.owner);
+  }
+  for (int32_t j = 0; j < p->n_cons; ++j)
+    if (P.row_shape[j] >= 0) {
+      if (P.owner[j] == rank) P.local_rows.push_back(j);
+      else P.row_shape[j] = -1;
+    }
+  tm.mark("shard");
   // ---------------------------------------------------------------- packing
   P.max_hops = 0;
   P.max_width = 0;
