@@ -5,8 +5,9 @@
 
 A step = one iteration of Alg. parallel-MMA: averaging -> forward
 pass -> averaging -> backward pass, each pass with its bound.  Workload at N=1:
-BASELINE.json configs[1] (synthetic graph matching shaped like 'worms'), fp32
-sweeps (north_star target).  L2 (126 MB) is flushed before every timed step;
+BASELINE.json configs[2] (synthetic Potts MRF shaped like 'color-seg-n8', 131.8 M
+BDD nodes: the largest single-GPU configuration the metric is quoted on "at
+1/2/4/8 B200"), fp32 sweeps (north_star target).  L2 (126 MB) is flushed before every timed step;
 each step is timed with CUDA events on the solver's stream and the step times
 are summed (max over ranks for N > 1).
 
@@ -14,7 +15,13 @@ value   = BDD arcs relaxed per second = 2 * nodes * 2 passes * steps / time (P:2
 e2e     = same metric through the public C ABI with host buffers: upload of the
           packed plan (H2D) + K x (iterate(1) + lower_bound D2H) + get_lambda D2H.
 roofline: the sweep kernels' algorithmic bytes per launch over
-          their CUDA-event launch time vs MEASURED_PEAKS.json hbm_gbs.
+          their CUDA-event launch time vs MEASURED_PEAKS.json hbm_gbs; traffic =
+          ncu dram__bytes_read.sum + dram__bytes_write.sum per sweep launch,
+          measured by this run (an ncu subprocess replaying one iteration of the
+          same workload) when ncu is available.
+per_hop_latency_ns: sweep time / partitions on the thin-hop microbench (one
+          at-most-one row over 10^4 variables) and on QAP50's 50-partition rows
+          (SURVEY §8(d)).
 cpu_baseline / --impl reference: the fp64 oracle (oracle/, test infrastructure)
           timed as it stands on the host cores, on a bounded sample.
 """
@@ -57,6 +64,107 @@ def _workload(name):
     if name == "thin_hop":
         return synth.thin_hop(0)
     raise SystemExit(f"unknown workload {name}")
+
+
+TARGETS = os.path.join(ROOT, "bench_targets.json")
+
+
+def _frozen_target(name):
+    """time-to-LB target: the fp64 bound after 1000 iterations,
+    recorded once per (workload, seed) by scripts/make_ttl_targets.py."""
+    try:
+        with open(TARGETS) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+def _ncu_traffic(workload, prec, timeout=600):
+    """DRAM bytes per sweep launch of this workload, measured now: ncu (cold
+    caches, as after the bench's L2 flush) on a subprocess that builds the same
+    solver and runs warm-up + one iteration; the last forward and backward sweep
+    launches are averaged.  None if ncu is missing or fails."""
+    import shutil
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu is None or os.environ.get("FDOG_UNDER_NCU"):
+        return None
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "-k", "regex:sweep_kernel", "--csv", "--clock-control", "none", "-c", "40",
+           sys.executable, os.path.abspath(__file__), "--probe-traffic", "--workload", workload]
+    if prec == 64:
+        cmd.append("--fp64")
+    try:
+        env = dict(os.environ, FDOG_UNDER_NCU="1")
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env).stdout
+    except Exception:
+        return None
+    import csv
+    import io
+    rows = [r for r in csv.reader(io.StringIO(out[out.find('"ID"'):])) if r]
+    if not rows:
+        return None
+    hdr = rows[0]
+    try:
+        iid, iname, imet, ival, iunit = (hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name",
+                                                              "Metric Value", "Metric Unit"))
+    except ValueError:
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+             "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
+    per = {}
+    for r in rows[1:]:
+        if len(r) <= max(iid, ival) or "sweep_kernel" not in r[iname]:
+            continue
+        v = float(r[ival].replace(",", "")) * scale.get(r[iunit], 1.0)
+        d = per.setdefault(int(r[iid]), {"name": r[iname]})
+        d[r[imet]] = v
+    import re
+    # sweep_kernel<T, MODE, ...>: MODE 0 forward, 1 backward (2, 3: distance-only sweeps)
+    passes = [d for _, d in sorted(per.items()) if re.search(r"sweep_kernel<\w+, [01][,>]", d["name"])]
+    last = passes[-2:]
+    if not last:
+        return None
+    tb = [d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0) for d in last]
+    return {"bytes_per_launch": sum(tb) / len(tb),
+            "read_per_launch": sum(d.get("dram__bytes_read.sum", 0.0) for d in last) / len(last),
+            "write_per_launch": sum(d.get("dram__bytes_write.sum", 0.0) for d in last) / len(last),
+            "ncu_launch_us": [1e6 * d.get("gpu__time_duration.sum", 0.0) for d in last],
+            "launches": len(last)}
+
+
+def _probe_traffic(args):
+    """ncu child of _ncu_traffic: build the bench's solver, warm up, one iteration."""
+    import paper_2111_10270_b200 as F
+    problem = _workload(args.workload)
+    prec = 64 if args.fp64 else 32
+    s = F.Solver(problem, precision=prec, device=0)
+    s.iterate(2, OMEGA)
+    s.iterate(1, OMEGA)
+    s.lower_bound()
+    s.close()
+
+
+def _hop_latency(F, local, stream, prec):
+    """Per-partition sweep latency: the thin-hop microbench (a
+    single BDD over 10^4 variables: one lane's dependent chain) and QAP50 (every
+    row 50 partitions long).  ns = mean sweep launch time / partitions per row."""
+    out = {}
+    for name, prob in (("thin_hop", synth.thin_hop(0)), ("qap50", synth.qap(0, 50))):
+        s = F.Solver(prob, precision=prec, device=local, stream=stream.cuda_stream)
+        s.iterate(3, OMEGA)
+        s.profile_enable(True)
+        s.profile_reset()
+        s.iterate(5, OMEGA)
+        prof = s.profile()
+        st = s.stats()
+        s.close()
+        hops = st["max_hops"]
+        ent = {"partitions_per_row": hops, "rows": st["bdds"]}
+        for k in ("sweep_forward", "sweep_backward"):
+            if k in prof and prof[k]["launches"]:
+                ent[k.split("_")[1] + "_ns"] = 1e6 * prof[k]["ms"] / prof[k]["launches"] / hops
+        out[name] = ent
+    return out
 
 
 def _peaks():
@@ -151,22 +259,30 @@ def run_reference(args):
     o = oracle.Oracle(problem)
     nodes = o.total_nodes()
     arcs_per_iter = 2 * nodes * 2
-    # bounded: each step is one full oracle iteration of the workload
+    # bounded: each step is one full oracle iteration of the workload; the
+    # timed steps stop early once `--ref-budget` seconds of CPU work are spent
+    # (MRF: ~1.6 s per fp64 iteration on 16 cores), so the run ends in minutes
+    t_start = time.perf_counter()
     for _ in range(args.warmup):
         o.iterate(1, OMEGA)
+        if time.perf_counter() - t_start > args.ref_budget / 4:
+            break
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
         o.iterate(1, OMEGA)
         times.append(time.perf_counter() - t0)
+        if sum(times) > args.ref_budget:
+            break
     tot = sum(times)
-    v = arcs_per_iter * args.steps / tot
+    v = arcs_per_iter * len(times) / tot
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": problem.name, "nodes": nodes, "omega": OMEGA},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": o.threads, "kind": "oracle",
-                             "sample": f"{args.steps} full oracle iterations after {args.warmup} warm-up",
+                             "sample": f"{len(times)} timed full oracle iterations (of {args.steps} requested; "
+                                       f"capped at {args.ref_budget:.0f} s of CPU work) after the warm-up",
                              "cpu": _cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -308,12 +424,10 @@ def run_gpu(args):
     sw_bytes = next(iter(sweep.values()))["bytes_per_launch"] if sweep else 0.0
     achieved = sw_bytes / (sw_ms / sw_n * 1e-3) / 1e9 if sw_n else 0.0
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "sweep_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(problem.name + f"/fp{prec}")
-        except Exception:
-            traffic = None
+    traffic_detail = None
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic_detail = _ncu_traffic(args.workload, prec)
+        traffic = traffic_detail["bytes_per_launch"] if traffic_detail else None
     # SURVEY §8(d) byte models of one sweep launch (per pass: store 16 B/node +
     # 20 B/slot, minimal/recompute 8 B/node + 20 B/slot, fp32), the same launch
     # time: the bandwidth a design moving those bytes would need (bytes_per_launch
@@ -335,6 +449,9 @@ def run_gpu(args):
     e2e = None
     if not args.no_e2e:
         runs, parts = [], []
+        # the caller-owned pinned host buffer get_lambda fills (allocated once,
+        # outside the timed runs, as an application would keep it)
+        lam_buf = torch.empty(st["slots"], dtype=torch.float64, pin_memory=True).numpy()
         for _rep in range(3):
             torch.cuda.synchronize()
             if world > 1:
@@ -346,7 +463,7 @@ def run_gpu(args):
                 s2.iterate(1, OMEGA)
                 s2.lower_bound()  # D2H of the step's result (8 bytes)
             t2 = time.perf_counter()
-            lam = s2.lam()
+            lam = s2.lam(out=lam_buf)
             el = time.perf_counter() - t0
             if world > 1:
                 t = torch.tensor([el], dtype=torch.float64, device=tdev)
@@ -365,19 +482,25 @@ def run_gpu(args):
                "d2h_bytes_per_step": int(8 + lam.nbytes / args.steps),
                "runs": runs, "parts": parts,
                "includes": "per run: device allocation + H2D upload of the packed plan, K x (iterate(1) + "
-                           "lower_bound D2H), get_lambda D2H; value = median of the runs"}
+                           "lower_bound D2H), get_lambda D2H into a caller-owned pinned buffer; "
+                           "value = median of the runs"}
 
     # time-to-LB (BASELINE metric): target = fp64 bound after 1000
     # iterations; fp32 solver from scratch, bound sampled every 10 iterations
     # (the D2H read of the bound is inside the timed interval)
     ttl = None
     if not args.no_ttl and world == 1:
-        plan64 = F.Plan(problem, precision=64)
-        ref = F.Solver(plan=plan64, precision=64, device=local, stream=stream.cuda_stream)
-        lb0_64 = ref.lower_bound()
-        ref.iterate(1000, OMEGA)
-        target = ref.lower_bound()
-        ref.close()
+        frozen = _frozen_target(problem.name)
+        if frozen is not None:
+            lb0_64, target, tsrc = frozen["lb0_fp64"], frozen["lb_1000_fp64"], "bench_targets.json (frozen)"
+        else:
+            plan64 = F.Plan(problem, precision=64)
+            ref = F.Solver(plan=plan64, precision=64, device=local, stream=stream.cuda_stream)
+            lb0_64 = ref.lower_bound()
+            ref.iterate(1000, OMEGA)
+            target = ref.lower_bound()
+            ref.close()
+            tsrc = "computed in this run (no frozen entry)"
         thr = lb0_64 + 0.99 * (target - lb0_64)
         s3 = F.Solver(plan=plan, precision=prec, device=local, stream=stream.cuda_stream)
         torch.cuda.synchronize()
@@ -390,7 +513,7 @@ def run_gpu(args):
         el = time.perf_counter() - t0
         s3.close()
         ttl = {"seconds": el, "iterations": its, "reached": bool(cur_lb >= thr), "lb0": lb0_64,
-               "target_lb_1000_fp64": target, "threshold": thr, "lb": cur_lb,
+               "target_lb_1000_fp64": target, "target_source": tsrc, "threshold": thr, "lb": cur_lb,
                "definition": "wall time from the first iterate until LB >= LB0 + 0.99 (LB*_1000 - LB0), "
                              "bound sampled every 10 iterations"}
 
@@ -427,6 +550,10 @@ def run_gpu(args):
                               "lb": cur_lb, "threshold": ttl["threshold"], "sampled_every": 2},
                "deferred_time_to_lb": {"seconds": ttl["seconds"], "iterations": ttl["iterations"]}}
 
+    hop = None
+    if rank == 0 and world == 1 and not args.no_hop:
+        hop = _hop_latency(F, local, stream, prec)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = _cpu_baseline(problem, 2 * 2 * st["nodes"], budget_s=args.cpu_budget)
@@ -444,10 +571,11 @@ def run_gpu(args):
                        "l2": "flushed before every timed step (256 MB write + 256 MB read, untimed)",
                        "plan_s": round(plan_s, 3)},
             "iters_per_s": iters_s,
-            "per_hop_latency_ns": (1e6 * sw_ms / sw_n / st["max_hops"]) if sw_n else None,
+            "per_hop_latency_ns": hop,
             "lower_bound": {"initial": lb0, "after": lb, "iterations": args.warmup + args.steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "sweep_forward+sweep_backward",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_ncu": traffic_detail,
+                         "kernel": "sweep_forward+sweep_backward",
                          "bytes_per_launch": sw_bytes, "peak_kind": peak_kind,
                          "launch_us": 1e3 * sw_ms / sw_n if sw_n else None,
                          "design": "recompute" if st.get("sweep_recompute") else "store",
@@ -483,7 +611,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="gm_worms_like")
+    ap.add_argument("--workload", default="mrf_potts")
     ap.add_argument("--fp64", action="store_true")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
                     help="N > 1: shared variables by ncclAllReduce or through peer memory (CUDA IPC)")
@@ -493,7 +621,15 @@ def main():
     ap.add_argument("--seq-compare", action="store_true",
                     help="also time the non-deferred variant (per iteration and to the time-to-LB threshold)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=120.0,
+                    help="--impl reference: seconds of timed oracle work at most")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic subprocess")
+    ap.add_argument("--no-hop", action="store_true", help="skip the per-partition latency probes")
+    ap.add_argument("--probe-traffic", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.probe_traffic:
+        _probe_traffic(args)
+        return
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -366,17 +366,22 @@ class Solver:
         _check(self._lib.fdog_slot_index(self._h, _ptr(con), _ptr(pos), n), "fdog_slot_index")
         return con[:n], pos[:n]
 
-    def _get(self, fn):
+    def _get(self, fn, out=None):
         n = self.num_slots()
-        out = np.empty(max(n, 1), np.float64)
+        if out is None:
+            out = np.empty(max(n, 1), np.float64)
+        elif out.dtype != np.float64 or not out.flags.c_contiguous or out.size < n:
+            raise ValueError("out: a contiguous float64 array of at least num_slots() elements")
         _check(getattr(self._lib, fn)(self._h, _ptr(out), n), fn)
         return out[:n]
 
-    def lam(self):
-        return self._get("fdog_get_lambda")
+    def lam(self, out=None):
+        """Current lambda per slot (canonical order); `out` (optional): a
+        caller-owned float64 buffer to fill, e.g. pinned host memory."""
+        return self._get("fdog_get_lambda", out)
 
-    def deferred(self):
-        return self._get("fdog_get_deferred")
+    def deferred(self, out=None):
+        return self._get("fdog_get_deferred", out)
 
     def min_marginals(self):
         n = self.num_slots()

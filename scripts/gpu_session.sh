@@ -1,7 +1,7 @@
 #!/bin/bash
 # Full GPU session: build, GPU tests, smoke, default bench (with CPU baseline,
 # e2e, time-to-LB), per-workload bench lines, ncu launch list + full capture.
-# Usage: scripts/gpu_round2.sh TAG [full]
+# Usage: scripts/gpu_session.sh TAG [full]
 set -u
 TAG=${1:-r1}
 OUT=gpurun_out; mkdir -p $OUT
@@ -10,7 +10,7 @@ python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1 ||
 timeout 1200 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest gpu rc=$?"; tail -3 $OUT/pytest_gpu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -1 $OUT/smoke_$TAG.log
 timeout 900 python bench.py --steps 50 --warmup 5 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"; cat $OUT/bench_$TAG.json; tail -3 $OUT/bench_$TAG.err
-for w in ${WORKLOADS:-mrf_potts celltrack qap50 qap128 lap4 thin_hop}; do
+for w in ${WORKLOADS:-gm_worms_like celltrack qap50 qap128 lap4 thin_hop}; do
 timeout 900 python bench.py --steps 30 --warmup 5 --no-cpu --workload $w > $OUT/bench_${TAG}_$w.json 2> $OUT/bench_${TAG}_$w.err; echo "bench $w rc=$?"; python -c "
 import json; d=json.load(open('$OUT/bench_${TAG}_$w.json'))
 print('$w value %.3e ms/step %.4f roof %.3f' % (d['value'], d['ms_per_step'], d['roofline']['frac']), {k: round(v['ms']/v['launches']*1e3,2) for k,v in d['kernels'].items()})" || tail -5 $OUT/bench_${TAG}_$w.err

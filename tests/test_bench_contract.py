@@ -64,3 +64,8 @@ def test_gpu_arm_line():
     e = d["e2e"]
     assert e["value"] > 0 and len(e["runs"]) == 3 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["config"]["workload"].startswith("qap")
+    # DRAM traffic measured by this run (ncu subprocess) and per-partition latency probes
+    assert rf["traffic"] is not None and rf["traffic"] > 0, rf.get("traffic_ncu")
+    hop = d["per_hop_latency_ns"]
+    assert hop["thin_hop"]["partitions_per_row"] == 10_000 and hop["thin_hop"]["forward_ns"] > 0
+    assert hop["qap50"]["partitions_per_row"] == 50 and hop["qap50"]["backward_ns"] > 0

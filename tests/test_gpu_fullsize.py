@@ -4,10 +4,14 @@ workloads besides GM (GM: test_gpu_parity.py::test_full_size_gm_*).
 
 - CellTrack (configs[3], 9.7 M nodes) and QAP n=50 (configs[4], 12.1 M nodes):
   every slot of lambda after one iteration against the oracle (fp64), the
-  bound after 20 iterations; fp64 builds every slot at 1e-9.
-- MRF Potts (configs[2], 131.8 M nodes) and QAP n=128 (the 8-GPU stress
-  configuration, 530.7 M nodes, on one GPU; the oracle would need minutes and
-  tens of GB): sampled.  The first pass from the initial state has
+  bound after 100 iterations (north_star's fp32 claim); fp64 builds every slot
+  at 1e-9 for two iterations.
+- MRF Potts (configs[2], 131.8 M nodes; the bench workload): fp64 every slot of
+  lambda and delta_bar plus the bound after each of two whole iterations at
+  1e-9 (the oracle holds ~10 GB and runs ~1.6 s per iteration on 16 cores);
+  fp32 every slot after two iterations, the bound after 20.
+- MRF and QAP n=128 (the 8-GPU stress configuration, 530.7 M nodes, on one
+  GPU; its oracle would need tens of GB): first passes sampled.  The first pass from the initial state has
   delta_bar = 0, so avg_i = 0 and every BDD is updated independently
   of the others; the oracle run on a sub-problem made of sampled rows,
   with costs rescaled so that the initial lambda = c_i / |J_i| is the
@@ -51,8 +55,8 @@ def test_full_size_fp32(oracle_mod, full_problem):
     o.iterate(1, 0.5)
     assert _err(g.lam(), o.lam(), 1e-5, s) <= 0
     assert _err(g.deferred(), o.deferred(), 1e-5, s) <= 0
-    g.iterate(19, 0.5)
-    o.iterate(19, 0.5)
+    g.iterate(99, 0.5)
+    o.iterate(99, 0.5)
     assert abs(g.lower_bound() - o.lower_bound()) <= 1e-4 * abs(o.lower_bound())
 
 
@@ -66,6 +70,33 @@ def test_full_size_fp64(oracle_mod, full_problem):
         o.iterate(1, 0.5)
         assert _err(g.lam(), o.lam(), 1e-9, s) <= 0
         assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+
+
+def test_full_size_mrf(oracle_mod):
+    """MRF Potts 300x400x8 (BASELINE configs[2], the bench workload) in bench.py's
+    launch configuration: fp64 every slot of lambda and delta_bar and the bound
+    after each of 2 whole iterations at 1e-9; fp32 every slot after 2 iterations
+    at 1e-5 and the bound after 20 within 1e-4 relative; node/arc counts exact."""
+    p = synth.mrf_potts(0)
+    s = _s(p)
+    o = oracle_mod.Oracle(p)
+    g64 = F.Solver(p, precision=64)
+    st = g64.stats()
+    assert st["nodes"] == o.total_nodes() == 131_789_344 and st["arcs"] == 2 * o.total_nodes()
+    for _ in range(2):
+        g64.iterate(1, 0.5)
+        o.iterate(1, 0.5)
+        assert _err(g64.lam(), o.lam(), 1e-9, s) <= 0
+        assert _err(g64.deferred(), o.deferred(), 1e-9, s) <= 0
+        assert abs(g64.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+    g64.close()
+    g32 = F.Solver(p, precision=32)
+    g32.iterate(2, 0.5)
+    assert _err(g32.lam(), o.lam(), 1e-5, s) <= 0
+    assert _err(g32.deferred(), o.deferred(), 1e-5, s) <= 0
+    g32.iterate(18, 0.5)
+    o.iterate(18, 0.5)
+    assert abs(g32.lower_bound() - o.lower_bound()) <= 1e-4 * abs(o.lower_bound())
 
 
 def sub_problem(p, rows):
