@@ -1,21 +1,27 @@
 #!/bin/bash
-# Full GPU session: build, GPU tests, smoke, default bench (with CPU baseline,
-# e2e, time-to-LB), per-workload bench lines, ncu launch list + full capture.
-# Usage: scripts/gpu_session.sh TAG [full]
+# Full GPU session: build, GPU tests, smoke, default bench (MRF; with CPU
+# baseline, e2e, time-to-LB, in-run ncu traffic), per-workload bench lines,
+# ncu launch list (+ optional full capture of the sweep and averaging kernels).
+# Usage: scripts/gpu_session.sh TAG [full]     env: WORKLOADS, SKIP_TESTS=1, TTL=1
 set -u
-TAG=${1:-r1}
+TAG=${1:-r2}
 OUT=gpurun_out; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu_$TAG.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1 || { echo BUILD FAILED; tail -30 $OUT/build_$TAG.log; exit 1; }
-timeout 1200 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest gpu rc=$?"; tail -3 $OUT/pytest_gpu_$TAG.log
+if [ "${TTL:-0}" = "1" ]; then timeout 900 python scripts/make_ttl_targets.py > $OUT/ttl_$TAG.log 2>&1; echo "ttl rc=$?"; cp bench_targets.json $OUT/bench_targets.json; fi
+if [ "${SKIP_TESTS:-0}" != "1" ]; then
+timeout 2400 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest gpu rc=$?"; tail -3 $OUT/pytest_gpu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -1 $OUT/smoke_$TAG.log
-timeout 900 python bench.py --steps 50 --warmup 5 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"; cat $OUT/bench_$TAG.json; tail -3 $OUT/bench_$TAG.err
+fi
+timeout 1200 python bench.py --steps 50 --warmup 5 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"; cut -c1-1500 $OUT/bench_$TAG.json; tail -3 $OUT/bench_$TAG.err
 for w in ${WORKLOADS:-gm_worms_like celltrack qap50 qap128 lap4 thin_hop}; do
-timeout 900 python bench.py --steps 30 --warmup 5 --no-cpu --workload $w > $OUT/bench_${TAG}_$w.json 2> $OUT/bench_${TAG}_$w.err; echo "bench $w rc=$?"; python -c "
+timeout 900 python bench.py --steps 30 --warmup 5 --no-cpu --no-hop --workload $w > $OUT/bench_${TAG}_$w.json 2> $OUT/bench_${TAG}_$w.err; echo "bench $w rc=$?"; python -c "
 import json; d=json.load(open('$OUT/bench_${TAG}_$w.json'))
-print('$w value %.3e ms/step %.4f roof %.3f' % (d['value'], d['ms_per_step'], d['roofline']['frac']), {k: round(v['ms']/v['launches']*1e3,2) for k,v in d['kernels'].items()})" || tail -5 $OUT/bench_${TAG}_$w.err
+print('$w value %.3e ms/step %.4f roof %.3f traffic %s' % (d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['traffic']), {k: round(v['ms']/v['launches']*1e3,2) for k,v in d['kernels'].items()})" || tail -5 $OUT/bench_${TAG}_$w.err
 done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-ttl > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-ttl --no-traffic --no-hop > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
 if [ "${2:-}" = "full" ]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel|avg_kernel" -s 8 -c 4 -o $OUT/prof_$TAG python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-ttl > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
+  for w in ${FULL_WORKLOADS:-mrf_potts}; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel|avg_kernel" -s 12 -c 3 -o $OUT/prof_${TAG}_$w python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-ttl --no-traffic --no-hop --workload $w > $OUT/ncu_full_${TAG}_$w.log 2>&1; echo "ncu full $w rc=$?"
+  done
 fi
