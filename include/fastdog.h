@@ -102,6 +102,9 @@ typedef struct {
                                       2: same, state resident in shared memory         */
   int32_t sweep_recompute;         /* 1: the passes recompute the opposite-direction
                                       distances on chip (no per-node HBM traffic)     */
+  int64_t tile_pairs;              /* variables with |J_i| = 2 whose two slots share a
+                                      tile: averaged on chip by the sweep (solver: only
+                                      when the sweep path supports it; plan: eligible) */
 } fdog_stats_t;
 
 typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */

@@ -64,7 +64,9 @@ struct TileDesc {
   int32_t max_w;    // widest partition of the tile
   int32_t lanes;    // L
   int32_t rec_base; // kind bit 2: first hop record, in 16-byte units of Plan::recs
-  int32_t pad_[2];  // 64 bytes: fetched as four 16-byte cp.async chunks
+  int32_t pair_base; // tile-closed pairs: partner map at Plan::pair_map[pair_base + h*L + lane]
+                     // (0xFFFF: the slot's average comes from the averaging kernel); -1: none
+  int32_t pad_;     // 64 bytes: fetched as four 16-byte cp.async chunks
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc layout");
 
@@ -123,7 +125,7 @@ FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (kWarpHeader + NB * SB +
 // creating a solver is one allocation and one host->device copy.
 enum ImageSection {
   kImTiles = 0, kImHopOff, kImTopo, kImSlotVar, kImVarPtr, kImVarSlots, kImVarXidx, kImDegList, kImEll, kImEllVar,
-  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImRecs, kImCanon, kImCount
+  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImRecs, kImCanon, kImPairs, kImCount
 };
 
 struct HostImage {
@@ -166,6 +168,9 @@ struct Plan {
   std::vector<int32_t> deg_list;    // |J_i| (global) per var_list entry
   std::vector<int32_t> ell;         // ELL part: slot pairs (second -1 if |J_i| = 1)
   std::vector<int32_t> ell_var;     // ELL part: the variables
+  int64_t n_ell_open = 0;           // ELL entries [0, n_ell_open) are averaged by the kernel; the rest
+                                    // are tile-closed pairs the sweep averages on chip (pair_map)
+  std::vector<uint16_t> pair_map;   // per tile with closed pairs (TileDesc::pair_base): partner offsets
   std::vector<int32_t> ell4;        // ELL-4 part (|J_i| = 3, 4): slot quads, -1 padded
   std::vector<int32_t> ell4_var;
   std::vector<int32_t> col_coef;    // copy of the rows (feasibility checks of primal labelings)
@@ -211,7 +216,10 @@ struct SweepArgs {
   const unsigned char *recs;  // hop records of arc-mask tiles
   const int32_t *slot_var;
   void *lambda;          // T*
-  void *delta_out;       // T*: per slot avg_i in, delta out (in place)
+  void *delta_out;       // T*: per slot delta out
+  const void *avg_in;    // T*: per slot avg_i in (== delta_out: in place; else the delta_bar buffer
+                         // holding avg_i for averaged slots and delta_bar for tile-closed pairs)
+  const uint16_t *pairs; // tile-closed pair maps (null: none)
   void *m0, *m1;         // T*, recorded min-marginals (may be null)
   double omega, clamp;
   double *lb_part;       // per tile bound contribution (reduced by lb_reduce_kernel)

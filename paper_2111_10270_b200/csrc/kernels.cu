@@ -951,7 +951,7 @@ __device__ __forceinline__ void issue_stage(const SweepArgs &a, const TileDesc &
   const uint32_t hop_b = masks ? 0u : (uint32_t)stage_hop_bytes(d.K);
   mbar_expect_tx(bar, lam_b + va_b + dist_b + topo_b + hop_b);
   bulk_g2s(s.lam, reinterpret_cast<const T *>(a.lambda) + d.slot_base, lam_b, bar);
-  if (va_b) bulk_g2s(s.va, reinterpret_cast<const T *>(a.delta_out) + d.slot_base, va_b, bar);
+  if (va_b) bulk_g2s(s.va, reinterpret_cast<const T *>(a.avg_in) + d.slot_base, va_b, bar);
   if (!RC) bulk_g2s(s.dist, reinterpret_cast<const T *>(a.dist) + d.dist_base, dist_b, bar);
   if (masks) {
     if (topo_b) bulk_g2s(s.topo, a.recs + 16 * (int64_t)d.rec_base, topo_b, bar);
@@ -1082,6 +1082,23 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
       const Stage<T> s = stage_at<T, RC>(b ? sbuf1 : sbuf0, d);
       mbar_wait(&bar[b], (phase >> b) & 1u);
       phase ^= 1u << b;
+      if (kUpd && a.pairs && d.pair_base >= 0) {
+        // tile-closed pairs (|J_i| = 2, both slots in this tile; plan.cpp): the
+        // stage holds their delta_bar; avg_i = (delta_bar_1 + delta_bar_2) / 2
+        // (A1 -- the averaging kernel's ELL arithmetic), written into
+        // both slots by the lane holding the lower tile offset
+        const uint16_t *__restrict__ pm = a.pairs + d.pair_base;
+        const int n = K * d.lanes;
+        for (int i = lane; i < n; i += 32) {
+          const int m = __ldg(pm + i);
+          if (m != 0xFFFF && i < m) {
+            const T v = (s.va[i] + s.va[m]) / T(2);
+            s.va[i] = v;
+            s.va[m] = v;
+          }
+        }
+        __syncwarp();
+      }
       if (d.kind & 4) {
         // arc-mask tile (narrow shape, shared topology)
         if (active) {

@@ -243,28 +243,24 @@ static fdog_status validate(const fdog_problem *p, int threads) {
   return FDOG_OK;
 }
 
-// Locality-aware sharder.  The only coupling
-// between BDDs is the per-variable average of P:641, so the exchange vector is
-// the set of variables whose subproblems land on more than one rank.
+// Row bundles and their locality order (used by the sharder and by the tile
+// packer).  The only coupling between BDDs is the per-variable average of
+// P:641.
 //  1. Bundles: rows joined by a variable held by exactly two rows (|J_i| = 2:
 //     an MRF edge's or a QAP pair's y variables) are united
-//     (union-find; the root of a component is its smallest row).  Such a
-//     variable is never exchanged if its bundle stays on one rank.
+//     (union-find; the root of a component is its smallest row).
 //  2. A bundle heavier than total / (4 world) nodes (e.g. cell tracking, where
 //     transitions chain every frame to the next) is dissolved into its rows.
-//  3. Units (bundles or dissolved rows) are ordered by a locality key: for a
-//     bundle the smallest index of its variables with |J_i| != 2 (the
-//     variables it shares with other bundles -- pixels, QAP assignment
-//     variables, graph-matching labels); for a dissolved row its smallest
-//     variable index.  Ties: the unit's smallest row.
-//  4. The ordered units are cut into `world` ranges of equal BDD node count
-//     (the rank whose share contains a unit's midpoint owns it).
-// Deterministic: every rank derives the same map from the same problem.
-static void shard_rows(const fdog_problem *p, int world, const std::vector<int32_t> &deg,
-                       const std::vector<int64_t> &weight, std::vector<int32_t> &owner) {
-  owner.assign(p->n_cons, 0);
-  if (world <= 1 || p->n_cons == 0) return;
+//  3. Units (bundles or dissolved rows) get a locality key: for a bundle the
+//     smallest index of its variables with |J_i| != 2 (the variables it shares
+//     with other bundles -- pixels, QAP assignment variables, graph-matching
+//     labels); for a dissolved row its smallest variable index.
+// unit[j]: the unit of row j (a row index); ukey[u]: the key of unit u.
+static void bundle_units(const fdog_problem *p, int world, const std::vector<int32_t> &deg,
+                         const std::vector<int64_t> &weight, std::vector<int32_t> &unit, std::vector<int64_t> &ukey) {
   const int32_t m = p->n_cons;
+  unit.assign(m, 0);
+  ukey.assign(m, INT64_MAX);
   std::vector<int32_t> parent(m);
   for (int32_t j = 0; j < m; ++j) parent[j] = j;
   auto find = [&](int32_t x) {
@@ -298,29 +294,45 @@ static void shard_rows(const fdog_problem *p, int world, const std::vector<int32
     compw[root[j]] += weight[j];
     total += weight[j];
   }
-  if (total <= 0) return;
-  const int64_t cap = std::max<int64_t>(1, total / (4 * (int64_t)world));
-  // unit of each row, and per unit: key, weight (unit ids are row indices)
-  std::vector<int32_t> unit(m);
-  std::vector<int64_t> kext(m, INT64_MAX), kall(m, INT64_MAX), uw(m, 0);
+  const int64_t cap = std::max<int64_t>(1, total / (4 * (int64_t)std::max(world, 1)));
+  std::vector<int64_t> kext(m, INT64_MAX);
   for (int32_t j = 0; j < m; ++j) {
     const bool dissolve = compw[root[j]] > cap;
     const int32_t u = dissolve ? j : root[j];
     unit[j] = u;
-    uw[u] += weight[j];
     for (int64_t q = p->row_ptr[j]; q < p->row_ptr[j + 1]; ++q) {
       const int32_t i = p->col_var[q];
-      kall[u] = std::min<int64_t>(kall[u], i);
+      ukey[u] = std::min<int64_t>(ukey[u], i);
       if (!dissolve && deg[i] != 2) kext[u] = std::min<int64_t>(kext[u], i);
     }
   }
+  for (int32_t u = 0; u < m; ++u)
+    if (kext[u] != INT64_MAX) ukey[u] = kext[u];
+}
+
+// Locality-aware sharder: the units of
+// bundle_units ordered by (key, smallest row) and cut into `world` ranges of
+// equal BDD node count (the rank whose share contains a unit's midpoint owns
+// it).  A bundle's |J_i| = 2 variables never cross ranks.  Deterministic:
+// every rank derives the same map from the same problem.
+static void shard_rows(const fdog_problem *p, int world, const std::vector<int32_t> &unit,
+                       const std::vector<int64_t> &ukey, const std::vector<int64_t> &weight,
+                       std::vector<int32_t> &owner) {
+  owner.assign(p->n_cons, 0);
+  if (world <= 1 || p->n_cons == 0) return;
+  const int32_t m = p->n_cons;
+  std::vector<int64_t> uw(m, 0);
+  int64_t total = 0;
+  for (int32_t j = 0; j < m; ++j) {
+    uw[unit[j]] += weight[j];
+    total += weight[j];
+  }
+  if (total <= 0) return;
   std::vector<int32_t> units;
   for (int32_t j = 0; j < m; ++j)
     if (unit[j] == j) units.push_back(j);
-  auto key = [&](int32_t u) { return kext[u] != INT64_MAX ? kext[u] : kall[u]; };
   std::sort(units.begin(), units.end(), [&](int32_t a, int32_t b) {
-    const int64_t ka = key(a), kb = key(b);
-    return ka != kb ? ka < kb : a < b;
+    return ukey[a] != ukey[b] ? ukey[a] < ukey[b] : a < b;
   });
   std::vector<int32_t> rank_of(m, 0);
   int64_t acc = 0;
@@ -579,11 +591,19 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         set_error("row_owner[%d] = %d outside [0, %d)", j, P.owner[j], world);
         return FDOG_EINVAL;
       }
-  } else {
+  }
+  // bundles + locality keys: the sharder's units, and the row order inside a
+  // shape's tiles (rows of one bundle in consecutive lanes, so that a bundle's
+  // |J_i| = 2 variables have both slots in one tile: the sweep averages them
+  // on chip)
+  std::vector<int32_t> unit;
+  std::vector<int64_t> ukey;
+  {
     std::vector<int64_t> wt(p->n_cons, 0);
     for (int32_t j = 0; j < p->n_cons; ++j)
       if (P.row_shape[j] >= 0) wt[j] = P.shapes[P.row_shape[j]].nodes();
-    shard_rows(p, world, P.deg_global, wt, P.owner);
+    bundle_units(p, world, P.deg_global, wt, unit, ukey);
+    if (!(o && o->row_owner && world > 1)) shard_rows(p, world, unit, ukey, wt, P.owner);
   }
   for (int32_t j = 0; j < p->n_cons; ++j)
     if (P.row_shape[j] >= 0) {
@@ -603,9 +623,18 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     P.n_nodes += S.nodes();
     P.n_slots += S.k;
   }
-  // group rows by shape (ascending j inside a group)
+  // group rows by shape, in locality order inside a group: (bundle key,
+  // bundle, j) -- a bundle's rows of one shape land in consecutive lanes
   std::vector<std::vector<int32_t>> by_shape(P.shapes.size());
   for (int32_t j : P.local_rows) by_shape[P.row_shape[j]].push_back(j);
+  par_for((int64_t)by_shape.size(), threads, [&](int, int64_t a, int64_t b) {
+    for (int64_t sh = a; sh < b; ++sh)
+      std::sort(by_shape[sh].begin(), by_shape[sh].end(), [&](int32_t x, int32_t y) {
+        const int32_t ux = unit[x], uy = unit[y];
+        if (ukey[ux] != ukey[uy]) return ukey[ux] < ukey[uy];
+        return ux != uy ? ux < uy : x < y;
+      });
+  });
 
   // ---- per-warp shared-memory budget: every tile's stage buffer
   // must fit SB and its distance arrays DB; a shape whose BDDs are too long for
@@ -1093,43 +1122,73 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // averaging layout: variables with <= 2 local slots that are not exchanged
   // keep their slot pair inline (ELL, one 8-byte load), with 3-4 the slot quad
   // (ELL-4); the rest stay in CSR.  (Per chunk counts, then the fill.)
+  // Tile-closed pairs: a variable with |J_i| = 2 whose two slots lie in one
+  // staged tile (a bundle's rows in consecutive lanes) is averaged by the sweep
+  // on chip (pair maps below); its ELL entry goes to the tail of the ELL list
+  // (after P.n_ell_open), used only by paths that average every variable
+  // (FDOG_PAIRS=0 keeps every pair in the averaging kernel).
   {
     const int64_t nv = (int64_t)P.var_list.size();
+    const char *pe = getenv("FDOG_PAIRS");
+    const bool pairs_ok = !(pe && pe[0] == '0');
+    auto tile_of = [&](int64_t slot) -> int32_t {  // tiles are emitted in slot order
+      int32_t lo = 0, hi = (int32_t)P.tiles.size() - 1;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi + 1) >> 1;
+        if (P.tiles[mid].slot_base <= slot) lo = mid;
+        else hi = mid - 1;
+      }
+      return lo;
+    };
+    auto closed = [&](int64_t q) {
+      if (!pairs_ok || P.var_xidx[q] >= 0 || P.var_ptr[q + 1] - P.var_ptr[q] != 2) return false;
+      const int32_t t = tile_of(P.var_slots[P.var_ptr[q]]);
+      const TileDesc &d = P.tiles[t];
+      return t == tile_of(P.var_slots[P.var_ptr[q] + 1]) && (d.kind & 2) && (int64_t)d.K * d.lanes < 0xFFFF;
+    };
     auto cat = [&](int64_t q) {
       const int64_t d = P.var_ptr[q + 1] - P.var_ptr[q];
-      return P.var_xidx[q] >= 0 ? 2 : d <= 2 ? 0 : d <= 4 ? 1 : 2;
+      if (P.var_xidx[q] >= 0) return 2;
+      if (d <= 2) return closed(q) ? 4 : 0;
+      return d <= 4 ? 1 : 2;
     };
     const int T = par_chunks(nv, threads);
-    std::vector<std::array<int64_t, 4>> cc(T + 1, {0, 0, 0, 0});  // ell, ell4, csr vars, csr slots
+    std::vector<std::array<int64_t, 5>> cc(T + 1, {0, 0, 0, 0, 0});  // ell, ell4, csr vars, csr slots, closed pairs
     par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
-      std::array<int64_t, 4> m = {0, 0, 0, 0};
+      std::array<int64_t, 5> m = {0, 0, 0, 0, 0};
       for (int64_t q = a; q < b; ++q) {
         const int k = cat(q);
-        m[k]++;
+        m[k == 4 ? 4 : k]++;
         if (k == 2) m[3] += P.var_ptr[q + 1] - P.var_ptr[q];
       }
       cc[c + 1] = m;
     });
     for (int c = 0; c < T; ++c)
-      for (int u = 0; u < 4; ++u) cc[c + 1][u] += cc[c][u];
+      for (int u = 0; u < 5; ++u) cc[c + 1][u] += cc[c][u];
     const auto &tot = cc[T];
-    P.ell.assign(2 * tot[0], -1);
-    P.ell_var.resize(tot[0]);
+    P.n_ell_open = tot[0];
+    P.ell.assign(2 * (tot[0] + tot[4]), -1);
+    P.ell_var.resize(tot[0] + tot[4]);
     P.ell4.assign(4 * tot[1], -1);
     P.ell4_var.resize(tot[1]);
     std::vector<int32_t> csr_list(tot[2]), csr_slots(tot[3]), csr_x(tot[2]);
     std::vector<int64_t> csr_ptr(tot[2] + 1, 0);
     csr_ptr[tot[2]] = tot[3];
     par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
-      std::array<int64_t, 4> o = cc[c];
+      std::array<int64_t, 5> o = cc[c];
+      o[4] += tot[0];  // closed pairs after the open ones
       for (int64_t q = a; q < b; ++q) {
         const int64_t p0 = P.var_ptr[q], p1 = P.var_ptr[q + 1];
-        switch (cat(q)) {
+        const int k = cat(q);
+        switch (k) {
           case 0:
-            P.ell[2 * o[0]] = P.var_slots[p0];
-            if (p1 - p0 == 2) P.ell[2 * o[0] + 1] = P.var_slots[p0 + 1];
-            P.ell_var[o[0]++] = P.var_list[q];
+          case 4: {
+            const int u = k;
+            P.ell[2 * o[u]] = P.var_slots[p0];
+            if (p1 - p0 == 2) P.ell[2 * o[u] + 1] = P.var_slots[p0 + 1];
+            P.ell_var[o[u]++] = P.var_list[q];
             break;
+          }
           case 1:
             for (int64_t u = 0; u < p1 - p0; ++u) P.ell4[4 * o[1] + u] = P.var_slots[p0 + u];
             P.ell4_var[o[1]++] = P.var_list[q];
@@ -1142,6 +1201,51 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         }
       }
     });
+    // pair maps: per staged tile with closed pairs, the partner of each slot
+    // (offset within the tile, 0xFFFF: none), identical maps stored once
+    P.pair_map.clear();
+    for (auto &d : P.tiles) d.pair_base = -1;
+    {
+      std::unordered_map<uint64_t, std::vector<int32_t>> seen;
+      std::vector<uint16_t> cur;
+      int32_t ct = -1;
+      auto flush_map = [&]() {
+        if (ct < 0) return;
+        uint64_t h = 1469598103934665603ull;
+        for (uint16_t v : cur) h = (h ^ v) * 1099511628211ull;
+        auto &cands = seen[h];
+        int32_t at = -1;
+        for (int32_t c0 : cands)
+          if (std::equal(cur.begin(), cur.end(), P.pair_map.begin() + c0)) {
+            at = c0;
+            break;
+          }
+        if (at < 0) {
+          at = (int32_t)P.pair_map.size();
+          P.pair_map.insert(P.pair_map.end(), cur.begin(), cur.end());
+          while (P.pair_map.size() % 8) P.pair_map.push_back(0xFFFF);
+          cands.push_back(at);
+        }
+        P.tiles[ct].pair_base = at;
+      };
+      for (int64_t e = tot[0]; e < tot[0] + tot[4]; ++e) {
+        const int64_t s1 = P.ell[2 * e], s2 = P.ell[2 * e + 1];
+        const int32_t t = tile_of(s1);
+        if (t != ct) {
+          flush_map();
+          ct = t;
+          cur.assign((size_t)P.tiles[t].K * P.tiles[t].lanes, 0xFFFF);
+        }
+        const int64_t b0 = P.tiles[t].slot_base;
+        cur[s1 - b0] = (uint16_t)(s2 - b0);
+        cur[s2 - b0] = (uint16_t)(s1 - b0);
+      }
+      flush_map();
+      if (P.pair_map.size() > 0x7fffffffULL) {
+        set_error("pair maps exceed 2^31 entries");
+        return FDOG_ETOOBIG;
+      }
+    }
     P.n_vars_local = nv;
     P.var_list.swap(csr_list);
     P.var_ptr.swap(csr_ptr);
@@ -1193,6 +1297,7 @@ fdog_status build_image(Plan &P) {
   sz[kImDist0] = 0;  // (allocated and initialised on the device, solver.cpp)
   sz[kImRecs] = P.recs.size();
   sz[kImCanon] = P.canon_slot.size() * 4;
+  sz[kImPairs] = P.pair_map.size() * 2;
   size_t at = 0;
   for (int q = 0; q < kImCount; ++q) {
     P.image.off[q] = at;
@@ -1234,6 +1339,7 @@ fdog_status build_image(Plan &P) {
   src[kImXLocal] = P.x_local.data();
   src[kImXDeg] = P.x_deg.data();
   src[kImRecs] = P.recs.data();
+  src[kImPairs] = P.pair_map.data();
   for (int q = 0; q < kImCount; ++q) {
     const size_t end = q + 1 < kImCount ? P.image.off[q + 1] : at;
     memset(P.image.data + P.image.off[q] + sz[q], 0, end - P.image.off[q] - sz[q]);
@@ -1339,6 +1445,7 @@ fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out) {
   out->staged_tiles = (int64_t)P.tiles.size() - P.direct_tiles;
   out->sweep_smem_per_warp = warp_bytes(P.SB, P.DB, P.NB);
   out->h2d_bytes = (int64_t)P.image.bytes;
+  out->tile_pairs = (int64_t)(P.ell.size() / 2) - P.n_ell_open;
   return FDOG_OK;
 }
 

@@ -119,6 +119,13 @@ struct fdog_solver {
   int4 *d_ell4 = nullptr;
   int32_t *d_ell4_var = nullptr;
   int32_t n_ell = 0, n_ell4 = 0, csr_group = 1;
+  // tile-closed pairs (Plan::n_ell_open): the sweep averages them
+  // on chip; the averaging kernel writes the other averages in place into the
+  // delta_bar buffer, the sweep writes delta into the other one
+  int32_t n_ell_open = 0;
+  const uint16_t *d_pairs = nullptr;
+  bool pairs = false;
+  bool avg_full = false;  // (fdog_finalize_averaged: every variable, into the other buffer)
   // primal rounding
   int32_t *d_ell_var = nullptr, *d_csr_var = nullptr;
   uint8_t *d_x = nullptr;
@@ -249,7 +256,11 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.recs = s->d_recs;
   a.slot_var = nullptr;  // (not uploaded)
   a.lambda = s->d_lambda;
-  a.delta_out = s->d_delta[s->cur ^ 1];  // avg_i in (avg_kernel), delta out
+  a.delta_out = s->d_delta[s->cur ^ 1];  // delta out
+  // avg_i in: in place in delta_out, or (tile-closed pairs) the delta_bar
+  // buffer, where the averaging kernel wrote the other averages in place
+  a.avg_in = s->pairs ? s->d_delta[s->cur] : s->d_delta[s->cur ^ 1];
+  a.pairs = s->pairs ? s->d_pairs : nullptr;
   a.m0 = s->d_m0;
   a.m1 = s->d_m1;
   a.omega = omega;
@@ -308,7 +319,8 @@ fdog_status run_peer_exchange(fdog_solver *s) {
 
 AvgArgs avg_args(fdog_solver *s) {
   AvgArgs a{};
-  a.n_ell = s->n_ell;
+  const bool inplace = s->pairs && !s->avg_full;
+  a.n_ell = inplace ? s->n_ell_open : s->n_ell;
   a.ell = s->d_ell;
   a.n_ell4 = s->n_ell4;
   a.ell4 = s->d_ell4;
@@ -323,7 +335,7 @@ AvgArgs avg_args(fdog_solver *s) {
   a.var_xidx = s->world > 1 ? s->d_var_xidx : nullptr;
   a.deg_l = s->d_deg_list;
   a.delta_bar = s->d_delta[s->cur];
-  a.avg_slot = s->d_delta[s->cur ^ 1];
+  a.avg_slot = inplace ? s->d_delta[s->cur] : s->d_delta[s->cur ^ 1];
   a.xbuf = s->d_xbuf;
   return a;
 }
@@ -723,6 +735,10 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
       return FDOG_EINVAL;
     }
   }
+  // tile-closed pairs are averaged by sweep_kernel only (the streaming,
+  // chunked and fused paths read every average from the averaging kernel)
+  s->pairs = P.n_ell_open < (int64_t)(P.ell.size() / 2) && !s->stream_mode && !s->chunk_mode && !s->use_fused &&
+             P.direct_tiles == 0;
   const char *wpb = getenv("FDOG_WPB");  // experiment knob: warps per sweep CTA (default 4, max 16)
   const size_t wmax = wpb ? std::max(1, std::min(16, atoi(wpb))) : 4;
   int warps = (int)std::max<size_t>(1, std::min<size_t>(wmax, (size_t)prop.smem_block / s->warp_bytes));
@@ -774,6 +790,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   fdog_status st;
   s->n_dist = P.n_dist;
   s->n_ell = (int32_t)(P.ell.size() / 2);
+  s->n_ell_open = (int32_t)P.n_ell_open;
   s->n_ell4 = (int32_t)(P.ell4.size() / 4);
   {
     int64_t maxdeg = 1;
@@ -819,6 +836,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_hop_off = (int32_t *)sec(kImHopOff);
   s->d_topo = (uint32_t *)sec(kImTopo);
   s->d_recs = (const unsigned char *)sec(kImRecs);
+  s->d_pairs = (const uint16_t *)sec(kImPairs);
   s->d_canon = (const int32_t *)sec(kImCanon);
   s->d_var_ptr = (int64_t *)sec(kImVarPtr);
   s->d_var_slots = (int32_t *)sec(kImVarSlots);
@@ -922,6 +940,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->st.h2d_bytes = s->upload_bytes;
   s->st.fused_small = s->use_fused ? (s->fused_smem ? 2 : 1) : 0;
   s->st.sweep_recompute = s->rc ? 1 : 0;
+  s->st.tile_pairs = s->pairs ? (int64_t)s->n_ell - s->n_ell_open : 0;
 
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;
@@ -1560,9 +1579,11 @@ fdog_status fdog_finalize_averaged(fdog_solver *s) {
   }
   // the averaging kernel (+ exchange) writes avg_i into every slot of the other
   // delta buffer; lambda += that buffer, then both buffers are zero
+  s->avg_full = true;
   fdog_status st = run_avg(s);
+  if (!st && s->peer && s->n_shared > 0) st = run_peer_exchange(s);
+  s->avg_full = false;
   if (st) return st;
-  if (s->peer && s->n_shared > 0 && (st = run_peer_exchange(s))) return st;
   int e;
   {
     Timed t(s, kKAddDeferred);

@@ -380,6 +380,49 @@ def test_stage_buffers_bitwise(oracle_mod, monkeypatch, mode, name, make):
     assert np.array_equal(gs[0].lam(), gs[1].lam())
 
 
+@pytest.mark.parametrize("mode", ["rc", "tma"])
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("name,make", [
+    ("mrf", lambda: synth.mrf_potts(8, H=20, W=24, L=5)),
+    ("gm", lambda: synth.gm_worms_like(8, n_src=90, k_cand=6, knn=8)),
+    ("qap", lambda: synth.qap(8, n=9)),
+])
+def test_tile_pairs_bitwise(oracle_mod, monkeypatch, mode, precision, name, make):
+    """Tile-closed pairs (|J_i| = 2, both slots in one tile) averaged on chip by
+    the sweep equal the averaging kernel's ELL path bit for bit (same
+    arithmetic, (d1 + d2) / 2): FDOG_PAIRS=0 vs the default, pass by pass and
+    through the graph-replayed iterate; the bound, finalize(averaged) and the
+    oracle (fp64) as well."""
+    p = make()
+    monkeypatch.setenv("FDOG_SWEEP", mode)
+    monkeypatch.setenv("FDOG_FUSED", "0")
+    monkeypatch.setenv("FDOG_PAIRS", "0")
+    g0 = F.Solver(p, precision=precision)
+    monkeypatch.delenv("FDOG_PAIRS")
+    g1 = F.Solver(p, precision=precision)
+    assert g0.stats()["tile_pairs"] == 0 and g1.stats()["tile_pairs"] > 0
+    o = oracle_mod.Oracle(p)
+    s = _s(p)
+    for t in range(4):
+        fwd = t % 2 == 0
+        g0.pass_(fwd, 0.5)
+        g1.pass_(fwd, 0.5)
+        o.pass_(fwd, 0.5)
+        assert np.array_equal(g0.lam(), g1.lam()) and np.array_equal(g0.deferred(), g1.deferred())
+        assert g0.lower_bound() == g1.lower_bound()
+        if precision == 64:
+            assert np.max(np.abs(g1.lam() - o.lam())) <= 1e-9 * s
+    g0.iterate(3, 0.5)
+    g1.iterate(3, 0.5)
+    assert np.array_equal(g0.lam(), g1.lam()) and g0.lower_bound() == g1.lower_bound()
+    g0.finalize(averaged=True)
+    g1.finalize(averaged=True)
+    assert np.array_equal(g0.lam(), g1.lam()) and g0.lower_bound() == g1.lower_bound()
+    g0.iterate(2, 0.5)
+    g1.iterate(2, 0.5)
+    assert np.array_equal(g0.lam(), g1.lam())
+
+
 def test_tile_schedules_bitwise(monkeypatch):
     """Static round-robin, dynamic claims of one tile and batched claims of
     several tiles per atomic give bit-identical iterates and bounds (a BDD's
