@@ -584,7 +584,7 @@ def run_gpu(args):
             "ms_per_step_profiled": float(sum(ms_prof)) / args.steps,
             "solver_stats": {k: st[k] for k in ("tiles", "tiles_shared_topology", "staged_tiles", "sweep_grid",
                                                  "sweep_block", "sweep_smem_per_warp", "sweep_streaming", "sweep_recompute", "padded_slots",
-                                                 "device_bytes", "shapes", "max_hops", "max_width")},
+                                                 "device_bytes", "shapes", "max_hops", "max_width", "tile_pairs")},
             "kernels": prof,
             "gpu_launches": launches,
             "clocks": clocks,
