@@ -64,9 +64,9 @@ struct TileDesc {
   int32_t max_w;    // widest partition of the tile
   int32_t lanes;    // L
   int32_t rec_base; // kind bit 2: first hop record, in 16-byte units of Plan::recs
-  int32_t pair_base; // tile-closed pairs: partner map at Plan::pair_map[pair_base + h*L + lane]
-                     // (0xFFFF: the slot's average comes from the averaging kernel); -1: none
-  int32_t pad_;     // 64 bytes: fetched as four 16-byte cp.async chunks
+  int32_t pair_base; // tile-closed pairs: Plan::pair_list[pair_base .. + n_pairs), each
+                     // (i | m << 16): tile slot offsets i < m of one variable (|J_i| = 2)
+  int32_t n_pairs;   // (64 bytes: fetched as four 16-byte cp.async chunks)
 };
 static_assert(sizeof(TileDesc) == 64, "TileDesc layout");
 
@@ -115,6 +115,8 @@ FDOG_HD int stage_bytes(int tsz, int kind, int K, int nodes, int L) {
 FDOG_HD int stage_bytes_rc(int tsz, int kind, int K, int nodes, int L) {
   return stage_lam_bytes(tsz, K, L) + stage_va_bytes(tsz, K, L) + stage_tail_bytes(tsz, kind, K, nodes, L);
 }
+// tile-closed pair list, staged after the tail (TileDesc::n_pairs entries of 4 bytes)
+FDOG_HD int stage_pairs_bytes(int n_pairs) { return r16(n_pairs * 4); }
 FDOG_HD int relax_slots(int W) { return 3 * (W + 1); }
 FDOG_HD int relax_bytes(int tsz, int W, int L) { return r16(relax_slots(W) * L * tsz); }
 constexpr int kWarpHeader = 256;
@@ -169,8 +171,8 @@ struct Plan {
   std::vector<int32_t> ell;         // ELL part: slot pairs (second -1 if |J_i| = 1)
   std::vector<int32_t> ell_var;     // ELL part: the variables
   int64_t n_ell_open = 0;           // ELL entries [0, n_ell_open) are averaged by the kernel; the rest
-                                    // are tile-closed pairs the sweep averages on chip (pair_map)
-  std::vector<uint16_t> pair_map;   // per tile with closed pairs (TileDesc::pair_base): partner offsets
+                                    // are tile-closed pairs the sweep averages on chip (pair_list)
+  std::vector<uint32_t> pair_list;  // per tile with closed pairs (TileDesc::pair_base, n_pairs)
   std::vector<int32_t> ell4;        // ELL-4 part (|J_i| = 3, 4): slot quads, -1 padded
   std::vector<int32_t> ell4_var;
   std::vector<int32_t> col_coef;    // copy of the rows (feasibility checks of primal labelings)
@@ -219,7 +221,7 @@ struct SweepArgs {
   void *delta_out;       // T*: per slot delta out
   const void *avg_in;    // T*: per slot avg_i in (== delta_out: in place; else the delta_bar buffer
                          // holding avg_i for averaged slots and delta_bar for tile-closed pairs)
-  const uint16_t *pairs; // tile-closed pair maps (null: none)
+  const uint32_t *pairs; // tile-closed pair lists (null: none)
   void *m0, *m1;         // T*, recorded min-marginals (may be null)
   double omega, clamp;
   double *lb_part;       // per tile bound contribution (reduced by lb_reduce_kernel)

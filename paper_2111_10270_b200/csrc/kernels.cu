@@ -916,6 +916,7 @@ struct Stage {
   T *dist;
   uint32_t *topo;
   int32_t *hop;
+  uint32_t *pairs;  // tile-closed pair list (after the tail)
 };
 
 // RC: recompute design, no distances in the stage buffer (internal.h)
@@ -933,6 +934,7 @@ __device__ __forceinline__ Stage<T> stage_at(unsigned char *base, const TileDesc
   s.topo = reinterpret_cast<uint32_t *>(p);
   p += stage_topo_bytes(d.kind, d.nodes, d.lanes);
   s.hop = reinterpret_cast<int32_t *>(p);
+  s.pairs = reinterpret_cast<uint32_t *>(s.topo) + stage_tail_bytes(tsz, d.kind, d.K, d.nodes, d.lanes) / 4;
   return s;
 }
 
@@ -949,7 +951,9 @@ __device__ __forceinline__ void issue_stage(const SweepArgs &a, const TileDesc &
   const uint32_t topo_b = masks ? ((d.kind & 16) ? 0u : (uint32_t)(d.K * rec_bytes((int)sizeof(T))))
                                 : (uint32_t)stage_topo_bytes(d.kind, d.nodes, d.lanes);
   const uint32_t hop_b = masks ? 0u : (uint32_t)stage_hop_bytes(d.K);
-  mbar_expect_tx(bar, lam_b + va_b + dist_b + topo_b + hop_b);
+  const uint32_t pair_b = (upd && a.pairs && d.n_pairs > 0) ? (uint32_t)stage_pairs_bytes(d.n_pairs) : 0u;
+  mbar_expect_tx(bar, lam_b + va_b + dist_b + topo_b + hop_b + pair_b);
+  if (pair_b) bulk_g2s(s.pairs, a.pairs + d.pair_base, pair_b, bar);
   bulk_g2s(s.lam, reinterpret_cast<const T *>(a.lambda) + d.slot_base, lam_b, bar);
   if (va_b) bulk_g2s(s.va, reinterpret_cast<const T *>(a.avg_in) + d.slot_base, va_b, bar);
   if (!RC) bulk_g2s(s.dist, reinterpret_cast<const T *>(a.dist) + d.dist_base, dist_b, bar);
@@ -1082,20 +1086,18 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
       const Stage<T> s = stage_at<T, RC>(b ? sbuf1 : sbuf0, d);
       mbar_wait(&bar[b], (phase >> b) & 1u);
       phase ^= 1u << b;
-      if (kUpd && a.pairs && d.pair_base >= 0) {
+      if (kUpd && a.pairs && d.n_pairs > 0) {
         // tile-closed pairs (|J_i| = 2, both slots in this tile; plan.cpp): the
         // stage holds their delta_bar; avg_i = (delta_bar_1 + delta_bar_2) / 2
         // (A1 -- the averaging kernel's ELL arithmetic), written into
-        // both slots by the lane holding the lower tile offset
-        const uint16_t *__restrict__ pm = a.pairs + d.pair_base;
-        const int n = K * d.lanes;
-        for (int i = lane; i < n; i += 32) {
-          const int m = __ldg(pm + i);
-          if (m != 0xFFFF && i < m) {
-            const T v = (s.va[i] + s.va[m]) / T(2);
-            s.va[i] = v;
-            s.va[m] = v;
-          }
+        // both slots
+#pragma unroll 4
+        for (int e = lane; e < d.n_pairs; e += 32) {
+          const uint32_t w = s.pairs[e];
+          const uint32_t i = w & 0xFFFFu, m = w >> 16;
+          const T v = (s.va[i] + s.va[m]) / T(2);
+          s.va[i] = v;
+          s.va[m] = v;
         }
         __syncwarp();
       }

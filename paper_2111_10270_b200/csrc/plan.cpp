@@ -623,18 +623,50 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     P.n_nodes += S.nodes();
     P.n_slots += S.k;
   }
-  // group rows by shape, in locality order inside a group: (bundle key,
-  // bundle, j) -- a bundle's rows of one shape land in consecutive lanes
+  // group rows by shape (ascending j inside a group), or in bundle order --
+  // (bundle key, bundle, j): a bundle's rows of one shape in consecutive lanes
+  // -- when that puts both rows of at least 90 % of the shape's internal
+  // |J_i| = 2 variables into one 32-row tile (their averages are then
+  // computed on chip by the sweep; e.g. MRF-LP: 16 marginalisation rows per
+  // edge, two edges per tile).  Otherwise the j order is kept: the generators'
+  // families there put a variable's two slots at the same lane of two tiles,
+  // which the averaging kernel reads coalesced (GM, QAP).
   std::vector<std::vector<int32_t>> by_shape(P.shapes.size());
   for (int32_t j : P.local_rows) by_shape[P.row_shape[j]].push_back(j);
-  par_for((int64_t)by_shape.size(), threads, [&](int, int64_t a, int64_t b) {
-    for (int64_t sh = a; sh < b; ++sh)
-      std::sort(by_shape[sh].begin(), by_shape[sh].end(), [&](int32_t x, int32_t y) {
+  std::vector<char> pair_room(P.shapes.size(), 0);  // bundle order: stages reserve room for a pair list
+  {
+    const char *pe = getenv("FDOG_PAIRS");
+    const bool pairs_ok = !(pe && pe[0] == '0');
+    std::vector<int64_t> seen(pairs_ok ? p->n_vars : 0, -1);  // first (row position / 32) of a |J_i| = 2 variable
+    for (size_t sh = 0; sh < by_shape.size() && pairs_ok; ++sh) {
+      auto &rows = by_shape[sh];
+      if (rows.size() < 2) continue;
+      std::vector<int32_t> b = rows;
+      std::sort(b.begin(), b.end(), [&](int32_t x, int32_t y) {
         const int32_t ux = unit[x], uy = unit[y];
         if (ukey[ux] != ukey[uy]) return ukey[ux] < ukey[uy];
         return ux != uy ? ux < uy : x < y;
       });
-  });
+      int64_t inside = 0, same = 0;
+      const int64_t tag = (int64_t)sh << 40;
+      for (size_t r = 0; r < b.size(); ++r)
+        for (int64_t q = p->row_ptr[b[r]]; q < p->row_ptr[b[r] + 1]; ++q) {
+          const int32_t i = p->col_var[q];
+          if (P.deg_global[i] != 2) continue;
+          const int64_t code = tag | (int64_t)(r / 32);
+          if (seen[i] >= 0 && (seen[i] >> 40) == (int64_t)sh) {
+            inside++;
+            same += seen[i] == code;
+          } else {
+            seen[i] = code;
+          }
+        }
+      if (inside > 0 && same >= 0.9 * inside) {
+        rows.swap(b);
+        pair_room[sh] = 1;
+      }
+    }
+  }
 
   // ---- per-warp shared-memory budget: every tile's stage buffer
   // must fit SB and its distance arrays DB; a shape whose BDDs are too long for
@@ -667,13 +699,15 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   auto pack = [&](bool rc, int nb) {
     std::vector<PendingTile> pend;
     P.NB = nbuf ? (atoi(nbuf) == 1 ? 1 : 2) : nb;
-    auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB) {
-      if (rc) return stage_bytes_rc(tsz, kind, K, nodes, L) <= SB && stage_dist_bytes(tsz, nodes, L) <= DB;
-      return stage_bytes(tsz, kind, K, nodes, L) <= SB && relax_bytes(tsz, W, L) <= DB;
+    // pr: the tile may carry a pair list (at most K L / 2 pairs)
+    auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB, bool pr = false) {
+      const int pb = pr ? stage_pairs_bytes(K * L / 2) : 0;
+      if (rc) return stage_bytes_rc(tsz, kind, K, nodes, L) + pb <= SB && stage_dist_bytes(tsz, nodes, L) <= DB;
+      return stage_bytes(tsz, kind, K, nodes, L) + pb <= SB && relax_bytes(tsz, W, L) <= DB;
     };
-    auto lanes_for = [&](int kind, int K, int nodes, int W, int SB, int DB) {
+    auto lanes_for = [&](int kind, int K, int nodes, int W, int SB, int DB, bool pr = false) {
       for (int L = 32; L >= 4; L /= 2)
-        if (fits(kind, K, nodes, W, L, SB, DB)) return L;
+        if (fits(kind, K, nodes, W, L, SB, DB, pr)) return L;
       return 0;
     };
     {
@@ -700,7 +734,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
           if (by_shape[s].empty()) continue;
           const Shape &S = P.shapes[s];
           const int k0 = S.max_w <= 2 ? 4 : 0;  // arc-mask tiles for narrow shapes
-          int L = lanes_for(k0, S.k, S.nodes(), S.max_w, SB, DB);
+          const bool pr = k0 && pair_room[s];
+          int L = lanes_for(k0, S.k, S.nodes(), S.max_w, SB, DB, pr);
           double pen = 1.0;
           if (L == 0) {  // direct from global memory: latency-bound
             L = 32;
@@ -708,7 +743,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
             // that leaves any is a fallback to the store design)
             pen = rc ? 1e6 : 10.0;
           } else {
-            usedSB = std::max(usedSB, rc ? stage_bytes_rc(tsz, k0, S.k, S.nodes(), L) : stage_bytes(tsz, k0, S.k, S.nodes(), L));
+            usedSB = std::max(usedSB, (rc ? stage_bytes_rc(tsz, k0, S.k, S.nodes(), L) : stage_bytes(tsz, k0, S.k, S.nodes(), L)) +
+                                          (pr ? stage_pairs_bytes(S.k * L / 2) : 0));
             if (rc) usedDB = std::max(usedDB, stage_dist_bytes(tsz, S.nodes(), L));
           }
           const double tiles = std::ceil((double)by_shape[s].size() / L);
@@ -738,7 +774,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       auto &rows = by_shape[s];
       const Shape &S = P.shapes[s];
       const int k0 = S.max_w <= 2 ? 4 : 0;
-      int L = lanes_for(k0, S.k, S.nodes(), S.max_w, P.SB, P.DB);
+      int L = lanes_for(k0, S.k, S.nodes(), S.max_w, P.SB, P.DB, k0 && pair_room[s]);
       const bool staged = L > 0;
       if (!staged) L = 32;
       // (rows too long to stage, of a narrow shape: the last tile keeps the
@@ -1140,11 +1176,32 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       }
       return lo;
     };
-    auto closed = [&](int64_t q) {
+    // candidate closed pairs per tile, then the tiles whose stage holds their
+    // pair list within the per-warp budget
+    auto candidate = [&](int64_t q, int32_t *tp) {
       if (!pairs_ok || P.var_xidx[q] >= 0 || P.var_ptr[q + 1] - P.var_ptr[q] != 2) return false;
       const int32_t t = tile_of(P.var_slots[P.var_ptr[q]]);
       const TileDesc &d = P.tiles[t];
-      return t == tile_of(P.var_slots[P.var_ptr[q] + 1]) && (d.kind & 2) && (int64_t)d.K * d.lanes < 0xFFFF;
+      *tp = t;
+      return t == tile_of(P.var_slots[P.var_ptr[q] + 1]) && (d.kind & 2) && (int64_t)d.K * d.lanes <= 0xFFFF;
+    };
+    std::vector<int32_t> tile_pairs(P.tiles.size(), 0);
+    par_for(nv, threads, [&](int, int64_t a, int64_t b) {
+      for (int64_t q = a; q < b; ++q) {
+        int32_t t;
+        if (candidate(q, &t)) __atomic_fetch_add(&tile_pairs[t], 1, __ATOMIC_RELAXED);
+      }
+    });
+    for (size_t t = 0; t < P.tiles.size(); ++t) {
+      const TileDesc &d = P.tiles[t];
+      if (!tile_pairs[t]) continue;
+      const int sb = P.rc ? stage_bytes_rc(tsz, d.kind, d.K, d.nodes, d.lanes)
+                          : stage_bytes(tsz, d.kind, d.K, d.nodes, d.lanes);
+      if (sb + stage_pairs_bytes(tile_pairs[t]) > P.SB) tile_pairs[t] = 0;  // keep them in the kernel
+    }
+    auto closed = [&](int64_t q) {
+      int32_t t;
+      return candidate(q, &t) && tile_pairs[t] > 0;
     };
     auto cat = [&](int64_t q) {
       const int64_t d = P.var_ptr[q + 1] - P.var_ptr[q];
@@ -1201,48 +1258,54 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         }
       }
     });
-    // pair maps: per staged tile with closed pairs, the partner of each slot
-    // (offset within the tile, 0xFFFF: none), identical maps stored once
-    P.pair_map.clear();
-    for (auto &d : P.tiles) d.pair_base = -1;
+    // pair lists: per staged tile with closed pairs, (i | m << 16) for the two
+    // tile slot offsets i < m of each pair, ascending i; identical lists stored
+    // once (every MRF-LP marginalisation tile has the same one)
+    P.pair_list.clear();
+    for (auto &d : P.tiles) {
+      d.pair_base = -1;
+      d.n_pairs = 0;
+    }
     {
-      std::unordered_map<uint64_t, std::vector<int32_t>> seen;
-      std::vector<uint16_t> cur;
+      std::unordered_map<uint64_t, std::vector<std::pair<int32_t, int32_t>>> seen;  // (offset, length)
+      std::vector<uint32_t> cur;
       int32_t ct = -1;
-      auto flush_map = [&]() {
+      auto flush_list = [&]() {
         if (ct < 0) return;
-        uint64_t h = 1469598103934665603ull;
-        for (uint16_t v : cur) h = (h ^ v) * 1099511628211ull;
+        std::sort(cur.begin(), cur.end(), [](uint32_t x, uint32_t y) { return (x & 0xFFFF) < (y & 0xFFFF); });
+        uint64_t h = 1469598103934665603ull ^ cur.size();
+        for (uint32_t v : cur) h = (h ^ v) * 1099511628211ull;
         auto &cands = seen[h];
         int32_t at = -1;
-        for (int32_t c0 : cands)
-          if (std::equal(cur.begin(), cur.end(), P.pair_map.begin() + c0)) {
-            at = c0;
+        for (const auto &c0 : cands)
+          if (c0.second == (int32_t)cur.size() && std::equal(cur.begin(), cur.end(), P.pair_list.begin() + c0.first)) {
+            at = c0.first;
             break;
           }
         if (at < 0) {
-          at = (int32_t)P.pair_map.size();
-          P.pair_map.insert(P.pair_map.end(), cur.begin(), cur.end());
-          while (P.pair_map.size() % 8) P.pair_map.push_back(0xFFFF);
-          cands.push_back(at);
+          at = (int32_t)P.pair_list.size();
+          P.pair_list.insert(P.pair_list.end(), cur.begin(), cur.end());
+          while (P.pair_list.size() % 4) P.pair_list.push_back(0);  // 16-byte aligned lists (TMA)
+          cands.emplace_back(at, (int32_t)cur.size());
         }
         P.tiles[ct].pair_base = at;
+        P.tiles[ct].n_pairs = (int32_t)cur.size();
       };
       for (int64_t e = tot[0]; e < tot[0] + tot[4]; ++e) {
         const int64_t s1 = P.ell[2 * e], s2 = P.ell[2 * e + 1];
         const int32_t t = tile_of(s1);
         if (t != ct) {
-          flush_map();
+          flush_list();
           ct = t;
-          cur.assign((size_t)P.tiles[t].K * P.tiles[t].lanes, 0xFFFF);
+          cur.clear();
         }
         const int64_t b0 = P.tiles[t].slot_base;
-        cur[s1 - b0] = (uint16_t)(s2 - b0);
-        cur[s2 - b0] = (uint16_t)(s1 - b0);
+        const uint32_t i = (uint32_t)(std::min(s1, s2) - b0), m = (uint32_t)(std::max(s1, s2) - b0);
+        cur.push_back(i | (m << 16));
       }
-      flush_map();
-      if (P.pair_map.size() > 0x7fffffffULL) {
-        set_error("pair maps exceed 2^31 entries");
+      flush_list();
+      if (P.pair_list.size() > 0x7fffffffULL) {
+        set_error("pair lists exceed 2^31 entries");
         return FDOG_ETOOBIG;
       }
     }
@@ -1297,7 +1360,7 @@ fdog_status build_image(Plan &P) {
   sz[kImDist0] = 0;  // (allocated and initialised on the device, solver.cpp)
   sz[kImRecs] = P.recs.size();
   sz[kImCanon] = P.canon_slot.size() * 4;
-  sz[kImPairs] = P.pair_map.size() * 2;
+  sz[kImPairs] = P.pair_list.size() * 4;
   size_t at = 0;
   for (int q = 0; q < kImCount; ++q) {
     P.image.off[q] = at;
@@ -1339,7 +1402,7 @@ fdog_status build_image(Plan &P) {
   src[kImXLocal] = P.x_local.data();
   src[kImXDeg] = P.x_deg.data();
   src[kImRecs] = P.recs.data();
-  src[kImPairs] = P.pair_map.data();
+  src[kImPairs] = P.pair_list.data();
   for (int q = 0; q < kImCount; ++q) {
     const size_t end = q + 1 < kImCount ? P.image.off[q + 1] : at;
     memset(P.image.data + P.image.off[q] + sz[q], 0, end - P.image.off[q] - sz[q]);

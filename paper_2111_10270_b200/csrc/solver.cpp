@@ -123,7 +123,7 @@ struct fdog_solver {
   // on chip; the averaging kernel writes the other averages in place into the
   // delta_bar buffer, the sweep writes delta into the other one
   int32_t n_ell_open = 0;
-  const uint16_t *d_pairs = nullptr;
+  const uint32_t *d_pairs = nullptr;
   bool pairs = false;
   bool avg_full = false;  // (fdog_finalize_averaged: every variable, into the other buffer)
   // primal rounding
@@ -836,7 +836,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_hop_off = (int32_t *)sec(kImHopOff);
   s->d_topo = (uint32_t *)sec(kImTopo);
   s->d_recs = (const unsigned char *)sec(kImRecs);
-  s->d_pairs = (const uint16_t *)sec(kImPairs);
+  s->d_pairs = (const uint32_t *)sec(kImPairs);
   s->d_canon = (const int32_t *)sec(kImCanon);
   s->d_var_ptr = (int64_t *)sec(kImVarPtr);
   s->d_var_slots = (int32_t *)sec(kImVarSlots);

@@ -383,16 +383,17 @@ def test_stage_buffers_bitwise(oracle_mod, monkeypatch, mode, name, make):
 @pytest.mark.parametrize("mode", ["rc", "tma"])
 @pytest.mark.parametrize("precision", [64, 32])
 @pytest.mark.parametrize("name,make", [
-    ("mrf", lambda: synth.mrf_potts(8, H=20, W=24, L=5)),
-    ("gm", lambda: synth.gm_worms_like(8, n_src=90, k_cand=6, knn=8)),
-    ("qap", lambda: synth.qap(8, n=9)),
+    ("mrf4", lambda: synth.mrf_potts(8, H=20, W=24, L=4)),
+    ("mrf8", lambda: synth.mrf_potts(8, H=10, W=12, L=8)),
+    ("gm8", lambda: synth.gm_worms_like(8, n_src=60, k_cand=7, knn=6)),
 ])
 def test_tile_pairs_bitwise(oracle_mod, monkeypatch, mode, precision, name, make):
     """Tile-closed pairs (|J_i| = 2, both slots in one tile) averaged on chip by
     the sweep equal the averaging kernel's ELL path bit for bit (same
     arithmetic, (d1 + d2) / 2): FDOG_PAIRS=0 vs the default, pass by pass and
     through the graph-replayed iterate; the bound, finalize(averaged) and the
-    oracle (fp64) as well."""
+    oracle (fp64) as well.  (Instances whose bundles -- 2 L marginalisation
+    rows per edge -- divide a 32-row tile, so the packer picks bundle order.)"""
     p = make()
     monkeypatch.setenv("FDOG_SWEEP", mode)
     monkeypatch.setenv("FDOG_FUSED", "0")
