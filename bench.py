@@ -53,6 +53,8 @@ def _workload(name):
         return synth.gm_worms_like(0)
     if name == "mrf_potts":
         return synth.mrf_potts(0)
+    if name == "mrf_potts_cut":
+        return synth.mrf_potts_cut(0)
     if name == "qap50":
         return synth.qap(0, 50)
     if name == "qap128":

@@ -259,6 +259,38 @@ def mrf_potts(seed=0, H=300, W=400, L=8, conn8=True) -> Problem:
     return rb.build(ybase + E * L * L, cost, f"mrf_potts(seed={seed},{H}x{W}x{L},{'8' if conn8 else '4'}-conn)")
 
 
+def mrf_potts_cut(seed=0, H=300, W=400, L=8, conn8=True) -> Problem:
+    """Potts MRF in the cut form ('Potts-cut variant'):
+    the same grid, unaries and Potts weights as mrf_potts, but one z_e per edge
+    (cost w_e) with rows x_il - x_jl - z_e <= 0 and x_jl - x_il - z_e <= 0 for
+    every label l, plus the per-pixel simplex.  n = H*W*L + E (1.44 M at full
+    size, the paper's n_max 1.4 M for color-seg-n8)."""
+    rng = np.random.default_rng(seed)
+    npx = H * W
+    xidx = np.arange(npx * L).reshape(npx, L)
+    pix = np.arange(npx).reshape(H, W)
+    edges = [np.stack([pix[:, :-1].ravel(), pix[:, 1:].ravel()], 1),
+             np.stack([pix[:-1, :].ravel(), pix[1:, :].ravel()], 1)]
+    if conn8:
+        edges += [np.stack([pix[:-1, :-1].ravel(), pix[1:, 1:].ravel()], 1),
+                  np.stack([pix[:-1, 1:].ravel(), pix[1:, :-1].ravel()], 1)]
+    e = np.concatenate(edges)
+    E = e.shape[0]
+    unary = rng.uniform(0, 10, size=(npx, L))
+    w = rng.uniform(0.5, 2.0, size=E)
+    zbase = npx * L
+    zidx = zbase + np.arange(E)
+    cost = np.concatenate([unary.ravel(), w])
+    rb = RowBuilder()
+    rb.add(xidx, np.ones((npx, L)), EQ, 1)
+    ei, ej = e[:, 0], e[:, 1]
+    for lab in range(L):
+        v = np.stack([xidx[ei, lab], xidx[ej, lab], zidx], axis=1)
+        rb.add(v, np.broadcast_to(np.array([1, -1, -1]), v.shape), LE, 0)
+        rb.add(v, np.broadcast_to(np.array([-1, 1, -1]), v.shape), LE, 0)
+    return rb.build(zbase + E, cost, f"mrf_potts_cut(seed={seed},{H}x{W}x{L},{'8' if conn8 else '4'}-conn)")
+
+
 def qap(seed=0, n=50) -> Problem:
     """QAPLib-like (tai-a): x_ik plus y_{ik,jl} (i<j, k!=l), assignment + product rows."""
     rng = np.random.default_rng(seed)
@@ -376,6 +408,7 @@ WORKLOADS = {
     "lap4": lambda seed=0: lap_random(4, seed),
     "gm_worms_like": gm_worms_like,
     "mrf_potts": mrf_potts,
+    "mrf_potts_cut": mrf_potts_cut,
     "celltrack": celltrack,
     "qap50": lambda seed=0: qap(seed, 50),
 }

@@ -100,6 +100,7 @@ def test_random_ilps_with_forced_vars(oracle_mod):
 @pytest.mark.parametrize("name,make", [
     ("gm", lambda: synth.gm_worms_like(4, n_src=80, k_cand=6, knn=8)),
     ("mrf", lambda: synth.mrf_potts(4, H=12, W=14, L=4)),
+    ("mrf_cut", lambda: synth.mrf_potts_cut(4, H=12, W=14, L=4)),
     ("qap", lambda: synth.qap(4, n=7)),
     ("celltrack", lambda: synth.celltrack(4, frames=5, dets=40)),
     ("wide_rows", lambda: synth.random_ilp(7, n=40, m=60, kmax=12, coef=5)),
@@ -119,6 +120,7 @@ def test_workload_shapes_fp64(oracle_mod, name, make):
     ("lap4", lambda: synth.lap_random(4, 0)),
     ("gm", lambda: synth.gm_worms_like(5, n_src=120, k_cand=8, knn=10)),
     ("mrf", lambda: synth.mrf_potts(5, H=20, W=20, L=5)),
+    ("mrf_cut", lambda: synth.mrf_potts_cut(5, H=20, W=20, L=5)),
     ("qap", lambda: synth.qap(5, n=8)),
 ])
 def test_fp32_lower_bound_100_iterations(oracle_mod, name, make):
@@ -380,6 +382,11 @@ def test_stage_buffers_bitwise(oracle_mod, monkeypatch, mode, name, make):
     assert np.array_equal(gs[0].lam(), gs[1].lam())
 
 
+def _same_bound(g0, g1):
+    a, b = g0.lower_bound(), g1.lower_bound()
+    return abs(a - b) <= 1e-12 * (1 + abs(b))
+
+
 @pytest.mark.parametrize("mode", ["rc", "tma"])
 @pytest.mark.parametrize("precision", [64, 32])
 @pytest.mark.parametrize("name,make", [
@@ -410,15 +417,15 @@ def test_tile_pairs_bitwise(oracle_mod, monkeypatch, mode, precision, name, make
         g1.pass_(fwd, 0.5)
         o.pass_(fwd, 0.5)
         assert np.array_equal(g0.lam(), g1.lam()) and np.array_equal(g0.deferred(), g1.deferred())
-        assert g0.lower_bound() == g1.lower_bound()
+        assert _same_bound(g0, g1)
         if precision == 64:
             assert np.max(np.abs(g1.lam() - o.lam())) <= 1e-9 * s
     g0.iterate(3, 0.5)
     g1.iterate(3, 0.5)
-    assert np.array_equal(g0.lam(), g1.lam()) and g0.lower_bound() == g1.lower_bound()
+    assert np.array_equal(g0.lam(), g1.lam()) and _same_bound(g0, g1)
     g0.finalize(averaged=True)
     g1.finalize(averaged=True)
-    assert np.array_equal(g0.lam(), g1.lam()) and g0.lower_bound() == g1.lower_bound()
+    assert np.array_equal(g0.lam(), g1.lam()) and _same_bound(g0, g1)
     g0.iterate(2, 0.5)
     g1.iterate(2, 0.5)
     assert np.array_equal(g0.lam(), g1.lam())

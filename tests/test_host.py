@@ -97,6 +97,7 @@ def test_node_counts_random_ilp(oracle_mod, seed):
     ("lap4", lambda: synth.lap(synth.LAP4_LITERAL)),
     ("gm_small", lambda: synth.gm_worms_like(1, n_src=40, k_cand=5, knn=6)),
     ("mrf_small", lambda: synth.mrf_potts(1, H=6, W=7, L=3)),
+    ("mrf_cut_small", lambda: synth.mrf_potts_cut(1, H=6, W=7, L=3)),
     ("qap_small", lambda: synth.qap(1, n=6)),
     ("celltrack_small", lambda: synth.celltrack(1, frames=4, dets=30)),
 ])
@@ -124,6 +125,19 @@ def test_mrf_full_size_counts():
     assert st["bdds"] == H * W + 2 * L * E
     assert st["nodes"] == H * W * (2 * L - 1) + 2 * L * E * (2 * (L + 1) - 1)
     assert st["shapes"] == 2
+
+
+def test_mrf_potts_cut_counts():
+    """Potts-cut closed form: simplex rows 2L-1 nodes, every
+    3-variable cut row x_il - x_jl - z_e <= 0 has 5 nodes (partitions 1, 2, 2)."""
+    H, W, L = 30, 40, 8
+    p = synth.mrf_potts_cut(0, H=H, W=W, L=L)
+    st = F.Plan(p).stats()
+    E = H * (W - 1) + (H - 1) * W + 2 * (H - 1) * (W - 1)
+    assert p.n_vars == H * W * L + E
+    assert st["bdds"] == H * W + 2 * L * E
+    assert st["nodes"] == H * W * (2 * L - 1) + 2 * L * E * 5
+    assert st["slots"] == H * W * L + 2 * L * E * 3
 
 
 def test_invalid_inputs():
