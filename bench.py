@@ -63,6 +63,10 @@ def _workload(name):
         return synth.celltrack(0)
     if name == "lap4":
         return synth.lap_random(4, 0)
+    if name == "mckp":
+        return synth.mckp(0)
+    if name == "gap":
+        return synth.gap(0)
     if name == "thin_hop":
         return synth.thin_hop(0)
     raise SystemExit(f"unknown workload {name}")
@@ -167,6 +171,21 @@ def _hop_latency(F, local, stream, prec):
                 ent[k.split("_")[1] + "_ns"] = 1e6 * prof[k]["ms"] / prof[k]["launches"] / hops
         out[name] = ent
     return out
+
+
+def _exchange_report(prof, st, world):
+    """N > 1: the exchange step per pass, reported separately --
+    ncclAllReduce of the shared partial sums (or the peer-memory sum) and the
+    scatter of their averages, each timed with CUDA events on the exchange
+    stream -- and how much of the sweep it overlaps (the interior tiles)."""
+    if world <= 1:
+        return None
+    ar = prof.get("allreduce", {"ms": 0.0, "launches": 0})
+    fin = prof.get("avg_finish", {"ms": 0.0, "launches": 0})
+    passes = max(prof.get("avg", {}).get("launches", 0), 1)  # one averaging launch per pass
+    return {"shared_vars": st["vars_shared"], "allreduce_us_per_pass": 1e3 * ar["ms"] / passes,
+            "finish_us_per_pass": 1e3 * fin["ms"] / passes,
+            "overlapped_tiles": st["interior_tiles"], "tiles": st["tiles"]}
 
 
 def _peaks():
@@ -422,7 +441,9 @@ def run_gpu(args):
     peak, peak_kind = _peaks()
     sweep = {k: v for k, v in prof.items() if k.startswith("sweep_")}
     sw_ms = sum(v["ms"] for v in sweep.values())
-    sw_n = sum(v["launches"] for v in sweep.values())
+    # per pass (world > 1 splits a pass's sweep into the interior and the
+    # boundary tiles' launches: count passes by the averaging launches)
+    sw_n = prof.get("avg", {}).get("launches", 0) or sum(v["launches"] for v in sweep.values())
     sw_bytes = next(iter(sweep.values()))["bytes_per_launch"] if sweep else 0.0
     achieved = sw_bytes / (sw_ms / sw_n * 1e-3) / 1e9 if sw_n else 0.0
     traffic = None
@@ -586,8 +607,10 @@ def run_gpu(args):
             "ms_per_step_profiled": float(sum(ms_prof)) / args.steps,
             "solver_stats": {k: st[k] for k in ("tiles", "tiles_shared_topology", "staged_tiles", "sweep_grid",
                                                  "sweep_block", "sweep_smem_per_warp", "sweep_streaming", "sweep_recompute", "padded_slots",
-                                                 "device_bytes", "shapes", "max_hops", "max_width", "tile_pairs")},
+                                                 "device_bytes", "shapes", "max_hops", "max_width", "tile_pairs",
+                                                 "interior_tiles", "coop_tiles")},
             "kernels": prof,
+            "exchange": _exchange_report(prof, st, world),
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,

@@ -105,6 +105,10 @@ typedef struct {
   int64_t tile_pairs;              /* variables with |J_i| = 2 whose two slots share a
                                       tile: averaged on chip by the sweep (solver: only
                                       when the sweep path supports it; plan: eligible) */
+  int64_t interior_tiles;          /* world > 1: tiles holding no exchanged variable,
+                                      swept while the exchange runs (= tiles if world 1) */
+  int64_t coop_tiles;              /* one-BDD tiles swept node-parallel by a warp
+                                      (a partition wider than 32 nodes)              */
 } fdog_stats_t;
 
 typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */

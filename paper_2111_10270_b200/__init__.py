@@ -68,7 +68,8 @@ class Stats(C.Structure):
                [("max_hops", C.c_int32), ("max_width", C.c_int32), ("staged_tiles", C.c_int64),
                 ("sweep_grid", C.c_int32), ("sweep_block", C.c_int32), ("sweep_smem_per_warp", C.c_int64),
                 ("sweep_streaming", C.c_int32), ("h2d_bytes", C.c_int64),
-                ("fused_small", C.c_int32), ("sweep_recompute", C.c_int32), ("tile_pairs", C.c_int64)]
+                ("fused_small", C.c_int32), ("sweep_recompute", C.c_int32), ("tile_pairs", C.c_int64),
+                ("interior_tiles", C.c_int64), ("coop_tiles", C.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

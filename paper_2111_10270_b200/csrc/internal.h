@@ -16,6 +16,10 @@ constexpr uint32_t kBot = 0xFFFFu;
 constexpr uint32_t kTop = 0xFFFEu;
 constexpr int32_t kMaxWidth = 0xFFFD;
 constexpr int kLanes = 32;  // BDDs per warp tile (one BDD per lane)
+// Shapes with a partition wider than this run node-parallel, one warp per BDD
+// (tile kind bit 5, kernels.cu process_bdd_coop).
+constexpr int kCoopWidth = 32;
+constexpr int kMaxTileRows = 128;  // rows of the widest tile (4 per lane)
 
 // A distinct compiled BDD topology (many rows share one: same coefficients,
 // relation and right-hand side).
@@ -48,6 +52,11 @@ struct Shape {
 //          is a chain hop (HopRec type 1); the sweeps fold those hops.
 //   kind bit 4 set (with bit 3): the first partition is a root hop (type 2)
 //          and the last a join into top (type 3); folded as well.
+//   kind bit 5 set ("cooperative", shapes wider than kCoopWidth): one BDD
+//          (L = 1), processed node-parallel by a whole warp from global
+//          memory; its topology is two 32-bit words per node (uint2 at
+//          topo[topo_base], absolute child index, top = nodes, bottom =
+//          nodes + 1): no 16-bit limit on the BDD size.
 // Topology entries are absolute child indices within the tile (s^0 in the low
 // 16 bits, s^1 in the high 16 bits), top = nodes, bottom = nodes + 1.
 // Partition offsets of the tile: hop_off[hop_base + h], h = 0..K.
@@ -188,6 +197,12 @@ struct Plan {
   bool rc = false;                  // recompute design: tiles packed for sweep_kernel<..., RC>
   int64_t n_dist = 0;               // elements of the distance array
   int64_t direct_tiles = 0;
+  int64_t n_interior_tiles = 0;     // world > 1: tiles [0, n) hold no exchanged variable (swept while
+                                    // the exchange runs); the boundary tiles follow
+  int64_t coop_tiles = 0;           // kind bit 5 tiles (one wide BDD each)
+  int32_t coop_w = 0;               // widest partition of a cooperative tile
+  int32_t direct_w = 0;             // widest partition of the other unstaged tiles
+  bool coop_smem = false;           // the cooperative relaxation buffers fit the DB region
 
   HostImage image;                  // device image (see ImageSection)
 
@@ -238,6 +253,8 @@ struct SweepArgs {
   void *scratch;            // T*, [warps][scratch_stride] for direct tiles
   unsigned long long *trace;  // debug (FDOG_TRACE=1): per warp {start, end, tiles, smid}, else null
   int64_t scratch_stride;   // elements per warp
+  int32_t coop_bw;          // cooperative tiles: entries per relaxation buffer (two per warp)
+  int32_t coop_smem;        // 1: in the warp's DB region, 0: in scratch
 };
 
 struct AvgArgs {
@@ -317,12 +334,13 @@ int launch_dist_dp(int precision, const SeqArgs &a, int32_t n_tiles, int32_t for
 
 // returns the cudaError_t as int
 // rc: recompute design (sweep_kernel<..., RC = true>; plan packed with Plan::rc)
-int launch_sweep(int precision, int mode, bool record, bool rc, const SweepArgs &a, int grid, int block,
+// rw: the most rows per lane of any tile (1, 2, 4; TileDesc::lanes / 32)
+int launch_sweep(int precision, int mode, bool record, bool rc, int rw, const SweepArgs &a, int grid, int block,
                  size_t smem, void *stream);
 int launch_sweep_stream(int precision, int mode, bool record, const SweepArgs &a, void *stream);
 // chunked walk of rows too long to stage whole (store design; every tile an arc-mask tile)
 int launch_sweep_chunk(int precision, int mode, bool record, const SweepArgs &a, void *stream);
-int sweep_occupancy(int precision, int mode, bool record, bool rc, int block, size_t smem, int *blocks_per_sm);
+int sweep_occupancy(int precision, int mode, bool record, bool rc, int rw, int block, size_t smem, int *blocks_per_sm);
 int launch_avg(int precision, const AvgArgs &a, void *stream);
 int launch_peer_signal(const PeerArgs &pa, void *stream);
 int preload_kernels(int precision);

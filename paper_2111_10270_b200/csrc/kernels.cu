@@ -310,6 +310,205 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
   return acc;
 }
 
+// ---------------------------------------------------------------------------
+// Wide BDDs (a partition wider than kCoopWidth nodes, e.g. knapsack rows):
+// node-parallel, the way P:345-347 parallelises a hop over v in P_i.  One warp
+// per BDD; at every hop the 32 lanes split the partition's nodes, the min-
+// marginals m^0, m^1 are warp-shuffle min reductions (exact: min is
+// order-independent), every lane applies the same dual update, and the
+// forward relaxation into P_{h+1} is a shared-/global-memory atomic min
+// on an order-preserving integer image of the distances (exact as well; for
+// either order of the arcs, min(c + lambda) = min(c) + lambda under monotone
+// rounding, so every value equals the lane-serial process_bdd bit for bit).
+// Topology: two 32-bit absolute child indices per node (uint2), top = nodes,
+// bottom = nodes + 1 (the sentinels of D) -- no 16-bit limit on BDD size.
+// Single BDD per tile (L = 1): lambda / va / D are contiguous per hop / node.
+template <typename T>
+struct OrdOf;
+template <>
+struct OrdOf<float> {
+  using U = uint32_t;
+};
+template <>
+struct OrdOf<double> {
+  using U = unsigned long long;
+};
+// order-preserving map T -> unsigned (a < b <=> ord(a) < ord(b); -0 < +0)
+__device__ __forceinline__ uint32_t t_ord(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float t_unord(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+__device__ __forceinline__ unsigned long long t_ord(double f) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(f);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double t_unord(unsigned long long u) {
+  return __longlong_as_double((long long)((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u));
+}
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// buf: two relaxation buffers of `bw` entries (shared or global memory).
+// Returns the BDD's bound contribution on lane 0 (0 on the other lanes).
+// Every node loop runs in blocks of CB nodes per lane (lane l: nodes n0 + l +
+// 32 q), loads first and stores after, so a lane has 2 CB independent distance
+// gathers in flight (the BDD is in global memory / L2: latency-bound otherwise).
+template <typename T, int MODE, bool REC>
+__device__ __noinline__ double process_bdd_coop(const int K, const int nodes, const int32_t *ho, const uint2 *tp,
+                                                T *lam, T *va, T *D, typename OrdOf<T>::U *buf, const int bw,
+                                                const int lane, const T omega, const T clamp, T *m0g, T *m1g) {
+  using U = typename OrdOf<T>::U;
+  constexpr int CB = 4;
+  const T inf = t_inf<T>();
+  const U uinf = t_ord(inf);
+  double acc = 0.0;
+  // dual update of partition h from the reduced min-marginals
+  auto update = [&](int h, T m0, T m1r) -> T {
+    const T l = lam[h];
+    const T m1 = l + m1r;
+    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+    const T lam_new = add_rn(sub_rn(l, delta), va[h]);
+    __syncwarp();  // every lane has read lam[h] / va[h]
+    if (lane == 0) {
+      lam[h] = lam_new;
+      va[h] = delta;
+      if (REC) {
+        m0g[h] = m0;
+        m1g[h] = m1;
+      }
+      acc += (double)fmin(delta, T(0));
+    }
+    return lam_new;
+  };
+  if (MODE == kEnergy || MODE == kBackward) {
+    // backward: D holds shp(r, v) (forward pass); shp(v, T) of P_{h+1} is
+    // written by the previous hop.  kEnergy: shp(v, T) only.
+#pragma unroll 1
+    for (int h = K - 1; h >= 0; --h) {
+      const int n0 = ho[h], n1 = ho[h + 1];
+      T l = lam[h];
+      if (MODE == kBackward) {
+        T m0 = inf, m1r = inf;
+#pragma unroll 1
+        for (int nb = n0 + lane; nb < n1; nb += 32 * CB) {
+          uint2 e[CB];
+          T cf[CB], x0[CB], x1[CB];
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            const bool ok = nb + 32 * q < n1;
+            e[q] = ok ? tp[nb + 32 * q] : make_uint2(nodes + 1, nodes + 1);
+            cf[q] = ok ? D[nb + 32 * q] : inf;
+          }
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            x0[q] = D[e[q].x];
+            x1[q] = D[e[q].y];
+          }
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            m0 = fmin(m0, cf[q] + x0[q]);
+            m1r = fmin(m1r, cf[q] + x1[q]);
+          }
+        }
+        l = update(h, warp_min(m0), warp_min(m1r));
+      }
+#pragma unroll 1
+      for (int nb = n0 + lane; nb < n1; nb += 32 * CB) {
+        uint2 e[CB];
+        T v[CB];
+#pragma unroll
+        for (int q = 0; q < CB; ++q) e[q] = nb + 32 * q < n1 ? tp[nb + 32 * q] : make_uint2(nodes + 1, nodes + 1);
+#pragma unroll
+        for (int q = 0; q < CB; ++q) v[q] = fmin(D[e[q].x], l + D[e[q].y]);
+#pragma unroll
+        for (int q = 0; q < CB; ++q)
+          if (nb + 32 * q < n1) D[nb + 32 * q] = v[q];
+      }
+      __syncwarp();  // the next hop reads these as children
+    }
+    if (lane == 0) acc += (double)D[0];  // E^j = shp(r, T)
+    return acc;
+  }
+  // forward / kCfr: shp(r, .) of P_h in buffer `cur` (ord images), relaxed into
+  // `nxt` for P_{h+1}; D of P_h is overwritten with shp(r, v) (store design).
+  U *cur = buf, *nxt = buf + bw;
+  if (lane == 0) cur[0] = t_ord(T(0));  // shp(r, r)
+  __syncwarp();
+#pragma unroll 1
+  for (int h = 0; h < K; ++h) {
+    const int n0 = ho[h], n1 = ho[h + 1];
+    const bool last = h == K - 1;
+    const int Wn = last ? 0 : ho[h + 2] - n1;
+    for (int w = lane; w < Wn; w += 32) nxt[w] = uinf;
+    T m0 = inf, m1r = inf;
+    if (MODE == kForward || last) {  // min-marginals against shp(., T) of P_{h+1}; kCfr: E^j only
+#pragma unroll 1
+      for (int nb = n0 + lane; nb < n1; nb += 32 * CB) {
+        uint2 e[CB];
+        T cf[CB], x0[CB], x1[CB];
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          const bool ok = nb + 32 * q < n1;
+          e[q] = ok ? tp[nb + 32 * q] : make_uint2(nodes + 1, nodes + 1);
+          cf[q] = ok ? t_unord(cur[nb + 32 * q - n0]) : inf;
+        }
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          x0[q] = D[e[q].x];
+          x1[q] = D[e[q].y];
+        }
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          m0 = fmin(m0, cf[q] + x0[q]);
+          m1r = fmin(m1r, cf[q] + x1[q]);
+        }
+      }
+      m0 = warp_min(m0);
+      m1r = warp_min(m1r);
+    }
+    T l = lam[h];
+    if (MODE == kForward) l = update(h, m0, m1r);
+    __syncwarp();  // nxt initialised; the reads of D of P_{h+1} are done
+    // D of P_h <- shp(r, v); relax into P_{h+1} (A4: 1-arcs priced with the updated lambda_h)
+#pragma unroll 1
+    for (int nb = n0 + lane; nb < n1; nb += 32 * CB) {
+      uint2 e[CB];
+      T cf[CB];
+#pragma unroll
+      for (int q = 0; q < CB; ++q) {
+        const bool ok = nb + 32 * q < n1;
+        e[q] = ok ? tp[nb + 32 * q] : make_uint2(nodes + 1, nodes + 1);
+        cf[q] = ok ? t_unord(cur[nb + 32 * q - n0]) : inf;
+      }
+#pragma unroll
+      for (int q = 0; q < CB; ++q) {
+        if (nb + 32 * q >= n1) continue;
+        D[nb + 32 * q] = cf[q];
+        if (!last) {
+          if ((int)e[q].x < n1 + Wn) atomicMin(&nxt[e[q].x - n1], t_ord(cf[q]));      // 0-arc (bottom: skipped)
+          if ((int)e[q].y < n1 + Wn) atomicMin(&nxt[e[q].y - n1], t_ord(cf[q] + l));  // 1-arc
+        }
+      }
+    }
+    __syncwarp();
+    if (!last) {
+      U *t = cur;
+      cur = nxt;
+      nxt = t;
+    } else if (lane == 0) {
+      acc += (double)fmin(m0, l + m1r);  // E^j = shp(r, T) (at the updated lambda)
+    }
+  }
+  return acc;
+}
+
 // Narrow tiles (every partition has <= 2 nodes -- all one-hot, at-most-one and
 // marginalisation rows of the BASELINE workloads).  Same arithmetic and the
 // same D / va conventions as process_bdd, with the per-partition values of the
@@ -709,24 +908,41 @@ __device__ __forceinline__ int4 tail_of(const HopRec<T> *rec, int h, int hb = 0)
   return hop_tail(rec + (h - hb));
 }
 
-// shp(v, T) of every node under the current lambda (no update); returns
+// Rows per lane (R): a tile of L = 32 R rows of one shape gives lane l the rows
+// l, l + 32, ..., l + 32 (R - 1); their values sit at +32 k in every [index][L]
+// array.  The R chains share the hop tail, the addresses and the loop control,
+// and are independent (R-fold ILP on the dependent hop chain); each one runs
+// exactly the arithmetic of R = 1.
+
+// shp(v, T) of every node under the current lambda (no update); e[k] =
 // shp(r, T) = E^j.  (kEnergy; phase 1 of a recompute forward pass.)
-template <typename T, int LC, bool ENDS>
-__device__ __forceinline__ T mask_ctt_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                      const T *lam, T *D) {
+template <typename T, int LC, bool ENDS, int R>
+__device__ __forceinline__ void mask_ctt_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+                                              const T *lam, T *D, T (&e)[R]) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
-  T x0 = T(0), x1 = t_inf<T>();
+  T x0[R], x1[R], l[R];
   int4 tl = tail_of<ENDS>(rec, K - 1);
-  T l = lam[(K - 1) * L];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    x0[k] = T(0);
+    x1[k] = t_inf<T>();
+    l[k] = lam[(K - 1) * L + 32u * k];
+  }
   auto step = [&](auto ch, int h) {
     const uint32_t hn = h > 0 ? h - 1 : 0;
     const int4 tn = tail_of<ENDS>(rec, hn);
-    const T ln = lam[hn * L];
-    hop_ctt(decltype(ch)::value, rec + (uint32_t)h, x0, x1, l, x0, x1);
-    D[tl.x * L] = x0;
-    if (tl.z) D[(tl.x + 1) * L] = x1;
+    T ln[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) ln[k] = lam[hn * L + 32u * k];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      hop_ctt(decltype(ch)::value, rec + (uint32_t)h, x0[k], x1[k], l[k], x0[k], x1[k]);
+      D[tl.x * L + 32u * k] = x0[k];
+      if (tl.z) D[(tl.x + 1) * L + 32u * k] = x1[k];
+    }
     tl = tn;
-    l = ln;
+#pragma unroll
+    for (int k = 0; k < R; ++k) l[k] = ln[k];
   };
   int h = K - 1;
   if (chain) {  // bit 0: chain middle; bit 1: join last, root first
@@ -740,34 +956,46 @@ __device__ __forceinline__ T mask_ctt_impl(const int K, const int chain, const H
   }
 #pragma unroll 1
   for (; h >= 0; --h) step(Ty<0>(), h);
-  return x0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) e[k] = x0[k];
 }
 
-template <typename T, int LC>
-__device__ __forceinline__ T mask_ctt(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                      const T *lam, T *D) {
-  if (chain & 2) return mask_ctt_impl<T, LC, true>(K, chain, rec, L_rt, lam, D);
-  return mask_ctt_impl<T, LC, false>(K, chain, rec, L_rt, lam, D);
+template <typename T, int LC, int R>
+__device__ __forceinline__ void mask_ctt(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+                                         const T *lam, T *D, T (&e)[R]) {
+  if (chain & 2) mask_ctt_impl<T, LC, true, R>(K, chain, rec, L_rt, lam, D, e);
+  else mask_ctt_impl<T, LC, false, R>(K, chain, rec, L_rt, lam, D, e);
 }
 
-// shp(r, v) of every node under the current lambda (no update); returns
+// shp(r, v) of every node under the current lambda (no update); e[k] =
 // shp(r, T) = E^j.  (kCfr; phase 1 of a recompute backward pass.)
-template <typename T, int LC, bool ENDS>
-__device__ __forceinline__ T mask_cfr_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                      const T *lam, T *D) {
+template <typename T, int LC, bool ENDS, int R>
+__device__ __forceinline__ void mask_cfr_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+                                              const T *lam, T *D, T (&e)[R]) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
-  T c0 = T(0), c1 = t_inf<T>();
+  T c0[R], c1[R], l[R];
   int4 tl = tail_of<ENDS>(rec, 0);
-  T l = lam[0];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    c0[k] = T(0);
+    c1[k] = t_inf<T>();
+    l[k] = lam[32u * k];
+  }
   auto step = [&](auto ch, int h) {
     const uint32_t hn = h + 1 < K ? h + 1 : h;
     const int4 tn = tail_of<ENDS>(rec, hn);
-    const T ln = lam[hn * L];
-    D[tl.x * L] = c0;
-    if (tl.z) D[(tl.x + 1) * L] = c1;
-    hop_relax(decltype(ch)::value, rec + (uint32_t)h, c0, c1, l, c0, c1);
+    T ln[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) ln[k] = lam[hn * L + 32u * k];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      D[tl.x * L + 32u * k] = c0[k];
+      if (tl.z) D[(tl.x + 1) * L + 32u * k] = c1[k];
+      hop_relax(decltype(ch)::value, rec + (uint32_t)h, c0[k], c1[k], l[k], c0[k], c1[k]);
+    }
     tl = tn;
-    l = ln;
+#pragma unroll
+    for (int k = 0; k < R; ++k) l[k] = ln[k];
   };
   int h = 0;
   if (chain) {  // bit 0: chain middle; bit 1: root first, join last (kind bits 3, 4)
@@ -781,48 +1009,71 @@ __device__ __forceinline__ T mask_cfr_impl(const int K, const int chain, const H
   }
 #pragma unroll 1
   for (; h < K; ++h) step(Ty<0>(), h);
-  return c0;  // after the last partition: the relaxation into top
+#pragma unroll
+  for (int k = 0; k < R; ++k) e[k] = c0[k];  // after the last partition: the relaxation into top
 }
 
-template <typename T, int LC>
-__device__ __forceinline__ T mask_cfr(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                      const T *lam, T *D) {
-  if (chain & 2) return mask_cfr_impl<T, LC, true>(K, chain, rec, L_rt, lam, D);
-  return mask_cfr_impl<T, LC, false>(K, chain, rec, L_rt, lam, D);
+template <typename T, int LC, int R>
+__device__ __forceinline__ void mask_cfr(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
+                                         const T *lam, T *D, T (&e)[R]) {
+  if (chain & 2) mask_cfr_impl<T, LC, true, R>(K, chain, rec, L_rt, lam, D, e);
+  else mask_cfr_impl<T, LC, false, R>(K, chain, rec, L_rt, lam, D, e);
 }
 
 // forward pass with updates.  D holds shp(v, T) (stored by the
 // previous backward pass, or recomputed by mask_ctt); STORE: D of P_h is
 // overwritten with shp(r, v) for the next backward pass (P:315-316 reuse).
-template <typename T, bool STORE, bool REC, int LC, bool ENDS>
+// vm: bit k set if row k of the lane is a real row (not padding).
+template <typename T, bool STORE, bool REC, int LC, bool ENDS, int R>
 __device__ __forceinline__ double mask_forward_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                               T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
-                                               T *m0g, T *m1g) {
+                                                    T *lam, T *va, T *D, const uint32_t vm, const T omega,
+                                                    const T clamp, T *m0g, T *m1g) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   double acc = 0.0;
-  T c0 = T(0), c1 = t_inf<T>();
+  T c0[R], c1[R], l[R], av[R], x0[R], x1[R];
   int4 tl = tail_of<ENDS>(rec, 0);
-  T l = lam[0], av = va[0];
-  T x0 = D[tl.y * L], x1 = D[(tl.y + 1) * L];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    c0[k] = T(0);
+    c1[k] = t_inf<T>();
+    l[k] = lam[32u * k];
+    av[k] = va[32u * k];
+    x0[k] = D[tl.y * L + 32u * k];
+    x1[k] = D[(tl.y + 1) * L + 32u * k];
+  }
   auto step = [&](auto ch, int h) {
     constexpr int ty = decltype(ch)::value;
     const uint32_t hn = h + 1 < K ? h + 1 : h;
     const int4 tn = tail_of<ENDS>(rec, hn);
-    const T ln = lam[hn * L], avn = va[hn * L];
-    const T x0n = D[tn.y * L], x1n = D[(tn.y + 1) * L];
-    if (STORE) {
-      D[tl.x * L] = c0;
-      if (tl.z) D[(tl.x + 1) * L] = c1;
+    T ln[R], avn[R], x0n[R], x1n[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      ln[k] = lam[hn * L + 32u * k];
+      avn[k] = va[hn * L + 32u * k];
+      x0n[k] = D[tn.y * L + 32u * k];
+      x1n[k] = D[(tn.y + 1) * L + 32u * k];
     }
-    T m0, m1r;
-    hop_mm(ty, rec + (uint32_t)h, x0, x1, c0, c1, m0, m1r);
-    const T lam_new = mask_finish<T, REC>(lam, va, (uint32_t)h * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
-    hop_relax(ty, rec + (uint32_t)h, c0, c1, lam_new, c0, c1);  // A4: 1-arcs priced with the updated lambda_h
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      if (STORE) {
+        D[tl.x * L + 32u * k] = c0[k];
+        if (tl.z) D[(tl.x + 1) * L + 32u * k] = c1[k];
+      }
+      T m0, m1r;
+      hop_mm(ty, rec + (uint32_t)h, x0[k], x1[k], c0[k], c1[k], m0, m1r);
+      const T lam_new = mask_finish<T, REC>(lam + 32u * k, va + 32u * k, (uint32_t)h * L, l[k], av[k], m0, m1r,
+                                            (vm >> k) & 1u, omega, clamp, REC ? m0g + 32u * k : nullptr,
+                                            REC ? m1g + 32u * k : nullptr, acc);
+      hop_relax(ty, rec + (uint32_t)h, c0[k], c1[k], lam_new, c0[k], c1[k]);  // A4: 1-arcs priced with the updated lambda_h
+    }
     tl = tn;
-    l = ln;
-    av = avn;
-    x0 = x0n;
-    x1 = x1n;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      l[k] = ln[k];
+      av[k] = avn[k];
+      x0[k] = x0n[k];
+      x1[k] = x1n[k];
+    }
   };
   int h = 0;
   if (chain) {  // bit 0: chain middle; bit 1: root first, join last (kind bits 3, 4)
@@ -836,53 +1087,77 @@ __device__ __forceinline__ double mask_forward_impl(const int K, const int chain
   }
 #pragma unroll 1
   for (; h < K; ++h) step(Ty<0>(), h);
-  if (valid) acc += (double)c0;  // E^j = shp(r, T) at the updated lambda
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    if ((vm >> k) & 1u) acc += (double)c0[k];  // E^j = shp(r, T) at the updated lambda
   return acc;
 }
 
-template <typename T, bool STORE, bool REC, int LC>
+template <typename T, bool STORE, bool REC, int LC, int R>
 __device__ __forceinline__ double mask_forward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                               T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
+                                               T *lam, T *va, T *D, const uint32_t vm, const T omega, const T clamp,
                                                T *m0g, T *m1g) {
-  if (chain & 2) return mask_forward_impl<T, STORE, REC, LC, true>(K, chain, rec, L_rt, lam, va, D, valid, omega, clamp, m0g, m1g);
-  return mask_forward_impl<T, STORE, REC, LC, false>(K, chain, rec, L_rt, lam, va, D, valid, omega, clamp, m0g, m1g);
+  if (chain & 2)
+    return mask_forward_impl<T, STORE, REC, LC, true, R>(K, chain, rec, L_rt, lam, va, D, vm, omega, clamp, m0g, m1g);
+  return mask_forward_impl<T, STORE, REC, LC, false, R>(K, chain, rec, L_rt, lam, va, D, vm, omega, clamp, m0g, m1g);
 }
 
 // backward pass with updates.  D holds shp(r, v) (stored by the
 // forward pass, or recomputed by mask_cfr); STORE: D of P_h is overwritten
 // with shp(v, T) for the next forward pass.
-template <typename T, bool STORE, bool REC, int LC, bool ENDS>
+template <typename T, bool STORE, bool REC, int LC, bool ENDS, int R>
 __device__ __forceinline__ double mask_backward_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                                T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
-                                                T *m0g, T *m1g) {
+                                                     T *lam, T *va, T *D, const uint32_t vm, const T omega,
+                                                     const T clamp, T *m0g, T *m1g) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   const T inf = t_inf<T>();
   double acc = 0.0;
-  T x0 = T(0), x1 = inf;  // shp(., T) of P_{h+1}; the last partition's targets: top
+  T x0[R], x1[R], l[R], av[R], f0[R], f1[R];  // x: shp(., T) of P_{h+1}; the last partition's targets: top
   int4 tl = tail_of<ENDS>(rec, K - 1);
-  T l = lam[(K - 1) * L], av = va[(K - 1) * L];
   // (a one-node partition's second entry is not read: in global memory the
   // load would alias the store of the partition above)
-  T f0 = D[tl.x * L], f1 = tl.z ? D[(tl.x + 1) * L] : inf;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    x0[k] = T(0);
+    x1[k] = inf;
+    l[k] = lam[(K - 1) * L + 32u * k];
+    av[k] = va[(K - 1) * L + 32u * k];
+    f0[k] = D[tl.x * L + 32u * k];
+    f1[k] = tl.z ? D[(tl.x + 1) * L + 32u * k] : inf;
+  }
   auto step = [&](auto ch, int h) {
     constexpr int ty = decltype(ch)::value;
     const uint32_t hn = h > 0 ? h - 1 : 0;
     const int4 tn = tail_of<ENDS>(rec, hn);
-    const T ln = lam[hn * L], avn = va[hn * L];
-    const T f0n = D[tn.x * L], f1n = tn.z ? D[(tn.x + 1) * L] : inf;
-    T m0, m1r;
-    hop_mm(ty, rec + (uint32_t)h, x0, x1, f0, f1, m0, m1r);
-    const T lam_new = mask_finish<T, REC>(lam, va, (uint32_t)h * L, l, av, m0, m1r, valid, omega, clamp, m0g, m1g, acc);
-    hop_ctt(ty, rec + (uint32_t)h, x0, x1, lam_new, x0, x1);  // shp(v, T) with the updated lambda_h
-    if (STORE) {
-      D[tl.x * L] = x0;
-      if (tl.z) D[(tl.x + 1) * L] = x1;
+    T ln[R], avn[R], f0n[R], f1n[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      ln[k] = lam[hn * L + 32u * k];
+      avn[k] = va[hn * L + 32u * k];
+      f0n[k] = D[tn.x * L + 32u * k];
+      f1n[k] = tn.z ? D[(tn.x + 1) * L + 32u * k] : inf;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      T m0, m1r;
+      hop_mm(ty, rec + (uint32_t)h, x0[k], x1[k], f0[k], f1[k], m0, m1r);
+      const T lam_new = mask_finish<T, REC>(lam + 32u * k, va + 32u * k, (uint32_t)h * L, l[k], av[k], m0, m1r,
+                                            (vm >> k) & 1u, omega, clamp, REC ? m0g + 32u * k : nullptr,
+                                            REC ? m1g + 32u * k : nullptr, acc);
+      hop_ctt(ty, rec + (uint32_t)h, x0[k], x1[k], lam_new, x0[k], x1[k]);  // shp(v, T) with the updated lambda_h
+      if (STORE) {
+        D[tl.x * L + 32u * k] = x0[k];
+        if (tl.z) D[(tl.x + 1) * L + 32u * k] = x1[k];
+      }
     }
     tl = tn;
-    l = ln;
-    av = avn;
-    f0 = f0n;
-    f1 = f1n;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      l[k] = ln[k];
+      av[k] = avn[k];
+      f0[k] = f0n[k];
+      f1[k] = f1n[k];
+    }
   };
   int h = K - 1;
   if (chain) {  // bit 0: chain middle; bit 1: join last, root first
@@ -896,16 +1171,43 @@ __device__ __forceinline__ double mask_backward_impl(const int K, const int chai
   }
 #pragma unroll 1
   for (; h >= 0; --h) step(Ty<0>(), h);
-  if (valid) acc += (double)x0;  // E^j = shp(r, T)
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    if ((vm >> k) & 1u) acc += (double)x0[k];  // E^j = shp(r, T)
   return acc;
 }
 
-template <typename T, bool STORE, bool REC, int LC>
+template <typename T, bool STORE, bool REC, int LC, int R>
 __device__ __forceinline__ double mask_backward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                                T *lam, T *va, T *D, const bool valid, const T omega, const T clamp,
+                                                T *lam, T *va, T *D, const uint32_t vm, const T omega, const T clamp,
                                                 T *m0g, T *m1g) {
-  if (chain & 2) return mask_backward_impl<T, STORE, REC, LC, true>(K, chain, rec, L_rt, lam, va, D, valid, omega, clamp, m0g, m1g);
-  return mask_backward_impl<T, STORE, REC, LC, false>(K, chain, rec, L_rt, lam, va, D, valid, omega, clamp, m0g, m1g);
+  if (chain & 2)
+    return mask_backward_impl<T, STORE, REC, LC, true, R>(K, chain, rec, L_rt, lam, va, D, vm, omega, clamp, m0g, m1g);
+  return mask_backward_impl<T, STORE, REC, LC, false, R>(K, chain, rec, L_rt, lam, va, D, vm, omega, clamp, m0g, m1g);
+}
+
+// One arc-mask tile of one pass: the four modes over the lane's R rows.
+// Returns the lane's share of the tile's bound partial.
+template <typename T, int MODE, bool REC, bool RC, int LC, int R>
+__device__ __forceinline__ double mask_tile(const int K, const int chain, const HopRec<T> *rec, const int L,
+                                            T *lm, T *vp, T *D, const uint32_t vm, const T omega, const T clamp,
+                                            T *m0p, T *m1p) {
+  T e[R];
+  double acc = 0.0;
+  if (MODE == kEnergy || MODE == kCfr) {
+    if (MODE == kEnergy) mask_ctt<T, LC, R>(K, chain, rec, L, lm, D, e);
+    else mask_cfr<T, LC, R>(K, chain, rec, L, lm, D, e);
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+      if ((vm >> k) & 1u) acc += (double)e[k];
+  } else if (MODE == kForward) {
+    if (RC) mask_ctt<T, LC, R>(K, chain, rec, L, lm, D, e);
+    acc = mask_forward<T, !RC, REC, LC, R>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
+  } else {
+    if (RC) mask_cfr<T, LC, R>(K, chain, rec, L, lm, D, e);
+    acc = mask_backward<T, !RC, REC, LC, R>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
+  }
+  return acc;
 }
 
 // Stage buffer of one tile (layout: internal.h).
@@ -981,7 +1283,9 @@ __device__ __forceinline__ void fetch_desc(TileDesc *dst, const TileDesc *src, i
 // RC: recompute design (narrow tiles, every tile staged): the stage buffers
 // hold lambda, averages, topology and partition offsets only; the distances
 // live in a per-warp scratch column per lane (the DB region) and never touch HBM.
-template <typename T, int MODE, bool REC, bool RC>
+// RW: the most rows per lane of any tile (1, 2 or 4; separate instantiations so
+// that problems without wide tiles keep the register budget of RW = 1)
+template <typename T, int MODE, bool REC, bool RC, int RW>
 __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   constexpr bool kUpd = MODE == kForward || MODE == kBackward;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1107,42 +1411,25 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
           const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(s.topo);
           const int chain = ((d.kind & 8) ? 1 : 0) | ((d.kind & 16) ? 2 : 0);
           T *D = RC ? reinterpret_cast<T *>(rbase) + lane : s.dist + lane;
-          if (RC) {
-            D[d.nodes * L] = T(0);              // top
-            D[(d.nodes + 1) * L] = t_inf<T>();  // bottom
-          }
+          if (RC)
+            for (int o = 0; o < L; o += 32) {
+              D[d.nodes * L + o] = T(0);              // top
+              D[(d.nodes + 1) * L + o] = t_inf<T>();  // bottom
+            }
           T *m0p = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
           T *m1p = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
           T *lm = s.lam + lane, *vp = s.va + lane;
-          if (L == 32) {
-            if (MODE == kEnergy) {
-              const T e = mask_ctt<T, 32>(K, chain, rec, 32, lm, D);
-              acc = valid ? (double)e : 0.0;
-            } else if (MODE == kCfr) {
-              const T e = mask_cfr<T, 32>(K, chain, rec, 32, lm, D);
-              acc = valid ? (double)e : 0.0;
-            } else if (MODE == kForward) {
-              if (RC) mask_ctt<T, 32>(K, chain, rec, 32, lm, D);
-              acc = mask_forward<T, !RC, REC, 32>(K, chain, rec, 32, lm, vp, D, valid, omega, clamp, m0p, m1p);
-            } else {
-              if (RC) mask_cfr<T, 32>(K, chain, rec, 32, lm, D);
-              acc = mask_backward<T, !RC, REC, 32>(K, chain, rec, 32, lm, vp, D, valid, omega, clamp, m0p, m1p);
-            }
-          } else {
-            if (MODE == kEnergy) {
-              const T e = mask_ctt<T, 0>(K, chain, rec, L, lm, D);
-              acc = valid ? (double)e : 0.0;
-            } else if (MODE == kCfr) {
-              const T e = mask_cfr<T, 0>(K, chain, rec, L, lm, D);
-              acc = valid ? (double)e : 0.0;
-            } else if (MODE == kForward) {
-              if (RC) mask_ctt<T, 0>(K, chain, rec, L, lm, D);
-              acc = mask_forward<T, !RC, REC, 0>(K, chain, rec, L, lm, vp, D, valid, omega, clamp, m0p, m1p);
-            } else {
-              if (RC) mask_cfr<T, 0>(K, chain, rec, L, lm, D);
-              acc = mask_backward<T, !RC, REC, 0>(K, chain, rec, L, lm, vp, D, valid, omega, clamp, m0p, m1p);
-            }
-          }
+          // rows per lane: tiles of 64 / 128 rows (short rows, plan.cpp)
+          const uint32_t vm = (lane < d.n_lanes ? 1u : 0u) | (lane + 32 < d.n_lanes ? 2u : 0u) |
+                              (lane + 64 < d.n_lanes ? 4u : 0u) | (lane + 96 < d.n_lanes ? 8u : 0u);
+          if (L == 32)
+            acc = mask_tile<T, MODE, REC, RC, 32, 1>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
+          else if (RW >= 2 && L == 64)
+            acc = mask_tile<T, MODE, REC, RC, 64, 2>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
+          else if (RW >= 4 && L == 128)
+            acc = mask_tile<T, MODE, REC, RC, 128, 4>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
+          else
+            acc = mask_tile<T, MODE, REC, RC, 0, 1>(K, chain, rec, L, lm, vp, D, vm & 1u, omega, clamp, m0p, m1p);
         }
       } else if (RC) {
         if (active) {
@@ -1201,6 +1488,17 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
         if (!RC) bulk_s2g(gdist + d.dist_base, s.dist, (uint32_t)(d.nodes + 2) * L * sizeof(T));
         bulk_commit();
       }
+    } else if (d.kind & 32) {
+      // cooperative tile: one wide BDD, node-parallel over the warp
+      using U = typename OrdOf<T>::U;
+      U *buf = a.coop_smem ? reinterpret_cast<U *>(rbase)
+                           : reinterpret_cast<U *>(a.scratch) + (size_t)gwarp * a.scratch_stride;
+      T *m0p = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base : nullptr;
+      T *m1p = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base : nullptr;
+      acc = process_bdd_coop<T, MODE, REC>(K, d.nodes, a.hop_off + d.hop_base,
+                                           reinterpret_cast<const uint2 *>(a.topo) + d.topo_base,
+                                           lambda + d.slot_base, delta_out + d.slot_base, gdist + d.dist_base, buf,
+                                           a.coop_bw, lane, omega, clamp, m0p, m1p);
     } else {
       // direct tile (exceeds the per-warp budget; L = 32): global memory and a
       // per-warp scratch area for the relaxation buffers
@@ -1562,11 +1860,11 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
     T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
     const T omega = T(a.omega), clamp = T(a.clamp);
     if (L == 32) {
-      acc = MODE == kForward ? mask_forward<T, true, REC, 32>(K, chain, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g)
-                             : mask_backward<T, true, REC, 32>(K, chain, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g);
+      acc = MODE == kForward ? mask_forward<T, true, REC, 32, 1>(K, chain, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g)
+                             : mask_backward<T, true, REC, 32, 1>(K, chain, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g);
     } else {
-      acc = MODE == kForward ? mask_forward<T, true, REC, 0>(K, chain, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g)
-                             : mask_backward<T, true, REC, 0>(K, chain, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g);
+      acc = MODE == kForward ? mask_forward<T, true, REC, 0, 1>(K, chain, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g)
+                             : mask_backward<T, true, REC, 0, 1>(K, chain, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g);
     }
   } else if (lane < L) {
     const int32_t *ho = a.hop_off + d.hop_base;
@@ -2238,7 +2536,7 @@ __global__ void __launch_bounds__(128) seq_level_kernel(const SeqArgs a, int64_t
           e_j = fmin(e_j, fmin(c + D[l.dbase + (int64_t)(e & 0xFFFFu) * l.L],
                                c + lam_new + D[l.dbase + (int64_t)(e >> 16) * l.L]));
         }
-        a.e_lane[(int64_t)t * 32 + l.lane] = (double)e_j;
+        a.e_lane[(int64_t)t * kMaxTileRows + l.lane] = (double)e_j;
       }
     } else {
       for (int n = n0; n < n1; ++n) {
@@ -2246,7 +2544,7 @@ __global__ void __launch_bounds__(128) seq_level_kernel(const SeqArgs a, int64_t
         D[l.dbase + (int64_t)n * l.L] = fmin(D[l.dbase + (int64_t)(e & 0xFFFFu) * l.L],
                                              lam_new + D[l.dbase + (int64_t)(e >> 16) * l.L]);
       }
-      if (l.h == 0) a.e_lane[(int64_t)t * 32 + l.lane] = (double)D[l.dbase];  // E^j = shp(r, T)
+      if (l.h == 0) a.e_lane[(int64_t)t * kMaxTileRows + l.lane] = (double)D[l.dbase];  // E^j = shp(r, T)
     }
   }
 }
@@ -2257,9 +2555,13 @@ __global__ void __launch_bounds__(256) seq_bound_kernel(const TileDesc *tiles, i
   if (t >= n_tiles) return;
   const int nl = tiles[t].n_lanes;
   double s = 0.0;
-  for (int l = 0; l < nl; ++l) s += e_lane[(int64_t)t * 32 + l];
+  for (int l = 0; l < nl; ++l) s += e_lane[(int64_t)t * kMaxTileRows + l];
   lb_part[t] = s;
 }
+
+template <typename T>
+__device__ __forceinline__ void dist_dp_row(const SeqArgs &a, const TileDesc &d, const int lane, const int L,
+                                            const int K, const int32_t forward);
 
 // one thread per (tile, lane): the store-design distances from the current lambda
 template <typename T>
@@ -2268,8 +2570,14 @@ __global__ void __launch_bounds__(256) dist_dp_kernel(const SeqArgs a, int32_t n
   const int32_t t = (int32_t)(g >> 5), lane = (int32_t)(g & 31);
   if (t >= n_tiles) return;
   const TileDesc &d = a.tiles[t];
-  if (lane >= d.lanes) return;
   const int L = d.lanes, K = d.K;
+  for (int l = lane; l < L; l += 32)  // (tiles of 64 / 128 rows: several rows per thread)
+    dist_dp_row<T>(a, d, l, L, K, forward);
+}
+
+template <typename T>
+__device__ __forceinline__ void dist_dp_row(const SeqArgs &a, const TileDesc &d, const int lane, const int L,
+                                            const int K, const int32_t forward) {
   const int32_t *ho = a.hop_off + d.hop_base;
   const int ts = (d.kind & 1) ? L : 1;
   const uint32_t *tp = a.topo + d.topo_base + ((d.kind & 1) ? lane : 0);
@@ -2304,19 +2612,26 @@ __global__ void __launch_bounds__(256) dist_dp_kernel(const SeqArgs a, int32_t n
 
 // ---------------------------------------------------------------- launchers
 
-template <typename T, bool RC>
-static const void *sweep_fn(int mode, bool rec) {
+template <typename T, bool RC, int RW>
+static const void *sweep_fn_rw(int mode, bool rec) {
   if (mode == kForward)
-    return rec ? (const void *)sweep_kernel<T, kForward, true, RC> : (const void *)sweep_kernel<T, kForward, false, RC>;
+    return rec ? (const void *)sweep_kernel<T, kForward, true, RC, RW> : (const void *)sweep_kernel<T, kForward, false, RC, RW>;
   if (mode == kBackward)
-    return rec ? (const void *)sweep_kernel<T, kBackward, true, RC> : (const void *)sweep_kernel<T, kBackward, false, RC>;
-  if (mode == kCfr) return RC ? nullptr : (const void *)sweep_kernel<T, kCfr, false, false>;
-  return (const void *)sweep_kernel<T, kEnergy, false, RC>;
+    return rec ? (const void *)sweep_kernel<T, kBackward, true, RC, RW> : (const void *)sweep_kernel<T, kBackward, false, RC, RW>;
+  if (mode == kCfr) return RC ? nullptr : (const void *)sweep_kernel<T, kCfr, false, false, RW>;
+  return (const void *)sweep_kernel<T, kEnergy, false, RC, RW>;
 }
 
-static const void *sweep_ptr(int precision, int mode, bool rec, bool rc) {
-  if (precision == 64) return rc ? sweep_fn<double, true>(mode, rec) : sweep_fn<double, false>(mode, rec);
-  return rc ? sweep_fn<float, true>(mode, rec) : sweep_fn<float, false>(mode, rec);
+template <typename T, bool RC>
+static const void *sweep_fn(int mode, bool rec, int rw) {
+  if (rw >= 4 && sizeof(T) == 4) return sweep_fn_rw<T, RC, 4>(mode, rec);  // (fp64 plans stop at 2 rows per lane)
+  if (rw >= 2) return sweep_fn_rw<T, RC, 2>(mode, rec);
+  return sweep_fn_rw<T, RC, 1>(mode, rec);
+}
+
+static const void *sweep_ptr(int precision, int mode, bool rec, bool rc, int rw) {
+  if (precision == 64) return rc ? sweep_fn<double, true>(mode, rec, rw) : sweep_fn<double, false>(mode, rec, rw);
+  return rc ? sweep_fn<float, true>(mode, rec, rw) : sweep_fn<float, false>(mode, rec, rw);
 }
 
 // The dynamic shared-memory limit is a per-function attribute shared by every
@@ -2330,8 +2645,8 @@ static cudaError_t allow_max_smem(const void *f) {
   return e;
 }
 
-int sweep_occupancy(int precision, int mode, bool rec, bool rc, int block, size_t smem, int *blocks_per_sm) {
-  const void *f = sweep_ptr(precision, mode, rec, rc);
+int sweep_occupancy(int precision, int mode, bool rec, bool rc, int rw, int block, size_t smem, int *blocks_per_sm) {
+  const void *f = sweep_ptr(precision, mode, rec, rc, rw);
   if (!f) return 0;
   cudaError_t e = allow_max_smem(f);
   if (e != cudaSuccess) return (int)e;
@@ -2394,7 +2709,7 @@ int preload_kernels(int precision) {
   for (int mode = 0; mode < 4 && e == cudaSuccess; ++mode)
     for (int rec = 0; rec < 2 && e == cudaSuccess; ++rec)
       for (int rc = 0; rc < 2 && e == cudaSuccess; ++rc) {
-        e = load(sweep_ptr(precision, mode, rec != 0, rc != 0));
+        for (int rw = 1; rw <= 4 && e == cudaSuccess; rw *= 2) e = load(sweep_ptr(precision, mode, rec != 0, rc != 0, rw));
         if (e == cudaSuccess && !rc)
           e = load(precision == 64 ? stream_fn<double>(mode, rec != 0) : stream_fn<float>(mode, rec != 0));
         if (e == cudaSuccess && !rc)
@@ -2411,9 +2726,9 @@ int preload_kernels(int precision) {
   return (int)e;
 }
 
-int launch_sweep(int precision, int mode, bool rec, bool rc, const SweepArgs &a, int grid, int block, size_t smem,
-                 void *stream) {
-  const void *f = sweep_ptr(precision, mode, rec, rc);
+int launch_sweep(int precision, int mode, bool rec, bool rc, int rw, const SweepArgs &a, int grid, int block,
+                 size_t smem, void *stream) {
+  const void *f = sweep_ptr(precision, mode, rec, rc, rw);
   if (!f) return (int)cudaErrorInvalidValue;
   void *args[] = {(void *)&a};
   return launch_pdl(f, dim3(grid), dim3(block), smem, stream, args);
@@ -2551,10 +2866,11 @@ __global__ void __launch_bounds__(256) dist_sentinel_kernel(const TileDesc *tile
   const int32_t t = (int32_t)(g >> 5), lane = (int32_t)(g & 31);
   if (t >= n_tiles) return;
   const TileDesc &d = tiles[t];
-  if (lane >= d.lanes) return;
-  T *top = dist + d.dist_base + (int64_t)d.nodes * d.lanes + lane;
-  top[0] = T(0);
-  top[d.lanes] = t_inf<T>();
+  for (int l = lane; l < d.lanes; l += 32) {
+    T *top = dist + d.dist_base + (int64_t)d.nodes * d.lanes + l;
+    top[0] = T(0);
+    top[d.lanes] = t_inf<T>();
+  }
 }
 
 int launch_dist_sentinels(int precision, const TileDesc *tiles, int32_t n_tiles, void *dist, void *stream) {

@@ -611,6 +611,24 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       else P.row_shape[j] = -1;
     }
   tm.mark("shard");
+  // variables held by two or more ranks (the exchange vector, below) and the
+  // "boundary" rows that hold one: their tiles are swept after the others, so
+  // that the exchange of a pass overlaps the sweep of the interior tiles
+  //
+  std::vector<uint8_t> multi(world > 1 ? p->n_vars : 0, 0);
+  std::vector<uint8_t> boundary_row(world > 1 ? p->n_cons : 0, 0);
+  if (world > 1) {
+    std::vector<int32_t> first(p->n_vars, -1);
+    for (int32_t j = 0; j < p->n_cons; ++j)
+      for (int64_t q = P.row_ptr[j]; q < P.row_ptr[j + 1]; ++q) {
+        const int32_t i = P.col_var[q];
+        if (first[i] < 0) first[i] = P.owner[j];
+        else if (first[i] != P.owner[j]) multi[i] = 1;
+      }
+    for (int32_t j : P.local_rows)
+      for (int64_t q = P.row_ptr[j]; q < P.row_ptr[j + 1]; ++q)
+        if (multi[P.col_var[q]]) boundary_row[j] = 1;
+  }
   // ---------------------------------------------------------------- packing
   P.max_hops = 0;
   P.max_width = 0;
@@ -632,7 +650,35 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // families there put a variable's two slots at the same lane of two tiles,
   // which the averaging kernel reads coalesced (GM, QAP).
   std::vector<std::vector<int32_t>> by_shape(P.shapes.size());
-  for (int32_t j : P.local_rows) by_shape[P.row_shape[j]].push_back(j);
+  std::vector<int32_t> coop_rows;  // rows of shapes wider than kCoopWidth: one cooperative tile each
+  for (int32_t j : P.local_rows) {
+    if (P.shapes[P.row_shape[j]].max_w > kCoopWidth) coop_rows.push_back(j);
+    else by_shape[P.row_shape[j]].push_back(j);
+  }
+  // Rows per lane (kernels.cu mask_tile): staged arc-mask tiles of a short
+  // shape hold 32 R rows, lane l the rows l + 32 k.  The per-tile work (claim,
+  // descriptor, TMA issue, bound partial) and the per-hop tail, addresses and
+  // loop control are shared by the R rows, and the R hop chains are
+  // independent.  R = 4 for K <= 4 (fp32), 2 for K <= 16 (when the shape fills
+  // such a tile), when the budget model below prefers them; not for small
+  // problems (fused path) or the streaming kernel.  FDOG_WIDE=0 / 1 (tests and
+  // A/B runs): never / whenever eligible.
+  const char *sw = getenv("FDOG_SWEEP");
+  const char *fz = getenv("FDOG_FUSED");
+  const char *wd = getenv("FDOG_WIDE");
+  const bool wide_force = wd && wd[0] == '1';
+  // (measured, same box: MRF-LP 0.650 -> 0.579 ms per iteration, Potts-cut
+  // 0.701 -> 0.593; with a few tiles per warp -- GM-worms 6 k tiles, cell
+  // tracking 17 k -- the longer tiles cost more in the tail than they save:
+  // GM 40.9 -> 45.7 us.  So: problems of at least 10^6 rows.)
+  const bool wide_ok = (wide_force || P.local_rows.size() >= 1000000) && P.n_slots > (1 << 15) && !(sw && sw[0] == 's') && !(fz && fz[0] == '1') && !(wd && wd[0] == '0');
+  auto rows_per_lane = [&](size_t sh) -> int {
+    const Shape &S = P.shapes[sh];
+    if (!wide_ok || S.max_w > 2) return 1;
+    int R = (S.k <= 4 && !(o && o->precision == 64)) ? 4 : S.k <= 16 ? 2 : 1;  // (fp64: at most 2)
+    while (R > 1 && by_shape[sh].size() < (size_t)(32 * R)) R /= 2;
+    return R;
+  };
   std::vector<char> pair_room(P.shapes.size(), 0);  // bundle order: stages reserve room for a pair list
   {
     const char *pe = getenv("FDOG_PAIRS");
@@ -654,7 +700,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
           const int32_t i = p->col_var[q];
           if (P.deg_global[i] != 2) continue;
           slots2++;
-          const int64_t code = tag | (int64_t)(r / 32);
+          const int64_t code = tag | (int64_t)(r / (32 * rows_per_lane(sh)));
           if (seen[i] >= 0 && (seen[i] >> 40) == (int64_t)sh) same += seen[i] == code;
           else seen[i] = code;
         }
@@ -686,12 +732,17 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // a packing-structure assertion of test_edge_cases: open)
   const char *pt = getenv("FDOG_PARTIAL");
   const bool partial_ok = pt && pt[0] == '1';
+  // (world > 1: a shape's boundary rows after its interior rows, stable)
+  if (world > 1)
+    for (auto &rows : by_shape)
+      std::stable_partition(rows.begin(), rows.end(), [&](int32_t j) { return !boundary_row[j]; });
   struct PendingTile {
     int kind;                    // bit 0 per-lane topology, bit 1 staged
     int32_t shape;               // kind 0
     int L;
     std::vector<int32_t> rows;   // lanes
     int64_t cost;
+    bool boundary = false;       // holds a row with an exchanged variable
   };
   // pack(rc): budget + tiles for the store design (rc = false) or the
   // recompute design (rc = true, narrow shapes only); returns the tiles in
@@ -703,10 +754,11 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB, bool pr = false) {
       const int pb = pr ? stage_pairs_bytes(K * L / 2) : 0;
       if (rc) return stage_bytes_rc(tsz, kind, K, nodes, L) + pb <= SB && stage_dist_bytes(tsz, nodes, L) <= DB;
-      return stage_bytes(tsz, kind, K, nodes, L) + pb <= SB && relax_bytes(tsz, W, L) <= DB;
+      // (arc-mask tiles never use the relaxation buffers)
+      return stage_bytes(tsz, kind, K, nodes, L) + pb <= SB && ((kind & 4) || relax_bytes(tsz, W, L) <= DB);
     };
-    auto lanes_for = [&](int kind, int K, int nodes, int W, int SB, int DB, bool pr = false) {
-      for (int L = 32; L >= 4; L /= 2)
+    auto lanes_for = [&](int kind, int K, int nodes, int W, int SB, int DB, bool pr = false, int Lmax = 32) {
+      for (int L = Lmax; L >= 4; L /= 2)
         if (fits(kind, K, nodes, W, L, SB, DB, pr)) return L;
       return 0;
     };
@@ -735,8 +787,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
           const Shape &S = P.shapes[s];
           const int k0 = S.max_w <= 2 ? 4 : 0;  // arc-mask tiles for narrow shapes
           const bool pr = k0 && pair_room[s];
-          int L = lanes_for(k0, S.k, S.nodes(), S.max_w, SB, DB, pr);
-          double pen = 1.0;
+          int L = lanes_for(k0, S.k, S.nodes(), S.max_w, SB, DB, pr, 32 * rows_per_lane(s));
+          double pen = (wide_force && L > 0 && L < 32 * rows_per_lane(s)) ? 1e6 : 1.0;
           if (L == 0) {  // direct from global memory: latency-bound
             L = 32;
             // (the recompute design cannot run direct tiles at all: a budget
@@ -748,11 +800,15 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
             if (rc) usedDB = std::max(usedDB, stage_dist_bytes(tsz, S.nodes(), L));
           }
           const double tiles = std::ceil((double)by_shape[s].size() / L);
+          const double R = L > 32 ? L / 32 : 1;  // rows per lane: R chains per tile
           // per-tile sequential chain and issued instructions (the recompute
           // design adds the on-chip distance pass)
           const double cn = rc ? 70.0 : 50.0, ck = rc ? 160.0 : 120.0, in = rc ? 30.0 : 20.0, ik = rc ? 50.0 : 35.0;
-          chain += pen * tiles * (cn * S.nodes() + ck * S.k + (P.NB == 1 ? 1500.0 : 0.0));
-          instr += tiles * (in * S.nodes() + ik * S.k);
+          // (R chains per lane overlap: ~1 + 0.4 (R - 1) of one chain's
+          // latency; the per-tile instructions -- claim, descriptor, TMA
+          // issue, bound partial, ~500 per tile on MRF-LP -- are shared)
+          chain += pen * tiles * ((1.0 + 0.4 * (R - 1)) * (cn * S.nodes() + ck * S.k) + (P.NB == 1 ? 1500.0 : 0.0));
+          instr += tiles * (500.0 + R * 0.55 * (in * S.nodes() + ik * S.k));
         }
         if (!rc) usedDB = DB;
         const int wb = warp_bytes(usedSB, usedDB, P.NB);
@@ -774,7 +830,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       auto &rows = by_shape[s];
       const Shape &S = P.shapes[s];
       const int k0 = S.max_w <= 2 ? 4 : 0;
-      int L = lanes_for(k0, S.k, S.nodes(), S.max_w, P.SB, P.DB, k0 && pair_room[s]);
+      int L = lanes_for(k0, S.k, S.nodes(), S.max_w, P.SB, P.DB, k0 && pair_room[s], 32 * rows_per_lane(s));
       const bool staged = L > 0;
       if (!staged) L = 32;
       // (rows too long to stage, of a narrow shape: the last tile keeps the
@@ -785,22 +841,26 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       // that holds them, instead of a per-lane-topology tile -- that path
       // walks the topology node by node and its tile became the last to
       // finish: QAP50 36 us against 28 for every other warp)
+      // (tiles of 32 R rows: the rest of the shape in 32-row tiles, then as above)
       size_t full = rows.size() / L * L;
-      if (k0 && (!staged || (rows.size() >= (size_t)L && partial_ok))) full = rows.size();
-      for (size_t q = 0; q < full; q += L) {
+      const size_t wide_end = full;
+      if (L > 32) full += (rows.size() - full) / 32 * 32;
+      if (k0 && (!staged || (rows.size() >= (size_t)std::min(L, 32) && partial_ok))) full = rows.size();
+      for (size_t q = 0; q < full;) {
         PendingTile t;
         const bool ch = k0 && chain_shape(S);
         t.kind = (staged ? 2 : 0) | k0 | (ch ? 8 : 0) | (ch && ends_shape(S) ? 16 : 0);  // records also serve the streaming kernel
         t.shape = (int32_t)s;
-        t.L = L;
-        const size_t nrow = std::min(rows.size() - q, (size_t)L);
-        if (staged && nrow < (size_t)L) {
+        t.L = q < wide_end ? L : std::min(L, 32);
+        const size_t nrow = std::min(rows.size() - q, (size_t)t.L);
+        if (staged && nrow < (size_t)t.L) {
           t.L = 4;
           while ((size_t)t.L < nrow) t.L *= 2;
         }
-        t.rows.assign(rows.begin() + q, rows.begin() + std::min(rows.size(), q + L));
+        t.rows.assign(rows.begin() + q, rows.begin() + q + nrow);
         t.cost = (int64_t)S.nodes() + S.k;
         pend.push_back(std::move(t));
+        q += nrow;
       }
       pool.insert(pool.end(), rows.begin() + full, rows.end());
     }
@@ -859,23 +919,37 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       t.cost = c + K;
       pend.push_back(std::move(t));
     }
+    for (int32_t j : coop_rows) {
+      PendingTile t;
+      t.kind = 32;
+      t.shape = P.row_shape[j];
+      t.L = 1;
+      t.rows = {j};
+      t.cost = (int64_t)P.shapes[t.shape].nodes() / 8 + P.shapes[t.shape].k;  // (32 lanes split the nodes)
+      pend.push_back(std::move(t));
+    }
     // direct tiles first (slowest), then expensive tiles, so the dynamic
     // scheduler does not leave them for the tail
+    if (world > 1)
+      for (auto &t : pend)
+        for (int32_t j : t.rows) t.boundary = t.boundary || boundary_row[j];
     std::stable_sort(pend.begin(), pend.end(), [](const PendingTile &a, const PendingTile &b) {
+      if (a.boundary != b.boundary) return b.boundary;  // interior tiles first
       const bool da = !(a.kind & 2), db = !(b.kind & 2);
       if (da != db) return da;
-      return a.cost * 32 / a.L > b.cost * 32 / b.L;
+      // (a tile of L < 32 rows takes about as long as a full one; a tile of
+      // 32 R rows about R times as long)
+      auto key = [](const PendingTile &t) { return t.L >= 32 ? t.cost * t.L / 32 : t.cost * 32 / t.L; };
+      return key(a) > key(b);
     });
 
     return pend;
   };
   tm.mark("group by shape");
-  bool narrow = true;
+  bool narrow = coop_rows.empty();
   for (size_t s = 0; s < P.shapes.size(); ++s)
     if (!by_shape[s].empty()) narrow = narrow && P.shapes[s].max_w <= 2;
   // design choice (experiment knobs: FDOG_SWEEP = rc | tma | stream; FDOG_FUSED)
-  const char *sw = getenv("FDOG_SWEEP");
-  const char *fz = getenv("FDOG_FUSED");
   // The recompute design halves the HBM bytes of a pass at ~30 % more
   // instructions.  When the store design's per-pass working set (distances +
   // slot data) stays resident in the 126 MB L2 across the four kernels of an
@@ -915,6 +989,10 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   P.slot_var.clear();
   P.tiles_shared = 0;
   P.direct_tiles = 0;
+  P.n_interior_tiles = 0;
+  P.coop_tiles = 0;
+  P.coop_w = 0;
+  P.direct_w = 0;
   P.max_tile_nodes = 0;
   std::vector<int64_t> shape_topo(P.shapes.size(), -1);
   std::vector<int32_t> shape_hop(P.shapes.size(), -1);
@@ -934,7 +1012,33 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     d.lanes = L;
     d.slot_base = slot_base;
     d.dist_base = dist_base;
-    if (!(t.kind & 1)) {
+    if (t.kind & 32) {
+      // cooperative tile: uint2 topology (absolute 32-bit child indices), per shape
+      if (shape_topo[t.shape] < 0) {
+        pad16(P.topo);
+        pad16(P.hop_off);
+        shape_topo[t.shape] = (int64_t)P.topo.size();
+        shape_hop[t.shape] = (int32_t)P.hop_off.size();
+        const int32_t nn = S0.nodes();
+        auto code = [&](uint16_t rel, int32_t next) -> uint32_t {
+          return rel == kBot ? (uint32_t)nn + 1 : rel == kTop ? (uint32_t)nn : (uint32_t)(next + rel);
+        };
+        for (int32_t h = 0; h < S0.k; ++h)
+          for (int32_t n = S0.hop_start[h]; n < S0.hop_start[h + 1]; ++n) {
+            P.topo.push_back(code(S0.lo[n], S0.hop_start[h + 1]));
+            P.topo.push_back(code(S0.hi[n], S0.hop_start[h + 1]));
+          }
+        for (int32_t h = 0; h <= S0.k; ++h) P.hop_off.push_back(S0.hop_start[h]);
+        pad16(P.topo);
+        pad16(P.hop_off);
+      }
+      d.topo_base = shape_topo[t.shape] / 2;  // in uint2 units
+      d.hop_base = shape_hop[t.shape];
+      d.nodes = S0.nodes();
+      d.max_w = S0.max_w;
+      P.coop_tiles++;
+      P.coop_w = std::max(P.coop_w, S0.max_w);
+    } else if (!(t.kind & 1)) {
       if (shape_topo[t.shape] < 0) {
         pad16(P.topo);
         pad16(P.hop_off);
@@ -1000,7 +1104,11 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         }
       }
     }
-    if (!(t.kind & 2)) P.direct_tiles++;
+    if (!t.boundary) P.n_interior_tiles++;
+    if (!(t.kind & 2)) {
+      P.direct_tiles++;
+      if (!(t.kind & 32)) P.direct_w = std::max(P.direct_w, d.max_w);
+    }
     P.max_tile_nodes = std::max(P.max_tile_nodes, d.nodes);
     // slots
     P.slot_var.resize((size_t)(slot_base + (int64_t)d.K * L), -1);
@@ -1011,15 +1119,25 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       const int32_t *vars = P.col_var.data() + P.row_ptr[j];
       for (int32_t h = 0; h < d.K; ++h) P.slot_var[slot_base + (int64_t)h * L + l] = vars[h];
     }
-    slot_base += (int64_t)d.K * L;
-    dist_base += (int64_t)(d.nodes + 2) * L;
+    // (bases stay multiples of 4 elements -- 16-byte aligned TMA sources --
+    // after a one-BDD cooperative tile too; the gap is padding)
+    slot_base = (slot_base + (int64_t)d.K * L + 3) & ~(int64_t)3;
+    dist_base = (dist_base + (int64_t)(d.nodes + 2) * L + 3) & ~(int64_t)3;
     P.tiles.push_back(d);
+  }
+  // cooperative tiles: two relaxation buffers of coop_w + 1 entries, in the
+  // warp's DB region when they fit 32 KB (else in the solver's scratch)
+  P.coop_smem = false;
+  if (P.coop_tiles > 0 && 2 * (P.coop_w + 1) * tsz <= 32768) {
+    P.DB = std::max(P.DB, r16(2 * (P.coop_w + 1) * tsz));
+    P.coop_smem = true;
   }
   pad16(P.topo);
   P.topo.resize(P.topo.size() + 4, 0);  // 16-byte reads of the last topology may run past it
+  P.slot_var.resize((size_t)slot_base, -1);
   P.n_dist = dist_base;
   for (const auto &d : P.tiles)
-    if (d.nodes + 1 > 0xFFFF) {
+    if (!(d.kind & 32) && d.nodes + 1 > 0xFFFF) {
       set_error("a BDD tile has %d nodes; the 16-bit topology codes allow 65534", d.nodes);
       return FDOG_ETOOBIG;
     }
@@ -1140,14 +1258,6 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   if (world > 1) {
     // the exchange vector must be identical on every rank: all variables held
     // by >= 2 ranks, ascending; this rank contributes zeros for those it lacks
-    std::vector<int32_t> first(p->n_vars, -1);
-    std::vector<uint8_t> multi(p->n_vars, 0);
-    for (int32_t j = 0; j < p->n_cons; ++j)
-      for (int64_t q = P.row_ptr[j]; q < P.row_ptr[j + 1]; ++q) {
-        int32_t i = P.col_var[q];
-        if (first[i] < 0) first[i] = P.owner[j];
-        else if (first[i] != P.owner[j]) multi[i] = 1;
-      }
     for (int32_t i = 0; i < p->n_vars; ++i)
       if (multi[i]) P.shared_vars.push_back(i);
     std::vector<int32_t> xpos(p->n_vars, -1);
@@ -1509,6 +1619,8 @@ fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out) {
   out->sweep_smem_per_warp = warp_bytes(P.SB, P.DB, P.NB);
   out->h2d_bytes = (int64_t)P.image.bytes;
   out->tile_pairs = (int64_t)(P.ell.size() / 2) - P.n_ell_open;
+  out->interior_tiles = P.world > 1 ? P.n_interior_tiles : (int64_t)P.tiles.size();
+  out->coop_tiles = P.coop_tiles;
   return FDOG_OK;
 }
 

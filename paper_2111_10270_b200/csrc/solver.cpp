@@ -74,8 +74,18 @@ struct fdog_solver {
   size_t region_stride = 0;  // bytes per partial-sum buffer
   bool peer = false;
   int32_t peer_par = 0;      // parity of the next pass's buffer
+  // world > 1: the exchange of a pass runs on xstream while the interior tiles
+  // [0, n_int) sweep on stream; the boundary tiles wait for it
+  int64_t n_int = 0;
+  bool overlap_ok = true;
+  cudaStream_t xstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   PeerArgs peer_args{};
   bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
+  int rw = 1;                // most rows per lane of any tile (sweep_kernel instantiation)
+  int32_t coop_bw = 0;       // cooperative tiles: relaxation buffer entries
+  bool coop_smem = false;
+  int64_t n_coop = 0;
   bool chunk_mode = false;   // ... or sweep_chunk_kernel (every tile an arc-mask tile)
   bool rc = false;           // recompute design (Plan::rc): no distance traffic, no dist_state
   bool dbar_zero = true;     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
@@ -206,18 +216,19 @@ cudaEvent_t get_event(fdog_solver *s) {
 struct Timed {
   fdog_solver *s;
   int k;
+  cudaStream_t st;
   cudaEvent_t a = nullptr;
-  Timed(fdog_solver *s_, int k_) : s(s_), k(k_) {
+  Timed(fdog_solver *s_, int k_, cudaStream_t st_ = nullptr) : s(s_), k(k_), st(st_ ? st_ : s_->stream) {
     s->launches++;
     if (s->profile) {
       a = get_event(s);
-      cudaEventRecord(a, s->stream);
+      cudaEventRecord(a, st);
     }
   }
   ~Timed() {
     if (s->profile) {
       cudaEvent_t b = get_event(s);
-      cudaEventRecord(b, s->stream);
+      cudaEventRecord(b, st);
       s->events.push_back({k, a, b});
     }
   }
@@ -225,11 +236,21 @@ struct Timed {
 
 SweepArgs sweep_args(fdog_solver *s, double omega);
 
-fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
+// one sweep over tiles [t0, t1) (default: all)
+fdog_status run_sweep(fdog_solver *s, int mode, double omega, int64_t t0 = 0, int64_t t1 = -1) {
+  if (t1 < 0) t1 = s->n_tiles;
+  if (t1 <= t0 && s->n_tiles > 0) return FDOG_OK;
   SweepArgs a = sweep_args(s, omega);
+  a.tiles += t0;
+  a.lb_part += t0;
+  a.n_tiles = (int32_t)(t1 - t0);
   const bool rec = s->record_mm && (mode == kForward || mode == kBackward);
   int e;
-  if (mode != kForward && mode != kBackward) {
+  if (t0 > 0) {
+    // the second sweep of a split pass: its own claim counter
+    a.tile_counter = s->d_counter + 2;
+    CK(cudaMemsetAsync(s->d_counter + 2, 0, sizeof(unsigned int), s->stream), "memset");
+  } else if (mode != kForward && mode != kBackward) {
     // not preceded by avg_kernel: reset the dynamic tile counter here
     CK(cudaMemsetAsync(s->d_counter + 1, 0, sizeof(unsigned int), s->stream), "memset");
   }
@@ -239,8 +260,11 @@ fdog_status run_sweep(fdog_solver *s, int mode, double omega) {
       e = launch_sweep_chunk(s->precision, mode, rec, a, s->stream);
     else if (s->stream_mode && (mode == kForward || mode == kBackward))
       e = launch_sweep_stream(s->precision, mode, rec, a, s->stream);
-    else
-      e = launch_sweep(s->precision, mode, rec, s->rc, a, s->grid, s->block, s->smem, s->stream);
+    else {
+      const int64_t warps = s->block / 32;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(s->grid, (a.n_tiles + warps - 1) / warps));
+      e = launch_sweep(s->precision, mode, rec, s->rc, s->rw, a, grid, s->block, s->smem, s->stream);
+    }
   }
   if (e) return cuda_fail((cudaError_t)e, "sweep launch");
   s->lb_dirty = true;
@@ -283,18 +307,21 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.trace = s->d_trace;
   a.scratch = s->d_scratch;  // relaxation buffers of direct (unstaged) tiles
   a.scratch_stride = s->scratch_stride;
+  a.coop_bw = s->coop_bw;
+  a.coop_smem = s->coop_smem ? 1 : 0;
   return a;
 }
 
 AvgArgs avg_args(fdog_solver *s);
 
-fdog_status run_avg_finish(fdog_solver *s) {
+fdog_status run_avg_finish(fdog_solver *s, cudaStream_t st = nullptr) {
   if (s->world <= 1 || s->n_shared <= 0) return FDOG_OK;
+  if (!st) st = s->stream;
   AvgArgs a = avg_args(s);
   int e;
   {
-    Timed t(s, kKAvgFinish);
-    e = launch_avg_finish(s->precision, a, s->n_shared, s->d_x_local, s->d_x_deg, s->stream);
+    Timed t(s, kKAvgFinish, st);
+    e = launch_avg_finish(s->precision, a, s->n_shared, s->d_x_local, s->d_x_deg, st);
   }
   if (e) return cuda_fail((cudaError_t)e, "avg_finish launch");
   return FDOG_OK;
@@ -303,14 +330,15 @@ fdog_status run_avg_finish(fdog_solver *s) {
 // peer-memory exchange of one pass (after run_avg published this rank's
 // partials): wait for the peers', sum them in rank order over NVLink, scatter
 // the averages
-fdog_status run_peer_exchange(fdog_solver *s) {
+fdog_status run_peer_exchange(fdog_solver *s, cudaStream_t st = nullptr) {
+  if (!st) st = s->stream;
   AvgArgs a = avg_args(s);
   PeerArgs pa = s->peer_args;
   pa.buf_off = kRegionBuf + (int64_t)s->peer_par * (int64_t)s->region_stride;
   int e;
   {
-    Timed t(s, kKAvgFinish);
-    e = launch_peer_finish(s->precision, a, s->n_shared, s->d_x_local, s->d_x_deg, pa, s->stream);
+    Timed t(s, kKAvgFinish, st);
+    e = launch_peer_finish(s->precision, a, s->n_shared, s->d_x_local, s->d_x_deg, pa, st);
   }
   if (e) return cuda_fail((cudaError_t)e, "peer exchange launch");
   s->peer_par ^= 1;
@@ -357,21 +385,35 @@ fdog_status run_avg(fdog_solver *s) {
     s->launches++;
     return FDOG_OK;
   }
-  if (s->world > 1 && s->n_shared > 0 && !s->external) {
-    int r;
-    {
-      Timed t(s, kKAllreduce);
-      s->launches--;  // not our kernel
-      r = s->nccl.allreduce(s->d_xbuf, s->d_xbuf, (size_t)s->n_shared, s->precision == 64 ? kNcclFloat64 : kNcclFloat32,
-                            kNcclSum, s->nccl.comm, s->stream);
-    }
-    if (r) {
-      set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(r) : "error");
-      return FDOG_ENCCL;
-    }
-    return run_avg_finish(s);
-  }
   return FDOG_OK;
+}
+
+// the exchange step of a pass (P:641 across ranks) on stream st:
+// ncclAllReduce of the shared partial sums + avg_finish, or the peer-memory
+// sum + scatter
+fdog_status run_exchange(fdog_solver *s, cudaStream_t st) {
+  if (s->world <= 1 || s->n_shared <= 0) return FDOG_OK;
+  if (s->peer) return run_peer_exchange(s, st);
+  if (s->external) return run_avg_finish(s, st);  // (the caller summed the partials)
+  int r;
+  {
+    Timed t(s, kKAllreduce, st);
+    s->launches--;  // not our kernel
+    r = s->nccl.allreduce(s->d_xbuf, s->d_xbuf, (size_t)s->n_shared, s->precision == 64 ? kNcclFloat64 : kNcclFloat32,
+                          kNcclSum, s->nccl.comm, st);
+  }
+  if (r) {
+    set_error("ncclAllReduce: %s", s->nccl.errstr ? s->nccl.errstr(r) : "error");
+    return FDOG_ENCCL;
+  }
+  return run_avg_finish(s, st);
+}
+
+// the exchange overlaps the interior tiles' sweep (NCCL or peer exchange with
+// boundary tiles; FDOG_OVERLAP=0 runs it first, on the solver's stream)
+bool overlapped(const fdog_solver *s) {
+  return s->world > 1 && s->n_shared > 0 && (s->peer || !s->external) && s->n_int > 0 && s->n_int < s->n_tiles &&
+         s->overlap_ok;
 }
 
 // stage 0: conversions + averaging (partials of the exchanged variables in
@@ -386,13 +428,24 @@ fdog_status pass_stage(fdog_solver *s, bool forward, double omega, int stage) {
     if (!s->rc && !forward && s->dist_state != 1 && (st = run_sweep(s, kCfr, omega))) return st;
     return run_avg(s);
   }
-  if (s->peer && s->n_shared > 0) {
-    if ((st = run_peer_exchange(s))) return st;
-  } else if (s->external && (st = run_avg_finish(s))) {
-    return st;
+  const int mode = forward ? kForward : kBackward;
+  if (overlapped(s)) {
+    if (!s->xstream) {
+      CK(cudaStreamCreateWithFlags(&s->xstream, cudaStreamNonBlocking), "cudaStreamCreate");
+      CK(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+      CK(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    CK(cudaEventRecord(s->ev_fork, s->stream), "cudaEventRecord");
+    CK(cudaStreamWaitEvent(s->xstream, s->ev_fork, 0), "cudaStreamWaitEvent");
+    if ((st = run_exchange(s, s->xstream))) return st;
+    CK(cudaEventRecord(s->ev_join, s->xstream), "cudaEventRecord");
+    if ((st = run_sweep(s, mode, omega, 0, s->n_int))) return st;  // interior tiles: no exchanged variable
+    CK(cudaStreamWaitEvent(s->stream, s->ev_join, 0), "cudaStreamWaitEvent");
+    if ((st = run_sweep(s, mode, omega, s->n_int, s->n_tiles))) return st;
+  } else {
+    if ((st = run_exchange(s, s->stream))) return st;
+    if ((st = run_sweep(s, mode, omega))) return st;
   }
-  st = run_sweep(s, forward ? kForward : kBackward, omega);
-  if (st) return st;
   s->dist_state = s->rc ? 2 : (forward ? 1 : 0);  // (the recompute design keeps no distances in HBM)
   s->cur ^= 1;  // mbar <- m
   s->passes++;
@@ -433,7 +486,7 @@ fdog_status seq_schedule(fdog_solver *s) {
     for (int64_t x = 0; x < (int64_t)d.K * d.lanes; ++x) slot_tile[d.slot_base + x] = t;
   }
   const size_t bytes = slot_tile.size() * 4 + 2 * ((size_t)(n + 1) * 8 + (size_t)std::max<int64_t>(S, 1) * 4) +
-                       (size_t)std::max(s->n_tiles, 1) * 32 * 8 + 8 * 256;  // + alignment of six sections
+                       (size_t)std::max(s->n_tiles, 1) * kMaxTileRows * 8 + 8 * 256;  // + alignment of six sections
   unsigned char *base = nullptr;
   CK(cudaMalloc((void **)&base, bytes), "cudaMalloc (seq schedule)");
   s->allocs.push_back(base);
@@ -488,8 +541,8 @@ fdog_status seq_schedule(fdog_solver *s) {
       CK(cudaMemcpyAsync(s->d_seq_slots[dir], slots.data(), slots.size() * 4, cudaMemcpyHostToDevice, s->stream), "H2D");
     CK(cudaStreamSynchronize(s->stream), "sync");  // host vectors go out of scope
   }
-  s->d_e_lane = (double *)carve((size_t)std::max(s->n_tiles, 1) * 32 * 8);
-  CK(cudaMemsetAsync(s->d_e_lane, 0, (size_t)std::max(s->n_tiles, 1) * 32 * 8, s->stream), "memset");
+  s->d_e_lane = (double *)carve((size_t)std::max(s->n_tiles, 1) * kMaxTileRows * 8);
+  CK(cudaMemsetAsync(s->d_e_lane, 0, (size_t)std::max(s->n_tiles, 1) * kMaxTileRows * 8, s->stream), "memset");
   s->seq_ready = true;
   return FDOG_OK;
 }
@@ -555,6 +608,12 @@ void free_solver(fdog_solver *s) {
   for (auto e : s->event_pool) cudaEventDestroy(e);
   if (s->graph) cudaGraphExecDestroy(s->graph);
   if (s->seq_graph) cudaGraphExecDestroy(s->seq_graph);
+  if (s->xstream) {
+    cudaStreamSynchronize(s->xstream);
+    cudaStreamDestroy(s->xstream);
+  }
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   for (void *p : s->allocs) cudaFree(p);
   if (s->nccl.comm && s->nccl.destroy) s->nccl.destroy(s->nccl.comm);
   if (s->nccl.lib) dlclose(s->nccl.lib);
@@ -630,7 +689,12 @@ fdog_status init_nccl(fdog_solver *s, const fdog_options *o) {
   }
   nccl_uid uid;
   std::memcpy(uid.internal, o->nccl_unique_id, sizeof uid.internal);
-  int r = s->nccl.init(&s->nccl.comm, s->world, uid, s->rank);
+  // FDOG_NCCL_SELF=1 (test knob, one GPU): a one-rank communicator even for
+  // world > 1 -- the exchange's allreduce is then the identity, which the
+  // tests compare with the external-exchange mode doing the same
+  const char *ns = getenv("FDOG_NCCL_SELF");
+  const bool self = ns && ns[0] == '1';
+  int r = s->nccl.init(&s->nccl.comm, self ? 1 : s->world, uid, self ? 0 : s->rank);
   if (r) {
     set_error("ncclCommInitRank: %s", s->nccl.errstr ? s->nccl.errstr(r) : "error");
     return FDOG_ENCCL;
@@ -653,6 +717,8 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   {
     const char *g = getenv("FDOG_GRAPHS");  // experiment knob: FDOG_GRAPHS=0 disables graph replay
     s->use_graphs = !(g && g[0] == '0');
+    const char *ov = getenv("FDOG_OVERLAP");  // test knob: FDOG_OVERLAP=0 runs the exchange before the sweep
+    s->overlap_ok = !(ov && ov[0] == '0');
   }
   s->rank = P.rank;
   s->world = P.world;
@@ -673,6 +739,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->free_term = P.rank == 0 ? P.free_term : 0.0;
   s->n_dev_slots = (int64_t)P.slot_var.size();
   s->n_tiles = (int32_t)P.tiles.size();
+  s->n_int = P.world > 1 ? P.n_interior_tiles : s->n_tiles;
   s->n_varlist = (int32_t)P.var_list.size();
   s->n_shared = (int32_t)P.shared_vars.size();
   s->n_vars = P.n_vars;
@@ -703,7 +770,9 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   if (const char *cf = getenv("FDOG_AVG_CSR_FIRST")) s->csr_first = atoi(cf) ? 1 : 0;
   if (const char *gd = getenv("FDOG_GET_DIRECT")) s->get_direct = gd[0] == '1';
   s->warp_bytes = (size_t)warp_bytes(P.SB, P.DB, P.NB);
+  for (const auto &d : tiles) s->rw = std::max(s->rw, d.lanes / 32);
   s->n_direct = P.direct_tiles;
+  s->n_coop = P.coop_tiles;
   {
     // all tiles narrow: the passes stream from global memory (no staging)
     bool narrow = true;
@@ -735,6 +804,10 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
       return FDOG_EINVAL;
     }
   }
+  if (s->rw > 1 && (s->stream_mode || s->chunk_mode || s->use_fused)) {  // (plan.cpp never packs them so)
+    set_error("tiles of %d rows need the staged sweep kernel", 32 * s->rw);
+    return FDOG_EINVAL;
+  }
   // tile-closed pairs are averaged by sweep_kernel only (the streaming,
   // chunked and fused paths read every average from the averaging kernel)
   s->pairs = P.n_ell_open < (int64_t)(P.ell.size() / 2) && !s->stream_mode && !s->chunk_mode && !s->use_fused &&
@@ -748,7 +821,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   for (int mode = 0; mode < 4; ++mode)
     for (int rec = 0; rec < 2; ++rec) {
       int b = 0;
-      int e = sweep_occupancy(s->precision, mode, rec && mode != kEnergy, s->rc, s->block, s->smem, &b);
+      int e = sweep_occupancy(s->precision, mode, rec && mode != kEnergy, s->rc, s->rw, s->block, s->smem, &b);
       if (e) return cuda_fail((cudaError_t)e, "occupancy");
       if (mode == kForward && rec == (int)s->record_mm) bps = std::max(1, b);
     }
@@ -785,7 +858,12 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     // either way: a grid that is not a multiple of the SM count leaves SMs
     // with different warp counts, i.e. different per-tile times.)
   }
-  s->scratch_stride = (int64_t)relax_slots(s->max_w) * 32;
+  // direct tiles: the lane-serial relaxation buffers (32 lanes); cooperative
+  // tiles: two buffers of coop_w + 1 entries unless they sit in shared memory
+  s->scratch_stride = std::max<int64_t>(P.direct_w > 0 ? (int64_t)relax_slots(P.direct_w) * 32 : 0,
+                                        (P.coop_tiles > 0 && !P.coop_smem) ? 2 * ((int64_t)P.coop_w + 1) : 0);
+  s->coop_bw = P.coop_w + 1;
+  s->coop_smem = P.coop_smem;
 
   fdog_status st;
   s->n_dist = P.n_dist;
@@ -818,8 +896,8 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   const size_t o_xbuf = carve((size_t)std::max<int32_t>(s->n_shared, 1) * s->tsz);
   const size_t o_lbp = carve((size_t)std::max(s->n_tiles, 1) * sizeof(double));
   const size_t o_lb = carve(2 * sizeof(double));
-  const size_t o_ctr = carve(2 * sizeof(unsigned int));
-  const size_t o_scr = carve(s->n_direct ? (size_t)s->grid * (s->block / 32) * s->scratch_stride * s->tsz : 16);
+  const size_t o_ctr = carve(4 * sizeof(unsigned int));  // done, tile claims, split-pass claims
+  const size_t o_scr = carve(std::max<size_t>(s->n_direct ? (size_t)s->grid * (s->block / 32) * s->scratch_stride * s->tsz : 0, 16));
   const size_t o_x = carve((size_t)std::max<int64_t>(P.n_vars, 1));
   const size_t o_und = carve(sizeof(unsigned long long));
   const size_t o_canon = carve((size_t)std::max<size_t>(P.canon_slot.size(), 1) * 8);  // (fp64 when widened)
@@ -941,6 +1019,8 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->st.fused_small = s->use_fused ? (s->fused_smem ? 2 : 1) : 0;
   s->st.sweep_recompute = s->rc ? 1 : 0;
   s->st.tile_pairs = s->pairs ? (int64_t)s->n_ell - s->n_ell_open : 0;
+  s->st.interior_tiles = s->n_int;
+  s->st.coop_tiles = s->n_coop;
 
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;
@@ -1216,6 +1296,11 @@ fdog_status fdog_pass_seq(fdog_solver *s, int32_t forward, double omega) {
     set_error("the non-deferred variant is single-GPU");
     return FDOG_ESTATE;
   }
+  if (s->n_coop > 0) {
+    set_error("the non-deferred variant walks 16-bit topology codes; BDDs wider than %d nodes per partition "
+              "run the deferred passes only", kCoopWidth);
+    return FDOG_EINVAL;
+  }
   if (!s->dbar_zero) {
     set_error("a deferred correction is pending: fdog_finalize first");
     return FDOG_ESTATE;
@@ -1470,9 +1555,11 @@ fdog_status fdog_iterate(fdog_solver *s, int32_t n_iter, double omega) {
     s->dbar_zero = false;
     return FDOG_OK;
   }
-  // CUDA graph of one iteration: used when the passes alternate normally, no
-  // per-kernel events are requested and there is no NCCL exchange
-  const bool graphs = s->use_graphs && !s->profile && s->world == 1 && (s->rc || s->dist_state == 0) && n_iter > 0;
+  // CUDA graph of one iteration: used when the passes alternate normally and
+  // no per-kernel events are requested.  With world > 1 the graph holds the
+  // exchange too (ncclAllReduce is captured, or the peer-memory kernels), forked
+  // onto xstream and joined before the boundary tiles' sweep.
+  const bool graphs = s->use_graphs && !s->profile && (s->rc || s->dist_state == 0) && n_iter > 0;
   if (graphs) {
     if (!s->graph || s->graph_omega != omega || s->graph_cur != s->cur) {
       if (s->graph) {
@@ -1581,7 +1668,7 @@ fdog_status fdog_finalize_averaged(fdog_solver *s) {
   // delta buffer; lambda += that buffer, then both buffers are zero
   s->avg_full = true;
   fdog_status st = run_avg(s);
-  if (!st && s->peer && s->n_shared > 0) st = run_peer_exchange(s);
+  if (!st) st = run_exchange(s, s->stream);
   s->avg_full = false;
   if (st) return st;
   int e;

@@ -398,6 +398,44 @@ def celltrack(seed=0, frames=100, dets=2150, n_trans=5, n_div=3, excl_pairs=None
     return rb.build(nv, np.concatenate(cost), f"celltrack(seed={seed},{frames}x{dets})")
 
 
+def gap(seed=0, jobs=300, agents=20, wmax=100, load=0.6) -> Problem:
+    """Knapsack-style workload (a single constraint may itself be a
+    Knapsack): a generalized assignment problem.  x_ja = 1 if job j goes to
+    agent a, cost U[0, 20); every job on exactly one agent (one-hot rows over the
+    agents) and every agent within capacity, sum_j w_ja x_ja <= C_a with
+    w_ja ~ U{5..wmax} and C_a = load * (jobs / agents) * E[w].  The capacity
+    rows have `jobs` variables and partitions of up to C_a + 1 nodes (hundreds
+    at the defaults): the wide-BDD case of the sweep."""
+    rng = np.random.default_rng(seed)
+    x = np.arange(jobs * agents).reshape(jobs, agents)
+    w = rng.integers(5, wmax + 1, size=(jobs, agents))
+    cap = int(load * jobs / agents * (5 + wmax) / 2)
+    cost = rng.uniform(0, 20, size=jobs * agents)
+    rb = RowBuilder()
+    rb.add(x, np.ones((jobs, agents)), EQ, 1)
+    rb.add(x.T.copy(), w.T.copy(), LE, cap)
+    return rb.build(jobs * agents, cost, f"gap(seed={seed},{jobs}x{agents},w<={wmax},cap={cap})")
+
+
+def mckp(seed=0, classes=20_000, items=8, knaps=1200, k=40, wmax=100, frac=0.35) -> Problem:
+    """Multiple-choice multi-knapsack (knapsack-style, many wide BDDs): items in
+    classes of `items`, exactly one item per class (one-hot rows), and `knaps`
+    capacity rows sum_t w_t x_t <= frac * sum_t w_t over k items of k distinct
+    random classes, w ~ U{1..wmax}.  Item cost U[-10, 0) (a profit).  Capacity
+    rows have partitions of up to ~frac * k * E[w] nodes (hundreds)."""
+    rng = np.random.default_rng(seed)
+    n = classes * items
+    cost = rng.uniform(-10, 0, size=n)
+    rb = RowBuilder()
+    rb.add(np.arange(n).reshape(classes, items), np.ones((classes, items)), EQ, 1)
+    cls = np.stack([rng.choice(classes, size=k, replace=False) for _ in range(knaps)])
+    var = cls * items + rng.integers(0, items, size=(knaps, k))
+    w = rng.integers(1, wmax + 1, size=(knaps, k))
+    cap = np.floor(frac * w.sum(axis=1)).astype(np.int64)
+    rb.add(var, w, LE, cap)
+    return rb.build(n, cost, f"mckp(seed={seed},{classes}x{items},{knaps}x{k},w<={wmax})")
+
+
 def thin_hop(seed=0, k=10_000) -> Problem:
     """Thin-hop microbench: one at-most-one row over k variables, c ~ U[-1,1)."""
     rng = np.random.default_rng(seed)

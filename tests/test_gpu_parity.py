@@ -104,6 +104,8 @@ def test_random_ilps_with_forced_vars(oracle_mod):
     ("qap", lambda: synth.qap(4, n=7)),
     ("celltrack", lambda: synth.celltrack(4, frames=5, dets=40)),
     ("wide_rows", lambda: synth.random_ilp(7, n=40, m=60, kmax=12, coef=5)),
+    ("gap", lambda: synth.gap(4, jobs=40, agents=5)),
+    ("mckp", lambda: synth.mckp(4, classes=200, knaps=12, k=20)),
 ])
 def test_workload_shapes_fp64(oracle_mod, name, make):
     """Several tiles, ragged tails, both tile kinds: 1 iteration element-wise, then 10 more."""
@@ -122,6 +124,8 @@ def test_workload_shapes_fp64(oracle_mod, name, make):
     ("mrf", lambda: synth.mrf_potts(5, H=20, W=20, L=5)),
     ("mrf_cut", lambda: synth.mrf_potts_cut(5, H=20, W=20, L=5)),
     ("qap", lambda: synth.qap(5, n=8)),
+    ("gap", lambda: synth.gap(5, jobs=40, agents=5)),
+    ("mckp", lambda: synth.mckp(5, classes=200, knaps=12, k=20)),
 ])
 def test_fp32_lower_bound_100_iterations(oracle_mod, name, make):
     """fp32 build: LB within 1e-4 relative after 100 iterations; monotone within
@@ -581,3 +585,97 @@ def test_nccl_one_rank_communicator(monkeypatch):
         g.iterate(1, 0.5); h.iterate(1, 0.5)
         assert g.lower_bound() == h.lower_bound()
     g.close()
+
+
+def _max_lanes(p, precision, monkeypatch=None):
+    return int(F.Plan(p, precision=precision).tiles()[:, 2].max())
+
+
+@pytest.mark.parametrize("mode", ["rc", "tma"])
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("name,make,lanes", [
+    ("mrf", lambda: synth.mrf_potts(9, H=20, W=24, L=4), 128),         # K = 4 rows: 4 per lane (fp32)
+    ("mrf8", lambda: synth.mrf_potts(9, H=12, W=12, L=8), 64),         # K = 8 / 9 rows: 2 per lane
+    ("mrf_cut", lambda: synth.mrf_potts_cut(9, H=16, W=18, L=5), 128),  # K = 3 rows: 4 per lane (fp32)
+    ("gm", lambda: synth.gm_worms_like(9, n_src=150, k_cand=8, knn=10), 64),
+])
+def test_wide_tiles_bitwise(oracle_mod, monkeypatch, mode, precision, name, make, lanes):
+    """Tiles of 32 R rows (R rows per lane, kernels.cu mask_tile) run each row's
+    arithmetic exactly as 32-row tiles: FDOG_WIDE=0 vs the default, pass by pass
+    (lambda, delta_bar, min-marginals bit for bit; the bound at 1e-12, its
+    per-tile partials are summed in another order), through the graph-replayed
+    iterate, finalize and a restart; fp64 against the oracle at 1e-9."""
+    p = make()
+    monkeypatch.setenv("FDOG_SWEEP", mode)
+    monkeypatch.setenv("FDOG_FUSED", "0")
+    monkeypatch.setenv("FDOG_WIDE", "1")  # whenever eligible (the default asks the budget model)
+    want = lanes if precision == 32 else min(lanes, 64)
+    assert _max_lanes(p, precision) == want
+    g1 = F.Solver(p, precision=precision, record_mm=True)
+    monkeypatch.setenv("FDOG_WIDE", "0")
+    assert _max_lanes(p, precision) == 32
+    g0 = F.Solver(p, precision=precision, record_mm=True)
+    o = oracle_mod.Oracle(p)
+    s = _s(p)
+    for t in range(4):
+        fwd = t % 2 == 0
+        for g in (g0, g1, o):
+            g.pass_(fwd, 0.5)
+        assert np.array_equal(g0.lam(), g1.lam()) and np.array_equal(g0.deferred(), g1.deferred())
+        for a, b in zip(g0.min_marginals(), g1.min_marginals()):
+            assert np.array_equal(a, b)
+        assert _same_bound(g0, g1)
+        if precision == 64:
+            assert np.max(np.abs(g1.lam() - o.lam())) <= 1e-9 * s
+            assert abs(g1.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+    for g in (g0, g1):
+        g.iterate(3, 0.5)
+    assert np.array_equal(g0.lam(), g1.lam()) and _same_bound(g0, g1)
+    for g in (g0, g1):
+        g.finalize()
+        g.iterate(2, 0.5)
+    assert np.array_equal(g0.lam(), g1.lam()) and _same_bound(g0, g1)
+
+
+def test_cooperative_wide_bdds(oracle_mod):
+    """Knapsack rows wider than 32 nodes per partition run node-parallel (one
+    warp per BDD, warp-shuffle min-marginals, atomic-min relaxation):
+    a generalized assignment instance with 130 k-node capacity BDDs (beyond the
+    16-bit codes of lane tiles), fp64, every slot, min-marginals and the bound
+    after every pass for two iterations at 1e-9; then 10 more iterations; the
+    non-deferred variant refuses such BDDs."""
+    p = synth.gap(6, jobs=300, agents=20)
+    g, o = _compare_pass_by_pass(p, oracle_mod, passes=4)
+    t = F.Plan(p).tiles()
+    assert ((t[:, 0] & 32) != 0).sum() == 20 and t[:, 4].max() > 65534
+    g.iterate(10, 0.5)
+    o.iterate(10, 0.5)
+    s = _s(p)
+    assert abs(g.lower_bound() - o.lower_bound()) <= 1e-8 * (abs(o.lower_bound()) + s)
+    assert np.allclose(g.lam(), o.lam(), rtol=1e-8, atol=1e-8 * s)
+    with pytest.raises(F.FastdogError) as e:
+        g.pass_seq(True, 0.5)
+    assert e.value.code == 1
+
+
+def test_cooperative_unusual_orders_and_finalize(oracle_mod):
+    """Cooperative tiles through the distance recomputes (backward first, two
+    forwards: kEnergy / kCfr sweeps), finalize and the averaged finalize."""
+    p = synth.mckp(7, classes=300, knaps=20, k=24)
+    o = oracle_mod.Oracle(p)
+    g = F.Solver(p, precision=64, record_mm=True)
+    s = _s(p)
+    for fwd in (False, False, True, True, False):
+        g.pass_(fwd, 0.5)
+        o.pass_(fwd, 0.5)
+        assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s
+        assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+    g.finalize()
+    o.finalize()
+    assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s
+    assert abs(g.lower_bound() - o.lower_bound()) <= 1e-9 * (abs(o.lower_bound()) + s)
+    g.iterate(3, 0.5)
+    o.iterate(3, 0.5)
+    g.finalize(averaged=True)
+    o.finalize(averaged=True)
+    assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s

@@ -69,12 +69,18 @@ def test_seq_random_wide_rows(oracle_mod):
         _compare(p, oracle_mod, SEQ6[:4])
 
 
-@pytest.mark.parametrize("mode", ["rc", "tma", "stream"])
+@pytest.mark.parametrize("mode", ["rc", "tma", "stream", "rc-wide", "tma-wide"])
 def test_seq_composes_with_deferred_passes(oracle_mod, monkeypatch, mode):
     """seq -> deferred -> finalize -> seq, under each sweep design (the store-design
-    distances are rebuilt on the device whenever the deferred design left none)."""
-    monkeypatch.setenv("FDOG_SWEEP", mode)
-    p = synth.gm_worms_like(43, n_src=60, k_cand=5, knn=6)
+    distances are rebuilt on the device whenever the deferred design left none);
+    '-wide': tiles of 64 rows (two per lane)."""
+    monkeypatch.setenv("FDOG_SWEEP", mode.split("-")[0])
+    if mode.endswith("wide"):
+        monkeypatch.setenv("FDOG_WIDE", "1")
+        monkeypatch.setenv("FDOG_FUSED", "0")
+    p = synth.gm_worms_like(43, n_src=150, k_cand=8, knn=10)
+    if mode.endswith("wide"):
+        assert F.Plan(p).tiles()[:, 2].max() == 64
     steps = [("seq", True, 0.5), ("seq", False, 0.5), ("def", True, 0.5), ("def", False, 0.3),
              ("fin", None, None), ("seq", False, 0.4), ("seq", True, 0.5), ("seq", False, 0.5)]
     _compare(p, oracle_mod, steps)

@@ -165,3 +165,49 @@ def test_peer_exchange_errors_and_timeout():
     with pytest.raises(F.FastdogError) as e:
         ranks[1].set_peer_regions(regions)              # after a pass
     assert e.value.code == 6
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("name,make", [
+    ("gm", lambda: synth.gm_worms_like(14, n_src=80, k_cand=6, knn=8)),
+    ("mrf", lambda: synth.mrf_potts(14, H=16, W=18, L=4)),
+])
+def test_nccl_graph_overlap_one_gpu(monkeypatch, precision, name, make):
+    """The NCCL path of a world-2 rank on one GPU (FDOG_NCCL_SELF=1: a one-rank
+    communicator, so ncclAllReduce is the identity on this rank's partials):
+    fdog_iterate captures the whole iteration -- averaging, the exchange forked
+    onto a second stream (ncclAllReduce + avg_finish), the interior tiles'
+    sweep overlapping it, the boundary tiles' sweep after the join -- into one
+    CUDA graph.  Bit for bit equal to (a) the same solver with direct launches
+    and the exchange run first (FDOG_GRAPHS=0, FDOG_OVERLAP=0) and (b) the
+    external-exchange mode where the test writes each rank's own partials back
+    (the identity exchange, host-driven)."""
+    import os
+    import torch
+    import nvidia.nccl
+    lib = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+    p = make()
+    monkeypatch.setenv("FDOG_NCCL_SELF", "1")
+    g = F.Solver(p, precision=precision, rank=0, world=2, nccl_unique_id=torch.cuda.nccl.unique_id(),
+                 nccl_library=lib)
+    st = g.stats()
+    assert 0 < st["vars_shared"] and 0 < st["interior_tiles"] < st["tiles"]
+    monkeypatch.setenv("FDOG_GRAPHS", "0")
+    monkeypatch.setenv("FDOG_OVERLAP", "0")
+    d = F.Solver(p, precision=precision, rank=0, world=2, nccl_unique_id=torch.cuda.nccl.unique_id(),
+                 nccl_library=lib)
+    monkeypatch.delenv("FDOG_GRAPHS")
+    monkeypatch.delenv("FDOG_OVERLAP")
+    monkeypatch.delenv("FDOG_NCCL_SELF")
+    h = F.Solver(p, precision=precision, rank=0, world=2)  # external exchange
+    for it in range(4):
+        g.iterate(1, 0.5)
+        d.iterate(1, 0.5)
+        for fwd in (True, False):
+            h.pass_begin(fwd, 0.5)
+            h.exchange_write(h.exchange_read())
+            h.pass_end(fwd, 0.5)
+        assert np.array_equal(g.lam(), d.lam()) and np.array_equal(g.lam(), h.lam()), f"iteration {it}"
+        assert np.array_equal(g.deferred(), h.deferred())
+    g.close()
+    d.close()

@@ -98,6 +98,8 @@ def test_node_counts_random_ilp(oracle_mod, seed):
     ("gm_small", lambda: synth.gm_worms_like(1, n_src=40, k_cand=5, knn=6)),
     ("mrf_small", lambda: synth.mrf_potts(1, H=6, W=7, L=3)),
     ("mrf_cut_small", lambda: synth.mrf_potts_cut(1, H=6, W=7, L=3)),
+    ("gap_small", lambda: synth.gap(1, jobs=40, agents=5)),
+    ("mckp_small", lambda: synth.mckp(1, classes=200, knaps=12, k=20)),
     ("qap_small", lambda: synth.qap(1, n=6)),
     ("celltrack_small", lambda: synth.celltrack(1, frames=4, dets=30)),
 ])
@@ -138,6 +140,21 @@ def test_mrf_potts_cut_counts():
     assert st["bdds"] == H * W + 2 * L * E
     assert st["nodes"] == H * W * (2 * L - 1) + 2 * L * E * 5
     assert st["slots"] == H * W * L + 2 * L * E * 3
+
+
+def test_cooperative_tiles():
+    """Shapes with a partition wider than 32 nodes (knapsack rows) become one-BDD
+    cooperative tiles (kind bit 5, L = 1) with 32-bit child codes: a BDD over
+    65 534 nodes is packed (the 16-bit limit applies to the lane tiles only)."""
+    p = synth.gap(0, jobs=300, agents=20)
+    pl = F.Plan(p)
+    t = pl.tiles()
+    coop = t[(t[:, 0] & 32) != 0]
+    assert len(coop) == 20 and np.all(coop[:, 2] == 1) and np.all(coop[:, 3] == 1)
+    assert coop[:, 4].max() > 65534
+    assert pl.stats()["sweep_recompute"] == 0
+    hs, lo, hi = pl.bdd(300)  # the first capacity row
+    assert hs[-1] == coop[:, 4].max() or hs[-1] in set(coop[:, 4].tolist())
 
 
 def test_invalid_inputs():
