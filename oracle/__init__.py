@@ -72,6 +72,8 @@ def _load():
         lib.oracle_bdd_get.argtypes = [P, C.c_int32, P, P, P, P]
         lib.oracle_total_nodes.argtypes = [P, P]
         lib.oracle_num_threads.argtypes = [P]
+        lib.oracle_set_lifted.argtypes = [P]
+        lib.oracle_get_lifted.argtypes = [P, P, P, C.c_int64]
         lib.oracle_primal_step.argtypes = [P, C.c_int32, C.c_double, C.c_uint64, P, P]
         lib.oracle_round_primal.argtypes = [P, C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_uint64,
                                             C.c_double, P, P]
@@ -151,6 +153,17 @@ class Oracle:
         x = C.c_double()
         self._chk(self._lib.oracle_dual_energy(self._h, C.byref(x)), "dual_energy")
         return x.value
+
+    def set_lifted(self):
+        """Switch to the lifted representation before the first pass."""
+        self._chk(self._lib.oracle_set_lifted(self._h), "set_lifted")
+
+    def lifted(self):
+        """(lambda^{j,0}, lambda^{j,1}) per slot, canonical order (lifted mode)."""
+        n = self.num_slots()
+        a, b = np.empty(max(n, 1)), np.empty(max(n, 1))
+        self._chk(self._lib.oracle_get_lifted(self._h, _ptr(a), _ptr(b), a.size), "get_lifted")
+        return a[:n], b[:n]
 
     def finalize(self, averaged: bool = False):
         fn = self._lib.oracle_finalize_avg if averaged else self._lib.oracle_finalize

@@ -77,6 +77,11 @@ struct oracle_solver {
    * reuse of P:315-316 holds when forward and backward passes alternate; any
    * other sequence recomputes them from their definition */
   int ctt_ok, cfr_ok;
+  /* lifted representation (oracle_set_lifted): lambda holds
+   * lambda^{j,1}, lam0 holds lambda^{j,0} (the 0-arc costs) */
+  int lifted;
+  double *lam0;
+  double *avg0;        /* (1/|J_i|) sum_k max(-delta_bar_ik, 0)     */
 };
 
 /* ------------------------------------------------------------------ */
@@ -387,7 +392,7 @@ static void free_solver(oracle_solver *s) {
   }
   free(s->bdd); free(s->cost); free(s->slot_var); free(s->slot_bdd); free(s->lambda); free(s->delta_bar);
   free(s->delta_new); free(s->m0); free(s->m1); free(s->var_ptr); free(s->var_slots);
-  free(s->avg); free(s->energy);
+  free(s->avg); free(s->energy); free(s->lam0); free(s->avg0);
   free(s);
 }
 
@@ -514,9 +519,13 @@ fail:
 
 void oracle_destroy(oracle_solver *s) { free_solver(s); }
 
+static int lifted_pass(oracle_solver *s, int forward, double omega);
+static double lifted_bound(const oracle_solver *s);
+
 int oracle_pass(oracle_solver *s, int forward, double omega) {
   if (!s) return O_EINVAL;
   if (!(omega > 0.0 && omega <= 1.0)) return O_EINVAL; /* A14 */
+  if (s->lifted) return lifted_pass(s, forward, omega);
   /* deferred averaging from the previous pass's delta_bar (A1, A2) */
   for (int32_t i = 0; i < s->n_vars; ++i) {
     int64_t deg = s->var_ptr[i + 1] - s->var_ptr[i];
@@ -571,6 +580,7 @@ int oracle_pass(oracle_solver *s, int forward, double omega) {
 /* remains (delta_bar = 0) and sum_j E^j is the bound.                   */
 int oracle_pass_seq(oracle_solver *s, int forward, double omega) {
   if (!s) return O_EINVAL;
+  if (s->lifted) return O_ESTATE;
   if (!(omega > 0.0 && omega <= 1.0)) return O_EINVAL; /* A14 */
   /* a pending deferred correction is not part of this scheme */
   for (int64_t q = 0; q < s->n_slots; ++q)
@@ -667,12 +677,24 @@ int oracle_lower_bound(const oracle_solver *s, double *out) {
 
 int oracle_dual_energy(const oracle_solver *s, double *out) {
   if (!s || !out) return O_EINVAL;
+  if (s->lifted) return O_ESTATE;
   *out = raw_energy(s);
   return O_OK;
 }
 
 int oracle_finalize(oracle_solver *s) {
   if (!s) return O_EINVAL;
+  if (s->lifted) {
+    /* lambda^{j,b} += omega max(mbar^b - mbar^{1-b}, 0) (lifted form) */
+    for (int64_t q = 0; q < s->n_slots; ++q) {
+      const double x = s->delta_bar[q];
+      s->lambda[q] += x > 0 ? x : 0.0;
+      s->lam0[q] += x < 0 ? -x : 0.0;
+      s->delta_bar[q] = 0.0;
+    }
+    s->lb = lifted_bound(s);
+    return O_OK;
+  }
   /* lambda_i^j += omega (mbar1_ij - mbar0_ij)  (per slot, A11) */
   for (int64_t q = 0; q < s->n_slots; ++q) {
     s->lambda[q] += s->delta_bar[q];
@@ -692,6 +714,7 @@ int oracle_finalize(oracle_solver *s) {
  * Dual feasible like the per-slot form: sum_j [lambda + avg] = c_i. */
 int oracle_finalize_avg(oracle_solver *s) {
   if (!s) return O_EINVAL;
+  if (s->lifted) return O_ESTATE;
   for (int32_t i = 0; i < s->n_vars; ++i) {
     int64_t deg = s->var_ptr[i + 1] - s->var_ptr[i];
     if (deg == 0) continue;
@@ -724,7 +747,10 @@ static int copy_out(const double *src, int64_t n, double *dst, int64_t len) {
 
 int oracle_get_lambda(const oracle_solver *s, double *out, int64_t len) {
   if (!s) return O_EINVAL;
-  return copy_out(s->lambda, s->n_slots, out, len);
+  int rc = copy_out(s->lambda, s->n_slots, out, len);
+  if (!rc && s->lifted) /* original space: lambda = lambda^1 - lambda^0 */
+    for (int64_t q = 0; q < s->n_slots; ++q) out[q] -= s->lam0[q];
+  return rc;
 }
 
 int oracle_get_deferred(const oracle_solver *s, double *out, int64_t len) {
@@ -741,6 +767,7 @@ int oracle_min_marginals(const oracle_solver *s, double *m0, double *m1, int64_t
 
 int oracle_set_lambda(oracle_solver *s, const double *lambda, int64_t len) {
   if (!s || !lambda || len != s->n_slots) return O_EINVAL;
+  if (s->lifted) return O_ESTATE;
   memcpy(s->lambda, lambda, (size_t)len * sizeof(double));
   for (int32_t j = 0; j < s->n_cons; ++j) {
     backward_dp(&s->bdd[j], s->lambda + s->bdd[j].slot0);
@@ -814,7 +841,7 @@ static int mm_sign(double m1, double m0, double clamp) {
 int oracle_primal_step(oracle_solver *s, int32_t round, double delta, uint64_t seed, int64_t *conflicts,
                        uint8_t *x) {
   if (!s || !conflicts) return O_EINVAL;
-  if (s->passes == 0) return O_ESTATE;
+  if (s->passes == 0 || s->lifted) return O_ESTATE;
   int64_t nc = 0;
   for (int32_t i = 0; i < s->n_vars; ++i) {
     int64_t a = s->var_ptr[i], b = s->var_ptr[i + 1];
@@ -892,4 +919,176 @@ int oracle_round_primal(oracle_solver *s, double delta0, double alpha, int32_t i
     rc = oracle_iterate(s, inner, omega);
     if (rc) return rc;
   }
+}
+
+/* ------------------------------------------------------------------ */
+/* Lifted representation: every BDD j keeps two costs per     */
+/* variable, lambda^{j,0} on 0-arcs and lambda^{j,1} on 1-arcs, so      */
+/* E^j = min over paths of sum_h lambda^{j, x_h}_h and the bound is the */
+/* plain sum of per-BDD shortest paths (the appendix's lifted energy).  */
+/* Initialisation lambda^{j,beta} = beta c_i / |J_i|.  Update,  */
+/* reading A8 (P:53-56 with max(., 0)):                                 */
+/*   lambda^{j,b} <- lambda^{j,b} - omega max(m^b - m^{1-b}, 0)         */
+/*                  + (omega/|J_i|) sum_k max(mbar^b_ik - mbar^{1-b}_ik, 0) */
+/* with m^1 - m^0 clamped as A5 (d = clamp(m1 - m0); omega max(d, 0) =  */
+/* max(delta, 0) for delta = omega d, and omega max(-d, 0) =            */
+/* max(-delta, 0)).  lambda^1 - lambda^0 follows the original-space      */
+/* update P:641.  Each pass recomputes the opposite-direction  */
+/* distances from their definition at its start, then walks */
+/* the hops as Alg. forward_pass_mm / backward_pass_mm with */
+/* the two arc costs.                                                   */
+
+/* shp(v, T) with lifted arc costs */
+static void lifted_backward_dp(obdd *d, const double *l0, const double *l1) {
+  for (int32_t h = d->k - 1; h >= 0; --h)
+    for (int32_t v = d->hop_start[h]; v < d->hop_start[h + 1]; ++v) {
+      double a = l0[h] + ctt_of(d, d->lo[v]);
+      double b = l1[h] + ctt_of(d, d->hi[v]);
+      d->ctt[v] = a < b ? a : b;
+    }
+}
+
+/* shp(r, v) of P_h from P_{h-1} with lifted arc costs (A4) */
+static void lifted_relax_into(obdd *d, const double *l0, const double *l1, int32_t h) {
+  for (int32_t v = d->hop_start[h]; v < d->hop_start[h + 1]; ++v) {
+    double best = INFINITY;
+    for (int32_t u = d->hop_start[h - 1]; u < d->hop_start[h]; ++u) {
+      if (d->lo[u] == v && d->cfr[u] + l0[h - 1] < best) best = d->cfr[u] + l0[h - 1];
+      if (d->hi[u] == v && d->cfr[u] + l1[h - 1] < best) best = d->cfr[u] + l1[h - 1];
+    }
+    d->cfr[v] = best;
+  }
+}
+
+static void lifted_forward_dp(obdd *d, const double *l0, const double *l1) {
+  if (d->k == 0) return;
+  d->cfr[0] = 0.0;
+  for (int32_t h = 1; h < d->k; ++h) lifted_relax_into(d, l0, l1, h);
+}
+
+/* m^beta = min_{v in P_h} shp(r, v) + lambda^{j,beta}_h + shp(s^beta(v), T) */
+static void lifted_min_marginals_at(const obdd *d, const double *l0, const double *l1, int32_t h, double *m0,
+                                    double *m1) {
+  double b0 = INFINITY, b1 = INFINITY;
+  for (int32_t v = d->hop_start[h]; v < d->hop_start[h + 1]; ++v) {
+    if (d->lo[v] != BOT) {
+      double x = (d->cfr[v] + l0[h]) + ctt_of(d, d->lo[v]);
+      if (x < b0) b0 = x;
+    }
+    if (d->hi[v] != BOT) {
+      double x = (d->cfr[v] + l1[h]) + ctt_of(d, d->hi[v]);
+      if (x < b1) b1 = x;
+    }
+  }
+  *m0 = b0;
+  *m1 = b1;
+}
+
+static void lifted_update_slot(oracle_solver *s, int64_t slot, double *l0, double *l1, double m0, double m1,
+                               double omega) {
+  const double d = mm_difference(m1, m0, s->clamp);
+  const double delta = omega * d;
+  const int32_t i = s->slot_var[slot];
+  s->m0[slot] = m0;
+  s->m1[slot] = m1;
+  *l1 = (*l1 - (delta > 0 ? delta : 0.0)) + s->avg[i];   /* beta = 1 */
+  *l0 = (*l0 - (delta < 0 ? -delta : 0.0)) + s->avg0[i]; /* beta = 0 */
+  s->delta_new[slot] = delta;
+}
+
+static double lifted_energy_of(const obdd *d, const double *l0, const double *l1) {
+  double *t = (double *)malloc((size_t)(d->n_nodes ? d->n_nodes : 1) * sizeof(double));
+  if (!t) return NAN;
+  for (int32_t h = d->k - 1; h >= 0; --h)
+    for (int32_t v = d->hop_start[h]; v < d->hop_start[h + 1]; ++v) {
+      double a = l0[h] + (d->lo[v] == TOP ? 0.0 : d->lo[v] == BOT ? INFINITY : t[d->lo[v]]);
+      double b = l1[h] + (d->hi[v] == TOP ? 0.0 : d->hi[v] == BOT ? INFINITY : t[d->hi[v]]);
+      t[v] = a < b ? a : b;
+    }
+  double e = t[0];
+  free(t);
+  return e;
+}
+
+/* sum_j E_lifted^j + free term: the bound of the lifted representation */
+static double lifted_bound(const oracle_solver *s) {
+  const int32_t m = s->n_cons;
+  int j;
+#pragma omp parallel for num_threads(s->n_threads) schedule(dynamic, 256)
+  for (j = 0; j < m; ++j) {
+    const obdd *d = &s->bdd[j];
+    s->energy[j] = d->k ? lifted_energy_of(d, s->lam0 + d->slot0, s->lambda + d->slot0) : 0.0;
+  }
+  double e = 0.0;
+  for (int32_t q = 0; q < m; ++q) e += s->energy[q]; /* fixed order */
+  return e + s->free_term;
+}
+
+int oracle_set_lifted(oracle_solver *s) {
+  if (!s) return O_EINVAL;
+  if (s->lifted) return O_OK;
+  if (s->passes != 0) return O_ESTATE;
+  int64_t S = s->n_slots ? s->n_slots : 1;
+  s->lam0 = (double *)calloc((size_t)S, sizeof(double)); /* lambda^{j,0} = 0 */
+  s->avg0 = (double *)calloc((size_t)(s->n_vars ? s->n_vars : 1), sizeof(double));
+  if (!s->lam0 || !s->avg0) return O_ENOMEM;
+  s->lifted = 1; /* lambda^{j,1} = c_i / |J_i| is the lambda set at create */
+  s->lb = lifted_bound(s);
+  return O_OK;
+}
+
+static int lifted_pass(oracle_solver *s, int forward, double omega) {
+  /* the two deferred averages from the previous pass (j ascending, A1) */
+  for (int32_t i = 0; i < s->n_vars; ++i) {
+    int64_t deg = s->var_ptr[i + 1] - s->var_ptr[i];
+    double sp = 0.0, sn = 0.0;
+    for (int64_t q = s->var_ptr[i]; q < s->var_ptr[i + 1]; ++q) {
+      const double x = s->delta_bar[s->var_slots[q]];
+      sp += x > 0 ? x : 0.0;
+      sn += x < 0 ? -x : 0.0;
+    }
+    s->avg[i] = deg ? sp / (double)deg : 0.0;
+    s->avg0[i] = deg ? sn / (double)deg : 0.0;
+  }
+  int j;
+#pragma omp parallel for num_threads(s->n_threads) schedule(dynamic, 256)
+  for (j = 0; j < s->n_cons; ++j) {
+    obdd *d = &s->bdd[j];
+    if (d->k == 0) continue;
+    double *l0 = s->lam0 + d->slot0, *l1 = s->lambda + d->slot0;
+    if (forward) {
+      lifted_backward_dp(d, l0, l1); /* shp(v, T) at the pass's start */
+      for (int32_t h = 0; h < d->k; ++h) {
+        if (h == 0) d->cfr[0] = 0.0;
+        else lifted_relax_into(d, l0, l1, h); /* with the updated lambda_{h-1} */
+        double m0, m1;
+        lifted_min_marginals_at(d, l0, l1, h, &m0, &m1);
+        lifted_update_slot(s, d->slot0 + h, &l0[h], &l1[h], m0, m1, omega);
+      }
+    } else {
+      lifted_forward_dp(d, l0, l1); /* shp(r, v) at the pass's start */
+      for (int32_t h = d->k - 1; h >= 0; --h) {
+        double m0, m1;
+        lifted_min_marginals_at(d, l0, l1, h, &m0, &m1);
+        lifted_update_slot(s, d->slot0 + h, &l0[h], &l1[h], m0, m1, omega);
+        for (int32_t v = d->hop_start[h]; v < d->hop_start[h + 1]; ++v) {
+          double a = l0[h] + ctt_of(d, d->lo[v]);
+          double b = l1[h] + ctt_of(d, d->hi[v]);
+          d->ctt[v] = a < b ? a : b;
+        }
+      }
+    }
+  }
+  double *t = s->delta_bar; /* mbar <- m */
+  s->delta_bar = s->delta_new;
+  s->delta_new = t;
+  s->lb = lifted_bound(s);
+  s->passes++;
+  return O_OK;
+}
+
+int oracle_get_lifted(const oracle_solver *s, double *lam0, double *lam1, int64_t len) {
+  if (!s || !s->lifted) return O_EINVAL;
+  int rc = copy_out(s->lam0, s->n_slots, lam0, len);
+  return rc ? rc : copy_out(s->lambda, s->n_slots, lam1, len);
 }

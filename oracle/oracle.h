@@ -104,6 +104,17 @@ int oracle_round_primal(oracle_solver *s, double delta0, double alpha, int32_t i
                         uint64_t seed, double omega, uint8_t *x, int32_t *rounds);
 int oracle_num_threads(const oracle_solver *s);
 
+/* Lifted representation: switch a fresh solver (no pass yet, else
+ * 6) to two costs per slot, lambda^{j,0} = 0 and lambda^{j,1} = c_i/|J_i|
+ * (P:622), updated by reading A8 (P:53-56 with max(., 0)).  Afterwards
+ * oracle_pass runs lifted passes, oracle_lower_bound is the plain sum of the
+ * per-BDD shortest paths (+ free term), oracle_get_lambda returns lambda^1 -
+ * lambda^0, oracle_finalize adds max(+-delta_bar, 0) to the two
+ * sides; pass_seq, set_lambda, dual_energy, finalize_avg and the primal
+ * rounding return 6. */
+int oracle_set_lifted(oracle_solver *s);
+int oracle_get_lifted(const oracle_solver *s, double *lam0, double *lam1, int64_t len);
+
 #ifdef __cplusplus
 }
 #endif
