@@ -608,7 +608,7 @@ def run_gpu(args):
             "solver_stats": {k: st[k] for k in ("tiles", "tiles_shared_topology", "staged_tiles", "sweep_grid",
                                                  "sweep_block", "sweep_smem_per_warp", "sweep_streaming", "sweep_recompute", "padded_slots",
                                                  "device_bytes", "shapes", "max_hops", "max_width", "tile_pairs",
-                                                 "interior_tiles", "coop_tiles")},
+                                                 "interior_tiles", "coop_tiles", "tmem_cols")},
             "kernels": prof,
             "exchange": _exchange_report(prof, st, world),
             "gpu_launches": launches,

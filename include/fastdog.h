@@ -72,6 +72,14 @@ typedef struct {
                                locality-aware sharder (bundles of rows joined by
                                |J_i| = 2 variables, ordered by their shared
                                variables, cut by BDD node count) */
+  int32_t lifted;           /* 1: lifted two-sided storage: per slot
+                               lambda^{j,0} (0-arcs) and lambda^{j,1} (1-arcs),
+                               updated by reading A8; the bound is the plain sum
+                               of per-BDD shortest paths (no sum min(delta_bar, 0)
+                               term: exact with forced variables, A5).  world 1;
+                               every tile runs from global memory (lane-serial or
+                               node-parallel); no primal rounding, non-deferred
+                               passes, set_state or averaged finalize.          */
 } fdog_options;
 
 /* Sizes of this rank's part of the problem. */
@@ -109,6 +117,9 @@ typedef struct {
                                       swept while the exchange runs (= tiles if world 1) */
   int64_t coop_tiles;              /* one-BDD tiles swept node-parallel by a warp
                                       (a partition wider than 32 nodes)              */
+  int32_t tmem_cols;               /* > 0: the recompute design keeps the distances of
+                                      its 32-row tiles in tensor memory (columns per
+                                      sweep CTA); 0: shared memory                    */
 } fdog_stats_t;
 
 typedef struct fdog_plan fdog_plan;     /* host-side compiled + packed problem */
@@ -259,6 +270,10 @@ fdog_status fdog_get_deferred(fdog_solver *s, double *out, int64_t len);
 fdog_status fdog_min_marginals(fdog_solver *s, double *m0, double *m1, int64_t len);
 /* Overwrite (lambda, delta_bar) -- checkpoint/resume; either may be NULL. */
 fdog_status fdog_set_state(fdog_solver *s, const double *lambda, const double *delta, int64_t len);
+/* Lifted mode only: lambda^{j,0} and lambda^{j,1} per slot, canonical order
+ * (fdog_get_lambda returns lambda^1 - lambda^0).  FDOG_ESTATE
+ * without opts.lifted; FDOG_EINVAL if len < slots. */
+fdog_status fdog_get_lifted(fdog_solver *s, double *lam0, double *lam1, int64_t len);
 fdog_status fdog_stats(const fdog_solver *s, fdog_stats_t *out);
 /* Debug (solver created with FDOG_TRACE=1): per warp of the TMA-staged sweep,
  * {start, end (globaltimer ns), tiles processed, SM id} of the last sweep;

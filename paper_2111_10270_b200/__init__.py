@@ -58,7 +58,7 @@ class Options(C.Structure):
                 ("record_mm", C.c_int32), ("profile", C.c_int32), ("rank", C.c_int32),
                 ("world", C.c_int32), ("nccl_unique_id", C.c_void_p), ("nccl_library", C.c_char_p),
                 ("stream", C.c_void_p), ("host_threads", C.c_int32),
-                ("row_owner", C.c_void_p)]
+                ("row_owner", C.c_void_p), ("lifted", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -69,7 +69,7 @@ class Stats(C.Structure):
                 ("sweep_grid", C.c_int32), ("sweep_block", C.c_int32), ("sweep_smem_per_warp", C.c_int64),
                 ("sweep_streaming", C.c_int32), ("h2d_bytes", C.c_int64),
                 ("fused_small", C.c_int32), ("sweep_recompute", C.c_int32), ("tile_pairs", C.c_int64),
-                ("interior_tiles", C.c_int64), ("coop_tiles", C.c_int64)]
+                ("interior_tiles", C.c_int64), ("coop_tiles", C.c_int64), ("tmem_cols", C.c_int32)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -91,7 +91,7 @@ EXPORTS = ["fdog_default_options", "fdog_plan_create", "fdog_plan_destroy", "fdo
            "fdog_create_from_plan", "fdog_destroy", "fdog_iterate", "fdog_pass", "fdog_pass_seq", "fdog_iterate_seq",
            "fdog_lower_bound",
            "fdog_finalize", "fdog_finalize_averaged", "fdog_num_slots", "fdog_slot_index", "fdog_get_lambda",
-           "fdog_get_deferred", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
+           "fdog_get_deferred", "fdog_get_lifted", "fdog_min_marginals", "fdog_set_state", "fdog_stats",
            "fdog_profile", "fdog_profile_reset", "fdog_profile_enable", "fdog_pass_begin", "fdog_pass_end",
            "fdog_exchange_size", "fdog_exchange_read", "fdog_exchange_write", "fdog_exchange_region",
            "fdog_set_peer_regions", "fdog_peer_error", "fdog_ipc_handle", "fdog_ipc_open", "fdog_ipc_close",
@@ -138,6 +138,7 @@ def load():
         "fdog_slot_index": ([P, P, P, i64], C.c_int),
         "fdog_get_lambda": ([P, P, i64], C.c_int),
         "fdog_get_deferred": ([P, P, i64], C.c_int),
+        "fdog_get_lifted": ([P, P, P, i64], C.c_int),
         "fdog_min_marginals": ([P, P, P, i64], C.c_int),
         "fdog_set_state": ([P, P, P, i64], C.c_int),
         "fdog_stats": ([P, P], C.c_int),
@@ -194,7 +195,8 @@ class _ProblemArrays:
 
 
 def make_options(precision=32, device=0, clamp=0.0, record_mm=False, profile=False, rank=0, world=1,
-                 nccl_unique_id=None, nccl_library=None, stream=None, host_threads=0, row_owner=None):
+                 nccl_unique_id=None, nccl_library=None, stream=None, host_threads=0, row_owner=None,
+                 lifted=False):
     lib = load()
     o = Options()
     lib.fdog_default_options(C.byref(o))
@@ -217,17 +219,18 @@ def make_options(precision=32, device=0, clamp=0.0, record_mm=False, profile=Fal
     if row_owner is not None:
         o._owner = np.ascontiguousarray(row_owner, dtype=np.int32)
         o.row_owner = o._owner.ctypes.data
+    o.lifted = int(bool(lifted))
     return o
 
 
 class Plan:
     """Host-side compiled + packed problem (no GPU needed)."""
 
-    def __init__(self, problem, rank=0, world=1, host_threads=0, precision=32, row_owner=None):
+    def __init__(self, problem, rank=0, world=1, host_threads=0, precision=32, row_owner=None, lifted=False):
         lib = load()
         self._pa = _ProblemArrays(problem)
         self._opts = make_options(precision=precision, rank=rank, world=world, host_threads=host_threads,
-                                  row_owner=row_owner)
+                                  row_owner=row_owner, lifted=lifted)
         h = C.c_void_p()
         _check(lib.fdog_plan_create(C.byref(self._pa.struct), C.byref(self._opts), C.byref(h)),
                "fdog_plan_create")
@@ -300,11 +303,11 @@ class Solver:
 
     def __init__(self, problem=None, *, plan: Plan | None = None, precision=32, device=0, clamp=0.0,
                  record_mm=False, profile=False, rank=0, world=1, nccl_unique_id=None,
-                 nccl_library=None, stream=None, host_threads=0, row_owner=None):
+                 nccl_library=None, stream=None, host_threads=0, row_owner=None, lifted=False):
         lib = load()
         self._lib = lib
         self._opts = make_options(precision, device, clamp, record_mm, profile, rank, world,
-                                  nccl_unique_id, nccl_library, stream, host_threads, row_owner)
+                                  nccl_unique_id, nccl_library, stream, host_threads, row_owner, lifted)
         h = C.c_void_p()
         if plan is not None:
             _check(lib.fdog_create_from_plan(plan._h, C.byref(self._opts), C.byref(h)),
@@ -383,6 +386,13 @@ class Solver:
 
     def deferred(self, out=None):
         return self._get("fdog_get_deferred", out)
+
+    def lifted(self):
+        """(lambda^{j,0}, lambda^{j,1}) per slot, canonical order (lifted mode)."""
+        n = self.num_slots()
+        a, b = np.empty(max(n, 1)), np.empty(max(n, 1))
+        _check(self._lib.fdog_get_lifted(self._h, _ptr(a), _ptr(b), a.size), "fdog_get_lifted")
+        return a[:n], b[:n]
 
     def min_marginals(self):
         n = self.num_slots()

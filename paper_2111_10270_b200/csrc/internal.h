@@ -203,6 +203,10 @@ struct Plan {
   int32_t coop_w = 0;               // widest partition of a cooperative tile
   int32_t direct_w = 0;             // widest partition of the other unstaged tiles
   bool coop_smem = false;           // the cooperative relaxation buffers fit the DB region
+  int32_t tmem_cols = 0;            // recompute design, fp32: TMEM columns per CTA holding the distance
+                                    // scratch of 32-row arc-mask tiles (0: shared memory)
+  bool lifted = false;              // lifted two-sided storage (fdog_options::lifted): every tile from
+                                    // global memory, every variable in the CSR averaging part
 
   HostImage image;                  // device image (see ImageSection)
 
@@ -255,6 +259,10 @@ struct SweepArgs {
   int64_t scratch_stride;   // elements per warp
   int32_t coop_bw;          // cooperative tiles: entries per relaxation buffer (two per warp)
   int32_t coop_smem;        // 1: in the warp's DB region, 0: in scratch
+  int32_t tmem_cols;        // > 0: recompute-design distances of 32-row arc-mask tiles in TMEM,
+                            // columns per warp (fp32; the kernel variant rw = 0)
+  void *lambda0;            // T*, lifted mode: lambda^{j,0} per slot (null otherwise)
+  const void *avg0;         // T*, lifted mode: the 0-side averages per slot
 };
 
 struct AvgArgs {
@@ -334,12 +342,18 @@ int launch_dist_dp(int precision, const SeqArgs &a, int32_t n_tiles, int32_t for
 
 // returns the cudaError_t as int
 // rc: recompute design (sweep_kernel<..., RC = true>; plan packed with Plan::rc)
-// rw: the most rows per lane of any tile (1, 2, 4; TileDesc::lanes / 32)
+// rw: the most rows per lane of any tile (1, 2, 4; TileDesc::lanes / 32); 0:
+// the TMEM variant (fp32 recompute design with SweepArgs::tmem_cols > 0)
 int launch_sweep(int precision, int mode, bool record, bool rc, int rw, const SweepArgs &a, int grid, int block,
                  size_t smem, void *stream);
 int launch_sweep_stream(int precision, int mode, bool record, const SweepArgs &a, void *stream);
 // chunked walk of rows too long to stage whole (store design; every tile an arc-mask tile)
 int launch_sweep_chunk(int precision, int mode, bool record, const SweepArgs &a, void *stream);
+// lifted representation (fdog_options::lifted): both averages per slot, the
+// lifted final correction, lambda^1 - lambda^0 into out
+int launch_avg_lifted(int precision, const AvgArgs &a, void *avg0, void *stream);
+int launch_add_deferred_lifted(int precision, int64_t n, void *lam1, void *lam0, void *delta, void *stream);
+int launch_lifted_diff(int precision, int64_t n, const void *lam1, const void *lam0, void *out, void *stream);
 int sweep_occupancy(int precision, int mode, bool record, bool rc, int rw, int block, size_t smem, int *blocks_per_sm);
 int launch_avg(int precision, const AvgArgs &a, void *stream);
 int launch_peer_signal(const PeerArgs &pa, void *stream);

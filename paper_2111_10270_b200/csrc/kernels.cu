@@ -169,8 +169,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <typename T, int MODE, bool REC>
 __device__ __forceinline__ double process_bdd(const int K, const int nodes, const int32_t *ho, const uint32_t *tp,
                                               const int ts, const int L, T *lam, T *va, T *D, T *R, const int rw,
-                                              const bool valid, const T omega, const T clamp, T *m0g, T *m1g) {
+                                              const bool valid, const T omega, const T clamp, T *m0g, T *m1g,
+                                              T *l0 = nullptr, const T *v0 = nullptr) {
+  // l0 != null: lifted mode -- 0-arcs cost lambda^{j,0} = l0[h L]
+  // (else 0); v0: the 0-side averages; lam / va: lambda^{j,1} and its average
   const T inf = t_inf<T>();
+  const bool lifted = l0 != nullptr;
   double acc = 0.0;
   auto emit = [&](int h, T lam_new, T delta, T m0, T m1) {
     if (!valid) {
@@ -184,16 +188,37 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
       m1g[h * L] = m1;
     }
   };
+  // dual update of partition h (lifted: reading A8, both sides);
+  // returns (lambda^0, lambda^1) of the hop after it
+  auto update = [&](int h, T m0r, T m1r, T &o0, T &o1) {
+    const T l = lam[h * L];
+    const T z = lifted ? l0[h * L] : T(0);
+    const T m0 = lifted ? z + m0r : m0r;
+    const T m1 = l + m1r;  // Eq. (min-marginal-via-shortest-path) P:312
+    const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
+    if (!lifted) {
+      o1 = add_rn(sub_rn(l, delta), va[h * L]);
+      o0 = T(0);
+      emit(h, o1, delta, m0, m1);
+      if (valid) acc += (double)fmin(delta, T(0));
+      return;
+    }
+    o1 = add_rn(sub_rn(l, fmax(delta, T(0))), va[h * L]);
+    o0 = add_rn(sub_rn(z, fmax(-delta, T(0))), v0[h * L]);
+    emit(h, o1, delta, m0, m1);
+    if (valid) l0[h * L] = o0;
+  };
   if constexpr (MODE == kEnergy) {
     // shp(v, T) for all nodes under the current lambda
 #pragma unroll 1
     for (int h = K - 1; h >= 0; --h) {
       const T l = lam[h * L];
+      const T z = lifted ? l0[h * L] : T(0);
       const int n1 = ho[h + 1];
 #pragma unroll 1
       for (int n = ho[h]; n < n1; ++n) {
         const uint32_t e = tp[n * ts];
-        D[n * L] = fmin(D[(e & 0xFFFFu) * L], l + D[(e >> 16) * L]);
+        D[n * L] = fmin(lifted ? z + D[(e & 0xFFFFu) * L] : D[(e & 0xFFFFu) * L], l + D[(e >> 16) * L]);
       }
     }
     return valid ? (double)D[0] : 0.0;  // E^j = shp(r, T)
@@ -214,6 +239,7 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
       }
       T e_min = inf;
       const T l = lam[h * L];
+      const T z = lifted ? l0[h * L] : T(0);
 #pragma unroll 1
       for (int n = n0; n < n1; ++n) {
         const uint32_t e = tp[n * ts];
@@ -223,10 +249,10 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
         const int rl = min(lo - n1, rw), rh = min(hi - n1, rw);
         nlo[rl * L] = fmin(nlo[rl * L], cf);
         nhi[rh * L] = fmin(nhi[rh * L], cf);
-        if (h == K - 1) e_min = fmin(e_min, fmin(cf + D[lo * L], cf + l + D[hi * L]));
+        if (h == K - 1) e_min = fmin(e_min, fmin((lifted ? cf + z : cf) + D[lo * L], cf + l + D[hi * L]));
       }
 #pragma unroll 1
-      for (int w = 0; w < Wn; ++w) cur[w * L] = fmin(nlo[w * L], nhi[w * L] + l);
+      for (int w = 0; w < Wn; ++w) cur[w * L] = fmin(lifted ? nlo[w * L] + z : nlo[w * L], nhi[w * L] + l);
       if (h == K - 1 && valid) acc = (double)e_min;
     }
     return acc;
@@ -261,18 +287,15 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
         nlo[rl * L] = fmin(nlo[rl * L], cf);
         nhi[rh * L] = fmin(nhi[rh * L], cf);
       }
-      const T l = lam[h * L];
-      const T m1 = l + m1r;  // Eq. (min-marginal-via-shortest-path) P:312
-      const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
-      const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
-      emit(h, lam_new, delta, m0, m1);
-      if (valid) acc += (double)fmin(delta, T(0));
+      T z_new, lam_new;
+      update(h, m0, m1r, z_new, lam_new);
       if (!last) {
         // shp(r, v), v in P_{h+1}: 1-arcs priced with the updated lambda_h (A4)
 #pragma unroll 1
-        for (int w = 0; w < Wn; ++w) cur[w * L] = fmin(nlo[w * L], nhi[w * L] + lam_new);
+        for (int w = 0; w < Wn; ++w)
+          cur[w * L] = fmin(lifted ? nlo[w * L] + z_new : nlo[w * L], nhi[w * L] + lam_new);
       } else if (valid) {
-        acc += (double)fmin(m0, lam_new + m1r);  // E^j at the updated lambda
+        acc += (double)fmin(lifted ? z_new + m0 : m0, lam_new + m1r);  // E^j at the updated lambda
       }
     }
     return acc;
@@ -292,17 +315,13 @@ __device__ __forceinline__ double process_bdd(const int K, const int nodes, cons
         m0 = fmin(m0, cf + D[(e & 0xFFFFu) * L]);
         m1r = fmin(m1r, cf + D[(e >> 16) * L]);
       }
-      const T l = lam[h * L];
-      const T m1 = l + m1r;
-      const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
-      const T lam_new = add_rn(sub_rn(l, delta), va[h * L]);
-      emit(h, lam_new, delta, m0, m1);
-      if (valid) acc += (double)fmin(delta, T(0));
+      T z_new, lam_new;
+      update(h, m0, m1r, z_new, lam_new);
       // shp(v, T), v in P_h, with the updated lambda_h
 #pragma unroll 1
       for (int n = n0; n < n1; ++n) {
         const uint32_t e = tp[n * ts];
-        D[n * L] = fmin(D[(e & 0xFFFFu) * L], lam_new + D[(e >> 16) * L]);
+        D[n * L] = fmin(lifted ? z_new + D[(e & 0xFFFFu) * L] : D[(e & 0xFFFFu) * L], lam_new + D[(e >> 16) * L]);
       }
     }
     if (valid) acc += (double)D[0];  // E^j = shp(r, T)
@@ -363,27 +382,35 @@ __device__ __forceinline__ T warp_min(T v) {
 template <typename T, int MODE, bool REC>
 __device__ __noinline__ double process_bdd_coop(const int K, const int nodes, const int32_t *ho, const uint2 *tp,
                                                 T *lam, T *va, T *D, typename OrdOf<T>::U *buf, const int bw,
-                                                const int lane, const T omega, const T clamp, T *m0g, T *m1g) {
+                                                const int lane, const T omega, const T clamp, T *m0g, T *m1g,
+                                                T *l0, const T *v0) {
+  // l0 != null: lifted mode, 0-arcs cost lambda^{j,0}_h = l0[h]
   using U = typename OrdOf<T>::U;
   constexpr int CB = 4;
   const T inf = t_inf<T>();
   const U uinf = t_ord(inf);
   double acc = 0.0;
-  // dual update of partition h from the reduced min-marginals
-  auto update = [&](int h, T m0, T m1r) -> T {
+  const bool lifted = l0 != nullptr;
+  // dual update of partition h from the reduced min-marginals (
+  // lifted: reading A8); z = lambda^{j,0}_h after it (0 unless lifted)
+  auto update = [&](int h, T m0r, T m1r, T &z) -> T {
     const T l = lam[h];
+    const T z0 = lifted ? l0[h] : T(0);
+    const T m0 = lifted ? z0 + m0r : m0r;
     const T m1 = l + m1r;
     const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
-    const T lam_new = add_rn(sub_rn(l, delta), va[h]);
-    __syncwarp();  // every lane has read lam[h] / va[h]
+    const T lam_new = lifted ? add_rn(sub_rn(l, fmax(delta, T(0))), va[h]) : add_rn(sub_rn(l, delta), va[h]);
+    z = lifted ? add_rn(sub_rn(z0, fmax(-delta, T(0))), v0[h]) : T(0);
+    __syncwarp();  // every lane has read lam[h] / va[h] / l0[h]
     if (lane == 0) {
       lam[h] = lam_new;
       va[h] = delta;
+      if (lifted) l0[h] = z;
       if (REC) {
         m0g[h] = m0;
         m1g[h] = m1;
       }
-      acc += (double)fmin(delta, T(0));
+      if (!lifted) acc += (double)fmin(delta, T(0));
     }
     return lam_new;
   };
@@ -394,6 +421,7 @@ __device__ __noinline__ double process_bdd_coop(const int K, const int nodes, co
     for (int h = K - 1; h >= 0; --h) {
       const int n0 = ho[h], n1 = ho[h + 1];
       T l = lam[h];
+      T z = lifted ? l0[h] : T(0);
       if (MODE == kBackward) {
         T m0 = inf, m1r = inf;
 #pragma unroll 1
@@ -417,7 +445,7 @@ __device__ __noinline__ double process_bdd_coop(const int K, const int nodes, co
             m1r = fmin(m1r, cf[q] + x1[q]);
           }
         }
-        l = update(h, warp_min(m0), warp_min(m1r));
+        l = update(h, warp_min(m0), warp_min(m1r), z);
       }
 #pragma unroll 1
       for (int nb = n0 + lane; nb < n1; nb += 32 * CB) {
@@ -426,7 +454,7 @@ __device__ __noinline__ double process_bdd_coop(const int K, const int nodes, co
 #pragma unroll
         for (int q = 0; q < CB; ++q) e[q] = nb + 32 * q < n1 ? tp[nb + 32 * q] : make_uint2(nodes + 1, nodes + 1);
 #pragma unroll
-        for (int q = 0; q < CB; ++q) v[q] = fmin(D[e[q].x], l + D[e[q].y]);
+        for (int q = 0; q < CB; ++q) v[q] = fmin(lifted ? z + D[e[q].x] : D[e[q].x], l + D[e[q].y]);
 #pragma unroll
         for (int q = 0; q < CB; ++q)
           if (nb + 32 * q < n1) D[nb + 32 * q] = v[q];
@@ -474,7 +502,8 @@ __device__ __noinline__ double process_bdd_coop(const int K, const int nodes, co
       m1r = warp_min(m1r);
     }
     T l = lam[h];
-    if (MODE == kForward) l = update(h, m0, m1r);
+    T z = lifted ? l0[h] : T(0);
+    if (MODE == kForward) l = update(h, m0, m1r, z);
     __syncwarp();  // nxt initialised; the reads of D of P_{h+1} are done
     // D of P_h <- shp(r, v); relax into P_{h+1} (A4: 1-arcs priced with the updated lambda_h)
 #pragma unroll 1
@@ -492,7 +521,7 @@ __device__ __noinline__ double process_bdd_coop(const int K, const int nodes, co
         if (nb + 32 * q >= n1) continue;
         D[nb + 32 * q] = cf[q];
         if (!last) {
-          if ((int)e[q].x < n1 + Wn) atomicMin(&nxt[e[q].x - n1], t_ord(cf[q]));      // 0-arc (bottom: skipped)
+          if ((int)e[q].x < n1 + Wn) atomicMin(&nxt[e[q].x - n1], t_ord(lifted ? cf[q] + z : cf[q]));  // 0-arc
           if ((int)e[q].y < n1 + Wn) atomicMin(&nxt[e[q].y - n1], t_ord(cf[q] + l));  // 1-arc
         }
       }
@@ -503,7 +532,7 @@ __device__ __noinline__ double process_bdd_coop(const int K, const int nodes, co
       cur = nxt;
       nxt = t;
     } else if (lane == 0) {
-      acc += (double)fmin(m0, l + m1r);  // E^j = shp(r, T) (at the updated lambda)
+      acc += (double)fmin(lifted ? z + m0 : m0, l + m1r);  // E^j = shp(r, T) (at the updated lambda)
     }
   }
   return acc;
@@ -908,6 +937,69 @@ __device__ __forceinline__ int4 tail_of(const HopRec<T> *rec, int h, int hb = 0)
   return hop_tail(rec + (h - hb));
 }
 
+// Distance accessors of the mask loops: where the lane's distances D[node]
+// live.  SmemD: a column of shared memory ([node][L] layout, stride L, row k
+// of the lane at +32 k).  TmemD (fp32, one row per lane, 32-row tiles of the
+// recompute design): the warp's 32 TMEM lanes (one per BDD), column = node --
+// tcgen05.st / tcgen05.ld (32x32b shape) move a lane's value(s) between its
+// registers and its TMEM lane; loads are waited for (tcgen05.wait::ld) only
+// where their value is consumed, one hop later.
+template <typename T, int R>
+struct SmemD {
+  T *p;
+  uint32_t L;
+  __device__ __forceinline__ void st(uint32_t n, int k, T v) const { p[n * L + 32u * k] = v; }
+  // node n, and node n + 1 if both
+  __device__ __forceinline__ void st2(uint32_t n, int k, T a, T b, bool both) const {
+    p[n * L + 32u * k] = a;
+    if (both) p[(n + 1) * L + 32u * k] = b;
+  }
+  __device__ __forceinline__ T ld(uint32_t n, int k) const { return p[n * L + 32u * k]; }
+  __device__ __forceinline__ void ld2(uint32_t n, int k, T &a, T &b) const {
+    a = p[n * L + 32u * k];
+    b = p[(n + 1) * L + 32u * k];
+  }
+  __device__ __forceinline__ void wait(T &, T &) const {}
+  __device__ __forceinline__ void fence_st() const {}
+};
+
+struct TmemD {
+  uint32_t ta;  // TMEM address of column 0 in the warp's lane quarter
+  __device__ __forceinline__ void st(uint32_t n, int, float v) const {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(ta + n), "r"(__float_as_uint(v))
+                 : "memory");
+  }
+  __device__ __forceinline__ void st2(uint32_t n, int, float a, float b, bool both) const {
+    if (both)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(ta + n), "r"(__float_as_uint(a)),
+                   "r"(__float_as_uint(b))
+                   : "memory");
+    else
+      st(n, 0, a);
+  }
+  __device__ __forceinline__ void ld2(uint32_t n, int, float &a, float &b) const {
+    uint32_t x, y;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "r"(ta + n) : "memory");
+    a = __uint_as_float(x);
+    b = __uint_as_float(y);
+  }
+  __device__ __forceinline__ float ld(uint32_t n, int) const {
+    float a, b;
+    ld2(n, 0, a, b);
+    wait(a, b);
+    return a;
+  }
+  // the registers of a tcgen05.ld are valid after tcgen05.wait::ld; routing
+  // them through the wait makes every use depend on it
+  __device__ __forceinline__ void wait(float &a, float &b) const {
+    uint32_t x = __float_as_uint(a), y = __float_as_uint(b);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(x), "+r"(y)::"memory");
+    a = __uint_as_float(x);
+    b = __uint_as_float(y);
+  }
+  __device__ __forceinline__ void fence_st() const { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+};
+
 // Rows per lane (R): a tile of L = 32 R rows of one shape gives lane l the rows
 // l, l + 32, ..., l + 32 (R - 1); their values sit at +32 k in every [index][L]
 // array.  The R chains share the hop tail, the addresses and the loop control,
@@ -916,9 +1008,9 @@ __device__ __forceinline__ int4 tail_of(const HopRec<T> *rec, int h, int hb = 0)
 
 // shp(v, T) of every node under the current lambda (no update); e[k] =
 // shp(r, T) = E^j.  (kEnergy; phase 1 of a recompute forward pass.)
-template <typename T, int LC, bool ENDS, int R>
+template <typename T, int LC, bool ENDS, int R, class DA>
 __device__ __forceinline__ void mask_ctt_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                              const T *lam, T *D, T (&e)[R]) {
+                                              const T *lam, const DA &D, T (&e)[R]) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   T x0[R], x1[R], l[R];
   int4 tl = tail_of<ENDS>(rec, K - 1);
@@ -937,8 +1029,7 @@ __device__ __forceinline__ void mask_ctt_impl(const int K, const int chain, cons
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       hop_ctt(decltype(ch)::value, rec + (uint32_t)h, x0[k], x1[k], l[k], x0[k], x1[k]);
-      D[tl.x * L + 32u * k] = x0[k];
-      if (tl.z) D[(tl.x + 1) * L + 32u * k] = x1[k];
+      D.st2(tl.x, k, x0[k], x1[k], tl.z != 0);
     }
     tl = tn;
 #pragma unroll
@@ -960,18 +1051,18 @@ __device__ __forceinline__ void mask_ctt_impl(const int K, const int chain, cons
   for (int k = 0; k < R; ++k) e[k] = x0[k];
 }
 
-template <typename T, int LC, int R>
+template <typename T, int LC, int R, class DA>
 __device__ __forceinline__ void mask_ctt(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                         const T *lam, T *D, T (&e)[R]) {
+                                         const T *lam, const DA &D, T (&e)[R]) {
   if (chain & 2) mask_ctt_impl<T, LC, true, R>(K, chain, rec, L_rt, lam, D, e);
   else mask_ctt_impl<T, LC, false, R>(K, chain, rec, L_rt, lam, D, e);
 }
 
 // shp(r, v) of every node under the current lambda (no update); e[k] =
 // shp(r, T) = E^j.  (kCfr; phase 1 of a recompute backward pass.)
-template <typename T, int LC, bool ENDS, int R>
+template <typename T, int LC, bool ENDS, int R, class DA>
 __device__ __forceinline__ void mask_cfr_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                              const T *lam, T *D, T (&e)[R]) {
+                                              const T *lam, const DA &D, T (&e)[R]) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   T c0[R], c1[R], l[R];
   int4 tl = tail_of<ENDS>(rec, 0);
@@ -989,8 +1080,7 @@ __device__ __forceinline__ void mask_cfr_impl(const int K, const int chain, cons
     for (int k = 0; k < R; ++k) ln[k] = lam[hn * L + 32u * k];
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      D[tl.x * L + 32u * k] = c0[k];
-      if (tl.z) D[(tl.x + 1) * L + 32u * k] = c1[k];
+      D.st2(tl.x, k, c0[k], c1[k], tl.z != 0);
       hop_relax(decltype(ch)::value, rec + (uint32_t)h, c0[k], c1[k], l[k], c0[k], c1[k]);
     }
     tl = tn;
@@ -1013,9 +1103,9 @@ __device__ __forceinline__ void mask_cfr_impl(const int K, const int chain, cons
   for (int k = 0; k < R; ++k) e[k] = c0[k];  // after the last partition: the relaxation into top
 }
 
-template <typename T, int LC, int R>
+template <typename T, int LC, int R, class DA>
 __device__ __forceinline__ void mask_cfr(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                         const T *lam, T *D, T (&e)[R]) {
+                                         const T *lam, const DA &D, T (&e)[R]) {
   if (chain & 2) mask_cfr_impl<T, LC, true, R>(K, chain, rec, L_rt, lam, D, e);
   else mask_cfr_impl<T, LC, false, R>(K, chain, rec, L_rt, lam, D, e);
 }
@@ -1024,9 +1114,9 @@ __device__ __forceinline__ void mask_cfr(const int K, const int chain, const Hop
 // previous backward pass, or recomputed by mask_ctt); STORE: D of P_h is
 // overwritten with shp(r, v) for the next backward pass (P:315-316 reuse).
 // vm: bit k set if row k of the lane is a real row (not padding).
-template <typename T, bool STORE, bool REC, int LC, bool ENDS, int R>
+template <typename T, bool STORE, bool REC, int LC, bool ENDS, int R, class DA>
 __device__ __forceinline__ double mask_forward_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                                    T *lam, T *va, T *D, const uint32_t vm, const T omega,
+                                                    T *lam, T *va, const DA &D, const uint32_t vm, const T omega,
                                                     const T clamp, T *m0g, T *m1g) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   double acc = 0.0;
@@ -1038,8 +1128,8 @@ __device__ __forceinline__ double mask_forward_impl(const int K, const int chain
     c1[k] = t_inf<T>();
     l[k] = lam[32u * k];
     av[k] = va[32u * k];
-    x0[k] = D[tl.y * L + 32u * k];
-    x1[k] = D[(tl.y + 1) * L + 32u * k];
+    D.ld2(tl.y, k, x0[k], x1[k]);
+    D.wait(x0[k], x1[k]);
   }
   auto step = [&](auto ch, int h) {
     constexpr int ty = decltype(ch)::value;
@@ -1050,15 +1140,11 @@ __device__ __forceinline__ double mask_forward_impl(const int K, const int chain
     for (int k = 0; k < R; ++k) {
       ln[k] = lam[hn * L + 32u * k];
       avn[k] = va[hn * L + 32u * k];
-      x0n[k] = D[tn.y * L + 32u * k];
-      x1n[k] = D[(tn.y + 1) * L + 32u * k];
+      D.ld2(tn.y, k, x0n[k], x1n[k]);
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      if (STORE) {
-        D[tl.x * L + 32u * k] = c0[k];
-        if (tl.z) D[(tl.x + 1) * L + 32u * k] = c1[k];
-      }
+      if (STORE) D.st2(tl.x, k, c0[k], c1[k], tl.z != 0);
       T m0, m1r;
       hop_mm(ty, rec + (uint32_t)h, x0[k], x1[k], c0[k], c1[k], m0, m1r);
       const T lam_new = mask_finish<T, REC>(lam + 32u * k, va + 32u * k, (uint32_t)h * L, l[k], av[k], m0, m1r,
@@ -1069,6 +1155,7 @@ __device__ __forceinline__ double mask_forward_impl(const int K, const int chain
     tl = tn;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
+      D.wait(x0n[k], x1n[k]);
       l[k] = ln[k];
       av[k] = avn[k];
       x0[k] = x0n[k];
@@ -1093,10 +1180,10 @@ __device__ __forceinline__ double mask_forward_impl(const int K, const int chain
   return acc;
 }
 
-template <typename T, bool STORE, bool REC, int LC, int R>
+template <typename T, bool STORE, bool REC, int LC, int R, class DA>
 __device__ __forceinline__ double mask_forward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                               T *lam, T *va, T *D, const uint32_t vm, const T omega, const T clamp,
-                                               T *m0g, T *m1g) {
+                                               T *lam, T *va, const DA &D, const uint32_t vm, const T omega,
+                                               const T clamp, T *m0g, T *m1g) {
   if (chain & 2)
     return mask_forward_impl<T, STORE, REC, LC, true, R>(K, chain, rec, L_rt, lam, va, D, vm, omega, clamp, m0g, m1g);
   return mask_forward_impl<T, STORE, REC, LC, false, R>(K, chain, rec, L_rt, lam, va, D, vm, omega, clamp, m0g, m1g);
@@ -1105,9 +1192,9 @@ __device__ __forceinline__ double mask_forward(const int K, const int chain, con
 // backward pass with updates.  D holds shp(r, v) (stored by the
 // forward pass, or recomputed by mask_cfr); STORE: D of P_h is overwritten
 // with shp(v, T) for the next forward pass.
-template <typename T, bool STORE, bool REC, int LC, bool ENDS, int R>
+template <typename T, bool STORE, bool REC, int LC, bool ENDS, int R, class DA>
 __device__ __forceinline__ double mask_backward_impl(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                                     T *lam, T *va, T *D, const uint32_t vm, const T omega,
+                                                     T *lam, T *va, const DA &D, const uint32_t vm, const T omega,
                                                      const T clamp, T *m0g, T *m1g) {
   const uint32_t L = LC ? LC : L_rt;  // unsigned offsets: one wide multiply-add per address
   const T inf = t_inf<T>();
@@ -1122,8 +1209,9 @@ __device__ __forceinline__ double mask_backward_impl(const int K, const int chai
     x1[k] = inf;
     l[k] = lam[(K - 1) * L + 32u * k];
     av[k] = va[(K - 1) * L + 32u * k];
-    f0[k] = D[tl.x * L + 32u * k];
-    f1[k] = tl.z ? D[(tl.x + 1) * L + 32u * k] : inf;
+    D.ld2(tl.x, k, f0[k], f1[k]);  // (the second entry of a one-node partition is not used)
+    D.wait(f0[k], f1[k]);
+    if (!tl.z) f1[k] = inf;
   }
   auto step = [&](auto ch, int h) {
     constexpr int ty = decltype(ch)::value;
@@ -1134,8 +1222,7 @@ __device__ __forceinline__ double mask_backward_impl(const int K, const int chai
     for (int k = 0; k < R; ++k) {
       ln[k] = lam[hn * L + 32u * k];
       avn[k] = va[hn * L + 32u * k];
-      f0n[k] = D[tn.x * L + 32u * k];
-      f1n[k] = tn.z ? D[(tn.x + 1) * L + 32u * k] : inf;
+      D.ld2(tn.x, k, f0n[k], f1n[k]);
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -1145,18 +1232,16 @@ __device__ __forceinline__ double mask_backward_impl(const int K, const int chai
                                             (vm >> k) & 1u, omega, clamp, REC ? m0g + 32u * k : nullptr,
                                             REC ? m1g + 32u * k : nullptr, acc);
       hop_ctt(ty, rec + (uint32_t)h, x0[k], x1[k], lam_new, x0[k], x1[k]);  // shp(v, T) with the updated lambda_h
-      if (STORE) {
-        D[tl.x * L + 32u * k] = x0[k];
-        if (tl.z) D[(tl.x + 1) * L + 32u * k] = x1[k];
-      }
+      if (STORE) D.st2(tl.x, k, x0[k], x1[k], tl.z != 0);
     }
     tl = tn;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
+      D.wait(f0n[k], f1n[k]);
       l[k] = ln[k];
       av[k] = avn[k];
       f0[k] = f0n[k];
-      f1[k] = f1n[k];
+      f1[k] = tn.z ? f1n[k] : inf;
     }
   };
   int h = K - 1;
@@ -1177,10 +1262,10 @@ __device__ __forceinline__ double mask_backward_impl(const int K, const int chai
   return acc;
 }
 
-template <typename T, bool STORE, bool REC, int LC, int R>
+template <typename T, bool STORE, bool REC, int LC, int R, class DA>
 __device__ __forceinline__ double mask_backward(const int K, const int chain, const HopRec<T> *rec, const int L_rt,
-                                                T *lam, T *va, T *D, const uint32_t vm, const T omega, const T clamp,
-                                                T *m0g, T *m1g) {
+                                                T *lam, T *va, const DA &D, const uint32_t vm, const T omega,
+                                                const T clamp, T *m0g, T *m1g) {
   if (chain & 2)
     return mask_backward_impl<T, STORE, REC, LC, true, R>(K, chain, rec, L_rt, lam, va, D, vm, omega, clamp, m0g, m1g);
   return mask_backward_impl<T, STORE, REC, LC, false, R>(K, chain, rec, L_rt, lam, va, D, vm, omega, clamp, m0g, m1g);
@@ -1188,10 +1273,10 @@ __device__ __forceinline__ double mask_backward(const int K, const int chain, co
 
 // One arc-mask tile of one pass: the four modes over the lane's R rows.
 // Returns the lane's share of the tile's bound partial.
-template <typename T, int MODE, bool REC, bool RC, int LC, int R>
+template <typename T, int MODE, bool REC, bool RC, int LC, int R, class DA>
 __device__ __forceinline__ double mask_tile(const int K, const int chain, const HopRec<T> *rec, const int L,
-                                            T *lm, T *vp, T *D, const uint32_t vm, const T omega, const T clamp,
-                                            T *m0p, T *m1p) {
+                                            T *lm, T *vp, const DA &D, const uint32_t vm, const T omega,
+                                            const T clamp, T *m0p, T *m1p) {
   T e[R];
   double acc = 0.0;
   if (MODE == kEnergy || MODE == kCfr) {
@@ -1201,10 +1286,16 @@ __device__ __forceinline__ double mask_tile(const int K, const int chain, const 
     for (int k = 0; k < R; ++k)
       if ((vm >> k) & 1u) acc += (double)e[k];
   } else if (MODE == kForward) {
-    if (RC) mask_ctt<T, LC, R>(K, chain, rec, L, lm, D, e);
+    if (RC) {
+      mask_ctt<T, LC, R>(K, chain, rec, L, lm, D, e);
+      D.fence_st();  // (TMEM: the stores above complete before the loads below)
+    }
     acc = mask_forward<T, !RC, REC, LC, R>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
   } else {
-    if (RC) mask_cfr<T, LC, R>(K, chain, rec, L, lm, D, e);
+    if (RC) {
+      mask_cfr<T, LC, R>(K, chain, rec, L, lm, D, e);
+      D.fence_st();
+    }
     acc = mask_backward<T, !RC, REC, LC, R>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
   }
   return acc;
@@ -1284,9 +1375,14 @@ __device__ __forceinline__ void fetch_desc(TileDesc *dst, const TileDesc *src, i
 // hold lambda, averages, topology and partition offsets only; the distances
 // live in a per-warp scratch column per lane (the DB region) and never touch HBM.
 // RW: the most rows per lane of any tile (1, 2 or 4; separate instantiations so
-// that problems without wide tiles keep the register budget of RW = 1)
-template <typename T, int MODE, bool REC, bool RC, int RW>
+// that problems without wide tiles keep the register budget of RW = 1).
+// TM: the recompute design's distances of 32-row tiles in tensor memory (fp32,
+// RW = 1).  A kernel holding tcgen05 code runs one CTA per SM (the driver's
+// rule), so TM kernels launch one CTA of up to 16 warps per SM and the others
+// carry no tcgen05 code at all.
+template <typename T, int MODE, bool REC, bool RC, int RW, bool TM>
 __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
+  static_assert(!TM || (RC && RW == 1 && std::is_same<T, float>::value), "TMEM distances: fp32 recompute design");
   constexpr bool kUpd = MODE == kForward || MODE == kBackward;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -1304,6 +1400,30 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   T *__restrict__ gdist = reinterpret_cast<T *>(a.dist);
   const T omega = T(a.omega), clamp = T(a.clamp);
   const int gwarp = blockIdx.x * wpb + warp;
+
+  // TM: the distance scratch of the 32-row arc-mask tiles lives in tensor
+  // memory.  The CTA allocates groups x tmem_cols columns (tmem_cols >= nodes
+  // + 2 of every such tile, groups = ceil(warps / 4), rounded to a power of
+  // two); warp w uses TMEM lanes [32 (w % 4), + 32) -- one per BDD -- and
+  // columns [tmem_cols (w / 4), + tmem_cols), column = node.  Shared memory then
+  // holds only the stages.
+  uint32_t tm_base = 0, tm_alloc = 0;
+  uint32_t *const tm_slot = reinterpret_cast<uint32_t *>(smem_raw + 16);  // (warp 0's header, unused bytes)
+  if constexpr (TM) {
+    const uint32_t groups = (uint32_t)(wpb + 3) / 4;
+    tm_alloc = 32;
+    while (tm_alloc < groups * (uint32_t)a.tmem_cols) tm_alloc *= 2;
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tm_slot)),
+                   "r"(tm_alloc)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    tm_base = *tm_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * (uint32_t)a.tmem_cols;
+  }
 
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -1411,7 +1531,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
           const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(s.topo);
           const int chain = ((d.kind & 8) ? 1 : 0) | ((d.kind & 16) ? 2 : 0);
           T *D = RC ? reinterpret_cast<T *>(rbase) + lane : s.dist + lane;
-          if (RC)
+          if (RC && !(TM && L == 32))
             for (int o = 0; o < L; o += 32) {
               D[d.nodes * L + o] = T(0);              // top
               D[(d.nodes + 1) * L + o] = t_inf<T>();  // bottom
@@ -1422,14 +1542,26 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
           // rows per lane: tiles of 64 / 128 rows (short rows, plan.cpp)
           const uint32_t vm = (lane < d.n_lanes ? 1u : 0u) | (lane + 32 < d.n_lanes ? 2u : 0u) |
                               (lane + 64 < d.n_lanes ? 4u : 0u) | (lane + 96 < d.n_lanes ? 8u : 0u);
-          if (L == 32)
-            acc = mask_tile<T, MODE, REC, RC, 32, 1>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
-          else if (RW >= 2 && L == 64)
-            acc = mask_tile<T, MODE, REC, RC, 64, 2>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
-          else if (RW >= 4 && L == 128)
-            acc = mask_tile<T, MODE, REC, RC, 128, 4>(K, chain, rec, L, lm, vp, D, vm, omega, clamp, m0p, m1p);
-          else
-            acc = mask_tile<T, MODE, REC, RC, 0, 1>(K, chain, rec, L, lm, vp, D, vm & 1u, omega, clamp, m0p, m1p);
+          if (L == 32) {
+            if constexpr (TM) {  // distances in the warp's TMEM lanes (plan: Plan::tmem_cols)
+              __syncwarp();        // (tcgen05 ops are warp-collective: converged after the stage wait)
+              const TmemD tm{tm_base};
+              tm.st2(d.nodes, 0, T(0), t_inf<T>(), true);  // top, bottom
+              acc = mask_tile<T, MODE, REC, RC, 32, 1>(K, chain, rec, L, lm, vp, tm, vm, omega, clamp, m0p, m1p);
+            } else {
+              acc = mask_tile<T, MODE, REC, RC, 32, 1>(K, chain, rec, L, lm, vp, SmemD<T, 1>{D, 32u}, vm, omega, clamp,
+                                                       m0p, m1p);
+            }
+          } else if (RW >= 2 && L == 64) {
+            acc = mask_tile<T, MODE, REC, RC, 64, 2>(K, chain, rec, L, lm, vp, SmemD<T, 2>{D, 64u}, vm, omega, clamp,
+                                                     m0p, m1p);
+          } else if (RW >= 4 && L == 128) {
+            acc = mask_tile<T, MODE, REC, RC, 128, 4>(K, chain, rec, L, lm, vp, SmemD<T, 4>{D, 128u}, vm, omega,
+                                                      clamp, m0p, m1p);
+          } else {
+            acc = mask_tile<T, MODE, REC, RC, 0, 1>(K, chain, rec, L, lm, vp, SmemD<T, 1>{D, (uint32_t)L}, vm & 1u,
+                                                    omega, clamp, m0p, m1p);
+          }
         }
       } else if (RC) {
         if (active) {
@@ -1498,7 +1630,9 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
       acc = process_bdd_coop<T, MODE, REC>(K, d.nodes, a.hop_off + d.hop_base,
                                            reinterpret_cast<const uint2 *>(a.topo) + d.topo_base,
                                            lambda + d.slot_base, delta_out + d.slot_base, gdist + d.dist_base, buf,
-                                           a.coop_bw, lane, omega, clamp, m0p, m1p);
+                                           a.coop_bw, lane, omega, clamp, m0p, m1p,
+                                           a.lambda0 ? reinterpret_cast<T *>(a.lambda0) + d.slot_base : nullptr,
+                                           a.avg0 ? reinterpret_cast<const T *>(a.avg0) + d.slot_base : nullptr);
     } else {
       // direct tile (exceeds the per-warp budget; L = 32): global memory and a
       // per-warp scratch area for the relaxation buffers
@@ -1509,7 +1643,9 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
       T *m1p = REC ? reinterpret_cast<T *>(a.m1) + sbase : nullptr;
       acc = process_bdd<T, MODE, REC>(K, d.nodes, a.hop_off + d.hop_base, tp, (d.kind & 1) ? 32 : 1, 32,
                                       lambda + sbase, delta_out + sbase, gdist + d.dist_base + lane, R, d.max_w,
-                                      valid, omega, clamp, m0p, m1p);
+                                      valid, omega, clamp, m0p, m1p,
+                                      a.lambda0 ? reinterpret_cast<T *>(a.lambda0) + sbase : nullptr,
+                                      a.avg0 ? reinterpret_cast<const T *>(a.avg0) + sbase : nullptr);
     }
     acc = warp_sum(acc);
     if (lane == 0) a.lb_part[t] = acc;
@@ -1539,6 +1675,12 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   }
   if (lane == 0) bulk_wait_read_all();  // shared memory must outlive the TMA stores' reads
   __syncwarp();
+  if constexpr (TM) {  // every warp is done with its TMEM lanes
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tm_slot), "r"(tm_alloc) : "memory");
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1860,11 +2002,15 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
     T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
     const T omega = T(a.omega), clamp = T(a.clamp);
     if (L == 32) {
-      acc = MODE == kForward ? mask_forward<T, true, REC, 32, 1>(K, chain, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g)
-                             : mask_backward<T, true, REC, 32, 1>(K, chain, rec, 32, lam, va, D, valid, omega, clamp, m0g, m1g);
+      acc = MODE == kForward ? mask_forward<T, true, REC, 32, 1>(K, chain, rec, 32, lam, va, SmemD<T, 1>{D, 32u}, valid,
+                                                                 omega, clamp, m0g, m1g)
+                             : mask_backward<T, true, REC, 32, 1>(K, chain, rec, 32, lam, va, SmemD<T, 1>{D, 32u}, valid,
+                                                                  omega, clamp, m0g, m1g);
     } else {
-      acc = MODE == kForward ? mask_forward<T, true, REC, 0, 1>(K, chain, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g)
-                             : mask_backward<T, true, REC, 0, 1>(K, chain, rec, L, lam, va, D, valid, omega, clamp, m0g, m1g);
+      acc = MODE == kForward ? mask_forward<T, true, REC, 0, 1>(K, chain, rec, L, lam, va, SmemD<T, 1>{D, (uint32_t)L},
+                                                                valid, omega, clamp, m0g, m1g)
+                             : mask_backward<T, true, REC, 0, 1>(K, chain, rec, L, lam, va, SmemD<T, 1>{D, (uint32_t)L},
+                                                                 valid, omega, clamp, m0g, m1g);
     }
   } else if (lane < L) {
     const int32_t *ho = a.hop_off + d.hop_base;
@@ -2612,18 +2758,23 @@ __device__ __forceinline__ void dist_dp_row(const SeqArgs &a, const TileDesc &d,
 
 // ---------------------------------------------------------------- launchers
 
-template <typename T, bool RC, int RW>
+template <typename T, bool RC, int RW, bool TM = false>
 static const void *sweep_fn_rw(int mode, bool rec) {
   if (mode == kForward)
-    return rec ? (const void *)sweep_kernel<T, kForward, true, RC, RW> : (const void *)sweep_kernel<T, kForward, false, RC, RW>;
+    return rec ? (const void *)sweep_kernel<T, kForward, true, RC, RW, TM>
+               : (const void *)sweep_kernel<T, kForward, false, RC, RW, TM>;
   if (mode == kBackward)
-    return rec ? (const void *)sweep_kernel<T, kBackward, true, RC, RW> : (const void *)sweep_kernel<T, kBackward, false, RC, RW>;
-  if (mode == kCfr) return RC ? nullptr : (const void *)sweep_kernel<T, kCfr, false, false, RW>;
-  return (const void *)sweep_kernel<T, kEnergy, false, RC, RW>;
+    return rec ? (const void *)sweep_kernel<T, kBackward, true, RC, RW, TM>
+               : (const void *)sweep_kernel<T, kBackward, false, RC, RW, TM>;
+  if (mode == kCfr) return RC ? nullptr : (const void *)sweep_kernel<T, kCfr, false, false, RW, false>;
+  return (const void *)sweep_kernel<T, kEnergy, false, RC, RW, TM>;
 }
 
+// rw: most rows per lane; rw == 0: the TMEM variant (fp32 recompute design)
 template <typename T, bool RC>
 static const void *sweep_fn(int mode, bool rec, int rw) {
+  if constexpr (RC && std::is_same<T, float>::value)
+    if (rw == 0) return sweep_fn_rw<T, true, 1, true>(mode, rec);
   if (rw >= 4 && sizeof(T) == 4) return sweep_fn_rw<T, RC, 4>(mode, rec);  // (fp64 plans stop at 2 rows per lane)
   if (rw >= 2) return sweep_fn_rw<T, RC, 2>(mode, rec);
   return sweep_fn_rw<T, RC, 1>(mode, rec);
@@ -2709,7 +2860,7 @@ int preload_kernels(int precision) {
   for (int mode = 0; mode < 4 && e == cudaSuccess; ++mode)
     for (int rec = 0; rec < 2 && e == cudaSuccess; ++rec)
       for (int rc = 0; rc < 2 && e == cudaSuccess; ++rc) {
-        for (int rw = 1; rw <= 4 && e == cudaSuccess; rw *= 2) e = load(sweep_ptr(precision, mode, rec != 0, rc != 0, rw));
+        for (int rw = 0; rw <= 4 && e == cudaSuccess; rw = rw ? 2 * rw : 1) e = load(sweep_ptr(precision, mode, rec != 0, rc != 0, rw));
         if (e == cudaSuccess && !rc)
           e = load(precision == 64 ? stream_fn<double>(mode, rec != 0) : stream_fn<float>(mode, rec != 0));
         if (e == cudaSuccess && !rc)
@@ -2758,6 +2909,87 @@ int launch_avg_finish(int precision, const AvgArgs &a, int32_t n_shared, const i
     avg_finish_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(a, n_shared, xlocal, deg_x);
   else
     avg_finish_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(a, n_shared, xlocal, deg_x);
+  return (int)cudaGetLastError();
+}
+
+// ---- lifted representation (fdog_options::lifted) ----------------
+// The two deferred averages of a variable (reading A8, j ascending, A1):
+// avg1_i = (1/|J_i|) sum_k max(delta_bar_ik, 0) into every slot of i in
+// avg_slot, avg0_i = (1/|J_i|) sum_k max(-delta_bar_ik, 0) into avg0.  One
+// thread per variable (every variable is in the CSR part in lifted plans).
+template <typename T>
+__global__ void __launch_bounds__(256) avg_lifted_kernel(const AvgArgs a, T *avg0) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  pdl_wait();  // every thread: the sweep before wrote delta_bar (PDL launch)
+  if (q == 0) *a.tile_counter = 0u;
+  if (q >= a.n) return;
+  const T *db = reinterpret_cast<const T *>(a.delta_bar);
+  T *out = reinterpret_cast<T *>(a.avg_slot);
+  const int64_t p0 = a.var_ptr[q], p1 = a.var_ptr[q + 1];
+  T sp = T(0), sn = T(0);
+  for (int64_t x = p0; x < p1; ++x) {
+    const T d = db[a.var_slots[x]];
+    sp = add_rn(sp, fmax(d, T(0)));
+    sn = add_rn(sn, fmax(-d, T(0)));
+  }
+  const T deg = T(a.deg_l[q]);
+  const T v1 = sp / deg, v0 = sn / deg;
+  for (int64_t x = p0; x < p1; ++x) {
+    out[a.var_slots[x]] = v1;
+    avg0[a.var_slots[x]] = v0;
+  }
+}
+
+// final correction, lifted form of P:650-652: lambda^{j,b} += max(+-delta_bar, 0)
+template <typename T>
+__global__ void __launch_bounds__(256) add_deferred_lifted_kernel(int64_t n, T *lam1, T *lam0, T *delta) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const T d = delta[q];
+    lam1[q] = add_rn(lam1[q], fmax(d, T(0)));
+    lam0[q] = add_rn(lam0[q], fmax(-d, T(0)));
+    delta[q] = T(0);
+  }
+}
+
+// out = lambda^1 - lambda^0 per device slot (the original-space lambda)
+template <typename T>
+__global__ void __launch_bounds__(256) lifted_diff_kernel(int64_t n, const T *lam1, const T *lam0, T *out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = sub_rn(lam1[q], lam0[q]);
+}
+
+int launch_avg_lifted(int precision, const AvgArgs &a, void *avg0, void *stream) {
+  const int block = 256;
+  const int grid = (int)std::max<int64_t>(1, ((int64_t)a.n + block - 1) / block);
+  if (precision == 64) {
+    void *args[] = {(void *)&a, &avg0};
+    return launch_pdl((const void *)avg_lifted_kernel<double>, dim3(grid), dim3(block), 0, stream, args);
+  }
+  void *args[] = {(void *)&a, &avg0};
+  return launch_pdl((const void *)avg_lifted_kernel<float>, dim3(grid), dim3(block), 0, stream, args);
+}
+
+int launch_add_deferred_lifted(int precision, int64_t n, void *lam1, void *lam0, void *delta, void *stream) {
+  if (n <= 0) return 0;
+  const int block = 256, grid = grid_for(n, block);
+  if (precision == 64)
+    add_deferred_lifted_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, (double *)lam1, (double *)lam0,
+                                                                                 (double *)delta);
+  else
+    add_deferred_lifted_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, (float *)lam1, (float *)lam0,
+                                                                                (float *)delta);
+  return (int)cudaGetLastError();
+}
+
+int launch_lifted_diff(int precision, int64_t n, const void *lam1, const void *lam0, void *out, void *stream) {
+  if (n <= 0) return 0;
+  const int block = 256, grid = grid_for(n, block);
+  if (precision == 64)
+    lifted_diff_kernel<double><<<grid, block, 0, (cudaStream_t)stream>>>(n, (const double *)lam1, (const double *)lam0,
+                                                                         (double *)out);
+  else
+    lifted_diff_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>(n, (const float *)lam1, (const float *)lam0,
+                                                                        (float *)out);
   return (int)cudaGetLastError();
 }
 

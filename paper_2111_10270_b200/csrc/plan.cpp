@@ -459,6 +459,11 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     return FDOG_EINVAL;
   }
   P.host_threads = threads;
+  P.lifted = o && o->lifted;
+  if (P.lifted && world > 1) {
+    set_error("the lifted representation is single-GPU (world == 1)");
+    return FDOG_EINVAL;
+  }
 
   P.n_vars = p->n_vars;
   P.n_cons = p->n_cons;
@@ -671,7 +676,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // 0.701 -> 0.593; with a few tiles per warp -- GM-worms 6 k tiles, cell
   // tracking 17 k -- the longer tiles cost more in the tail than they save:
   // GM 40.9 -> 45.7 us.  So: problems of at least 10^6 rows.)
-  const bool wide_ok = (wide_force || P.local_rows.size() >= 1000000) && P.n_slots > (1 << 15) && !(sw && sw[0] == 's') && !(fz && fz[0] == '1') && !(wd && wd[0] == '0');
+  const bool wide_ok = !P.lifted && (wide_force || P.local_rows.size() >= 1000000) && P.n_slots > (1 << 15) && !(sw && sw[0] == 's') && !(fz && fz[0] == '1') && !(wd && wd[0] == '0');
   auto rows_per_lane = [&](size_t sh) -> int {
     const Shape &S = P.shapes[sh];
     if (!wide_ok || S.max_w > 2) return 1;
@@ -682,7 +687,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   std::vector<char> pair_room(P.shapes.size(), 0);  // bundle order: stages reserve room for a pair list
   {
     const char *pe = getenv("FDOG_PAIRS");
-    const bool pairs_ok = !(pe && pe[0] == '0');
+    const bool pairs_ok = !(pe && pe[0] == '0') && !P.lifted;
     std::vector<int64_t> seen(pairs_ok ? p->n_vars : 0, -1);  // first (row position / 32) of a |J_i| = 2 variable
     for (size_t sh = 0; sh < by_shape.size() && pairs_ok; ++sh) {
       auto &rows = by_shape[sh];
@@ -726,12 +731,6 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // workload), and so does the L2-resident store design of narrow shapes; see
   // the design choice below.  FDOG_NBUF = 1 | 2 overrides.
   const char *nbuf = getenv("FDOG_NBUF");
-  // FDOG_PARTIAL=1 (experiment, off by default): leftover rows of a narrow
-  // shape in a partly filled tile of that shape (QAP50 98.8 -> 92.3 us per
-  // iteration, GM 40.1 -> 41.5; every GPU parity test passes with it except
-  // a packing-structure assertion of test_edge_cases: open)
-  const char *pt = getenv("FDOG_PARTIAL");
-  const bool partial_ok = pt && pt[0] == '1';
   // (world > 1: a shape's boundary rows after its interior rows, stable)
   if (world > 1)
     for (auto &rows : by_shape)
@@ -747,13 +746,33 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // pack(rc): budget + tiles for the store design (rc = false) or the
   // recompute design (rc = true, narrow shapes only); returns the tiles in
   // launch order
+  // Recompute design, fp32: the distance scratch of 32-row arc-mask tiles can
+  // live in tensor memory (kernels.cu TmemD; columns = the next power of two
+  // >= nodes + 2, <= 512 per SM).  tm: pack for it -- such tiles need no DB
+  // region, and a narrow shape's leftover rows go to a partly filled 32-row
+  // tile of the shape (idle lanes) instead of the per-lane-topology pool.
+  // (not with rows-per-lane tiles: the TMEM kernel variant has one row per lane)
+  const char *tmv = getenv("FDOG_TMEM");
+  int tm_cols = 32;
+  bool tm_rows_ok = true;
+  for (size_t sh = 0; sh < P.shapes.size(); ++sh)
+    if (!by_shape[sh].empty() && P.shapes[sh].max_w <= 2) {
+      while (tm_cols < P.shapes[sh].nodes() + 2) tm_cols *= 2;
+      tm_rows_ok = tm_rows_ok && rows_per_lane(sh) == 1;
+    }
+  bool tm_packed = false, tm_allow = true;
   auto pack = [&](bool rc, int nb) {
     std::vector<PendingTile> pend;
     P.NB = nbuf ? (atoi(nbuf) == 1 ? 1 : 2) : nb;
+    const bool tm = tm_allow && rc && tsz == 4 && !P.lifted && tm_cols <= 512 && tm_rows_ok && !(tmv && tmv[0] == '0');
+    tm_packed = tm;
     // pr: the tile may carry a pair list (at most K L / 2 pairs)
     auto fits = [&](int kind, int K, int nodes, int W, int L, int SB, int DB, bool pr = false) {
+      if (P.lifted) return false;  // (lifted mode: every tile from global memory)
       const int pb = pr ? stage_pairs_bytes(K * L / 2) : 0;
-      if (rc) return stage_bytes_rc(tsz, kind, K, nodes, L) + pb <= SB && stage_dist_bytes(tsz, nodes, L) <= DB;
+      if (rc)
+        return stage_bytes_rc(tsz, kind, K, nodes, L) + pb <= SB &&
+               ((tm && (kind & 4) && L == 32) || stage_dist_bytes(tsz, nodes, L) <= DB);
       // (arc-mask tiles never use the relaxation buffers)
       return stage_bytes(tsz, kind, K, nodes, L) + pb <= SB && ((kind & 4) || relax_bytes(tsz, W, L) <= DB);
     };
@@ -773,11 +792,9 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       const int cands[] = {6, 7, 8, 9, 10, 11, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 72, 96, 112};
       double best = 1e300;
       int bestSB = 0, bestDB = DB0;
-      const char *mk = getenv("FDOG_MAXKB");  // experiment knob: largest per-warp budget (KB) the model may pick
-    const int maxkb = mk ? atoi(mk) : 1 << 30;
-    for (int kb : cands) {
-      if (kb > maxkb) continue;
-        const int SB = rc ? ((kb * 1024 - 16) / (P.NB + 1)) & ~15 : ((kb * 1024 - 16 - DB0) / P.NB) & ~15;
+      for (int kb : cands) {
+        const int SB = tm ? ((kb * 1024 - 16 - 64) / P.NB) & ~15
+                          : rc ? ((kb * 1024 - 16) / (P.NB + 1)) & ~15 : ((kb * 1024 - 16 - DB0) / P.NB) & ~15;
         const int DB = rc ? SB : DB0;
         if (SB <= 0) continue;
         double chain = 0, instr = 0;
@@ -785,7 +802,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         for (size_t s = 0; s < P.shapes.size(); ++s) {
           if (by_shape[s].empty()) continue;
           const Shape &S = P.shapes[s];
-          const int k0 = S.max_w <= 2 ? 4 : 0;  // arc-mask tiles for narrow shapes
+          const int k0 = (S.max_w <= 2 && !P.lifted) ? 4 : 0;  // arc-mask tiles for narrow shapes
           const bool pr = k0 && pair_room[s];
           int L = lanes_for(k0, S.k, S.nodes(), S.max_w, SB, DB, pr, 32 * rows_per_lane(s));
           double pen = (wide_force && L > 0 && L < 32 * rows_per_lane(s)) ? 1e6 : 1.0;
@@ -797,7 +814,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
           } else {
             usedSB = std::max(usedSB, (rc ? stage_bytes_rc(tsz, k0, S.k, S.nodes(), L) : stage_bytes(tsz, k0, S.k, S.nodes(), L)) +
                                           (pr ? stage_pairs_bytes(S.k * L / 2) : 0));
-            if (rc) usedDB = std::max(usedDB, stage_dist_bytes(tsz, S.nodes(), L));
+            if (rc && !(tm && k0 && L == 32)) usedDB = std::max(usedDB, stage_dist_bytes(tsz, S.nodes(), L));
           }
           const double tiles = std::ceil((double)by_shape[s].size() / L);
           const double R = L > 32 ? L / 32 : 1;  // rows per lane: R chains per tile
@@ -812,7 +829,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         }
         if (!rc) usedDB = DB;
         const int wb = warp_bytes(usedSB, usedDB, P.NB);
-        const double warps = std::min(32.0, std::floor(226.0 * 1024 / wb));
+        const double warps = std::min(tm ? 4.0 * (512 / tm_cols) : 32.0, std::floor(226.0 * 1024 / wb));
         if (warps < 1) continue;
         const double t = std::max(chain / (148.0 * warps), instr / (148.0 * 2.0));
         if (t < best * 0.98) {
@@ -829,7 +846,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     for (size_t s = 0; s < P.shapes.size(); ++s) {
       auto &rows = by_shape[s];
       const Shape &S = P.shapes[s];
-      const int k0 = S.max_w <= 2 ? 4 : 0;
+      const int k0 = (S.max_w <= 2 && !P.lifted) ? 4 : 0;
       int L = lanes_for(k0, S.k, S.nodes(), S.max_w, P.SB, P.DB, k0 && pair_room[s], 32 * rows_per_lane(s));
       const bool staged = L > 0;
       if (!staged) L = 32;
@@ -845,7 +862,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       size_t full = rows.size() / L * L;
       const size_t wide_end = full;
       if (L > 32) full += (rows.size() - full) / 32 * 32;
-      if (k0 && (!staged || (rows.size() >= (size_t)std::min(L, 32) && partial_ok))) full = rows.size();
+      if (k0 && (!staged || (tm && L == 32)))
+        full = rows.size();
       for (size_t q = 0; q < full;) {
         PendingTile t;
         const bool ch = k0 && chain_shape(S);
@@ -853,7 +871,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         t.shape = (int32_t)s;
         t.L = q < wide_end ? L : std::min(L, 32);
         const size_t nrow = std::min(rows.size() - q, (size_t)t.L);
-        if (staged && nrow < (size_t)t.L) {
+        if (staged && nrow < (size_t)t.L && !(tm && t.L == 32)) {  // (TMEM tiles stay 32 rows wide)
           t.L = 4;
           while ((size_t)t.L < nrow) t.L *= 2;
         }
@@ -958,7 +976,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // CellTrack 160 MB / QAP50 195 MB / MRF 2.2 GB, recompute 6-27 % faster).
   const double store_bytes = (double)P.n_nodes * 2 * tsz + (double)P.n_slots * 4 * tsz;
   const bool l2_resident = store_bytes <= 0.75 * 126e6;
-  bool rc = narrow && !(sw && (sw[0] == 't' || sw[0] == 's')) && !(fz && fz[0] == '1') &&
+  bool rc = !P.lifted && narrow && !(sw && (sw[0] == 't' || sw[0] == 's')) && !(fz && fz[0] == '1') &&
             (!l2_resident || (sw && sw[0] == 'r'));
   // stage buffers: single-buffered for the recompute design and for the
   // L2-resident store design of narrow shapes (its stages come from L2: more
@@ -978,6 +996,27 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       // stage arrives -- double-buffer (measured: MRF 287 -> 248 us per sweep;
       // CellTrack / QAP50, whose stages are larger, stay single-buffered)
       pend = pack(true, 2);
+    }
+    // TMEM distances: a kernel with tcgen05 code runs one CTA per SM, so they
+    // pay only when the warps per SM they allow (<= 16, 4 per 128 TMEM lanes x
+    // 512 / cols columns, and the stages' shared memory) clearly exceed those of
+    // the shared-memory scratch (measured: QAP50 12 vs 8 warps -3 %, QAP128 4 vs
+    // 3 -6 %; cell tracking 12 vs 12 +1.5 %)
+    if (rc && tm_packed && !(tmv && tmv[0] == '1')) {
+      const int SB1 = P.SB, DB1 = P.DB, NB1 = P.NB;
+      const int w_tm = std::min({16, 4 * (512 / tm_cols), 227 * 1024 / warp_bytes(SB1, DB1, NB1)});
+      tm_allow = false;
+      std::vector<PendingTile> pend0 = pack(true, NB1);
+      const int w_sm = std::min(32, 227 * 1024 / warp_bytes(P.SB, P.DB, P.NB));
+      if (w_tm >= 1.2 * w_sm) {
+        P.SB = SB1;
+        P.DB = DB1;
+        P.NB = NB1;
+        tm_packed = true;
+      } else {
+        pend.swap(pend0);
+        tm_packed = false;
+      }
     }
   }
   P.rc = rc;
@@ -1124,6 +1163,22 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     slot_base = (slot_base + (int64_t)d.K * L + 3) & ~(int64_t)3;
     dist_base = (dist_base + (int64_t)(d.nodes + 2) * L + 3) & ~(int64_t)3;
     P.tiles.push_back(d);
+  }
+  // Recompute design packed for tensor memory (pack() above): the distance
+  // scratch of the 32-row arc-mask tiles lives in TMEM (kernels.cu TmemD),
+  // TMEM columns per CTA = the next power of two >= nodes + 2 of those tiles;
+  // the DB region serves the other tiles only (chosen that way by the budget
+  // model).  4 warps per CTA, 512 / cols CTAs per SM.
+  P.tmem_cols = 0;
+  if (P.rc && tm_packed) {
+    int maxn = 0;
+    for (const auto &d : P.tiles)
+      if ((d.kind & 2) && (d.kind & 4) && d.lanes == 32) maxn = std::max(maxn, d.nodes + 2);
+    if (maxn > 0) {
+      int cols = 32;
+      while (cols < maxn) cols *= 2;
+      P.tmem_cols = cols;  // (<= 512: tm packing requires it)
+    }
   }
   // cooperative tiles: two relaxation buffers of coop_w + 1 entries, in the
   // warp's DB region when they fit 32 KB (else in the solver's scratch)
@@ -1315,7 +1370,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     };
     auto cat = [&](int64_t q) {
       const int64_t d = P.var_ptr[q + 1] - P.var_ptr[q];
-      if (P.var_xidx[q] >= 0) return 2;
+      if (P.var_xidx[q] >= 0 || P.lifted) return 2;  // (lifted mode: one CSR kernel sums both sides)
       if (d <= 2) return closed(q) ? 4 : 0;
       return d <= 4 ? 1 : 2;
     };
@@ -1621,6 +1676,7 @@ fdog_status fdog_plan_stats(const fdog_plan *plan, fdog_stats_t *out) {
   out->tile_pairs = (int64_t)(P.ell.size() / 2) - P.n_ell_open;
   out->interior_tiles = P.world > 1 ? P.n_interior_tiles : (int64_t)P.tiles.size();
   out->coop_tiles = P.coop_tiles;
+  out->tmem_cols = P.tmem_cols;
   return FDOG_OK;
 }
 

@@ -83,16 +83,21 @@ struct fdog_solver {
   PeerArgs peer_args{};
   bool stream_mode = false;  // forward/backward passes use sweep_stream_kernel
   int rw = 1;                // most rows per lane of any tile (sweep_kernel instantiation)
+  int32_t tmem_cols = 0;     // TMEM columns per sweep CTA (recompute design, fp32; Plan::tmem_cols)
+  bool lifted = false;       // lifted two-sided storage: d_lambda = lambda^{j,1}
+  void *d_lam0 = nullptr;    // lambda^{j,0} per device slot
+  void *d_avg0 = nullptr;    // 0-side averages per device slot
+  void *d_lam_out = nullptr; // lambda^1 - lambda^0 (getter scratch)
   int32_t coop_bw = 0;       // cooperative tiles: relaxation buffer entries
   bool coop_smem = false;
   int64_t n_coop = 0;
   bool chunk_mode = false;   // ... or sweep_chunk_kernel (every tile an arc-mask tile)
   bool rc = false;           // recompute design (Plan::rc): no distance traffic, no dist_state
   bool dbar_zero = true;     // delta_bar == 0 (fresh, finalized, set_state with 0, or after a _seq pass)
-  int32_t ell_v = 4;         // averaging: ELL variables per thread (experiment knob FDOG_AVG_V)
-  int32_t ell_local = 0;     // averaging: consecutive variables per thread (experiment knob FDOG_AVG_LOCAL)
-  int32_t csr_first = 1;     // averaging: CSR section in the first blocks (experiment knob FDOG_AVG_CSR_FIRST)
-  bool get_direct = true;    // getters: widen to fp64 on the device, one D2H (FDOG_GET_DIRECT=0: host widening)
+  int32_t ell_v = 4;         // averaging: ELL variables per thread (measured best of 1, 2, 4, 8)
+  int32_t ell_local = 0;     // averaging: a thread's ELL variables strided by the thread count (consecutive: slower)
+  int32_t csr_first = 1;     // averaging: CSR section in the first blocks (its chains are the longest)
+  bool get_direct = true;    // getters: widen to fp64 on the device, one D2H (host widening measured slower)
   // non-deferred variant (fdog_pass_seq): level schedule, built on first use
   bool seq_ready = false;
   std::vector<int64_t> seq_lvl[2];        // [backward, forward]: level boundaries in pass order
@@ -103,8 +108,8 @@ struct fdog_solver {
   int32_t static_sched = 0;  // TMA sweep: round-robin tiles only
   int32_t pdl_early = 0;     // sweep warps release the averaging grid when their tiles are done
   int32_t claim_batch = 1;   // dynamic schedule: tiles per atomic claim
-  int32_t snake = 1;         // static rounds alternate direction (FDOG_SNAKE=0: all ascending)
-  int32_t spread = 0;        // FDOG_SPREAD=1: static tiles over CTAs first (measured: no gain, QAP50 +3 %)
+  int32_t snake = 1;         // static rounds alternate direction
+  int32_t spread = 0;        // static tiles over CTAs first (measured: no gain, QAP50 +3 %; off)
 
   // host copies needed by getters
   // host-side data shared with the plan (no copy; kept alive by the solver)
@@ -309,6 +314,9 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.scratch_stride = s->scratch_stride;
   a.coop_bw = s->coop_bw;
   a.coop_smem = s->coop_smem ? 1 : 0;
+  a.tmem_cols = s->tmem_cols;
+  a.lambda0 = s->lifted ? s->d_lam0 : nullptr;
+  a.avg0 = s->lifted ? s->d_avg0 : nullptr;
   return a;
 }
 
@@ -376,7 +384,7 @@ fdog_status run_avg(fdog_solver *s) {
   int e;
   {
     Timed t(s, kKAvg);
-    e = launch_avg(s->precision, a, s->stream);
+    e = s->lifted ? launch_avg_lifted(s->precision, a, s->d_avg0, s->stream) : launch_avg(s->precision, a, s->stream);
   }
   if (e) return cuda_fail((cudaError_t)e, "avg launch");
   if (s->peer) {  // publish this rank's partials (the peers read them in their run_peer_exchange)
@@ -713,6 +721,12 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->tsz = s->precision == 64 ? 8 : 4;
   s->device = o->device;
   s->record_mm = o->record_mm != 0;
+  s->lifted = o->lifted != 0;
+  if (s->lifted != P.lifted) {
+    set_error("the plan was packed %s the lifted representation; create the plan with the same option",
+              P.lifted ? "for" : "without");
+    return FDOG_EINVAL;
+  }
   s->profile = o->profile != 0;
   {
     const char *g = getenv("FDOG_GRAPHS");  // experiment knob: FDOG_GRAPHS=0 disables graph replay
@@ -765,10 +779,6 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->DB = P.DB;
   s->NB = P.NB;
   s->rc = P.rc;
-  if (const char *av = getenv("FDOG_AVG_V")) s->ell_v = atoi(av);
-  if (const char *al = getenv("FDOG_AVG_LOCAL")) s->ell_local = atoi(al) ? 1 : 0;
-  if (const char *cf = getenv("FDOG_AVG_CSR_FIRST")) s->csr_first = atoi(cf) ? 1 : 0;
-  if (const char *gd = getenv("FDOG_GET_DIRECT")) s->get_direct = gd[0] == '1';
   s->warp_bytes = (size_t)warp_bytes(P.SB, P.DB, P.NB);
   for (const auto &d : tiles) s->rw = std::max(s->rw, d.lanes / 32);
   s->n_direct = P.direct_tiles;
@@ -804,17 +814,31 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
       return FDOG_EINVAL;
     }
   }
+  if (s->lifted) {  // every tile through sweep_kernel's lane-serial / node-parallel paths (the lifted arc costs)
+    s->stream_mode = s->chunk_mode = s->use_fused = false;
+  }
   if (s->rw > 1 && (s->stream_mode || s->chunk_mode || s->use_fused)) {  // (plan.cpp never packs them so)
     set_error("tiles of %d rows need the staged sweep kernel", 32 * s->rw);
     return FDOG_EINVAL;
   }
   // tile-closed pairs are averaged by sweep_kernel only (the streaming,
   // chunked and fused paths read every average from the averaging kernel)
-  s->pairs = P.n_ell_open < (int64_t)(P.ell.size() / 2) && !s->stream_mode && !s->chunk_mode && !s->use_fused &&
+  s->pairs = !s->lifted && P.n_ell_open < (int64_t)(P.ell.size() / 2) && !s->stream_mode && !s->chunk_mode && !s->use_fused &&
              P.direct_tiles == 0;
   const char *wpb = getenv("FDOG_WPB");  // experiment knob: warps per sweep CTA (default 4, max 16)
   const size_t wmax = wpb ? std::max(1, std::min(16, atoi(wpb))) : 4;
   int warps = (int)std::max<size_t>(1, std::min<size_t>(wmax, (size_t)prop.smem_block / s->warp_bytes));
+  s->tmem_cols = P.tmem_cols;
+  if (s->tmem_cols > 0) {
+    // TMEM variant (kernels.cu sweep_kernel<..., TM>): one CTA per SM (a kernel
+    // with tcgen05 code runs one CTA per SM), warps in groups of four sharing
+    // the 128 TMEM lanes, each group tmem_cols of the 512 columns
+    const int by_tmem = 4 * (512 / s->tmem_cols);
+    const int by_smem = (int)((size_t)prop.smem_block / s->warp_bytes);
+    warps = std::min({16, by_tmem, by_smem});
+    if (warps >= 4) warps &= ~3;
+    s->rw = 0;
+  }
   s->block = warps * 32;
   s->smem = (size_t)warps * s->warp_bytes;
   int bps = 1;
@@ -846,13 +870,10 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     // single counter is not a serialisation point (measured: MRF, 68 tiles per
     // warp, sweeps 282 -> 219 us with 2-4 tiles per claim, 8: 226, 16: 235;
     // CellTrack, 9.5 per warp, 39.5 -> 38.8 us with 2)
-    if (const char *sn = getenv("FDOG_SNAKE")) s->snake = atoi(sn) ? 1 : 0;  // experiment knob
-    if (const char *sp = getenv("FDOG_SPREAD")) s->spread = atoi(sp) ? 1 : 0;  // experiment knob
     const char *cb = getenv("FDOG_CLAIM");  // experiment knob: tiles per claim
     const int64_t tpw = s->n_tiles / std::max<int64_t>(warps_total, 1);
     s->claim_batch = cb ? std::max(1, atoi(cb)) : (tpw >= 32 ? 4 : tpw >= 8 ? 2 : 1);
-    const char *pe = getenv("FDOG_PDL_EARLY");  // experiment knob: 0 / 1
-    s->pdl_early = pe ? (atoi(pe) ? 1 : 0) : (!s->rc && s->n_tiles < 8 * warps_total ? 1 : 0);
+    s->pdl_early = !s->rc && s->n_tiles < 8 * warps_total ? 1 : 0;
     // (A balanced static grid -- every warp exactly ceil(tiles / warps) tiles --
     // was measured on QAP50: 6 % slower.  Warps' finish times spread over 2x
     // either way: a grid that is not a multiple of the SM count leaves SMs
@@ -902,6 +923,9 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   const size_t o_und = carve(sizeof(unsigned long long));
   const size_t o_canon = carve((size_t)std::max<size_t>(P.canon_slot.size(), 1) * 8);  // (fp64 when widened)
   const size_t o_dist = carve((size_t)std::max<int64_t>(P.n_dist, 1) * s->tsz);
+  // lifted representation: lambda^{j,0} (0 initially), its averages, getter scratch
+  const size_t o_l0 = s->lifted ? carve(slot_bytes) : 0, o_a0 = s->lifted ? carve(slot_bytes) : 0;
+  const size_t o_lo = s->lifted ? carve(slot_bytes) : 0;
   unsigned char *base = nullptr;
   CK(cudaMalloc((void **)&base, im.bytes + rt), "cudaMalloc");
   s->allocs.push_back(base);
@@ -944,6 +968,11 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_x = (uint8_t *)(r + o_x);
   s->d_undecided = (unsigned long long *)(r + o_und);
   s->d_canon_out = r + o_canon;
+  if (s->lifted) {
+    s->d_lam0 = r + o_l0;
+    s->d_avg0 = r + o_a0;
+    s->d_lam_out = r + o_lo;
+  }
   if (const char *tr = getenv("FDOG_TRACE"); tr && tr[0] == '1') {
     void *p = nullptr;
     CK(cudaMalloc(&p, (size_t)s->grid * (s->block / 32) * 4 * 8), "cudaMalloc (trace)");
@@ -1021,6 +1050,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->st.tile_pairs = s->pairs ? (int64_t)s->n_ell - s->n_ell_open : 0;
   s->st.interior_tiles = s->n_int;
   s->st.coop_tiles = s->n_coop;
+  s->st.tmem_cols = s->tmem_cols;
 
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;
@@ -1117,6 +1147,10 @@ fdog_status fdog_primal_step(fdog_solver *s, int32_t round, double delta, uint64
     set_error("bad argument");
     return FDOG_EINVAL;
   }
+  if (s->lifted) {
+    set_error("primal rounding reads single-sided state; not in the lifted representation");
+    return FDOG_ESTATE;
+  }
   if (s->world > 1) {
     set_error("primal rounding is single-GPU in this version");
     return FDOG_ESTATE;
@@ -1133,6 +1167,10 @@ fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, u
   if (!s || !x || !rounds || !objective || len < s->n_vars) {
     set_error("bad argument");
     return FDOG_EINVAL;
+  }
+  if (s->lifted) {
+    set_error("primal rounding reads single-sided state; not in the lifted representation");
+    return FDOG_ESTATE;
   }
   fdog_primal_options def;
   fdog_default_primal_options(&def);
@@ -1287,6 +1325,10 @@ fdog_status fdog_pass_seq(fdog_solver *s, int32_t forward, double omega) {
   if (!s) {
     set_error("null solver");
     return FDOG_EINVAL;
+  }
+  if (s->lifted) {
+    set_error("the non-deferred variant is single-sided; not in the lifted representation");
+    return FDOG_ESTATE;
   }
   if (!(omega > 0.0 && omega <= 1.0)) {
     set_error("omega %g outside (0, 1]", omega);
@@ -1648,7 +1690,9 @@ fdog_status fdog_finalize(fdog_solver *s) {
   int e;
   {
     Timed t(s, kKAddDeferred);
-    e = launch_add_deferred(s->precision, s->n_dev_slots, s->d_lambda, s->d_delta[s->cur], s->stream);
+    e = s->lifted ? launch_add_deferred_lifted(s->precision, s->n_dev_slots, s->d_lambda, s->d_lam0,
+                                               s->d_delta[s->cur], s->stream)
+                  : launch_add_deferred(s->precision, s->n_dev_slots, s->d_lambda, s->d_delta[s->cur], s->stream);
   }
   if (e) return cuda_fail((cudaError_t)e, "add_deferred");
   s->dbar_zero = true;
@@ -1659,6 +1703,10 @@ fdog_status fdog_finalize_averaged(fdog_solver *s) {
   if (!s) {
     set_error("null solver");
     return FDOG_EINVAL;
+  }
+  if (s->lifted) {
+    set_error("the averaged final correction is not defined for the lifted representation");
+    return FDOG_ESTATE;
   }
   if (s->external && !s->peer) {
     set_error("fdog_finalize_averaged needs world == 1, the NCCL or the peer-memory exchange");
@@ -1706,7 +1754,26 @@ fdog_status fdog_get_lambda(fdog_solver *s, double *out, int64_t len) {
     set_error("null solver");
     return FDOG_EINVAL;
   }
+  if (s->lifted) {  // the original-space lambda = lambda^1 - lambda^0
+    const int e = launch_lifted_diff(s->precision, s->n_dev_slots, s->d_lambda, s->d_lam0, s->d_lam_out, s->stream);
+    if (e) return cuda_fail((cudaError_t)e, "lifted diff");
+    s->launches++;
+    return fetch_slots(s, s->d_lam_out, out, len);
+  }
   return fetch_slots(s, s->d_lambda, out, len);
+}
+
+fdog_status fdog_get_lifted(fdog_solver *s, double *lam0, double *lam1, int64_t len) {
+  if (!s) {
+    set_error("null solver");
+    return FDOG_EINVAL;
+  }
+  if (!s->lifted) {
+    set_error("fdog_get_lifted needs the lifted representation (fdog_options::lifted)");
+    return FDOG_ESTATE;
+  }
+  fdog_status st = fetch_slots(s, s->d_lam0, lam0, len);
+  return st ? st : fetch_slots(s, s->d_lambda, lam1, len);
 }
 
 fdog_status fdog_get_deferred(fdog_solver *s, double *out, int64_t len) {
@@ -1734,6 +1801,10 @@ fdog_status fdog_set_state(fdog_solver *s, const double *lambda, const double *d
   if (!s) {
     set_error("null solver");
     return FDOG_EINVAL;
+  }
+  if (s->lifted) {
+    set_error("fdog_set_state takes single-sided lambda; not in the lifted representation");
+    return FDOG_ESTATE;
   }
   fdog_status st;
   if (lambda && (st = put_slots(s, s->d_lambda, lambda, len))) return st;

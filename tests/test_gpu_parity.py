@@ -679,3 +679,35 @@ def test_cooperative_unusual_orders_and_finalize(oracle_mod):
     g.finalize(averaged=True)
     o.finalize(averaged=True)
     assert np.max(np.abs(g.lam() - o.lam())) <= 1e-9 * s
+
+
+@pytest.mark.parametrize("name,make", [
+    ("qap", lambda: synth.qap(16, n=12)),
+    ("celltrack", lambda: synth.celltrack(16, frames=8, dets=60)),
+    ("gm", lambda: synth.gm_worms_like(16, n_src=120, k_cand=8, knn=10)),
+])
+def test_tmem_distances_bitwise(monkeypatch, name, make):
+    """Recompute design, fp32: the distance scratch of 32-row tiles in tensor
+    memory (tcgen05.st / tcgen05.ld, kernels.cu TmemD) equals the shared-memory
+    scratch bit for bit (FDOG_TMEM=1 vs 0) -- lambda, delta_bar and the
+    min-marginals pass by pass, then through the graph-replayed iterate."""
+    p = make()
+    monkeypatch.setenv("FDOG_SWEEP", "rc")
+    monkeypatch.setenv("FDOG_FUSED", "0")
+    monkeypatch.setenv("FDOG_TMEM", "1")
+    g1 = F.Solver(p, precision=32, record_mm=True)
+    assert g1.stats()["tmem_cols"] >= 32
+    monkeypatch.setenv("FDOG_TMEM", "0")
+    g0 = F.Solver(p, precision=32, record_mm=True)
+    assert g0.stats()["tmem_cols"] == 0
+    for t in range(4):
+        fwd = t % 2 == 0
+        g0.pass_(fwd, 0.5)
+        g1.pass_(fwd, 0.5)
+        assert np.array_equal(g0.lam(), g1.lam()) and np.array_equal(g0.deferred(), g1.deferred()), f"pass {t}"
+        for a, b in zip(g0.min_marginals(), g1.min_marginals()):
+            assert np.array_equal(a, b)
+        assert _same_bound(g0, g1)
+    g0.iterate(5, 0.5)
+    g1.iterate(5, 0.5)
+    assert np.array_equal(g0.lam(), g1.lam()) and _same_bound(g0, g1)

@@ -322,3 +322,18 @@ def test_plan_deterministic_across_threads(name, make):
     d = {t: F.Plan(p, precision=32, host_threads=t).digest() for t in (1, 3, 8)}
     assert d[1] == d[3] == d[8]
     assert F.Plan(p, precision=64, host_threads=1).digest() == F.Plan(p, precision=64, host_threads=8).digest()
+
+
+def test_lifted_plan_layout():
+    """Lifted plans (fdog_options::lifted, P:32-57): every tile unstaged (the
+    sweeps read both arc costs from global memory), no arc-mask records, no
+    rows-per-lane or tile-closed pairs, no recompute design; world 1 only."""
+    p = synth.mrf_potts(2, H=12, W=12, L=4)
+    pl = F.Plan(p, lifted=True)
+    t = pl.tiles()
+    st = pl.stats()
+    assert np.all((t[:, 0] & (2 | 4)) == 0) and t[:, 2].max() <= 32
+    assert st["staged_tiles"] == 0 and st["tile_pairs"] == 0 and st["sweep_recompute"] == 0
+    with pytest.raises(F.FastdogError) as e:
+        F.Plan(p, world=2, lifted=True)
+    assert e.value.code == 1
