@@ -20,6 +20,7 @@ constexpr int kLanes = 32;  // BDDs per warp tile (one BDD per lane)
 // (tile kind bit 5, kernels.cu process_bdd_coop).
 constexpr int kCoopWidth = 32;
 constexpr int kMaxTileRows = 128;  // rows of the widest tile (4 per lane)
+constexpr int kMaxElld = 8;        // ELL-D degree groups of the averaging layout
 
 // A distinct compiled BDD topology (many rows share one: same coefficients,
 // relation and right-hand side).
@@ -136,7 +137,8 @@ FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (kWarpHeader + NB * SB +
 // creating a solver is one allocation and one host->device copy.
 enum ImageSection {
   kImTiles = 0, kImHopOff, kImTopo, kImSlotVar, kImVarPtr, kImVarSlots, kImVarXidx, kImDegList, kImEll, kImEllVar,
-  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImRecs, kImCanon, kImPairs, kImCount
+  kImCsrVar, kImXLocal, kImXDeg, kImLambda0, kImDist0, kImEll4, kImEll4Var, kImRecs, kImCanon, kImPairs, kImElld,
+  kImElldVar, kImCount
 };
 
 struct HostImage {
@@ -184,6 +186,13 @@ struct Plan {
   std::vector<uint32_t> pair_list;  // per tile with closed pairs (TileDesc::pair_base, n_pairs)
   std::vector<int32_t> ell4;        // ELL-4 part (|J_i| = 3, 4): slot quads, -1 padded
   std::vector<int32_t> ell4_var;
+  // ELL-D part: frequent degrees d in [5, 32] (not exchanged), one group per d,
+  // slot k of variable v at elld[elld_off[g] + k * elld_n[g] + v] (column-major:
+  // a warp's index loads are coalesced; k ascending = j ascending, A1)
+  std::vector<int32_t> elld;
+  std::vector<int32_t> elld_var;    // the variables, group by group
+  std::vector<int32_t> elld_d, elld_n;
+  std::vector<int64_t> elld_off;
   std::vector<int32_t> col_coef;    // copy of the rows (feasibility checks of primal labelings)
   std::vector<int8_t> rel;
   std::vector<int64_t> rhs;
@@ -270,6 +279,10 @@ struct AvgArgs {
   const int2 *ell;           // their slot pairs (y = -1 if |J_i| = 1)
   int32_t n_ell4;            // variables in the ELL-4 part (|J_i| = 3, 4, not exchanged)
   const int4 *ell4;          // their slot quads (-1 padded)
+  int32_t n_elld_g;          // ELL-D groups (<= kMaxElld)
+  int32_t elld_d[8], elld_n[8];  // degree and variables of group g
+  int64_t elld_off[8];       // first entry of group g in elld
+  const int32_t *elld;       // column-major slot indices of the ELL-D part
   int32_t n;                 // variables in the CSR part
   int32_t group;             // lanes per CSR variable (power of two <= 32)
   const int64_t *var_ptr;    // CSR over the CSR part
@@ -298,6 +311,10 @@ struct PeerArgs {
 
 struct PrimalArgs {
   int32_t n_ell, n_ell4, n_csr;
+  int32_t n_elld_g;           // ELL-D groups (AvgArgs), after the CSR entries
+  int32_t elld_d[8], elld_n[8];
+  int64_t elld_off[8];
+  const int32_t *elld, *elld_var;
   const int2 *ell;
   const int32_t *ell_var;     // variable of each ELL entry
   const int4 *ell4;

@@ -2198,6 +2198,51 @@ __host__ __device__ __forceinline__ int64_t avg_csr_threads(const AvgArgs &a) {
   return ((int64_t)a.n * a.group + 31) & ~(int64_t)31;
 }
 
+// threads of the ELL-D part: one per variable, each group in whole warps
+__host__ __device__ __forceinline__ int64_t avg_elld_threads(const AvgArgs &a) {
+  int64_t t = 0;
+  for (int g = 0; g < a.n_elld_g; ++g) t += ((int64_t)a.elld_n[g] + 31) & ~(int64_t)31;
+  return t;
+}
+
+// ELL-D part: variable v of group g (degree d) sums its d slots in ascending j
+// (k ascending), eight index loads and eight gathers in flight at a time, then
+// writes the average into every slot.  Column-major indices: the k-th index
+// loads of a warp are coalesced, and so are its gathers and scatters wherever
+// neighbouring variables have neighbouring k-th slots (MRF pixels, Potts edges).
+template <typename T, bool NC, bool PRE>
+__device__ __forceinline__ void avg_elld(const AvgArgs &a, int64_t t) {
+  int g = 0;
+  int64_t base = 0;
+  for (; g < a.n_elld_g; ++g) {
+    const int64_t w = ((int64_t)a.elld_n[g] + 31) & ~(int64_t)31;
+    if (t < base + w) break;
+    base += w;
+  }
+  if (g >= a.n_elld_g) return;
+  const int64_t v = t - base;
+  const int n = a.elld_n[g], d = a.elld_d[g];
+  if (PRE) pdl_wait();
+  if (v >= n) return;
+  const int32_t *ix = a.elld + a.elld_off[g] + v;
+  const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
+  T *__restrict__ out = reinterpret_cast<T *>(a.avg_slot);
+  T s = T(0);
+  for (int k0 = 0; k0 < d; k0 += 8) {
+    int32_t q[8];
+    T x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = k0 + u < d ? __ldg(ix + (int64_t)(k0 + u) * n) : -1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = q[u] >= 0 ? ld<NC>(db + q[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (q[u] >= 0) s += x[u];
+  }
+  const T avg = s / T(d);
+  for (int k = 0; k < d; ++k) out[__ldg(ix + (int64_t)k * n)] = avg;
+}
+
 // PRE: the standalone kernel launched behind a sweep (PDL): the constant index
 // loads of a thread are issued before griddepcontrol.wait, the gathers of
 // delta_bar after it
@@ -2272,8 +2317,13 @@ __device__ __forceinline__ void avg_body(const AvgArgs &a, int tid) {
     }
     return;
   }
+  const int64_t n_elld_thr = avg_elld_threads(a);
+  if (tid < n_ell_thr + n_ell4_thr + n_elld_thr) {
+    avg_elld<T, NC, PRE>(a, tid - n_ell_thr - n_ell4_thr);
+    return;
+  }
   if (a.csr_first) return;  // (past the last section: padding threads)
-  avg_csr<T, NC, PRE>(a, tid - n_ell_thr - n_ell4_thr);
+  avg_csr<T, NC, PRE>(a, tid - n_ell_thr - n_ell4_thr - (int)n_elld_thr);
 }
 
 template <typename T>
@@ -2293,7 +2343,7 @@ __global__ void __launch_bounds__(256) avg_kernel(const AvgArgs a) {
 __host__ __device__ __forceinline__ int64_t avg_threads(const AvgArgs &a) {
   const int v = (a.ell_v == 8 || a.ell_v == 2 || a.ell_v == 1) ? a.ell_v : 4;
   return (int64_t)((((a.n_ell + v - 1) / v) + 31) & ~31) + (int64_t)((((a.n_ell4 + 1) >> 1) + 31) & ~31) +
-         avg_csr_threads(a);
+         avg_elld_threads(a) + avg_csr_threads(a);
 }
 
 // ---------------------------------------------------------------------------
@@ -2395,11 +2445,15 @@ __device__ __forceinline__ double primal_uniform(uint64_t seed, int64_t round, i
 template <typename T>
 __global__ void __launch_bounds__(256) primal_kernel(const PrimalArgs a) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= a.n_ell + a.n_ell4 + a.n_csr) return;
+  int n_elld = 0;
+  for (int g = 0; g < a.n_elld_g; ++g) n_elld += a.elld_n[g];
+  if (q >= a.n_ell + a.n_ell4 + a.n_csr + n_elld) return;
   const T *__restrict__ db = reinterpret_cast<const T *>(a.delta_bar);
   int i, sl[4] = {-1, -1, -1, -1};
   int64_t p0 = 0, p1 = 0, deg;
-  const int kind = q < a.n_ell ? 0 : q < a.n_ell + a.n_ell4 ? 1 : 2;
+  const int kind = q < a.n_ell ? 0 : q < a.n_ell + a.n_ell4 ? 1 : q < a.n_ell + a.n_ell4 + a.n_csr ? 2 : 3;
+  const int32_t *ed = nullptr;  // ELL-D: slot k at ed[k * en]
+  int64_t en = 0;
   if (kind == 0) {
     const int2 pr = a.ell[q];
     i = a.ell_var[q];
@@ -2414,14 +2468,21 @@ __global__ void __launch_bounds__(256) primal_kernel(const PrimalArgs a) {
     sl[2] = pr.z;
     sl[3] = pr.w;
     deg = pr.w >= 0 ? 4 : 3;
-  } else {
+  } else if (kind == 2) {
     const int c = q - a.n_ell - a.n_ell4;
     i = a.csr_var[c];
     p0 = a.var_ptr[c];
     p1 = a.var_ptr[c + 1];
     deg = p1 - p0;
+  } else {
+    int v = q - a.n_ell - a.n_ell4 - a.n_csr, g = 0;
+    i = a.elld_var[v];
+    while (v >= a.elld_n[g]) v -= a.elld_n[g++];
+    ed = a.elld + a.elld_off[g] + v;
+    en = a.elld_n[g];
+    deg = a.elld_d[g];
   }
-  auto slot_at = [&](int64_t u) -> int { return kind < 2 ? sl[u] : a.var_slots[p0 + u]; };
+  auto slot_at = [&](int64_t u) -> int { return kind < 2 ? sl[u] : kind == 2 ? a.var_slots[p0 + u] : ed[u * en]; };
   bool pos = true, neg = true, zero = true;
   double dsum = 0.0;  // sign of d_i = sum_j (m1 - m0) = sign of sum_j delta_bar (omega > 0)
   for (int64_t u = 0; u < deg; ++u) {
@@ -3015,7 +3076,8 @@ int launch_lb_deferred(int precision, const TileDesc *tiles, int32_t n_tiles, co
 }
 
 int launch_primal(int precision, const PrimalArgs &a, void *stream) {
-  const int n = a.n_ell + a.n_ell4 + a.n_csr;
+  int n = a.n_ell + a.n_ell4 + a.n_csr;
+  for (int g = 0; g < a.n_elld_g; ++g) n += a.elld_n[g];
   if (n <= 0) return 0;
   const int block = 256, grid = (n + block - 1) / block;
   if (precision == 64)

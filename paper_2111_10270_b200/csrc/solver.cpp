@@ -132,6 +132,10 @@ struct fdog_solver {
   int32_t *d_var_slots = nullptr, *d_var_xidx = nullptr, *d_deg_list = nullptr;
   int2 *d_ell = nullptr;
   int4 *d_ell4 = nullptr;
+  const int32_t *d_elld = nullptr;  // ELL-D part of the averaging (Plan::elld)
+  const int32_t *d_elld_var = nullptr;
+  int32_t n_elld_g = 0, elld_d[kMaxElld] = {0}, elld_n[kMaxElld] = {0};
+  int64_t elld_off[kMaxElld] = {0};
   int32_t *d_ell4_var = nullptr;
   int32_t n_ell = 0, n_ell4 = 0, csr_group = 1;
   // tile-closed pairs (Plan::n_ell_open): the sweep averages them
@@ -360,6 +364,13 @@ AvgArgs avg_args(fdog_solver *s) {
   a.ell = s->d_ell;
   a.n_ell4 = s->n_ell4;
   a.ell4 = s->d_ell4;
+  a.n_elld_g = s->n_elld_g;
+  for (int g = 0; g < s->n_elld_g; ++g) {
+    a.elld_d[g] = s->elld_d[g];
+    a.elld_n[g] = s->elld_n[g];
+    a.elld_off[g] = s->elld_off[g];
+  }
+  a.elld = s->d_elld;
   a.tile_counter = s->d_counter + 1;
   a.ell_v = s->ell_v;
   a.ell_local = s->ell_local;
@@ -891,6 +902,12 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->n_ell = (int32_t)(P.ell.size() / 2);
   s->n_ell_open = (int32_t)P.n_ell_open;
   s->n_ell4 = (int32_t)(P.ell4.size() / 4);
+  s->n_elld_g = (int32_t)P.elld_d.size();
+  for (int g = 0; g < s->n_elld_g; ++g) {
+    s->elld_d[g] = P.elld_d[g];
+    s->elld_n[g] = P.elld_n[g];
+    s->elld_off[g] = P.elld_off[g];
+  }
   {
     int64_t maxdeg = 1;
     for (size_t q = 0; q + 1 < P.var_ptr.size(); ++q) maxdeg = std::max<int64_t>(maxdeg, P.var_ptr[q + 1] - P.var_ptr[q]);
@@ -947,6 +964,8 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->d_ell = (int2 *)sec(kImEll);
   s->d_ell_var = (int32_t *)sec(kImEllVar);
   s->d_ell4 = (int4 *)sec(kImEll4);
+  s->d_elld = (const int32_t *)sec(kImElld);
+  s->d_elld_var = (const int32_t *)sec(kImElldVar);
   s->d_ell4_var = (int32_t *)sec(kImEll4Var);
   s->d_csr_var = (int32_t *)sec(kImCsrVar);
   s->d_x_local = (int32_t *)sec(kImXLocal);
@@ -1074,6 +1093,14 @@ PrimalArgs primal_args(fdog_solver *s, int mode, int32_t round, double delta, ui
   a.csr_var = s->d_csr_var;
   a.var_ptr = s->d_var_ptr;
   a.var_slots = s->d_var_slots;
+  a.n_elld_g = s->n_elld_g;
+  for (int g = 0; g < s->n_elld_g; ++g) {
+    a.elld_d[g] = s->elld_d[g];
+    a.elld_n[g] = s->elld_n[g];
+    a.elld_off[g] = s->elld_off[g];
+  }
+  a.elld = s->d_elld;
+  a.elld_var = s->d_elld_var;
   a.delta_bar = s->d_delta[s->cur];
   a.lambda = s->d_lambda;
   a.x = s->d_x;

@@ -3,8 +3,8 @@
 usage: python scripts/summarize_ncu.py TAG [bench.json]
   reads gpurun_out/launches_TAG.csv (launch list, gpu__time_duration) and
   gpurun_out/prof_TAG.ncu-rep (--set full capture); writes
-  profiles/TAG_launches.csv, profiles/TAG_ncu_summary.md and updates
-  profiles/sweep_traffic.json (dram bytes per sweep launch, for bench.py).
+  profiles/TAG_launches.csv and profiles/TAG_ncu_summary.md.  (bench.py
+  measures roofline.traffic itself, with an ncu subprocess of the same run.)
 """
 import csv
 import io
@@ -93,11 +93,4 @@ if len(sys.argv) > 2 and os.path.exists(sys.argv[2]):
 lines.insert(0, f"# ncu summary, {tag}\n")
 with open(os.path.join(out, f"{tag}_ncu_summary.md"), "w") as f:
     f.write("\n".join(lines) + "\n")
-if traffic:
-    tp = os.path.join(out, "sweep_traffic.json")
-    cur = json.load(open(tp)) if os.path.exists(tp) else {}
-    allv = [v for vs in traffic.values() for v in vs]
-    cur["gm_worms_like(seed=0,n=500,K=10,knn=30)/fp32"] = sum(allv) / len(allv)
-    cur["_note"] = f"dram__bytes_read.sum + dram__bytes_write.sum per sweep launch, ncu --set full, round tag {tag}"
-    json.dump(cur, open(tp, "w"), indent=1)
 print("\n".join(lines))

@@ -711,3 +711,31 @@ def test_tmem_distances_bitwise(monkeypatch, name, make):
     g0.iterate(5, 0.5)
     g1.iterate(5, 0.5)
     assert np.array_equal(g0.lam(), g1.lam()) and _same_bound(g0, g1)
+
+
+@pytest.mark.parametrize("name,make", [
+    ("mrf", lambda: synth.mrf_potts(17, H=12, W=14, L=4)),
+    ("mrf_cut", lambda: synth.mrf_potts_cut(17, H=12, W=14, L=4)),
+    ("gm", lambda: synth.gm_worms_like(17, n_src=80, k_cand=6, knn=8)),
+])
+def test_elld_averaging(oracle_mod, monkeypatch, name, make):
+    """Averaging of frequent degrees 5..32 in column-major ELL-D groups (one
+    thread per variable, slots summed in ascending j -- the oracle's order, A1):
+    fp64 pass by pass against the oracle at 1e-9 (lambda, delta_bar,
+    min-marginals, bound), then the primal rounding (its classify / perturb
+    kernel walks the same groups): a feasible labeling, objective >= LB."""
+    monkeypatch.setenv("FDOG_ELLD_MIN", "1")
+    monkeypatch.setenv("FDOG_FUSED", "0")
+    p = make()
+    g, o = _compare_pass_by_pass(p, oracle_mod, passes=4)
+    lb = g.lower_bound()
+    try:
+        x, rounds, obj = g.round_primal(max_rounds=100)
+    except F.FastdogError as e:  # no consensus within max_rounds (allowed by Alg. 2)
+        assert e.code == 8
+        return
+    for j in range(p.n_cons):
+        v, c, rel, rhs = p.row(j)
+        s = int(np.dot(c, x[v]))
+        assert (s <= rhs) if rel < 0 else (s >= rhs) if rel > 0 else (s == rhs)
+    assert obj >= lb - 1e-6 * (1 + abs(lb))
