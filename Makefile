@@ -7,13 +7,26 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v -Iin
 
 all: $(PKG)/libfastdog.so oracle/liboracle.so
 
-$(PKG)/libfastdog.so: $(SRC) $(PKG)/csrc/internal.h include/fastdog.h
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -ldl 2> build_ptxas.log || (cat build_ptxas.log; false)
+OBJ := $(patsubst $(PKG)/csrc/%,build/obj/%.o,$(SRC))
+
+# (make -j: the four sources compile concurrently; kernels.cu also splits its
+# device code over the cores)
+build/obj/%.cu.o: $(PKG)/csrc/%.cu $(PKG)/csrc/internal.h include/fastdog.h
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) --split-compile=0 -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+
+build/obj/%.cpp.o: $(PKG)/csrc/%.cpp $(PKG)/csrc/internal.h include/fastdog.h
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(PKG)/libfastdog.so: $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -ldl
+	@cat build/obj/*.ptxas.log > build_ptxas.log 2>/dev/null || true
 
 oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
 	gcc -O2 -std=c11 -fopenmp -fPIC -shared -Wall -o $@ oracle/oracle.c -lm
 
 clean:
-	rm -f $(PKG)/libfastdog.so oracle/liboracle.so build_ptxas.log
+	rm -rf $(PKG)/libfastdog.so oracle/liboracle.so build_ptxas.log build/obj
 
 .PHONY: all clean

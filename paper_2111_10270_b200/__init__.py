@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfastdog.so")
+# (FDOG_LIB: another build of the same library, for same-box A/B runs)
+LIB_PATH = os.environ.get("FDOG_LIB") or os.path.join(_HERE, "libfastdog.so")
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "EINFEASIBLE", 3: "ENOMEM", 4: "ECUDA", 5: "ENCCL", 6: "ESTATE",
           7: "ETOOBIG", 8: "ENOSOLUTION"}

@@ -2836,7 +2836,8 @@ template <typename T, bool RC>
 static const void *sweep_fn(int mode, bool rec, int rw) {
   if constexpr (RC && std::is_same<T, float>::value)
     if (rw == 0) return sweep_fn_rw<T, true, 1, true>(mode, rec);
-  if (rw >= 4 && sizeof(T) == 4) return sweep_fn_rw<T, RC, 4>(mode, rec);  // (fp64 plans stop at 2 rows per lane)
+  if constexpr (sizeof(T) == 4)  // (fp64 plans stop at 2 rows per lane)
+    if (rw >= 4) return sweep_fn_rw<T, RC, 4>(mode, rec);
   if (rw >= 2) return sweep_fn_rw<T, RC, 2>(mode, rec);
   return sweep_fn_rw<T, RC, 1>(mode, rec);
 }

@@ -2,7 +2,8 @@
 (fp32, the design the plan picks, CUDA-graph replay for iterate), for the
 workloads besides GM (GM: test_gpu_parity.py::test_full_size_gm_*).
 
-- CellTrack (configs[3], 9.7 M nodes) and QAP n=50 (configs[4], 12.1 M nodes):
+- CellTrack (configs[3], 9.7 M nodes), QAP n=50 (configs[4], 12.1 M nodes) and
+  the MRF Potts-cut variant (40.0 M nodes; rows per lane, ELL-D averaging):
   every slot of lambda after one iteration against the oracle (fp64), the
   bound after 100 iterations (north_star's fp32 claim); fp64 builds every slot
   at 1e-9 for two iterations.
@@ -37,10 +38,12 @@ def _err(a, b, rtol, s):
     return float(np.max(np.abs(a - b) - rtol * np.abs(b), initial=-1.0)) - rtol * s
 
 
-@pytest.fixture(scope="module", params=["celltrack", "qap50"])
+@pytest.fixture(scope="module", params=["celltrack", "qap50", "mrf_potts_cut"])
 def full_problem(request):
     if request.param == "celltrack":
         return synth.celltrack(0)
+    if request.param == "mrf_potts_cut":  # the Potts-cut variant of the metric's MRF line (40.0 M nodes)
+        return synth.mrf_potts_cut(0)
     return synth.qap(0, 50)
 
 
