@@ -2,7 +2,8 @@
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 PKG := paper_2111_10270_b200
-SRC := $(PKG)/csrc/plan.cpp $(PKG)/csrc/solver.cpp $(PKG)/csrc/kernels.cu $(PKG)/csrc/compile_gpu.cu
+SRC := $(PKG)/csrc/plan.cpp $(PKG)/csrc/solver.cpp $(PKG)/csrc/kernels.cu $(PKG)/csrc/compile_gpu.cu \
+       $(PKG)/csrc/pack_gpu.cu
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v -Iinclude -I$(PKG)/csrc
 
 all: $(PKG)/libfastdog.so oracle/liboracle.so

@@ -230,6 +230,12 @@ struct Plan {
 // FDOG_ETOOBIG when a shape exceeds the GPU scratch bound (compile on the host)
 fdog_status gpu_compile_shapes(std::vector<Shape> &shapes, int device);
 
+// the packer's canonical-slot and variable phases on the GPU (pack_gpu.cu,
+// FDOG_GPU_PACK=1): fills canon_slot / canon_con / canon_pos, var_list,
+// var_ptr, var_slots exactly as the host phases do
+fdog_status gpu_pack_slots(Plan &P, const std::vector<int64_t> &row_slot, const std::vector<int32_t> &row_L,
+                           int device);
+
 // host-side helpers implemented in plan.cpp
 void set_error(const char *fmt, ...);
 fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &plan);

@@ -1208,110 +1208,128 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     return FDOG_ETOOBIG;
   }
   tm.mark("tile emission");
-  // canonical slots and CSR variable -> device slots (j ascending, A1)
-  P.canon_slot.clear();
-  P.canon_con.clear();
-  P.canon_pos.clear();
-  std::vector<int64_t> cnt(p->n_vars + 1, 0);
-  P.canon_slot.resize((size_t)P.n_slots);
-  P.canon_con.resize((size_t)P.n_slots);
-  P.canon_pos.resize((size_t)P.n_slots);
-  {
-    const int64_t nr = (int64_t)P.local_rows.size();
-    std::vector<int64_t> q0(nr + 1, 0);  // first canonical slot of each local row
-    for (int64_t r = 0; r < nr; ++r) {
-      const int32_t j = P.local_rows[r];
-      q0[r + 1] = q0[r] + (P.row_ptr[j + 1] - P.row_ptr[j]);
+  // canonical slots and CSR variable -> device slots (j ascending, A1):
+  // on the GPU with FDOG_GPU_PACK=1 (pack_gpu.cu, identical arrays), else here
+  bool packed_gpu = false;
+  if (const char *gp = getenv("FDOG_GPU_PACK"); gp && gp[0] == '1') {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+      const int dev = o ? o->device : 0;
+      const fdog_status r = gpu_pack_slots(P, row_slot, row_L, dev >= 0 && dev < ndev ? dev : 0);
+      if (r) {
+        set_error("GPU packing failed (%s)", cudaGetErrorString(cudaGetLastError()));
+        return r;
+      }
+      packed_gpu = true;
+    } else {
+      cudaGetLastError();
     }
-    par_for(nr, threads, [&](int, int64_t r0, int64_t r1) {
-      for (int64_t r = r0; r < r1; ++r) {
+  }
+  if (!packed_gpu) {
+    P.canon_slot.clear();
+    P.canon_con.clear();
+    P.canon_pos.clear();
+    std::vector<int64_t> cnt(p->n_vars + 1, 0);
+    P.canon_slot.resize((size_t)P.n_slots);
+    P.canon_con.resize((size_t)P.n_slots);
+    P.canon_pos.resize((size_t)P.n_slots);
+    {
+      const int64_t nr = (int64_t)P.local_rows.size();
+      std::vector<int64_t> q0(nr + 1, 0);  // first canonical slot of each local row
+      for (int64_t r = 0; r < nr; ++r) {
         const int32_t j = P.local_rows[r];
-        const int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
-        const int32_t *vars = P.col_var.data() + P.row_ptr[j];
-        for (int32_t h = 0; h < k; ++h) {
-          const int64_t q = q0[r] + h;
-          P.canon_slot[q] = row_slot[j] + (int64_t)h * row_L[j];
-          P.canon_con[q] = j;
-          P.canon_pos[q] = h;
-          __atomic_fetch_add(&cnt[vars[h]], 1, __ATOMIC_RELAXED);
+        q0[r + 1] = q0[r] + (P.row_ptr[j + 1] - P.row_ptr[j]);
+      }
+      par_for(nr, threads, [&](int, int64_t r0, int64_t r1) {
+        for (int64_t r = r0; r < r1; ++r) {
+          const int32_t j = P.local_rows[r];
+          const int32_t k = (int32_t)(P.row_ptr[j + 1] - P.row_ptr[j]);
+          const int32_t *vars = P.col_var.data() + P.row_ptr[j];
+          for (int32_t h = 0; h < k; ++h) {
+            const int64_t q = q0[r] + h;
+            P.canon_slot[q] = row_slot[j] + (int64_t)h * row_L[j];
+            P.canon_con[q] = j;
+            P.canon_pos[q] = h;
+            __atomic_fetch_add(&cnt[vars[h]], 1, __ATOMIC_RELAXED);
+          }
         }
-      }
-    });
-  }
-  tm.mark("canonical slots + CSR");
-  // variables in the order of their first device slot, so that neighbouring
-  // averaging threads gather and scatter neighbouring slots (the tile layout
-  // puts consecutive rows of a shape in consecutive lanes): each variable's
-  // first device slot (atomic min), then the device slots that are a first
-  // occurrence, compacted in device-slot order -- the order of a sort by first
-  // device slot, without the sort
-  P.var_list.clear();
-  {
-    const int64_t ns = (int64_t)P.slot_var.size();
-    std::vector<int32_t> first(p->n_vars, INT32_MAX);  // (device slots < 2^31, checked above)
-    par_for(ns, threads, [&](int, int64_t a, int64_t b) {
-      for (int64_t d = a; d < b; ++d)
-        if (P.slot_var[d] >= 0) atomic_min32(&first[P.slot_var[d]], (int32_t)d);
-    });
-    const int T = par_chunks(ns, threads);
-    std::vector<int64_t> cc(T + 1, 0);
-    auto is_first = [&](int64_t d) { return P.slot_var[d] >= 0 && first[P.slot_var[d]] == d; };
-    par_for(ns, threads, [&](int c, int64_t a, int64_t b) {
-      int64_t m = 0;
-      for (int64_t d = a; d < b; ++d) m += is_first(d);
-      cc[c + 1] = m;
-    });
-    for (int c = 0; c < T; ++c) cc[c + 1] += cc[c];
-    P.var_list.resize(cc[T]);
-    par_for(ns, threads, [&](int c, int64_t a, int64_t b) {
-      int64_t o = cc[c];
-      for (int64_t d = a; d < b; ++d)
-        if (is_first(d)) P.var_list[o++] = P.slot_var[d];
-    });
-  }
-  // CSR over var_list: prefix of the local degrees
-  std::vector<int64_t> where(p->n_vars, -1);
-  {
-    const int64_t nv = (int64_t)P.var_list.size();
-    const int T = par_chunks(nv, threads);
-    std::vector<int64_t> cs(T + 1, 0);
-    par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
-      int64_t m = 0;
-      for (int64_t k = a; k < b; ++k) m += cnt[P.var_list[k]];
-      cs[c + 1] = m;
-    });
-    for (int c = 0; c < T; ++c) cs[c + 1] += cs[c];
-    P.var_ptr.resize(nv + 1);
-    P.var_ptr[nv] = cs[T];
-    par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
-      int64_t o = cs[c];
-      for (int64_t k = a; k < b; ++k) {
-        P.var_ptr[k] = o;
-        where[P.var_list[k]] = o;
-        o += cnt[P.var_list[k]];
-      }
-    });
-  }
-  // fill: canonical slot indices claimed with an atomic cursor per variable,
-  // then each variable's (short) list sorted -- ascending canonical index is
-  // ascending j (A1) -- and mapped to device slots
-  {
-    const int64_t nq = (int64_t)P.canon_slot.size();
-    std::vector<int32_t> tq((size_t)std::max<int64_t>(nq, 1));
-    par_for(nq, threads, [&](int, int64_t a, int64_t b) {
-      for (int64_t q = a; q < b; ++q) {
-        const int32_t i = P.col_var[P.row_ptr[P.canon_con[q]] + P.canon_pos[q]];
-        tq[__atomic_fetch_add(&where[i], 1, __ATOMIC_RELAXED)] = (int32_t)q;
-      }
-    });
-    P.var_slots.assign(P.var_ptr.back(), -1);
-    par_for((int64_t)P.var_list.size(), threads, [&](int, int64_t a, int64_t b) {
-      for (int64_t k = a; k < b; ++k) {
-        const int64_t p0 = P.var_ptr[k], p1 = P.var_ptr[k + 1];
-        std::sort(tq.begin() + p0, tq.begin() + p1);
-        for (int64_t x = p0; x < p1; ++x) P.var_slots[x] = (int32_t)P.canon_slot[tq[x]];
-      }
-    });
+      });
+    }
+    tm.mark("canonical slots + CSR");
+    // variables in the order of their first device slot, so that neighbouring
+    // averaging threads gather and scatter neighbouring slots (the tile layout
+    // puts consecutive rows of a shape in consecutive lanes): each variable's
+    // first device slot (atomic min), then the device slots that are a first
+    // occurrence, compacted in device-slot order -- the order of a sort by first
+    // device slot, without the sort
+    P.var_list.clear();
+    {
+      const int64_t ns = (int64_t)P.slot_var.size();
+      std::vector<int32_t> first(p->n_vars, INT32_MAX);  // (device slots < 2^31, checked above)
+      par_for(ns, threads, [&](int, int64_t a, int64_t b) {
+        for (int64_t d = a; d < b; ++d)
+          if (P.slot_var[d] >= 0) atomic_min32(&first[P.slot_var[d]], (int32_t)d);
+      });
+      const int T = par_chunks(ns, threads);
+      std::vector<int64_t> cc(T + 1, 0);
+      auto is_first = [&](int64_t d) { return P.slot_var[d] >= 0 && first[P.slot_var[d]] == d; };
+      par_for(ns, threads, [&](int c, int64_t a, int64_t b) {
+        int64_t m = 0;
+        for (int64_t d = a; d < b; ++d) m += is_first(d);
+        cc[c + 1] = m;
+      });
+      for (int c = 0; c < T; ++c) cc[c + 1] += cc[c];
+      P.var_list.resize(cc[T]);
+      par_for(ns, threads, [&](int c, int64_t a, int64_t b) {
+        int64_t o = cc[c];
+        for (int64_t d = a; d < b; ++d)
+          if (is_first(d)) P.var_list[o++] = P.slot_var[d];
+      });
+    }
+    // CSR over var_list: prefix of the local degrees
+    std::vector<int64_t> where(p->n_vars, -1);
+    {
+      const int64_t nv = (int64_t)P.var_list.size();
+      const int T = par_chunks(nv, threads);
+      std::vector<int64_t> cs(T + 1, 0);
+      par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
+        int64_t m = 0;
+        for (int64_t k = a; k < b; ++k) m += cnt[P.var_list[k]];
+        cs[c + 1] = m;
+      });
+      for (int c = 0; c < T; ++c) cs[c + 1] += cs[c];
+      P.var_ptr.resize(nv + 1);
+      P.var_ptr[nv] = cs[T];
+      par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
+        int64_t o = cs[c];
+        for (int64_t k = a; k < b; ++k) {
+          P.var_ptr[k] = o;
+          where[P.var_list[k]] = o;
+          o += cnt[P.var_list[k]];
+        }
+      });
+    }
+    // fill: canonical slot indices claimed with an atomic cursor per variable,
+    // then each variable's (short) list sorted -- ascending canonical index is
+    // ascending j (A1) -- and mapped to device slots
+    {
+      const int64_t nq = (int64_t)P.canon_slot.size();
+      std::vector<int32_t> tq((size_t)std::max<int64_t>(nq, 1));
+      par_for(nq, threads, [&](int, int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q) {
+          const int32_t i = P.col_var[P.row_ptr[P.canon_con[q]] + P.canon_pos[q]];
+          tq[__atomic_fetch_add(&where[i], 1, __ATOMIC_RELAXED)] = (int32_t)q;
+        }
+      });
+      P.var_slots.assign(P.var_ptr.back(), -1);
+      par_for((int64_t)P.var_list.size(), threads, [&](int, int64_t a, int64_t b) {
+        for (int64_t k = a; k < b; ++k) {
+          const int64_t p0 = P.var_ptr[k], p1 = P.var_ptr[k + 1];
+          std::sort(tq.begin() + p0, tq.begin() + p1);
+          for (int64_t x = p0; x < p1; ++x) P.var_slots[x] = (int32_t)P.canon_slot[tq[x]];
+        }
+      });
+    }
   }
   tm.mark("variable order");
   // shared variables: held by this rank and by another one

@@ -1,12 +1,25 @@
-"""Host plan wall time per workload (FDOG_PLAN_TRACE=1 prints the phases)."""
-import os, sys, time
+"""Plan wall time per workload, host packer and GPU packer + compiler
+(FDOG_GPU_PACK=1 FDOG_GPU_COMPILE=1), with the digests (identical); with
+FDOG_PLAN_TRACE=1 the phases are printed to stderr."""
+import os
+import sys
+import time
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import synth, paper_2111_10270_b200 as F
-for name in sys.argv[1:] or ["gm_worms_like", "mrf_potts", "celltrack", "qap50", "qap128"]:
-    p = {"gm_worms_like": lambda: synth.gm_worms_like(0), "mrf_potts": lambda: synth.mrf_potts(0),
-         "celltrack": lambda: synth.celltrack(0), "qap50": lambda: synth.qap(0, 50),
-         "qap128": lambda: synth.qap(0, 128)}[name]()
-    t = time.perf_counter()
-    pl = F.Plan(p, precision=32)
-    print(f"{name}: plan {time.perf_counter() - t:.2f} s on {os.cpu_count()} host threads", flush=True)
-    pl.close()
+import paper_2111_10270_b200 as F  # noqa: E402
+import synth  # noqa: E402
+
+for name in sys.argv[1:] or ["mrf_potts", "mrf_potts_cut", "celltrack", "qap50", "qap128"]:
+    p = synth.WORKLOADS[name](0) if name in synth.WORKLOADS else synth.qap(0, 128)
+    out = {}
+    for mode in ("host", "gpu"):
+        for k in ("FDOG_GPU_PACK", "FDOG_GPU_COMPILE"):
+            os.environ.pop(k, None)
+            if mode == "gpu":
+                os.environ[k] = "1"
+        t = time.perf_counter()
+        pl = F.Plan(p, precision=32)
+        out[mode] = (time.perf_counter() - t, pl.digest())
+        pl.close()
+    print(f"{name}: plan host {out['host'][0]:.2f} s, GPU pack + compile {out['gpu'][0]:.2f} s "
+          f"({os.cpu_count()} host threads); digests equal: {out['host'][1] == out['gpu'][1]}", flush=True)

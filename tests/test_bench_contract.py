@@ -69,3 +69,27 @@ def test_gpu_arm_line():
     hop = d["per_hop_latency_ns"]
     assert hop["thin_hop"]["partitions_per_row"] == 10_000 and hop["thin_hop"]["forward_ns"] > 0
     assert hop["qap50"]["partitions_per_row"] == 50 and hop["qap50"]["backward_ns"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks_one_gpu():
+    """bench.py --gpus 2 under torchrun (the launch the driver uses for N > 1),
+    both ranks on GPU 0 with the peer-memory exchange (FDOG_SAME_DEVICE=1; NCCL
+    refuses two ranks on one GPU): a functional check of the sharded,
+    overlapped, graph-captured pass -- rank 0 alone prints one line, with the
+    exchange reported separately.  (Its times are two contexts sharing one
+    GPU, not a measurement.)"""
+    env = dict(os.environ, FDOG_SAME_DEVICE="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-ttl", "--no-e2e",
+                        "--no-traffic", "--no-hop", "--exchange", "peer", "--workload", "qap50"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    x = d["exchange"]
+    assert x["shared_vars"] > 0 and 0 < x["overlapped_tiles"] < x["tiles"]
+    assert x["finish_us_per_pass"] > 0

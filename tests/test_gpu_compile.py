@@ -61,3 +61,51 @@ def test_gpu_compile_infeasible_row(monkeypatch):
         with pytest.raises(F.FastdogError) as e:
             F.Plan(p)
         assert e.value.code == 2
+
+
+@pytest.mark.parametrize("name,make", CASES + [
+    ("mrf", lambda: synth.mrf_potts(7, H=20, W=24, L=4)),
+    ("mrf_cut", lambda: synth.mrf_potts_cut(7, H=16, W=18, L=5)),
+    ("gap", lambda: synth.gap(7, jobs=40, agents=5)),
+])
+@pytest.mark.parametrize("opts", [{}, {"world": 2, "rank": 1}, {"lifted": True}, {"precision": 64}])
+def test_gpu_pack_identical(monkeypatch, name, make, opts):
+    """The packer's canonical-slot and variable phases on the GPU
+    (FDOG_GPU_PACK=1, pack_gpu.cu: scans, atomic-min first slots, a stable
+    radix sort) give the host packer's plan byte for byte (digest of every
+    array and the device image), for sharded, lifted and fp64 plans too."""
+    if opts.get("lifted") and opts.get("world", 1) > 1:
+        pytest.skip("lifted plans are single-GPU")
+    p = make()
+    monkeypatch.delenv("FDOG_GPU_PACK", raising=False)
+    host = F.Plan(p, **opts).digest()
+    monkeypatch.setenv("FDOG_GPU_PACK", "1")
+    gpu = F.Plan(p, **opts).digest()
+    assert gpu == host
+
+
+def test_gpu_pack_full_mrf_digest():
+    """MRF-LP at full size packed on the GPU: same digest as the host packer."""
+    import os
+    p = synth.mrf_potts(0)
+    os.environ["FDOG_GPU_PACK"] = "1"
+    try:
+        a = F.Plan(p).digest()
+    finally:
+        del os.environ["FDOG_GPU_PACK"]
+    assert a == F.Plan(p).digest()
+
+
+@pytest.mark.parametrize("name,make", CASES[:3] + [("gap", lambda: synth.gap(8, jobs=40, agents=5))])
+def test_gpu_compile_vs_oracle_compiler(monkeypatch, oracle_mod, name, make):
+    """The GPU compiler against the oracle's independent compiler A (top-down
+    partial sums, bottom-up signature merge): per-partition node counts of
+    every BDD equal (the canonical quasi-reduced form is unique, A12)."""
+    p = make()
+    monkeypatch.setenv("FDOG_GPU_COMPILE", "1")
+    pl = F.Plan(p)
+    o = oracle_mod.Oracle(p)
+    assert pl.stats()["nodes"] == o.total_nodes()
+    for j in range(p.n_cons):
+        hs, _, _ = pl.bdd(j)
+        assert np.array_equal(np.diff(hs), o.hop_widths(j)), f"row {j}"
