@@ -77,22 +77,22 @@ def test_gpu_pack_identical(monkeypatch, name, make, opts):
     if opts.get("lifted") and opts.get("world", 1) > 1:
         pytest.skip("lifted plans are single-GPU")
     p = make()
-    monkeypatch.delenv("FDOG_GPU_PACK", raising=False)
+    monkeypatch.setenv("FDOG_GPU_PACK", "0")
     host = F.Plan(p, **opts).digest()
     monkeypatch.setenv("FDOG_GPU_PACK", "1")
     gpu = F.Plan(p, **opts).digest()
     assert gpu == host
 
 
-def test_gpu_pack_full_mrf_digest():
-    """MRF-LP at full size packed on the GPU: same digest as the host packer."""
-    import os
+def test_gpu_pack_full_mrf_digest(monkeypatch):
+    """MRF-LP at full size, compiled and packed on the GPU (the default at
+    this size): same digest as the host compiler and packer."""
     p = synth.mrf_potts(0)
-    os.environ["FDOG_GPU_PACK"] = "1"
-    try:
-        a = F.Plan(p).digest()
-    finally:
-        del os.environ["FDOG_GPU_PACK"]
+    monkeypatch.setenv("FDOG_GPU_PACK", "1")
+    monkeypatch.setenv("FDOG_GPU_COMPILE", "1")
+    a = F.Plan(p).digest()
+    monkeypatch.setenv("FDOG_GPU_PACK", "0")
+    monkeypatch.setenv("FDOG_GPU_COMPILE", "0")
     assert a == F.Plan(p).digest()
 
 
