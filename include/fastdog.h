@@ -12,8 +12,9 @@
  *   - Input arrays are HOST pointers borrowed for the duration of the call
  *     (copied).  Output arrays are caller-allocated HOST arrays with an
  *     explicit length; a length that is too small returns FDOG_EINVAL.
- *   - A solver handle owns all of its device memory (and its NCCL
- *     communicator when world > 1); fdog_destroy frees them.  A handle is
+ *   - A solver handle owns all of its device memory (obtained through
+ *     opts.dev_alloc when given, e.g. torch's caching allocator) and its
+ *     NCCL communicator when world > 1; fdog_destroy frees them.  A handle is
  *     not thread-safe.  Device work is stream-ordered on opts.stream;
  *     getters synchronise that stream.
  *   - Slot = one multiplier lambda_i^j, i.e. one (constraint j, position h
@@ -22,6 +23,7 @@
  */
 #ifndef FASTDOG_H
 #define FASTDOG_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -80,6 +82,21 @@ typedef struct {
                                every tile runs from global memory (lane-serial or
                                node-parallel); no primal rounding, non-deferred
                                passes, set_state or averaged finalize.          */
+  /* Caller-owned device memory (north_star: "PyTorch is used only for device
+     memory, streams and process groups").  If dev_alloc is set, every device
+     buffer a solver holds -- the plan image with the runtime state, the
+     non-deferred schedule, the primal-rounding snapshot -- is obtained by
+     dev_alloc(bytes, device, stream, alloc_ctx), stream-ordered on the
+     solver's stream (the caller's opts.stream or the solver-owned one), and
+     returned by dev_free(ptr, device, stream, alloc_ctx) after that stream
+     has been synchronised (fdog_destroy, end of fdog_round_primal).  A NULL
+     return fails the call with FDOG_ENOMEM.  The one exception is the
+     peer-exchange region (external-exchange mode), a cudaMalloc of its own
+     so that one CUDA IPC handle maps exactly it.  dev_alloc NULL: cudaMalloc
+     / cudaFree.  The Python binding passes torch's caching allocator. */
+  void *(*dev_alloc)(size_t bytes, int32_t device, void *stream, void *alloc_ctx);
+  void (*dev_free)(void *ptr, int32_t device, void *stream, void *alloc_ctx);
+  void *alloc_ctx;
 } fdog_options;
 
 /* Sizes of this rank's part of the problem. */

@@ -59,7 +59,43 @@ class Options(C.Structure):
                 ("record_mm", C.c_int32), ("profile", C.c_int32), ("rank", C.c_int32),
                 ("world", C.c_int32), ("nccl_unique_id", C.c_void_p), ("nccl_library", C.c_char_p),
                 ("stream", C.c_void_p), ("host_threads", C.c_int32),
-                ("row_owner", C.c_void_p), ("lifted", C.c_int32)]
+                ("row_owner", C.c_void_p), ("lifted", C.c_int32),
+                ("dev_alloc", C.c_void_p), ("dev_free", C.c_void_p), ("alloc_ctx", C.c_void_p)]
+
+
+# fdog_options::dev_alloc / dev_free: the solver's device memory from torch's
+# caching allocator, stream-ordered on the solver's stream.
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p)
+_live_solvers = None  # weak set of solvers holding torch memory (closed at exit, before torch)
+
+
+@_ALLOC_FN
+def _torch_alloc(nbytes, device, stream, ctx):
+    import torch
+    try:
+        return torch.cuda.caching_allocator_alloc(int(nbytes), int(device), int(stream or 0))
+    except (RuntimeError, torch.OutOfMemoryError):
+        return None  # -> FDOG_ENOMEM
+
+
+@_FREE_FN
+def _torch_free(ptr, device, stream, ctx):
+    import torch
+    torch.cuda.caching_allocator_delete(int(ptr))
+
+
+def _torch_memory(solver):
+    """Register a solver whose memory comes from torch; returns the two callbacks."""
+    global _live_solvers
+    if _live_solvers is None:
+        import atexit
+        import weakref
+        import torch  # noqa: F401  (imported first: its exit handlers run after ours)
+        _live_solvers = weakref.WeakSet()
+        atexit.register(lambda: [x.close() for x in list(_live_solvers)])
+    _live_solvers.add(solver)
+    return C.cast(_torch_alloc, C.c_void_p), C.cast(_torch_free, C.c_void_p)
 
 
 class Stats(C.Structure):
@@ -304,11 +340,18 @@ class Solver:
 
     def __init__(self, problem=None, *, plan: Plan | None = None, precision=32, device=0, clamp=0.0,
                  record_mm=False, profile=False, rank=0, world=1, nccl_unique_id=None,
-                 nccl_library=None, stream=None, host_threads=0, row_owner=None, lifted=False):
+                 nccl_library=None, stream=None, host_threads=0, row_owner=None, lifted=False,
+                 allocator="torch"):
+        """allocator: "torch" (device memory from torch's caching allocator, the
+        default) or "cuda" (the library's own cudaMalloc)."""
         lib = load()
         self._lib = lib
         self._opts = make_options(precision, device, clamp, record_mm, profile, rank, world,
                                   nccl_unique_id, nccl_library, stream, host_threads, row_owner, lifted)
+        if allocator == "torch":
+            self._opts.dev_alloc, self._opts.dev_free = _torch_memory(self)
+        elif allocator != "cuda":
+            raise ValueError(f"allocator must be 'torch' or 'cuda', not {allocator!r}")
         h = C.c_void_p()
         if plan is not None:
             _check(lib.fdog_create_from_plan(plan._h, C.byref(self._opts), C.byref(h)),

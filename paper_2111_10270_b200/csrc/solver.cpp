@@ -62,6 +62,11 @@ struct fdog_solver {
   size_t tsz = 4;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // caller-owned device memory (fdog_options::dev_alloc); allocs come from it
+  void *(*dev_alloc)(size_t, int32_t, void *, void *) = nullptr;
+  void (*dev_free)(void *, int32_t, void *, void *) = nullptr;
+  void *alloc_ctx = nullptr;
+  std::vector<void *> own_allocs;  // cudaMalloc'ed regardless (the IPC-mapped exchange region)
   bool record_mm = false;
   bool profile = false;
   double clamp = 0.0;
@@ -196,6 +201,23 @@ struct fdog_solver {
   int64_t prof_n[kKCount] = {0};
   double bytes[kKCount] = {0};
 };
+
+// Device memory of a solver: the caller's allocator if it gave one, else cudaMalloc.
+static cudaError_t dev_alloc(fdog_solver *s, void **p, size_t bytes) {
+  if (!s->dev_alloc) return cudaMalloc(p, bytes);
+  *p = s->dev_alloc(bytes, s->device, (void *)s->stream, s->alloc_ctx);
+  return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+
+static void dev_free(fdog_solver *s, void *p) {
+  if (!p) return;
+  if (s->dev_alloc) {
+    if (s->dev_free) s->dev_free(p, s->device, (void *)s->stream, s->alloc_ctx);
+  } else {
+    cudaFree(p);
+  }
+}
+
 
 namespace {
 
@@ -507,7 +529,7 @@ fdog_status seq_schedule(fdog_solver *s) {
   const size_t bytes = slot_tile.size() * 4 + 2 * ((size_t)(n + 1) * 8 + (size_t)std::max<int64_t>(S, 1) * 4) +
                        (size_t)std::max(s->n_tiles, 1) * kMaxTileRows * 8 + 8 * 256;  // + alignment of six sections
   unsigned char *base = nullptr;
-  CK(cudaMalloc((void **)&base, bytes), "cudaMalloc (seq schedule)");
+  CK(dev_alloc(s, (void **)&base, bytes), "device allocation (seq schedule)");
   s->allocs.push_back(base);
   size_t at = 0;
   auto carve = [&](size_t b) {
@@ -633,7 +655,8 @@ void free_solver(fdog_solver *s) {
   }
   if (s->ev_fork) cudaEventDestroy(s->ev_fork);
   if (s->ev_join) cudaEventDestroy(s->ev_join);
-  for (void *p : s->allocs) cudaFree(p);
+  for (void *p : s->allocs) dev_free(s, p);
+  for (void *p : s->own_allocs) cudaFree(p);
   if (s->nccl.comm && s->nccl.destroy) s->nccl.destroy(s->nccl.comm);
   if (s->nccl.lib) dlclose(s->nccl.lib);
   if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
@@ -731,6 +754,9 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   }
   s->tsz = s->precision == 64 ? 8 : 4;
   s->device = o->device;
+  s->dev_alloc = o->dev_alloc;
+  s->dev_free = o->dev_free;
+  s->alloc_ctx = o->alloc_ctx;
   s->record_mm = o->record_mm != 0;
   s->lifted = o->lifted != 0;
   if (s->lifted != P.lifted) {
@@ -944,7 +970,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   const size_t o_l0 = s->lifted ? carve(slot_bytes) : 0, o_a0 = s->lifted ? carve(slot_bytes) : 0;
   const size_t o_lo = s->lifted ? carve(slot_bytes) : 0;
   unsigned char *base = nullptr;
-  CK(cudaMalloc((void **)&base, im.bytes + rt), "cudaMalloc");
+  CK(dev_alloc(s, (void **)&base, im.bytes + rt), "device allocation");
   s->allocs.push_back(base);
   s->st.device_bytes = (int64_t)(im.bytes + rt);
   s->upload_bytes = (int64_t)im.bytes;
@@ -994,7 +1020,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   }
   if (const char *tr = getenv("FDOG_TRACE"); tr && tr[0] == '1') {
     void *p = nullptr;
-    CK(cudaMalloc(&p, (size_t)s->grid * (s->block / 32) * 4 * 8), "cudaMalloc (trace)");
+    CK(dev_alloc(s, &p, (size_t)s->grid * (s->block / 32) * 4 * 8), "device allocation (trace)");
     s->allocs.push_back(p);
     s->d_trace = (unsigned long long *)p;
   }
@@ -1012,7 +1038,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     s->region_stride = ((size_t)std::max<int32_t>(s->n_shared, 1) * s->tsz + 255) & ~(size_t)255;
     const size_t rb = kRegionBuf + 2 * s->region_stride;
     CK(cudaMalloc((void **)&s->d_region, rb), "cudaMalloc (exchange region)");
-    s->allocs.push_back(s->d_region);
+    s->own_allocs.push_back(s->d_region);
     CK(cudaMemsetAsync(s->d_region, 0, rb, s->stream), "memset");
   }
   // FDOG_NCCL_SELF=1 (test knob): a one-rank NCCL communicator for world == 1,
@@ -1216,7 +1242,8 @@ fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, u
   const size_t db = (size_t)std::max<int64_t>(s->n_dist, 1) * s->tsz;
   std::vector<void *> snap;
   auto cleanup = [&]() {
-    for (void *p : snap) cudaFree(p);
+    if (!snap.empty()) cudaStreamSynchronize(s->stream);
+    for (void *p : snap) dev_free(s, p);
   };
   const int cur0 = s->cur, ds0 = s->dist_state;
   const int64_t passes0 = s->passes;
@@ -1235,10 +1262,10 @@ fdog_status fdog_round_primal(fdog_solver *s, const fdog_primal_options *opts, u
   if (!o->keep_state) {
     for (size_t q = 0; q < live.size(); ++q) {
       void *pq = nullptr;
-      cudaError_t e = cudaMalloc(&pq, sz[q]);
+      cudaError_t e = dev_alloc(s, &pq, sz[q]);
       if (e != cudaSuccess) {
         cleanup();
-        return cuda_fail(e, "cudaMalloc (primal snapshot)");
+        return cuda_fail(e, "device allocation (primal snapshot)");
       }
       snap.push_back(pq);
       e = cudaMemcpyAsync(pq, live[q], sz[q], cudaMemcpyDeviceToDevice, s->stream);

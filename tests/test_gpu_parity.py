@@ -739,3 +739,27 @@ def test_elld_averaging(oracle_mod, monkeypatch, name, make):
         s = int(np.dot(c, x[v]))
         assert (s <= rhs) if rel < 0 else (s >= rhs) if rel > 0 else (s == rhs)
     assert obj >= lb - 1e-6 * (1 + abs(lb))
+
+
+def test_device_memory_from_torch():
+    """fdog_options::dev_alloc: the solver's device memory comes from torch's
+    caching allocator (the binding's default), results bit-identical to the
+    library's own cudaMalloc, and destroy hands it back."""
+    import gc
+    import torch
+    p = synth.gm_worms_like(5, n_src=60, k_cand=6, knn=6)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    g1 = F.Solver(p, precision=32)                      # allocator="torch"
+    held = torch.cuda.memory_allocated() - before
+    assert held >= g1.stats()["device_bytes"] > 0
+    g2 = F.Solver(p, precision=32, allocator="cuda")
+    assert torch.cuda.memory_allocated() - before == held
+    for s in (g1, g2):
+        s.iterate(5, 0.5)
+    assert np.array_equal(g1.lam(), g2.lam()) and g1.lower_bound() == g2.lower_bound()
+    g1.close(); g2.close()
+    gc.collect()
+    assert torch.cuda.memory_allocated() == before
+    with pytest.raises(ValueError):
+        F.Solver(p, allocator="numpy")
