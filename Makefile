@@ -10,11 +10,11 @@ all: $(PKG)/libfastdog.so oracle/liboracle.so
 
 OBJ := $(patsubst $(PKG)/csrc/%,build/obj/%.o,$(SRC))
 
-# (make -j: the four sources compile concurrently; kernels.cu also splits its
-# device code over the cores)
+# (make -j: the four sources compile concurrently; no --split-compile, which
+# made ptxas's output vary from build to build)
 build/obj/%.cu.o: $(PKG)/csrc/%.cu $(PKG)/csrc/internal.h include/fastdog.h
 	@mkdir -p build/obj
-	$(NVCC) $(NVFLAGS) --split-compile=0 -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
 build/obj/%.cpp.o: $(PKG)/csrc/%.cpp $(PKG)/csrc/internal.h include/fastdog.h
 	@mkdir -p build/obj

@@ -53,6 +53,11 @@ struct Shape {
 //          is a chain hop (HopRec type 1); the sweeps fold those hops.
 //   kind bit 4 set (with bit 3): the first partition is a root hop (type 2)
 //          and the last a join into top (type 3); folded as well.
+//   kind bit 6 set (with bit 2): the hop records are not staged; the
+//          kernels read them from global memory (set by the packer for tiles
+//          whose stage would not fit the budget with them; a shape's records
+//          are shared by its tiles, i.e. L1 / L2-resident).  Bit 4 tiles
+//          never read their records and stage none either.
 //   kind bit 5 set ("cooperative", shapes wider than kCoopWidth): one BDD
 //          (L = 1), processed node-parallel by a whole warp from global
 //          memory; its topology is two 32-bit words per node (uint2 at
@@ -115,8 +120,12 @@ FDOG_HD int stage_hop_bytes(int K) { return r16((K + 1) * 4); }
 //   type     0 generic; 1..3 a specialised pattern (plan.cpp append_recs,
 //            kernels.cu hop_type): the kernels then skip the masks.
 FDOG_HD int rec_bytes(int tsz) { return 8 * tsz + 16; }
+constexpr int kKindRecGlobal = 64;  // kind bit 6
+// (arc-mask tiles: the records, unless bit 4 (never read) or bit 6 (read from
+// global memory) is set)
 FDOG_HD int stage_tail_bytes(int tsz, int kind, int K, int nodes, int L) {
-  return (kind & 4) ? r16(K * rec_bytes(tsz)) : stage_topo_bytes(kind, nodes, L) + stage_hop_bytes(K);
+  if (kind & 4) return (kind & (16 | kKindRecGlobal)) ? 0 : r16(K * rec_bytes(tsz));
+  return stage_topo_bytes(kind, nodes, L) + stage_hop_bytes(K);
 }
 FDOG_HD int stage_bytes(int tsz, int kind, int K, int nodes, int L) {
   return stage_lam_bytes(tsz, K, L) + stage_va_bytes(tsz, K, L) + stage_dist_bytes(tsz, nodes, L) +
@@ -258,6 +267,7 @@ struct SweepArgs {
   const uint32_t *pairs; // tile-closed pair lists (null: none)
   void *m0, *m1;         // T*, recorded min-marginals (may be null)
   double omega, clamp;
+  float omega_f, clamp_f;  // the same, rounded once to fp32 (fp32 kernels read them as operands)
   double *lb_part;       // per tile bound contribution (reduced by lb_reduce_kernel)
   unsigned int *done_counter;
   unsigned int *tile_counter;  // dynamic tile scheduler (reset by the last CTA)
@@ -354,6 +364,7 @@ struct SeqArgs {
   void *m0, *m1;              // T*, recorded min-marginals (may be null)
   double *e_lane;             // per (tile, lane): E^j, written at the BDD's last visited partition
   double omega, clamp;
+  float omega_f, clamp_f;     // the same in fp32
   int32_t forward;
 };
 int launch_seq_level(int precision, bool record, const SeqArgs &a, int64_t q0, int64_t q1, void *stream);

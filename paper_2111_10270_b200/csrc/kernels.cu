@@ -57,6 +57,20 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 // discarded), so one test of |m1 - m0| and a copysign give the reading.
 __device__ __forceinline__ float copysign_t(float c, float s) { return copysignf(c, s); }
 __device__ __forceinline__ double copysign_t(double c, double s) { return copysign(c, s); }
+// omega and the clamp of a launch in the kernel's precision (T(double) rounds
+// once; the fp32 copies are the same values, read straight from the
+// parameter bank instead of converted per use)
+template <typename T, class A>
+__device__ __forceinline__ T arg_omega(const A &a) {
+  if constexpr (sizeof(T) == 4) return a.omega_f;
+  else return a.omega;
+}
+template <typename T, class A>
+__device__ __forceinline__ T arg_clamp(const A &a) {
+  if constexpr (sizeof(T) == 4) return a.clamp_f;
+  else return a.clamp;
+}
+
 template <typename T>
 __device__ __forceinline__ T mm_difference(T m1, T m0, T clamp) {
   const T d = sub_rn(m1, m0);
@@ -904,17 +918,17 @@ __device__ __forceinline__ T mask_finish(T *lam, T *va, uint32_t hL, T l, T av, 
   const T m1 = l + m1r;
   const T delta = mul_rn(omega, mm_difference(m1, m0, clamp));
   const T lam_new = add_rn(sub_rn(l, delta), av);
-  if (valid) {
-    lam[hL] = lam_new;
-    va[hL] = delta;
-    if (REC) {
-      m0g[hL] = m0;
-      m1g[hL] = m1;
-    }
-    acc += (double)fmin(delta, T(0));
-  } else {
-    va[hL] = T(0);
+  // branch-free: a padding row keeps its lambda and writes delta = 0 (selects
+  // instead of a branch per row and hop, whose reconvergence made the
+  // compiler re-derive the lane's addresses every hop)
+  const T dv = valid ? delta : T(0);
+  lam[hL] = valid ? lam_new : l;
+  va[hL] = dv;
+  if (REC && valid) {
+    m0g[hL] = m0;
+    m1g[hL] = m1;
   }
+  acc += (double)fmin(dv, T(0));  // (+0 for padding: acc >= +0 sums stay exact)
   return lam_new;
 }
 
@@ -1340,8 +1354,9 @@ __device__ __forceinline__ void issue_stage(const SweepArgs &a, const TileDesc &
   const uint32_t va_b = upd ? lam_b : 0u;
   const uint32_t dist_b = RC ? 0u : (uint32_t)(d.nodes + 2) * d.lanes * sizeof(T);
   const bool masks = d.kind & 4;  // hop records instead of topology + partition offsets
-  // (fully folded tiles, kind bit 4, never read their records)
-  const uint32_t topo_b = masks ? ((d.kind & 16) ? 0u : (uint32_t)(d.K * rec_bytes((int)sizeof(T))))
+  // (records: none staged for fully folded tiles, which never read them, and
+  // for kind bit 6 tiles, which read them from global memory)
+  const uint32_t topo_b = masks ? (uint32_t)stage_tail_bytes((int)sizeof(T), d.kind, d.K, d.nodes, d.lanes)
                                 : (uint32_t)stage_topo_bytes(d.kind, d.nodes, d.lanes);
   const uint32_t hop_b = masks ? 0u : (uint32_t)stage_hop_bytes(d.K);
   const uint32_t pair_b = (upd && a.pairs && d.n_pairs > 0) ? (uint32_t)stage_pairs_bytes(d.n_pairs) : 0u;
@@ -1380,8 +1395,14 @@ __device__ __forceinline__ void fetch_desc(TileDesc *dst, const TileDesc *src, i
 // RW = 1).  A kernel holding tcgen05 code runs one CTA per SM (the driver's
 // rule), so TM kernels launch one CTA of up to 16 warps per SM and the others
 // carry no tcgen05 code at all.
+// Registers, stated: CTAs of 4 warps (solver.cpp), at least 6 resident per SM
+// (<= 80 registers; 4 with four rows per lane: <= 128); TM kernels one CTA of
+// up to 16 warps.  Left to ptxas, the same source compiled to 64 (spilling)
+// or to 97-106 registers depending on how --split-compile partitioned the
+// module, which moved MRF-LP between 5 and 4 resident CTAs per SM (541 vs 571
+// us per iteration) and GM-worms between 6 and 4 (42.6 vs 45.5 us).
 template <typename T, int MODE, bool REC, bool RC, int RW, bool TM>
-__global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(TM ? 512 : 128, TM ? 1 : (RW >= 4 ? 4 : 6)) sweep_kernel(const SweepArgs a) {
   static_assert(!TM || (RC && RW == 1 && std::is_same<T, float>::value), "TMEM distances: fp32 recompute design");
   constexpr bool kUpd = MODE == kForward || MODE == kBackward;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1398,7 +1419,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
   T *__restrict__ lambda = reinterpret_cast<T *>(a.lambda);
   T *__restrict__ delta_out = reinterpret_cast<T *>(a.delta_out);
   T *__restrict__ gdist = reinterpret_cast<T *>(a.dist);
-  const T omega = T(a.omega), clamp = T(a.clamp);
+  const T omega = arg_omega<T>(a), clamp = arg_clamp<T>(a);
   const int gwarp = blockIdx.x * wpb + warp;
 
   // TM: the distance scratch of the 32-row arc-mask tiles lives in tensor
@@ -1528,7 +1549,10 @@ __global__ void __launch_bounds__(512) sweep_kernel(const SweepArgs a) {
       if (d.kind & 4) {
         // arc-mask tile (narrow shape, shared topology)
         if (active) {
-          const HopRec<T> *rec = reinterpret_cast<const HopRec<T> *>(s.topo);
+          // (kind bit 6: the shape's records in global memory, not staged)
+          const HopRec<T> *rec = (d.kind & kKindRecGlobal)
+                                     ? reinterpret_cast<const HopRec<T> *>(a.recs + 16 * (int64_t)d.rec_base)
+                                     : reinterpret_cast<const HopRec<T> *>(s.topo);
           const int chain = ((d.kind & 8) ? 1 : 0) | ((d.kind & 16) ? 2 : 0);
           T *D = RC ? reinterpret_cast<T *>(rbase) + lane : s.dist + lane;
           if (RC && !(TM && L == 32))
@@ -1889,7 +1913,7 @@ __global__ void __launch_bounds__(128) sweep_chunk_kernel(const SweepArgs a) {
   T *gD = reinterpret_cast<T *>(a.dist) + d.dist_base;
   T *m0g = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
   T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
-  const T omega = T(a.omega), clamp = T(a.clamp), inf = t_inf<T>();
+  const T omega = arg_omega<T>(a), clamp = arg_clamp<T>(a), inf = t_inf<T>();
   if (lane == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -2000,7 +2024,7 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
     T *D = reinterpret_cast<T *>(a.dist) + d.dist_base + lane;
     T *m0g = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
     T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
-    const T omega = T(a.omega), clamp = T(a.clamp);
+    const T omega = arg_omega<T>(a), clamp = arg_clamp<T>(a);
     if (L == 32) {
       acc = MODE == kForward ? mask_forward<T, true, REC, 32, 1>(K, chain, rec, 32, lam, va, SmemD<T, 1>{D, 32u}, valid,
                                                                  omega, clamp, m0g, m1g)
@@ -2022,7 +2046,7 @@ __global__ void __launch_bounds__(128) sweep_stream_kernel(const SweepArgs a) {
     T *m0g = REC ? reinterpret_cast<T *>(a.m0) + d.slot_base + lane : nullptr;
     T *m1g = REC ? reinterpret_cast<T *>(a.m1) + d.slot_base + lane : nullptr;
     const T inf = t_inf<T>();
-    const T omega = T(a.omega), clamp = T(a.clamp);
+    const T omega = arg_omega<T>(a), clamp = arg_clamp<T>(a);
     const int top = d.nodes;
     auto finish = [&](int h, T l, T av, T m0, T m1r) -> T {
       const T m1 = l + m1r;
@@ -2361,7 +2385,7 @@ __global__ void __launch_bounds__(1024) fused_small_kernel(const SweepArgs sa, c
   T *const g_lambda = reinterpret_cast<T *>(sa.lambda);
   T *const g_dist = reinterpret_cast<T *>(sa.dist);
   T *dbar = g_dbar, *va_all = g_va, *lambda = g_lambda, *gdist = g_dist;
-  const T omega = T(sa.omega), clamp = T(sa.clamp);
+  const T omega = arg_omega<T>(sa), clamp = arg_clamp<T>(sa);
   extern __shared__ __align__(16) unsigned char fsm[];
   pdl_wait();
   if (resident) {
@@ -2681,7 +2705,7 @@ __global__ void __launch_bounds__(128) seq_level_kernel(const SeqArgs a, int64_t
   T *__restrict__ lam = reinterpret_cast<T *>(a.lambda);
   T *__restrict__ D = reinterpret_cast<T *>(a.dist);
   T *__restrict__ dl = reinterpret_cast<T *>(a.delta);
-  const T omega = T(a.omega), clamp = T(a.clamp), inf = t_inf<T>();
+  const T omega = arg_omega<T>(a), clamp = arg_clamp<T>(a), inf = t_inf<T>();
   const int64_t p0 = a.ptr[q], p1 = a.ptr[q + 1];
   // min-marginals of the variable in every j in J_i
   T sum = T(0);
@@ -2855,6 +2879,12 @@ static cudaError_t allow_max_smem(const void *f) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  // all of the unified L1 / shared storage as shared memory: without a stated
+  // preference the occupancy query and the carveout the driver picks at launch
+  // varied between boxes (MRF-LP sweeps at 4 or 5 CTAs per SM with the same
+  // binary: 570 vs 541 us per iteration)
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
   return e;
 }
 

@@ -778,6 +778,9 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       tm_rows_ok = tm_rows_ok && rows_per_lane(sh) == 1;
     }
   bool tm_packed = false, tm_allow = true;
+  const bool tm_trace = getenv("FDOG_PLAN_TRACE") != nullptr;
+  const char *rg = getenv("FDOG_RECS");  // test knob: FDOG_RECS=global reads every tile's records from global memory
+  const bool recs_global = rg && rg[0] == 'g';
   auto pack = [&](bool rc, int nb) {
     std::vector<PendingTile> pend;
     P.NB = nbuf ? (atoi(nbuf) == 1 ? 1 : 2) : nb;
@@ -806,9 +809,10 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       // recompute design: DB = SB holds the distance scratch (for partitions of
       // <= 2 nodes the distances of a tile are about as large as its stage)
       const int DB0 = relax_bytes(tsz, std::min(maxW, 64), 32);
-      const int cands[] = {6, 7, 8, 9, 10, 11, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 72, 96, 112};
+      const int cands[] = {6, 7, 8, 9, 10, 11, 12, 14, 16, 18, 20, 22, 24, 28, 32, 40, 48, 56, 72, 96, 112};
       double best = 1e300;
       int bestSB = 0, bestDB = DB0;
+      std::vector<std::array<double, 4>> cand_t;  // (modelled time, warps per SM, SB, DB)
       for (int kb : cands) {
         const int SB = tm ? ((kb * 1024 - 16 - 64) / P.NB) & ~15
                           : rc ? ((kb * 1024 - 16) / (P.NB + 1)) & ~15 : ((kb * 1024 - 16 - DB0) / P.NB) & ~15;
@@ -820,8 +824,9 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
           if (by_shape[s].empty()) continue;
           const Shape &S = P.shapes[s];
           const int k0 = (S.max_w <= 2 && !P.lifted) ? 4 : 0;  // arc-mask tiles for narrow shapes
+          const int kb0 = k0 ? k0 | kKindRecGlobal : 0;  // (sized without records: they may stay in global memory)
           const bool pr = k0 && pair_room[s];
-          int L = lanes_for(k0, S.k, S.nodes(), S.max_w, SB, DB, pr, 32 * rows_per_lane(s));
+          int L = lanes_for(kb0, S.k, S.nodes(), S.max_w, SB, DB, pr, 32 * rows_per_lane(s));
           double pen = (wide_force && L > 0 && L < 32 * rows_per_lane(s)) ? 1e6 : 1.0;
           if (L == 0) {  // direct from global memory: latency-bound
             L = 32;
@@ -829,7 +834,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
             // that leaves any is a fallback to the store design)
             pen = rc ? 1e6 : 10.0;
           } else {
-            usedSB = std::max(usedSB, (rc ? stage_bytes_rc(tsz, k0, S.k, S.nodes(), L) : stage_bytes(tsz, k0, S.k, S.nodes(), L)) +
+            usedSB = std::max(usedSB, (rc ? stage_bytes_rc(tsz, kb0, S.k, S.nodes(), L) : stage_bytes(tsz, kb0, S.k, S.nodes(), L)) +
                                           (pr ? stage_pairs_bytes(S.k * L / 2) : 0));
             if (rc && !(tm && k0 && L == 32)) usedDB = std::max(usedDB, stage_dist_bytes(tsz, S.nodes(), L));
           }
@@ -846,15 +851,26 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         }
         if (!rc) usedDB = DB;
         const int wb = warp_bytes(usedSB, usedDB, P.NB);
-        const double warps = std::min(tm ? 4.0 * (512 / tm_cols) : 32.0, std::floor(226.0 * 1024 / wb));
+        double warps = std::min(tm ? 4.0 * (512 / tm_cols) : 32.0, std::floor(226.0 * 1024 / wb));
+        if (tm) warps = std::floor(warps / 4) * 4;  // (the TMEM kernel's CTAs: groups of 4 warps)
         if (warps < 1) continue;
         const double t = std::max(chain / (148.0 * warps), instr / (148.0 * 2.0));
-        if (t < best * 0.98) {
-          best = t;
-          bestSB = usedSB;
-          bestDB = usedDB;
-        }
+        if (tm_trace) fprintf(stderr, "[plan] budget rc=%d tm=%d kb=%d SB=%d usedSB=%d usedDB=%d warps=%.0f chain=%.3g instr=%.3g t=%.4g\n",
+                              (int)rc, (int)tm, kb, SB, usedSB, usedDB, warps, chain, instr, t);
+        cand_t.push_back({t, warps, (double)usedSB, (double)usedDB});
       }
+      // the candidate with the most resident warps among those within 0.5 % of
+      // the best modelled time (the model is issue-bound for most problems,
+      // and more warps hide more of the latency it does not model); ties: the
+      // first, i.e. the smallest budget
+      for (const auto &c : cand_t) best = std::min(best, c[0]);
+      double best_w = -1;
+      for (const auto &c : cand_t)
+        if (c[0] <= 1.005 * best && c[1] > best_w) {
+          best_w = c[1];
+          bestSB = (int)c[2];
+          bestDB = (int)c[3];
+        }
       P.SB = std::max(bestSB, 64);
       P.DB = rc ? std::max(bestDB, 64) : DB0;
     }
@@ -864,7 +880,8 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       auto &rows = by_shape[s];
       const Shape &S = P.shapes[s];
       const int k0 = (S.max_w <= 2 && !P.lifted) ? 4 : 0;
-      int L = lanes_for(k0, S.k, S.nodes(), S.max_w, P.SB, P.DB, k0 && pair_room[s], 32 * rows_per_lane(s));
+      int L = lanes_for(k0 ? k0 | kKindRecGlobal : 0, S.k, S.nodes(), S.max_w, P.SB, P.DB, k0 && pair_room[s],
+                        32 * rows_per_lane(s));
       const bool staged = L > 0;
       if (!staged) L = 32;
       // (rows too long to stage, of a narrow shape: the last tile keeps the
@@ -1021,7 +1038,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     // 3 -6 %; cell tracking 12 vs 12 +1.5 %)
     if (rc && tm_packed && !(tmv && tmv[0] == '1')) {
       const int SB1 = P.SB, DB1 = P.DB, NB1 = P.NB;
-      const int w_tm = std::min({16, 4 * (512 / tm_cols), 227 * 1024 / warp_bytes(SB1, DB1, NB1)});
+      const int w_tm = std::min({16, 4 * (512 / tm_cols), 227 * 1024 / warp_bytes(SB1, DB1, NB1)}) & ~3;
       tm_allow = false;
       std::vector<PendingTile> pend0 = pack(true, NB1);
       const int w_sm = std::min(32, 227 * 1024 / warp_bytes(P.SB, P.DB, P.NB));
@@ -1037,6 +1054,33 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     }
   }
   P.rc = rc;
+  // Hop records of staged arc-mask tiles (not fully folded): read from global
+  // memory (kind bit 6) when the stages leave L1 room for a shape's records
+  // (>= 48 KB of the SM's 256 KB L1 / shared storage); else staged with the
+  // tile where the stage still fits the budget with them.  (Measured: cell
+  // tracking, 220 KB of stages per SM, +5 % with records in global memory --
+  // an L2 round trip per hop; Potts-cut, 139 KB, -6 % -- no TMA bytes and
+  // smaller stages.)
+  {
+    const int wb = warp_bytes(P.SB, P.DB, P.NB);
+    int warps_sm;
+    if (tm_packed) {
+      warps_sm = std::min({16, 4 * (512 / std::max(tm_cols, 32)), 227 * 1024 / wb}) & ~3;
+    } else {
+      int rw = 1;
+      for (const auto &t : pend) rw = std::max(rw, t.L / 32);
+      const int ctas = std::min(rw >= 4 ? 4 : 6, 227 * 1024 / (4 * wb + 1024));  // (sweep_kernel launch bounds)
+      warps_sm = 4 * std::max(ctas, 1);
+    }
+    const bool l1_room = 256 * 1024 - warps_sm * wb - (warps_sm / 4) * 1024 >= 48 * 1024;
+    for (auto &t : pend) {
+      if ((t.kind & 6) != 6 || (t.kind & 16)) continue;
+      const Shape &S = P.shapes[t.shape];
+      const int pb = pair_room[t.shape] ? stage_pairs_bytes(S.k * t.L / 2) : 0;
+      const int sb = rc ? stage_bytes_rc(tsz, t.kind, S.k, S.nodes(), t.L) : stage_bytes(tsz, t.kind, S.k, S.nodes(), t.L);
+      if (l1_room || sb + pb > P.SB || recs_global) t.kind |= kKindRecGlobal;
+    }
+  }
 
   tm.mark("budget + tile packing");
   P.tiles.clear();

@@ -320,6 +320,8 @@ SweepArgs sweep_args(fdog_solver *s, double omega) {
   a.m1 = s->d_m1;
   a.omega = omega;
   a.clamp = s->clamp;
+  a.omega_f = (float)omega;
+  a.clamp_f = (float)s->clamp;
   a.lb_part = s->d_lb_part;
   a.done_counter = s->d_counter;
   a.tile_counter = s->d_counter + 1;
@@ -604,6 +606,8 @@ SeqArgs seq_args(fdog_solver *s, bool forward, double omega) {
   a.e_lane = s->d_e_lane;
   a.omega = omega;
   a.clamp = s->clamp;
+  a.omega_f = (float)omega;
+  a.clamp_f = (float)s->clamp;
   a.forward = forward ? 1 : 0;
   return a;
 }
@@ -862,8 +866,9 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   // chunked and fused paths read every average from the averaging kernel)
   s->pairs = !s->lifted && P.n_ell_open < (int64_t)(P.ell.size() / 2) && !s->stream_mode && !s->chunk_mode && !s->use_fused &&
              P.direct_tiles == 0;
-  const char *wpb = getenv("FDOG_WPB");  // experiment knob: warps per sweep CTA (default 4, max 16)
-  const size_t wmax = wpb ? std::max(1, std::min(16, atoi(wpb))) : 4;
+  // (4 warps per CTA: sweep_kernel's launch bounds; TMEM kernels below)
+  const char *wpb = getenv("FDOG_WPB");  // test knob: fewer warps per sweep CTA (default and max 4)
+  const size_t wmax = wpb ? std::max(1, std::min(4, atoi(wpb))) : 4;
   int warps = (int)std::max<size_t>(1, std::min<size_t>(wmax, (size_t)prop.smem_block / s->warp_bytes));
   s->tmem_cols = P.tmem_cols;
   if (s->tmem_cols > 0) {

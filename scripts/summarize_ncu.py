@@ -41,48 +41,51 @@ if os.path.exists(lp):
         lines.append(f"| `{k}` | {n} | {ns/1e3:.1f} | {ns/n/1e3:.2f} | {ns/tot:.3f} |")
     lines.append("")
 
-# full capture
-rp = os.path.join(root, "gpurun_out", f"prof_{tag}.ncu-rep")
-traffic = {}
-if os.path.exists(rp):
-    raw = subprocess.run(["ncu", "-i", rp, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+# full captures: prof_TAG.ncu-rep and prof_TAG_<workload>_<kernel>.ncu-rep
+import glob  # noqa: E402
+want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "lts__t_bytes.sum", "sm__cycles_active.avg", "sm__cycles_elapsed.avg", "smsp__inst_executed.sum",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum",
+        "lts__t_sectors.avg.pct_of_peak_sustained_elapsed",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size"]
+for rp in sorted(glob.glob(os.path.join(root, "gpurun_out", f"prof_{tag}.ncu-rep")) +
+                 glob.glob(os.path.join(root, "gpurun_out", f"prof_{tag}_*.ncu-rep")) +
+                 glob.glob(os.path.join(root, "gpurun_out", f"prof_{tag}_*.raw.csv"))):
+    if rp.endswith(".raw.csv"):  # exported on the box (scripts/gpu_ncu.sh)
+        raw = open(rp).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rp, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
-    hdr = rr[0]
-    want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
-            "sm__cycles_active.avg", "sm__cycles_elapsed.avg", "smsp__inst_executed.sum",
-            "smsp__issue_active.avg.pct_of_peak_sustained_active",
-            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
-            "launch__grid_size", "launch__block_size"]
+    if len(rr) < 3:
+        continue
+    hdr, units = rr[0], rr[1]
     lines.append(f"## ncu --set full ({rp.split('/')[-1]})\n")
-    lines.append("| kernel | " + " | ".join(w for w in want) + " |")
-    lines.append("|---|" + "---|" * len(want))
-    units = rr[1]
     for row in rr[2:]:
         d = dict(zip(hdr, row))
         u = dict(zip(hdr, units))
         name = d["Kernel Name"].split("(")[0].replace("void ", "")
-        vals = []
+        lines.append(f"`{name}`\n")
+        lines.append("| metric | value |\n|---|---|")
         for w in want:
-            vals.append(f"{d.get(w, '')} {u.get(w, '')}".strip())
-        lines.append(f"| `{name}` | " + " | ".join(vals) + " |")
-        if "sweep_kernel<float, 0" in name or "sweep_kernel<float, 1" in name:
-            def mb(w):
-                v = float(d[w])
-                return v * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}.get(u[w], 1)
-            traffic.setdefault(name, []).append(mb("dram__bytes_read.sum") + mb("dram__bytes_write.sum"))
-    lines.append("")
-    # stall reasons per kernel
-    lines.append("### warp stall reasons (cycles per issued instruction)\n")
-    for row in rr[2:]:
-        d = dict(zip(hdr, row))
-        name = d["Kernel Name"].split("(")[0].replace("void ", "")
+            if w in d:
+                lines.append(f"| {w} | {d[w]} {u.get(w, '')} |")
+        ld_r = d.get("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "")
+        st_r = d.get("l1tex__t_requests_pipe_lsu_mem_global_op_st.sum", "")
+        try:
+            lines.append(f"| sectors per global load request | "
+                         f"{float(d['l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum'].replace(',', '')) / float(ld_r.replace(',', '')):.2f} |")
+            lines.append(f"| sectors per global store request | "
+                         f"{float(d['l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum'].replace(',', '')) / float(st_r.replace(',', '')):.2f} |")
+        except (KeyError, ValueError, ZeroDivisionError):
+            pass
         st = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""): float(v)
               for k, v in d.items() if k.startswith("smsp__average_warps_issue_stalled_")
               and k.endswith("per_issue_active.ratio") and v not in ("", "n/a")}
         top = sorted(st.items(), key=lambda x: -x[1])[:6]
-        lines.append(f"- `{name}`: " + ", ".join(f"{k} {v:.2f}" for k, v in top))
-    lines.append("")
+        lines.append("\nstalls (cycles per issued instruction): " + ", ".join(f"{k} {v:.2f}" for k, v in top) + "\n")
 
 if len(sys.argv) > 2 and os.path.exists(sys.argv[2]):
     b = json.load(open(sys.argv[2]))

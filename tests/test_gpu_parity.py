@@ -763,3 +763,36 @@ def test_device_memory_from_torch():
     assert torch.cuda.memory_allocated() == before
     with pytest.raises(ValueError):
         F.Solver(p, allocator="numpy")
+
+
+@pytest.mark.parametrize("mode", ["rc", "tma"])
+@pytest.mark.parametrize("name,make", [
+    ("gm", lambda: synth.gm_worms_like(23, n_src=60, k_cand=6, knn=6)),
+    ("ct", lambda: synth.celltrack(23, frames=4, dets=40)),
+    ("cut", lambda: synth.mrf_potts_cut(23, H=8, W=10, L=3)),
+    ("qap", lambda: synth.qap(23, 7)),
+])
+def test_records_global_bitwise(oracle_mod, monkeypatch, mode, name, make):
+    """Hop records read from global memory (tile kind bit 6, FDOG_RECS=global)
+    instead of the stage give bit-identical iterates and bounds; one of them
+    against the oracle (fp64)."""
+    p = make()
+    monkeypatch.setenv("FDOG_SWEEP", mode)
+    monkeypatch.setenv("FDOG_FUSED", "0")
+    gs = []
+    for rg in ("", "global"):
+        monkeypatch.setenv("FDOG_RECS", rg)
+        gs.append(F.Solver(p, precision=64))
+    o = oracle_mod.Oracle(p)
+    s = _s(p)
+    for t in range(4):
+        fwd = t % 2 == 0
+        for g in gs:
+            g.pass_(fwd, 0.5)
+        o.pass_(fwd, 0.5)
+        assert np.array_equal(gs[0].lam(), gs[1].lam()) and np.array_equal(gs[0].deferred(), gs[1].deferred())
+        assert gs[0].lower_bound() == gs[1].lower_bound()
+        assert np.max(np.abs(gs[1].lam() - o.lam())) <= 1e-9 * s
+    gs[0].iterate(3, 0.5)
+    gs[1].iterate(3, 0.5)
+    assert np.array_equal(gs[0].lam(), gs[1].lam()) and gs[0].lower_bound() == gs[1].lower_bound()
