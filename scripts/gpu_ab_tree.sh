@@ -1,11 +1,12 @@
 #!/bin/bash
 # Same-box A/B of two whole trees: this one (new) and the tree under $OLD
-# (e.g. a `git worktree` of an earlier commit, built, copied to build/ab/old).
+# (e.g. a `git worktree` of an earlier commit, built, copied to build/ab/old);
+# both libraries are the ones built in this container (no rebuild on the box).
 # Usage: OLD=build/ab/old WL="gm_worms_like celltrack" scripts/gpu_ab_tree.sh TAG
 set -u
 TAG=$1; OLD=${OLD:-build/ab/old}
 OUT=$PWD/gpurun_out; mkdir -p $OUT
-python -c "import __graft_entry__ as g; g.build()" > $OUT/abt_build_$TAG.log 2>&1 || { tail $OUT/abt_build_$TAG.log; exit 1; }
+# (both trees built HERE beforehand: builds on different hosts differ in SASS)
 cuobjdump -sass paper_2111_10270_b200/libfastdog.so | md5sum > $OUT/abt_md5_$TAG.txt
 for rep in 1 2; do
 for w in ${WL:-gm_worms_like celltrack qap50}; do

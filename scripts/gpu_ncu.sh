@@ -4,7 +4,7 @@
 set -u
 TAG=$1; WL=${2:-celltrack qap50}
 OUT=gpurun_out; mkdir -p $OUT
-python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1 || { tail -20 $OUT/build_$TAG.log; exit 1; }
+[ -f paper_2111_10270_b200/libfastdog.so ] || python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1 || { tail -20 $OUT/build_$TAG.log; exit 1; }
 for w in $WL; do
   for ks in ${KERNELS:-sweep_kernel:5 avg_kernel:4}; do
     k=${ks%%:*}; sk=${ks##*:}

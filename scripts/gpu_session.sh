@@ -8,7 +8,10 @@ set -u
 TAG=${1:-r2}
 OUT=gpurun_out; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu_$TAG.txt 2>&1
-python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1 || { echo BUILD FAILED; tail -30 $OUT/build_$TAG.log; exit 1; }
+# (the library built in this container travels with the snapshot; build here
+# only if it is missing -- builds on different hosts differ in SASS)
+[ -f paper_2111_10270_b200/libfastdog.so ] || python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1 || { echo BUILD FAILED; tail -30 $OUT/build_$TAG.log; exit 1; }
+cuobjdump -sass paper_2111_10270_b200/libfastdog.so | md5sum > $OUT/sass_md5_$TAG.txt
 if [ "${TTL:-0}" = "1" ]; then timeout 900 python scripts/make_ttl_targets.py > $OUT/ttl_$TAG.log 2>&1; echo "ttl rc=$?"; cp bench_targets.json $OUT/bench_targets.json; fi
 if [ "${SKIP_TESTS:-0}" != "1" ]; then
 timeout 2400 python -m pytest tests -q -m gpu > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest gpu rc=$?"; grep -E "FAILED|passed|failed" $OUT/pytest_gpu_$TAG.log | tail -5
