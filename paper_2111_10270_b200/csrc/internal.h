@@ -1,6 +1,7 @@
 // internal.h -- shared declarations of the product library (host plan + device runtime).
 // Not part of the ABI; include/fastdog.h is.
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <vector_types.h>
 #include <string>
@@ -140,6 +141,22 @@ FDOG_HD int relax_slots(int W) { return 3 * (W + 1); }
 FDOG_HD int relax_bytes(int tsz, int W, int L) { return r16(relax_slots(W) * L * tsz); }
 constexpr int kWarpHeader = 256;
 FDOG_HD int warp_bytes(int SB, int DB, int NB) { return (kWarpHeader + NB * SB + DB + 127) & ~127; }
+// Warps per sweep CTA (<= wmax, the launch bounds' 4): the count that keeps
+// the most warps resident on an SM with smem_sm bytes of shared memory
+// (1 KB reserved per CTA), larger CTAs on ties.  (CTAs of 4 warps of 33 KB
+// each left QAP128 at 4 warps per SM where 2 or 3 per CTA fit 6.)
+inline int sweep_warps_per_cta(int wb, int wmax, int smem_block, int smem_sm, int *resident = nullptr) {
+  int best = 1, best_res = -1;
+  for (int w = std::max(1, std::min(wmax, smem_block / std::max(wb, 1))); w >= 1; --w) {
+    const int res = w * (smem_sm / (w * wb + 1024));
+    if (res > best_res) {
+      best_res = res;
+      best = w;
+    }
+  }
+  if (resident) *resident = best_res;
+  return best;
+}
 
 // One contiguous device image of everything a solver uploads (built by the
 // plan, untimed; pinned host memory when a CUDA device is present), so that

@@ -1041,8 +1041,18 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       const int w_tm = std::min({16, 4 * (512 / tm_cols), 227 * 1024 / warp_bytes(SB1, DB1, NB1)}) & ~3;
       tm_allow = false;
       std::vector<PendingTile> pend0 = pack(true, NB1);
-      const int w_sm = std::min(32, 227 * 1024 / warp_bytes(P.SB, P.DB, P.NB));
-      if (w_tm >= 1.2 * w_sm) {
+      // (compared in active lanes: TMEM tiles have 32 rows; the shared-memory
+      // pack may use narrower tiles for the longest rows, whose idle lanes
+      // cost the same issue slots -- QAP128: 4 TMEM warps of 32 rows 5.4 ms
+      // per iteration, 4 warps of 16-row tiles 6.5)
+      int w_sm = 0;
+      sweep_warps_per_cta(warp_bytes(P.SB, P.DB, P.NB), 4, 227 * 1024, 228 * 1024, &w_sm);
+      auto rows_per_tile = [](const std::vector<PendingTile> &v) {
+        double rows = 0;
+        for (const auto &t : v) rows += (double)t.rows.size();
+        return v.empty() ? 32.0 : rows / (double)v.size();
+      };
+      if (w_tm * rows_per_tile(pend) >= 1.2 * w_sm * rows_per_tile(pend0)) {
         P.SB = SB1;
         P.DB = DB1;
         P.NB = NB1;

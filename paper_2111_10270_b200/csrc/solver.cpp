@@ -869,7 +869,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   // (4 warps per CTA: sweep_kernel's launch bounds; TMEM kernels below)
   const char *wpb = getenv("FDOG_WPB");  // test knob: fewer warps per sweep CTA (default and max 4)
   const size_t wmax = wpb ? std::max(1, std::min(4, atoi(wpb))) : 4;
-  int warps = (int)std::max<size_t>(1, std::min<size_t>(wmax, (size_t)prop.smem_block / s->warp_bytes));
+  int warps = sweep_warps_per_cta(s->warp_bytes, (int)wmax, prop.smem_block, prop.smem_sm);
   s->tmem_cols = P.tmem_cols;
   if (s->tmem_cols > 0) {
     // TMEM variant (kernels.cu sweep_kernel<..., TM>): one CTA per SM (a kernel

@@ -25,10 +25,6 @@ import json; d=json.load(open('$OUT/bench_${TAG}_$w.json'))
 print('$w value %.3e ms/step %.4f roof %.3f traffic %s' % (d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['traffic']), {k: round(v['ms']/v['launches']*1e3,2) for k,v in d['kernels'].items()})" || tail -5 $OUT/bench_${TAG}_$w.err
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-ttl --no-traffic --no-hop > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
-for w in ${FULL_WORKLOADS:-mrf_potts}; do
-  # (launch order: energy sweep at create, then forward / backward: skip 5 -> a forward sweep)
-  for ks in "sweep_kernel:5" "avg_kernel:4"; do
-    k=${ks%%:*}; sk=${ks##*:}
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$k" -s $sk -c 1 -o $OUT/prof_${TAG}_${w}_${k%%_*} python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-ttl --no-traffic --no-hop --workload $w > $OUT/ncu_full_${TAG}_${w}_${k%%_*}.log 2>&1; echo "ncu full $w $k rc=$?"
-  done
-done
+# ncu --set full of a forward sweep and an averaging launch per workload (raw
+# metrics + SASS hotspots exported on the box, reports left there)
+bash scripts/gpu_ncu.sh $TAG "${FULL_WORKLOADS:-mrf_potts celltrack qap50 gm_worms_like}"
