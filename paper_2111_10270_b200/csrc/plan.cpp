@@ -62,6 +62,33 @@ static void par_for(int64_t n, int threads, F f) {  // f(chunk, begin, end)
   f(0, (int64_t)0, n / T);
   for (auto &th : pool) th.join();
 }
+// Sort with a strict total order (ties impossible), chunks sorted in parallel
+// and merged pairwise: the same result as std::sort for any thread count.
+template <typename V, typename C>
+static void par_sort(std::vector<V> &v, int threads, C cmp) {
+  const int64_t n = (int64_t)v.size();
+  const int T = par_chunks(n, threads);
+  if (T == 1) {
+    std::sort(v.begin(), v.end(), cmp);
+    return;
+  }
+  std::vector<int64_t> b(T + 1);
+  for (int t = 0; t <= T; ++t) b[t] = n * t / T;
+  par_for(n, threads, [&](int c, int64_t, int64_t) { std::sort(v.begin() + b[c], v.begin() + b[c + 1], cmp); });
+  std::vector<V> tmp(v.size());
+  for (int w = 1; w < T; w *= 2) {
+    const int pairs = (T + 2 * w - 1) / (2 * w);
+    std::vector<std::thread> pool;
+    for (int k = 0; k < pairs; ++k)
+      pool.emplace_back([&, k] {
+        const int64_t lo = b[std::min(T, 2 * w * k)], mid = b[std::min(T, 2 * w * k + w)],
+                      hi = b[std::min(T, 2 * w * k + 2 * w)];
+        std::merge(v.begin() + lo, v.begin() + mid, v.begin() + mid, v.begin() + hi, tmp.begin() + lo, cmp);
+      });
+    for (auto &th : pool) th.join();
+    v.swap(tmp);
+  }
+}
 static inline void atomic_min32(int32_t *p, int32_t v) {
   int32_t cur = __atomic_load_n(p, __ATOMIC_RELAXED);
   while (v < cur && !__atomic_compare_exchange_n(p, &cur, v, true, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
@@ -694,10 +721,12 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
   // tracking 17 k -- the longer tiles cost more in the tail than they save:
   // GM 40.9 -> 45.7 us.  So: problems of at least 10^6 rows.)
   const bool wide_ok = !P.lifted && (wide_force || P.local_rows.size() >= 1000000) && P.n_slots > (1 << 15) && !(sw && sw[0] == 's') && !(fz && fz[0] == '1') && !(wd && wd[0] == '0');
+  const char *r4k = getenv("FDOG_R4K");  // experiment knob: longest rows with four rows per lane (default 4)
+  const int r4_max_k = r4k ? atoi(r4k) : 4;
   auto rows_per_lane = [&](size_t sh) -> int {
     const Shape &S = P.shapes[sh];
     if (!wide_ok || S.max_w > 2) return 1;
-    int R = (S.k <= 4 && !(o && o->precision == 64)) ? 4 : S.k <= 16 ? 2 : 1;  // (fp64: at most 2)
+    int R = (S.k <= r4_max_k && !(o && o->precision == 64)) ? 4 : S.k <= 16 ? 2 : 1;  // (fp64: at most 2)
     while (R > 1 && by_shape[sh].size() < (size_t)(32 * R)) R /= 2;
     return R;
   };
@@ -710,7 +739,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       auto &rows = by_shape[sh];
       if (rows.size() < 2) continue;
       std::vector<int32_t> b = rows;
-      std::sort(b.begin(), b.end(), [&](int32_t x, int32_t y) {
+      par_sort(b, threads, [&](int32_t x, int32_t y) {
         const int32_t ux = unit[x], uy = unit[y];
         if (ukey[ux] != ukey[uy]) return ukey[ux] < ukey[uy];
         return ux != uy ? ux < uy : x < y;
@@ -1453,6 +1482,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
                           : stage_bytes(tsz, d.kind, d.K, d.nodes, d.lanes);
       if (sb + stage_pairs_bytes(tile_pairs[t]) > P.SB) tile_pairs[t] = 0;  // keep them in the kernel
     }
+    tm.mark("avg: closed pairs");
     auto closed = [&](int64_t q) {
       int32_t t;
       return candidate(q, &t) && tile_pairs[t] > 0;
@@ -1482,13 +1512,19 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       for (size_t g = 0; g < ds.size(); ++g) grp_of[ds[g]] = (int32_t)g;
       P.elld_d = ds;
     }
-    auto cat = [&](int64_t q) {
+    tm.mark("avg: ELL-D degrees");
+    auto cat_of = [&](int64_t q) {
       const int64_t d = P.var_ptr[q + 1] - P.var_ptr[q];
       if (P.var_xidx[q] >= 0 || P.lifted) return 2;  // (lifted mode: one CSR kernel sums both sides)
       if (d <= 2) return closed(q) ? 4 : 0;
       if (d <= 4) return 1;
       return (d <= 32 && grp_of[d] >= 0) ? 5 : 2;
     };
+    std::vector<uint8_t> cat_v((size_t)std::max<int64_t>(nv, 1));
+    par_for(nv, threads, [&](int, int64_t a, int64_t b) {
+      for (int64_t q = a; q < b; ++q) cat_v[q] = (uint8_t)cat_of(q);
+    });
+    auto cat = [&](int64_t q) { return (int)cat_v[q]; };
     const int T = par_chunks(nv, threads);
     std::vector<std::array<int64_t, 5>> cc(T + 1, {0, 0, 0, 0, 0});  // ell, ell4, csr vars, csr slots, closed pairs
     par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
@@ -1501,17 +1537,28 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       }
       cc[c + 1] = m;
     });
+    tm.mark("avg: category counts");
     // ELL-D fill (variables in var_list order within a group)
     {
       const int G = (int)P.elld_d.size();
       P.elld_n.assign(G, 0);
       P.elld_off.assign(G, 0);
+      // positions within a group in var_list order: per-chunk counts, prefix
       std::vector<int64_t> pos(nv, -1);
-      for (int64_t q = 0; q < nv; ++q)
-        if (cat(q) == 5) {
-          const int g = grp_of[P.var_ptr[q + 1] - P.var_ptr[q]];
-          pos[q] = P.elld_n[g]++;
-        }
+      const int TC = par_chunks(nv, threads);
+      std::vector<std::vector<int64_t>> gc(TC + 1, std::vector<int64_t>(std::max(G, 1), 0));
+      par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
+        for (int64_t q = a; q < b; ++q)
+          if (cat(q) == 5) gc[c + 1][grp_of[P.var_ptr[q + 1] - P.var_ptr[q]]]++;
+      });
+      for (int c = 0; c < TC; ++c)
+        for (int g = 0; g < G; ++g) gc[c + 1][g] += gc[c][g];
+      for (int g = 0; g < G; ++g) P.elld_n[g] = gc[TC][g];
+      par_for(nv, threads, [&](int c, int64_t a, int64_t b) {
+        std::vector<int64_t> o = gc[c];
+        for (int64_t q = a; q < b; ++q)
+          if (cat(q) == 5) pos[q] = o[grp_of[P.var_ptr[q + 1] - P.var_ptr[q]]]++;
+      });
       int64_t off = 0;
       for (int g = 0; g < G; ++g) {
         P.elld_off[g] = off;
@@ -1522,8 +1569,10 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       {
         std::vector<int64_t> vb(G + 1, 0);
         for (int g = 0; g < G; ++g) vb[g + 1] = vb[g] + P.elld_n[g];
-        for (int64_t q = 0; q < nv; ++q)
-          if (pos[q] >= 0) P.elld_var[vb[grp_of[P.var_ptr[q + 1] - P.var_ptr[q]]] + pos[q]] = P.var_list[q];
+        par_for(nv, threads, [&](int, int64_t a, int64_t b) {
+          for (int64_t q = a; q < b; ++q)
+            if (pos[q] >= 0) P.elld_var[vb[grp_of[P.var_ptr[q + 1] - P.var_ptr[q]]] + pos[q]] = P.var_list[q];
+        });
       }
       par_for(nv, threads, [&](int, int64_t a, int64_t b) {
         for (int64_t q = a; q < b; ++q) {
@@ -1535,6 +1584,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         }
       });
     }
+    tm.mark("avg: ELL-D fill");
     for (int c = 0; c < T; ++c)
       for (int u = 0; u < 5; ++u) cc[c + 1][u] += cc[c][u];
     const auto &tot = cc[T];
@@ -1575,6 +1625,7 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
         }
       }
     });
+    tm.mark("avg: ELL / CSR fill");
     // pair lists: per staged tile with closed pairs, (i | m << 16) for the two
     // tile slot offsets i < m of each pair, ascending i; identical lists stored
     // once (every MRF-LP marginalisation tile has the same one)
@@ -1584,48 +1635,62 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
       d.n_pairs = 0;
     }
     {
+      // (parallel: each closed pair's tile and code, then per run of pairs of
+      // one tile the sorted list and its hash; the lists are deduplicated in
+      // run order, as a sequential pass would)
+      const int64_t e0 = tot[0], ne = tot[4];
+      std::vector<int32_t> tl((size_t)std::max<int64_t>(ne, 1));
+      std::vector<uint32_t> code((size_t)std::max<int64_t>(ne, 1));
+      par_for(ne, threads, [&](int, int64_t a, int64_t b) {
+        for (int64_t x = a; x < b; ++x) {
+          const int64_t s1 = P.ell[2 * (e0 + x)], s2 = P.ell[2 * (e0 + x) + 1];
+          const int32_t t = tile_of(s1);
+          const int64_t b0 = P.tiles[t].slot_base;
+          tl[x] = t;
+          code[x] = (uint32_t)(std::min(s1, s2) - b0) | ((uint32_t)(std::max(s1, s2) - b0) << 16);
+        }
+      });
+      std::vector<int64_t> run_at;  // run starts (+ ne)
+      for (int64_t x = 0; x < ne; ++x)
+        if (x == 0 || tl[x] != tl[x - 1]) run_at.push_back(x);
+      const int64_t nr = (int64_t)run_at.size();
+      run_at.push_back(ne);
+      std::vector<uint64_t> run_hash((size_t)std::max<int64_t>(nr, 1));
+      par_for(nr, threads, [&](int, int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; ++r) {
+          const auto lo = code.begin() + run_at[r], hi = code.begin() + run_at[r + 1];
+          std::sort(lo, hi, [](uint32_t x, uint32_t y) { return (x & 0xFFFF) < (y & 0xFFFF); });
+          uint64_t h = 1469598103934665603ull ^ (uint64_t)(hi - lo);
+          for (auto it = lo; it != hi; ++it) h = (h ^ *it) * 1099511628211ull;
+          run_hash[r] = h;
+        }
+      });
       std::unordered_map<uint64_t, std::vector<std::pair<int32_t, int32_t>>> seen;  // (offset, length)
-      std::vector<uint32_t> cur;
-      int32_t ct = -1;
-      auto flush_list = [&]() {
-        if (ct < 0) return;
-        std::sort(cur.begin(), cur.end(), [](uint32_t x, uint32_t y) { return (x & 0xFFFF) < (y & 0xFFFF); });
-        uint64_t h = 1469598103934665603ull ^ cur.size();
-        for (uint32_t v : cur) h = (h ^ v) * 1099511628211ull;
-        auto &cands = seen[h];
+      for (int64_t r = 0; r < nr; ++r) {
+        const auto lo = code.begin() + run_at[r], hi = code.begin() + run_at[r + 1];
+        const int32_t len = (int32_t)(hi - lo);
+        auto &cands = seen[run_hash[r]];
         int32_t at = -1;
         for (const auto &c0 : cands)
-          if (c0.second == (int32_t)cur.size() && std::equal(cur.begin(), cur.end(), P.pair_list.begin() + c0.first)) {
+          if (c0.second == len && std::equal(lo, hi, P.pair_list.begin() + c0.first)) {
             at = c0.first;
             break;
           }
         if (at < 0) {
           at = (int32_t)P.pair_list.size();
-          P.pair_list.insert(P.pair_list.end(), cur.begin(), cur.end());
+          P.pair_list.insert(P.pair_list.end(), lo, hi);
           while (P.pair_list.size() % 4) P.pair_list.push_back(0);  // 16-byte aligned lists (TMA)
-          cands.emplace_back(at, (int32_t)cur.size());
+          cands.emplace_back(at, len);
         }
-        P.tiles[ct].pair_base = at;
-        P.tiles[ct].n_pairs = (int32_t)cur.size();
-      };
-      for (int64_t e = tot[0]; e < tot[0] + tot[4]; ++e) {
-        const int64_t s1 = P.ell[2 * e], s2 = P.ell[2 * e + 1];
-        const int32_t t = tile_of(s1);
-        if (t != ct) {
-          flush_list();
-          ct = t;
-          cur.clear();
-        }
-        const int64_t b0 = P.tiles[t].slot_base;
-        const uint32_t i = (uint32_t)(std::min(s1, s2) - b0), m = (uint32_t)(std::max(s1, s2) - b0);
-        cur.push_back(i | (m << 16));
+        P.tiles[tl[run_at[r]]].pair_base = at;
+        P.tiles[tl[run_at[r]]].n_pairs = len;
       }
-      flush_list();
       if (P.pair_list.size() > 0x7fffffffULL) {
         set_error("pair lists exceed 2^31 entries");
         return FDOG_ETOOBIG;
       }
     }
+    tm.mark("avg: pair lists");
     P.n_vars_local = nv;
     P.var_list.swap(csr_list);
     P.var_ptr.swap(csr_ptr);
