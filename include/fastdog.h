@@ -86,10 +86,12 @@ typedef struct {
      memory, streams and process groups").  If dev_alloc is set, every device
      buffer a solver holds -- the plan image with the runtime state, the
      non-deferred schedule, the primal-rounding snapshot -- is obtained by
-     dev_alloc(bytes, device, stream, alloc_ctx), stream-ordered on the
-     solver's stream (the caller's opts.stream or the solver-owned one), and
-     returned by dev_free(ptr, device, stream, alloc_ctx) after that stream
-     has been synchronised (fdog_destroy, end of fdog_round_primal).  A NULL
+     dev_alloc(bytes, device, stream, alloc_ctx) (stream: the solver's stream,
+     the caller's opts.stream or the solver-owned one; first used on it after
+     the call returns), and returned by dev_free(ptr, device, stream,
+     alloc_ctx) only after that stream has been synchronised (fdog_destroy,
+     end of fdog_round_primal), so the allocator may hand the memory to any
+     stream afterwards.  A NULL
      return fails the call with FDOG_ENOMEM.  The one exception is the
      peer-exchange region (external-exchange mode), a cudaMalloc of its own
      so that one CUDA IPC handle maps exactly it.  dev_alloc NULL: cudaMalloc

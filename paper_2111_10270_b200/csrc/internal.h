@@ -223,6 +223,8 @@ struct Plan {
   std::vector<int8_t> rel;
   std::vector<int64_t> rhs;
   int64_t n_vars_local = 0;         // variables with local slots (ELL + CSR)
+  int64_t n_vars_shared = 0;        // of those, held by another rank too (counted once per plan)
+  int64_t n_free_vars = 0;          // |J_i| = 0 (A13)
   std::vector<int32_t> x_local;     // per shared var: index into var_list or -1
   std::vector<int32_t> x_deg;       // per shared var: |J_i| (global)
 

@@ -9,6 +9,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -748,7 +750,21 @@ fdog_status init_nccl(fdog_solver *s, const fdog_options *o) {
   return FDOG_OK;
 }
 
+// FDOG_PLAN_TRACE=1: phase times of a solver's create on stderr (host time;
+// device work is asynchronous until the final synchronisation)
+struct CreateTimer {
+  bool on = getenv("FDOG_PLAN_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char *what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[create] %-26s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o, fdog_solver *s) {
+  CreateTimer ctm;
   s->plan = plan;
   const Plan &P = *plan;
   s->precision = o->precision == 64 ? 64 : 32;
@@ -769,6 +785,10 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     return FDOG_EINVAL;
   }
   s->profile = o->profile != 0;
+  if (const char *ev = getenv("FDOG_ELLV")) {  // experiment knob: ELL variables per averaging thread (1, 2, 4, 8)
+    const int v = atoi(ev);
+    if (v == 1 || v == 2 || v == 4 || v == 8) s->ell_v = v;
+  }
   {
     const char *g = getenv("FDOG_GRAPHS");  // experiment knob: FDOG_GRAPHS=0 disables graph replay
     s->use_graphs = !(g && g[0] == '0');
@@ -975,6 +995,7 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   const size_t o_l0 = s->lifted ? carve(slot_bytes) : 0, o_a0 = s->lifted ? carve(slot_bytes) : 0;
   const size_t o_lo = s->lifted ? carve(slot_bytes) : 0;
   unsigned char *base = nullptr;
+  ctm.mark("setup");
   CK(dev_alloc(s, (void **)&base, im.bytes + rt), "device allocation");
   s->allocs.push_back(base);
   s->st.device_bytes = (int64_t)(im.bytes + rt);
@@ -1075,14 +1096,15 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     s->bytes[kKAllreduce] = (double)s->n_shared * T;
     s->bytes[kKAddDeferred] = (double)s->n_dev_slots * 4 * T;
   }
+  ctm.mark("allocation, upload, launch setup");
   // stats
   s->st.bdds = (int64_t)P.local_rows.size();
   s->st.nodes = P.n_nodes;
   s->st.arcs = 2 * P.n_nodes;
   s->st.slots = P.n_slots;
-  s->st.vars_local = (int64_t)P.var_list.size();
-  for (int32_t x : P.var_xidx) s->st.vars_shared += x >= 0;
-  for (int32_t d : P.deg_global) s->st.free_vars += d == 0;
+  s->st.vars_local = P.n_vars_local;
+  s->st.vars_shared = P.n_vars_shared;
+  s->st.free_vars = P.n_free_vars;
   s->st.shapes = (int64_t)P.shapes.size();
   s->st.tiles = (int64_t)P.tiles.size();
   s->st.tiles_shared_topology = P.tiles_shared;
@@ -1102,9 +1124,11 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
   s->st.coop_tiles = s->n_coop;
   s->st.tmem_cols = s->tmem_cols;
 
+  ctm.mark("stats");
   // initial bound sum_j E^j(lambda) (+ free term on the host)
   if ((st = energy(s))) return st;
   CK(cudaStreamSynchronize(s->stream), "sync");
+  ctm.mark("energy sweep + sync");
   return FDOG_OK;
 }
 

@@ -796,3 +796,25 @@ def test_records_global_bitwise(oracle_mod, monkeypatch, mode, name, make):
     gs[0].iterate(3, 0.5)
     gs[1].iterate(3, 0.5)
     assert np.array_equal(gs[0].lam(), gs[1].lam()) and gs[0].lower_bound() == gs[1].lower_bound()
+
+
+def test_torch_memory_reused_across_solvers():
+    """A destroyed solver's device memory goes back to torch's cache and serves
+    the next solver (no new cudaMalloc: torch's reserved memory stays flat),
+    with identical results."""
+    import gc
+    import torch
+    p = synth.gm_worms_like(6, n_src=80, k_cand=6, knn=6)
+    pl = F.Plan(p, precision=32)
+    g = F.Solver(plan=pl, precision=32)
+    g.iterate(3, 0.5)
+    ref = g.lam()
+    g.close()
+    gc.collect()
+    reserved = torch.cuda.memory_reserved()
+    for _ in range(3):
+        h = F.Solver(plan=pl, precision=32)
+        h.iterate(3, 0.5)
+        assert np.array_equal(h.lam(), ref)
+        h.close()
+        assert torch.cuda.memory_reserved() == reserved
