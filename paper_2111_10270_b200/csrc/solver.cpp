@@ -931,10 +931,12 @@ fdog_status create_impl(std::shared_ptr<const Plan> plan, const fdog_options *o,
     // many tiles per warp: one claim takes several consecutive tiles, so the
     // single counter is not a serialisation point (measured: MRF, 68 tiles per
     // warp, sweeps 282 -> 219 us with 2-4 tiles per claim, 8: 226, 16: 235;
-    // CellTrack, 9.5 per warp, 39.5 -> 38.8 us with 2)
+    // CellTrack, 9.5 per warp, 39.5 -> 38.8 us with 2; round 2: see below)
     const char *cb = getenv("FDOG_CLAIM");  // experiment knob: tiles per claim
     const int64_t tpw = s->n_tiles / std::max<int64_t>(warps_total, 1);
-    s->claim_batch = cb ? std::max(1, atoi(cb)) : (tpw >= 32 ? 4 : tpw >= 8 ? 2 : 1);
+    // (64-row MRF-LP tiles, 41 per warp: 2 per claim 518, 4 per claim 526 us
+    // per iteration; Potts-cut, 26 per warp, 1 / 2 equal)
+    s->claim_batch = cb ? std::max(1, atoi(cb)) : (tpw >= 64 ? 4 : tpw >= 8 ? 2 : 1);
     s->pdl_early = !s->rc && s->n_tiles < 8 * warps_total ? 1 : 0;
     // (A balanced static grid -- every warp exactly ceil(tiles / warps) tiles --
     // was measured on QAP50: 6 % slower.  Warps' finish times spread over 2x
