@@ -1054,9 +1054,11 @@ fdog_status build_plan(const fdog_problem *p, const fdog_options *o, Plan &P) {
     if (direct || (small && !(sw && sw[0] == 'r'))) {
       rc = false;
       pend = pack(false, 2);
-    } else if (warp_bytes(P.SB, P.DB, 1) <= 8192) {
+    } else if (warp_bytes(P.SB, P.DB, 1) <= 9216) {
       // short rows: single-buffered warps finish a tile faster than its TMA
       // stage arrives -- double-buffer (measured: MRF 287 -> 248 us per sweep;
+      // round 2: Potts-cut, 8.7 KB per warp, 411 -> 405 us per iteration;
+      // MRF-LP's 64-row tiles, 10.9 KB, 235 -> 264 us per sweep, and
       // CellTrack / QAP50, whose stages are larger, stay single-buffered)
       pend = pack(true, 2);
     }
